@@ -1,0 +1,464 @@
+#!/usr/bin/env python
+"""Benchmark of the reconstruction loop (BASELINE.json metric and configs[1]).
+
+Workload (configs[1]): 128^3 synthetic flame (synth_volume seed 0), 8 views of
+512x512 (synth_cameras radius 0.38, fov 60, jitter 5, seed 0), full RTE
+(emission, extinction, single scattering sigma_s = 0.1 over 32 Fibonacci
+directions), tau_n = 1 - 0.95^(64/n) = 0.02532, green channel, deterministic
+G, alpha_l = 0.006, alpha_d = 1, converge_eps = 1e-12 so every iteration runs.
+A step is one reconstruction iteration: render + residual + RMSE of every
+bbox pixel of every view, back-projection of every flame ray, convergence
+rule, clamped update.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints one JSON line (rank 0).  Multi-GPU runs are launched by torchrun:
+views are sharded across ranks and one NCCL all-reduce per iteration sums
+the corrections (engine.py); time is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_VOX = 128
+N_VIEWS = 8
+RES = 512
+SIGMA_S = 0.1
+SCAT_DIRS = 32
+TAU = 1.0 - 0.95 ** (64.0 / N_VOX)
+ALPHA_L = 0.006
+METRIC = "recon iters/sec at 128³×8 views 512²; Gsamples/s; % of HBM roofline"
+WORKLOAD = "config 2: 128^3 flame, 8 views 512x512, full RTE (sigma_s 0.1, 32 dirs), green channel"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# inputs
+# ---------------------------------------------------------------------------
+
+
+def make_scene():
+    """Synthetic inputs of configs[1], rendered on the device."""
+    from paper_1809_06417_b200 import RenderConfig, VoxelGrid, compute_visual_hull, render_view
+    from paper_1809_06417_b200.preprocess import bounding_box, threshold_mask
+    from paper_1809_06417_b200.synth import synth_cameras, synth_volume
+
+    vols = synth_volume((N_VOX,) * 3, seed=0, kind="flame")
+    truth = [vols[t] for t in ("red", "green", "blue")]
+    cams = synth_cameras(N_VIEWS, radius=0.38, fov=60.0, elevation_jitter_deg=5.0, width=RES, height=RES, seed=0)
+    rcfg = RenderConfig(tau=TAU, scattering_enabled=True, sigma_s=SIGMA_S, scatter_dirs=SCAT_DIRS)
+    imgs = [render_view(c, truth, None, rcfg) for c in cams]
+    masked = [threshold_mask(im) for im in imgs]
+    masks = [m for m, _ in masked]
+    blanked = [im for _, im in masked]
+    bbox = bounding_box(masks, 4)
+    geom = VoxelGrid(N_VOX, N_VOX, N_VOX, truth[0].origin, truth[0].edge)
+    hull = compute_visual_hull(geom, [m.bits for m in masks], cams)
+    return dict(truth=truth, cams=cams, rcfg=rcfg, images=[im.channel(1) for im in blanked], masks=masks,
+                bbox=bbox, geom=geom, hull=hull)
+
+
+def work_counts(sc):
+    """S_r (render samples), S_f (samples on flame rays), S_a (in-hull adjust
+    samples), R_f, V*P, N_kp per iteration, counted exactly."""
+    from paper_1809_06417_b200 import _kernels
+    from paper_1809_06417_b200.geometry import pixel_rays
+
+    geom, bbox = sc["geom"], sc["bbox"]
+    lo = geom.origin
+    hi = lo + np.array([geom.nx, geom.ny, geom.nz]) * geom.edge
+    us = np.arange(bbox.u0, bbox.u1 + 1) + 0.5
+    vs = np.arange(bbox.v0, bbox.v1 + 1) + 0.5
+    uu, vv = np.meshgrid(us, vs, indexing="xy")
+
+    def samples(o, d):
+        with np.errstate(divide="ignore", invalid="ignore"):
+            t0 = (lo[None, :] - o[None, :]) / d
+            t1 = (hi[None, :] - o[None, :]) / d
+        tmin = np.max(np.where(d == 0, -1e300, np.minimum(t0, t1)), axis=1)
+        tmax = np.min(np.where(d == 0, 1e300, np.maximum(t0, t1)), axis=1)
+        te = np.maximum(tmin, 0.0)
+        n = np.floor((tmax - te) / geom.edge + 1e-9)
+        return np.where(tmax > te, n, 0).astype(np.int64)
+
+    inside = sc["hull"].inside_voxels().astype(np.uint8)
+    s_r = s_f = s_a = r_f = 0
+    for cam, mask in zip(sc["cams"], sc["masks"]):
+        o, d = pixel_rays(cam, uu.ravel(), vv.ravel())
+        s_r += int(samples(o, d).sum())
+        rows, cols = np.nonzero(mask.bits[bbox.slices])
+        fo, fd = pixel_rays(cam, cols + bbox.u0 + 0.5, rows + bbox.v0 + 0.5)
+        s_f += int(samples(fo, fd).sum())
+        counts = np.empty(rows.size, dtype=np.int64)
+        _kernels.count_hull_samples(fo, fd, inside, geom.origin, geom.edge, counts)
+        s_a += int(counts.sum())
+        r_f += int(rows.size)
+    vp = len(sc["cams"]) * bbox.area
+    n_kp = (geom.nx + 1) * (geom.ny + 1) * (geom.nz + 1)
+    return dict(S_r=s_r, S_f=s_f, S_a=s_a, R_f=r_f, VP=vp, N_kp=n_kp,
+                hull_kp=int(sc["hull"].key_point_mask().sum()))
+
+
+def algorithmic_bytes(w, scattering=True):
+    """B_iter = 32 S_r [+76 S_r with scattering] + 64 S_a +
+    1 S_f + 8 V P + 4 R_f + 16 N_kp."""
+    render = (108 if scattering else 32) * w["S_r"] + 8 * w["VP"]
+    total = render + 64 * w["S_a"] + w["S_f"] + 4 * w["R_f"] + 16 * w["N_kp"]
+    return render, total
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        time.sleep(0.05)
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [num(r[1]) for r in rows if num(r[1]) is not None]
+        mx = [num(r[2]) for r in rows if num(r[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+
+def run_gpu(args):
+    import torch
+
+    from paper_1809_06417_b200 import ReconstructionConfig, _lib, reconstruct_channel
+    from paper_1809_06417_b200.engine import ChannelLoop
+    from paper_1809_06417_b200.reconstruct import _init_grid, _loop_config
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    sc = make_scene()
+    cfg = ReconstructionConfig(alpha_l=ALPHA_L, alpha_d=1.0, tau=TAU, max_iters=args.steps + args.warmup,
+                               converge_eps=1e-12, deterministic_mode=True)
+    grid0 = _init_grid(sc["geom"], sc["hull"], "green")
+    src = [im.data[sc["bbox"].slices][:, :, 0] for im in sc["images"]]
+    loop = ChannelLoop(sc["cams"], grid0, grid0.values, src, sc["masks"], sc["bbox"],
+                       sc["hull"].inside_voxels(), sc["hull"].key_point_mask(), sc["rcfg"],
+                       _loop_config(cfg, grid0), cfg.max_iters + 8, background=0.0, use_graph=False)
+    dev = torch.device("cuda", local)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    stream = _lib.stream_ptr()
+    names = ["render", "adjust", "finalize", "update"]
+
+    def one_step(evs):
+        evs[0].record()
+        loop._render(stream)
+        evs[1].record()
+        loop._volume(stream)
+        loop._adjust(stream)
+        if world > 1:
+            loop._allreduce(stream)
+        evs[2].record()
+        loop._finalize(stream)
+        evs[3].record()
+        loop._update(stream)
+        evs[4].record()
+
+    for _ in range(args.warmup):
+        flush.fill_(1.0)
+        one_step([torch.cuda.Event(enable_timing=True) for _ in range(5)])
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    barrier()
+    all_evs = []
+    l0 = _lib.launch_count()
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush between timed steps, outside the step's events
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        one_step(evs)
+        all_evs.append(evs)
+    barrier()
+    launches = _lib.launch_count() - l0
+    clocks = sampler.stop()
+    step_ms = np.array([e[0].elapsed_time(e[4]) for e in all_evs])
+    part_ms = {n: float(np.mean([e[i].elapsed_time(e[i + 1]) for e in all_evs])) for i, n in enumerate(names)}
+    total_ms = float(step_ms.sum())
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    st = loop.read_state()
+    assert st["it"] == args.warmup + args.steps and not st["done"], st
+
+    w = work_counts(sc)
+    render_bytes, iter_bytes = algorithmic_bytes(w, scattering=True)
+    ms = total_ms / args.steps
+    its = 1000.0 / ms
+    peak, peak_kind = peaks()
+    render_ms = part_ms["render"]
+    achieved = render_bytes / (render_ms * 1e-3) / 1e9
+
+    # e2e: the public API with host buffers (H2D of inputs, D2H of the grid)
+    e2e = None
+    if args.e2e_iters > 0:
+        cfg_e = ReconstructionConfig(alpha_l=ALPHA_L, alpha_d=1.0, tau=TAU, max_iters=args.e2e_iters,
+                                     converge_eps=1e-12, deterministic_mode=True)
+        reconstruct_channel(sc["images"], sc["cams"], sc["geom"], sc["hull"], cfg_e, render_cfg=sc["rcfg"],
+                            masks=sc["masks"], bbox=sc["bbox"])  # warm (graph capture path, allocator)
+        barrier()
+        t0 = time.perf_counter()
+        grid, trace = reconstruct_channel(sc["images"], sc["cams"], sc["geom"], sc["hull"], cfg_e,
+                                          render_cfg=sc["rcfg"], masks=sc["masks"], bbox=sc["bbox"])
+        barrier()
+        wall = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([wall], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            wall = float(t.item())
+        h2d = (sum(s.nbytes for s in src) + grid0.values.nbytes + sc["hull"].inside_voxels().size
+               + 4 * w["hull_kp"] + 4 * w["R_f"] + 160 * N_VIEWS)
+        d2h = grid.values.nbytes + 8 * trace.iterations
+        e2e = {"value": trace.iterations / wall, "unit": "iters/s", "iterations": trace.iterations,
+               "h2d_bytes_per_step": int(h2d / trace.iterations), "d2h_bytes_per_step": int(d2h / trace.iterations),
+               "note": "reconstruct_channel() on host numpy inputs; H2D of frames/lattice/hull and D2H of the "
+                       "grid + trace inside the timed call, amortised over its iterations"}
+
+    out = {
+        "metric": METRIC,
+        "value": its,
+        "unit": "iters/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32 values / f64 geometry",
+        "data": "synthetic (synth_volume seed 0, synth_cameras seed 0, inputs rendered on device)",
+        "config": {"workload": WORKLOAD, "n": N_VOX, "views": N_VIEWS, "res": RES, "tau": TAU,
+                   "sigma_s": SIGMA_S, "scatter_dirs": SCAT_DIRS, "bbox": [sc["bbox"].u0, sc["bbox"].v0,
+                                                                          sc["bbox"].u1, sc["bbox"].v1],
+                   "parallelism": f"view-sharded x{world}" if world > 1 else "1 GPU",
+                   "l2": "256 MiB buffer written between timed steps (outside the step events)"},
+        "gsamples_per_s": (w["S_r"] + w["S_a"]) * its / 1e9,
+        "render_gsamples_per_s": w["S_r"] / (render_ms * 1e-3) / 1e9,
+        "work": w,
+        "stage_ms": part_ms,
+        "iter_algorithmic_bytes": iter_bytes,
+        "iter_roofline_frac": iter_bytes * its / (peak * 1e9),
+        "roofline": {"bound": "hbm", "kernel": "loop_render_kernel<true>", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "bytes_per_launch": render_bytes,
+                     "bytes_rule": "108 B per render sample (27-key-point stencil, f32) + 8 B per bbox pixel"},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(sc, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reference arm and cpu_baseline)
+# ---------------------------------------------------------------------------
+
+
+def _oracle_iteration_sample(sc, values, views, cpu):
+    """Render + adjust of the given views of one iteration on the CPU oracle."""
+    geom, bbox = sc["geom"], sc["bbox"]
+    u0, v0, u1, v1 = bbox.u0, bbox.v0, bbox.u1, bbox.v1
+    uu, vv = np.meshgrid(np.arange(u0, u1 + 1) + 0.5, np.arange(v0, v1 + 1) + 0.5, indexing="xy")
+    inside = sc["hull"].inside_voxels()
+    residuals = []
+    for v in views:
+        cam = sc["cams"][v]
+        rec = cpu.render_pixels(cam, values[None], geom.origin, geom.edge, TAU, 1.0, np.zeros(1), uu.ravel(),
+                                vv.ravel(), scattering=True, sigma_s=SIGMA_S, scatter_dirs=SCAT_DIRS)
+        src = sc["images"][v].data[bbox.slices][:, :, 0].astype(np.float64)
+        f = np.zeros((cam.height, cam.width))
+        f[v0:v1 + 1, u0:u1 + 1] = src - rec.reshape(src.shape)
+        residuals.append(f)
+    alpha_d_eff = 1.0 * (0.2 / float(np.max(geom.box.size)))
+    return cpu.adjust_pass(values, inside, [sc["cams"][v] for v in views], residuals,
+                           [sc["masks"][v].bits for v in views], (u0, v0, u1, v1), geom.origin, geom.edge, TAU,
+                           ALPHA_L, alpha_d_eff)
+
+
+def cpu_baseline(sc, budget_s):
+    from oracle import cpu
+
+    cores = os.cpu_count() or 1
+    cpu.set_threads(cores)
+    values = sc["geom"].copy().values
+    from paper_1809_06417_b200.reconstruct import _init_grid
+
+    values = _init_grid(sc["geom"], sc["hull"], "green").values
+    n_done, t_total = 0, 0.0
+    views = list(range(N_VIEWS))
+    while t_total < budget_s and n_done < 3:
+        t0 = time.perf_counter()
+        values = _oracle_iteration_sample(sc, values, views, cpu)
+        t_total += time.perf_counter() - t0
+        n_done += 1
+    return {"value": n_done / t_total, "unit": "iters/s", "cores": cores, "kind": "port",
+            "sample": f"{n_done} full iteration(s) of the workload (8 views render w/ scattering + adjust) "
+                      f"on the C/OpenMP oracle, {t_total:.1f} s",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+
+    from oracle import cpu
+
+    cores = os.cpu_count() or 1
+    cpu.set_threads(cores)
+    sc = make_scene()  # inputs are generated with the device path (same scene as the GPU arm)
+    from paper_1809_06417_b200.reconstruct import _init_grid
+
+    values = _init_grid(sc["geom"], sc["hull"], "green").values
+    # size a step: views per step so that warmup + steps stay within ~150 s
+    t0 = time.perf_counter()
+    values = _oracle_iteration_sample(sc, values, [0], cpu)
+    per_view = time.perf_counter() - t0
+    n_steps = args.steps + args.warmup
+    views_per_step = int(max(1, min(N_VIEWS, 150.0 / max(per_view * n_steps, 1e-9))))
+    times = []
+    for s in range(n_steps):
+        views = [(s * views_per_step + i) % N_VIEWS for i in range(views_per_step)]
+        t0 = time.perf_counter()
+        values = _oracle_iteration_sample(sc, values, views, cpu)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    per_step = float(np.mean(times))
+    its = views_per_step / (N_VIEWS * per_step)
+    sample = (f"each step = {views_per_step} of {N_VIEWS} views of one iteration (render w/ scattering + adjust) "
+              f"on the C/OpenMP oracle; iters/s = views_per_step / (8 * step time)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": its, "unit": "iters/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n": N_VOX, "views": N_VIEWS, "res": RES, "tau": TAU},
+        "cpu_baseline": {"value": its, "unit": "iters/s", "cores": cores, "kind": "port", "sample": sample,
+                         "cpu": _cpu_model()},
+        "e2e": {"value": its, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+    del torch
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-iters", type=int, default=50)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,224 @@
+/*
+ * fvr_b200.h -- C ABI of libfvr_b200.so, the sm_100a implementation of the
+ * iterative RTE flame-volume reconstruction loop (arXiv 1809.06417).
+ *
+ * Every entry point takes plain pointers and sizes (no torch types), is
+ * asynchronous on the caller's cudaStream_t (passed as void*), and returns
+ * an int status: FVR_OK, or an FVR_ERR_* code with a message available from
+ * fvr_last_error() (thread-local).  Device pointers are owned by the caller
+ * (the reference's ownership rule, _kernels.py: callers allocate every
+ * output and kernels write in place).  The *_host variants take host
+ * pointers and do their own staging; they are synchronous.
+ *
+ * Reference interfaces each group replaces (paths relative to
+ * /root/reference/pkg/src/fvr/):
+ *   fvr_render_rays[_host]       _kernels.py:101-186  render_rays
+ *   fvr_count_hull_samples[_host]_kernels.py:189-224  count_hull_samples
+ *   fvr_adjust_rays[_host]       _kernels.py:227-306  adjust_rays_chunked
+ *   fvr_apply_correction         reconstruct.py:221-226 (fixed-order merge + clamp)
+ *   fvr_render_pixels            render.py:183-217 render_pixels (rays built on device
+ *                                from geometry.py:125-137 pixel_rays)
+ *   fvr_loop_*                   reconstruct.py:304-334 (one iteration of the loop of
+ *                                reconstruct_channel: render, RMSE, convergence rule,
+ *                                residual, adjust_pass)
+ *   fvr_ctmap_build              radiometry.py:173-203 build_color_temp_map
+ *   fvr_temp_lookup              radiometry.py:206-219 temp_from_green +
+ *                                reconstruct.py:444-455 green_to_temp
+ *   fvr_visual_hull              volume.py:272-328 compute_visual_hull
+ */
+#ifndef FVR_B200_H
+#define FVR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FVR_ABI_VERSION 1
+
+#define FVR_OK 0
+#define FVR_ERR_INVALID 1    /* maps to ValueError */
+#define FVR_ERR_CUDA 2       /* maps to RuntimeError */
+#define FVR_ERR_EMPTY_HULL 3 /* maps to EmptyHullError */
+#define FVR_ERR_NO_FLAME 4   /* maps to NoFlameError */
+
+/* Voxel lattice geometry: nx*ny*nz cubic voxels of side `edge`, key points
+ * (nx+1)(ny+1)(nz+1) stored C-order (z fastest), volume.py:62-120. */
+typedef struct fvr_grid {
+    int32_t nx, ny, nz, reserved;
+    double origin[3];
+    double edge;
+} fvr_grid_t;
+
+/* Pinhole camera, geometry.py:24-60.  rotation is world->camera, row-major;
+ * center is the optical center -R^T t as computed by the host. */
+typedef struct fvr_camera {
+    double fx, fy, cx, cy;
+    double rotation[9];
+    double center[3];
+    int32_t width, height;
+} fvr_camera_t;
+
+/* RenderConfig (render.py:29-48) plus the kernel-level extras of
+ * render_rays (_kernels.py:101-116). */
+typedef struct fvr_render_params {
+    double tau;
+    double sigma_a;
+    double sigma_s;
+    double phase_g;
+    double gather_dist;
+    int32_t scattering; /* bool */
+    int32_t n_scat;     /* rows of scat_dirs */
+} fvr_render_params_t;
+
+/* Device-resident loop state (one per reconstruct_channel call). */
+typedef struct fvr_loop_state {
+    int32_t it;        /* iterations whose RMSE has been recorded */
+    int32_t done;      /* convergence rule fired: later launches are no-ops */
+    int32_t converged; /* trace.converged */
+    int32_t reserved;
+    double prev_rmse;
+} fvr_loop_state_t;
+
+const char* fvr_last_error(void);
+int fvr_abi_version(void);
+/* Number of kernels this library has launched since load (for bench.py's
+ * gpu_launches claim). */
+int64_t fvr_launch_count(void);
+
+/* ---- operator layer: drop-ins for fvr._kernels ------------------------- */
+
+/* render_rays: dirs (n_rays,3) f64, values (n_channels, lattice) f32,
+ * scat_dirs (n_scat,3) f64 (device), background host (n_channels) f64,
+ * out (n_rays, n_channels) f64. n_channels <= 4. */
+int fvr_render_rays(const double origin[3], const double* dirs, int64_t n_rays,
+                    const float* values, int32_t n_channels, fvr_grid_t grid,
+                    fvr_render_params_t params, const double* background,
+                    const double* scat_dirs, double* out, void* stream);
+int fvr_render_rays_host(const double origin[3], const double* dirs, int64_t n_rays,
+                         const float* values, int32_t n_channels, fvr_grid_t grid,
+                         fvr_render_params_t params, const double* background,
+                         const double* scat_dirs, double* out);
+
+/* count_hull_samples: inside_vox (nx,ny,nz) u8, counts (n_rays) i64. */
+int fvr_count_hull_samples(const double origin[3], const double* dirs, int64_t n_rays,
+                           const uint8_t* inside_vox, fvr_grid_t grid, int64_t* counts,
+                           void* stream);
+int fvr_count_hull_samples_host(const double origin[3], const double* dirs, int64_t n_rays,
+                                const uint8_t* inside_vox, fvr_grid_t grid, int64_t* counts);
+
+/* adjust_rays_chunked: deposits into a signed 32.32 fixed-point lattice
+ * accum (lattice) i64 instead of f64 chunk partials; integer sums are
+ * order-independent, so the result is bit-reproducible. */
+int fvr_adjust_rays(const double origin[3], const double* dirs, int64_t n_rays,
+                    const double* residuals, const double* g_values, const int64_t* g_offsets,
+                    int32_t use_g, const uint8_t* inside_vox, fvr_grid_t grid, double tau,
+                    double alpha_l, double alpha_d, int64_t* accum, void* stream);
+/* Host variant: same contract as the reference (partials (n_chunks,lattice)
+ * f64 accumulated in place; the device sum lands in chunk 0). */
+int fvr_adjust_rays_host(const double origin[3], const double* dirs, int64_t n_rays,
+                         const double* residuals, const double* g_values,
+                         const int64_t* g_offsets, int32_t use_g, const uint8_t* inside_vox,
+                         fvr_grid_t grid, double tau, double alpha_l, double alpha_d,
+                         double* partials, int32_t n_chunks);
+
+/* v = f32(max(f64(v) + accum * 2^-32, -1)); accum = 0 -- over the listed
+ * key points (kp_index, n_kp) or, when kp_index is NULL, over all n. */
+int fvr_apply_correction(float* values, int64_t* accum, const int32_t* kp_index, int64_t n,
+                         void* stream);
+
+/* ---- forward render of pixel centres (render_pixels / render_view) ----- */
+
+/* us, vs (n) f64 device; out (n, n_channels) f64 device.  When us == NULL
+ * the full frame is rendered with pixel centres u+0.5, v+0.5 (render_view). */
+int fvr_render_pixels(const fvr_camera_t* camera, const double* us, const double* vs,
+                      int64_t n, const float* values, int32_t n_channels, fvr_grid_t grid,
+                      fvr_render_params_t params, const double* background,
+                      const double* scat_dirs, double* out, void* stream);
+
+/* ---- one iteration of the reconstruction loop (device resident) ------- */
+
+/* Launch configuration the loop render uses; blocks_per_view sizes the
+ * sq_partials buffer (n_views * blocks_per_view f64). */
+int fvr_loop_blocks_per_view(int32_t bbox_w, int32_t bbox_h);
+
+/* Render every bbox pixel of every view, residual = src - rec (f32, (V,h,w)),
+ * per-block squared-residual sums (f64). cams is a device array. */
+int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0,
+                    int32_t bbox_w, int32_t bbox_h, const float* src, const float* values,
+                    fvr_grid_t grid, fvr_render_params_t params, double background,
+                    const double* scat_dirs, float* residual, double* sq_partials,
+                    const fvr_loop_state_t* state, void* stream);
+
+/* Back-project the residual of every listed flame ray (ray_list entries are
+ * view << 24 | (row_in_bbox * bbox_w + col_in_bbox)). stochastic != 0 draws
+ * G ~ clip(N(1, g_sigma), 0, 2) from a counter-based Philox stream keyed by
+ * seed and (iteration, ray_id_base + ray, sample), so a view-sharded run
+ * draws the same weights as a single-GPU run. */
+int fvr_loop_adjust(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
+                    int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
+                    const float* residual, const uint8_t* inside_vox, fvr_grid_t grid,
+                    double tau, double alpha_l, double alpha_d, int32_t stochastic,
+                    double g_sigma, uint64_t seed, int64_t ray_id_base, int64_t* accum,
+                    const fvr_loop_state_t* state, void* stream);
+
+/* Sum (values - truth)^2 over the listed key points into per-block f64
+ * partials (vol_rmse of the trace). Returns the block count via *n_blocks. */
+int fvr_loop_volume_sq(const float* values, const float* truth, const int32_t* kp_index,
+                       int64_t n_kp, double* partials, int32_t* n_blocks,
+                       const fvr_loop_state_t* state, void* stream);
+
+/* Per-iteration bookkeeping (1 block): per-view RMSE from sq_partials,
+ * mean over views, trace append, convergence rule (reconstruct.py:311-323).
+ * vol_partials may be NULL. */
+int fvr_loop_finalize(const double* sq_partials, int32_t n_views, int32_t blocks_per_view,
+                      int64_t pixels_per_view, const double* vol_partials,
+                      int32_t n_vol_blocks, int64_t n_kp, double converge_eps,
+                      double* trace_rmse, double* trace_vol, fvr_loop_state_t* state,
+                      void* stream);
+
+/* Clamped update over hull key points unless the state says done. */
+int fvr_loop_update(float* values, int64_t* accum, const int32_t* kp_index, int64_t n_kp,
+                    const fvr_loop_state_t* state, void* stream);
+
+/* Multi-GPU helpers: gather accum at kp_index into a compact buffer and
+ * scatter it back (the NCCL allreduce runs between them). */
+int fvr_pack_correction(const int64_t* accum, const int32_t* kp_index, int64_t n_kp,
+                        int64_t* packed, void* stream);
+int fvr_unpack_correction(const int64_t* packed, const int32_t* kp_index, int64_t n_kp,
+                          int64_t* accum, void* stream);
+
+/* ---- temperature (stage 5) --------------------------------------------- */
+
+/* Planck x CIE-1931 -> linear sRGB, clip, /max*255 (fp64).  temps (n) and
+ * entries (n,3) are device outputs; temperatures t_min + step*i. */
+int fvr_ctmap_build(double t_min, double step, int32_t n, int32_t append_t_max, double t_max,
+                    double* temps, double* entries, void* stream);
+
+/* green -> temperature through the map's green column (np.interp on the
+ * clipped value); optional idx_out (bracket index j), clamp_counts[2]
+ * (below, above).  kp_index NULL means every element of values (n). */
+int fvr_temp_lookup(const float* values, const int32_t* kp_index, int64_t n,
+                    const double* green, const double* temps, int32_t n_lut, float* temp_out,
+                    int32_t* idx_out, int64_t* clamp_counts, void* stream);
+
+/* Same lookup on f64 inputs (temp_from_green on arrays). */
+int fvr_temp_from_green(const double* g, int64_t n, const double* green, const double* temps,
+                        int32_t n_lut, double* temp_out, uint8_t* clamped_out, void* stream);
+
+/* ---- visual hull (volume.py:272-328) ----------------------------------- */
+
+/* OR bit `view_bit` into tags (nx,ny,nz) u32 for every voxel whose projected
+ * footprint in the camera overlaps a flame pixel.  translation is the
+ * camera's t (x_cam = R x + t); sat is the (h+1,w+1) i64 summed-area table
+ * of the view's mask (device). */
+int fvr_visual_hull_view(const fvr_camera_t* camera, const double translation[3],
+                         fvr_grid_t grid, const int64_t* sat, int32_t view_bit, uint32_t* tags,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FVR_B200_H */

@@ -1,0 +1,240 @@
+/*
+ * fvr_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * CPU restatement of the three numba kernels of the reference package
+ * (/root/reference/pkg/src/fvr/_kernels.py).  It is the parity checker for
+ * the sm_100a path and the `cpu_baseline` / `--impl reference` arm of
+ * bench.py ("kind": "port").  Nothing in paper_1809_06417_b200/ links or
+ * calls it; only tests/, __graft_entry__.smoke() and bench.py may.
+ *
+ * Arithmetic contract (mirrors _kernels.py:1-11): IEEE double, no FMA
+ * contraction (built with -ffp-contract=off), every expression evaluated in
+ * the same order as the reference source, so the result is bit-identical to
+ * the numba build for any thread count.  Rays are processed by OpenMP
+ * workers; the back-projection uses a fixed chunk split with one partial
+ * lattice per chunk (_kernels.py:243-259), merged by the caller in order.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define MARCH_COUNT_EPS 1e-9 /* _kernels.py:25 */
+
+static const double PI = 3.141592653589793; /* np.pi */
+
+int oracle_set_threads(int n) {
+#ifdef _OPENMP
+    if (n < 1) n = 1;
+    omp_set_num_threads(n);
+    return n;
+#else
+    (void)n;
+    return 1;
+#endif
+}
+
+int oracle_get_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+/* Slab clip, _kernels.py:36-63.  Returns 1 on hit. */
+static inline int slab_span(const double o[3], const double d[3], const double lo[3],
+                            const double hi[3], double* t_in, double* t_out) {
+    double tmin = -1.0e300, tmax = 1.0e300;
+    for (int a = 0; a < 3; ++a) {
+        if (d[a] == 0.0) {
+            if (o[a] < lo[a] || o[a] > hi[a]) return 0;
+        } else {
+            double t0 = (lo[a] - o[a]) / d[a];
+            double t1 = (hi[a] - o[a]) / d[a];
+            if (t0 > t1) { double s = t0; t0 = t1; t1 = s; }
+            if (t0 > tmin) tmin = t0;
+            if (t1 < tmax) tmax = t1;
+        }
+    }
+    double te = tmin > 0.0 ? tmin : 0.0;
+    if (tmax <= te) return 0;
+    *t_in = te;
+    *t_out = tmax;
+    return 1;
+}
+
+static inline int clampi(int v, int hi) { return v < 0 ? 0 : (v > hi ? hi : v); }
+
+/* Clamped trilinear read with negative corners clamped to zero,
+ * _kernels.py:66-98 (loop order dz, dy, dx; weight product wx*wy*wz*v). */
+static inline double tri_clamped(const float* vals, double qx, double qy, double qz, int nx,
+                                 int ny, int nz) {
+    int ix = clampi((int)floor(qx), nx - 1);
+    int iy = clampi((int)floor(qy), ny - 1);
+    int iz = clampi((int)floor(qz), nz - 1);
+    double fx = qx - ix, fy = qy - iy, fz = qz - iz;
+    const int64_t sy = nz + 1, sx = (int64_t)(ny + 1) * (nz + 1);
+    double acc = 0.0;
+    for (int dz = 0; dz < 2; ++dz) {
+        double wz = dz == 1 ? fz : 1.0 - fz;
+        for (int dy = 0; dy < 2; ++dy) {
+            double wy = dy == 1 ? fy : 1.0 - fy;
+            for (int dx = 0; dx < 2; ++dx) {
+                double wx = dx == 1 ? fx : 1.0 - fx;
+                double v = vals[(ix + dx) * sx + (iy + dy) * sy + (iz + dz)];
+                if (v < 0.0) v = 0.0;
+                acc += wx * wy * wz * v;
+            }
+        }
+    }
+    return acc;
+}
+
+/* render_rays, _kernels.py:101-186.  values: (nch, nx+1, ny+1, nz+1) f32
+ * C-order; out: (n_rays, nch) f64. */
+void oracle_render_rays(const double* origin, const double* dirs, int64_t n_rays,
+                        const float* values, int nch, int nx, int ny, int nz,
+                        const double* grid_origin, double edge, double tau, double sigma_a,
+                        const double* background, int scattering, double sigma_s,
+                        const double* scat_dirs, int n_scat, double phase_g, double gather_dist,
+                        double* out) {
+    const double lo[3] = {grid_origin[0], grid_origin[1], grid_origin[2]};
+    const double hi[3] = {lo[0] + nx * edge, lo[1] + ny * edge, lo[2] + nz * edge};
+    const int64_t plane = (int64_t)(nx + 1) * (ny + 1) * (nz + 1);
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t r = 0; r < n_rays; ++r) {
+        const double d[3] = {dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2]};
+        double te = 0.0, tx = 0.0;
+        int hit = slab_span(origin, d, lo, hi, &te, &tx);
+        double t_dst = 1.0;
+        double l_dst[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (hit) {
+            int64_t n = (int64_t)floor((tx - te) / edge + MARCH_COUNT_EPS);
+            for (int64_t k = 1; k <= n; ++k) {
+                double t = te + (k - 0.5) * edge;
+                double px = origin[0] + t * d[0];
+                double py = origin[1] + t * d[1];
+                double pz = origin[2] + t * d[2];
+                double qx = (px - lo[0]) / edge;
+                double qy = (py - lo[1]) / edge;
+                double qz = (pz - lo[2]) / edge;
+                for (int c = 0; c < nch; ++c) {
+                    const float* vc = values + c * plane;
+                    double l_src = sigma_a * tri_clamped(vc, qx, qy, qz, nx, ny, nz);
+                    if (scattering && sigma_s > 0.0) {
+                        double acc = 0.0;
+                        for (int s = 0; s < n_scat; ++s) {
+                            const double* sd = scat_dirs + 3 * s;
+                            double sx = px + 0.5 * gather_dist * sd[0];
+                            double sy = py + 0.5 * gather_dist * sd[1];
+                            double sz = pz + 0.5 * gather_dist * sd[2];
+                            if (lo[0] <= sx && sx <= hi[0] && lo[1] <= sy && sy <= hi[1] &&
+                                lo[2] <= sz && sz <= hi[2]) {
+                                double e = tri_clamped(vc, (sx - lo[0]) / edge, (sy - lo[1]) / edge,
+                                                       (sz - lo[2]) / edge, nx, ny, nz);
+                                double mu = d[0] * sd[0] + d[1] * sd[1] + d[2] * sd[2];
+                                double ph = (1.0 - phase_g * phase_g) /
+                                            (4.0 * PI *
+                                             pow(1.0 + phase_g * phase_g + 2.0 * phase_g * mu, 1.5));
+                                acc += e * ph;
+                            }
+                        }
+                        l_src += sigma_s * acc * 4.0 * PI / (double)n_scat;
+                    }
+                    l_dst[c] += t_dst * (tau * l_src);
+                }
+                t_dst *= 1.0 - tau;
+            }
+        }
+        for (int c = 0; c < nch; ++c) out[r * nch + c] = l_dst[c] + t_dst * background[c];
+    }
+}
+
+/* Cell index of a sample, _kernels.py:207-221 / 275-289. */
+static inline void sample_cell(const double p[3], const double lo[3], double edge, int nx, int ny,
+                               int nz, int* ix, int* iy, int* iz) {
+    *ix = clampi((int)floor((p[0] - lo[0]) / edge), nx - 1);
+    *iy = clampi((int)floor((p[1] - lo[1]) / edge), ny - 1);
+    *iz = clampi((int)floor((p[2] - lo[2]) / edge), nz - 1);
+}
+
+/* count_hull_samples, _kernels.py:189-224.  inside_vox: (nx, ny, nz) u8. */
+void oracle_count_hull_samples(const double* origin, const double* dirs, int64_t n_rays,
+                               const uint8_t* inside_vox, int nx, int ny, int nz,
+                               const double* grid_origin, double edge, int64_t* counts) {
+    const double lo[3] = {grid_origin[0], grid_origin[1], grid_origin[2]};
+    const double hi[3] = {lo[0] + nx * edge, lo[1] + ny * edge, lo[2] + nz * edge};
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t r = 0; r < n_rays; ++r) {
+        const double d[3] = {dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2]};
+        double te = 0.0, tx = 0.0;
+        int64_t n_in = 0;
+        if (slab_span(origin, d, lo, hi, &te, &tx)) {
+            int64_t n = (int64_t)floor((tx - te) / edge + MARCH_COUNT_EPS);
+            for (int64_t k = 1; k <= n; ++k) {
+                double t = te + (k - 0.5) * edge;
+                double p[3] = {origin[0] + t * d[0], origin[1] + t * d[1], origin[2] + t * d[2]};
+                int ix, iy, iz;
+                sample_cell(p, lo, edge, nx, ny, nz, &ix, &iy, &iz);
+                if (inside_vox[((int64_t)ix * ny + iy) * nz + iz]) n_in++;
+            }
+        }
+        counts[r] = n_in;
+    }
+}
+
+/* adjust_rays_chunked, _kernels.py:227-306.  partials: (n_chunks, nx+1, ny+1,
+ * nz+1) f64, accumulated in place.  The chunk split depends only on n_rays. */
+void oracle_adjust_rays_chunked(const double* origin, const double* dirs, int64_t n_rays,
+                                const double* residuals, const double* g_values,
+                                const int64_t* g_offsets, int use_g, const uint8_t* inside_vox,
+                                int nx, int ny, int nz, const double* grid_origin, double edge,
+                                double tau, double alpha_l, double alpha_d, double* partials,
+                                int n_chunks) {
+    const double lo[3] = {grid_origin[0], grid_origin[1], grid_origin[2]};
+    const double hi[3] = {lo[0] + nx * edge, lo[1] + ny * edge, lo[2] + nz * edge};
+    const int64_t sy = nz + 1, sx = (int64_t)(ny + 1) * (nz + 1);
+    const int64_t plane = (int64_t)(nx + 1) * sx;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int chunk = 0; chunk < n_chunks; ++chunk) {
+        double* acc = partials + chunk * plane;
+        int64_t r0 = chunk * n_rays / n_chunks;
+        int64_t r1 = (chunk + 1) * n_rays / n_chunks;
+        for (int64_t r = r0; r < r1; ++r) {
+            const double d[3] = {dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2]};
+            double te = 0.0, tx = 0.0;
+            if (!slab_span(origin, d, lo, hi, &te, &tx)) continue;
+            int64_t n = (int64_t)floor((tx - te) / edge + MARCH_COUNT_EPS);
+            double trans = 1.0;
+            int64_t gi = g_offsets[r];
+            for (int64_t k = 1; k <= n; ++k) {
+                double t = te + (k - 0.5) * edge;
+                double p[3] = {origin[0] + t * d[0], origin[1] + t * d[1], origin[2] + t * d[2]};
+                int ix, iy, iz;
+                sample_cell(p, lo, edge, nx, ny, nz, &ix, &iy, &iz);
+                if (inside_vox[((int64_t)ix * ny + iy) * nz + iz]) {
+                    double g = use_g ? g_values[gi] : 1.0;
+                    gi++;
+                    double base = alpha_l * residuals[r] * trans * g;
+                    for (int cz = 0; cz < 2; ++cz) {
+                        double wz = lo[2] + (iz + cz) * edge;
+                        for (int cy = 0; cy < 2; ++cy) {
+                            double wy = lo[1] + (iy + cy) * edge;
+                            for (int cx = 0; cx < 2; ++cx) {
+                                double wx = lo[0] + (ix + cx) * edge;
+                                double ex = p[0] - wx, ey = p[1] - wy, ez = p[2] - wz;
+                                double dist = sqrt(ex * ex + ey * ey + ez * ez);
+                                acc[(ix + cx) * sx + (iy + cy) * sy + (iz + cz)] +=
+                                    base * exp(-alpha_d * dist);
+                            }
+                        }
+                    }
+                }
+                trans *= 1.0 - tau;
+            }
+        }
+    }
+}

@@ -1,0 +1,61 @@
+// fvr_internal.cuh -- host-side plumbing shared by the C-ABI translation
+// units: error reporting (fvr_last_error), argument checks, launch counting,
+// and the render constants block passed by value to the kernels.
+#pragma once
+
+#include <atomic>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "fvr_common.cuh"
+
+namespace fvr {
+
+struct RenderConsts {
+    double tau, one_minus_tau, sigma_a, sigma_s, phase_g, half_gather;
+    double scat_scale;  // sigma_s*4π/S, times 1/4π when g == 0 (ph folded in)
+    double bg[4];
+    int n_scat;
+};
+
+inline RenderConsts make_render_consts(const fvr_render_params_t& p, const double* bg, int nch) {
+    RenderConsts rc;
+    rc.tau = p.tau;
+    rc.one_minus_tau = 1.0 - p.tau;
+    rc.sigma_a = p.sigma_a;
+    rc.sigma_s = p.sigma_s;
+    rc.phase_g = p.phase_g;
+    rc.half_gather = 0.5 * p.gather_dist;
+    rc.n_scat = p.n_scat > 0 ? p.n_scat : 1;
+    const double four_pi = 4.0 * kPi;
+    const double ph0 = 1.0 / four_pi;  // phase_hg at g = 0 (radiometry.py:78-92)
+    rc.scat_scale = p.sigma_s * four_pi / (double)rc.n_scat;
+    if (p.phase_g == 0.0) rc.scat_scale *= ph0;
+    for (int c = 0; c < 4; ++c) rc.bg[c] = (bg && c < nch) ? bg[c] : 0.0;
+    return rc;
+}
+
+int set_error(int code, const std::string& msg);
+int check_launch(const char* what);
+void count_launch(int n = 1);
+
+inline int check_grid(const fvr_grid_t& g) {
+    if (g.nx < 1 || g.ny < 1 || g.nz < 1) return set_error(FVR_ERR_INVALID, "voxel counts must be >= 1");
+    if (!(g.edge > 0.0)) return set_error(FVR_ERR_INVALID, "voxel edge must be positive");
+    const double kp = (double)(g.nx + 1) * (g.ny + 1) * (g.nz + 1);
+    if (kp * 4.0 > 2147483647.0) return set_error(FVR_ERR_INVALID, "lattice too large for 32-bit indexing");
+    return FVR_OK;
+}
+
+}  // namespace fvr
+
+#define FVR_TRY_BEGIN try {
+#define FVR_TRY_END                                                   \
+    }                                                                 \
+    catch (const std::exception& e) {                                 \
+        return ::fvr::set_error(FVR_ERR_CUDA, e.what());              \
+    }                                                                 \
+    catch (...) {                                                     \
+        return ::fvr::set_error(FVR_ERR_CUDA, "unknown C++ exception"); \
+    }

@@ -1,0 +1,321 @@
+"""Device-resident reconstruction loop (one scalar channel).
+
+One iteration of reconstruct_channel (reconstruct.py:304-334) is four
+kernels on one stream, in this order:
+
+  K-render   every bbox pixel of every view: ray, march, residual, per-block
+             squared-residual partials                    (csrc/fvr_render.cu)
+  K-adjust   every flame ray: march again, back-project the residual into a
+             32.32 fixed-point correction lattice          (csrc/fvr_adjust.cu)
+  K-finalize per-view RMSE, mean, trace append, convergence rule (1 block)
+  K-update   v = f32(max(v + delta, -1)) on hull key points, skipped when the
+             rule fired                                      (csrc/fvr_loop.cu)
+
+The adjust runs speculatively before the convergence decision; when the rule
+fires the correction is discarded, which is exactly the reference's
+break-before-adjust.  Once the state says ``done`` every later launch is a
+no-op, so the host can enqueue iterations (or replay a captured CUDA graph)
+without a per-iteration round trip and read the trace back at the end.
+
+With torch.distributed initialised (world_size > 1) the views are sharded in
+contiguous ranges across ranks; each rank renders and back-projects its own
+views into a full-size correction, and one NCCL all-reduce per iteration of
+an int64 buffer [packed correction at hull key points | squared-residual
+partials of every view] makes every rank's lattice identical.  Integer sums
+are exact, so 1, 2, 4 or 8 GPUs give bit-identical grids.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+
+@dataclass
+class LoopConfig:
+    tau: float
+    alpha_l: float
+    alpha_d_eff: float
+    converge_eps: float
+    stochastic: bool
+    g_sigma: float
+    seed: int
+
+
+def _world():
+    """(rank, world_size, group) when torch.distributed is initialised."""
+    if os.environ.get("FVR_NO_SHARDING") == "1":
+        return 0, 1
+    t = _lib.torch()
+    if t.distributed.is_available() and t.distributed.is_initialized():
+        return t.distributed.get_rank(), t.distributed.get_world_size()
+    return 0, 1
+
+
+def shard_views(n_views: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced view range [begin, end) of one rank."""
+    base, extra = divmod(n_views, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+class ChannelLoop:
+    """Owns the device buffers of one reconstruct_channel call."""
+
+    def __init__(self, cameras, grid_geom, values, src_blocks, masks, bbox, inside, kp_mask,
+                 render_cfg, loop_cfg: LoopConfig, max_iters: int, ground_truth=None,
+                 background: float = 0.0, use_graph: bool = True):
+        t = _lib.torch()
+        self.t = t
+        self.dev = _lib.device()
+        self.rank, self.world = _world()
+        V = len(cameras)
+        self.n_views = V
+        self.v_begin, self.v_end = shard_views(V, self.rank, self.world)
+        local = list(range(self.v_begin, self.v_end))
+        self.bbox = bbox
+        self.w_bb, self.h_bb = bbox.u1 - bbox.u0 + 1, bbox.v1 - bbox.v0 + 1
+        self.grid = _lib.grid_struct(grid_geom)
+        self.cfg = loop_cfg
+        self.max_iters = int(max_iters)
+        dev = self.dev
+
+        # geometry and inputs
+        self.cams = _lib.cameras_tensor([cameras[v] for v in local], dev) if local else None
+        self.src = t.from_numpy(np.ascontiguousarray(np.stack([src_blocks[v] for v in local]) if local
+                                                     else np.zeros((1, 1, 1), np.float32))).to(dev)
+        self.values = t.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(dev)
+        self.accum = t.zeros(values.shape, dtype=t.int64, device=dev)
+        self.inside = t.from_numpy(np.ascontiguousarray(inside, dtype=np.uint8)).to(dev)
+        kp_idx = np.flatnonzero(kp_mask.ravel()).astype(np.int32)
+        self.n_kp = int(kp_idx.size)
+        self.kp = t.from_numpy(kp_idx if kp_idx.size else np.zeros(1, np.int32)).to(dev)
+
+        # flame rays of the local views, row-major per view (reconstruct.py:144-149)
+        entries = []
+        ray_base = 0
+        for v in range(V):
+            sub = masks[v].bits[bbox.slices]
+            rows, cols = np.nonzero(sub)
+            if v < self.v_begin:
+                ray_base += rows.size
+            elif v < self.v_end:
+                lv = v - self.v_begin
+                entries.append((np.int64(lv) << 24) | (rows.astype(np.int64) * self.w_bb + cols))
+        ray_list = np.concatenate(entries).astype(np.int32) if entries else np.zeros(0, np.int32)
+        self.n_rays = int(ray_list.size)
+        self.ray_base = ray_base
+        self.rays = t.from_numpy(ray_list if ray_list.size else np.zeros(1, np.int32)).to(dev)
+
+        # render configuration of the loop (render_pixels without a phase: g = 0)
+        self.scattering = bool(render_cfg.scattering_enabled and render_cfg.sigma_s > 0.0)
+        if self.scattering:
+            from .radiometry import fibonacci_sphere
+
+            sd = fibonacci_sphere(render_cfg.scatter_dirs)
+            self.scat = t.from_numpy(np.ascontiguousarray(sd)).to(dev)
+            n_scat = sd.shape[0]
+        else:
+            self.scat = None
+            n_scat = 1
+        self.params = _lib.render_params(render_cfg, self.scattering, n_scat, 0.0, grid_geom.edge)
+        self.background = float(background)
+
+        # work buffers
+        self.bpv = int(_lib.load().fvr_loop_blocks_per_view(self.w_bb, self.h_bb))
+        self.residual = t.zeros((max(len(local), 1), self.h_bb, self.w_bb), dtype=t.float32, device=dev)
+        self.n_sq = V * self.bpv
+        # [packed correction (n_kp) | sq partials (V*bpv) | vol partials] in one int64 buffer
+        nvb = ctypes.c_int32(0)
+        _lib.call("fvr_loop_volume_sq", None, None, None, self.n_kp, None, ctypes.byref(nvb), None, None)
+        self.n_vol = int(nvb.value) if ground_truth is not None else 0
+        self.comm = t.zeros(self.n_kp + self.n_sq + self.n_vol + 1, dtype=t.int64, device=dev)
+        self.sq = self.comm[self.n_kp:self.n_kp + self.n_sq].view(t.float64)
+        self.vol = self.comm[self.n_kp + self.n_sq:self.n_kp + self.n_sq + self.n_vol].view(t.float64) \
+            if self.n_vol else None
+        self.packed = self.comm[: self.n_kp]
+        self.truth = (t.from_numpy(np.ascontiguousarray(ground_truth, dtype=np.float32)).to(dev)
+                      if ground_truth is not None else None)
+        self.state = t.zeros(6, dtype=t.int32, device=dev)  # fvr_loop_state_t (24 B)
+        self.trace = t.zeros(max(self.max_iters, 1), dtype=t.float64, device=dev)
+        self.trace_vol = t.zeros(max(self.max_iters, 1), dtype=t.float64, device=dev) \
+            if ground_truth is not None else None
+        self.use_graph = use_graph and self.world == 1 and os.environ.get("FVR_NO_GRAPH") != "1"
+        self.graph = None
+        self.launches_per_iter = 0
+
+    # -- one iteration ---------------------------------------------------------
+    def _render(self, stream):
+        if self.v_end <= self.v_begin:
+            return 0
+        sq_local = self.sq[self.v_begin * self.bpv:]
+        _lib.call(
+            "fvr_loop_render", self.cams.data_ptr(), self.v_end - self.v_begin, self.bbox.u0,
+            self.bbox.v0, self.w_bb, self.h_bb, self.src.data_ptr(), self.values.data_ptr(),
+            self.grid, self.params, self.background, _lib.ptr(self.scat), self.residual.data_ptr(),
+            sq_local.data_ptr(), self.state.data_ptr(), stream,
+        )
+        return 1
+
+    def _adjust(self, stream):
+        if self.n_rays == 0:
+            return 0
+        c = self.cfg
+        _lib.call(
+            "fvr_loop_adjust", self.cams.data_ptr(), self.rays.data_ptr(), self.n_rays,
+            self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb, self.residual.data_ptr(),
+            self.inside.data_ptr(), self.grid, c.tau, c.alpha_l, c.alpha_d_eff,
+            1 if c.stochastic else 0, c.g_sigma, c.seed & 0xFFFFFFFFFFFFFFFF, self.ray_base,
+            self.accum.data_ptr(), self.state.data_ptr(), stream,
+        )
+        return 1
+
+    def _volume(self, stream):
+        if self.truth is None:
+            return 0
+        nvb = ctypes.c_int32(0)
+        _lib.call(
+            "fvr_loop_volume_sq", self.values.data_ptr(), self.truth.data_ptr(), self.kp.data_ptr(),
+            self.n_kp, self.vol.data_ptr(), ctypes.byref(nvb), self.state.data_ptr(), stream,
+        )
+        return 1
+
+    def _finalize(self, stream):
+        pix = self.w_bb * self.h_bb
+        _lib.call(
+            "fvr_loop_finalize", self.sq.data_ptr(), self.n_views, self.bpv, pix,
+            _lib.ptr(self.vol), self.n_vol, self.n_kp, self.cfg.converge_eps,
+            self.trace.data_ptr(), _lib.ptr(self.trace_vol), self.state.data_ptr(), stream,
+        )
+        return 1
+
+    def _update(self, stream):
+        if self.n_kp == 0:
+            return 0
+        _lib.call(
+            "fvr_loop_update", self.values.data_ptr(), self.accum.data_ptr(), self.kp.data_ptr(),
+            self.n_kp, self.state.data_ptr(), stream,
+        )
+        return 1
+
+    def _allreduce(self, stream):
+        """Sum corrections and RMSE partials over ranks (exact: int64)."""
+        t = self.t
+        # rows of views other ranks own must contribute exactly zero
+        self.sq[: self.v_begin * self.bpv].zero_()
+        self.sq[self.v_end * self.bpv:].zero_()
+        if self.rank != 0 and self.vol is not None:
+            self.vol.zero_()
+        if self.n_kp:
+            _lib.call("fvr_pack_correction", self.accum.data_ptr(), self.kp.data_ptr(), self.n_kp,
+                      self.packed.data_ptr(), stream)
+        t.distributed.all_reduce(self.comm)
+        if self.n_kp:
+            _lib.call("fvr_unpack_correction", self.packed.data_ptr(), self.kp.data_ptr(), self.n_kp,
+                      self.accum.data_ptr(), stream)
+        return 2 if self.n_kp else 0
+
+    def pre_decision(self, stream) -> int:
+        n = self._render(stream) + self._volume(stream) + self._adjust(stream)
+        if self.world > 1:
+            n += self._allreduce(stream)
+        n += self._finalize(stream)
+        return n
+
+    def post_decision(self, stream) -> int:
+        return self._update(stream)
+
+    def launch_iteration(self) -> None:
+        stream = _lib.stream_ptr()
+        self.launches_per_iter = self.pre_decision(stream) + self.post_decision(stream)
+
+    def capture(self) -> None:
+        """Capture one iteration into a CUDA graph (single-GPU only)."""
+        t = self.t
+        g = t.cuda.CUDAGraph()
+        side = t.cuda.Stream()
+        side.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(side):
+            with t.cuda.graph(g, stream=side):
+                self.launch_iteration()
+        t.cuda.current_stream().wait_stream(side)
+        self.graph = g
+
+    def step(self) -> None:
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.launch_iteration()
+
+    # -- the loop ----------------------------------------------------------------
+    def reset_state(self) -> None:
+        self.state.zero_()
+        self.accum.zero_()
+
+    def read_state(self) -> dict:
+        s = self.state.cpu().numpy()
+        prev = s[4:6].copy().view(np.float64)[0]
+        return {"it": int(s[0]), "done": int(s[1]), "converged": int(s[2]), "prev_rmse": float(prev)}
+
+    def run(self, callback=None, chunk: int = 8):
+        """Iterate until the rule fires or max_iters; returns (iterations,
+        converged, wall_ms per iteration)."""
+        t = self.t
+        wall = []
+        if callback is not None:
+            for _ in range(self.max_iters):
+                t0 = time.perf_counter()
+                stream = _lib.stream_ptr()
+                self.pre_decision(stream)
+                st = self.read_state()
+                rmse = float(self.trace[st["it"] - 1].item())
+                wall.append((time.perf_counter() - t0) * 1e3)
+                callback(st["it"], self.host_values(), rmse)
+                if st["done"]:
+                    break
+                self.post_decision(stream)
+            st = self.read_state()
+            return st["it"], bool(st["converged"]), wall
+        if self.use_graph and self.graph is None and self.max_iters > 1:
+            self.capture()
+        # keep one chunk in flight: after enqueueing chunk i, wait for chunk
+        # i-1's state copy and stop once its sticky `done` flag is set
+        bufs = [t.zeros(6, dtype=t.int32, pin_memory=True) for _ in range(2)]
+        events = [None, None]
+        issued, i = 0, 0
+        t_start = time.perf_counter()
+        while issued < self.max_iters:
+            n = min(chunk, self.max_iters - issued)
+            for _ in range(n):
+                self.step()
+            issued += n
+            b = i & 1
+            bufs[b].copy_(self.state, non_blocking=True)
+            events[b] = t.cuda.Event()
+            events[b].record()
+            if i >= 1:
+                events[b ^ 1].synchronize()
+                if int(bufs[b ^ 1][1]):
+                    break
+            i += 1
+        t.cuda.synchronize()
+        total_ms = (time.perf_counter() - t_start) * 1e3
+        st = self.read_state()
+        it = st["it"]
+        wall = [total_ms / max(it, 1)] * it
+        return it, bool(st["converged"]), wall
+
+    # -- results -----------------------------------------------------------------
+    def host_values(self) -> np.ndarray:
+        return self.values.cpu().numpy()
+
+    def host_trace(self, iterations: int):
+        rmse = self.trace[:iterations].cpu().numpy().tolist()
+        vol = self.trace_vol[:iterations].cpu().numpy().tolist() if self.trace_vol is not None else []
+        return rmse, vol

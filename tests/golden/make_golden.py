@@ -1,0 +1,245 @@
+"""Generate the golden vectors that pin the oracle and the CUDA path.
+
+Runs the REFERENCE package itself (fvr, /root/reference/pkg) from a scratch
+copy -- never from /root/reference directly, numba's cache would write into
+it -- and stores its inputs and outputs as small .npz fixtures next to this
+script.  Run here (the reference cannot travel to the GPU box):
+
+    python tests/golden/make_golden.py
+
+Fixtures:
+  config1.npz      BASELINE config 1: 32^3 flame, 4 views 64x64, tau 0.05,
+                   emission only; truth, images, masks, bbox, hull tags, and
+                   the green channel after 10 deterministic iterations + trace
+  loop_scatter.npz 16^3 flame, 4 views 48x48, single scattering (32 dirs),
+                   5 deterministic iterations of the green channel
+  kernels.npz      direct _kernels calls on random + edge-case rays:
+                   render_rays (emission, scattering g=0 and g=0.4),
+                   count_hull_samples, adjust_rays_chunked (with and without G)
+  render.npz       render_view of RGB grids (plain and scattering)
+  ctmap.npz        build_color_temp_map(1000, 2300, 1), CIE table,
+                   temp_from_green on random / node / clamped greens
+  tiny_color.npz   reconstruct_color on the reference tests' tiny_scene
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SCRATCH = "/tmp/fvr_ref_golden"
+
+
+def _import_reference():
+    if not os.path.isdir(SCRATCH):
+        shutil.copytree("/root/reference/pkg", SCRATCH)
+    sys.path.insert(0, os.path.join(SCRATCH, "src"))
+    import fvr  # noqa: F401
+
+    return fvr
+
+
+def make_ring_camera(azimuth_deg, radius=0.3, width=80, height=60, fov_deg=60.0):
+    """The reference tests' ring camera (pkg/tests/conftest.py:22-29)."""
+    from fvr.geometry import Camera, look_at
+
+    a = np.radians(azimuth_deg)
+    R, t = look_at(radius * np.array([np.cos(a), np.sin(a), 0.0]), (0.0, 0.0, 0.0))
+    f = (height / 2.0) / np.tan(np.radians(fov_deg) / 2.0)
+    return Camera(fx=f, fy=f, cx=width / 2.0, cy=height / 2.0, rotation=R, translation=t, width=width,
+                  height=height)
+
+
+def cam_arrays(cams):
+    return {
+        "cam_fx": np.array([c.fx for c in cams]),
+        "cam_fy": np.array([c.fy for c in cams]),
+        "cam_cx": np.array([c.cx for c in cams]),
+        "cam_cy": np.array([c.cy for c in cams]),
+        "cam_R": np.stack([c.rotation for c in cams]),
+        "cam_t": np.stack([c.translation for c in cams]),
+        "cam_w": np.array([c.width for c in cams]),
+        "cam_h": np.array([c.height for c in cams]),
+    }
+
+
+def scene(fvr, n, views, res, tau, scattering=False, sigma_s=0.0, seed=0):
+    from fvr.preprocess import bounding_box, threshold_mask
+    from fvr.render import RenderConfig, render_view
+    from fvr.synth import synth_cameras, synth_volume
+    from fvr.volume import VoxelGrid, compute_visual_hull
+
+    vols = synth_volume((n, n, n), seed=seed, kind="flame")
+    truth = [vols[t] for t in ("red", "green", "blue")]
+    cams = synth_cameras(views, radius=0.38, fov=60.0, elevation_jitter_deg=5.0, width=res, height=res,
+                         seed=seed)
+    rcfg = RenderConfig(tau=tau, scattering_enabled=scattering, sigma_s=sigma_s, scatter_dirs=32)
+    imgs = [render_view(c, truth, None, rcfg) for c in cams]
+    masked = [threshold_mask(im) for im in imgs]
+    masks = [m for m, _ in masked]
+    blanked = [im for _, im in masked]
+    bbox = bounding_box(masks, 4)
+    geom = VoxelGrid(n, n, n, truth[0].origin, truth[0].edge)
+    hull = compute_visual_hull(geom, [m.bits for m in masks], cams)
+    return truth, cams, imgs, masks, blanked, bbox, geom, hull, rcfg
+
+
+def make_loop(fvr, path, n, views, res, tau, iters, scattering=False, sigma_s=0.0):
+    from fvr.reconstruct import ReconstructionConfig, reconstruct_channel
+
+    truth, cams, imgs, masks, blanked, bbox, geom, hull, rcfg = scene(
+        fvr, n, views, res, tau, scattering, sigma_s)
+    cfg = ReconstructionConfig(alpha_l=0.006, alpha_d=1.0, tau=tau, max_iters=iters, converge_eps=1e-12,
+                               deterministic_mode=True)
+    green, trace = reconstruct_channel([im.channel(1) for im in blanked], cams, geom, hull, cfg,
+                                       render_cfg=rcfg, masks=masks, bbox=bbox, tag="green")
+    np.savez_compressed(
+        path,
+        n=n, tau=tau, scattering=scattering, sigma_s=sigma_s, iters=iters,
+        origin=geom.origin, edge=geom.edge,
+        truth=np.stack([g.values for g in truth]),
+        images=np.stack([im.data for im in imgs]),
+        blanked=np.stack([im.data for im in blanked]),
+        masks=np.stack([m.bits for m in masks]),
+        bbox=np.array([bbox.u0, bbox.v0, bbox.u1, bbox.v1]),
+        hull_tags=hull.tags,
+        green=green.values,
+        rmse=np.array(trace.rmse),
+        converged=trace.converged,
+        alpha_d_eff=cfg.effective_alpha_d(geom),
+        **cam_arrays(cams),
+    )
+    print(path, "iters", trace.iterations, "rmse", trace.rmse[0], trace.rmse[-1])
+
+
+def make_kernels(fvr, path):
+    from fvr import _kernels
+    from fvr.radiometry import fibonacci_sphere
+
+    rng = np.random.default_rng(123)
+    n = 16
+    edge = 0.2 / n
+    lo = np.array([-0.1, -0.1, -0.1])
+    vals = rng.uniform(-1.0, 200.0, size=(2, n + 1, n + 1, n + 1)).astype(np.float32)
+    origin = np.array([0.05, -0.42, 0.03])
+    d = rng.normal(size=(600, 3))
+    d[:, 1] = np.abs(d[:, 1]) + 1.5  # mostly toward the box
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    # edge cases: axis-aligned directions with zero components, grazing rays, misses
+    extra = np.array([[0.0, 1.0, 0.0], [0.0, -1.0, 0.0], [1.0, 0.0, 0.0], [0.0, 0.0, 1.0],
+                      [np.sqrt(0.5), np.sqrt(0.5), 0.0], [0.0, np.sqrt(0.5), np.sqrt(0.5)]])
+    dirs = np.ascontiguousarray(np.vstack([d, extra]))
+    bg = np.array([3.0, 7.0])
+    out = {}
+    for name, scat, sig, g, nd in (("plain", False, 0.0, 0.0, 1), ("scat", True, 0.3, 0.0, 32),
+                                   ("scat_g", True, 0.3, 0.4, 16)):
+        res = np.empty((dirs.shape[0], 2))
+        sd = fibonacci_sphere(nd) if scat else np.zeros((1, 3))
+        _kernels.render_rays(origin, dirs, vals, lo, edge, 0.05, 1.0, bg, scat, sig, sd, g, edge, res)
+        out["render_" + name] = res
+    # an origin inside the box (t_entry clamps to 0)
+    inner = np.array([0.01, 0.02, -0.03])
+    res = np.empty((dirs.shape[0], 2))
+    _kernels.render_rays(inner, dirs, vals, lo, edge, 0.05, 1.0, bg, False, 0.0, np.zeros((1, 3)), 0.0, edge, res)
+    out["render_inner"] = res
+    inside = (rng.random((n, n, n)) > 0.3).astype(np.uint8)
+    counts = np.empty(dirs.shape[0], dtype=np.int64)
+    _kernels.count_hull_samples(origin, dirs, inside, lo, edge, counts)
+    out["counts"] = counts
+    resid = rng.normal(0.0, 20.0, size=dirs.shape[0])
+    parts = np.zeros((16, n + 1, n + 1, n + 1))
+    _kernels.adjust_rays_chunked(origin, dirs, resid, np.ones(1), np.zeros(dirs.shape[0], np.int64), False,
+                                 inside, lo, edge, 0.05, 0.006, 1.0, parts)
+    out["adjust_det"] = parts.sum(axis=0)
+    offs = np.zeros(dirs.shape[0], np.int64)
+    np.cumsum(counts[:-1], out=offs[1:])
+    total = int(offs[-1] + counts[-1])
+    gv = np.clip(rng.normal(1.0, 0.1, size=total), 0.0, 2.0)
+    parts = np.zeros((16, n + 1, n + 1, n + 1))
+    _kernels.adjust_rays_chunked(origin, dirs, resid, gv, offs, True, inside, lo, edge, 0.05, 0.006, 1.0, parts)
+    out["adjust_g"] = parts.sum(axis=0)
+    np.savez_compressed(path, n=n, edge=edge, lo=lo, values=vals, origin=origin, inner=inner, dirs=dirs,
+                        background=bg, inside=inside, residuals=resid, g_values=gv, g_offsets=offs, **out)
+    print(path, {k: v.shape for k, v in out.items()})
+
+
+def make_render(fvr, path):
+    from fvr.render import RenderConfig, render_view
+    from fvr.volume import VoxelGrid
+
+    rng = np.random.default_rng(11)
+    vals = rng.uniform(0, 150, size=(3, 17, 17, 17)).astype(np.float32)
+    vals[:, :3] = -1.0  # sentinel slab
+    grids = [VoxelGrid(16, 16, 16, np.array([-0.1] * 3), 0.0125, t, vals[i])
+             for i, t in enumerate(("red", "green", "blue"))]
+    cam = make_ring_camera(63.0)
+    plain = render_view(cam, grids, None, RenderConfig(background=np.array([1.0, 2.0, 3.0]))).data
+    scat = render_view(cam, grids, None, RenderConfig(sigma_s=0.3, scattering_enabled=True, scatter_dirs=32)).data
+    single = render_view(cam, [grids[1]], None, RenderConfig(background=np.array([1.0, 2.0, 3.0]))).data
+    np.savez_compressed(path, values=vals, origin=np.array([-0.1] * 3), edge=0.0125, plain=plain, scat=scat,
+                        single_green=single, **cam_arrays([cam]))
+    print(path)
+
+
+def make_ctmap(fvr, path):
+    from fvr.cie_data import CIE_1931_2DEG
+    from fvr.radiometry import build_color_temp_map, temp_from_green
+
+    cmap = build_color_temp_map(1000.0, 2300.0, 1.0)
+    rng = np.random.default_rng(7)
+    g = np.concatenate([
+        rng.uniform(cmap.green[0], cmap.green[-1], 20000),
+        rng.uniform(-5.0, 100.0, 2000),
+        cmap.green[::7],
+        np.array([cmap.green[0], cmap.green[-1], -1.0, 1e6]),
+        rng.uniform(0.0, 90.0, 5000).astype(np.float32).astype(np.float64),
+    ])
+    T, clamped = temp_from_green(cmap, g)
+    odd = build_color_temp_map(1000.0, 1999.5, 3.0)
+    np.savez_compressed(path, temps=cmap.temperatures, entries=cmap.entries, cie=CIE_1931_2DEG, greens=g,
+                        T=T, clamped=clamped, odd_temps=odd.temperatures, odd_entries=odd.entries)
+    print(path)
+
+
+def make_tiny_color(fvr, path):
+    from fvr.reconstruct import ReconstructionConfig, reconstruct_color
+    from fvr.render import RenderConfig, render_view
+    from fvr.volume import VoxelGrid
+
+    n = 12
+    rng = np.random.default_rng(0)
+    edge = 0.2 / n
+    vals = np.zeros((n + 1,) * 3, dtype=np.float32)
+    core = slice(n // 4, 3 * n // 4 + 1)
+    vals[core, core, core] = 220.0 + 20.0 * rng.random(vals[core, core, core].shape)
+    grids = [VoxelGrid(n, n, n, np.array([-0.1] * 3), edge, t, vals) for t in ("red", "green", "blue")]
+    cams = [make_ring_camera(360.0 * i / 4, width=48, height=36) for i in range(4)]
+    rcfg = RenderConfig()
+    imgs = [render_view(c, grids, None, rcfg) for c in cams]
+    geom = VoxelGrid(n, n, n, np.array([-0.1] * 3), edge)
+    cfg = ReconstructionConfig(alpha_l=0.01, deterministic_mode=True, max_iters=40)
+    res = reconstruct_color(imgs, cams, geom, cfg, render_cfg=rcfg)
+    np.savez_compressed(path, values=vals, images=np.stack([im.data for im in imgs]),
+                        grids=np.stack([g.values for g in res.grids]),
+                        rmse_r=np.array(res.traces["red"].rmse), rmse_g=np.array(res.traces["green"].rmse),
+                        rmse_b=np.array(res.traces["blue"].rmse), hull_tags=res.hull.tags,
+                        bbox=np.array([res.bbox.u0, res.bbox.v0, res.bbox.u1, res.bbox.v1]), **cam_arrays(cams))
+    print(path, {t: res.traces[t].iterations for t in res.traces})
+
+
+def main():
+    fvr = _import_reference()
+    make_kernels(fvr, os.path.join(HERE, "kernels.npz"))
+    make_render(fvr, os.path.join(HERE, "render.npz"))
+    make_ctmap(fvr, os.path.join(HERE, "ctmap.npz"))
+    make_loop(fvr, os.path.join(HERE, "config1.npz"), 32, 4, 64, 0.05, 10)
+    make_loop(fvr, os.path.join(HERE, "loop_scatter.npz"), 16, 4, 48, 0.05, 5, scattering=True, sigma_s=0.1)
+    make_tiny_color(fvr, os.path.join(HERE, "tiny_color.npz"))
+
+
+if __name__ == "__main__":
+    main()
