@@ -91,11 +91,14 @@ int64_t fvr_launch_count(void);
 
 /* render_rays: dirs (n_rays,3) f64, values (n_channels, lattice) f32,
  * scat_dirs (n_scat,3) f64 (device), background host (n_channels) f64,
- * out (n_rays, n_channels) f64. n_channels <= 4. */
+ * out (n_rays, n_channels) f64. n_channels <= 4.  layout (optional, device,
+ * n_channels * lattice * 4 f32) is scratch for the packed copy the fast
+ * evaluators read (see fvr_render_layout_kind); NULL selects the general
+ * per-sample path. */
 int fvr_render_rays(const double origin[3], const double* dirs, int64_t n_rays,
                     const float* values, int32_t n_channels, fvr_grid_t grid,
                     fvr_render_params_t params, const double* background,
-                    const double* scat_dirs, double* out, void* stream);
+                    const double* scat_dirs, float* layout, double* out, void* stream);
 int fvr_render_rays_host(const double origin[3], const double* dirs, int64_t n_rays,
                          const float* values, int32_t n_channels, fvr_grid_t grid,
                          fvr_render_params_t params, const double* background,
@@ -135,7 +138,16 @@ int fvr_apply_correction(float* values, int64_t* accum, const int32_t* kp_index,
 int fvr_render_pixels(const fvr_camera_t* camera, const double* us, const double* vs,
                       int64_t n, const float* values, int32_t n_channels, fvr_grid_t grid,
                       fvr_render_params_t params, const double* background,
-                      const double* scat_dirs, double* out, void* stream);
+                      const double* scat_dirs, float* layout, double* out, void* stream);
+
+/* Packed copies of max(v, 0) read by the fast render paths: kind 1 (YZQ,
+ * emission only) or 2 (Z4, single scattering); 0 = none applies.  The Z4
+ * path needs the 32 Fibonacci directions loaded once per process with
+ * fvr_set_scatter_dirs (radiometry.py:222-230, gather = edge, g = 0). */
+int fvr_set_scatter_dirs(const double* dirs_host, int32_t n);
+int fvr_render_layout_kind(fvr_render_params_t params, fvr_grid_t grid);
+int fvr_pack_layout(const float* values, int32_t n_channels, fvr_grid_t grid, int32_t kind,
+                    float* layout, void* stream);
 
 /* ---- one iteration of the reconstruction loop (device resident) ------- */
 
@@ -147,7 +159,7 @@ int fvr_loop_blocks_per_view(int32_t bbox_w, int32_t bbox_h);
  * per-block squared-residual sums (f64). cams is a device array. */
 int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0,
                     int32_t bbox_w, int32_t bbox_h, const float* src, const float* values,
-                    fvr_grid_t grid, fvr_render_params_t params, double background,
+                    const float* layout, fvr_grid_t grid, fvr_render_params_t params, double background,
                     const double* scat_dirs, float* residual, double* sq_partials,
                     const fvr_loop_state_t* state, void* stream);
 
@@ -178,8 +190,10 @@ int fvr_loop_finalize(const double* sq_partials, int32_t n_views, int32_t blocks
                       double* trace_rmse, double* trace_vol, fvr_loop_state_t* state,
                       void* stream);
 
-/* Clamped update over hull key points unless the state says done. */
+/* Clamped update over hull key points unless the state says done; keeps the
+ * renderer's packed layout (may be NULL) in sync. */
 int fvr_loop_update(float* values, int64_t* accum, const int32_t* kp_index, int64_t n_kp,
+                    float* layout, int32_t layout_kind, fvr_grid_t grid,
                     const fvr_loop_state_t* state, void* stream);
 
 /* Multi-GPU helpers: gather accum at kp_index into a compact buffer and

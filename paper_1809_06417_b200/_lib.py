@@ -79,7 +79,7 @@ _SIGNATURES = {
     "fvr_last_error": (c_char_p, []),
     "fvr_abi_version": (c_int, []),
     "fvr_launch_count": (c_int64, []),
-    "fvr_render_rays": (c_int, [_P, _P, c_int64, _P, c_int32, _GRID, _PARAMS, _P, _P, _P, _P]),
+    "fvr_render_rays": (c_int, [_P, _P, c_int64, _P, c_int32, _GRID, _PARAMS, _P, _P, _P, _P, _P]),
     "fvr_render_rays_host": (c_int, [_P, _P, c_int64, _P, c_int32, _GRID, _PARAMS, _P, _P, _P]),
     "fvr_count_hull_samples": (c_int, [_P, _P, c_int64, _P, _GRID, _P, _P]),
     "fvr_count_hull_samples_host": (c_int, [_P, _P, c_int64, _P, _GRID, _P]),
@@ -94,12 +94,15 @@ _SIGNATURES = {
     "fvr_apply_correction": (c_int, [_P, _P, _P, c_int64, _P]),
     "fvr_render_pixels": (
         c_int,
-        [_P, _P, _P, c_int64, _P, c_int32, _GRID, _PARAMS, _P, _P, _P, _P],
+        [_P, _P, _P, c_int64, _P, c_int32, _GRID, _PARAMS, _P, _P, _P, _P, _P],
     ),
+    "fvr_set_scatter_dirs": (c_int, [_P, c_int32]),
+    "fvr_render_layout_kind": (c_int, [_PARAMS, _GRID]),
+    "fvr_pack_layout": (c_int, [_P, c_int32, _GRID, c_int32, _P, _P]),
     "fvr_loop_blocks_per_view": (c_int, [c_int32, c_int32]),
     "fvr_loop_render": (
         c_int,
-        [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _P, _P, _GRID, _PARAMS, c_double, _P,
+        [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _P, _P, _P, _GRID, _PARAMS, c_double, _P,
          _P, _P, _P, _P],
     ),
     "fvr_loop_adjust": (
@@ -112,7 +115,7 @@ _SIGNATURES = {
         c_int,
         [_P, c_int32, c_int32, c_int64, _P, c_int32, c_int64, c_double, _P, _P, _P, _P],
     ),
-    "fvr_loop_update": (c_int, [_P, _P, _P, c_int64, _P, _P]),
+    "fvr_loop_update": (c_int, [_P, _P, _P, c_int64, _P, c_int32, _GRID, _P, _P]),
     "fvr_pack_correction": (c_int, [_P, _P, c_int64, _P, _P]),
     "fvr_unpack_correction": (c_int, [_P, _P, c_int64, _P, _P]),
     "fvr_ctmap_build": (c_int, [c_double, c_double, c_int32, c_int32, c_double, _P, _P, _P]),
@@ -233,6 +236,29 @@ def cameras_tensor(cameras, dev):
     arr = (FvrCamera * n)(*[camera_struct(c) for c in cameras])
     host = t.frombuffer(bytearray(bytes(arr)), dtype=t.uint8)
     return host.to(dev)
+
+
+_dirs_loaded = False
+
+
+def ensure_scatter_dirs() -> None:
+    """Load fibonacci_sphere(32) into the stencil path's constant memory (once)."""
+    global _dirs_loaded
+    if _dirs_loaded:
+        return
+    import numpy as np
+
+    from .radiometry import fibonacci_sphere
+
+    d = np.ascontiguousarray(fibonacci_sphere(32))
+    call("fvr_set_scatter_dirs", d.ctypes.data, 32)
+    _dirs_loaded = True
+
+
+def layout_kind(params: FvrRenderParams, grid: FvrGrid) -> int:
+    """0 (none), 1 (YZQ) or 2 (Z4): the packed layout the fast render path reads."""
+    ensure_scatter_dirs()
+    return int(load().fvr_render_layout_kind(params, grid))
 
 
 def render_params(cfg, scattering: bool, n_scat: int, phase_g: float, gather: float) -> FvrRenderParams:

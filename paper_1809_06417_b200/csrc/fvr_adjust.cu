@@ -133,24 +133,52 @@ __global__ void __launch_bounds__(128) loop_adjust_kernel(
                                 (uint32_t)(ray_id_base + r), accum);
 }
 
-// v = f32(max(f64(v) + acc*2^-32, -1)); acc = 0  (reconstruct.py:221-226)
+// v = f32(max(f64(v) + acc*2^-32, -1)); acc = 0  (reconstruct.py:221-226).
+// When the renderer's packed copy of max(v, 0) exists (fvr_stencil.cuh), the
+// new value is written into every float4 slot that holds it.
+struct LayoutRef {
+    float* p;   // float4 array viewed as floats, or nullptr
+    int kind;   // 1 = YZQ, 2 = Z4
+    int sy;     // nz + 1
+    int ny1;    // ny + 1
+};
+
+__device__ __forceinline__ void layout_store(const LayoutRef& L, int64_t idx, float v) {
+    const float c = fmaxf(v, 0.f);
+    const int z = (int)(idx % L.sy);
+    if (L.kind == 2) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (z >= k) L.p[4 * (idx - k) + k] = c;
+    } else {
+        const int y = (int)((idx / L.sy) % L.ny1);
+        L.p[4 * idx] = c;
+        if (z >= 1) L.p[4 * (idx - 1) + 1] = c;
+        if (y >= 1) L.p[4 * (idx - L.sy) + 2] = c;
+        if (y >= 1 && z >= 1) L.p[4 * (idx - L.sy - 1) + 3] = c;
+    }
+}
+
 __device__ __forceinline__ void apply_one(float* __restrict__ values,
-                                          long long* __restrict__ accum, int64_t idx) {
+                                          long long* __restrict__ accum, int64_t idx,
+                                          const LayoutRef& L) {
     const long long a = accum[idx];
     if (a != 0) {
         const double nv = (double)values[idx] + (double)a * kFixInv;
-        values[idx] = (float)(nv > -1.0 ? nv : -1.0);
+        const float f = (float)(nv > -1.0 ? nv : -1.0);
+        values[idx] = f;
         accum[idx] = 0;
+        if (L.p) layout_store(L, idx, f);
     }
 }
 
 __global__ void apply_correction_kernel(float* __restrict__ values, long long* __restrict__ accum,
-                                        const int32_t* __restrict__ kp, int64_t n,
+                                        const int32_t* __restrict__ kp, int64_t n, LayoutRef L,
                                         const fvr_loop_state_t* __restrict__ state) {
     if (state && state->done) return;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        apply_one(values, accum, kp ? (int64_t)kp[i] : i);
+        apply_one(values, accum, kp ? (int64_t)kp[i] : i, L);
 }
 
 __global__ void pack_kernel(const long long* __restrict__ accum, const int32_t* __restrict__ kp,
@@ -229,7 +257,7 @@ extern "C" int fvr_apply_correction(float* values, int64_t* accum, const int32_t
     FVR_TRY_BEGIN
     if (n == 0) return FVR_OK;
     apply_correction_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
-        values, reinterpret_cast<long long*>(accum), kp_index, n, nullptr);
+        values, reinterpret_cast<long long*>(accum), kp_index, n, LayoutRef{nullptr, 0, 1, 1}, nullptr);
     return check_launch("apply_correction");
     FVR_TRY_END
 }
@@ -260,11 +288,14 @@ extern "C" int fvr_loop_adjust(const fvr_camera_t* cams, const int32_t* ray_list
 }
 
 extern "C" int fvr_loop_update(float* values, int64_t* accum, const int32_t* kp_index, int64_t n_kp,
+                               float* layout, int32_t layout_kind, fvr_grid_t grid,
                                const fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
     if (n_kp == 0) return FVR_OK;
+    if (layout && layout_kind != 1 && layout_kind != 2) return set_error(FVR_ERR_INVALID, "unknown layout kind");
+    const LayoutRef L{layout, layout_kind, grid.nz + 1, grid.ny + 1};
     apply_correction_kernel<<<grid_for(n_kp, 256), 256, 0, (cudaStream_t)stream>>>(
-        values, reinterpret_cast<long long*>(accum), kp_index, n_kp, state);
+        values, reinterpret_cast<long long*>(accum), kp_index, n_kp, L, state);
     return check_launch("loop_update");
     FVR_TRY_END
 }

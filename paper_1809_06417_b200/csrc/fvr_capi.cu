@@ -30,6 +30,7 @@ int check_launch(const char* what) {
 }
 
 int fix_to_f64(const int64_t* accum, int64_t n, double* out, cudaStream_t st);
+bool scatter_dirs_match(const double* host_dirs, int n);
 
 // RAII device buffer for the host variants.
 struct DevBuf {
@@ -82,12 +83,17 @@ extern "C" int fvr_render_rays_host(const double origin[3], const double* dirs, 
     const size_t lat = lattice_size(grid) * (size_t)n_channels;
     const int n_scat = params.n_scat > 0 ? params.n_scat : 0;
     DevBuf d_dirs(sizeof(double) * 3 * n_rays), d_vals(sizeof(float) * lat),
-        d_scat(sizeof(double) * 3 * (n_scat ? n_scat : 1)), d_out(sizeof(double) * n_rays * n_channels);
+        d_scat(sizeof(double) * 3 * (n_scat ? n_scat : 1)), d_out(sizeof(double) * n_rays * n_channels),
+        d_layout(sizeof(float) * 4 * lat);
     h2d(d_dirs.p, dirs, sizeof(double) * 3 * n_rays);
     h2d(d_vals.p, values, sizeof(float) * lat);
     if (n_scat && scat_dirs) h2d(d_scat.p, scat_dirs, sizeof(double) * 3 * n_scat);
+    // the stencil path may only see the directions loaded by fvr_set_scatter_dirs
+    const bool scat = params.scattering && params.sigma_s > 0.0;
+    const bool same_dirs = !scat || scatter_dirs_match(scat_dirs, n_scat);
     int rc = fvr_render_rays(origin, d_dirs.as<double>(), n_rays, d_vals.as<float>(), n_channels, grid,
-                             params, background, d_scat.as<double>(), d_out.as<double>(), nullptr);
+                             params, background, d_scat.as<double>(),
+                             same_dirs ? d_layout.as<float>() : nullptr, d_out.as<double>(), nullptr);
     if (rc) return rc;
     if ((rc = sync_check("render_rays_host"))) return rc;
     d2h(out, d_out.p, sizeof(double) * n_rays * n_channels);

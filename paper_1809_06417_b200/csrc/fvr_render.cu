@@ -8,9 +8,10 @@
 // L2/L1-resident lattice.  Blending state (transparency, radiance) is fp64 as
 // in the reference; each trilinear read is fp32.  Position and sample count
 // use the exact fp64 helpers of fvr_common.cuh.
-#include "fvr_internal.cuh"
+#include "fvr_stencil.cuh"
 
 namespace fvr {
+
 
 template <int NCH, bool SCAT, bool G0>
 __device__ __forceinline__ void march_render(const double o[3], const double d[3], const Geom& g,
@@ -78,14 +79,126 @@ __device__ __forceinline__ void march_render(const double o[3], const double d[3
     for (int c = 0; c < NCH; ++c) out[c] = l[c] + t_dst * rc.bg[c];
 }
 
+// Fast evaluator over a packed layout (fvr_stencil.cuh).  Per sample the
+// lattice coordinate is q = qb + k*d in fp64 (continuous quantities only);
+// the sample count, and for samples within half a voxel of a box face the
+// exact gather points, follow the reference arithmetic.
+template <int NCH, bool SCAT>
+__device__ __forceinline__ void march_render_fast(const double o[3], const double d[3], const Geom& g,
+                                                  const float* __restrict__ values, int plane,
+                                                  const float4* __restrict__ layout,
+                                                  const RenderConsts& rc, double out[NCH]) {
+    double l[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) l[c] = 0.0;
+    double t_dst = 1.0;
+    double te, tx;
+    if (slab_span(o, d, g, te, tx)) {
+        const int n = sample_count(te, tx, g.edge);
+        const double t0 = te - 0.5 * g.edge;
+        double qb[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) qb[a] = ((o[a] - g.lo[a]) + t0 * d[a]) * g.inv_edge;
+        const double nmax[3] = {(double)g.nx, (double)g.ny, (double)g.nz};
+        for (int k = 1; k <= n; ++k) {
+            double q[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) q[a] = fma((double)k, d[a], qb[a]);
+            if (!SCAT) {
+                int ix, iy, iz;
+                float fx, fy, fz;
+                cell_frac(q[0], g.nx, ix, fx);
+                cell_frac(q[1], g.ny, iy, fy);
+                cell_frac(q[2], g.nz, iz, fz);
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    const float e = tri_yzq(layout + (int64_t)c * plane, g, ix, iy, iz, fx, fy, fz);
+                    l[c] += t_dst * (rc.tau * (rc.sigma_a * (double)e));
+                }
+            } else {
+                bool interior = true;
+                int m[3];
+                float dl[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    interior = interior && q[a] >= 0.5 + 1e-7 && q[a] <= nmax[a] - 0.5 - 1e-7;
+                    const double r = rint(q[a]);
+                    m[a] = min(max((int)r, 0), a == 0 ? g.nx : (a == 1 ? g.ny : g.nz));
+                    dl[a] = (float)(q[a] - (double)m[a]);
+                }
+                uint32_t mask = 0xffffffffu;
+                if (!interior) {
+                    double p[3];
+                    sample_pos(o, d, te, g.edge, k, p);
+                    mask = inbox_mask(p, g, rc.half_gather);
+                }
+#pragma unroll 1
+                for (int c = 0; c < NCH; ++c) {
+                    float v[27];
+                    if (interior)
+                        load_stencil_z4(layout + (int64_t)c * plane, g, m[0], m[1], m[2], v);
+                    else
+                        load_stencil_clamped(values + (int64_t)c * plane, g, m[0], m[1], m[2], v);
+                    Stencil st;
+                    stencil_from(v, st);
+                    const float e = stencil_tri(st, dl[0], dl[1], dl[2]);
+                    const float acc = stencil_scatter<true>(st, dl[0], dl[1], dl[2], mask);
+                    const double l_src = rc.sigma_a * (double)e + (double)acc * rc.scat_scale;
+                    l[c] += t_dst * (rc.tau * l_src);
+                }
+            }
+            t_dst *= rc.one_minus_tau;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) out[c] = l[c] + t_dst * rc.bg[c];
+}
+
+// Packed layouts of max(v, 0): see fvr_stencil.cuh.
+__global__ void pack_layout_kernel(const float* __restrict__ values, int64_t n_kp, int nch, int kind,
+                                   int sy, float4* __restrict__ out) {
+    const int64_t total = n_kp * nch;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / n_kp, j = i - c * n_kp;
+        const float* v = values + c * n_kp;
+        auto at = [&](int64_t k) { return k < n_kp ? fmaxf(v[k], 0.f) : 0.f; };
+        float4 r;
+        if (kind == kLayoutZ4)
+            r = make_float4(at(j), at(j + 1), at(j + 2), at(j + 3));
+        else
+            r = make_float4(at(j), at(j + 1), at(j + sy), at(j + sy + 1));
+        out[i] = r;
+    }
+}
+
+// ---- mode dispatch ------------------------------------------------------------
+// MODE: 0 general emission, 1 general scattering g = 0, 2 general scattering
+// g != 0, 3 fast emission (YZQ layout), 4 fast scattering (Z4 layout).
+enum { kModePlain = 0, kModeScatG0 = 1, kModeScatG = 2, kModeFastPlain = 3, kModeFastScat = 4 };
+
+template <int NCH, int MODE>
+__device__ __forceinline__ void march_dispatch(const double o[3], const double d[3], const Geom& g,
+                                               const float* __restrict__ values, int plane,
+                                               const float4* __restrict__ layout,
+                                               const RenderConsts& rc, const double* __restrict__ scat,
+                                               double out[NCH]) {
+    if (MODE == kModePlain) march_render<NCH, false, true>(o, d, g, values, plane, rc, scat, out);
+    if (MODE == kModeScatG0) march_render<NCH, true, true>(o, d, g, values, plane, rc, scat, out);
+    if (MODE == kModeScatG) march_render<NCH, true, false>(o, d, g, values, plane, rc, scat, out);
+    if (MODE == kModeFastPlain) march_render_fast<NCH, false>(o, d, g, values, plane, layout, rc, out);
+    if (MODE == kModeFastScat) march_render_fast<NCH, true>(o, d, g, values, plane, layout, rc, out);
+}
+
 // ---- _kernels.render_rays drop-in -----------------------------------------
 
-template <int NCH, bool SCAT, bool G0>
+template <int NCH, int MODE>
 __global__ void __launch_bounds__(128) render_rays_kernel(double ox, double oy, double oz,
                                                           const double* __restrict__ dirs,
                                                           int64_t n_rays,
                                                           const float* __restrict__ values,
-                                                          int plane, Geom g, RenderConsts rc,
+                                                          int plane, const float4* __restrict__ layout,
+                                                          Geom g, RenderConsts rc,
                                                           const double* __restrict__ scat,
                                                           double* __restrict__ out) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -93,20 +206,21 @@ __global__ void __launch_bounds__(128) render_rays_kernel(double ox, double oy, 
     const double o[3] = {ox, oy, oz};
     const double d[3] = {dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2]};
     double res[NCH];
-    march_render<NCH, SCAT, G0>(o, d, g, values, plane, rc, scat, res);
+    march_dispatch<NCH, MODE>(o, d, g, values, plane, layout, rc, scat, res);
 #pragma unroll
     for (int c = 0; c < NCH; ++c) out[r * NCH + c] = res[c];
 }
 
 // ---- render_pixels / render_view: rays built on the device ----------------
 
-template <int NCH, bool SCAT, bool G0>
+template <int NCH, int MODE>
 __global__ void __launch_bounds__(128) render_pixels_kernel(fvr_camera_t cam,
                                                             const double* __restrict__ us,
                                                             const double* __restrict__ vs,
                                                             int64_t n,
                                                             const float* __restrict__ values,
-                                                            int plane, Geom g, RenderConsts rc,
+                                                            int plane, const float4* __restrict__ layout,
+                                                            Geom g, RenderConsts rc,
                                                             const double* __restrict__ scat,
                                                             double* __restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -122,7 +236,7 @@ __global__ void __launch_bounds__(128) render_pixels_kernel(fvr_camera_t cam,
     double d[3];
     pixel_dir(cam, u, v, d);
     double res[NCH];
-    march_render<NCH, SCAT, G0>(cam.center, d, g, values, plane, rc, scat, res);
+    march_dispatch<NCH, MODE>(cam.center, d, g, values, plane, layout, rc, scat, res);
 #pragma unroll
     for (int c = 0; c < NCH; ++c) out[i * NCH + c] = res[c];
 }
@@ -131,12 +245,13 @@ __global__ void __launch_bounds__(128) render_pixels_kernel(fvr_camera_t cam,
 
 constexpr int kTileW = 16, kTileH = 8, kTileThreads = kTileW * kTileH;
 
-template <bool SCAT>
+template <int MODE>
 __global__ void __launch_bounds__(kTileThreads) loop_render_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int tiles_x,
-    const float* __restrict__ src, const float* __restrict__ values, Geom g, RenderConsts rc,
-    const double* __restrict__ scat, float* __restrict__ residual,
-    double* __restrict__ sq_partials, const fvr_loop_state_t* __restrict__ state) {
+    const float* __restrict__ src, const float* __restrict__ values,
+    const float4* __restrict__ layout, Geom g, RenderConsts rc, const double* __restrict__ scat,
+    float* __restrict__ residual, double* __restrict__ sq_partials,
+    const fvr_loop_state_t* __restrict__ state) {
     if (state && state->done) return;
     __shared__ double red[kTileThreads / 32];
     const int view = blockIdx.y;
@@ -149,7 +264,7 @@ __global__ void __launch_bounds__(kTileThreads) loop_render_kernel(
         double d[3];
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         double rec[1];
-        march_render<1, SCAT, true>(cam.center, d, g, values, 0, rc, scat, rec);
+        march_dispatch<1, MODE>(cam.center, d, g, values, 0, layout, rc, scat, rec);
         const int64_t pix = ((int64_t)view * h + row) * w + col;
         const double r = (double)src[pix] - rec[0];
         residual[pix] = (float)r;
@@ -165,63 +280,154 @@ using namespace fvr;
 
 namespace {
 
-template <int NCH>
-void launch_render_rays(const double origin[3], const double* dirs, int64_t n_rays,
-                        const float* values, int plane, const Geom& g, const RenderConsts& rc,
-                        bool scat, bool g0, const double* scat_dirs, double* out,
-                        cudaStream_t st) {
-    const dim3 grid((unsigned)((n_rays + 127) / 128)), block(128);
-    if (!scat)
-        render_rays_kernel<NCH, false, true><<<grid, block, 0, st>>>(
-            origin[0], origin[1], origin[2], dirs, n_rays, values, plane, g, rc, scat_dirs, out);
-    else if (g0)
-        render_rays_kernel<NCH, true, true><<<grid, block, 0, st>>>(
-            origin[0], origin[1], origin[2], dirs, n_rays, values, plane, g, rc, scat_dirs, out);
-    else
-        render_rays_kernel<NCH, true, false><<<grid, block, 0, st>>>(
-            origin[0], origin[1], origin[2], dirs, n_rays, values, plane, g, rc, scat_dirs, out);
+bool g_dirs_ready = false;
+double g_dirs_host[3 * kScatDirs];
+
+int pick_mode(const fvr_render_params_t& p, const float4* layout, bool& scat) {
+    scat = p.scattering && p.sigma_s > 0.0;
+    if (!scat) return layout ? kModeFastPlain : kModePlain;
+    const bool g0 = p.phase_g == 0.0;
+    const bool stencil_ok = g0 && p.n_scat == kScatDirs && layout && g_dirs_ready;
+    return stencil_ok ? kModeFastScat : (g0 ? kModeScatG0 : kModeScatG);
+}
+
+// the stencil path also needs gather_dist == edge (all gathers within the 3^3 block)
+int effective_mode(const fvr_render_params_t& p, const fvr_grid_t& grid, const float4* layout, bool& scat) {
+    int mode = pick_mode(p, layout, scat);
+    if (mode == kModeFastScat && p.gather_dist != grid.edge) mode = kModeScatG0;
+    return mode;
+}
+
+int layout_kind(int mode) {
+    return mode == kModeFastScat ? kLayoutZ4 : (mode == kModeFastPlain ? kLayoutYZQ : kLayoutNone);
+}
+
+int pack(const float* values, int nch, const fvr_grid_t& grid, int kind, float4* out, cudaStream_t st) {
+    const int64_t n_kp = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
+    int64_t blocks = (n_kp * nch + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    pack_layout_kernel<<<(unsigned)blocks, 256, 0, st>>>(values, n_kp, nch, kind, grid.nz + 1, out);
+    return check_launch("pack_layout");
+}
+
+template <int NCH, int MODE>
+void launch_rays(const double origin[3], const double* dirs, int64_t n_rays, const float* values,
+                 int plane, const float4* layout, const Geom& g, const RenderConsts& rc,
+                 const double* scat_dirs, double* out, cudaStream_t st) {
+    render_rays_kernel<NCH, MODE><<<(unsigned)((n_rays + 127) / 128), 128, 0, st>>>(
+        origin[0], origin[1], origin[2], dirs, n_rays, values, plane, layout, g, rc, scat_dirs, out);
 }
 
 template <int NCH>
-void launch_render_pixels(const fvr_camera_t& cam, const double* us, const double* vs, int64_t n,
-                          const float* values, int plane, const Geom& g, const RenderConsts& rc,
-                          bool scat, bool g0, const double* scat_dirs, double* out,
-                          cudaStream_t st) {
-    const dim3 grid((unsigned)((n + 127) / 128)), block(128);
-    if (!scat)
-        render_pixels_kernel<NCH, false, true>
-            <<<grid, block, 0, st>>>(cam, us, vs, n, values, plane, g, rc, scat_dirs, out);
-    else if (g0)
-        render_pixels_kernel<NCH, true, true>
-            <<<grid, block, 0, st>>>(cam, us, vs, n, values, plane, g, rc, scat_dirs, out);
-    else
-        render_pixels_kernel<NCH, true, false>
-            <<<grid, block, 0, st>>>(cam, us, vs, n, values, plane, g, rc, scat_dirs, out);
+void launch_rays_mode(int mode, const double origin[3], const double* dirs, int64_t n_rays,
+                      const float* values, int plane, const float4* layout, const Geom& g,
+                      const RenderConsts& rc, const double* scat_dirs, double* out, cudaStream_t st) {
+    switch (mode) {
+        case kModePlain: launch_rays<NCH, kModePlain>(origin, dirs, n_rays, values, plane, layout, g, rc, scat_dirs, out, st); break;
+        case kModeScatG0: launch_rays<NCH, kModeScatG0>(origin, dirs, n_rays, values, plane, layout, g, rc, scat_dirs, out, st); break;
+        case kModeScatG: launch_rays<NCH, kModeScatG>(origin, dirs, n_rays, values, plane, layout, g, rc, scat_dirs, out, st); break;
+        case kModeFastPlain: launch_rays<NCH, kModeFastPlain>(origin, dirs, n_rays, values, plane, layout, g, rc, scat_dirs, out, st); break;
+        default: launch_rays<NCH, kModeFastScat>(origin, dirs, n_rays, values, plane, layout, g, rc, scat_dirs, out, st); break;
+    }
+}
+
+template <int NCH, int MODE>
+void launch_pix(const fvr_camera_t& cam, const double* us, const double* vs, int64_t n,
+                const float* values, int plane, const float4* layout, const Geom& g,
+                const RenderConsts& rc, const double* scat_dirs, double* out, cudaStream_t st) {
+    render_pixels_kernel<NCH, MODE><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+        cam, us, vs, n, values, plane, layout, g, rc, scat_dirs, out);
+}
+
+template <int NCH>
+void launch_pix_mode(int mode, const fvr_camera_t& cam, const double* us, const double* vs, int64_t n,
+                     const float* values, int plane, const float4* layout, const Geom& g,
+                     const RenderConsts& rc, const double* scat_dirs, double* out, cudaStream_t st) {
+    switch (mode) {
+        case kModePlain: launch_pix<NCH, kModePlain>(cam, us, vs, n, values, plane, layout, g, rc, scat_dirs, out, st); break;
+        case kModeScatG0: launch_pix<NCH, kModeScatG0>(cam, us, vs, n, values, plane, layout, g, rc, scat_dirs, out, st); break;
+        case kModeScatG: launch_pix<NCH, kModeScatG>(cam, us, vs, n, values, plane, layout, g, rc, scat_dirs, out, st); break;
+        case kModeFastPlain: launch_pix<NCH, kModeFastPlain>(cam, us, vs, n, values, plane, layout, g, rc, scat_dirs, out, st); break;
+        default: launch_pix<NCH, kModeFastScat>(cam, us, vs, n, values, plane, layout, g, rc, scat_dirs, out, st); break;
+    }
+}
+
+int check_common(int32_t n_channels, const fvr_grid_t& grid, const fvr_render_params_t& params,
+                 const double* scat_dirs) {
+    if (n_channels < 1 || n_channels > 4) return set_error(FVR_ERR_INVALID, "n_channels must be 1..4");
+    if (int rc = check_grid(grid)) return rc;
+    const bool scat = params.scattering && params.sigma_s > 0.0;
+    if (scat && (params.n_scat < 1 || !scat_dirs))
+        return set_error(FVR_ERR_INVALID, "scattering needs n_scat >= 1 directions");
+    return FVR_OK;
 }
 
 }  // namespace
 
+namespace fvr {
+bool scatter_dirs_match(const double* host_dirs, int n) {
+    if (!g_dirs_ready || n != kScatDirs || !host_dirs) return false;
+    for (int i = 0; i < 3 * kScatDirs; ++i)
+        if (host_dirs[i] != g_dirs_host[i]) return false;
+    return true;
+}
+}  // namespace fvr
+
+extern "C" int fvr_set_scatter_dirs(const double* dirs_host, int32_t n) {
+    FVR_TRY_BEGIN
+    if (n != kScatDirs) return set_error(FVR_ERR_INVALID, "the stencil path is compiled for 32 directions");
+    double d[3][kScatDirs];
+    float h[3][kScatDirs];
+    for (int s = 0; s < n; ++s)
+        for (int a = 0; a < 3; ++a) {
+            d[a][s] = dirs_host[3 * s + a];
+            h[a][s] = (float)(0.5 * dirs_host[3 * s + a]);
+        }
+    if (cudaMemcpyToSymbol(c_dir, d, sizeof(d)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_half_dir, h, sizeof(h)) != cudaSuccess)
+        return set_error(FVR_ERR_CUDA, "cudaMemcpyToSymbol failed");
+    for (int i = 0; i < 3 * kScatDirs; ++i) g_dirs_host[i] = dirs_host[i];
+    g_dirs_ready = true;
+    return FVR_OK;
+    FVR_TRY_END
+}
+
+extern "C" int fvr_pack_layout(const float* values, int32_t n_channels, fvr_grid_t grid, int32_t kind,
+                               float* layout, void* stream) {
+    FVR_TRY_BEGIN
+    if (int rc = check_grid(grid)) return rc;
+    if (kind != kLayoutYZQ && kind != kLayoutZ4) return set_error(FVR_ERR_INVALID, "unknown layout kind");
+    return pack(values, n_channels, grid, kind, reinterpret_cast<float4*>(layout), (cudaStream_t)stream);
+    FVR_TRY_END
+}
+
+extern "C" int fvr_render_layout_kind(fvr_render_params_t params, fvr_grid_t grid) {
+    bool scat;
+    const float4* dummy = reinterpret_cast<const float4*>(16);
+    return layout_kind(effective_mode(params, grid, dummy, scat));
+}
+
 extern "C" int fvr_render_rays(const double origin[3], const double* dirs, int64_t n_rays,
                                const float* values, int32_t n_channels, fvr_grid_t grid,
                                fvr_render_params_t params, const double* background,
-                               const double* scat_dirs, double* out, void* stream) {
+                               const double* scat_dirs, float* layout, double* out, void* stream) {
     FVR_TRY_BEGIN
-    if (n_channels < 1 || n_channels > 4) return set_error(FVR_ERR_INVALID, "n_channels must be 1..4");
-    if (int rc = check_grid(grid)) return rc;
+    if (int rc = check_common(n_channels, grid, params, scat_dirs)) return rc;
     if (n_rays == 0) return FVR_OK;
-    const bool scat = params.scattering && params.sigma_s > 0.0;
-    if (scat && (params.n_scat < 1 || !scat_dirs))
-        return set_error(FVR_ERR_INVALID, "scattering needs n_scat >= 1 directions");
+    bool scat;
+    const float4* lay = reinterpret_cast<const float4*>(layout);
+    const int mode = effective_mode(params, grid, lay, scat);
     const Geom g = make_geom(grid);
     const RenderConsts rc = make_render_consts(params, background, n_channels);
     const int plane = (grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
-    const bool g0 = params.phase_g == 0.0;
     cudaStream_t st = (cudaStream_t)stream;
+    if (layout_kind(mode) != kLayoutNone)
+        if (int e = pack(values, n_channels, grid, layout_kind(mode), reinterpret_cast<float4*>(layout), st)) return e;
     switch (n_channels) {
-        case 1: launch_render_rays<1>(origin, dirs, n_rays, values, plane, g, rc, scat, g0, scat_dirs, out, st); break;
-        case 2: launch_render_rays<2>(origin, dirs, n_rays, values, plane, g, rc, scat, g0, scat_dirs, out, st); break;
-        case 3: launch_render_rays<3>(origin, dirs, n_rays, values, plane, g, rc, scat, g0, scat_dirs, out, st); break;
-        default: launch_render_rays<4>(origin, dirs, n_rays, values, plane, g, rc, scat, g0, scat_dirs, out, st); break;
+        case 1: launch_rays_mode<1>(mode, origin, dirs, n_rays, values, plane, lay, g, rc, scat_dirs, out, st); break;
+        case 2: launch_rays_mode<2>(mode, origin, dirs, n_rays, values, plane, lay, g, rc, scat_dirs, out, st); break;
+        case 3: launch_rays_mode<3>(mode, origin, dirs, n_rays, values, plane, lay, g, rc, scat_dirs, out, st); break;
+        default: launch_rays_mode<4>(mode, origin, dirs, n_rays, values, plane, lay, g, rc, scat_dirs, out, st); break;
     }
     return check_launch("render_rays");
     FVR_TRY_END
@@ -230,28 +436,28 @@ extern "C" int fvr_render_rays(const double origin[3], const double* dirs, int64
 extern "C" int fvr_render_pixels(const fvr_camera_t* camera, const double* us, const double* vs,
                                  int64_t n, const float* values, int32_t n_channels,
                                  fvr_grid_t grid, fvr_render_params_t params,
-                                 const double* background, const double* scat_dirs, double* out,
-                                 void* stream) {
+                                 const double* background, const double* scat_dirs, float* layout,
+                                 double* out, void* stream) {
     FVR_TRY_BEGIN
     if (!camera) return set_error(FVR_ERR_INVALID, "camera is NULL");
-    if (n_channels < 1 || n_channels > 4) return set_error(FVR_ERR_INVALID, "n_channels must be 1..4");
-    if (int rc = check_grid(grid)) return rc;
+    if (int rc = check_common(n_channels, grid, params, scat_dirs)) return rc;
     if ((us == nullptr) != (vs == nullptr)) return set_error(FVR_ERR_INVALID, "us and vs must both be given");
     if (!us) n = (int64_t)camera->width * camera->height;
     if (n == 0) return FVR_OK;
-    const bool scat = params.scattering && params.sigma_s > 0.0;
-    if (scat && (params.n_scat < 1 || !scat_dirs))
-        return set_error(FVR_ERR_INVALID, "scattering needs n_scat >= 1 directions");
+    bool scat;
+    const float4* lay = reinterpret_cast<const float4*>(layout);
+    const int mode = effective_mode(params, grid, lay, scat);
     const Geom g = make_geom(grid);
     const RenderConsts rc = make_render_consts(params, background, n_channels);
     const int plane = (grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
-    const bool g0 = params.phase_g == 0.0;
     cudaStream_t st = (cudaStream_t)stream;
+    if (layout_kind(mode) != kLayoutNone)
+        if (int e = pack(values, n_channels, grid, layout_kind(mode), reinterpret_cast<float4*>(layout), st)) return e;
     switch (n_channels) {
-        case 1: launch_render_pixels<1>(*camera, us, vs, n, values, plane, g, rc, scat, g0, scat_dirs, out, st); break;
-        case 2: launch_render_pixels<2>(*camera, us, vs, n, values, plane, g, rc, scat, g0, scat_dirs, out, st); break;
-        case 3: launch_render_pixels<3>(*camera, us, vs, n, values, plane, g, rc, scat, g0, scat_dirs, out, st); break;
-        default: launch_render_pixels<4>(*camera, us, vs, n, values, plane, g, rc, scat, g0, scat_dirs, out, st); break;
+        case 1: launch_pix_mode<1>(mode, *camera, us, vs, n, values, plane, lay, g, rc, scat_dirs, out, st); break;
+        case 2: launch_pix_mode<2>(mode, *camera, us, vs, n, values, plane, lay, g, rc, scat_dirs, out, st); break;
+        case 3: launch_pix_mode<3>(mode, *camera, us, vs, n, values, plane, lay, g, rc, scat_dirs, out, st); break;
+        default: launch_pix_mode<4>(mode, *camera, us, vs, n, values, plane, lay, g, rc, scat_dirs, out, st); break;
     }
     return check_launch("render_pixels");
     FVR_TRY_END
@@ -263,32 +469,34 @@ extern "C" int fvr_loop_blocks_per_view(int32_t bbox_w, int32_t bbox_h) {
 
 extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0,
                                int32_t bbox_w, int32_t bbox_h, const float* src,
-                               const float* values, fvr_grid_t grid, fvr_render_params_t params,
-                               double background, const double* scat_dirs, float* residual,
-                               double* sq_partials, const fvr_loop_state_t* state, void* stream) {
+                               const float* values, const float* layout, fvr_grid_t grid,
+                               fvr_render_params_t params, double background,
+                               const double* scat_dirs, float* residual, double* sq_partials,
+                               const fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
     if (n_views < 1 || n_views > 65535) return set_error(FVR_ERR_INVALID, "bad view count");
     if (bbox_w < 1 || bbox_h < 1) return set_error(FVR_ERR_INVALID, "empty bounding box");
-    if (int rc = check_grid(grid)) return rc;
-    const bool scat = params.scattering && params.sigma_s > 0.0;
-    if (scat && (params.n_scat < 1 || !scat_dirs))
-        return set_error(FVR_ERR_INVALID, "scattering needs n_scat >= 1 directions");
-    if (scat && params.phase_g != 0.0)
-        return set_error(FVR_ERR_INVALID, "the reconstruction loop renders with g = 0 (render.py:196)");
+    if (int rc = check_common(1, grid, params, scat_dirs)) return rc;
+    bool scat;
+    const float4* lay = reinterpret_cast<const float4*>(layout);
+    const int mode = effective_mode(params, grid, lay, scat);
+    if (mode == kModeScatG) return set_error(FVR_ERR_INVALID, "the reconstruction loop renders with g = 0 (render.py:196)");
     const Geom g = make_geom(grid);
     const RenderConsts rc = make_render_consts(params, &background, 1);
     const int tiles_x = (bbox_w + kTileW - 1) / kTileW;
     const int tiles = fvr_loop_blocks_per_view(bbox_w, bbox_h);
     const dim3 gridd((unsigned)tiles, (unsigned)n_views), block(kTileThreads);
     cudaStream_t st = (cudaStream_t)stream;
-    if (scat)
-        loop_render_kernel<true><<<gridd, block, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, tiles_x, src,
-                                                          values, g, rc, scat_dirs, residual,
-                                                          sq_partials, state);
-    else
-        loop_render_kernel<false><<<gridd, block, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, tiles_x, src,
-                                                           values, g, rc, scat_dirs, residual,
-                                                           sq_partials, state);
+#define FVR_LOOP_RENDER(M)                                                                          \
+    loop_render_kernel<M><<<gridd, block, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, tiles_x, src, values, \
+                                                   lay, g, rc, scat_dirs, residual, sq_partials, state)
+    switch (mode) {
+        case kModePlain: FVR_LOOP_RENDER(kModePlain); break;
+        case kModeScatG0: FVR_LOOP_RENDER(kModeScatG0); break;
+        case kModeFastPlain: FVR_LOOP_RENDER(kModeFastPlain); break;
+        default: FVR_LOOP_RENDER(kModeFastScat); break;
+    }
+#undef FVR_LOOP_RENDER
     return check_launch("loop_render");
     FVR_TRY_END
 }

@@ -126,6 +126,13 @@ class ChannelLoop:
             n_scat = 1
         self.params = _lib.render_params(render_cfg, self.scattering, n_scat, 0.0, grid_geom.edge)
         self.background = float(background)
+        # packed copy of max(v, 0) read by the fast render path, kept in sync by K-update
+        self.layout_kind = _lib.layout_kind(self.params, self.grid)
+        self.layout = None
+        if self.layout_kind:
+            self.layout = t.empty(values.shape + (4,), dtype=t.float32, device=dev)
+            _lib.call("fvr_pack_layout", self.values.data_ptr(), 1, self.grid, self.layout_kind,
+                      self.layout.data_ptr(), _lib.stream_ptr())
 
         # work buffers
         self.bpv = int(_lib.load().fvr_loop_blocks_per_view(self.w_bb, self.h_bb))
@@ -158,7 +165,7 @@ class ChannelLoop:
         _lib.call(
             "fvr_loop_render", self.cams.data_ptr(), self.v_end - self.v_begin, self.bbox.u0,
             self.bbox.v0, self.w_bb, self.h_bb, self.src.data_ptr(), self.values.data_ptr(),
-            self.grid, self.params, self.background, _lib.ptr(self.scat), self.residual.data_ptr(),
+            _lib.ptr(self.layout), self.grid, self.params, self.background, _lib.ptr(self.scat), self.residual.data_ptr(),
             sq_local.data_ptr(), self.state.data_ptr(), stream,
         )
         return 1
@@ -200,7 +207,7 @@ class ChannelLoop:
             return 0
         _lib.call(
             "fvr_loop_update", self.values.data_ptr(), self.accum.data_ptr(), self.kp.data_ptr(),
-            self.n_kp, self.state.data_ptr(), stream,
+            self.n_kp, _lib.ptr(self.layout), self.layout_kind, self.grid, self.state.data_ptr(), stream,
         )
         return 1
 
