@@ -223,40 +223,37 @@ def run_gpu(args):
         torch.cuda.synchronize()
 
     stream = _lib.stream_ptr()
-    names = ["render", "adjust", "finalize", "update"]
+    stages = [(n, f) for n, f in loop.stages() if f is not None]
+    names = [n for n, _ in stages]
 
     def one_step(evs):
+        launches = 0
         evs[0].record()
-        loop._render(stream)
-        evs[1].record()
-        loop._volume(stream)
-        loop._adjust(stream)
-        if world > 1:
-            loop._allreduce(stream)
-        evs[2].record()
-        loop._finalize(stream)
-        evs[3].record()
-        loop._update(stream)
-        evs[4].record()
+        for i, (_, fn) in enumerate(stages):
+            launches += fn(stream)
+            evs[i + 1].record()
+        return launches
+
+    def new_events():
+        return [torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)]
 
     for _ in range(args.warmup):
         flush.fill_(1.0)
-        one_step([torch.cuda.Event(enable_timing=True) for _ in range(5)])
+        one_step(new_events())
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
     barrier()
     all_evs = []
-    l0 = _lib.launch_count()
+    launches = 0
     for _ in range(args.steps):
         flush.fill_(1.0)  # L2 flush between timed steps, outside the step's events
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-        one_step(evs)
+        evs = new_events()
+        launches += one_step(evs)
         all_evs.append(evs)
     barrier()
-    launches = _lib.launch_count() - l0
     clocks = sampler.stop()
-    step_ms = np.array([e[0].elapsed_time(e[4]) for e in all_evs])
+    step_ms = np.array([e[0].elapsed_time(e[-1]) for e in all_evs])
     part_ms = {n: float(np.mean([e[i].elapsed_time(e[i + 1]) for e in all_evs])) for i, n in enumerate(names)}
     total_ms = float(step_ms.sum())
     if world > 1:
@@ -328,6 +325,7 @@ def run_gpu(args):
                      "bytes_per_launch": render_bytes,
                      "bytes_rule": "108 B per render sample (27-key-point stencil, f32) + 8 B per bbox pixel"},
         "gpu_launches": int(launches),
+        "adjust_path": "voxel-driven gather (CSR plan, nnz %d)" % loop.plan_nnz if loop.plan else "ray-driven scatter",
         "clocks": clocks,
         "e2e": e2e,
     }

@@ -196,6 +196,33 @@ int fvr_loop_update(float* values, int64_t* accum, const int32_t* kp_index, int6
                     float* layout, int32_t layout_kind, fvr_grid_t grid,
                     const fvr_loop_state_t* state, void* stream);
 
+/* ---- deterministic back-projection as a voxel-driven gather ------------
+ * (reconstruct.py:152-227 with G = 1).  The operator A (delta = A . res) is
+ * fixed for a reconstruction: build its CSR by hull key point once, then
+ * apply it every iteration.  kp_map (lattice) maps a key point to its row
+ * (hull key points) or -1; row_counts (n_kp) i32 zeroed by the caller;
+ * cursor (n_kp) i64 = row offsets (exclusive scan of the counts); entries
+ * (2*nnz) i32 = (residual index, f32 bits of W) pairs. */
+int fvr_adjust_plan_count(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
+                          int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
+                          const uint8_t* inside_vox, fvr_grid_t grid, const int32_t* kp_map,
+                          int32_t* row_counts, void* stream);
+int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
+                         int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
+                         const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
+                         double alpha_d, const int32_t* kp_map, int64_t* cursor, int32_t* entries,
+                         void* stream);
+/* Per iteration: row sums in 32.32 fixed point; with packed == NULL the
+ * clamped update is applied in place (and the packed layout refreshed),
+ * otherwise the sums go to packed (n_kp) for the multi-GPU all-reduce. */
+int fvr_loop_gather(const int64_t* row_offsets, const int32_t* entries, int64_t n_kp,
+                    const float* residual, const int32_t* kp_index, float* values, float* layout,
+                    int32_t layout_kind, fvr_grid_t grid, int64_t* packed,
+                    const fvr_loop_state_t* state, void* stream);
+int fvr_loop_update_packed(const int64_t* packed, int64_t n_kp, const int32_t* kp_index,
+                           float* values, float* layout, int32_t layout_kind, fvr_grid_t grid,
+                           const fvr_loop_state_t* state, void* stream);
+
 /* Multi-GPU helpers: gather accum at kp_index into a compact buffer and
  * scatter it back (the NCCL allreduce runs between them). */
 int fvr_pack_correction(const int64_t* accum, const int32_t* kp_index, int64_t n_kp,

@@ -1,0 +1,284 @@
+// fvr_plan.cu -- K-adjust as a voxel-driven gather (deterministic mode).
+//
+// In deterministic mode (G = 1) every in-hull sample of every flame ray adds
+// res[ray] * W to its 8 corner key points with W = alpha_l * (1-tau)^(k-1) *
+// exp(-alpha_d' |p - corner|) (_kernels.py:290-306).  Rays, samples, cells
+// and W depend only on the cameras, the grid and the hull -- not on the
+// iteration -- so the back-projection of one iteration is the sparse
+// product delta = A . res with a fixed A.  The plan (built once per
+// reconstruct_channel call) stores A in CSR by hull key point: each entry is
+// (index of the residual pixel, W).  Per iteration one warp per key point
+// gathers its row, sums res * W in 32.32 fixed point (order-independent, so
+// the result is bit-reproducible and identical under view sharding) and
+// applies the clamped update -- no atomics, and ~8 bytes of streamed HBM
+// traffic per (ray, corner) pair instead of an L2 read-modify-write.
+//
+// ncu on the ray-driven scatter (fvr_adjust.cu, kept for stochastic mode and
+// the operator layer): 504 us per iteration at config 2, L2 56% busy with
+// 62 M RED.ADD.64, IPC 1.25 (profiles/r1a_*).
+#include "fvr_internal.cuh"
+
+namespace fvr {
+
+// Visit every in-hull sample of a ray: f(k, q[3], cell[3], trans).  Cells use
+// q = qb + k*d (fp64) and fall back to the reference's exact expression
+// (sample_pos + exact_cell) only when a coordinate is within 1e-9 of an
+// integer; q_est differs from the exact quotient by < 1e-12 lattice units.
+template <class F>
+__device__ __forceinline__ void visit_inhull(const double o[3], const double d[3], const Geom& g,
+                                             const uint8_t* __restrict__ inside, double tau_keep,
+                                             F&& f) {
+    double te, tx;
+    if (!slab_span(o, d, g, te, tx)) return;
+    const int n = sample_count(te, tx, g.edge);
+    const double t0 = te - 0.5 * g.edge;
+    double qb[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) qb[a] = ((o[a] - g.lo[a]) + t0 * d[a]) * g.inv_edge;
+    const int nn[3] = {g.nx, g.ny, g.nz};
+    double trans = 1.0;
+    for (int k = 1; k <= n; ++k) {
+        double q[3];
+        int c[3];
+        bool safe = true;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            q[a] = fma((double)k, d[a], qb[a]);
+            const double fl = floor(q[a]);
+            const double fr = q[a] - fl;
+            safe = safe && fr > 1e-9 && fr < 1.0 - 1e-9;
+            c[a] = (int)fl;
+        }
+        if (!safe) {
+            double p[3];
+            sample_pos(o, d, te, g.edge, k, p);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) c[a] = exact_cell(p[a], g.lo[a], g.edge, g.inv_edge);
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) c[a] = clampi(c[a], nn[a] - 1);
+        if (__ldg(inside + ((int64_t)c[0] * g.ny + c[1]) * g.nz + c[2])) f(k, q, c, trans);
+        trans *= tau_keep;
+    }
+}
+
+struct PlanRay {
+    double d[3];
+    const double* o;
+    int res_index;
+};
+
+__device__ __forceinline__ bool plan_ray(const fvr_camera_t* __restrict__ cams,
+                                         const int32_t* __restrict__ ray_list, int64_t r, int u0,
+                                         int v0, int w, int h, PlanRay& pr) {
+    const int32_t e = ray_list[r];
+    const int view = e >> 24, pix = e & 0xFFFFFF;
+    const int row = pix / w, col = pix - row * w;
+    const fvr_camera_t& cam = cams[view];
+    pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, pr.d);
+    pr.o = cam.center;
+    pr.res_index = view * w * h + pix;
+    return true;
+}
+
+__global__ void __launch_bounds__(128) plan_count_kernel(
+    const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
+    int u0, int v0, int w, int h, const uint8_t* __restrict__ inside, Geom g,
+    const int32_t* __restrict__ kp_map, int32_t* __restrict__ counts) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rays) return;
+    PlanRay pr;
+    plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
+    visit_inhull(pr.o, pr.d, g, inside, 1.0, [&](int, const double*, const int* c, double) {
+        const int base = c[0] * g.sx + c[1] * g.sy + c[2];
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8) {
+            const int kp = base + (k8 >> 2) * g.sx + ((k8 >> 1) & 1) * g.sy + (k8 & 1);
+            atomicAdd(counts + kp_map[kp], 1);
+        }
+    });
+}
+
+__global__ void __launch_bounds__(128) plan_fill_kernel(
+    const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
+    int u0, int v0, int w, int h, const uint8_t* __restrict__ inside, Geom g, double tau_keep,
+    double alpha_l, float alpha_d, const int32_t* __restrict__ kp_map,
+    unsigned long long* __restrict__ cursor, int2* __restrict__ entries) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rays) return;
+    PlanRay pr;
+    plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
+    const float edge = (float)g.edge;
+    visit_inhull(pr.o, pr.d, g, inside, tau_keep, [&](int, const double* q, const int* c, double trans) {
+        const float base = (float)(alpha_l * trans);
+        float e[3][2];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float f = (float)(q[a] - (double)c[a]);
+            e[a][0] = f * edge;
+            e[a][1] = (f - 1.0f) * edge;
+        }
+        const int base_kp = c[0] * g.sx + c[1] * g.sy + c[2];
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8) {
+            const int cx = k8 >> 2, cy = (k8 >> 1) & 1, cz = k8 & 1;
+            const float dist = sqrtf(fmaf(e[0][cx], e[0][cx], fmaf(e[1][cy], e[1][cy], e[2][cz] * e[2][cz])));
+            const float wgt = base * expf(-alpha_d * dist);
+            const int kp = base_kp + cx * g.sx + cy * g.sy + cz;
+            const unsigned long long pos = atomicAdd(cursor + kp_map[kp], 1ull);
+            entries[pos] = make_int2(pr.res_index, __float_as_int(wgt));
+        }
+    });
+}
+
+// One warp per hull key point: delta = sum_e res[idx_e] * W_e (32.32 fixed point).
+template <bool PACKED>
+__global__ void __launch_bounds__(256) gather_kernel(
+    const long long* __restrict__ row_off, const int2* __restrict__ entries, int64_t n_rows,
+    const float* __restrict__ residual, const int32_t* __restrict__ kp_index,
+    float* __restrict__ values, float* __restrict__ layout, int layout_kind, int sy, int ny1,
+    long long* __restrict__ packed, const fvr_loop_state_t* __restrict__ state) {
+    if (state && state->done) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t row = warp; row < n_rows; row += n_warps) {
+        const long long b = row_off[row], e = row_off[row + 1];
+        long long acc = 0;
+        for (long long i = b + lane; i < e; i += 32) {
+            const int2 en = __ldg(entries + i);
+            const float prod = __ldg(residual + en.x) * __int_as_float(en.y);
+            acc += __float2ll_rn(prod * 4294967296.0f);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) {
+            if (PACKED) {
+                packed[row] = acc;
+            } else if (acc != 0) {
+                const int64_t idx = kp_index[row];
+                const double nv = (double)values[idx] + (double)acc * kFixInv;
+                const float f = (float)(nv > -1.0 ? nv : -1.0);
+                values[idx] = f;
+                if (layout) {
+                    const float cpos = fmaxf(f, 0.f);
+                    const int z = (int)(idx % sy);
+                    if (layout_kind == 2) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (z >= k) layout[4 * (idx - k) + k] = cpos;
+                    } else {
+                        const int y = (int)((idx / sy) % ny1);
+                        layout[4 * idx] = cpos;
+                        if (z >= 1) layout[4 * (idx - 1) + 1] = cpos;
+                        if (y >= 1) layout[4 * (idx - sy) + 2] = cpos;
+                        if (y >= 1 && z >= 1) layout[4 * (idx - sy - 1) + 3] = cpos;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Apply a packed (all-reduced) correction: one thread per hull key point.
+__global__ void update_packed_kernel(const long long* __restrict__ packed, int64_t n_rows,
+                                     const int32_t* __restrict__ kp_index, float* __restrict__ values,
+                                     float* __restrict__ layout, int layout_kind, int sy, int ny1,
+                                     const fvr_loop_state_t* __restrict__ state) {
+    if (state && state->done) return;
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n_rows;
+         row += (int64_t)gridDim.x * blockDim.x) {
+        const long long acc = packed[row];
+        if (acc == 0) continue;
+        const int64_t idx = kp_index[row];
+        const double nv = (double)values[idx] + (double)acc * kFixInv;
+        const float f = (float)(nv > -1.0 ? nv : -1.0);
+        values[idx] = f;
+        if (layout) {
+            const float cpos = fmaxf(f, 0.f);
+            const int z = (int)(idx % sy);
+            if (layout_kind == 2) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (z >= k) layout[4 * (idx - k) + k] = cpos;
+            } else {
+                const int y = (int)((idx / sy) % ny1);
+                layout[4 * idx] = cpos;
+                if (z >= 1) layout[4 * (idx - 1) + 1] = cpos;
+                if (y >= 1) layout[4 * (idx - sy) + 2] = cpos;
+                if (y >= 1 && z >= 1) layout[4 * (idx - sy - 1) + 3] = cpos;
+            }
+        }
+    }
+}
+
+}  // namespace fvr
+
+using namespace fvr;
+
+extern "C" int fvr_adjust_plan_count(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
+                                     int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
+                                     const uint8_t* inside_vox, fvr_grid_t grid, const int32_t* kp_map,
+                                     int32_t* row_counts, void* stream) {
+    FVR_TRY_BEGIN
+    if (int rc = check_grid(grid)) return rc;
+    if (n_rays == 0) return FVR_OK;
+    const Geom g = make_geom(grid);
+    plan_count_kernel<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, kp_map, row_counts);
+    return check_launch("adjust_plan_count");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
+                                    int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
+                                    const uint8_t* inside_vox, fvr_grid_t grid, double tau,
+                                    double alpha_l, double alpha_d, const int32_t* kp_map,
+                                    int64_t* cursor, int32_t* entries, void* stream) {
+    FVR_TRY_BEGIN
+    if (int rc = check_grid(grid)) return rc;
+    if (n_rays == 0) return FVR_OK;
+    const Geom g = make_geom(grid);
+    plan_fill_kernel<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d,
+        kp_map, reinterpret_cast<unsigned long long*>(cursor), reinterpret_cast<int2*>(entries));
+    return check_launch("adjust_plan_fill");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_loop_gather(const int64_t* row_offsets, const int32_t* entries, int64_t n_kp,
+                               const float* residual, const int32_t* kp_index, float* values,
+                               float* layout, int32_t layout_kind, fvr_grid_t grid, int64_t* packed,
+                               const fvr_loop_state_t* state, void* stream) {
+    FVR_TRY_BEGIN
+    if (n_kp == 0) return FVR_OK;
+    int64_t blocks = (n_kp * 32 + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    const int sy = grid.nz + 1, ny1 = grid.ny + 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    const auto* ro = reinterpret_cast<const long long*>(row_offsets);
+    const auto* en = reinterpret_cast<const int2*>(entries);
+    if (packed)
+        gather_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(ro, en, n_kp, residual, kp_index, values, layout,
+                                                              layout_kind, sy, ny1,
+                                                              reinterpret_cast<long long*>(packed), state);
+    else
+        gather_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(ro, en, n_kp, residual, kp_index, values, layout,
+                                                               layout_kind, sy, ny1, nullptr, state);
+    return check_launch("loop_gather");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_loop_update_packed(const int64_t* packed, int64_t n_kp, const int32_t* kp_index,
+                                      float* values, float* layout, int32_t layout_kind, fvr_grid_t grid,
+                                      const fvr_loop_state_t* state, void* stream) {
+    FVR_TRY_BEGIN
+    if (n_kp == 0) return FVR_OK;
+    int64_t blocks = (n_kp + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    update_packed_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const long long*>(packed), n_kp, kp_index, values, layout, layout_kind, grid.nz + 1,
+        grid.ny + 1, state);
+    return check_launch("loop_update_packed");
+    FVR_TRY_END
+}

@@ -153,6 +153,12 @@ class ChannelLoop:
         self.trace = t.zeros(max(self.max_iters, 1), dtype=t.float64, device=dev)
         self.trace_vol = t.zeros(max(self.max_iters, 1), dtype=t.float64, device=dev) \
             if ground_truth is not None else None
+        # deterministic mode back-projects through the precomputed gather plan
+        self.plan = (not loop_cfg.stochastic and self.n_rays > 0 and self.n_kp > 0
+                     and os.environ.get("FVR_ADJUST") != "scatter")
+        self.plan_nnz = 0
+        if self.plan:
+            self._build_plan()
         self.use_graph = use_graph and self.world == 1 and os.environ.get("FVR_NO_GRAPH") != "1"
         self.graph = None
         self.launches_per_iter = 0
@@ -228,15 +234,93 @@ class ChannelLoop:
                       self.accum.data_ptr(), stream)
         return 2 if self.n_kp else 0
 
+    # -- the back-projection plan (deterministic mode) --------------------------
+    def _build_plan(self) -> None:
+        """CSR of the fixed back-projection operator A (fvr_plan.cu): row = hull
+        key point, entry = (residual pixel, W).  Built once per call."""
+        t = self.t
+        dev = self.dev
+        stream = _lib.stream_ptr()
+        n_lat = self.values.numel()
+        kp_map = t.full((n_lat,), -1, dtype=t.int32, device=dev)
+        kp_map[self.kp[: self.n_kp].long()] = t.arange(self.n_kp, dtype=t.int32, device=dev)
+        counts = t.zeros(self.n_kp, dtype=t.int32, device=dev)
+        _lib.call("fvr_adjust_plan_count", self.cams.data_ptr(), self.rays.data_ptr(), self.n_rays,
+                  self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb, self.inside.data_ptr(), self.grid,
+                  kp_map.data_ptr(), counts.data_ptr(), stream)
+        offsets = t.zeros(self.n_kp + 1, dtype=t.int64, device=dev)
+        offsets[1:] = t.cumsum(counts.long(), 0)
+        nnz = int(offsets[-1].item())
+        cursor = offsets[:-1].clone()
+        entries = t.empty(max(2 * nnz, 2), dtype=t.int32, device=dev)
+        c = self.cfg
+        _lib.call("fvr_adjust_plan_fill", self.cams.data_ptr(), self.rays.data_ptr(), self.n_rays,
+                  self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb, self.inside.data_ptr(), self.grid,
+                  c.tau, c.alpha_l, c.alpha_d_eff, kp_map.data_ptr(), cursor.data_ptr(), entries.data_ptr(),
+                  stream)
+        self.plan_offsets = offsets
+        self.plan_entries = entries
+        self.plan_nnz = nnz
+
+    def _gather(self, stream, packed: bool):
+        if self.n_kp == 0:
+            return 0
+        _lib.call("fvr_loop_gather", self.plan_offsets.data_ptr(), self.plan_entries.data_ptr(), self.n_kp,
+                  self.residual.data_ptr(), self.kp.data_ptr(), self.values.data_ptr(), _lib.ptr(self.layout),
+                  self.layout_kind, self.grid, self.packed.data_ptr() if packed else None,
+                  self.state.data_ptr(), stream)
+        return 1
+
+    def _update_packed(self, stream):
+        if self.n_kp == 0:
+            return 0
+        _lib.call("fvr_loop_update_packed", self.packed.data_ptr(), self.n_kp, self.kp.data_ptr(),
+                  self.values.data_ptr(), _lib.ptr(self.layout), self.layout_kind, self.grid,
+                  self.state.data_ptr(), stream)
+        return 1
+
+    def _allreduce_packed(self, stream):
+        """All-reduce [packed | sq | vol] once the gather filled ``packed``."""
+        self.sq[: self.v_begin * self.bpv].zero_()
+        self.sq[self.v_end * self.bpv:].zero_()
+        if self.rank != 0 and self.vol is not None:
+            self.vol.zero_()
+        self.t.distributed.all_reduce(self.comm)
+        return 0
+
+    def stages(self):
+        """[(name, fn(stream) -> launches)] of one iteration, in order; the
+        name 'decision' marks where the convergence rule has been evaluated."""
+        s = [("render", self._render), ("volume", self._volume)]
+        if self.plan:
+            if self.world > 1:
+                s += [("adjust", lambda st: self._gather(st, True)), ("allreduce", self._allreduce_packed),
+                      ("finalize", self._finalize), ("decision", None), ("update", self._update_packed)]
+            else:
+                s += [("finalize", self._finalize), ("decision", None),
+                      ("adjust", lambda st: self._gather(st, False))]
+        else:
+            s += [("adjust", self._adjust)]
+            if self.world > 1:
+                s += [("allreduce", self._allreduce)]
+            s += [("finalize", self._finalize), ("decision", None), ("update", self._update)]
+        return s
+
     def pre_decision(self, stream) -> int:
-        n = self._render(stream) + self._volume(stream) + self._adjust(stream)
-        if self.world > 1:
-            n += self._allreduce(stream)
-        n += self._finalize(stream)
+        n = 0
+        for name, fn in self.stages():
+            if name == "decision":
+                break
+            n += fn(stream)
         return n
 
     def post_decision(self, stream) -> int:
-        return self._update(stream)
+        n, after = 0, False
+        for name, fn in self.stages():
+            if after:
+                n += fn(stream)
+            after = after or name == "decision"
+        return n
 
     def launch_iteration(self) -> None:
         stream = _lib.stream_ptr()
