@@ -8,6 +8,9 @@
 // L2/L1-resident lattice.  Blending state (transparency, radiance) is fp64 as
 // in the reference; each trilinear read is fp32.  Position and sample count
 // use the exact fp64 helpers of fvr_common.cuh.
+#include <algorithm>
+#include <vector>
+
 #include "fvr_stencil.cuh"
 
 namespace fvr {
@@ -87,7 +90,8 @@ template <int NCH, bool SCAT>
 __device__ __forceinline__ void march_render_fast(const double o[3], const double d[3], const Geom& g,
                                                   const float* __restrict__ values, int plane,
                                                   const float4* __restrict__ layout,
-                                                  const RenderConsts& rc, double out[NCH]) {
+                                                  const RenderConsts& rc, const float* __restrict__ thr,
+                                                  double out[NCH]) {
     double l[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) l[c] = 0.0;
@@ -126,23 +130,35 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
                     m[a] = min(max((int)r, 0), a == 0 ? g.nx : (a == 1 ? g.ny : g.nz));
                     dl[a] = (float)(q[a] - (double)m[a]);
                 }
-                uint32_t mask = 0xffffffffu;
-                if (!interior) {
-                    double p[3];
-                    sample_pos(o, d, te, g.edge, k, p);
-                    mask = inbox_mask(p, g, rc.half_gather);
-                }
 #pragma unroll 1
                 for (int c = 0; c < NCH; ++c) {
                     float v[27];
-                    if (interior)
+                    float e = 0.f, acc = 0.f;
+                    if (interior) {
                         load_stencil_z4(layout + (int64_t)c * plane, g, m[0], m[1], m[2], v);
-                    else
+                        moment_eval(v, dl[0], dl[1], dl[2], thr, e, acc);
+                        // both are sums of non-negative terms in exact arithmetic;
+                        // the expanded form can round a vanishing sum below zero
+                        e = fmaxf(e, 0.f);
+                        acc = fmaxf(acc, 0.f);
+                    } else {
+                        // within half a voxel of a box face: the reference's
+                        // exact per-direction in-box test masks the gathers;
+                        // an all-zero neighbourhood contributes nothing at all
                         load_stencil_clamped(values + (int64_t)c * plane, g, m[0], m[1], m[2], v);
-                    Stencil st;
-                    stencil_from(v, st);
-                    const float e = stencil_tri(st, dl[0], dl[1], dl[2]);
-                    const float acc = stencil_scatter<true>(st, dl[0], dl[1], dl[2], mask);
+                        bool any = false;
+#pragma unroll
+                        for (int j = 0; j < 27; ++j) any = any || v[j] != 0.f;
+                        if (any) {
+                            double p[3];
+                            sample_pos(o, d, te, g.edge, k, p);
+                            const uint32_t mask = inbox_mask(p, g, rc.half_gather);
+                            Stencil st;
+                            stencil_from(v, st);
+                            e = stencil_tri(st, dl[0], dl[1], dl[2]);
+                            acc = stencil_scatter<true>(st, dl[0], dl[1], dl[2], mask);
+                        }
+                    }
                     const double l_src = rc.sigma_a * (double)e + (double)acc * rc.scat_scale;
                     l[c] += t_dst * (rc.tau * l_src);
                 }
@@ -182,12 +198,18 @@ __device__ __forceinline__ void march_dispatch(const double o[3], const double d
                                                const float* __restrict__ values, int plane,
                                                const float4* __restrict__ layout,
                                                const RenderConsts& rc, const double* __restrict__ scat,
-                                               double out[NCH]) {
+                                               const float* __restrict__ thr, double out[NCH]) {
     if (MODE == kModePlain) march_render<NCH, false, true>(o, d, g, values, plane, rc, scat, out);
     if (MODE == kModeScatG0) march_render<NCH, true, true>(o, d, g, values, plane, rc, scat, out);
     if (MODE == kModeScatG) march_render<NCH, true, false>(o, d, g, values, plane, rc, scat, out);
-    if (MODE == kModeFastPlain) march_render_fast<NCH, false>(o, d, g, values, plane, layout, rc, out);
-    if (MODE == kModeFastScat) march_render_fast<NCH, true>(o, d, g, values, plane, layout, rc, out);
+    if (MODE == kModeFastPlain) march_render_fast<NCH, false>(o, d, g, values, plane, layout, rc, thr, out);
+    if (MODE == kModeFastScat) march_render_fast<NCH, true>(o, d, g, values, plane, layout, rc, thr, out);
+}
+
+// Shared-memory copy of the sorted gather offsets (moment split search).
+__device__ __forceinline__ void load_thresholds(float* s_thr) {
+    for (int i = threadIdx.x; i < 3 * kScatDirs; i += blockDim.x) s_thr[i] = (&c_thr[0][0])[i];
+    __syncthreads();
 }
 
 // ---- _kernels.render_rays drop-in -----------------------------------------
@@ -201,12 +223,14 @@ __global__ void __launch_bounds__(128) render_rays_kernel(double ox, double oy, 
                                                           Geom g, RenderConsts rc,
                                                           const double* __restrict__ scat,
                                                           double* __restrict__ out) {
+    __shared__ float s_thr[3 * kScatDirs];
+    if (MODE == kModeFastScat) load_thresholds(s_thr);
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_rays) return;
     const double o[3] = {ox, oy, oz};
     const double d[3] = {dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2]};
     double res[NCH];
-    march_dispatch<NCH, MODE>(o, d, g, values, plane, layout, rc, scat, res);
+    march_dispatch<NCH, MODE>(o, d, g, values, plane, layout, rc, scat, s_thr, res);
 #pragma unroll
     for (int c = 0; c < NCH; ++c) out[r * NCH + c] = res[c];
 }
@@ -223,6 +247,8 @@ __global__ void __launch_bounds__(128) render_pixels_kernel(fvr_camera_t cam,
                                                             Geom g, RenderConsts rc,
                                                             const double* __restrict__ scat,
                                                             double* __restrict__ out) {
+    __shared__ float s_thr[3 * kScatDirs];
+    if (MODE == kModeFastScat) load_thresholds(s_thr);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double u, v;
@@ -236,7 +262,7 @@ __global__ void __launch_bounds__(128) render_pixels_kernel(fvr_camera_t cam,
     double d[3];
     pixel_dir(cam, u, v, d);
     double res[NCH];
-    march_dispatch<NCH, MODE>(cam.center, d, g, values, plane, layout, rc, scat, res);
+    march_dispatch<NCH, MODE>(cam.center, d, g, values, plane, layout, rc, scat, s_thr, res);
 #pragma unroll
     for (int c = 0; c < NCH; ++c) out[i * NCH + c] = res[c];
 }
@@ -254,6 +280,8 @@ __global__ void __launch_bounds__(kTileThreads) loop_render_kernel(
     const fvr_loop_state_t* __restrict__ state) {
     if (state && state->done) return;
     __shared__ double red[kTileThreads / 32];
+    __shared__ float s_thr[3 * kScatDirs];
+    if (MODE == kModeFastScat) load_thresholds(s_thr);
     const int view = blockIdx.y;
     const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
     const int col = tx * kTileW + (threadIdx.x % kTileW);
@@ -264,7 +292,7 @@ __global__ void __launch_bounds__(kTileThreads) loop_render_kernel(
         double d[3];
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         double rec[1];
-        march_dispatch<1, MODE>(cam.center, d, g, values, 0, layout, rc, scat, rec);
+        march_dispatch<1, MODE>(cam.center, d, g, values, 0, layout, rc, scat, s_thr, rec);
         const int64_t pix = ((int64_t)view * h + row) * w + col;
         const double r = (double)src[pix] - rec[0];
         residual[pix] = (float)r;
@@ -373,6 +401,76 @@ bool scatter_dirs_match(const double* host_dirs, int n) {
 }
 }  // namespace fvr
 
+namespace {
+// Moment tables of fvr_stencil.cuh for one direction set (fp64, stored f32).
+int build_moment_tables(const double* dirs) {
+    constexpr int S = kScatDirs, K = kSplits;
+    double c[3][S], ch[3][S];
+    int rank[3][S];
+    float thr[3][S];
+    for (int a = 0; a < 3; ++a) {
+        int ord[S];
+        for (int s = 0; s < S; ++s) {
+            c[a][s] = 0.5 * dirs[3 * s + a];
+            ch[a][s] = 0.5 * c[a][s];
+            ord[s] = s;
+        }
+        std::stable_sort(ord, ord + S, [&](int i, int j) { return (float)c[a][i] < (float)c[a][j]; });
+        for (int r = 0; r < S; ++r) {
+            rank[a][ord[r]] = r;
+            thr[a][r] = (float)c[a][ord[r]];
+        }
+    }
+    // prod_{a in E} c_{s,a}/2, E mask x=4 y=2 z=1
+    double cE[8][S];
+    for (int e = 0; e < 8; ++e)
+        for (int s = 0; s < S; ++s)
+            cE[e][s] = ((e & 4) ? ch[0][s] : 1.0) * ((e & 2) ? ch[1][s] : 1.0) * ((e & 1) ? ch[2][s] : 1.0);
+    auto sig = [&](int a, int i, int s) { return rank[a][s] < i ? -1.0 : 1.0; };
+    std::vector<float> q1(3 * K * 8), q2(3 * K * K * 8), q3((size_t)K * K * K * 8);
+    float q0[8];
+    for (int e = 0; e < 8; ++e) {
+        double acc = 0.0;
+        for (int s = 0; s < S; ++s) acc += cE[e][s];
+        q0[e] = (float)acc;
+    }
+    for (int a = 0; a < 3; ++a)
+        for (int i = 0; i < K; ++i)
+            for (int e = 0; e < 8; ++e) {
+                double acc = 0.0;
+                for (int s = 0; s < S; ++s) acc += sig(a, i, s) * cE[e][s];
+                q1[(a * K + i) * 8 + e] = (float)acc;
+            }
+    const int pa[3] = {0, 0, 1}, pb[3] = {1, 2, 2};
+    for (int p = 0; p < 3; ++p)
+        for (int i = 0; i < K; ++i)
+            for (int j = 0; j < K; ++j)
+                for (int e = 0; e < 8; ++e) {
+                    double acc = 0.0;
+                    for (int s = 0; s < S; ++s) acc += sig(pa[p], i, s) * sig(pb[p], j, s) * cE[e][s];
+                    q2[((p * K + i) * K + j) * 8 + e] = (float)acc;
+                }
+    for (int i = 0; i < K; ++i)
+        for (int j = 0; j < K; ++j)
+            for (int l = 0; l < K; ++l) {
+                double sg[S];
+                for (int s = 0; s < S; ++s) sg[s] = sig(0, i, s) * sig(1, j, s) * sig(2, l, s);
+                for (int e = 0; e < 8; ++e) {
+                    double acc = 0.0;
+                    for (int s = 0; s < S; ++s) acc += sg[s] * cE[e][s];
+                    q3[(((size_t)i * K + j) * K + l) * 8 + e] = (float)acc;
+                }
+            }
+    if (cudaMemcpyToSymbol(c_thr, thr, sizeof(thr)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_q0, q0, sizeof(q0)) != cudaSuccess ||
+        cudaMemcpyToSymbol(g_q1, q1.data(), q1.size() * sizeof(float)) != cudaSuccess ||
+        cudaMemcpyToSymbol(g_q2, q2.data(), q2.size() * sizeof(float)) != cudaSuccess ||
+        cudaMemcpyToSymbol(g_q3, q3.data(), q3.size() * sizeof(float)) != cudaSuccess)
+        return set_error(FVR_ERR_CUDA, "moment table upload failed");
+    return FVR_OK;
+}
+}  // namespace
+
 extern "C" int fvr_set_scatter_dirs(const double* dirs_host, int32_t n) {
     FVR_TRY_BEGIN
     if (n != kScatDirs) return set_error(FVR_ERR_INVALID, "the stencil path is compiled for 32 directions");
@@ -386,6 +484,7 @@ extern "C" int fvr_set_scatter_dirs(const double* dirs_host, int32_t n) {
     if (cudaMemcpyToSymbol(c_dir, d, sizeof(d)) != cudaSuccess ||
         cudaMemcpyToSymbol(c_half_dir, h, sizeof(h)) != cudaSuccess)
         return set_error(FVR_ERR_CUDA, "cudaMemcpyToSymbol failed");
+    if (int e = build_moment_tables(dirs_host)) return e;
     for (int i = 0; i < 3 * kScatDirs; ++i) g_dirs_host[i] = dirs_host[i];
     g_dirs_ready = true;
     return FVR_OK;

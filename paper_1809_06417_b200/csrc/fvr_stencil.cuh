@@ -144,4 +144,130 @@ __device__ __forceinline__ uint32_t inbox_mask(const double p[3], const Geom& g,
     return m;
 }
 
+// ---- moment evaluation of the 32-direction gather (interior samples) -------
+//
+// In the basis (1, x/2, |x|/2) per axis the trilinear read at offset x from
+// the stencil centre is  sum_k V[k] prod_a u_{k_a}(x_a)  with the separable
+// stencil transform  V = (v0, v+ - v-, v+ + v- - 2 v0)^{(x) 3}.  Summed over
+// the gathers x_s = delta + c_s (c_s = s/2), the direction sum becomes
+//
+//   S = sum_k V[k] M[k],   M[k] = sum_{E subset P(k)} delta'^{P(k) \ E} Q_{A(k)}[E]
+//
+// where P(k) are the axes with k_a != 1, A(k) the axes with k_a = |x|,
+// delta' = delta/2, and Q_A[E] = sum_s sigma_s^A prod_{a in E} c_{s,a}/2 with
+// sigma_{s,a} = sign(delta_a + c_{s,a}).  Q_A depends on delta only through
+// the split index i_a = #{s : c_{s,a} < -delta_a} of each axis in A, so it
+// is tabulated once per direction set: Q1 (3 x 33 x 8), Q2 (3 x 33^2 x 8),
+// Q3 (33^3 x 8).  Exact in real arithmetic (checked against the brute-force
+// sum to 1e-15 in fp64); ~400 instructions per sample instead of ~1400.
+constexpr int kSplits = kScatDirs + 1;
+__constant__ float c_thr[3][kScatDirs];  // sorted c_{s,a} = s_a / 2 per axis
+__constant__ float c_q0[8];              // Q_{empty}[E]
+__device__ float4 g_q1[3 * kSplits * 2];
+__device__ float4 g_q2[3 * kSplits * kSplits * 2];
+__device__ float4 g_q3[kSplits * kSplits * kSplits * 2];
+
+// #{thr < key} over 32 sorted thresholds in shared memory
+__device__ __forceinline__ int split_index(const float* __restrict__ thr, float key) {
+    int i = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1)
+        if (thr[i + step - 1] < key) i += step;
+    if (i == 31 && thr[31] < key) i = 32;
+    return i;
+}
+
+__device__ __forceinline__ void load_q8(const float4* __restrict__ t, int row, float q[8]) {
+    const float4 a = __ldg(t + 2 * row), b = __ldg(t + 2 * row + 1);
+    q[0] = a.x; q[1] = a.y; q[2] = a.z; q[3] = a.w;
+    q[4] = b.x; q[5] = b.y; q[6] = b.z; q[7] = b.w;
+}
+
+// (emission, direction sum) at the stencil centre offset delta; v as in
+// load_stencil_z4, thr the shared-memory copy of c_thr.
+__device__ __forceinline__ void moment_eval(const float v[27], float dx, float dy, float dz,
+                                            const float* __restrict__ thr, float& emit, float& scat) {
+    // separable transform of the stencil: V[kx][ky][kz]
+    float V[27];
+    {
+        float t1[27];
+        // along z (innermost)
+#pragma unroll
+        for (int l = 0; l < 9; ++l) {
+            const float m = v[3 * l], c = v[3 * l + 1], p = v[3 * l + 2];
+            t1[3 * l] = c;
+            t1[3 * l + 1] = p - m;
+            t1[3 * l + 2] = fmaf(-2.f, c, p + m);
+        }
+        float t2[27];
+        // along y
+#pragma unroll
+        for (int jx = 0; jx < 3; ++jx)
+#pragma unroll
+            for (int kz = 0; kz < 3; ++kz) {
+                const float m = t1[(jx * 3 + 0) * 3 + kz], c = t1[(jx * 3 + 1) * 3 + kz],
+                            p = t1[(jx * 3 + 2) * 3 + kz];
+                t2[(jx * 3 + 0) * 3 + kz] = c;
+                t2[(jx * 3 + 1) * 3 + kz] = p - m;
+                t2[(jx * 3 + 2) * 3 + kz] = fmaf(-2.f, c, p + m);
+            }
+        // along x
+#pragma unroll
+        for (int l = 0; l < 9; ++l) {
+            const float m = t2[l], c = t2[9 + l], p = t2[18 + l];
+            V[l] = c;
+            V[9 + l] = p - m;
+            V[18 + l] = fmaf(-2.f, c, p + m);
+        }
+    }
+    const float hx = 0.5f * dx, hy = 0.5f * dy, hz = 0.5f * dz;
+    // emission: basis values (1, x/2, |x|/2) at delta
+    {
+        const float ux[3] = {1.f, hx, fabsf(hx)}, uy[3] = {1.f, hy, fabsf(hy)}, uz[3] = {1.f, hz, fabsf(hz)};
+        float e = 0.f;
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+            for (int ky = 0; ky < 3; ++ky) {
+                const float uxy = ux[kx] * uy[ky];
+#pragma unroll
+                for (int kz = 0; kz < 3; ++kz) e = fmaf(V[(kx * 3 + ky) * 3 + kz], uxy * uz[kz], e);
+            }
+        emit = e;
+    }
+    // split indices and the sign-dependent moment tables
+    const int ix = split_index(thr, -dx), iy = split_index(thr + kScatDirs, -dy),
+              iz = split_index(thr + 2 * kScatDirs, -dz);
+    float Q[8][8];  // Q[A mask: x=4,y=2,z=1][E mask]
+#pragma unroll
+    for (int e = 0; e < 8; ++e) Q[0][e] = c_q0[e];
+    load_q8(g_q1, 0 * kSplits + ix, Q[4]);
+    load_q8(g_q1, 1 * kSplits + iy, Q[2]);
+    load_q8(g_q1, 2 * kSplits + iz, Q[1]);
+    load_q8(g_q2, (0 * kSplits + ix) * kSplits + iy, Q[6]);
+    load_q8(g_q2, (1 * kSplits + ix) * kSplits + iz, Q[5]);
+    load_q8(g_q2, (2 * kSplits + iy) * kSplits + iz, Q[3]);
+    load_q8(g_q3, (ix * kSplits + iy) * kSplits + iz, Q[7]);
+    // delta' monomials D[m] = prod_{a in m} delta'_a
+    float D[8];
+    D[0] = 1.f; D[4] = hx; D[2] = hy; D[1] = hz;
+    D[6] = hx * hy; D[5] = hx * hz; D[3] = hy * hz; D[7] = D[6] * hz;
+    float s = 0.f;
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+            for (int kz = 0; kz < 3; ++kz) {
+                const int P = ((kx != 0) << 2) | ((ky != 0) << 1) | (kz != 0);
+                const int A = ((kx == 2) << 2) | ((ky == 2) << 1) | (kz == 2);
+                float M = 0.f;
+#pragma unroll
+                for (int E = 0; E < 8; ++E)
+                    if ((E & ~P) == 0) M = fmaf(D[P ^ E], Q[A][E], M);
+                s = fmaf(V[(kx * 3 + ky) * 3 + kz], M, s);
+            }
+    scat = s;
+}
+
 }  // namespace fvr
