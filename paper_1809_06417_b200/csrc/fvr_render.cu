@@ -91,7 +91,7 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
                                                   const float* __restrict__ values, int plane,
                                                   const float4* __restrict__ layout,
                                                   const RenderConsts& rc, const float* __restrict__ thr,
-                                                  double out[NCH]) {
+                                                  const float4* q1, const float4* q2, double out[NCH]) {
     double l[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) l[c] = 0.0;
@@ -136,7 +136,7 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
                     float e = 0.f, acc = 0.f;
                     if (interior) {
                         load_stencil_z4(layout + (int64_t)c * plane, g, m[0], m[1], m[2], v);
-                        moment_eval(v, dl[0], dl[1], dl[2], thr, e, acc);
+                        moment_eval(v, dl[0], dl[1], dl[2], thr, q1, q2, e, acc);
                         // both are sums of non-negative terms in exact arithmetic;
                         // the expanded form can round a vanishing sum below zero
                         e = fmaxf(e, 0.f);
@@ -202,8 +202,8 @@ __device__ __forceinline__ void march_dispatch(const double o[3], const double d
     if (MODE == kModePlain) march_render<NCH, false, true>(o, d, g, values, plane, rc, scat, out);
     if (MODE == kModeScatG0) march_render<NCH, true, true>(o, d, g, values, plane, rc, scat, out);
     if (MODE == kModeScatG) march_render<NCH, true, false>(o, d, g, values, plane, rc, scat, out);
-    if (MODE == kModeFastPlain) march_render_fast<NCH, false>(o, d, g, values, plane, layout, rc, thr, out);
-    if (MODE == kModeFastScat) march_render_fast<NCH, true>(o, d, g, values, plane, layout, rc, thr, out);
+    if (MODE == kModeFastPlain) march_render_fast<NCH, false>(o, d, g, values, plane, layout, rc, thr, g_q1, g_q2, out);
+    if (MODE == kModeFastScat) march_render_fast<NCH, true>(o, d, g, values, plane, layout, rc, thr, g_q1, g_q2, out);
 }
 
 // Shared-memory copy of the sorted gather offsets (moment split search).
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(128) render_pixels_kernel(fvr_camera_t cam,
 
 // ---- loop render: every bbox pixel of every view + residual + RMSE partials
 
-constexpr int kTileW = 16, kTileH = 8, kTileThreads = kTileW * kTileH;
+constexpr int kTileW = 16, kTileH = 16, kTileThreads = kTileW * kTileH;
 
 template <int MODE>
 __global__ void __launch_bounds__(kTileThreads) loop_render_kernel(
@@ -300,6 +300,51 @@ __global__ void __launch_bounds__(kTileThreads) loop_render_kernel(
     }
     const double total = block_sum<kTileThreads>(sq, red);
     if (threadIdx.x == 0) sq_partials[(int64_t)view * gridDim.x + blockIdx.x] = total;
+}
+
+// Persistent variant for the single-scattering fast path: two CTAs per SM,
+// each stages the Q1/Q2 moment tables (107 KB) and the split thresholds in
+// shared memory once and then walks the (view, tile) list.
+constexpr int kQ1Vec = 3 * kSplits * 2, kQ2Vec = 3 * kSplits * kSplits * 2;
+constexpr size_t kScatSmem = sizeof(float4) * (kQ1Vec + kQ2Vec) + sizeof(float) * 3 * kScatDirs;
+
+__global__ void __launch_bounds__(kTileThreads, 2) loop_render_scat_kernel(
+    const fvr_camera_t* __restrict__ cams, int n_views, int u0, int v0, int w, int h, int tiles_x,
+    int tiles_per_view, const float* __restrict__ src, const float* __restrict__ values,
+    const float4* __restrict__ layout, Geom g, RenderConsts rc, float* __restrict__ residual,
+    double* __restrict__ sq_partials, const fvr_loop_state_t* __restrict__ state) {
+    if (state && state->done) return;
+    extern __shared__ float4 smem[];
+    float4* s_q1 = smem;
+    float4* s_q2 = smem + kQ1Vec;
+    float* s_thr = reinterpret_cast<float*>(smem + kQ1Vec + kQ2Vec);
+    for (int i = threadIdx.x; i < kQ1Vec; i += blockDim.x) s_q1[i] = g_q1[i];
+    for (int i = threadIdx.x; i < kQ2Vec; i += blockDim.x) s_q2[i] = g_q2[i];
+    for (int i = threadIdx.x; i < 3 * kScatDirs; i += blockDim.x) s_thr[i] = (&c_thr[0][0])[i];
+    __syncthreads();
+    __shared__ double red[kTileThreads / 32];
+    const int total = n_views * tiles_per_view;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int view = t / tiles_per_view, tile = t - view * tiles_per_view;
+        const int tx = tile % tiles_x, ty = tile / tiles_x;
+        const int col = tx * kTileW + (threadIdx.x % kTileW);
+        const int row = ty * kTileH + (threadIdx.x / kTileW);
+        double sq = 0.0;
+        if (col < w && row < h) {
+            const fvr_camera_t& cam = cams[view];
+            double d[3];
+            pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
+            double rec[1];
+            march_render_fast<1, true>(cam.center, d, g, values, 0, layout, rc, s_thr, s_q1, s_q2, rec);
+            const int64_t pix = ((int64_t)view * h + row) * w + col;
+            const double r = (double)src[pix] - rec[0];
+            residual[pix] = (float)r;
+            sq = r * r;
+        }
+        const double tot = block_sum<kTileThreads>(sq, red);
+        if (threadIdx.x == 0) sq_partials[t] = tot;
+        __syncthreads();  // red[] is reused by the next tile
+    }
 }
 
 }  // namespace fvr
@@ -593,7 +638,24 @@ extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_
         case kModePlain: FVR_LOOP_RENDER(kModePlain); break;
         case kModeScatG0: FVR_LOOP_RENDER(kModeScatG0); break;
         case kModeFastPlain: FVR_LOOP_RENDER(kModeFastPlain); break;
-        default: FVR_LOOP_RENDER(kModeFastScat); break;
+        default: {
+            static bool attr_set = false;
+            if (!attr_set) {
+                if (cudaFuncSetAttribute(loop_render_scat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kScatSmem) != cudaSuccess)
+                    return set_error(FVR_ERR_CUDA, "cannot reserve shared memory for the moment tables");
+                attr_set = true;
+            }
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const int total = tiles * n_views;
+            const int blocks = total < 2 * sms ? total : 2 * sms;
+            loop_render_scat_kernel<<<blocks, kTileThreads, kScatSmem, st>>>(
+                cams, n_views, u0, v0, bbox_w, bbox_h, tiles_x, tiles, src, values, lay, g, rc, residual,
+                sq_partials, state);
+            break;
+        }
     }
 #undef FVR_LOOP_RENDER
     return check_launch("loop_render");

@@ -178,15 +178,20 @@ __device__ __forceinline__ int split_index(const float* __restrict__ thr, float 
 }
 
 __device__ __forceinline__ void load_q8(const float4* __restrict__ t, int row, float q[8]) {
-    const float4 a = __ldg(t + 2 * row), b = __ldg(t + 2 * row + 1);
+    const float4 a = t[2 * row], b = t[2 * row + 1];
     q[0] = a.x; q[1] = a.y; q[2] = a.z; q[3] = a.w;
     q[4] = b.x; q[5] = b.y; q[6] = b.z; q[7] = b.w;
 }
 
 // (emission, direction sum) at the stencil centre offset delta; v as in
-// load_stencil_z4, thr the shared-memory copy of c_thr.
+// load_stencil_z4, thr the shared-memory copy of c_thr, q1/q2 the Q1/Q2
+// tables (shared memory in the persistent loop kernel, else global).  The
+// all-|x| moment M[|x|,|y|,|z|] = 1/8 sum_s |x_s y_s z_s| is summed directly:
+// its table (Q3, 1.15 MB) would cost a random 32-byte L2 gather per sample,
+// the L1/TEX bottleneck measured by ncu (profiles/r1b_*).
 __device__ __forceinline__ void moment_eval(const float v[27], float dx, float dy, float dz,
-                                            const float* __restrict__ thr, float& emit, float& scat) {
+                                            const float* __restrict__ thr, const float4* q1,
+                                            const float4* q2, float& emit, float& scat) {
     // separable transform of the stencil: V[kx][ky][kz]
     float V[27];
     {
@@ -241,13 +246,19 @@ __device__ __forceinline__ void moment_eval(const float v[27], float dx, float d
     float Q[8][8];  // Q[A mask: x=4,y=2,z=1][E mask]
 #pragma unroll
     for (int e = 0; e < 8; ++e) Q[0][e] = c_q0[e];
-    load_q8(g_q1, 0 * kSplits + ix, Q[4]);
-    load_q8(g_q1, 1 * kSplits + iy, Q[2]);
-    load_q8(g_q1, 2 * kSplits + iz, Q[1]);
-    load_q8(g_q2, (0 * kSplits + ix) * kSplits + iy, Q[6]);
-    load_q8(g_q2, (1 * kSplits + ix) * kSplits + iz, Q[5]);
-    load_q8(g_q2, (2 * kSplits + iy) * kSplits + iz, Q[3]);
-    load_q8(g_q3, (ix * kSplits + iy) * kSplits + iz, Q[7]);
+    load_q8(q1, 0 * kSplits + ix, Q[4]);
+    load_q8(q1, 1 * kSplits + iy, Q[2]);
+    load_q8(q1, 2 * kSplits + iz, Q[1]);
+    load_q8(q2, (0 * kSplits + ix) * kSplits + iy, Q[6]);
+    load_q8(q2, (1 * kSplits + ix) * kSplits + iz, Q[5]);
+    load_q8(q2, (2 * kSplits + iy) * kSplits + iz, Q[3]);
+    float m222 = 0.f;
+#pragma unroll
+    for (int d = 0; d < kScatDirs; ++d) {
+        const float p = (dx + c_half_dir[0][d]) * (dy + c_half_dir[1][d]) * (dz + c_half_dir[2][d]);
+        m222 += fabsf(p);
+    }
+    m222 *= 0.125f;
     // delta' monomials D[m] = prod_{a in m} delta'_a
     float D[8];
     D[0] = 1.f; D[4] = hx; D[2] = hy; D[1] = hz;
@@ -262,9 +273,13 @@ __device__ __forceinline__ void moment_eval(const float v[27], float dx, float d
                 const int P = ((kx != 0) << 2) | ((ky != 0) << 1) | (kz != 0);
                 const int A = ((kx == 2) << 2) | ((ky == 2) << 1) | (kz == 2);
                 float M = 0.f;
+                if (A == 7) {
+                    M = m222;
+                } else {
 #pragma unroll
-                for (int E = 0; E < 8; ++E)
-                    if ((E & ~P) == 0) M = fmaf(D[P ^ E], Q[A][E], M);
+                    for (int E = 0; E < 8; ++E)
+                        if ((E & ~P) == 0) M = fmaf(D[P ^ E], Q[A][E], M);
+                }
                 s = fmaf(V[(kx * 3 + ky) * 3 + kz], M, s);
             }
     scat = s;
