@@ -94,11 +94,12 @@ int64_t fvr_launch_count(void);
  * out (n_rays, n_channels) f64. n_channels <= 4.  layout (optional, device,
  * n_channels * lattice * 4 f32) is scratch for the packed copy the fast
  * evaluators read (see fvr_render_layout_kind); NULL selects the general
- * per-sample path. */
+ * per-sample path.  occ (optional, device, lattice u8) is scratch for the
+ * empty-space occupancy map (fvr_occupancy) the fast paths skip with. */
 int fvr_render_rays(const double origin[3], const double* dirs, int64_t n_rays,
                     const float* values, int32_t n_channels, fvr_grid_t grid,
                     fvr_render_params_t params, const double* background,
-                    const double* scat_dirs, float* layout, double* out, void* stream);
+                    const double* scat_dirs, float* layout, uint8_t* occ, double* out, void* stream);
 int fvr_render_rays_host(const double origin[3], const double* dirs, int64_t n_rays,
                          const float* values, int32_t n_channels, fvr_grid_t grid,
                          fvr_render_params_t params, const double* background,
@@ -138,7 +139,7 @@ int fvr_apply_correction(float* values, int64_t* accum, const int32_t* kp_index,
 int fvr_render_pixels(const fvr_camera_t* camera, const double* us, const double* vs,
                       int64_t n, const float* values, int32_t n_channels, fvr_grid_t grid,
                       fvr_render_params_t params, const double* background,
-                      const double* scat_dirs, float* layout, double* out, void* stream);
+                      const double* scat_dirs, float* layout, uint8_t* occ, double* out, void* stream);
 
 /* Packed copies of max(v, 0) read by the fast render paths: kind 1 (YZQ,
  * emission only) or 2 (Z4, single scattering); 0 = none applies.  The Z4
@@ -148,6 +149,11 @@ int fvr_set_scatter_dirs(const double* dirs_host, int32_t n);
 int fvr_render_layout_kind(fvr_render_params_t params, fvr_grid_t grid);
 int fvr_pack_layout(const float* values, int32_t n_channels, fvr_grid_t grid, int32_t kind,
                     float* layout, void* stream);
+/* occ[j] = 1 when a key point within Chebyshev distance 1 of j is positive in
+ * some channel or set in force_mask (lattice u8, may be NULL).  Samples whose
+ * neighbourhood is unoccupied contribute exactly 0 and are skipped. */
+int fvr_occupancy(const float* values, int32_t n_channels, const uint8_t* force_mask,
+                  fvr_grid_t grid, uint8_t* occ, void* stream);
 
 /* ---- one iteration of the reconstruction loop (device resident) ------- */
 
@@ -159,7 +165,7 @@ int fvr_loop_blocks_per_view(int32_t bbox_w, int32_t bbox_h);
  * per-block squared-residual sums (f64). cams is a device array. */
 int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0,
                     int32_t bbox_w, int32_t bbox_h, const float* src, const float* values,
-                    const float* layout, fvr_grid_t grid, fvr_render_params_t params, double background,
+                    const float* layout, const uint8_t* occ, fvr_grid_t grid, fvr_render_params_t params, double background,
                     const double* scat_dirs, float* residual, double* sq_partials,
                     const fvr_loop_state_t* state, void* stream);
 

@@ -79,7 +79,7 @@ _SIGNATURES = {
     "fvr_last_error": (c_char_p, []),
     "fvr_abi_version": (c_int, []),
     "fvr_launch_count": (c_int64, []),
-    "fvr_render_rays": (c_int, [_P, _P, c_int64, _P, c_int32, _GRID, _PARAMS, _P, _P, _P, _P, _P]),
+    "fvr_render_rays": (c_int, [_P, _P, c_int64, _P, c_int32, _GRID, _PARAMS, _P, _P, _P, _P, _P, _P]),
     "fvr_render_rays_host": (c_int, [_P, _P, c_int64, _P, c_int32, _GRID, _PARAMS, _P, _P, _P]),
     "fvr_count_hull_samples": (c_int, [_P, _P, c_int64, _P, _GRID, _P, _P]),
     "fvr_count_hull_samples_host": (c_int, [_P, _P, c_int64, _P, _GRID, _P]),
@@ -94,15 +94,16 @@ _SIGNATURES = {
     "fvr_apply_correction": (c_int, [_P, _P, _P, c_int64, _P]),
     "fvr_render_pixels": (
         c_int,
-        [_P, _P, _P, c_int64, _P, c_int32, _GRID, _PARAMS, _P, _P, _P, _P, _P],
+        [_P, _P, _P, c_int64, _P, c_int32, _GRID, _PARAMS, _P, _P, _P, _P, _P, _P],
     ),
+    "fvr_occupancy": (c_int, [_P, c_int32, _P, _GRID, _P, _P]),
     "fvr_set_scatter_dirs": (c_int, [_P, c_int32]),
     "fvr_render_layout_kind": (c_int, [_PARAMS, _GRID]),
     "fvr_pack_layout": (c_int, [_P, c_int32, _GRID, c_int32, _P, _P]),
     "fvr_loop_blocks_per_view": (c_int, [c_int32, c_int32]),
     "fvr_loop_render": (
         c_int,
-        [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _P, _P, _P, _GRID, _PARAMS, c_double, _P,
+        [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _P, _P, _P, _P, _GRID, _PARAMS, c_double, _P,
          _P, _P, _P, _P],
     ),
     "fvr_loop_adjust": (

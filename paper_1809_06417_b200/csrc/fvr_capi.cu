@@ -84,7 +84,7 @@ extern "C" int fvr_render_rays_host(const double origin[3], const double* dirs, 
     const int n_scat = params.n_scat > 0 ? params.n_scat : 0;
     DevBuf d_dirs(sizeof(double) * 3 * n_rays), d_vals(sizeof(float) * lat),
         d_scat(sizeof(double) * 3 * (n_scat ? n_scat : 1)), d_out(sizeof(double) * n_rays * n_channels),
-        d_layout(sizeof(float) * 4 * lat);
+        d_layout(sizeof(float) * 4 * lat), d_occ(lattice_size(grid));
     h2d(d_dirs.p, dirs, sizeof(double) * 3 * n_rays);
     h2d(d_vals.p, values, sizeof(float) * lat);
     if (n_scat && scat_dirs) h2d(d_scat.p, scat_dirs, sizeof(double) * 3 * n_scat);
@@ -93,7 +93,8 @@ extern "C" int fvr_render_rays_host(const double origin[3], const double* dirs, 
     const bool same_dirs = !scat || scatter_dirs_match(scat_dirs, n_scat);
     int rc = fvr_render_rays(origin, d_dirs.as<double>(), n_rays, d_vals.as<float>(), n_channels, grid,
                              params, background, d_scat.as<double>(),
-                             same_dirs ? d_layout.as<float>() : nullptr, d_out.as<double>(), nullptr);
+                             same_dirs ? d_layout.as<float>() : nullptr, same_dirs ? d_occ.as<uint8_t>() : nullptr,
+                             d_out.as<double>(), nullptr);
     if (rc) return rc;
     if ((rc = sync_check("render_rays_host"))) return rc;
     d2h(out, d_out.p, sizeof(double) * n_rays * n_channels);

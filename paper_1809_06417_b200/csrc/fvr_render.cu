@@ -90,6 +90,7 @@ template <int NCH, bool SCAT>
 __device__ __forceinline__ void march_render_fast(const double o[3], const double d[3], const Geom& g,
                                                   const float* __restrict__ values, int plane,
                                                   const float4* __restrict__ layout,
+                                                  const uint8_t* __restrict__ occ,
                                                   const RenderConsts& rc, const float* __restrict__ thr,
                                                   const float4* q1, const float4* q2, double out[NCH]) {
     double l[NCH];
@@ -114,10 +115,14 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
                 cell_frac(q[0], g.nx, ix, fx);
                 cell_frac(q[1], g.ny, iy, fy);
                 cell_frac(q[2], g.nz, iz, fz);
+                // empty-space skip: every corner of the cell is zero, so the
+                // sample adds exactly 0 (only the transparency advances)
+                if (!occ || __ldg(occ + ix * g.sx + iy * g.sy + iz)) {
 #pragma unroll
-                for (int c = 0; c < NCH; ++c) {
-                    const float e = tri_yzq(layout + (int64_t)c * plane, g, ix, iy, iz, fx, fy, fz);
-                    l[c] += t_dst * (rc.tau * (rc.sigma_a * (double)e));
+                    for (int c = 0; c < NCH; ++c) {
+                        const float e = tri_yzq(layout + (int64_t)c * plane, g, ix, iy, iz, fx, fy, fz);
+                        l[c] += t_dst * (rc.tau * (rc.sigma_a * (double)e));
+                    }
                 }
             } else {
                 bool interior = true;
@@ -130,8 +135,11 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
                     m[a] = min(max((int)r, 0), a == 0 ? g.nx : (a == 1 ? g.ny : g.nz));
                     dl[a] = (float)(q[a] - (double)m[a]);
                 }
+                // empty-space skip: the whole 3x3x3 neighbourhood is zero, so the
+                // emission read and all 32 gathers are exactly 0
+                const bool live = !occ || __ldg(occ + m[0] * g.sx + m[1] * g.sy + m[2]);
 #pragma unroll 1
-                for (int c = 0; c < NCH; ++c) {
+                for (int c = 0; c < (live ? NCH : 0); ++c) {
                     float v[27];
                     float e = 0.f, acc = 0.f;
                     if (interior) {
@@ -170,6 +178,38 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
     for (int c = 0; c < NCH; ++c) out[c] = l[c] + t_dst * rc.bg[c];
 }
 
+// Occupancy for empty-space skipping: occ[j] = 1 when any key point within
+// Chebyshev distance 1 of j may be non-zero -- i.e. has a positive value in
+// some channel or is flagged by `force` (the hull key points of the loop,
+// whose values change).  A sample whose 3x3x3 neighbourhood (or 2x2x2 cell)
+// is unoccupied reads only zeros and adds exactly 0 to the pixel.
+__global__ void occupancy_kernel(const float* __restrict__ values, int64_t n_kp, int nch,
+                                 const uint8_t* __restrict__ force, int nx, int ny, int nz,
+                                 uint8_t* __restrict__ occ) {
+    const int sy = nz + 1, sx = (ny + 1) * (nz + 1);
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_kp;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(j / sx), y = (int)((j / sy) % (ny + 1)), z = (int)(j % sy);
+        bool any = false;
+        for (int dx = -1; dx <= 1 && !any; ++dx) {
+            const int xx = x + dx;
+            if (xx < 0 || xx > nx) continue;
+            for (int dy = -1; dy <= 1 && !any; ++dy) {
+                const int yy = y + dy;
+                if (yy < 0 || yy > ny) continue;
+                for (int dz = -1; dz <= 1 && !any; ++dz) {
+                    const int zz = z + dz;
+                    if (zz < 0 || zz > nz) continue;
+                    const int64_t k = (int64_t)xx * sx + yy * sy + zz;
+                    if (force && force[k]) any = true;
+                    for (int c = 0; c < nch && !any; ++c) any = values[c * n_kp + k] > 0.f;
+                }
+            }
+        }
+        occ[j] = any ? 1 : 0;
+    }
+}
+
 // Packed layouts of max(v, 0): see fvr_stencil.cuh.
 __global__ void pack_layout_kernel(const float* __restrict__ values, int64_t n_kp, int nch, int kind,
                                    int sy, float4* __restrict__ out) {
@@ -197,13 +237,14 @@ template <int NCH, int MODE>
 __device__ __forceinline__ void march_dispatch(const double o[3], const double d[3], const Geom& g,
                                                const float* __restrict__ values, int plane,
                                                const float4* __restrict__ layout,
+                                               const uint8_t* __restrict__ occ,
                                                const RenderConsts& rc, const double* __restrict__ scat,
                                                const float* __restrict__ thr, double out[NCH]) {
     if (MODE == kModePlain) march_render<NCH, false, true>(o, d, g, values, plane, rc, scat, out);
     if (MODE == kModeScatG0) march_render<NCH, true, true>(o, d, g, values, plane, rc, scat, out);
     if (MODE == kModeScatG) march_render<NCH, true, false>(o, d, g, values, plane, rc, scat, out);
-    if (MODE == kModeFastPlain) march_render_fast<NCH, false>(o, d, g, values, plane, layout, rc, thr, g_q1, g_q2, out);
-    if (MODE == kModeFastScat) march_render_fast<NCH, true>(o, d, g, values, plane, layout, rc, thr, g_q1, g_q2, out);
+    if (MODE == kModeFastPlain) march_render_fast<NCH, false>(o, d, g, values, plane, layout, occ, rc, thr, g_q1, g_q2, out);
+    if (MODE == kModeFastScat) march_render_fast<NCH, true>(o, d, g, values, plane, layout, occ, rc, thr, g_q1, g_q2, out);
 }
 
 // Shared-memory copy of the sorted gather offsets (moment split search).
@@ -220,7 +261,7 @@ __global__ void __launch_bounds__(128) render_rays_kernel(double ox, double oy, 
                                                           int64_t n_rays,
                                                           const float* __restrict__ values,
                                                           int plane, const float4* __restrict__ layout,
-                                                          Geom g, RenderConsts rc,
+                                                          const uint8_t* __restrict__ occ, Geom g, RenderConsts rc,
                                                           const double* __restrict__ scat,
                                                           double* __restrict__ out) {
     __shared__ float s_thr[3 * kScatDirs];
@@ -230,7 +271,7 @@ __global__ void __launch_bounds__(128) render_rays_kernel(double ox, double oy, 
     const double o[3] = {ox, oy, oz};
     const double d[3] = {dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2]};
     double res[NCH];
-    march_dispatch<NCH, MODE>(o, d, g, values, plane, layout, rc, scat, s_thr, res);
+    march_dispatch<NCH, MODE>(o, d, g, values, plane, layout, occ, rc, scat, s_thr, res);
 #pragma unroll
     for (int c = 0; c < NCH; ++c) out[r * NCH + c] = res[c];
 }
@@ -244,7 +285,7 @@ __global__ void __launch_bounds__(128) render_pixels_kernel(fvr_camera_t cam,
                                                             int64_t n,
                                                             const float* __restrict__ values,
                                                             int plane, const float4* __restrict__ layout,
-                                                            Geom g, RenderConsts rc,
+                                                            const uint8_t* __restrict__ occ, Geom g, RenderConsts rc,
                                                             const double* __restrict__ scat,
                                                             double* __restrict__ out) {
     __shared__ float s_thr[3 * kScatDirs];
@@ -262,7 +303,7 @@ __global__ void __launch_bounds__(128) render_pixels_kernel(fvr_camera_t cam,
     double d[3];
     pixel_dir(cam, u, v, d);
     double res[NCH];
-    march_dispatch<NCH, MODE>(cam.center, d, g, values, plane, layout, rc, scat, s_thr, res);
+    march_dispatch<NCH, MODE>(cam.center, d, g, values, plane, layout, occ, rc, scat, s_thr, res);
 #pragma unroll
     for (int c = 0; c < NCH; ++c) out[i * NCH + c] = res[c];
 }
@@ -275,7 +316,8 @@ template <int MODE>
 __global__ void __launch_bounds__(kTileThreads) loop_render_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int tiles_x,
     const float* __restrict__ src, const float* __restrict__ values,
-    const float4* __restrict__ layout, Geom g, RenderConsts rc, const double* __restrict__ scat,
+    const float4* __restrict__ layout, const uint8_t* __restrict__ occ, Geom g, RenderConsts rc,
+    const double* __restrict__ scat,
     float* __restrict__ residual, double* __restrict__ sq_partials,
     const fvr_loop_state_t* __restrict__ state) {
     if (state && state->done) return;
@@ -292,7 +334,7 @@ __global__ void __launch_bounds__(kTileThreads) loop_render_kernel(
         double d[3];
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         double rec[1];
-        march_dispatch<1, MODE>(cam.center, d, g, values, 0, layout, rc, scat, s_thr, rec);
+        march_dispatch<1, MODE>(cam.center, d, g, values, 0, layout, occ, rc, scat, s_thr, rec);
         const int64_t pix = ((int64_t)view * h + row) * w + col;
         const double r = (double)src[pix] - rec[0];
         residual[pix] = (float)r;
@@ -311,7 +353,8 @@ constexpr size_t kScatSmem = sizeof(float4) * (kQ1Vec + kQ2Vec) + sizeof(float) 
 __global__ void __launch_bounds__(kTileThreads, 2) loop_render_scat_kernel(
     const fvr_camera_t* __restrict__ cams, int n_views, int u0, int v0, int w, int h, int tiles_x,
     int tiles_per_view, const float* __restrict__ src, const float* __restrict__ values,
-    const float4* __restrict__ layout, Geom g, RenderConsts rc, float* __restrict__ residual,
+    const float4* __restrict__ layout, const uint8_t* __restrict__ occ, Geom g, RenderConsts rc,
+    float* __restrict__ residual,
     double* __restrict__ sq_partials, const fvr_loop_state_t* __restrict__ state) {
     if (state && state->done) return;
     extern __shared__ float4 smem[];
@@ -335,7 +378,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) loop_render_scat_kernel(
             double d[3];
             pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
             double rec[1];
-            march_render_fast<1, true>(cam.center, d, g, values, 0, layout, rc, s_thr, s_q1, s_q2, rec);
+            march_render_fast<1, true>(cam.center, d, g, values, 0, layout, occ, rc, s_thr, s_q1, s_q2, rec);
             const int64_t pix = ((int64_t)view * h + row) * w + col;
             const double r = (double)src[pix] - rec[0];
             residual[pix] = (float)r;
@@ -383,45 +426,54 @@ int pack(const float* values, int nch, const fvr_grid_t& grid, int kind, float4*
     return check_launch("pack_layout");
 }
 
+int occupancy(const float* values, int nch, const uint8_t* force, const fvr_grid_t& grid, uint8_t* occ,
+              cudaStream_t st) {
+    const int64_t n_kp = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
+    int64_t blocks = (n_kp + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    occupancy_kernel<<<(unsigned)blocks, 256, 0, st>>>(values, n_kp, nch, force, grid.nx, grid.ny, grid.nz, occ);
+    return check_launch("occupancy");
+}
+
 template <int NCH, int MODE>
 void launch_rays(const double origin[3], const double* dirs, int64_t n_rays, const float* values,
-                 int plane, const float4* layout, const Geom& g, const RenderConsts& rc,
+                 int plane, const float4* layout, const uint8_t* occ, const Geom& g, const RenderConsts& rc,
                  const double* scat_dirs, double* out, cudaStream_t st) {
     render_rays_kernel<NCH, MODE><<<(unsigned)((n_rays + 127) / 128), 128, 0, st>>>(
-        origin[0], origin[1], origin[2], dirs, n_rays, values, plane, layout, g, rc, scat_dirs, out);
+        origin[0], origin[1], origin[2], dirs, n_rays, values, plane, layout, occ, g, rc, scat_dirs, out);
 }
 
 template <int NCH>
 void launch_rays_mode(int mode, const double origin[3], const double* dirs, int64_t n_rays,
-                      const float* values, int plane, const float4* layout, const Geom& g,
+                      const float* values, int plane, const float4* layout, const uint8_t* occ, const Geom& g,
                       const RenderConsts& rc, const double* scat_dirs, double* out, cudaStream_t st) {
     switch (mode) {
-        case kModePlain: launch_rays<NCH, kModePlain>(origin, dirs, n_rays, values, plane, layout, g, rc, scat_dirs, out, st); break;
-        case kModeScatG0: launch_rays<NCH, kModeScatG0>(origin, dirs, n_rays, values, plane, layout, g, rc, scat_dirs, out, st); break;
-        case kModeScatG: launch_rays<NCH, kModeScatG>(origin, dirs, n_rays, values, plane, layout, g, rc, scat_dirs, out, st); break;
-        case kModeFastPlain: launch_rays<NCH, kModeFastPlain>(origin, dirs, n_rays, values, plane, layout, g, rc, scat_dirs, out, st); break;
-        default: launch_rays<NCH, kModeFastScat>(origin, dirs, n_rays, values, plane, layout, g, rc, scat_dirs, out, st); break;
+        case kModePlain: launch_rays<NCH, kModePlain>(origin, dirs, n_rays, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
+        case kModeScatG0: launch_rays<NCH, kModeScatG0>(origin, dirs, n_rays, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
+        case kModeScatG: launch_rays<NCH, kModeScatG>(origin, dirs, n_rays, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
+        case kModeFastPlain: launch_rays<NCH, kModeFastPlain>(origin, dirs, n_rays, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
+        default: launch_rays<NCH, kModeFastScat>(origin, dirs, n_rays, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
     }
 }
 
 template <int NCH, int MODE>
 void launch_pix(const fvr_camera_t& cam, const double* us, const double* vs, int64_t n,
-                const float* values, int plane, const float4* layout, const Geom& g,
+                const float* values, int plane, const float4* layout, const uint8_t* occ, const Geom& g,
                 const RenderConsts& rc, const double* scat_dirs, double* out, cudaStream_t st) {
     render_pixels_kernel<NCH, MODE><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
-        cam, us, vs, n, values, plane, layout, g, rc, scat_dirs, out);
+        cam, us, vs, n, values, plane, layout, occ, g, rc, scat_dirs, out);
 }
 
 template <int NCH>
 void launch_pix_mode(int mode, const fvr_camera_t& cam, const double* us, const double* vs, int64_t n,
-                     const float* values, int plane, const float4* layout, const Geom& g,
+                     const float* values, int plane, const float4* layout, const uint8_t* occ, const Geom& g,
                      const RenderConsts& rc, const double* scat_dirs, double* out, cudaStream_t st) {
     switch (mode) {
-        case kModePlain: launch_pix<NCH, kModePlain>(cam, us, vs, n, values, plane, layout, g, rc, scat_dirs, out, st); break;
-        case kModeScatG0: launch_pix<NCH, kModeScatG0>(cam, us, vs, n, values, plane, layout, g, rc, scat_dirs, out, st); break;
-        case kModeScatG: launch_pix<NCH, kModeScatG>(cam, us, vs, n, values, plane, layout, g, rc, scat_dirs, out, st); break;
-        case kModeFastPlain: launch_pix<NCH, kModeFastPlain>(cam, us, vs, n, values, plane, layout, g, rc, scat_dirs, out, st); break;
-        default: launch_pix<NCH, kModeFastScat>(cam, us, vs, n, values, plane, layout, g, rc, scat_dirs, out, st); break;
+        case kModePlain: launch_pix<NCH, kModePlain>(cam, us, vs, n, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
+        case kModeScatG0: launch_pix<NCH, kModeScatG0>(cam, us, vs, n, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
+        case kModeScatG: launch_pix<NCH, kModeScatG>(cam, us, vs, n, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
+        case kModeFastPlain: launch_pix<NCH, kModeFastPlain>(cam, us, vs, n, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
+        default: launch_pix<NCH, kModeFastScat>(cam, us, vs, n, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
     }
 }
 
@@ -545,6 +597,14 @@ extern "C" int fvr_pack_layout(const float* values, int32_t n_channels, fvr_grid
     FVR_TRY_END
 }
 
+extern "C" int fvr_occupancy(const float* values, int32_t n_channels, const uint8_t* force_mask,
+                             fvr_grid_t grid, uint8_t* occ, void* stream) {
+    FVR_TRY_BEGIN
+    if (int rc = check_grid(grid)) return rc;
+    return occupancy(values, n_channels, force_mask, grid, occ, (cudaStream_t)stream);
+    FVR_TRY_END
+}
+
 extern "C" int fvr_render_layout_kind(fvr_render_params_t params, fvr_grid_t grid) {
     bool scat;
     const float4* dummy = reinterpret_cast<const float4*>(16);
@@ -554,7 +614,8 @@ extern "C" int fvr_render_layout_kind(fvr_render_params_t params, fvr_grid_t gri
 extern "C" int fvr_render_rays(const double origin[3], const double* dirs, int64_t n_rays,
                                const float* values, int32_t n_channels, fvr_grid_t grid,
                                fvr_render_params_t params, const double* background,
-                               const double* scat_dirs, float* layout, double* out, void* stream) {
+                               const double* scat_dirs, float* layout, uint8_t* occ, double* out,
+                               void* stream) {
     FVR_TRY_BEGIN
     if (int rc = check_common(n_channels, grid, params, scat_dirs)) return rc;
     if (n_rays == 0) return FVR_OK;
@@ -567,11 +628,14 @@ extern "C" int fvr_render_rays(const double origin[3], const double* dirs, int64
     cudaStream_t st = (cudaStream_t)stream;
     if (layout_kind(mode) != kLayoutNone)
         if (int e = pack(values, n_channels, grid, layout_kind(mode), reinterpret_cast<float4*>(layout), st)) return e;
+    if (layout_kind(mode) == kLayoutNone) occ = nullptr;  // the general path never skips
+    if (occ)
+        if (int e = occupancy(values, n_channels, nullptr, grid, occ, st)) return e;
     switch (n_channels) {
-        case 1: launch_rays_mode<1>(mode, origin, dirs, n_rays, values, plane, lay, g, rc, scat_dirs, out, st); break;
-        case 2: launch_rays_mode<2>(mode, origin, dirs, n_rays, values, plane, lay, g, rc, scat_dirs, out, st); break;
-        case 3: launch_rays_mode<3>(mode, origin, dirs, n_rays, values, plane, lay, g, rc, scat_dirs, out, st); break;
-        default: launch_rays_mode<4>(mode, origin, dirs, n_rays, values, plane, lay, g, rc, scat_dirs, out, st); break;
+        case 1: launch_rays_mode<1>(mode, origin, dirs, n_rays, values, plane, lay, occ, g, rc, scat_dirs, out, st); break;
+        case 2: launch_rays_mode<2>(mode, origin, dirs, n_rays, values, plane, lay, occ, g, rc, scat_dirs, out, st); break;
+        case 3: launch_rays_mode<3>(mode, origin, dirs, n_rays, values, plane, lay, occ, g, rc, scat_dirs, out, st); break;
+        default: launch_rays_mode<4>(mode, origin, dirs, n_rays, values, plane, lay, occ, g, rc, scat_dirs, out, st); break;
     }
     return check_launch("render_rays");
     FVR_TRY_END
@@ -581,7 +645,7 @@ extern "C" int fvr_render_pixels(const fvr_camera_t* camera, const double* us, c
                                  int64_t n, const float* values, int32_t n_channels,
                                  fvr_grid_t grid, fvr_render_params_t params,
                                  const double* background, const double* scat_dirs, float* layout,
-                                 double* out, void* stream) {
+                                 uint8_t* occ, double* out, void* stream) {
     FVR_TRY_BEGIN
     if (!camera) return set_error(FVR_ERR_INVALID, "camera is NULL");
     if (int rc = check_common(n_channels, grid, params, scat_dirs)) return rc;
@@ -597,11 +661,14 @@ extern "C" int fvr_render_pixels(const fvr_camera_t* camera, const double* us, c
     cudaStream_t st = (cudaStream_t)stream;
     if (layout_kind(mode) != kLayoutNone)
         if (int e = pack(values, n_channels, grid, layout_kind(mode), reinterpret_cast<float4*>(layout), st)) return e;
+    if (layout_kind(mode) == kLayoutNone) occ = nullptr;  // the general path never skips
+    if (occ)
+        if (int e = occupancy(values, n_channels, nullptr, grid, occ, st)) return e;
     switch (n_channels) {
-        case 1: launch_pix_mode<1>(mode, *camera, us, vs, n, values, plane, lay, g, rc, scat_dirs, out, st); break;
-        case 2: launch_pix_mode<2>(mode, *camera, us, vs, n, values, plane, lay, g, rc, scat_dirs, out, st); break;
-        case 3: launch_pix_mode<3>(mode, *camera, us, vs, n, values, plane, lay, g, rc, scat_dirs, out, st); break;
-        default: launch_pix_mode<4>(mode, *camera, us, vs, n, values, plane, lay, g, rc, scat_dirs, out, st); break;
+        case 1: launch_pix_mode<1>(mode, *camera, us, vs, n, values, plane, lay, occ, g, rc, scat_dirs, out, st); break;
+        case 2: launch_pix_mode<2>(mode, *camera, us, vs, n, values, plane, lay, occ, g, rc, scat_dirs, out, st); break;
+        case 3: launch_pix_mode<3>(mode, *camera, us, vs, n, values, plane, lay, occ, g, rc, scat_dirs, out, st); break;
+        default: launch_pix_mode<4>(mode, *camera, us, vs, n, values, plane, lay, occ, g, rc, scat_dirs, out, st); break;
     }
     return check_launch("render_pixels");
     FVR_TRY_END
@@ -613,8 +680,8 @@ extern "C" int fvr_loop_blocks_per_view(int32_t bbox_w, int32_t bbox_h) {
 
 extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0,
                                int32_t bbox_w, int32_t bbox_h, const float* src,
-                               const float* values, const float* layout, fvr_grid_t grid,
-                               fvr_render_params_t params, double background,
+                               const float* values, const float* layout, const uint8_t* occ,
+                               fvr_grid_t grid, fvr_render_params_t params, double background,
                                const double* scat_dirs, float* residual, double* sq_partials,
                                const fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
@@ -633,7 +700,7 @@ extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_
     cudaStream_t st = (cudaStream_t)stream;
 #define FVR_LOOP_RENDER(M)                                                                          \
     loop_render_kernel<M><<<gridd, block, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, tiles_x, src, values, \
-                                                   lay, g, rc, scat_dirs, residual, sq_partials, state)
+                                                   lay, occ, g, rc, scat_dirs, residual, sq_partials, state)
     switch (mode) {
         case kModePlain: FVR_LOOP_RENDER(kModePlain); break;
         case kModeScatG0: FVR_LOOP_RENDER(kModeScatG0); break;
@@ -652,7 +719,7 @@ extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_
             const int total = tiles * n_views;
             const int blocks = total < 2 * sms ? total : 2 * sms;
             loop_render_scat_kernel<<<blocks, kTileThreads, kScatSmem, st>>>(
-                cams, n_views, u0, v0, bbox_w, bbox_h, tiles_x, tiles, src, values, lay, g, rc, residual,
+                cams, n_views, u0, v0, bbox_w, bbox_h, tiles_x, tiles, src, values, lay, occ, g, rc, residual,
                 sq_partials, state);
             break;
         }

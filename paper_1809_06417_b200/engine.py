@@ -133,6 +133,15 @@ class ChannelLoop:
             self.layout = t.empty(values.shape + (4,), dtype=t.float32, device=dev)
             _lib.call("fvr_pack_layout", self.values.data_ptr(), 1, self.grid, self.layout_kind,
                       self.layout.data_ptr(), _lib.stream_ptr())
+        # empty-space occupancy: hull key points (their values change) plus any
+        # positive initial value; key points outside the hull are never written,
+        # so the map stays valid for the whole loop
+        self.occ = None
+        if self.layout_kind and os.environ.get("FVR_NO_SKIP") != "1":
+            force = t.from_numpy(np.ascontiguousarray(kp_mask, dtype=np.uint8)).to(dev)
+            self.occ = t.empty(values.shape, dtype=t.uint8, device=dev)
+            _lib.call("fvr_occupancy", self.values.data_ptr(), 1, force.data_ptr(), self.grid,
+                      self.occ.data_ptr(), _lib.stream_ptr())
 
         # work buffers
         self.bpv = int(_lib.load().fvr_loop_blocks_per_view(self.w_bb, self.h_bb))
@@ -171,7 +180,7 @@ class ChannelLoop:
         _lib.call(
             "fvr_loop_render", self.cams.data_ptr(), self.v_end - self.v_begin, self.bbox.u0,
             self.bbox.v0, self.w_bb, self.h_bb, self.src.data_ptr(), self.values.data_ptr(),
-            _lib.ptr(self.layout), self.grid, self.params, self.background, _lib.ptr(self.scat), self.residual.data_ptr(),
+            _lib.ptr(self.layout), _lib.ptr(self.occ), self.grid, self.params, self.background, _lib.ptr(self.scat), self.residual.data_ptr(),
             sq_local.data_ptr(), self.state.data_ptr(), stream,
         )
         return 1

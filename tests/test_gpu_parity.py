@@ -238,3 +238,23 @@ def test_stochastic_seed_determinism_and_grayscale(cuda_device):
                                                                    rng_seed=5), render_cfg=RenderConfig())
     assert np.array_equal(res.grids[0].values, res.grids[1].values)
     assert np.array_equal(res.grids[0].values, res.grids[2].values)
+
+
+def test_empty_space_skipping_is_exact(cuda_device, monkeypatch):
+    """Skipping samples whose neighbourhood is unoccupied changes nothing: the
+    skipped samples add exactly 0 (the transparency still advances)."""
+    g = load_golden("loop_scatter.npz")
+    cams, hull, images, masks, bbox, geom, rcfg = _loop_inputs(g)
+    cfg = ReconstructionConfig(alpha_l=0.006, tau=float(g["tau"]), max_iters=3, converge_eps=1e-12,
+                               deterministic_mode=True)
+    a, ta = reconstruct_channel(images, cams, geom, hull, cfg, render_cfg=rcfg, masks=masks, bbox=bbox)
+    monkeypatch.setenv("FVR_NO_SKIP", "1")
+    b, tb = reconstruct_channel(images, cams, geom, hull, cfg, render_cfg=rcfg, masks=masks, bbox=bbox)
+    assert np.array_equal(a.values, b.values)
+    assert ta.rmse == tb.rmse
+    truth = [VoxelGrid(16, 16, 16, g["origin"], float(g["edge"]), t, g["truth"][i])
+             for i, t in enumerate(("red", "green", "blue"))]
+    img_noskip = render_view(cams[0], truth, None, rcfg)
+    monkeypatch.delenv("FVR_NO_SKIP")
+    img_skip = render_view(cams[0], truth, None, rcfg)
+    assert np.array_equal(img_skip.data, img_noskip.data)
