@@ -65,6 +65,27 @@ def shard_views(n_views: int, rank: int, world: int) -> tuple[int, int]:
     return begin, begin + base + (1 if rank < extra else 0)
 
 
+def exchange(comm, sq, vol, v_begin: int, v_end: int, rows_per_view: int, rank: int, group=None) -> None:
+    """The one collective of an iteration (§8e): all-reduce(sum) of the i64
+    buffer ``comm`` = [packed correction | squared-residual partials (f64 bits)
+    | volume partials (f64 bits)] across the ranks of ``group``.
+
+    Corrections are 32.32 fixed-point integers, so their sum is exact and
+    independent of the partition.  Each f64 partial has exactly one owner
+    (the rank of its view; rank 0 for the replicated volume term): all other
+    ranks contribute the bit pattern of +0.0, i.e. integer 0, so the integer
+    sum reproduces the owner's bits exactly.  ``sq``/``vol`` are f64 views into
+    ``comm``; works on CUDA (NCCL) and CPU (gloo) tensors alike.
+    """
+    import torch.distributed as dist
+
+    sq[: v_begin * rows_per_view].zero_()
+    sq[v_end * rows_per_view:].zero_()
+    if vol is not None and rank != 0:
+        vol.zero_()
+    dist.all_reduce(comm, op=dist.ReduceOp.SUM, group=group)
+
+
 class ChannelLoop:
     """Owns the device buffers of one reconstruct_channel call."""
 
@@ -228,16 +249,10 @@ class ChannelLoop:
 
     def _allreduce(self, stream):
         """Sum corrections and RMSE partials over ranks (exact: int64)."""
-        t = self.t
-        # rows of views other ranks own must contribute exactly zero
-        self.sq[: self.v_begin * self.bpv].zero_()
-        self.sq[self.v_end * self.bpv:].zero_()
-        if self.rank != 0 and self.vol is not None:
-            self.vol.zero_()
         if self.n_kp:
             _lib.call("fvr_pack_correction", self.accum.data_ptr(), self.kp.data_ptr(), self.n_kp,
                       self.packed.data_ptr(), stream)
-        t.distributed.all_reduce(self.comm)
+        exchange(self.comm, self.sq, self.vol, self.v_begin, self.v_end, self.bpv, self.rank)
         if self.n_kp:
             _lib.call("fvr_unpack_correction", self.packed.data_ptr(), self.kp.data_ptr(), self.n_kp,
                       self.accum.data_ptr(), stream)
@@ -290,11 +305,7 @@ class ChannelLoop:
 
     def _allreduce_packed(self, stream):
         """All-reduce [packed | sq | vol] once the gather filled ``packed``."""
-        self.sq[: self.v_begin * self.bpv].zero_()
-        self.sq[self.v_end * self.bpv:].zero_()
-        if self.rank != 0 and self.vol is not None:
-            self.vol.zero_()
-        self.t.distributed.all_reduce(self.comm)
+        exchange(self.comm, self.sq, self.vol, self.v_begin, self.v_end, self.bpv, self.rank)
         return 0
 
     def stages(self):
