@@ -39,6 +39,10 @@ SIGMA_S = 0.1
 SCAT_DIRS = 32
 TAU = 1.0 - 0.95 ** (64.0 / N_VOX)
 ALPHA_L = 0.006
+# dram__bytes_read.sum + dram__bytes_write.sum of loop_render_scat_kernel from one
+# `ncu --set full` capture (profiles/r1_ncu_full_render_gather_raw.csv)
+TRAFFIC_BYTES_PER_LAUNCH = 10_187_008
+TRAFFIC_SOURCE = "profiles/r1_ncu_full_render_gather_raw.csv (round 1)"
 METRIC = "recon iters/sec at 128³×8 views 512²; Gsamples/s; % of HBM roofline"
 WORKLOAD = "config 2: 128^3 flame, 8 views 512x512, full RTE (sigma_s 0.1, 32 dirs), green channel"
 
@@ -117,6 +121,51 @@ def work_counts(sc):
     n_kp = (geom.nx + 1) * (geom.ny + 1) * (geom.nz + 1)
     return dict(S_r=s_r, S_f=s_f, S_a=s_a, R_f=r_f, VP=vp, N_kp=n_kp,
                 hull_kp=int(sc["hull"].key_point_mask().sum()))
+
+
+def live_samples(sc, occ) -> int:
+    """Render samples whose 3x3x3 neighbourhood is occupied (the ones K-render
+    evaluates; the rest add exactly 0 and are skipped), counted on the device
+    with torch in fp64 from the same q = qb + k*d as the kernel."""
+    import torch
+
+    from paper_1809_06417_b200.geometry import pixel_rays
+
+    geom, bbox = sc["geom"], sc["bbox"]
+    dev = occ.device
+    lo = torch.tensor(geom.origin, dtype=torch.float64, device=dev)
+    n = torch.tensor([geom.nx, geom.ny, geom.nz], dtype=torch.float64, device=dev)
+    hi = lo + n * geom.edge
+    occ_flat = occ.reshape(-1)
+    sx, sy = (geom.ny + 1) * (geom.nz + 1), geom.nz + 1
+    us = np.arange(bbox.u0, bbox.u1 + 1) + 0.5
+    vs = np.arange(bbox.v0, bbox.v1 + 1) + 0.5
+    uu, vv = np.meshgrid(us, vs, indexing="xy")
+    live = 0
+    for cam in sc["cams"]:
+        o_np, d_np = pixel_rays(cam, uu.ravel(), vv.ravel())
+        o = torch.tensor(o_np, dtype=torch.float64, device=dev)
+        for chunk in np.array_split(np.arange(d_np.shape[0]), 8):
+            d = torch.tensor(d_np[chunk], dtype=torch.float64, device=dev)
+            with np.errstate(all="ignore"):
+                t0 = (lo - o) / d
+                t1 = (hi - o) / d
+            tmin = torch.where(d == 0, torch.full_like(d, -1e300), torch.minimum(t0, t1)).amax(1)
+            tmax = torch.where(d == 0, torch.full_like(d, 1e300), torch.maximum(t0, t1)).amin(1)
+            te = tmin.clamp(min=0.0)
+            cnt = torch.where(tmax > te, torch.floor((tmax - te) / geom.edge + 1e-9), torch.zeros_like(te)).long()
+            kmax = int(cnt.max().item()) if cnt.numel() else 0
+            if kmax == 0:
+                continue
+            qb = ((o - lo)[None, :] + (te - 0.5 * geom.edge)[:, None] * d) / geom.edge
+            k = torch.arange(1, kmax + 1, dtype=torch.float64, device=dev)
+            q = qb[:, None, :] + k[None, :, None] * d[:, None, :]
+            m = torch.round(q).long()
+            m = torch.minimum(torch.clamp(m, min=0), n.long())
+            idx = m[..., 0] * sx + m[..., 1] * sy + m[..., 2]
+            valid = k[None, :] <= cnt[:, None]
+            live += int((occ_flat[idx.clamp(max=occ_flat.numel() - 1)].bool() & valid).sum().item())
+    return live
 
 
 def algorithmic_bytes(w, scattering=True):
@@ -264,6 +313,8 @@ def run_gpu(args):
     assert st["it"] == args.warmup + args.steps and not st["done"], st
 
     w = work_counts(sc)
+    if loop.occ is not None:
+        w["S_r_live"] = live_samples(sc, loop.occ)
     render_bytes, iter_bytes = algorithmic_bytes(w, scattering=True)
     ms = total_ms / args.steps
     its = 1000.0 / ms
@@ -320,10 +371,17 @@ def run_gpu(args):
         "stage_ms": part_ms,
         "iter_algorithmic_bytes": iter_bytes,
         "iter_roofline_frac": iter_bytes * its / (peak * 1e9),
-        "roofline": {"bound": "hbm", "kernel": "loop_render_kernel<true>", "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+        "roofline": {"bound": "hbm", "kernel": "loop_render_scat_kernel", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": TRAFFIC_BYTES_PER_LAUNCH, "traffic_source": TRAFFIC_SOURCE,
                      "bytes_per_launch": render_bytes,
-                     "bytes_rule": "108 B per render sample (27-key-point stencil, f32) + 8 B per bbox pixel"},
+                     "bytes_rule": "SURVEY 8(d): 108 B per render sample (27-key-point f32 stencil) + 8 B per "
+                                   "bbox pixel; the lattice is L2-resident, so DRAM traffic is ~10 MB/launch"},
+        "roofline_live": None if "S_r_live" not in w else {
+            "bytes_per_launch": 108 * w["S_r_live"] + (w["S_r"] - w["S_r_live"]) + 8 * w["VP"],
+            "achieved": (108 * w["S_r_live"] + (w["S_r"] - w["S_r_live"]) + 8 * w["VP"]) / (render_ms * 1e-3) / 1e9,
+            "frac": (108 * w["S_r_live"] + (w["S_r"] - w["S_r_live"]) + 8 * w["VP"]) / (render_ms * 1e-3) / 1e9 / peak,
+            "rule": "empty-space skipping: 108 B per occupied sample, 1 B (occupancy probe) per skipped sample"},
         "gpu_launches": int(launches),
         "adjust_path": "voxel-driven gather (CSR plan, nnz %d)" % loop.plan_nnz if loop.plan else "ray-driven scatter",
         "clocks": clocks,

@@ -81,6 +81,71 @@ __device__ __forceinline__ bool plan_ray(const fvr_camera_t* __restrict__ cams,
     return true;
 }
 
+// The (key point, W) entries of one ray, with runs merged: consecutive
+// in-hull samples whose cells share corners would emit the same key point
+// again; a straight ray meets the 2x2x2 cell block around a key point in one
+// contiguous run, so carrying the previous sample's 8 corners and summing
+// matches removes most duplicates (about 2-3x fewer plan entries).  Count and
+// fill run the identical merge, so their entry counts agree.
+template <bool WEIGHTS, class Emit>
+__device__ __forceinline__ void ray_entries(const PlanRay& pr, const Geom& g, const uint8_t* __restrict__ inside,
+                                            double tau_keep, double alpha_l, float alpha_d, Emit&& emit) {
+    int pk[8];
+    float pw[8];
+    bool have = false;
+    const float edge = (float)g.edge;
+    visit_inhull(pr.o, pr.d, g, inside, tau_keep, [&](int, const double* q, const int* c, double trans) {
+        int nk[8];
+        float nw[8];
+        const int base_kp = c[0] * g.sx + c[1] * g.sy + c[2];
+        float e[3][2];
+        if (WEIGHTS) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const float f = (float)(q[a] - (double)c[a]);
+                e[a][0] = f * edge;
+                e[a][1] = (f - 1.0f) * edge;
+            }
+        }
+        const float base = WEIGHTS ? (float)(alpha_l * trans) : 0.f;
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8) {
+            const int cx = k8 >> 2, cy = (k8 >> 1) & 1, cz = k8 & 1;
+            nk[k8] = base_kp + cx * g.sx + cy * g.sy + cz;
+            if (WEIGHTS) {
+                const float dist = sqrtf(fmaf(e[0][cx], e[0][cx], fmaf(e[1][cy], e[1][cy], e[2][cz] * e[2][cz])));
+                nw[k8] = base * expf(-alpha_d * dist);
+            } else {
+                nw[k8] = 0.f;
+            }
+        }
+        if (have) {
+            uint32_t carried = 0;
+#pragma unroll
+            for (int n = 0; n < 8; ++n)
+#pragma unroll
+                for (int p = 0; p < 8; ++p)
+                    if (pk[p] == nk[n]) {
+                        if (WEIGHTS) nw[n] += pw[p];
+                        carried |= 1u << p;
+                    }
+#pragma unroll
+            for (int p = 0; p < 8; ++p)
+                if (!((carried >> p) & 1u)) emit(pk[p], pw[p]);
+        }
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8) {
+            pk[k8] = nk[k8];
+            pw[k8] = nw[k8];
+        }
+        have = true;
+    });
+    if (have) {
+#pragma unroll
+        for (int p = 0; p < 8; ++p) emit(pk[p], pw[p]);
+    }
+}
+
 __global__ void __launch_bounds__(128) plan_count_kernel(
     const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
     int u0, int v0, int w, int h, const uint8_t* __restrict__ inside, Geom g,
@@ -89,14 +154,8 @@ __global__ void __launch_bounds__(128) plan_count_kernel(
     if (r >= n_rays) return;
     PlanRay pr;
     plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
-    visit_inhull(pr.o, pr.d, g, inside, 1.0, [&](int, const double*, const int* c, double) {
-        const int base = c[0] * g.sx + c[1] * g.sy + c[2];
-#pragma unroll
-        for (int k8 = 0; k8 < 8; ++k8) {
-            const int kp = base + (k8 >> 2) * g.sx + ((k8 >> 1) & 1) * g.sy + (k8 & 1);
-            atomicAdd(counts + kp_map[kp], 1);
-        }
-    });
+    ray_entries<false>(pr, g, inside, 1.0, 0.0, 0.f,
+                       [&](int kp, float) { atomicAdd(counts + kp_map[kp], 1); });
 }
 
 __global__ void __launch_bounds__(128) plan_fill_kernel(
@@ -108,26 +167,9 @@ __global__ void __launch_bounds__(128) plan_fill_kernel(
     if (r >= n_rays) return;
     PlanRay pr;
     plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
-    const float edge = (float)g.edge;
-    visit_inhull(pr.o, pr.d, g, inside, tau_keep, [&](int, const double* q, const int* c, double trans) {
-        const float base = (float)(alpha_l * trans);
-        float e[3][2];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const float f = (float)(q[a] - (double)c[a]);
-            e[a][0] = f * edge;
-            e[a][1] = (f - 1.0f) * edge;
-        }
-        const int base_kp = c[0] * g.sx + c[1] * g.sy + c[2];
-#pragma unroll
-        for (int k8 = 0; k8 < 8; ++k8) {
-            const int cx = k8 >> 2, cy = (k8 >> 1) & 1, cz = k8 & 1;
-            const float dist = sqrtf(fmaf(e[0][cx], e[0][cx], fmaf(e[1][cy], e[1][cy], e[2][cz] * e[2][cz])));
-            const float wgt = base * expf(-alpha_d * dist);
-            const int kp = base_kp + cx * g.sx + cy * g.sy + cz;
-            const unsigned long long pos = atomicAdd(cursor + kp_map[kp], 1ull);
-            entries[pos] = make_int2(pr.res_index, __float_as_int(wgt));
-        }
+    ray_entries<true>(pr, g, inside, tau_keep, alpha_l, alpha_d, [&](int kp, float wgt) {
+        const unsigned long long pos = atomicAdd(cursor + kp_map[kp], 1ull);
+        entries[pos] = make_int2(pr.res_index, __float_as_int(wgt));
     });
 }
 
@@ -145,10 +187,20 @@ __global__ void __launch_bounds__(256) gather_kernel(
     for (int64_t row = warp; row < n_rows; row += n_warps) {
         const long long b = row_off[row], e = row_off[row + 1];
         long long acc = 0;
-        for (long long i = b + lane; i < e; i += 32) {
-            const int2 en = __ldg(entries + i);
-            const float prod = __ldg(residual + en.x) * __int_as_float(en.y);
-            acc += __float2ll_rn(prod * 4294967296.0f);
+        // four independent streaming loads in flight per lane (the plan is
+        // read once per iteration: evict-first, keep L2 for the residual)
+        for (long long base = b; base < e; base += 128) {
+            int2 en[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const long long i = base + lane + 32 * u;
+                en[u] = i < e ? __ldcs(entries + i) : make_int2(0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float prod = __ldg(residual + en[u].x) * __int_as_float(en[u].y);
+                acc += __float2ll_rn(prod * 4294967296.0f);
+            }
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
