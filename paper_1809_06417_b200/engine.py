@@ -189,7 +189,13 @@ class ChannelLoop:
         self.plan_nnz = 0
         if self.plan:
             self._build_plan()
-        self.use_graph = use_graph and self.world == 1 and os.environ.get("FVR_NO_GRAPH") != "1"
+        # A CUDA graph only pays off when an iteration is launch-bound (a few
+        # tens of microseconds of device work); for larger problems the host
+        # enqueues 3-4 launches (~30 us) far ahead of the device, and graph
+        # instantiation costs milliseconds per call.
+        small = V * self.w_bb * self.h_bb <= 65536
+        self.use_graph = (use_graph and small and self.world == 1
+                          and os.environ.get("FVR_NO_GRAPH") != "1") or os.environ.get("FVR_GRAPH") == "1"
         self.graph = None
         self.launches_per_iter = 0
 
@@ -348,13 +354,18 @@ class ChannelLoop:
 
     def capture(self) -> None:
         """Capture one iteration into a CUDA graph (single-GPU only)."""
+        # capture_begin/end directly: the torch.cuda.graph context manager also
+        # runs gc.collect() and empty_cache(), which cost 2-300 ms per call
         t = self.t
         g = t.cuda.CUDAGraph()
         side = t.cuda.Stream()
         side.wait_stream(t.cuda.current_stream())
         with t.cuda.stream(side):
-            with t.cuda.graph(g, stream=side):
+            g.capture_begin(capture_error_mode="thread_local")
+            try:
                 self.launch_iteration()
+            finally:
+                g.capture_end()
         t.cuda.current_stream().wait_stream(side)
         self.graph = g
 
