@@ -160,6 +160,9 @@ __device__ __forceinline__ uint32_t inbox_mask(const double p[3], const Geom& g,
 // is tabulated once per direction set: Q1 (3 x 33 x 8), Q2 (3 x 33^2 x 8),
 // Q3 (33^3 x 8).  Exact in real arithmetic (checked against the brute-force
 // sum to 1e-15 in fp64); ~400 instructions per sample instead of ~1400.
+#ifndef FVR_Q3_TABLE
+#define FVR_Q3_TABLE 1
+#endif
 constexpr int kSplits = kScatDirs + 1;
 __constant__ float c_thr[3][kScatDirs];  // sorted c_{s,a} = s_a / 2 per axis
 __constant__ float c_q0[8];              // Q_{empty}[E]
@@ -252,17 +255,26 @@ __device__ __forceinline__ void moment_eval(const float v[27], float dx, float d
     load_q8(q2, (0 * kSplits + ix) * kSplits + iy, Q[6]);
     load_q8(q2, (1 * kSplits + ix) * kSplits + iz, Q[5]);
     load_q8(q2, (2 * kSplits + iy) * kSplits + iz, Q[3]);
+    // delta' monomials D[m] = prod_{a in m} delta'_a
+    float D[8];
+    D[0] = 1.f; D[4] = hx; D[2] = hy; D[1] = hz;
+    D[6] = hx * hy; D[5] = hx * hz; D[3] = hy * hz; D[7] = D[6] * hz;
     float m222 = 0.f;
+#if FVR_Q3_TABLE
+    {
+        float q3[8];
+        load_q8(g_q3, (ix * kSplits + iy) * kSplits + iz, q3);
+#pragma unroll
+        for (int E = 0; E < 8; ++E) m222 = fmaf(D[7 ^ E], q3[E], m222);
+    }
+#else
 #pragma unroll
     for (int d = 0; d < kScatDirs; ++d) {
         const float p = (dx + c_half_dir[0][d]) * (dy + c_half_dir[1][d]) * (dz + c_half_dir[2][d]);
         m222 += fabsf(p);
     }
     m222 *= 0.125f;
-    // delta' monomials D[m] = prod_{a in m} delta'_a
-    float D[8];
-    D[0] = 1.f; D[4] = hx; D[2] = hy; D[1] = hz;
-    D[6] = hx * hy; D[5] = hx * hz; D[3] = hy * hz; D[7] = D[6] * hz;
+#endif
     float s = 0.f;
 #pragma unroll
     for (int kx = 0; kx < 3; ++kx)
