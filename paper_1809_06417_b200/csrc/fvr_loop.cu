@@ -33,11 +33,14 @@ __global__ void finalize_kernel(const double* __restrict__ sq, int n_views, int 
                                 double* __restrict__ trace_vol, fvr_loop_state_t* __restrict__ st) {
     if (st->done) return;
     __shared__ double view_rmse[32];
-    const int v = threadIdx.x;
+    // warp v reduces view v: lane-strided partial sums, then a fixed shuffle tree
+    const int v = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (v < n_views) {
         double s = 0.0;
-        for (int b = 0; b < bpv; ++b) s += sq[(int64_t)v * bpv + b];
-        view_rmse[v] = sqrt(s / pixels);
+        for (int b = lane; b < bpv; b += 32) s += sq[(int64_t)v * bpv + b];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) view_rmse[v] = sqrt(s / pixels);
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
@@ -87,7 +90,7 @@ extern "C" int fvr_loop_finalize(const double* sq_partials, int32_t n_views, int
     FVR_TRY_BEGIN
     if (n_views < 1 || n_views > 32) return set_error(FVR_ERR_INVALID, "n_views must be in 1..32");
     if (pixels_per_view < 1) return set_error(FVR_ERR_INVALID, "empty bounding box");
-    finalize_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(
+    finalize_kernel<<<1, 32 * n_views, 0, (cudaStream_t)stream>>>(
         sq_partials, n_views, blocks_per_view, (double)pixels_per_view, vol_partials, n_vol_blocks,
         (double)n_kp, converge_eps, trace_rmse, trace_vol, state);
     return check_launch("loop_finalize");

@@ -310,52 +310,79 @@ __global__ void __launch_bounds__(128) render_pixels_kernel(fvr_camera_t cam,
 
 // ---- loop render: every bbox pixel of every view + residual + RMSE partials
 
-constexpr int kTileW = 16, kTileH = 16, kTileThreads = kTileW * kTileH;
+// Work unit = one warp = an 8x4 patch of bbox pixels of one view.  Each warp
+// reduces its 32 squared residuals itself (fixed shuffle tree) and writes one
+// f64 partial per unit, so no CTA-wide barrier ever makes a warp wait for the
+// longest ray of its neighbours.
+constexpr int kUnitW = 8, kUnitH = 4, kBlockThreads = 256, kWarpsPerBlock = kBlockThreads / 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
 
 template <int MODE>
-__global__ void __launch_bounds__(kTileThreads) loop_render_kernel(
-    const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int tiles_x,
-    const float* __restrict__ src, const float* __restrict__ values,
-    const float4* __restrict__ layout, const uint8_t* __restrict__ occ, Geom g, RenderConsts rc,
-    const double* __restrict__ scat,
-    float* __restrict__ residual, double* __restrict__ sq_partials,
-    const fvr_loop_state_t* __restrict__ state) {
-    if (state && state->done) return;
-    __shared__ double red[kTileThreads / 32];
-    __shared__ float s_thr[3 * kScatDirs];
-    if (MODE == kModeFastScat) load_thresholds(s_thr);
-    const int view = blockIdx.y;
-    const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
-    const int col = tx * kTileW + (threadIdx.x % kTileW);
-    const int row = ty * kTileH + (threadIdx.x / kTileW);
+__device__ __forceinline__ void render_unit(int unit, int units_x, int units_per_view,
+                                            const fvr_camera_t* __restrict__ cams, int u0, int v0, int w,
+                                            int h, const float* __restrict__ src,
+                                            const float* __restrict__ values, const float4* __restrict__ layout,
+                                            const uint8_t* __restrict__ occ, const Geom& g,
+                                            const RenderConsts& rc, const double* __restrict__ scat,
+                                            const float* thr, const float4* q1, const float4* q2,
+                                            float* __restrict__ residual, double* __restrict__ sq_partials) {
+    const int lane = threadIdx.x & 31;
+    const int view = unit / units_per_view, u = unit - view * units_per_view;
+    const int ux = u % units_x, uy = u / units_x;
+    const int col = ux * kUnitW + (lane % kUnitW);
+    const int row = uy * kUnitH + (lane / kUnitW);
     double sq = 0.0;
     if (col < w && row < h) {
         const fvr_camera_t& cam = cams[view];
         double d[3];
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         double rec[1];
-        march_dispatch<1, MODE>(cam.center, d, g, values, 0, layout, occ, rc, scat, s_thr, rec);
+        if (MODE == kModeFastScat)
+            march_render_fast<1, true>(cam.center, d, g, values, 0, layout, occ, rc, thr, q1, q2, rec);
+        else
+            march_dispatch<1, MODE>(cam.center, d, g, values, 0, layout, occ, rc, scat, thr, rec);
         const int64_t pix = ((int64_t)view * h + row) * w + col;
         const double r = (double)src[pix] - rec[0];
         residual[pix] = (float)r;
         sq = r * r;
     }
-    const double total = block_sum<kTileThreads>(sq, red);
-    if (threadIdx.x == 0) sq_partials[(int64_t)view * gridDim.x + blockIdx.x] = total;
+    const double tot = warp_sum(sq);
+    if (lane == 0) sq_partials[unit] = tot;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kBlockThreads) loop_render_kernel(
+    const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
+    int n_units, const float* __restrict__ src, const float* __restrict__ values,
+    const float4* __restrict__ layout, const uint8_t* __restrict__ occ, Geom g, RenderConsts rc,
+    const double* __restrict__ scat, float* __restrict__ residual, double* __restrict__ sq_partials,
+    const fvr_loop_state_t* __restrict__ state) {
+    if (state && state->done) return;
+    __shared__ float s_thr[3 * kScatDirs];
+    if (MODE == kModeFastScat) load_thresholds(s_thr);
+    const int unit = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (unit >= n_units) return;
+    render_unit<MODE == kModeFastScat ? kModeScatG0 : MODE>(unit, units_x, units_per_view, cams, u0, v0, w, h,
+                                                            src, values, layout, occ, g, rc, scat, s_thr, g_q1,
+                                                            g_q2, residual, sq_partials);
 }
 
 // Persistent variant for the single-scattering fast path: two CTAs per SM,
 // each stages the Q1/Q2 moment tables (107 KB) and the split thresholds in
-// shared memory once and then walks the (view, tile) list.
+// shared memory once; every warp then walks the unit list on its own.
 constexpr int kQ1Vec = 3 * kSplits * 2, kQ2Vec = 3 * kSplits * kSplits * 2;
 constexpr size_t kScatSmem = sizeof(float4) * (kQ1Vec + kQ2Vec) + sizeof(float) * 3 * kScatDirs;
 
-__global__ void __launch_bounds__(kTileThreads, 2) loop_render_scat_kernel(
-    const fvr_camera_t* __restrict__ cams, int n_views, int u0, int v0, int w, int h, int tiles_x,
-    int tiles_per_view, const float* __restrict__ src, const float* __restrict__ values,
+__global__ void __launch_bounds__(kBlockThreads, 2) loop_render_scat_kernel(
+    const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
+    int n_units, const float* __restrict__ src, const float* __restrict__ values,
     const float4* __restrict__ layout, const uint8_t* __restrict__ occ, Geom g, RenderConsts rc,
-    float* __restrict__ residual,
-    double* __restrict__ sq_partials, const fvr_loop_state_t* __restrict__ state) {
+    float* __restrict__ residual, double* __restrict__ sq_partials, const fvr_loop_state_t* __restrict__ state) {
     if (state && state->done) return;
     extern __shared__ float4 smem[];
     float4* s_q1 = smem;
@@ -365,29 +392,10 @@ __global__ void __launch_bounds__(kTileThreads, 2) loop_render_scat_kernel(
     for (int i = threadIdx.x; i < kQ2Vec; i += blockDim.x) s_q2[i] = g_q2[i];
     for (int i = threadIdx.x; i < 3 * kScatDirs; i += blockDim.x) s_thr[i] = (&c_thr[0][0])[i];
     __syncthreads();
-    __shared__ double red[kTileThreads / 32];
-    const int total = n_views * tiles_per_view;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int view = t / tiles_per_view, tile = t - view * tiles_per_view;
-        const int tx = tile % tiles_x, ty = tile / tiles_x;
-        const int col = tx * kTileW + (threadIdx.x % kTileW);
-        const int row = ty * kTileH + (threadIdx.x / kTileW);
-        double sq = 0.0;
-        if (col < w && row < h) {
-            const fvr_camera_t& cam = cams[view];
-            double d[3];
-            pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
-            double rec[1];
-            march_render_fast<1, true>(cam.center, d, g, values, 0, layout, occ, rc, s_thr, s_q1, s_q2, rec);
-            const int64_t pix = ((int64_t)view * h + row) * w + col;
-            const double r = (double)src[pix] - rec[0];
-            residual[pix] = (float)r;
-            sq = r * r;
-        }
-        const double tot = block_sum<kTileThreads>(sq, red);
-        if (threadIdx.x == 0) sq_partials[t] = tot;
-        __syncthreads();  // red[] is reused by the next tile
-    }
+    const int stride = gridDim.x * kWarpsPerBlock;
+    for (int unit = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); unit < n_units; unit += stride)
+        render_unit<kModeFastScat>(unit, units_x, units_per_view, cams, u0, v0, w, h, src, values, layout, occ, g,
+                                   rc, nullptr, s_thr, s_q1, s_q2, residual, sq_partials);
 }
 
 }  // namespace fvr
@@ -675,7 +683,7 @@ extern "C" int fvr_render_pixels(const fvr_camera_t* camera, const double* us, c
 }
 
 extern "C" int fvr_loop_blocks_per_view(int32_t bbox_w, int32_t bbox_h) {
-    return ((bbox_w + kTileW - 1) / kTileW) * ((bbox_h + kTileH - 1) / kTileH);
+    return ((bbox_w + kUnitW - 1) / kUnitW) * ((bbox_h + kUnitH - 1) / kUnitH);
 }
 
 extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0,
@@ -694,13 +702,15 @@ extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_
     if (mode == kModeScatG) return set_error(FVR_ERR_INVALID, "the reconstruction loop renders with g = 0 (render.py:196)");
     const Geom g = make_geom(grid);
     const RenderConsts rc = make_render_consts(params, &background, 1);
-    const int tiles_x = (bbox_w + kTileW - 1) / kTileW;
-    const int tiles = fvr_loop_blocks_per_view(bbox_w, bbox_h);
-    const dim3 gridd((unsigned)tiles, (unsigned)n_views), block(kTileThreads);
+    const int units_x = (bbox_w + kUnitW - 1) / kUnitW;
+    const int upv = fvr_loop_blocks_per_view(bbox_w, bbox_h);
+    const int n_units = upv * n_views;
     cudaStream_t st = (cudaStream_t)stream;
-#define FVR_LOOP_RENDER(M)                                                                          \
-    loop_render_kernel<M><<<gridd, block, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, tiles_x, src, values, \
-                                                   lay, occ, g, rc, scat_dirs, residual, sq_partials, state)
+    const unsigned blocks = (unsigned)((n_units + kWarpsPerBlock - 1) / kWarpsPerBlock);
+#define FVR_LOOP_RENDER(M)                                                                              \
+    loop_render_kernel<M><<<blocks, kBlockThreads, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, \
+                                                            n_units, src, values, lay, occ, g, rc,        \
+                                                            scat_dirs, residual, sq_partials, state)
     switch (mode) {
         case kModePlain: FVR_LOOP_RENDER(kModePlain); break;
         case kModeScatG0: FVR_LOOP_RENDER(kModeScatG0); break;
@@ -716,10 +726,9 @@ extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_
             int dev = 0, sms = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            const int total = tiles * n_views;
-            const int blocks = total < 2 * sms ? total : 2 * sms;
-            loop_render_scat_kernel<<<blocks, kTileThreads, kScatSmem, st>>>(
-                cams, n_views, u0, v0, bbox_w, bbox_h, tiles_x, tiles, src, values, lay, occ, g, rc, residual,
+            const int pblocks = (int)blocks < 2 * sms ? (int)blocks : 2 * sms;
+            loop_render_scat_kernel<<<pblocks, kBlockThreads, kScatSmem, st>>>(
+                cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, src, values, lay, occ, g, rc, residual,
                 sq_partials, state);
             break;
         }

@@ -161,7 +161,7 @@ __device__ __forceinline__ uint32_t inbox_mask(const double p[3], const Geom& g,
 // Q3 (33^3 x 8).  Exact in real arithmetic (checked against the brute-force
 // sum to 1e-15 in fp64); ~400 instructions per sample instead of ~1400.
 #ifndef FVR_Q3_TABLE
-#define FVR_Q3_TABLE 1
+#define FVR_Q3_TABLE 0
 #endif
 constexpr int kSplits = kScatDirs + 1;
 __constant__ float c_thr[3][kScatDirs];  // sorted c_{s,a} = s_a / 2 per axis
