@@ -105,29 +105,20 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
 #pragma unroll
         for (int a = 0; a < 3; ++a) qb[a] = ((o[a] - g.lo[a]) + t0 * d[a]) * g.inv_edge;
         const double nmax[3] = {(double)g.nx, (double)g.ny, (double)g.nz};
-        for (int k = 1; k <= n; ++k) {
+        int k = 1;
+        while (k <= n) {
             double q[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) q[a] = fma((double)k, d[a], qb[a]);
+            int m[3];
+            float dl[3];
+            bool interior = true;
             if (!SCAT) {
-                int ix, iy, iz;
-                float fx, fy, fz;
-                cell_frac(q[0], g.nx, ix, fx);
-                cell_frac(q[1], g.ny, iy, fy);
-                cell_frac(q[2], g.nz, iz, fz);
-                // empty-space skip: every corner of the cell is zero, so the
-                // sample adds exactly 0 (only the transparency advances)
-                if (!occ || __ldg(occ + ix * g.sx + iy * g.sy + iz)) {
-#pragma unroll
-                    for (int c = 0; c < NCH; ++c) {
-                        const float e = tri_yzq(layout + (int64_t)c * plane, g, ix, iy, iz, fx, fy, fz);
-                        l[c] += t_dst * (rc.tau * (rc.sigma_a * (double)e));
-                    }
-                }
+                // cell of the trilinear read (the 2x2x2 corners are within distance 1 of it)
+                cell_frac(q[0], g.nx, m[0], dl[0]);
+                cell_frac(q[1], g.ny, m[1], dl[1]);
+                cell_frac(q[2], g.nz, m[2], dl[2]);
             } else {
-                bool interior = true;
-                int m[3];
-                float dl[3];
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
                     interior = interior && q[a] >= 0.5 + 1e-7 && q[a] <= nmax[a] - 0.5 - 1e-7;
@@ -135,78 +126,116 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
                     m[a] = min(max((int)r, 0), a == 0 ? g.nx : (a == 1 ? g.ny : g.nz));
                     dl[a] = (float)(q[a] - (double)m[a]);
                 }
-                // empty-space skip: the whole 3x3x3 neighbourhood is zero, so the
-                // emission read and all 32 gathers are exactly 0
-                const bool live = !occ || __ldg(occ + m[0] * g.sx + m[1] * g.sy + m[2]);
-#pragma unroll 1
-                for (int c = 0; c < (live ? NCH : 0); ++c) {
-                    float v[27];
-                    float e = 0.f, acc = 0.f;
-                    if (interior) {
-                        load_stencil_z4(layout + (int64_t)c * plane, g, m[0], m[1], m[2], v);
-                        moment_eval(v, dl[0], dl[1], dl[2], thr, q1, q2, e, acc);
-                        // both are sums of non-negative terms in exact arithmetic;
-                        // the expanded form can round a vanishing sum below zero
-                        e = fmaxf(e, 0.f);
-                        acc = fmaxf(acc, 0.f);
-                    } else {
-                        // within half a voxel of a box face: the reference's
-                        // exact per-direction in-box test masks the gathers;
-                        // an all-zero neighbourhood contributes nothing at all
-                        load_stencil_clamped(values + (int64_t)c * plane, g, m[0], m[1], m[2], v);
-                        bool any = false;
-#pragma unroll
-                        for (int j = 0; j < 27; ++j) any = any || v[j] != 0.f;
-                        if (any) {
-                            double p[3];
-                            sample_pos(o, d, te, g.edge, k, p);
-                            const uint32_t mask = inbox_mask(p, g, rc.half_gather);
-                            Stencil st;
-                            stencil_from(v, st);
-                            e = stencil_tri(st, dl[0], dl[1], dl[2]);
-                            acc = stencil_scatter<true>(st, dl[0], dl[1], dl[2], mask);
-                        }
-                    }
-                    const double l_src = rc.sigma_a * (double)e + (double)acc * rc.scat_scale;
-                    l[c] += t_dst * (rc.tau * l_src);
-                }
             }
-            t_dst *= rc.one_minus_tau;
+            // Empty-space skipping.  dist[j] is a lower bound on the Chebyshev
+            // distance from key point j to the nearest key point that may be
+            // non-zero.  dist <= 1: the sample's neighbourhood may be live.
+            // Otherwise samples k .. k+s-1 read only zeros and add exactly 0,
+            // s = max(1, dist-2) (sample k+j stays within j+1 of m, its
+            // neighbourhood within j+2).  The skip is the minimum over the
+            // warp so the lanes stay aligned on k; the transparency still
+            // advances by repeated multiplication, as in the reference.
+            const int D = occ ? (int)__ldg(occ + m[0] * g.sx + m[1] * g.sy + m[2]) : 0;
+            const unsigned act = __activemask();
+            if (__any_sync(act, D <= 1)) {
+                if (D <= 1) {
+#pragma unroll 1
+                    for (int c = 0; c < NCH; ++c) {
+                        float e = 0.f, acc = 0.f;
+                        if (!SCAT) {
+                            e = tri_yzq(layout + (int64_t)c * plane, g, m[0], m[1], m[2], dl[0], dl[1], dl[2]);
+                        } else if (interior) {
+                            float v[27];
+                            load_stencil_z4(layout + (int64_t)c * plane, g, m[0], m[1], m[2], v);
+                            moment_eval(v, dl[0], dl[1], dl[2], thr, q1, q2, e, acc);
+                            // sums of non-negative terms in exact arithmetic; the
+                            // expanded form can round a vanishing sum below zero
+                            e = fmaxf(e, 0.f);
+                            acc = fmaxf(acc, 0.f);
+                        } else {
+                            // within half a voxel of a box face: the reference's exact
+                            // per-direction in-box test masks the gathers
+                            float v[27];
+                            load_stencil_clamped(values + (int64_t)c * plane, g, m[0], m[1], m[2], v);
+                            bool any = false;
+#pragma unroll
+                            for (int j = 0; j < 27; ++j) any = any || v[j] != 0.f;
+                            if (any) {
+                                double p[3];
+                                sample_pos(o, d, te, g.edge, k, p);
+                                const uint32_t mask = inbox_mask(p, g, rc.half_gather);
+                                Stencil st;
+                                stencil_from(v, st);
+                                e = stencil_tri(st, dl[0], dl[1], dl[2]);
+                                acc = stencil_scatter<true>(st, dl[0], dl[1], dl[2], mask);
+                            }
+                        }
+                        const double l_src = SCAT ? rc.sigma_a * (double)e + (double)acc * rc.scat_scale
+                                                  : rc.sigma_a * (double)e;
+                        l[c] += t_dst * (rc.tau * l_src);
+                    }
+                }
+                t_dst *= rc.one_minus_tau;
+                ++k;
+            } else {
+                int s = D - 2 > 1 ? D - 2 : 1;
+                s = (int)__reduce_min_sync(act, (unsigned)s);
+                s = min(s, n - k + 1);
+                for (int j = 0; j < s; ++j) t_dst *= rc.one_minus_tau;
+                k += s;
+            }
         }
     }
 #pragma unroll
     for (int c = 0; c < NCH; ++c) out[c] = l[c] + t_dst * rc.bg[c];
 }
 
-// Occupancy for empty-space skipping: occ[j] = 1 when any key point within
-// Chebyshev distance 1 of j may be non-zero -- i.e. has a positive value in
-// some channel or is flagged by `force` (the hull key points of the loop,
-// whose values change).  A sample whose 3x3x3 neighbourhood (or 2x2x2 cell)
-// is unoccupied reads only zeros and adds exactly 0 to the pixel.
-__global__ void occupancy_kernel(const float* __restrict__ values, int64_t n_kp, int nch,
-                                 const uint8_t* __restrict__ force, int nx, int ny, int nz,
-                                 uint8_t* __restrict__ occ) {
-    const int sy = nz + 1, sx = (ny + 1) * (nz + 1);
+// Empty-space distance map.  M[j] = 1 when key point j may be non-zero: it
+// is positive in some channel, or flagged by `force` (the hull key points of
+// the loop, whose values change).  dist[j] = min(L-inf distance from j to the
+// nearest M = 1 key point, kDistCap + 1), computed separably (z, y, x passes):
+// f_z = 1-D distance along z; g = min_dy max(|dy|, f_z); D = min_dx max(|dx|, g).
+// Windows are limited to +-kDistCap, which keeps every value a lower bound on
+// the true distance -- what the skip in march_render_fast needs.
+constexpr int kDistCap = 30;
+
+__global__ void dist_z_kernel(const float* __restrict__ values, int64_t n_kp, int nch,
+                              const uint8_t* __restrict__ force, int nx, int ny, int nz,
+                              uint8_t* __restrict__ out) {
+    const int64_t n_lines = (int64_t)(nx + 1) * (ny + 1);
+    for (int64_t line = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; line < n_lines;
+         line += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t base = line * (nz + 1);
+        int last = -1000000;
+        for (int z = 0; z <= nz; ++z) {  // forward: distance to the nearest M=1 at or below z
+            const int64_t j = base + z;
+            bool m = force && force[j];
+            for (int c = 0; c < nch && !m; ++c) m = values[c * n_kp + j] > 0.f;
+            if (m) last = z;
+            out[j] = (uint8_t)min(z - last, kDistCap + 1);
+        }
+        last = 1000000;
+        for (int z = nz; z >= 0; --z) {  // backward: combine with the nearest above
+            const int64_t j = base + z;
+            if (out[j] == 0) last = z;
+            const int dz = min(last - z, kDistCap + 1);
+            if (dz < out[j]) out[j] = (uint8_t)dz;
+        }
+    }
+}
+
+// one separable pass along an axis with stride `st` and extent `len`
+__global__ void dist_pass_kernel(const uint8_t* __restrict__ in, int64_t n_kp, int st, int len, int period,
+                                 uint8_t* __restrict__ out) {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_kp;
          j += (int64_t)gridDim.x * blockDim.x) {
-        const int x = (int)(j / sx), y = (int)((j / sy) % (ny + 1)), z = (int)(j % sy);
-        bool any = false;
-        for (int dx = -1; dx <= 1 && !any; ++dx) {
-            const int xx = x + dx;
-            if (xx < 0 || xx > nx) continue;
-            for (int dy = -1; dy <= 1 && !any; ++dy) {
-                const int yy = y + dy;
-                if (yy < 0 || yy > ny) continue;
-                for (int dz = -1; dz <= 1 && !any; ++dz) {
-                    const int zz = z + dz;
-                    if (zz < 0 || zz > nz) continue;
-                    const int64_t k = (int64_t)xx * sx + yy * sy + zz;
-                    if (force && force[k]) any = true;
-                    for (int c = 0; c < nch && !any; ++c) any = values[c * n_kp + k] > 0.f;
-                }
-            }
+        const int pos = (int)((j / st) % period);
+        int best = in[j];
+        for (int dd = 1; dd <= kDistCap && dd < best; ++dd) {
+            if (pos - dd >= 0) best = min(best, max(dd, (int)in[j - (int64_t)dd * st]));
+            if (pos + dd < len) best = min(best, max(dd, (int)in[j + (int64_t)dd * st]));
         }
-        occ[j] = any ? 1 : 0;
+        out[j] = (uint8_t)best;
     }
 }
 
@@ -437,10 +466,17 @@ int pack(const float* values, int nch, const fvr_grid_t& grid, int kind, float4*
 int occupancy(const float* values, int nch, const uint8_t* force, const fvr_grid_t& grid, uint8_t* occ,
               cudaStream_t st) {
     const int64_t n_kp = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
-    int64_t blocks = (n_kp + 255) / 256;
-    if (blocks > 148 * 32) blocks = 148 * 32;
-    occupancy_kernel<<<(unsigned)blocks, 256, 0, st>>>(values, n_kp, nch, force, grid.nx, grid.ny, grid.nz, occ);
-    return check_launch("occupancy");
+    const int64_t n_lines = (int64_t)(grid.nx + 1) * (grid.ny + 1);
+    uint8_t* tmp = nullptr;
+    if (cudaMallocAsync(&tmp, (size_t)n_kp, st) != cudaSuccess) return set_error(FVR_ERR_CUDA, "cudaMallocAsync failed");
+    auto blocks = [](int64_t n) { int64_t b = (n + 255) / 256; return (unsigned)(b > 148 * 32 ? 148 * 32 : b); };
+    const int sy = grid.nz + 1, sx = (grid.ny + 1) * (grid.nz + 1);
+    dist_z_kernel<<<blocks(n_lines), 256, 0, st>>>(values, n_kp, nch, force, grid.nx, grid.ny, grid.nz, occ);
+    dist_pass_kernel<<<blocks(n_kp), 256, 0, st>>>(occ, n_kp, sy, grid.ny + 1, grid.ny + 1, tmp);
+    dist_pass_kernel<<<blocks(n_kp), 256, 0, st>>>(tmp, n_kp, sx, grid.nx + 1, grid.nx + 1, occ);
+    count_launch(2);
+    cudaFreeAsync(tmp, st);
+    return check_launch("occupancy_distance");
 }
 
 template <int NCH, int MODE>
