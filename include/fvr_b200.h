@@ -141,6 +141,14 @@ int fvr_render_pixels(const fvr_camera_t* camera, const double* us, const double
                       fvr_render_params_t params, const double* background,
                       const double* scat_dirs, float* layout, uint8_t* occ, double* out, void* stream);
 
+/* Every pixel centre of n_views same-size cameras (cams: device array) in one
+ * launch; out (n_views, height, width, n_channels) f32.  layout / occ must
+ * have been prepared with fvr_pack_layout / fvr_occupancy (or be NULL). */
+int fvr_render_views(const fvr_camera_t* cams, int32_t n_views, int32_t width, int32_t height,
+                     const float* values, int32_t n_channels, fvr_grid_t grid,
+                     fvr_render_params_t params, const double* background, const double* scat_dirs,
+                     const float* layout, const uint8_t* occ, float* out, void* stream);
+
 /* Packed copies of max(v, 0) read by the fast render paths: kind 1 (YZQ,
  * emission only) or 2 (Z4, single scattering); 0 = none applies.  The Z4
  * path needs the 32 Fibonacci directions loaded once per process with

@@ -97,6 +97,8 @@ _SIGNATURES = {
         [_P, _P, _P, c_int64, _P, c_int32, _GRID, _PARAMS, _P, _P, _P, _P, _P, _P],
     ),
     "fvr_occupancy": (c_int, [_P, c_int32, _P, _GRID, _P, _P]),
+    "fvr_render_views": (
+        c_int, [_P, c_int32, c_int32, c_int32, _P, c_int32, _GRID, _PARAMS, _P, _P, _P, _P, _P, _P]),
     "fvr_set_scatter_dirs": (c_int, [_P, c_int32]),
     "fvr_render_layout_kind": (c_int, [_PARAMS, _GRID]),
     "fvr_pack_layout": (c_int, [_P, c_int32, _GRID, c_int32, _P, _P]),

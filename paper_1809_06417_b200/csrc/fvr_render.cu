@@ -337,6 +337,34 @@ __global__ void __launch_bounds__(128) render_pixels_kernel(fvr_camera_t cam,
     for (int c = 0; c < NCH; ++c) out[i * NCH + c] = res[c];
 }
 
+// ---- render_views: every pixel of several same-size views, one launch ------
+
+template <int NCH, int MODE>
+__global__ void __launch_bounds__(128) render_views_kernel(const fvr_camera_t* __restrict__ cams, int width,
+                                                           int height, const float* __restrict__ values,
+                                                           int plane, const float4* __restrict__ layout,
+                                                           const uint8_t* __restrict__ occ, Geom g,
+                                                           RenderConsts rc, const double* __restrict__ scat,
+                                                           float* __restrict__ out) {
+    __shared__ float s_thr[3 * kScatDirs];
+    if (MODE == kModeFastScat) load_thresholds(s_thr);
+    const int view = blockIdx.y;
+    // 8x4 pixel patches per warp for ray coherence
+    const int lane = threadIdx.x & 31;
+    const int unit = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int units_x = (width + 7) / 8;
+    const int col = (unit % units_x) * 8 + (lane & 7), row = (unit / units_x) * 4 + (lane >> 3);
+    if (col >= width || row >= height) return;
+    const fvr_camera_t& cam = cams[view];
+    double d[3];
+    pixel_dir(cam, (double)col + 0.5, (double)row + 0.5, d);
+    double res[NCH];
+    march_dispatch<NCH, MODE>(cam.center, d, g, values, plane, layout, occ, rc, scat, s_thr, res);
+    float* o = out + (((int64_t)view * height + row) * width + col) * NCH;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) o[c] = (float)res[c];
+}
+
 // ---- loop render: every bbox pixel of every view + residual + RMSE partials
 
 // Work unit = one warp = an 8x4 patch of bbox pixels of one view.  Each warp
@@ -518,6 +546,29 @@ void launch_pix_mode(int mode, const fvr_camera_t& cam, const double* us, const 
         case kModeScatG: launch_pix<NCH, kModeScatG>(cam, us, vs, n, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
         case kModeFastPlain: launch_pix<NCH, kModeFastPlain>(cam, us, vs, n, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
         default: launch_pix<NCH, kModeFastScat>(cam, us, vs, n, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
+    }
+}
+
+template <int NCH, int MODE>
+void launch_views(const fvr_camera_t* cams, int n_views, int width, int height, const float* values, int plane,
+                  const float4* layout, const uint8_t* occ, const Geom& g, const RenderConsts& rc,
+                  const double* scat_dirs, float* out, cudaStream_t st) {
+    const int units = ((width + 7) / 8) * ((height + 3) / 4);
+    const dim3 grid((unsigned)((units + 3) / 4), (unsigned)n_views);
+    render_views_kernel<NCH, MODE><<<grid, 128, 0, st>>>(cams, width, height, values, plane, layout, occ, g, rc,
+                                                         scat_dirs, out);
+}
+
+template <int NCH>
+void launch_views_mode(int mode, const fvr_camera_t* cams, int n_views, int width, int height,
+                       const float* values, int plane, const float4* layout, const uint8_t* occ, const Geom& g,
+                       const RenderConsts& rc, const double* scat_dirs, float* out, cudaStream_t st) {
+    switch (mode) {
+        case kModePlain: launch_views<NCH, kModePlain>(cams, n_views, width, height, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
+        case kModeScatG0: launch_views<NCH, kModeScatG0>(cams, n_views, width, height, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
+        case kModeScatG: launch_views<NCH, kModeScatG>(cams, n_views, width, height, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
+        case kModeFastPlain: launch_views<NCH, kModeFastPlain>(cams, n_views, width, height, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
+        default: launch_views<NCH, kModeFastScat>(cams, n_views, width, height, values, plane, layout, occ, g, rc, scat_dirs, out, st); break;
     }
 }
 
@@ -715,6 +766,33 @@ extern "C" int fvr_render_pixels(const fvr_camera_t* camera, const double* us, c
         default: launch_pix_mode<4>(mode, *camera, us, vs, n, values, plane, lay, occ, g, rc, scat_dirs, out, st); break;
     }
     return check_launch("render_pixels");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_render_views(const fvr_camera_t* cams, int32_t n_views, int32_t width, int32_t height,
+                                const float* values, int32_t n_channels, fvr_grid_t grid,
+                                fvr_render_params_t params, const double* background,
+                                const double* scat_dirs, const float* layout, const uint8_t* occ, float* out,
+                                void* stream) {
+    FVR_TRY_BEGIN
+    if (!cams || n_views < 1 || n_views > 65535) return set_error(FVR_ERR_INVALID, "bad camera array");
+    if (width < 1 || height < 1) return set_error(FVR_ERR_INVALID, "empty frame");
+    if (int rc = check_common(n_channels, grid, params, scat_dirs)) return rc;
+    bool scat;
+    const float4* lay = reinterpret_cast<const float4*>(layout);
+    const int mode = effective_mode(params, grid, lay, scat);
+    if (layout_kind(mode) == kLayoutNone) occ = nullptr;
+    const Geom g = make_geom(grid);
+    const RenderConsts rc = make_render_consts(params, background, n_channels);
+    const int plane = (grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (n_channels) {
+        case 1: launch_views_mode<1>(mode, cams, n_views, width, height, values, plane, lay, occ, g, rc, scat_dirs, out, st); break;
+        case 2: launch_views_mode<2>(mode, cams, n_views, width, height, values, plane, lay, occ, g, rc, scat_dirs, out, st); break;
+        case 3: launch_views_mode<3>(mode, cams, n_views, width, height, values, plane, lay, occ, g, rc, scat_dirs, out, st); break;
+        default: launch_views_mode<4>(mode, cams, n_views, width, height, values, plane, lay, occ, g, rc, scat_dirs, out, st); break;
+    }
+    return check_launch("render_views");
     FVR_TRY_END
 }
 
