@@ -49,13 +49,16 @@ class LoopConfig:
 
 
 def _world():
-    """(rank, world_size, group) when torch.distributed is initialised."""
+    """(rank, world_size, sharded): sharded when torch.distributed is
+    initialised with more than one rank (or FVR_FORCE_SHARDED=1, which runs the
+    exchange path on a 1-rank group -- used to test it on one GPU)."""
     if os.environ.get("FVR_NO_SHARDING") == "1":
-        return 0, 1
+        return 0, 1, False
     t = _lib.torch()
     if t.distributed.is_available() and t.distributed.is_initialized():
-        return t.distributed.get_rank(), t.distributed.get_world_size()
-    return 0, 1
+        rank, world = t.distributed.get_rank(), t.distributed.get_world_size()
+        return rank, world, world > 1 or os.environ.get("FVR_FORCE_SHARDED") == "1"
+    return 0, 1, False
 
 
 def shard_views(n_views: int, rank: int, world: int) -> tuple[int, int]:
@@ -95,7 +98,7 @@ class ChannelLoop:
         t = _lib.torch()
         self.t = t
         self.dev = _lib.device()
-        self.rank, self.world = _world()
+        self.rank, self.world, self.sharded = _world()
         V = len(cameras)
         self.n_views = V
         self.v_begin, self.v_end = shard_views(V, self.rank, self.world)
@@ -194,7 +197,7 @@ class ChannelLoop:
         # enqueues 3-4 launches (~30 us) far ahead of the device, and graph
         # instantiation costs milliseconds per call.
         small = V * self.w_bb * self.h_bb <= 65536
-        self.use_graph = (use_graph and small and self.world == 1
+        self.use_graph = (use_graph and small and not self.sharded
                           and os.environ.get("FVR_NO_GRAPH") != "1") or os.environ.get("FVR_GRAPH") == "1"
         self.graph = None
         self.launches_per_iter = 0
@@ -319,7 +322,7 @@ class ChannelLoop:
         name 'decision' marks where the convergence rule has been evaluated."""
         s = [("render", self._render), ("volume", self._volume)]
         if self.plan:
-            if self.world > 1:
+            if self.sharded:
                 s += [("adjust", lambda st: self._gather(st, True)), ("allreduce", self._allreduce_packed),
                       ("finalize", self._finalize), ("decision", None), ("update", self._update_packed)]
             else:
@@ -327,7 +330,7 @@ class ChannelLoop:
                       ("adjust", lambda st: self._gather(st, False))]
         else:
             s += [("adjust", self._adjust)]
-            if self.world > 1:
+            if self.sharded:
                 s += [("allreduce", self._allreduce)]
             s += [("finalize", self._finalize), ("decision", None), ("update", self._update)]
         return s

@@ -1,0 +1,147 @@
+"""Loop features on the device: the NCCL exchange path (1-rank group, forced),
+per-iteration callbacks, ground-truth volume RMSE, temperature snapshots,
+the max-iters quirk and the convergence rule."""
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_1809_06417_b200 import (
+    Camera,
+    HullTags,
+    Image,
+    ReconstructionConfig,
+    RenderConfig,
+    VoxelGrid,
+    build_color_temp_map,
+    reconstruct_channel,
+    reconstruct_temperature,
+    rmse_volume,
+)
+from paper_1809_06417_b200.preprocess import FlameMask, Rect
+from tests.conftest import cameras_from, load_golden, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _inputs(name="loop_scatter.npz"):
+    g = load_golden(name)
+    cams = cameras_from(g, Camera)
+    n = int(g["n"])
+    hull = HullTags(g["hull_tags"], len(cams))
+    images = [Image(im.shape[1], im.shape[0], 1, im[:, :, 1:2]) for im in g["blanked"]]
+    masks = [FlameMask(m.shape[1], m.shape[0], m) for m in g["masks"]]
+    u0, v0, u1, v1 = (int(x) for x in g["bbox"])
+    geom = VoxelGrid(n, n, n, g["origin"], float(g["edge"]))
+    rcfg = RenderConfig(tau=float(g["tau"]), scattering_enabled=bool(g["scattering"]), sigma_s=float(g["sigma_s"]))
+    return g, cams, hull, images, masks, Rect(u0, v0, u1, v1), geom, rcfg
+
+
+@pytest.fixture
+def nccl_group(cuda_device):
+    import torch.distributed as dist
+
+    if dist.is_initialized():
+        dist.destroy_process_group()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        os.environ["MASTER_PORT"] = str(s.getsockname()[1])
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    yield
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("stochastic", [False, True])
+def test_exchange_path_matches_single_gpu(nccl_group, monkeypatch, stochastic):
+    """The sharded stages (gather -> packed -> NCCL all-reduce -> finalize ->
+    update_packed; scatter -> pack -> all-reduce -> unpack -> update) give the
+    bit-identical grid and trace of the single-GPU stages."""
+    g, cams, hull, images, masks, bbox, geom, rcfg = _inputs()
+    kw = dict(alpha_l=0.006, tau=float(g["tau"]), max_iters=4, converge_eps=1e-12)
+    cfg = ReconstructionConfig(g_sigma=0.1, rng_seed=3, **kw) if stochastic else \
+        ReconstructionConfig(deterministic_mode=True, **kw)
+    monkeypatch.setenv("FVR_NO_SHARDING", "1")
+    a, ta = reconstruct_channel(images, cams, geom, hull, cfg, render_cfg=rcfg, masks=masks, bbox=bbox)
+    monkeypatch.delenv("FVR_NO_SHARDING")
+    monkeypatch.setenv("FVR_FORCE_SHARDED", "1")
+    b, tb = reconstruct_channel(images, cams, geom, hull, cfg, render_cfg=rcfg, masks=masks, bbox=bbox)
+    assert np.array_equal(a.values, b.values)
+    assert ta.rmse == tb.rmse
+
+
+def test_callback_and_ground_truth_trace(cuda_device):
+    g, cams, hull, images, masks, bbox, geom, rcfg = _inputs()
+    truth = VoxelGrid(geom.nx, geom.ny, geom.nz, geom.origin, geom.edge, "green", g["truth"][1])
+    cfg = ReconstructionConfig(alpha_l=0.006, tau=float(g["tau"]), max_iters=4, converge_eps=1e-12,
+                               deterministic_mode=True)
+    seen = []
+
+    def cb(it, grid, rmse):
+        seen.append((it, rmse, rmse_volume(grid, truth, hull)))
+
+    grid, trace = reconstruct_channel(images, cams, geom, hull, cfg, render_cfg=rcfg, masks=masks, bbox=bbox,
+                                      ground_truth=truth, callback=cb)
+    plain, ptrace = reconstruct_channel(images, cams, geom, hull, cfg, render_cfg=rcfg, masks=masks, bbox=bbox)
+    assert [s[0] for s in seen] == [1, 2, 3, 4]
+    assert [s[1] for s in seen] == trace.rmse == ptrace.rmse
+    # device vol_rmse (pre-update grid of each iteration) matches the host metric
+    np.testing.assert_allclose(trace.vol_rmse, [s[2] for s in seen], rtol=1e-9)
+    assert np.array_equal(grid.values, plain.values)
+    np.testing.assert_allclose(trace.rmse, g["rmse"][:4], rtol=1e-6)
+
+
+def test_max_iters_quirk_and_convergence(cuda_device):
+    """max_iters ends the loop after the last adjustment (the returned grid is
+    one adjustment past the last RMSE); a large eps converges at iteration 2
+    and returns the grid that produced the last RMSE."""
+    g, cams, hull, images, masks, bbox, geom, rcfg = _inputs()
+    base = dict(alpha_l=0.006, tau=float(g["tau"]), deterministic_mode=True)
+    one, t1 = reconstruct_channel(images, cams, geom, hull, ReconstructionConfig(max_iters=1, converge_eps=1e-12,
+                                                                                  **base),
+                                  render_cfg=rcfg, masks=masks, bbox=bbox)
+    two, t2 = reconstruct_channel(images, cams, geom, hull, ReconstructionConfig(max_iters=2, converge_eps=1e-12,
+                                                                                  **base),
+                                  render_cfg=rcfg, masks=masks, bbox=bbox)
+    assert t1.iterations == 1 and not t1.converged
+    assert np.any(one.values != np.where(hull.key_point_mask(), 0.0, -1.0))  # adjusted once
+    conv, tc = reconstruct_channel(images, cams, geom, hull,
+                                   ReconstructionConfig(max_iters=50, converge_eps=1e3, **base),
+                                   render_cfg=rcfg, masks=masks, bbox=bbox)
+    # rmse < eps fires at iteration 1: no adjustment at all
+    assert tc.converged and tc.iterations == 1
+    assert np.array_equal(conv.values, np.where(hull.key_point_mask(), np.float32(0.0), np.float32(-1.0)))
+    d = abs(t2.rmse[1] - t2.rmse[0])
+    conv2, tc2 = reconstruct_channel(images, cams, geom, hull,
+                                     ReconstructionConfig(max_iters=50, converge_eps=d * 1.0001, **base),
+                                     render_cfg=rcfg, masks=masks, bbox=bbox)
+    # |rmse_2 - rmse_1| < eps fires at iteration 2: the grid is the one after one adjustment
+    assert tc2.converged and tc2.iterations == 2
+    assert np.array_equal(conv2.values, one.values)
+
+
+def test_temperature_with_snapshots(cuda_device):
+    g, cams, hull, images, masks, bbox, geom, rcfg = _inputs("config1.npz")
+    rgb_imgs = [Image(im.shape[1], im.shape[0], 3, im) for im in g["images"]]
+    cmap = build_color_temp_map()
+    cfg = ReconstructionConfig(alpha_l=0.006, tau=0.05, max_iters=3, converge_eps=1e-12, deterministic_mode=True)
+    snaps = []
+    res = reconstruct_temperature(rgb_imgs, cams, cmap, geom, cfg, render_cfg=RenderConfig(),
+                                  snapshot_callback=lambda it, tg, rgb: snaps.append((it, tg, rgb)))
+    assert [s[0] for s in snaps] == [1, 2, 3]
+    kp = res.hull.key_point_mask()
+    assert np.all(res.temp_grid.values[~kp] == -1.0)
+    inside = res.temp_grid.values[kp]
+    assert inside.min() >= cmap.t_min and inside.max() <= cmap.t_max
+    assert res.n_clamped_low + res.n_clamped_high <= kp.sum()
+    # the reference's inversion of the final green grid (np.interp)
+    greens = res.green_grid.values[kp].astype(np.float64)
+    ref = np.interp(np.clip(greens, cmap.green[0], cmap.green[-1]), cmap.green, cmap.temperatures)
+    assert np.array_equal(inside, ref.astype(np.float32))
+    assert res.n_clamped_low == int(np.sum(greens < cmap.green[0]))
+    assert res.n_clamped_high == int(np.sum(greens > cmap.green[-1]))
+    assert len(snaps[-1][2]) == 3 and snaps[-1][2][1].channel_tag == "green"
+    assert rel_err(res.green_grid.values, res.green_grid.values) == 0.0
