@@ -124,7 +124,7 @@ def work_counts(sc):
 
 
 def live_samples(sc, occ) -> int:
-    """Render samples whose 3x3x3 neighbourhood is occupied (the ones K-render
+    """Render samples whose 3x3x3 neighbourhood may be non-zero (distance map <= 1; the ones K-render
     evaluates; the rest add exactly 0 and are skipped), counted on the device
     with torch in fp64 from the same q = qb + k*d as the kernel."""
     import torch
@@ -164,7 +164,7 @@ def live_samples(sc, occ) -> int:
             m = torch.minimum(torch.clamp(m, min=0), n.long())
             idx = m[..., 0] * sx + m[..., 1] * sy + m[..., 2]
             valid = k[None, :] <= cnt[:, None]
-            live += int((occ_flat[idx.clamp(max=occ_flat.numel() - 1)].bool() & valid).sum().item())
+            live += int(((occ_flat[idx.clamp(max=occ_flat.numel() - 1)] <= 1) & valid).sum().item())
     return live
 
 

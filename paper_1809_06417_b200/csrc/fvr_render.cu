@@ -199,28 +199,13 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
 // the true distance -- what the skip in march_render_fast needs.
 constexpr int kDistCap = 30;
 
-__global__ void dist_z_kernel(const float* __restrict__ values, int64_t n_kp, int nch,
-                              const uint8_t* __restrict__ force, int nx, int ny, int nz,
-                              uint8_t* __restrict__ out) {
-    const int64_t n_lines = (int64_t)(nx + 1) * (ny + 1);
-    for (int64_t line = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; line < n_lines;
-         line += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t base = line * (nz + 1);
-        int last = -1000000;
-        for (int z = 0; z <= nz; ++z) {  // forward: distance to the nearest M=1 at or below z
-            const int64_t j = base + z;
-            bool m = force && force[j];
-            for (int c = 0; c < nch && !m; ++c) m = values[c * n_kp + j] > 0.f;
-            if (m) last = z;
-            out[j] = (uint8_t)min(z - last, kDistCap + 1);
-        }
-        last = 1000000;
-        for (int z = nz; z >= 0; --z) {  // backward: combine with the nearest above
-            const int64_t j = base + z;
-            if (out[j] == 0) last = z;
-            const int dz = min(last - z, kDistCap + 1);
-            if (dz < out[j]) out[j] = (uint8_t)dz;
-        }
+__global__ void dist_seed_kernel(const float* __restrict__ values, int64_t n_kp, int nch,
+                                 const uint8_t* __restrict__ force, uint8_t* __restrict__ out) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_kp;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        bool m = force && force[j];
+        for (int c = 0; c < nch && !m; ++c) m = values[c * n_kp + j] > 0.f;
+        out[j] = m ? 0 : (uint8_t)(kDistCap + 1);
     }
 }
 
@@ -494,16 +479,23 @@ int pack(const float* values, int nch, const fvr_grid_t& grid, int kind, float4*
 int occupancy(const float* values, int nch, const uint8_t* force, const fvr_grid_t& grid, uint8_t* occ,
               cudaStream_t st) {
     const int64_t n_kp = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
-    const int64_t n_lines = (int64_t)(grid.nx + 1) * (grid.ny + 1);
-    uint8_t* tmp = nullptr;
-    if (cudaMallocAsync(&tmp, (size_t)n_kp, st) != cudaSuccess) return set_error(FVR_ERR_CUDA, "cudaMallocAsync failed");
+    // ping-pong scratch, grown on demand and kept for the process
+    static uint8_t* scratch = nullptr;
+    static int64_t scratch_size = 0;
+    if (scratch_size < n_kp) {
+        if (scratch) cudaFree(scratch);
+        scratch = nullptr;
+        scratch_size = 0;
+        if (cudaMalloc(&scratch, (size_t)n_kp) != cudaSuccess) return set_error(FVR_ERR_CUDA, "cudaMalloc failed");
+        scratch_size = n_kp;
+    }
     auto blocks = [](int64_t n) { int64_t b = (n + 255) / 256; return (unsigned)(b > 148 * 32 ? 148 * 32 : b); };
     const int sy = grid.nz + 1, sx = (grid.ny + 1) * (grid.nz + 1);
-    dist_z_kernel<<<blocks(n_lines), 256, 0, st>>>(values, n_kp, nch, force, grid.nx, grid.ny, grid.nz, occ);
-    dist_pass_kernel<<<blocks(n_kp), 256, 0, st>>>(occ, n_kp, sy, grid.ny + 1, grid.ny + 1, tmp);
-    dist_pass_kernel<<<blocks(n_kp), 256, 0, st>>>(tmp, n_kp, sx, grid.nx + 1, grid.nx + 1, occ);
-    count_launch(2);
-    cudaFreeAsync(tmp, st);
+    dist_seed_kernel<<<blocks(n_kp), 256, 0, st>>>(values, n_kp, nch, force, scratch);
+    dist_pass_kernel<<<blocks(n_kp), 256, 0, st>>>(scratch, n_kp, 1, grid.nz + 1, grid.nz + 1, occ);
+    dist_pass_kernel<<<blocks(n_kp), 256, 0, st>>>(occ, n_kp, sy, grid.ny + 1, grid.ny + 1, scratch);
+    dist_pass_kernel<<<blocks(n_kp), 256, 0, st>>>(scratch, n_kp, sx, grid.nx + 1, grid.nx + 1, occ);
+    count_launch(3);
     return check_launch("occupancy_distance");
 }
 
