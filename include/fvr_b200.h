@@ -262,6 +262,20 @@ int fvr_temp_lookup(const float* values, const int32_t* kp_index, int64_t n,
 int fvr_temp_from_green(const double* g, int64_t n, const double* green, const double* temps,
                         int32_t n_lut, double* temp_out, uint8_t* clamped_out, void* stream);
 
+/* ---- input preparation (preprocess.py:59-93, §8f rank 2) ---------------- */
+
+/* images (n_views, height, width, channels) f32 device.  bits (n_views,
+ * height, width) u8 = max over channels > threshold (compared in f32, as
+ * numpy does); blanked (same shape as images, may be NULL) = where(bits,
+ * images, 0); bbox4 (u0, v0, u1, v1) i32 device, initialised by the caller to
+ * (INT_MAX, INT_MAX, -1, -1), receives the tight union box of the set pixels
+ * (u1 < 0: no flame pixel). */
+int fvr_threshold_mask(const float* images, int32_t n_views, int32_t width, int32_t height,
+                       int32_t channels, double threshold, uint8_t* bits, float* blanked,
+                       int32_t* bbox4, void* stream);
+/* (height+1, width+1) i64 summed-area table of one view's mask (device). */
+int fvr_mask_sat(const uint8_t* bits, int32_t width, int32_t height, int64_t* sat, void* stream);
+
 /* ---- visual hull (volume.py:272-328) ----------------------------------- */
 
 /* OR bit `view_bit` into tags (nx,ny,nz) u32 for every voxel whose projected

@@ -112,8 +112,12 @@ class ChannelLoop:
 
         # geometry and inputs
         self.cams = _lib.cameras_tensor([cameras[v] for v in local], dev) if local else None
-        self.src = t.from_numpy(np.ascontiguousarray(np.stack([src_blocks[v] for v in local]) if local
-                                                     else np.zeros((1, 1, 1), np.float32))).to(dev)
+        if t.is_tensor(src_blocks):  # (V, h, w) f32 device crops (DeviceFrames)
+            self.src = src_blocks[self.v_begin:self.v_end].contiguous() if local else \
+                t.zeros((1, 1, 1), dtype=t.float32, device=dev)
+        else:
+            self.src = t.from_numpy(np.ascontiguousarray(np.stack([src_blocks[v] for v in local]) if local
+                                                         else np.zeros((1, 1, 1), np.float32))).to(dev)
         self.values = t.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(dev)
         self.accum = t.zeros(values.shape, dtype=t.int64, device=dev)
         self.inside = t.from_numpy(np.ascontiguousarray(inside, dtype=np.uint8)).to(dev)
@@ -122,20 +126,29 @@ class ChannelLoop:
         self.kp = t.from_numpy(kp_idx if kp_idx.size else np.zeros(1, np.int32)).to(dev)
 
         # flame rays of the local views, row-major per view (reconstruct.py:144-149)
-        entries = []
-        ray_base = 0
-        for v in range(V):
-            sub = masks[v].bits[bbox.slices]
-            rows, cols = np.nonzero(sub)
-            if v < self.v_begin:
-                ray_base += rows.size
-            elif v < self.v_end:
-                lv = v - self.v_begin
-                entries.append((np.int64(lv) << 24) | (rows.astype(np.int64) * self.w_bb + cols))
-        ray_list = np.concatenate(entries).astype(np.int32) if entries else np.zeros(0, np.int32)
-        self.n_rays = int(ray_list.size)
+        if t.is_tensor(masks):  # (V, H, W) u8 device masks: compact on the device
+            sub = masks[:, bbox.v0:bbox.v1 + 1, bbox.u0:bbox.u1 + 1]
+            per_view = sub.reshape(V, -1).sum(1).cpu().tolist()
+            ray_base = int(sum(per_view[: self.v_begin]))
+            nz = t.nonzero(sub[self.v_begin:self.v_end])  # (N, 3): view, row, col -- lexicographic
+            ray_list_t = ((nz[:, 0] << 24) | (nz[:, 1] * self.w_bb + nz[:, 2])).to(t.int32)
+            self.n_rays = int(ray_list_t.numel())
+            self.rays = ray_list_t if self.n_rays else t.zeros(1, dtype=t.int32, device=dev)
+        else:
+            entries = []
+            ray_base = 0
+            for v in range(V):
+                sub = masks[v].bits[bbox.slices]
+                rows, cols = np.nonzero(sub)
+                if v < self.v_begin:
+                    ray_base += rows.size
+                elif v < self.v_end:
+                    lv = v - self.v_begin
+                    entries.append((np.int64(lv) << 24) | (rows.astype(np.int64) * self.w_bb + cols))
+            ray_list = np.concatenate(entries).astype(np.int32) if entries else np.zeros(0, np.int32)
+            self.n_rays = int(ray_list.size)
+            self.rays = t.from_numpy(ray_list if ray_list.size else np.zeros(1, np.int32)).to(dev)
         self.ray_base = ray_base
-        self.rays = t.from_numpy(ray_list if ray_list.size else np.zeros(1, np.int32)).to(dev)
 
         # render configuration of the loop (render_pixels without a phase: g = 0)
         self.scattering = bool(render_cfg.scattering_enabled and render_cfg.sigma_s > 0.0)
