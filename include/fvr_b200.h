@@ -286,6 +286,13 @@ int fvr_visual_hull_view(const fvr_camera_t* camera, const double translation[3]
                          fvr_grid_t grid, const int64_t* sat, int32_t view_bit, uint32_t* tags,
                          void* stream);
 
+/* Key points adjacent to >= 1 inside voxel (volume.py:139-165 key_point_mask,
+ * core_erosion = 0): inside (nx, ny, nz) u8 -> kp_mask (nx+1, ny+1, nz+1) u8.
+ * When values is non-NULL it also receives the loop's initial lattice
+ * (0 at those key points, the outside-hull sentinel -1 elsewhere;
+ * reconstruct.py _init_grid). */
+int fvr_hull_keypoints(const uint8_t* inside, fvr_grid_t grid, uint8_t* kp_mask, float* values, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

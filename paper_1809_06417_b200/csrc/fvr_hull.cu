@@ -78,6 +78,32 @@ __global__ void hull_view_kernel(fvr_camera_t cam, double tx, double ty, double 
     }
 }
 
+// Key points adjacent to >= 1 inside voxel (volume.py:139-165,
+// key_point_mask with core_erosion = 0) and, optionally, the loop's initial
+// lattice: 0 at those key points, the outside-hull sentinel elsewhere
+// (reconstruct.py _init_grid).  One thread per key point reads its <= 8
+// neighbouring voxels.
+__global__ void hull_keypoints_kernel(const uint8_t* __restrict__ inside, int nx, int ny, int nz,
+                                      uint8_t* __restrict__ kp_mask, float* __restrict__ values) {
+    const int64_t n_kp = (int64_t)(nx + 1) * (ny + 1) * (nz + 1);
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_kp;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int iz = (int)(k % (nz + 1));
+        const int iy = (int)((k / (nz + 1)) % (ny + 1));
+        const int ix = (int)(k / ((int64_t)(ny + 1) * (nz + 1)));
+        bool hit = false;
+        for (int x = max(ix - 1, 0); x <= min(ix, nx - 1) && !hit; ++x)
+            for (int y = max(iy - 1, 0); y <= min(iy, ny - 1) && !hit; ++y)
+                for (int z = max(iz - 1, 0); z <= min(iz, nz - 1); ++z)
+                    if (inside[((int64_t)x * ny + y) * nz + z]) {
+                        hit = true;
+                        break;
+                    }
+        kp_mask[k] = hit ? 1 : 0;
+        if (values) values[k] = hit ? 0.f : -1.f;
+    }
+}
+
 }  // namespace fvr
 
 using namespace fvr;
@@ -97,5 +123,19 @@ extern "C" int fvr_visual_hull_view(const fvr_camera_t* camera, const double tra
         *camera, translation[0], translation[1], translation[2], g,
         reinterpret_cast<const long long*>(sat), 1u << view_bit, tags);
     return check_launch("visual_hull_view");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_hull_keypoints(const uint8_t* inside, fvr_grid_t grid, uint8_t* kp_mask, float* values,
+                                  void* stream) {
+    FVR_TRY_BEGIN
+    if (int rc = check_grid(grid)) return rc;
+    if (!inside || !kp_mask) return set_error(FVR_ERR_INVALID, "inside / kp_mask is NULL");
+    const int64_t n_kp = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
+    int64_t blocks = (n_kp + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    hull_keypoints_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(inside, grid.nx, grid.ny, grid.nz,
+                                                                           kp_mask, values);
+    return check_launch("hull_keypoints");
     FVR_TRY_END
 }

@@ -118,12 +118,28 @@ class ChannelLoop:
         else:
             self.src = t.from_numpy(np.ascontiguousarray(np.stack([src_blocks[v] for v in local]) if local
                                                          else np.zeros((1, 1, 1), np.float32))).to(dev)
-        self.values = t.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(dev)
-        self.accum = t.zeros(values.shape, dtype=t.int64, device=dev)
+        shape = (grid_geom.nx + 1, grid_geom.ny + 1, grid_geom.nz + 1)
         self.inside = t.from_numpy(np.ascontiguousarray(inside, dtype=np.uint8)).to(dev)
-        kp_idx = np.flatnonzero(kp_mask.ravel()).astype(np.int32)
-        self.n_kp = int(kp_idx.size)
-        self.kp = t.from_numpy(kp_idx if kp_idx.size else np.zeros(1, np.int32)).to(dev)
+        if kp_mask is None or values is None:
+            # hull key points (and the initial lattice when values is None)
+            # derived on the device from the inside voxels
+            kp_dev = t.empty(shape, dtype=t.uint8, device=dev)
+            self.values = t.empty(shape, dtype=t.float32, device=dev) if values is None else \
+                t.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(dev)
+            _lib.call("fvr_hull_keypoints", self.inside.data_ptr(), self.grid, kp_dev.data_ptr(),
+                      self.values.data_ptr() if values is None else None, _lib.stream_ptr())
+            if kp_mask is not None:
+                kp_dev = t.from_numpy(np.ascontiguousarray(kp_mask, dtype=np.uint8)).to(dev)
+            kp_t = t.nonzero(kp_dev.reshape(-1)).reshape(-1).to(t.int32)
+            self.n_kp = int(kp_t.numel())
+            self.kp = kp_t if self.n_kp else t.zeros(1, dtype=t.int32, device=dev)
+        else:
+            self.values = t.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(dev)
+            kp_dev = t.from_numpy(np.ascontiguousarray(kp_mask, dtype=np.uint8)).to(dev)
+            kp_idx = np.flatnonzero(kp_mask.ravel()).astype(np.int32)
+            self.n_kp = int(kp_idx.size)
+            self.kp = t.from_numpy(kp_idx if kp_idx.size else np.zeros(1, np.int32)).to(dev)
+        self.accum = t.zeros(shape, dtype=t.int64, device=dev)
 
         # flame rays of the local views, row-major per view (reconstruct.py:144-149)
         if t.is_tensor(masks):  # (V, H, W) u8 device masks: compact on the device
@@ -167,7 +183,7 @@ class ChannelLoop:
         self.layout_kind = _lib.layout_kind(self.params, self.grid)
         self.layout = None
         if self.layout_kind:
-            self.layout = t.empty(values.shape + (4,), dtype=t.float32, device=dev)
+            self.layout = t.empty(shape + (4,), dtype=t.float32, device=dev)
             _lib.call("fvr_pack_layout", self.values.data_ptr(), 1, self.grid, self.layout_kind,
                       self.layout.data_ptr(), _lib.stream_ptr())
         # empty-space occupancy: hull key points (their values change) plus any
@@ -175,9 +191,8 @@ class ChannelLoop:
         # so the map stays valid for the whole loop
         self.occ = None
         if self.layout_kind and os.environ.get("FVR_NO_SKIP") != "1":
-            force = t.from_numpy(np.ascontiguousarray(kp_mask, dtype=np.uint8)).to(dev)
-            self.occ = t.empty(values.shape, dtype=t.uint8, device=dev)
-            _lib.call("fvr_occupancy", self.values.data_ptr(), 1, force.data_ptr(), self.grid,
+            self.occ = t.empty(shape, dtype=t.uint8, device=dev)
+            _lib.call("fvr_occupancy", self.values.data_ptr(), 1, kp_dev.data_ptr(), self.grid,
                       self.occ.data_ptr(), _lib.stream_ptr())
 
         # work buffers

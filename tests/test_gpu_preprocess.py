@@ -101,3 +101,22 @@ def test_device_mask_ray_list_matches_host(cuda_device):
     b, tb = reconstruct_channel(images, cams, geom, hull, cfg, render_cfg=rcfg, masks=d_masks, bbox=bbox)
     assert np.array_equal(a.values, b.values)
     assert ta.rmse == tb.rmse
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (5, 7, 3), (40, 33, 29)])
+def test_hull_keypoints_match_key_point_mask(cuda_device, shape):
+    from paper_1809_06417_b200.volume import HullTags
+
+    t = _lib.torch()
+    rng = np.random.default_rng(sum(shape))
+    tags = np.where(rng.random(shape) < 0.2, 7, rng.integers(0, 7, shape)).astype(np.uint32)
+    hull = HullTags(tags, 3)
+    geom = VoxelGrid(*shape, np.zeros(3), 0.1)
+    inside = t.from_numpy(hull.inside_voxels().astype(np.uint8)).to(cuda_device)
+    kp = t.empty(geom.lattice_shape, dtype=t.uint8, device=cuda_device)
+    vals = t.empty(geom.lattice_shape, dtype=t.float32, device=cuda_device)
+    _lib.call("fvr_hull_keypoints", inside.data_ptr(), _lib.grid_struct(geom), kp.data_ptr(), vals.data_ptr(),
+              _lib.stream_ptr())
+    want = hull.key_point_mask()
+    assert np.array_equal(kp.cpu().numpy().astype(bool), want)
+    assert np.array_equal(vals.cpu().numpy(), np.where(want, np.float32(0), np.float32(-1)))
