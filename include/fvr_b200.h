@@ -79,6 +79,8 @@ typedef struct fvr_loop_state {
     int32_t converged; /* trace.converged */
     int32_t reserved;
     double prev_rmse;
+    int32_t work_next;    /* K-render work queue: next unit to hand out */
+    int32_t work_retired; /* warps that found the queue empty (the last one resets both) */
 } fvr_loop_state_t;
 
 const char* fvr_last_error(void);
@@ -175,7 +177,7 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
                     int32_t bbox_w, int32_t bbox_h, const float* src, const float* values,
                     const float* layout, const uint8_t* occ, fvr_grid_t grid, fvr_render_params_t params, double background,
                     const double* scat_dirs, float* residual, double* sq_partials,
-                    const fvr_loop_state_t* state, void* stream);
+                    fvr_loop_state_t* state, void* stream);
 
 /* Back-project the residual of every listed flame ray (ray_list entries are
  * view << 24 | (row_in_bbox * bbox_w + col_in_bbox)). stochastic != 0 draws

@@ -67,6 +67,8 @@ class FvrLoopState(ctypes.Structure):
         ("converged", c_int32),
         ("reserved", c_int32),
         ("prev_rmse", c_double),
+        ("work_next", c_int32),
+        ("work_retired", c_int32),
     ]
 
 

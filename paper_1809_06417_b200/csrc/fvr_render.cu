@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kBlockThreads, 2) loop_render_scat_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
     int n_units, const float* __restrict__ src, const float* __restrict__ values,
     const float4* __restrict__ layout, const uint8_t* __restrict__ occ, Geom g, RenderConsts rc,
-    float* __restrict__ residual, double* __restrict__ sq_partials, const fvr_loop_state_t* __restrict__ state) {
+    float* __restrict__ residual, double* __restrict__ sq_partials, fvr_loop_state_t* __restrict__ state) {
     if (state && state->done) return;
     extern __shared__ float4 smem[];
     float4* s_q1 = smem;
@@ -435,9 +435,34 @@ __global__ void __launch_bounds__(kBlockThreads, 2) loop_render_scat_kernel(
     for (int i = threadIdx.x; i < 3 * kScatDirs; i += blockDim.x) s_thr[i] = (&c_thr[0][0])[i];
     __syncthreads();
     const int stride = gridDim.x * kWarpsPerBlock;
-    for (int unit = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); unit < n_units; unit += stride)
+    if (!state) {
+        for (int unit = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); unit < n_units; unit += stride)
+            render_unit<kModeFastScat>(unit, units_x, units_per_view, cams, u0, v0, w, h, src, values, layout, occ,
+                                       g, rc, nullptr, s_thr, s_q1, s_q2, residual, sq_partials);
+        return;
+    }
+    // Work queue: a unit's cost ranges over two orders of magnitude (rays
+    // through the flame core vs. the bbox margin), so a static round-robin
+    // leaves most SMs idle behind the slowest warps.  Each warp takes the next
+    // unit from a global counter; the last warp to find the queue empty resets
+    // it for the next iteration (every warp retires exactly once).
+    const int lane = threadIdx.x & 31;
+    int* next = &state->work_next;
+    for (;;) {
+        int unit = 0;
+        if (lane == 0) unit = atomicAdd(next, 1);
+        unit = __shfl_sync(0xffffffffu, unit, 0);
+        if (unit >= n_units) break;
         render_unit<kModeFastScat>(unit, units_x, units_per_view, cams, u0, v0, w, h, src, values, layout, occ, g,
                                    rc, nullptr, s_thr, s_q1, s_q2, residual, sq_partials);
+    }
+    if (lane == 0) {
+        __threadfence();
+        if (atomicAdd(&state->work_retired, 1) == stride - 1) {
+            atomicExch(next, 0);
+            atomicExch(&state->work_retired, 0);
+        }
+    }
 }
 
 }  // namespace fvr
@@ -797,7 +822,7 @@ extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_
                                const float* values, const float* layout, const uint8_t* occ,
                                fvr_grid_t grid, fvr_render_params_t params, double background,
                                const double* scat_dirs, float* residual, double* sq_partials,
-                               const fvr_loop_state_t* state, void* stream) {
+                               fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
     if (n_views < 1 || n_views > 65535) return set_error(FVR_ERR_INVALID, "bad view count");
     if (bbox_w < 1 || bbox_h < 1) return set_error(FVR_ERR_INVALID, "empty bounding box");

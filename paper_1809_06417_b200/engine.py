@@ -210,7 +210,7 @@ class ChannelLoop:
         self.packed = self.comm[: self.n_kp]
         self.truth = (t.from_numpy(np.ascontiguousarray(ground_truth, dtype=np.float32)).to(dev)
                       if ground_truth is not None else None)
-        self.state = t.zeros(6, dtype=t.int32, device=dev)  # fvr_loop_state_t (24 B)
+        self.state = t.zeros(8, dtype=t.int32, device=dev)  # fvr_loop_state_t (32 B)
         self.trace = t.zeros(max(self.max_iters, 1), dtype=t.float64, device=dev)
         self.trace_vol = t.zeros(max(self.max_iters, 1), dtype=t.float64, device=dev) \
             if ground_truth is not None else None
@@ -439,7 +439,7 @@ class ChannelLoop:
             self.capture()
         # keep one chunk in flight: after enqueueing chunk i, wait for chunk
         # i-1's state copy and stop once its sticky `done` flag is set
-        bufs = [t.zeros(6, dtype=t.int32, pin_memory=True) for _ in range(2)]
+        bufs = [t.zeros(8, dtype=t.int32, pin_memory=True) for _ in range(2)]
         events = [None, None]
         issued, i = 0, 0
         t_start = time.perf_counter()
