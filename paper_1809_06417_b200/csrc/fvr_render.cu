@@ -145,9 +145,15 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
                         if (!SCAT) {
                             e = tri_yzq(layout + (int64_t)c * plane, g, m[0], m[1], m[2], dl[0], dl[1], dl[2]);
                         } else if (interior) {
+#if FVR_MOMENT_PACKED
+                            float4 r[9];
+                            load_stencil_z4_raw(layout + (int64_t)c * plane, g, m[0], m[1], m[2], r);
+                            moment_eval2(r, dl[0], dl[1], dl[2], thr, q1, q2, e, acc);
+#else
                             float v[27];
                             load_stencil_z4(layout + (int64_t)c * plane, g, m[0], m[1], m[2], v);
                             moment_eval(v, dl[0], dl[1], dl[2], thr, q1, q2, e, acc);
+#endif
                             // sums of non-negative terms in exact arithmetic; the
                             // expanded form can round a vanishing sum below zero
                             e = fmaxf(e, 0.f);
@@ -690,8 +696,12 @@ extern "C" int fvr_set_scatter_dirs(const double* dirs_host, int32_t n) {
             d[a][s] = dirs_host[3 * s + a];
             h[a][s] = (float)(0.5 * dirs_host[3 * s + a]);
         }
+    float2 h2[3][kScatDirs / 2];
+    for (int a = 0; a < 3; ++a)
+        for (int s = 0; s < kScatDirs / 2; ++s) h2[a][s] = make_float2(h[a][s], h[a][s + kScatDirs / 2]);
     if (cudaMemcpyToSymbol(c_dir, d, sizeof(d)) != cudaSuccess ||
-        cudaMemcpyToSymbol(c_half_dir, h, sizeof(h)) != cudaSuccess)
+        cudaMemcpyToSymbol(c_half_dir, h, sizeof(h)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_half_dir2, h2, sizeof(h2)) != cudaSuccess)
         return set_error(FVR_ERR_CUDA, "cudaMemcpyToSymbol failed");
     if (int e = build_moment_tables(dirs_host)) return e;
     for (int i = 0; i < 3 * kScatDirs; ++i) g_dirs_host[i] = dirs_host[i];

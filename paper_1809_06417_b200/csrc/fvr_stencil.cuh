@@ -163,6 +163,9 @@ __device__ __forceinline__ uint32_t inbox_mask(const double p[3], const Geom& g,
 #ifndef FVR_Q3_TABLE
 #define FVR_Q3_TABLE 0
 #endif
+#ifndef FVR_MOMENT_PACKED
+#define FVR_MOMENT_PACKED 1
+#endif
 constexpr int kSplits = kScatDirs + 1;
 __constant__ float c_thr[3][kScatDirs];  // sorted c_{s,a} = s_a / 2 per axis
 __constant__ float c_q0[8];              // Q_{empty}[E]
@@ -294,6 +297,174 @@ __device__ __forceinline__ void moment_eval(const float v[27], float dx, float d
                 }
                 s = fmaf(V[(kx * 3 + ky) * 3 + kz], M, s);
             }
+    scat = s;
+}
+
+// ---- packed (f32x2) moment evaluation -------------------------------------
+//
+// The same sums as moment_eval, arranged for Blackwell's paired FP32 ops
+// (FADD2 / FMUL2 / FFMA2: one issue slot for two lanes of math):
+//  * the stencil arrives as nine float4 z-runs r = (v[z-1], v[z], v[z+1], w)
+//    whose register pairs (x, y) and (z, w) carry the x- and y-stages of the
+//    separable transform two z-slots at a time (w is ignored);
+//  * each sign table Q_A[E] (E bits x=4 y=2 z=1) is four float2 pairs (E, E|z),
+//    and M_A[P] = sum_{E subset P} delta'^{P\E} Q_A[E] is its per-axis zeta
+//    transform: 4 scalar FFMA (z, inside the pairs) + 2 FFMA2 (y) + 2 FFMA2 (x)
+//    instead of one FFMA per (P, E) pair;
+//  * the all-|x| moment pairs direction s with s + 16 against a broadcast delta.
+// Rounding differs from moment_eval only in summation order.
+__constant__ float2 c_half_dir2[3][kScatDirs / 2];  // (c_half_dir[a][s], c_half_dir[a][s + 16])
+
+__device__ __forceinline__ float2 bcast2(float a) { return make_float2(a, a); }
+
+__device__ __forceinline__ void load_stencil_z4_raw(const float4* __restrict__ Z4, const Geom& g, int mx, int my,
+                                                    int mz, float4 r[9]) {
+    const int base = (mx - 1) * g.sx + (my - 1) * g.sy + (mz - 1);
+#pragma unroll
+    for (int jx = 0; jx < 3; ++jx)
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) r[jx * 3 + jy] = __ldg(Z4 + base + jx * g.sx + jy * g.sy);
+}
+
+__device__ __forceinline__ void zeta8(float2 q[4], float hx, float hy, float hz) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q[i].y = fmaf(hz, q[i].x, q[i].y);
+    q[1] = __ffma2_rn(bcast2(hy), q[0], q[1]);
+    q[3] = __ffma2_rn(bcast2(hy), q[2], q[3]);
+    q[2] = __ffma2_rn(bcast2(hx), q[0], q[2]);
+    q[3] = __ffma2_rn(bcast2(hx), q[1], q[3]);
+}
+
+__device__ __forceinline__ void load_q8x2(const float4* __restrict__ t, int row, float2 q[4]) {
+    const float4 a = t[2 * row], b = t[2 * row + 1];
+    q[0] = make_float2(a.x, a.y);
+    q[1] = make_float2(a.z, a.w);
+    q[2] = make_float2(b.x, b.y);
+    q[3] = make_float2(b.z, b.w);
+}
+
+__device__ __forceinline__ float pick8(const float2 q[4], int P) { return (P & 1) ? q[P >> 1].y : q[P >> 1].x; }
+
+// s += sum over the stencil moments k with A(k) = A of V[k] * M_A[P(k)]
+template <int A>
+__device__ __forceinline__ float dot_moments(const float V[27], const float2 q[4], float s) {
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+            for (int kz = 0; kz < 3; ++kz) {
+                const int Ak = ((kx == 2) << 2) | ((ky == 2) << 1) | (kz == 2);
+                const int Pk = ((kx != 0) << 2) | ((ky != 0) << 1) | (kz != 0);
+                if (Ak == A) s = fmaf(V[(kx * 3 + ky) * 3 + kz], pick8(q, Pk), s);
+            }
+    return s;
+}
+
+__device__ __forceinline__ void moment_eval2(const float4 r[9], float dx, float dy, float dz,
+                                             const float* __restrict__ thr, const float4* q1, const float4* q2,
+                                             float& emit, float& scat) {
+    float V[27];
+    {
+        // x- then y-stage on (z-1, z) and (z+1, w) pairs
+        float2 a[9], b[9];
+#pragma unroll
+        for (int l = 0; l < 9; ++l) {
+            a[l] = make_float2(r[l].x, r[l].y);
+            b[l] = make_float2(r[l].z, r[l].w);
+        }
+        float2 ta[9], tb[9];
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) {  // along x: l = jx*3 + jy
+            const float2 am = a[jy], ac = a[3 + jy], ap = a[6 + jy];
+            const float2 bm = b[jy], bc = b[3 + jy], bp = b[6 + jy];
+            ta[jy] = ac;
+            ta[3 + jy] = __fadd2_rn(ap, make_float2(-am.x, -am.y));
+            ta[6 + jy] = __ffma2_rn(bcast2(-2.f), ac, __fadd2_rn(ap, am));
+            tb[jy] = bc;
+            tb[3 + jy] = __fadd2_rn(bp, make_float2(-bm.x, -bm.y));
+            tb[6 + jy] = __ffma2_rn(bcast2(-2.f), bc, __fadd2_rn(bp, bm));
+        }
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {  // along y
+            const float2 am = ta[kx * 3], ac = ta[kx * 3 + 1], ap = ta[kx * 3 + 2];
+            const float2 bm = tb[kx * 3], bc = tb[kx * 3 + 1], bp = tb[kx * 3 + 2];
+            a[kx * 3] = ac;
+            a[kx * 3 + 1] = __fadd2_rn(ap, make_float2(-am.x, -am.y));
+            a[kx * 3 + 2] = __ffma2_rn(bcast2(-2.f), ac, __fadd2_rn(ap, am));
+            b[kx * 3] = bc;
+            b[kx * 3 + 1] = __fadd2_rn(bp, make_float2(-bm.x, -bm.y));
+            b[kx * 3 + 2] = __ffma2_rn(bcast2(-2.f), bc, __fadd2_rn(bp, bm));
+        }
+#pragma unroll
+        for (int l = 0; l < 9; ++l) {  // along z, inside the pairs
+            const float m = a[l].x, c = a[l].y, p = b[l].x;
+            V[3 * l] = c;
+            V[3 * l + 1] = p - m;
+            V[3 * l + 2] = fmaf(-2.f, c, p + m);
+        }
+    }
+    const float hx = 0.5f * dx, hy = 0.5f * dy, hz = 0.5f * dz;
+    {
+        const float ahx = fabsf(hx), ahy = fabsf(hy), ahz = fabsf(hz);
+        float ey[3];
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {
+            float t[3];
+#pragma unroll
+            for (int ky = 0; ky < 3; ++ky) {
+                const int l = kx * 3 + ky;
+                t[ky] = fmaf(ahz, V[3 * l + 2], fmaf(hz, V[3 * l + 1], V[3 * l]));
+            }
+            ey[kx] = fmaf(ahy, t[2], fmaf(hy, t[1], t[0]));
+        }
+        emit = fmaf(ahx, ey[2], fmaf(hx, ey[1], ey[0]));
+    }
+    const int ix = split_index(thr, -dx), iy = split_index(thr + kScatDirs, -dy),
+              iz = split_index(thr + 2 * kScatDirs, -dz);
+    float s = 0.f;
+    {
+        float2 q[4] = {make_float2(c_q0[0], c_q0[1]), make_float2(c_q0[2], c_q0[3]),
+                       make_float2(c_q0[4], c_q0[5]), make_float2(c_q0[6], c_q0[7])};
+        zeta8(q, hx, hy, hz);
+        s = dot_moments<0>(V, q, s);
+    }
+    {
+        float2 q[4];
+        load_q8x2(q1, 0 * kSplits + ix, q);
+        zeta8(q, hx, hy, hz);
+        s = dot_moments<4>(V, q, s);
+        load_q8x2(q1, 1 * kSplits + iy, q);
+        zeta8(q, hx, hy, hz);
+        s = dot_moments<2>(V, q, s);
+        load_q8x2(q1, 2 * kSplits + iz, q);
+        zeta8(q, hx, hy, hz);
+        s = dot_moments<1>(V, q, s);
+        load_q8x2(q2, (0 * kSplits + ix) * kSplits + iy, q);
+        zeta8(q, hx, hy, hz);
+        s = dot_moments<6>(V, q, s);
+        load_q8x2(q2, (1 * kSplits + ix) * kSplits + iz, q);
+        zeta8(q, hx, hy, hz);
+        s = dot_moments<5>(V, q, s);
+        load_q8x2(q2, (2 * kSplits + iy) * kSplits + iz, q);
+        zeta8(q, hx, hy, hz);
+        s = dot_moments<3>(V, q, s);
+    }
+    {
+        float2 acc = make_float2(0.f, 0.f);
+        const float2 DX = bcast2(dx), DY = bcast2(dy), DZ = bcast2(dz);
+#pragma unroll
+        for (int d = 0; d < kScatDirs / 2; ++d) {
+            const float2 x = __fadd2_rn(DX, c_half_dir2[0][d]);
+            const float2 y = __fadd2_rn(DY, c_half_dir2[1][d]);
+            const float2 z = __fadd2_rn(DZ, c_half_dir2[2][d]);
+            float2 p = __fmul2_rn(__fmul2_rn(x, y), z);
+            p.x = fabsf(p.x);
+            p.y = fabsf(p.y);
+            acc = __fadd2_rn(acc, p);
+        }
+        s = fmaf(V[26], 0.125f * (acc.x + acc.y), s);
+    }
     scat = s;
 }
 
