@@ -106,6 +106,27 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
         for (int a = 0; a < 3; ++a) qb[a] = ((o[a] - g.lo[a]) + t0 * d[a]) * g.inv_edge;
         const double nmax[3] = {(double)g.nx, (double)g.ny, (double)g.nz};
         int k = 1;
+        // occupancy probe of sample kk, issued one sample ahead of its use so
+        // the load overlaps the evaluation of the current sample
+        auto probe = [&](int kk) -> int {
+            if (!occ || kk > n) return 0;
+            int mm[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const double qa = fma((double)kk, d[a], qb[a]);
+                const int na = a == 0 ? g.nx : (a == 1 ? g.ny : g.nz);
+                if (SCAT) {
+                    mm[a] = min(max((int)rint(qa), 0), na);
+                } else {
+                    int ca;
+                    float fa;
+                    cell_frac(qa, na, ca, fa);
+                    mm[a] = ca;
+                }
+            }
+            return (int)__ldg(occ + (unsigned)(mm[0] * g.sx + mm[1] * g.sy + mm[2]));
+        };
+        int D_next = probe(1);
         while (k <= n) {
             double q[3];
 #pragma unroll
@@ -135,9 +156,10 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
             // neighbourhood within j+2).  The skip is the minimum over the
             // warp so the lanes stay aligned on k; the transparency still
             // advances by repeated multiplication, as in the reference.
-            const int D = occ ? (int)__ldg(occ + m[0] * g.sx + m[1] * g.sy + m[2]) : 0;
+            const int D = D_next;
             const unsigned act = __activemask();
             if (__any_sync(act, D <= 1)) {
+                D_next = probe(k + 1);
                 if (D <= 1) {
 #pragma unroll 1
                     for (int c = 0; c < NCH; ++c) {
@@ -189,6 +211,7 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
                 s = min(s, n - k + 1);
                 for (int j = 0; j < s; ++j) t_dst *= rc.one_minus_tau;
                 k += s;
+                D_next = probe(k);
             }
         }
     }

@@ -183,6 +183,19 @@ __device__ __forceinline__ int split_index(const float* __restrict__ thr, float 
     return i;
 }
 
+// The same count; the first two levels compare against the constant-bank copy
+// (no shared-memory round trip on the critical path), the last three read
+// the shared copy.
+__device__ __forceinline__ int split_index_c(int axis, const float* __restrict__ thr, float key) {
+    // sorted: #{t7, t15, t23 < key} * 8 is the first two levels of the search
+    int i = ((c_thr[axis][7] < key) + (c_thr[axis][15] < key) + (c_thr[axis][23] < key)) * 8;
+#pragma unroll
+    for (int step = 4; step >= 1; step >>= 1)
+        if (thr[i + step - 1] < key) i += step;
+    if (i == 31 && c_thr[axis][31] < key) i = 32;
+    return i;
+}
+
 __device__ __forceinline__ void load_q8(const float4* __restrict__ t, int row, float q[8]) {
     const float4 a = t[2 * row], b = t[2 * row + 1];
     q[0] = a.x; q[1] = a.y; q[2] = a.z; q[3] = a.w;
@@ -319,11 +332,11 @@ __device__ __forceinline__ float2 bcast2(float a) { return make_float2(a, a); }
 
 __device__ __forceinline__ void load_stencil_z4_raw(const float4* __restrict__ Z4, const Geom& g, int mx, int my,
                                                     int mz, float4 r[9]) {
-    const int base = (mx - 1) * g.sx + (my - 1) * g.sy + (mz - 1);
+    const float4* p = Z4 + ((mx - 1) * g.sx + (my - 1) * g.sy + (mz - 1));
 #pragma unroll
     for (int jx = 0; jx < 3; ++jx)
 #pragma unroll
-        for (int jy = 0; jy < 3; ++jy) r[jx * 3 + jy] = __ldg(Z4 + base + jx * g.sx + jy * g.sy);
+        for (int jy = 0; jy < 3; ++jy) r[jx * 3 + jy] = __ldg(p + (jx * g.sx + jy * g.sy));
 }
 
 __device__ __forceinline__ void zeta8(float2 q[4], float hx, float hy, float hz) {
@@ -420,8 +433,8 @@ __device__ __forceinline__ void moment_eval2(const float4 r[9], float dx, float 
         }
         emit = fmaf(ahx, ey[2], fmaf(hx, ey[1], ey[0]));
     }
-    const int ix = split_index(thr, -dx), iy = split_index(thr + kScatDirs, -dy),
-              iz = split_index(thr + 2 * kScatDirs, -dz);
+    const int ix = split_index_c(0, thr, -dx), iy = split_index_c(1, thr + kScatDirs, -dy),
+              iz = split_index_c(2, thr + 2 * kScatDirs, -dz);
     float s = 0.f;
     {
         float2 q[4] = {make_float2(c_q0[0], c_q0[1]), make_float2(c_q0[2], c_q0[3]),
