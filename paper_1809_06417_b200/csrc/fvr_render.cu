@@ -449,7 +449,14 @@ __global__ void __launch_bounds__(kBlockThreads) loop_render_kernel(
 constexpr int kQ1Vec = 3 * kSplits * 2, kQ2Vec = 3 * kSplits * kSplits * 2;
 constexpr size_t kScatSmem = sizeof(float4) * (kQ1Vec + kQ2Vec) + sizeof(float) * 3 * kScatDirs;
 
-__global__ void __launch_bounds__(kBlockThreads, 2) loop_render_scat_kernel(
+// One 512-thread CTA per SM: the tables are staged once per SM (105 KB), which
+// leaves the rest of the 256 KB L1/shared array to cache the stencil loads.
+#ifndef FVR_SCAT_THREADS
+#define FVR_SCAT_THREADS 512
+#endif
+constexpr int kScatThreads = FVR_SCAT_THREADS, kScatWarps = kScatThreads / 32, kScatCtasPerSm = 512 / kScatThreads;
+
+__global__ void __launch_bounds__(kScatThreads, kScatCtasPerSm) loop_render_scat_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
     int n_units, const float* __restrict__ src, const float* __restrict__ values,
     const float4* __restrict__ layout, const uint8_t* __restrict__ occ, Geom g, RenderConsts rc,
@@ -463,9 +470,9 @@ __global__ void __launch_bounds__(kBlockThreads, 2) loop_render_scat_kernel(
     for (int i = threadIdx.x; i < kQ2Vec; i += blockDim.x) s_q2[i] = g_q2[i];
     for (int i = threadIdx.x; i < 3 * kScatDirs; i += blockDim.x) s_thr[i] = (&c_thr[0][0])[i];
     __syncthreads();
-    const int stride = gridDim.x * kWarpsPerBlock;
+    const int stride = gridDim.x * kScatWarps;
     if (!state) {
-        for (int unit = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); unit < n_units; unit += stride)
+        for (int unit = blockIdx.x * kScatWarps + (threadIdx.x >> 5); unit < n_units; unit += stride)
             render_unit<kModeFastScat>(unit, units_x, units_per_view, cams, u0, v0, w, h, src, values, layout, occ,
                                        g, rc, nullptr, s_thr, s_q1, s_q2, residual, sq_partials);
         return;
@@ -885,13 +892,19 @@ extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_
                 if (cudaFuncSetAttribute(loop_render_scat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kScatSmem) != cudaSuccess)
                     return set_error(FVR_ERR_CUDA, "cannot reserve shared memory for the moment tables");
+                // smallest carveout that holds the tables: the remainder is L1
+                int carve = kScatCtasPerSm == 1 ? 50 : 100;
+                if (const char* e = getenv("FVR_SCAT_CARVEOUT")) carve = atoi(e);
+                if (carve >= 0) cudaFuncSetAttribute(loop_render_scat_kernel,
+                                                     cudaFuncAttributePreferredSharedMemoryCarveout, carve);
                 attr_set = true;
             }
             int dev = 0, sms = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            const int pblocks = (int)blocks < 2 * sms ? (int)blocks : 2 * sms;
-            loop_render_scat_kernel<<<pblocks, kBlockThreads, kScatSmem, st>>>(
+            const int want = (n_units + kScatWarps - 1) / kScatWarps;
+            const int pblocks = want < kScatCtasPerSm * sms ? want : kScatCtasPerSm * sms;
+            loop_render_scat_kernel<<<pblocks, kScatThreads, kScatSmem, st>>>(
                 cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, src, values, lay, occ, g, rc, residual,
                 sq_partials, state);
             break;
