@@ -15,7 +15,8 @@ from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint6
 
 from .errors import EmptyHullError, NoFlameError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfvr_b200.so")
+# FVR_LIB selects an experiment build of the same library (csrc/Makefile OUT=...)
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ.get("FVR_LIB", "libfvr_b200.so"))
 
 FVR_OK = 0
 FVR_ERR_INVALID = 1

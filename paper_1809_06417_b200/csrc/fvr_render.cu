@@ -86,13 +86,15 @@ __device__ __forceinline__ void march_render(const double o[3], const double d[3
 // lattice coordinate is q = qb + k*d in fp64 (continuous quantities only);
 // the sample count, and for samples within half a voxel of a box face the
 // exact gather points, follow the reference arithmetic.
-template <int NCH, bool SCAT>
+template <int NCH, bool SCAT, int NS = 0>
 __device__ __forceinline__ void march_render_fast(const double o[3], const double d[3], const Geom& g,
                                                   const float* __restrict__ values, int plane,
                                                   const float4* __restrict__ layout,
                                                   const uint8_t* __restrict__ occ,
                                                   const RenderConsts& rc, const float* __restrict__ thr,
                                                   const float4* q1, const float4* q2, double out[NCH]) {
+    // NS > 0: cubic lattice of NS key points per axis, strides known at compile time
+    const int SY = NS ? NS : g.sy, SX = NS ? NS * NS : g.sx;
     double l[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) l[c] = 0.0;
@@ -124,7 +126,7 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
                     mm[a] = ca;
                 }
             }
-            return (int)__ldg(occ + (unsigned)(mm[0] * g.sx + mm[1] * g.sy + mm[2]));
+            return (int)__ldg(occ + (unsigned)(mm[0] * SX + mm[1] * SY + mm[2]));
         };
         int D_next = probe(1);
         while (k <= n) {
@@ -169,7 +171,7 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
                         } else if (interior) {
 #if FVR_MOMENT_PACKED
                             float4 r[9];
-                            load_stencil_z4_raw(layout + (int64_t)c * plane, g, m[0], m[1], m[2], r);
+                            load_stencil_z4_raw(layout + (int64_t)c * plane, SX, SY, m[0], m[1], m[2], r);
                             moment_eval2(r, dl[0], dl[1], dl[2], thr, q1, q2, e, acc);
 #else
                             float v[27];
@@ -393,7 +395,7 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-template <int MODE>
+template <int MODE, int NS = 0>
 __device__ __forceinline__ void render_unit(int unit, int units_x, int units_per_view,
                                             const fvr_camera_t* __restrict__ cams, int u0, int v0, int w,
                                             int h, const float* __restrict__ src,
@@ -414,7 +416,7 @@ __device__ __forceinline__ void render_unit(int unit, int units_x, int units_per
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         double rec[1];
         if (MODE == kModeFastScat)
-            march_render_fast<1, true>(cam.center, d, g, values, 0, layout, occ, rc, thr, q1, q2, rec);
+            march_render_fast<1, true, NS>(cam.center, d, g, values, 0, layout, occ, rc, thr, q1, q2, rec);
         else
             march_dispatch<1, MODE>(cam.center, d, g, values, 0, layout, occ, rc, scat, thr, rec);
         const int64_t pix = ((int64_t)view * h + row) * w + col;
@@ -456,6 +458,7 @@ constexpr size_t kScatSmem = sizeof(float4) * (kQ1Vec + kQ2Vec) + sizeof(float) 
 #endif
 constexpr int kScatThreads = FVR_SCAT_THREADS, kScatWarps = kScatThreads / 32, kScatCtasPerSm = 512 / kScatThreads;
 
+template <int NS>
 __global__ void __launch_bounds__(kScatThreads, kScatCtasPerSm) loop_render_scat_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
     int n_units, const float* __restrict__ src, const float* __restrict__ values,
@@ -473,8 +476,8 @@ __global__ void __launch_bounds__(kScatThreads, kScatCtasPerSm) loop_render_scat
     const int stride = gridDim.x * kScatWarps;
     if (!state) {
         for (int unit = blockIdx.x * kScatWarps + (threadIdx.x >> 5); unit < n_units; unit += stride)
-            render_unit<kModeFastScat>(unit, units_x, units_per_view, cams, u0, v0, w, h, src, values, layout, occ,
-                                       g, rc, nullptr, s_thr, s_q1, s_q2, residual, sq_partials);
+            render_unit<kModeFastScat, NS>(unit, units_x, units_per_view, cams, u0, v0, w, h, src, values, layout,
+                                           occ, g, rc, nullptr, s_thr, s_q1, s_q2, residual, sq_partials);
         return;
     }
     // Work queue: a unit's cost ranges over two orders of magnitude (rays
@@ -489,8 +492,8 @@ __global__ void __launch_bounds__(kScatThreads, kScatCtasPerSm) loop_render_scat
         if (lane == 0) unit = atomicAdd(next, 1);
         unit = __shfl_sync(0xffffffffu, unit, 0);
         if (unit >= n_units) break;
-        render_unit<kModeFastScat>(unit, units_x, units_per_view, cams, u0, v0, w, h, src, values, layout, occ, g,
-                                   rc, nullptr, s_thr, s_q1, s_q2, residual, sq_partials);
+        render_unit<kModeFastScat, NS>(unit, units_x, units_per_view, cams, u0, v0, w, h, src, values, layout, occ,
+                                       g, rc, nullptr, s_thr, s_q1, s_q2, residual, sq_partials);
     }
     if (lane == 0) {
         __threadfence();
@@ -857,6 +860,31 @@ extern "C" int fvr_loop_blocks_per_view(int32_t bbox_w, int32_t bbox_h) {
     return ((bbox_w + kUnitW - 1) / kUnitW) * ((bbox_h + kUnitH - 1) / kUnitH);
 }
 
+namespace {
+template <int NS>
+int launch_scat(int blocks, cudaStream_t st, const fvr_camera_t* cams, int u0, int v0, int w, int h, int units_x,
+                int upv, int n_units, const float* src, const float* values, const float4* lay, const uint8_t* occ,
+                const Geom& g, const RenderConsts& rc, float* residual, double* sq_partials,
+                fvr_loop_state_t* state) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(loop_render_scat_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kScatSmem) != cudaSuccess)
+            return set_error(FVR_ERR_CUDA, "cannot reserve shared memory for the moment tables");
+        // smallest carveout that holds the tables: the remainder is L1
+        int carve = kScatCtasPerSm == 1 ? 50 : 100;
+        if (const char* e = getenv("FVR_SCAT_CARVEOUT")) carve = atoi(e);
+        if (carve >= 0)
+            cudaFuncSetAttribute(loop_render_scat_kernel<NS>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+        attr_set = true;
+    }
+    loop_render_scat_kernel<NS><<<blocks, kScatThreads, kScatSmem, st>>>(cams, u0, v0, w, h, units_x, upv, n_units,
+                                                                         src, values, lay, occ, g, rc, residual,
+                                                                         sq_partials, state);
+    return FVR_OK;
+}
+}  // namespace
+
 extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0,
                                int32_t bbox_w, int32_t bbox_h, const float* src,
                                const float* values, const float* layout, const uint8_t* occ,
@@ -887,26 +915,14 @@ extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_
         case kModeScatG0: FVR_LOOP_RENDER(kModeScatG0); break;
         case kModeFastPlain: FVR_LOOP_RENDER(kModeFastPlain); break;
         default: {
-            static bool attr_set = false;
-            if (!attr_set) {
-                if (cudaFuncSetAttribute(loop_render_scat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kScatSmem) != cudaSuccess)
-                    return set_error(FVR_ERR_CUDA, "cannot reserve shared memory for the moment tables");
-                // smallest carveout that holds the tables: the remainder is L1
-                int carve = kScatCtasPerSm == 1 ? 50 : 100;
-                if (const char* e = getenv("FVR_SCAT_CARVEOUT")) carve = atoi(e);
-                if (carve >= 0) cudaFuncSetAttribute(loop_render_scat_kernel,
-                                                     cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-                attr_set = true;
-            }
             int dev = 0, sms = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             const int want = (n_units + kScatWarps - 1) / kScatWarps;
             const int pblocks = want < kScatCtasPerSm * sms ? want : kScatCtasPerSm * sms;
-            loop_render_scat_kernel<<<pblocks, kScatThreads, kScatSmem, st>>>(
-                cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, src, values, lay, occ, g, rc, residual,
-                sq_partials, state);
+            if (int e = launch_scat<0>(pblocks, st, cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, src, values,
+                                       lay, occ, g, rc, residual, sq_partials, state))
+                return e;
             break;
         }
     }

@@ -330,13 +330,15 @@ __constant__ float2 c_half_dir2[3][kScatDirs / 2];  // (c_half_dir[a][s], c_half
 
 __device__ __forceinline__ float2 bcast2(float a) { return make_float2(a, a); }
 
-__device__ __forceinline__ void load_stencil_z4_raw(const float4* __restrict__ Z4, const Geom& g, int mx, int my,
+// sx, sy: lattice strides -- compile-time constants for the specialised
+// cubic lattices, so the nine loads are one pointer plus immediate offsets
+__device__ __forceinline__ void load_stencil_z4_raw(const float4* __restrict__ Z4, int sx, int sy, int mx, int my,
                                                     int mz, float4 r[9]) {
-    const float4* p = Z4 + ((mx - 1) * g.sx + (my - 1) * g.sy + (mz - 1));
+    const float4* p = Z4 + (mx * sx + my * sy + (mz - 1));
 #pragma unroll
     for (int jx = 0; jx < 3; ++jx)
 #pragma unroll
-        for (int jy = 0; jy < 3; ++jy) r[jx * 3 + jy] = __ldg(p + (jx * g.sx + jy * g.sy));
+        for (int jy = 0; jy < 3; ++jy) r[jx * 3 + jy] = __ldg(p + ((jx - 1) * sx + (jy - 1) * sy));
 }
 
 __device__ __forceinline__ void zeta8(float2 q[4], float hx, float hy, float hz) {
@@ -435,6 +437,11 @@ __device__ __forceinline__ void moment_eval2(const float4 r[9], float dx, float 
     }
     const int ix = split_index_c(0, thr, -dx), iy = split_index_c(1, thr + kScatDirs, -dy),
               iz = split_index_c(2, thr + 2 * kScatDirs, -dz);
+#if FVR_Q3_TABLE
+    // all-|x| moment from its table: issued first, consumed last
+    const float4 q3a = __ldg(g_q3 + 2 * ((ix * kSplits + iy) * kSplits + iz));
+    const float4 q3b = __ldg(g_q3 + 2 * ((ix * kSplits + iy) * kSplits + iz) + 1);
+#endif
     float s = 0.f;
     {
         float2 q[4] = {make_float2(c_q0[0], c_q0[1]), make_float2(c_q0[2], c_q0[3]),
@@ -463,6 +470,14 @@ __device__ __forceinline__ void moment_eval2(const float4 r[9], float dx, float 
         zeta8(q, hx, hy, hz);
         s = dot_moments<3>(V, q, s);
     }
+#if FVR_Q3_TABLE
+    {
+        float2 q[4] = {make_float2(q3a.x, q3a.y), make_float2(q3a.z, q3a.w), make_float2(q3b.x, q3b.y),
+                       make_float2(q3b.z, q3b.w)};
+        zeta8(q, hx, hy, hz);
+        s = fmaf(V[26], q[3].y, s);
+    }
+#else
     {
         float2 acc = make_float2(0.f, 0.f);
         const float2 DX = bcast2(dx), DY = bcast2(dy), DZ = bcast2(dz);
@@ -478,6 +493,7 @@ __device__ __forceinline__ void moment_eval2(const float4 r[9], float dx, float 
         }
         s = fmaf(V[26], 0.125f * (acc.x + acc.y), s);
     }
+#endif
     scat = s;
 }
 
