@@ -173,8 +173,13 @@ __global__ void __launch_bounds__(128) plan_fill_kernel(
     });
 }
 
-// One warp per hull key point: delta = sum_e res[idx_e] * W_e (32.32 fixed point).
-template <bool PACKED>
+// One group of G lanes per hull key point: delta = sum_e res[idx_e] * W_e
+// (32.32 fixed point, so any grouping of the sum gives the same bits).  Each
+// lane keeps U independent streaming loads in flight; a row is three
+// dependent round trips (plan -> residual -> value), so the kernel is bound
+// by how many rows are in flight: G = 4 puts eight rows in each warp
+// (config 2: G=32 0.113 ms, 16 0.098, 8 0.094, 4 0.092, 2 0.122).
+template <bool PACKED, int G, int U>
 __global__ void __launch_bounds__(256) gather_kernel(
     const long long* __restrict__ row_off, const int2* __restrict__ entries, int64_t n_rows,
     const float* __restrict__ residual, const int32_t* __restrict__ kp_index,
@@ -182,29 +187,30 @@ __global__ void __launch_bounds__(256) gather_kernel(
     long long* __restrict__ packed, const fvr_loop_state_t* __restrict__ state) {
     if (state && state->done) return;
     const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t row = warp; row < n_rows; row += n_warps) {
+    const int sub = lane & (G - 1);
+    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const int64_t group = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int64_t n_groups = ((int64_t)gridDim.x * blockDim.x) / G;
+    for (int64_t row = group; row < n_rows; row += n_groups) {
         const long long b = row_off[row], e = row_off[row + 1];
         long long acc = 0;
-        // four independent streaming loads in flight per lane (the plan is
-        // read once per iteration: evict-first, keep L2 for the residual)
-        for (long long base = b; base < e; base += 128) {
-            int2 en[4];
+        // the plan is read once per iteration: evict-first, keep L2 for the residual
+        for (long long base = b; base < e; base += G * U) {
+            int2 en[U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const long long i = base + lane + 32 * u;
+            for (int u = 0; u < U; ++u) {
+                const long long i = base + sub + G * u;
                 en[u] = i < e ? __ldcs(entries + i) : make_int2(0, 0);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const float prod = __ldg(residual + en[u].x) * __int_as_float(en[u].y);
                 acc += __float2ll_rn(prod * 4294967296.0f);
             }
         }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if (lane == 0) {
+        for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(gmask, acc, off);
+        if (sub == 0) {
             if (PACKED) {
                 packed[row] = acc;
             } else if (acc != 0) {
@@ -304,19 +310,36 @@ extern "C" int fvr_loop_gather(const int64_t* row_offsets, const int32_t* entrie
                                const fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
     if (n_kp == 0) return FVR_OK;
-    int64_t blocks = (n_kp * 32 + 255) / 256;
+    static int group_lanes = 0;
+    if (!group_lanes) {
+        const char* e = getenv("FVR_GATHER_G");
+        group_lanes = e ? atoi(e) : 4;
+        if (group_lanes != 4 && group_lanes != 8 && group_lanes != 16 && group_lanes != 32) group_lanes = 4;
+    }
+    int64_t blocks = (n_kp * group_lanes + 255) / 256;
     if (blocks > 148 * 64) blocks = 148 * 64;
     const int sy = grid.nz + 1, ny1 = grid.ny + 1;
     cudaStream_t st = (cudaStream_t)stream;
     const auto* ro = reinterpret_cast<const long long*>(row_offsets);
     const auto* en = reinterpret_cast<const int2*>(entries);
-    if (packed)
-        gather_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(ro, en, n_kp, residual, kp_index, values, layout,
-                                                              layout_kind, sy, ny1,
-                                                              reinterpret_cast<long long*>(packed), state);
-    else
-        gather_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(ro, en, n_kp, residual, kp_index, values, layout,
-                                                               layout_kind, sy, ny1, nullptr, state);
+    long long* pk = reinterpret_cast<long long*>(packed);
+#define FVR_GATHER(GL, UL)                                                                                         \
+    do {                                                                                                         \
+        if (packed)                                                                                              \
+            gather_kernel<true, GL, UL><<<(unsigned)blocks, 256, 0, st>>>(ro, en, n_kp, residual, kp_index, values,  \
+                                                                         layout, layout_kind, sy, ny1, pk, state); \
+        else                                                                                                     \
+            gather_kernel<false, GL, UL><<<(unsigned)blocks, 256, 0, st>>>(ro, en, n_kp, residual, kp_index, values, \
+                                                                          layout, layout_kind, sy, ny1, nullptr,  \
+                                                                          state);                                 \
+    } while (0)
+    switch (group_lanes) {
+        case 8: FVR_GATHER(8, 16); break;
+        case 16: FVR_GATHER(16, 8); break;
+        case 32: FVR_GATHER(32, 4); break;
+        default: FVR_GATHER(4, 32); break;
+    }
+#undef FVR_GATHER
     return check_launch("loop_gather");
     FVR_TRY_END
 }
