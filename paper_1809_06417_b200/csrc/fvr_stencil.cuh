@@ -479,19 +479,22 @@ __device__ __forceinline__ void moment_eval2(const float4 r[9], float dx, float 
     }
 #else
     {
-        float2 acc = make_float2(0.f, 0.f);
+        // |x y| * |z| accumulated by FFMA2 with |.| operand modifiers; two
+        // accumulators halve the dependent chain
+        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
         const float2 DX = bcast2(dx), DY = bcast2(dy), DZ = bcast2(dz);
 #pragma unroll
         for (int d = 0; d < kScatDirs / 2; ++d) {
             const float2 x = __fadd2_rn(DX, c_half_dir2[0][d]);
             const float2 y = __fadd2_rn(DY, c_half_dir2[1][d]);
             const float2 z = __fadd2_rn(DZ, c_half_dir2[2][d]);
-            float2 p = __fmul2_rn(__fmul2_rn(x, y), z);
-            p.x = fabsf(p.x);
-            p.y = fabsf(p.y);
-            acc = __fadd2_rn(acc, p);
+            float2 xy = __fmul2_rn(x, y);
+            xy.x = fabsf(xy.x);
+            xy.y = fabsf(xy.y);
+            acc[d & 1] = __ffma2_rn(xy, make_float2(fabsf(z.x), fabsf(z.y)), acc[d & 1]);
         }
-        s = fmaf(V[26], 0.125f * (acc.x + acc.y), s);
+        const float2 a2 = __fadd2_rn(acc[0], acc[1]);
+        s = fmaf(V[26], 0.125f * (a2.x + a2.y), s);
     }
 #endif
     scat = s;
