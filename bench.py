@@ -256,13 +256,6 @@ def run_gpu(args):
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     sc = make_scene()
-    cfg = ReconstructionConfig(alpha_l=ALPHA_L, alpha_d=1.0, tau=TAU, max_iters=args.steps + args.warmup,
-                               converge_eps=1e-12, deterministic_mode=True)
-    grid0 = _init_grid(sc["geom"], sc["hull"], "green")
-    src = [im.data[sc["bbox"].slices][:, :, 0] for im in sc["images"]]
-    loop = ChannelLoop(sc["cams"], grid0, grid0.values, src, sc["masks"], sc["bbox"],
-                       sc["hull"].inside_voxels(), sc["hull"].key_point_mask(), sc["rcfg"],
-                       _loop_config(cfg, grid0), cfg.max_iters + 8, background=0.0, use_graph=False)
     dev = torch.device("cuda", local)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
@@ -272,36 +265,52 @@ def run_gpu(args):
         torch.cuda.synchronize()
 
     stream = _lib.stream_ptr()
-    stages = [(n, f) for n, f in loop.stages() if f is not None]
-    names = [n for n, _ in stages]
 
-    def one_step(evs):
+    def timed_loop(deterministic: bool, steps: int, warmup: int, sampler=None):
+        """K timed iterations of one ChannelLoop; per-stage CUDA events."""
+        cfg = ReconstructionConfig(alpha_l=ALPHA_L, alpha_d=1.0, tau=TAU, max_iters=steps + warmup,
+                                   converge_eps=1e-12, deterministic_mode=deterministic, g_sigma=0.1, rng_seed=0)
+        grid0 = _init_grid(sc["geom"], sc["hull"], "green")
+        src = [im.data[sc["bbox"].slices][:, :, 0] for im in sc["images"]]
+        loop = ChannelLoop(sc["cams"], grid0, grid0.values, src, sc["masks"], sc["bbox"],
+                           sc["hull"].inside_voxels(), sc["hull"].key_point_mask(), sc["rcfg"],
+                           _loop_config(cfg, grid0), cfg.max_iters + 8, background=0.0, use_graph=False)
+        stages = [(n, f) for n, f in loop.stages() if f is not None]
+        names = [n for n, _ in stages]
+
+        def one_step(evs):
+            launches = 0
+            evs[0].record()
+            for i, (_, fn) in enumerate(stages):
+                launches += fn(stream)
+                evs[i + 1].record()
+            return launches
+
+        def new_events():
+            return [torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)]
+
+        for _ in range(warmup):
+            flush.fill_(1.0)
+            one_step(new_events())
+        if sampler is not None:
+            sampler.start()
+            time.sleep(0.3)
+        barrier()
+        all_evs = []
         launches = 0
-        evs[0].record()
-        for i, (_, fn) in enumerate(stages):
-            launches += fn(stream)
-            evs[i + 1].record()
-        return launches
+        for _ in range(steps):
+            flush.fill_(1.0)  # L2 flush between timed steps, outside the step's events
+            evs = new_events()
+            launches += one_step(evs)
+            all_evs.append(evs)
+        barrier()
+        clocks = sampler.stop() if sampler is not None else None
+        st = loop.read_state()
+        assert st["it"] == warmup + steps and not st["done"], st
+        return loop, names, all_evs, launches, clocks, grid0, src
 
-    def new_events():
-        return [torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)]
-
-    for _ in range(args.warmup):
-        flush.fill_(1.0)
-        one_step(new_events())
     sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.3)
-    barrier()
-    all_evs = []
-    launches = 0
-    for _ in range(args.steps):
-        flush.fill_(1.0)  # L2 flush between timed steps, outside the step's events
-        evs = new_events()
-        launches += one_step(evs)
-        all_evs.append(evs)
-    barrier()
-    clocks = sampler.stop()
+    loop, names, all_evs, launches, clocks, grid0, src = timed_loop(True, args.steps, args.warmup, sampler)
     step_ms = np.array([e[0].elapsed_time(e[-1]) for e in all_evs])
     part_ms = {n: float(np.mean([e[i].elapsed_time(e[i + 1]) for e in all_evs])) for i, n in enumerate(names)}
     total_ms = float(step_ms.sum())
@@ -309,8 +318,24 @@ def run_gpu(args):
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
-    st = loop.read_state()
-    assert st["it"] == args.warmup + args.steps and not st["done"], st
+
+    # the reference's default configuration draws a random G per sample
+    # (deterministic_mode=False): same workload through the stochastic path
+    stoch = None
+    if args.stochastic_steps > 0:
+        sl, snames, sevs, _, _, _, _ = timed_loop(False, args.stochastic_steps, args.warmup)
+        s_ms = float(np.mean([e[0].elapsed_time(e[-1]) for e in sevs]))
+        if world > 1:
+            t = torch.tensor([s_ms], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            s_ms = float(t.item())
+        stoch = {"value": 1000.0 / s_ms, "unit": "iters/s", "ms_per_step": s_ms, "steps": args.stochastic_steps,
+                 "stage_ms": {n: float(np.mean([e[i].elapsed_time(e[i + 1]) for e in sevs]))
+                              for i, n in enumerate(snames)},
+                 "adjust_path": ("sample-plan gather (nnz %d, %d samples)" % (sl.plan_nnz, sl.n_samples))
+                 if sl.plan else "ray-driven scatter",
+                 "note": "deterministic_mode=False, g_sigma 0.1 (the reference default): per-sample Philox G"}
+        del sl
 
     w = work_counts(sc)
     if loop.occ is not None:
@@ -333,13 +358,26 @@ def run_gpu(args):
         reconstruct_channel(sc["images"], sc["cams"], sc["geom"], sc["hull"], cfg_e, render_cfg=sc["rcfg"],
                             masks=sc["masks"], bbox=sc["bbox"])  # warm (graph capture path, allocator)
         walls = []
-        for _ in range(3):  # median of three calls: one call is ~25 ms of host + device time
+        prof = None
+        if os.environ.get("FVR_E2E_PROFILE"):
+            import cProfile
+
+            prof = cProfile.Profile()
+        for _ in range(5):  # median of five calls: one call is ~30 ms of host + device time
             barrier()
+            if prof:
+                prof.enable()
             t0 = time.perf_counter()
             grid, trace = reconstruct_channel(sc["images"], sc["cams"], sc["geom"], sc["hull"], cfg_e,
                                               render_cfg=sc["rcfg"], masks=sc["masks"], bbox=sc["bbox"])
             barrier()
             walls.append(time.perf_counter() - t0)
+            if prof:
+                prof.disable()
+        if prof:
+            import pstats
+
+            pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(15)
         wall = float(np.median(walls))
         if world > 1:
             t = torch.tensor([wall], dtype=torch.float64, device=dev)
@@ -352,7 +390,7 @@ def run_gpu(args):
                "h2d_bytes_per_step": int(h2d / trace.iterations), "d2h_bytes_per_step": int(d2h / trace.iterations),
                "calls_ms": [1e3 * x for x in walls],
                "note": "reconstruct_channel() on host numpy inputs; H2D of frames/lattice/hull and D2H of the "
-                       "grid + trace inside the timed call, amortised over its iterations; median of 3 calls"}
+                       "grid + trace inside the timed call, amortised over its iterations; median of 5 calls"}
 
     out = {
         "metric": METRIC,
@@ -395,6 +433,7 @@ def run_gpu(args):
         "gpu_launches": int(launches),
         "adjust_path": "voxel-driven gather (CSR plan, nnz %d)" % loop.plan_nnz if loop.plan else "ray-driven scatter",
         "clocks": clocks,
+        "stochastic": stoch,
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -515,6 +554,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-iters", type=int, default=50)
+    ap.add_argument("--stochastic-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

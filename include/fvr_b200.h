@@ -228,6 +228,27 @@ int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int6
                          const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
                          double alpha_d, const int32_t* kp_map, int64_t* cursor, int32_t* entries,
                          void* stream);
+/* Stochastic mode (random G, reconstruct.py:193-201): the sample plan.
+ * Count: per-row entry counts (8 per in-hull sample) and per-ray in-hull
+ * sample counts.  Fill (ray_sid0 = exclusive scan of ray_samples): entries
+ * (sample id, W) unmerged, sample_meta[sid] = (ray index, march index k).
+ * Per iteration fvr_loop_weighted_residual writes rho[sid] = residual[ray] *
+ * G(seed, iteration, ray_id_base + ray, k) -- the Philox stream of
+ * fvr_loop_adjust -- and fvr_loop_gather runs over the sample plan with rho
+ * in place of the residual. */
+int fvr_sample_plan_count(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
+                          int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
+                          const uint8_t* inside_vox, fvr_grid_t grid, const int32_t* kp_map,
+                          int32_t* row_counts, int32_t* ray_samples, void* stream);
+int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
+                         int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
+                         const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
+                         double alpha_d, const int32_t* kp_map, const int64_t* ray_sid0,
+                         int64_t* cursor, int32_t* entries, int32_t* sample_meta, void* stream);
+int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, const int32_t* ray_list,
+                               int32_t bbox_w, int32_t bbox_h, const float* residual, uint64_t seed,
+                               double g_sigma, int64_t ray_id_base, float* rho,
+                               const fvr_loop_state_t* state, void* stream);
 /* Per iteration: row sums in 32.32 fixed point; with packed == NULL the
  * clamped update is applied in place (and the packed layout refreshed),
  * otherwise the sums go to packed (n_kp) for the multi-GPU all-reduce. */

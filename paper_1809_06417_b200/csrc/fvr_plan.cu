@@ -173,6 +173,83 @@ __global__ void __launch_bounds__(128) plan_fill_kernel(
     });
 }
 
+// ---- stochastic mode: the sample plan ---------------------------------------
+//
+// With random G (reconstruct.py:193-201) each in-hull sample carries its own
+// weight, so runs cannot be merged and the operator changes every iteration
+// -- but only through the per-sample factor G.  The sample plan stores A
+// unmerged, one entry (sample id, W) per (sample, corner); per iteration a
+// flat kernel writes rho[sid] = res[ray] * G(seed, it, ray, k) with the same
+// Philox key as the ray-driven scatter (fvr_adjust.cu), and the gather above
+// runs over the plan with rho in place of the residual.
+__global__ void __launch_bounds__(128) splan_count_kernel(
+    const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
+    int u0, int v0, int w, int h, const uint8_t* __restrict__ inside, Geom g,
+    const int32_t* __restrict__ kp_map, int32_t* __restrict__ counts, int32_t* __restrict__ ray_samples) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rays) return;
+    PlanRay pr;
+    plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
+    int ns = 0;
+    visit_inhull(pr.o, pr.d, g, inside, 1.0, [&](int, const double*, const int* c, double) {
+        const int base_kp = c[0] * g.sx + c[1] * g.sy + c[2];
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8)
+            atomicAdd(counts + kp_map[base_kp + (k8 >> 2) * g.sx + ((k8 >> 1) & 1) * g.sy + (k8 & 1)], 1);
+        ++ns;
+    });
+    ray_samples[r] = ns;
+}
+
+__global__ void __launch_bounds__(128) splan_fill_kernel(
+    const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
+    int u0, int v0, int w, int h, const uint8_t* __restrict__ inside, Geom g, double tau_keep,
+    double alpha_l, float alpha_d, const int32_t* __restrict__ kp_map, const long long* __restrict__ ray_sid0,
+    unsigned long long* __restrict__ cursor, int2* __restrict__ entries, int2* __restrict__ meta) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rays) return;
+    PlanRay pr;
+    plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
+    long long sid = ray_sid0[r];
+    const float edge = (float)g.edge;
+    visit_inhull(pr.o, pr.d, g, inside, tau_keep, [&](int k, const double* q, const int* c, double trans) {
+        meta[sid] = make_int2((int)r, k);
+        float e[3][2];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float f = (float)(q[a] - (double)c[a]);
+            e[a][0] = f * edge;
+            e[a][1] = (f - 1.0f) * edge;
+        }
+        const float base = (float)(alpha_l * trans);
+        const int base_kp = c[0] * g.sx + c[1] * g.sy + c[2];
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8) {
+            const int cx = k8 >> 2, cy = (k8 >> 1) & 1, cz = k8 & 1;
+            const float dist = sqrtf(fmaf(e[0][cx], e[0][cx], fmaf(e[1][cy], e[1][cy], e[2][cz] * e[2][cz])));
+            const float wgt = base * expf(-alpha_d * dist);
+            const unsigned long long pos = atomicAdd(cursor + kp_map[base_kp + cx * g.sx + cy * g.sy + cz], 1ull);
+            entries[pos] = make_int2((int)sid, __float_as_int(wgt));
+        }
+        ++sid;
+    });
+}
+
+__global__ void __launch_bounds__(256) weighted_residual_kernel(
+    const int2* __restrict__ meta, int64_t n_samples, const int32_t* __restrict__ ray_list, int w, int h,
+    const float* __restrict__ residual, uint64_t seed, float g_sigma, int64_t ray_id_base,
+    float* __restrict__ rho, const fvr_loop_state_t* __restrict__ state) {
+    if (state && state->done) return;
+    const uint32_t it = state ? (uint32_t)state->it : 0u;
+    for (int64_t sid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sid < n_samples;
+         sid += (int64_t)gridDim.x * blockDim.x) {
+        const int2 m = meta[sid];
+        const int32_t e = __ldg(ray_list + m.x);
+        const float res = __ldg(residual + (int64_t)(e >> 24) * w * h + (e & 0xFFFFFF));
+        rho[sid] = res * gauss_weight(seed, it, (uint32_t)(ray_id_base + m.x), (uint32_t)m.y, g_sigma);
+    }
+}
+
 // One group of G lanes per hull key point: delta = sum_e res[idx_e] * W_e
 // (32.32 fixed point, so any grouping of the sum gives the same bits).  Each
 // lane keeps U independent streaming loads in flight; a row is three
@@ -355,5 +432,51 @@ extern "C" int fvr_loop_update_packed(const int64_t* packed, int64_t n_kp, const
         reinterpret_cast<const long long*>(packed), n_kp, kp_index, values, layout, layout_kind, grid.nz + 1,
         grid.ny + 1, state);
     return check_launch("loop_update_packed");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_sample_plan_count(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
+                                     int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
+                                     const uint8_t* inside_vox, fvr_grid_t grid, const int32_t* kp_map,
+                                     int32_t* row_counts, int32_t* ray_samples, void* stream) {
+    FVR_TRY_BEGIN
+    if (int rc = check_grid(grid)) return rc;
+    if (n_rays == 0) return FVR_OK;
+    const Geom g = make_geom(grid);
+    splan_count_kernel<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, kp_map, row_counts, ray_samples);
+    return check_launch("sample_plan_count");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
+                                    int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
+                                    const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
+                                    double alpha_d, const int32_t* kp_map, const int64_t* ray_sid0,
+                                    int64_t* cursor, int32_t* entries, int32_t* sample_meta, void* stream) {
+    FVR_TRY_BEGIN
+    if (int rc = check_grid(grid)) return rc;
+    if (n_rays == 0) return FVR_OK;
+    const Geom g = make_geom(grid);
+    splan_fill_kernel<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d, kp_map,
+        reinterpret_cast<const long long*>(ray_sid0), reinterpret_cast<unsigned long long*>(cursor),
+        reinterpret_cast<int2*>(entries), reinterpret_cast<int2*>(sample_meta));
+    return check_launch("sample_plan_fill");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, const int32_t* ray_list,
+                                          int32_t bbox_w, int32_t bbox_h, const float* residual, uint64_t seed,
+                                          double g_sigma, int64_t ray_id_base, float* rho,
+                                          const fvr_loop_state_t* state, void* stream) {
+    FVR_TRY_BEGIN
+    if (n_samples == 0) return FVR_OK;
+    int64_t blocks = (n_samples + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    weighted_residual_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const int2*>(sample_meta), n_samples, ray_list, bbox_w, bbox_h, residual, seed,
+        (float)g_sigma, ray_id_base, rho, state);
+    return check_launch("loop_weighted_residual");
     FVR_TRY_END
 }

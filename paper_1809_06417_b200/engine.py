@@ -214,12 +214,18 @@ class ChannelLoop:
         self.trace = t.zeros(max(self.max_iters, 1), dtype=t.float64, device=dev)
         self.trace_vol = t.zeros(max(self.max_iters, 1), dtype=t.float64, device=dev) \
             if ground_truth is not None else None
-        # deterministic mode back-projects through the precomputed gather plan
-        self.plan = (not loop_cfg.stochastic and self.n_rays > 0 and self.n_kp > 0
-                     and os.environ.get("FVR_ADJUST") != "scatter")
+        # K-adjust as a voxel-driven gather over a precomputed plan: the merged
+        # operator A in deterministic mode, the per-sample plan (weights G
+        # applied through rho each iteration) in stochastic mode; the
+        # ray-driven scatter remains for plans that would not fit
+        self.plan = (self.n_rays > 0 and self.n_kp > 0 and os.environ.get("FVR_ADJUST") != "scatter")
+        self.sample_plan = self.plan and loop_cfg.stochastic
         self.plan_nnz = 0
+        self.n_samples = 0
+        self.rho = None
         if self.plan:
-            self._build_plan()
+            self.plan = self._build_plan()
+            self.sample_plan = self.plan and self.sample_plan
         # A CUDA graph only pays off when an iteration is launch-bound (a few
         # tens of microseconds of device work); for larger problems the host
         # enqueues 3-4 launches (~30 us) far ahead of the device, and graph
@@ -296,9 +302,14 @@ class ChannelLoop:
         return 2 if self.n_kp else 0
 
     # -- the back-projection plan (deterministic mode) --------------------------
-    def _build_plan(self) -> None:
-        """CSR of the fixed back-projection operator A (fvr_plan.cu): row = hull
-        key point, entry = (residual pixel, W).  Built once per call."""
+    # plans larger than this fall back to the ray-driven scatter
+    PLAN_MAX_BYTES = 48 << 30
+
+    def _build_plan(self) -> bool:
+        """CSR of the back-projection operator (fvr_plan.cu): row = hull key
+        point, entry = (residual pixel, W) merged per ray run in deterministic
+        mode, (in-hull sample id, W) unmerged in stochastic mode.  Built once
+        per call; returns False (scatter fallback) when it would not fit."""
         t = self.t
         dev = self.dev
         stream = _lib.stream_ptr()
@@ -306,28 +317,56 @@ class ChannelLoop:
         kp_map = t.full((n_lat,), -1, dtype=t.int32, device=dev)
         kp_map[self.kp[: self.n_kp].long()] = t.arange(self.n_kp, dtype=t.int32, device=dev)
         counts = t.zeros(self.n_kp, dtype=t.int32, device=dev)
-        _lib.call("fvr_adjust_plan_count", self.cams.data_ptr(), self.rays.data_ptr(), self.n_rays,
-                  self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb, self.inside.data_ptr(), self.grid,
-                  kp_map.data_ptr(), counts.data_ptr(), stream)
+        c = self.cfg
+        geo = (self.cams.data_ptr(), self.rays.data_ptr(), self.n_rays, self.bbox.u0, self.bbox.v0, self.w_bb,
+               self.h_bb, self.inside.data_ptr(), self.grid)
+        if self.sample_plan:
+            ray_samples = t.zeros(self.n_rays, dtype=t.int32, device=dev)
+            _lib.call("fvr_sample_plan_count", *geo, kp_map.data_ptr(), counts.data_ptr(), ray_samples.data_ptr(),
+                      stream)
+        else:
+            _lib.call("fvr_adjust_plan_count", *geo, kp_map.data_ptr(), counts.data_ptr(), stream)
         offsets = t.zeros(self.n_kp + 1, dtype=t.int64, device=dev)
         offsets[1:] = t.cumsum(counts.long(), 0)
         nnz = int(offsets[-1].item())
+        n_samples = int(ray_samples.long().sum().item()) if self.sample_plan else 0
+        free = t.cuda.mem_get_info(dev)[0]
+        need = 8 * nnz + 12 * n_samples
+        if need > min(self.PLAN_MAX_BYTES, free // 2) or n_samples >= 2 ** 31:
+            return False
         cursor = offsets[:-1].clone()
         entries = t.empty(max(2 * nnz, 2), dtype=t.int32, device=dev)
-        c = self.cfg
-        _lib.call("fvr_adjust_plan_fill", self.cams.data_ptr(), self.rays.data_ptr(), self.n_rays,
-                  self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb, self.inside.data_ptr(), self.grid,
-                  c.tau, c.alpha_l, c.alpha_d_eff, kp_map.data_ptr(), cursor.data_ptr(), entries.data_ptr(),
-                  stream)
+        if self.sample_plan:
+            sid0 = t.zeros(self.n_rays, dtype=t.int64, device=dev)
+            sid0[1:] = t.cumsum(ray_samples[:-1].long(), 0)
+            meta = t.empty(max(2 * n_samples, 2), dtype=t.int32, device=dev)
+            _lib.call("fvr_sample_plan_fill", *geo, c.tau, c.alpha_l, c.alpha_d_eff, kp_map.data_ptr(),
+                      sid0.data_ptr(), cursor.data_ptr(), entries.data_ptr(), meta.data_ptr(), stream)
+            self.sample_meta = meta
+            self.n_samples = n_samples
+            self.rho = t.zeros(max(n_samples, 1), dtype=t.float32, device=dev)
+        else:
+            _lib.call("fvr_adjust_plan_fill", *geo, c.tau, c.alpha_l, c.alpha_d_eff, kp_map.data_ptr(),
+                      cursor.data_ptr(), entries.data_ptr(), stream)
         self.plan_offsets = offsets
         self.plan_entries = entries
         self.plan_nnz = nnz
+        return True
+
+    def _weigh(self, stream):
+        """rho = residual * G per in-hull sample (stochastic sample plan)."""
+        c = self.cfg
+        _lib.call("fvr_loop_weighted_residual", self.sample_meta.data_ptr(), self.n_samples, self.rays.data_ptr(),
+                  self.w_bb, self.h_bb, self.residual.data_ptr(), c.seed & 0xFFFFFFFFFFFFFFFF, c.g_sigma,
+                  self.ray_base, self.rho.data_ptr(), self.state.data_ptr(), stream)
+        return 1
 
     def _gather(self, stream, packed: bool):
         if self.n_kp == 0:
             return 0
+        src = self.rho if self.sample_plan else self.residual
         _lib.call("fvr_loop_gather", self.plan_offsets.data_ptr(), self.plan_entries.data_ptr(), self.n_kp,
-                  self.residual.data_ptr(), self.kp.data_ptr(), self.values.data_ptr(), _lib.ptr(self.layout),
+                  src.data_ptr(), self.kp.data_ptr(), self.values.data_ptr(), _lib.ptr(self.layout),
                   self.layout_kind, self.grid, self.packed.data_ptr() if packed else None,
                   self.state.data_ptr(), stream)
         return 1
@@ -349,6 +388,8 @@ class ChannelLoop:
         """[(name, fn(stream) -> launches)] of one iteration, in order; the
         name 'decision' marks where the convergence rule has been evaluated."""
         s = [("render", self._render), ("volume", self._volume)]
+        if self.sample_plan:
+            s += [("weigh", self._weigh)]
         if self.plan:
             if self.sharded:
                 s += [("adjust", lambda st: self._gather(st, True)), ("allreduce", self._allreduce_packed),
