@@ -171,13 +171,18 @@ int fvr_occupancy(const float* values, int32_t n_channels, const uint8_t* force_
  * sq_partials buffer (n_views * blocks_per_view f64). */
 int fvr_loop_blocks_per_view(int32_t bbox_w, int32_t bbox_h);
 
-/* Render every bbox pixel of every view, residual = src - rec (f32, (V,h,w)),
- * per-block squared-residual sums (f64). cams is a device array. */
+/* Render every bbox pixel of every view, residual = src - rec (f32), and
+ * per-block squared-residual sums (f64). cams is a device array.
+ * n_channels (1, or 3 for the batched RGB loop, reconstruct.py:370-385)
+ * channels share the rays: src / residual are (n_channels, V, h, w), values
+ * and layout hold n_channels lattice planes, background[c] per channel,
+ * sq_partials[c * sq_stride + unit], and state points at n_channels loop
+ * states (the launch is a no-op once every channel is done). */
 int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0,
                     int32_t bbox_w, int32_t bbox_h, const float* src, const float* values,
-                    const float* layout, const uint8_t* occ, fvr_grid_t grid, fvr_render_params_t params, double background,
-                    const double* scat_dirs, float* residual, double* sq_partials,
-                    fvr_loop_state_t* state, void* stream);
+                    const float* layout, const uint8_t* occ, fvr_grid_t grid, fvr_render_params_t params,
+                    const double* background, int32_t n_channels, const double* scat_dirs, float* residual,
+                    double* sq_partials, int64_t sq_stride, fvr_loop_state_t* state, void* stream);
 
 /* Back-project the residual of every listed flame ray (ray_list entries are
  * view << 24 | (row_in_bbox * bbox_w + col_in_bbox)). stochastic != 0 draws
@@ -251,11 +256,14 @@ int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, co
                                const fvr_loop_state_t* state, void* stream);
 /* Per iteration: row sums in 32.32 fixed point; with packed == NULL the
  * clamped update is applied in place (and the packed layout refreshed),
- * otherwise the sums go to packed (n_kp) for the multi-GPU all-reduce. */
+ * otherwise the sums go to packed (n_channels, n_kp) for the multi-GPU
+ * all-reduce.  n_channels (1 or 3) share the plan: residual channel c starts
+ * at residual + c * res_stride, values / layout hold n_channels lattice
+ * planes and state n_channels loop states (converged channels are skipped). */
 int fvr_loop_gather(const int64_t* row_offsets, const int32_t* entries, int64_t n_kp,
-                    const float* residual, const int32_t* kp_index, float* values, float* layout,
-                    int32_t layout_kind, fvr_grid_t grid, int64_t* packed,
-                    const fvr_loop_state_t* state, void* stream);
+                    const float* residual, int64_t res_stride, int32_t n_channels,
+                    const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
+                    fvr_grid_t grid, int64_t* packed, const fvr_loop_state_t* state, void* stream);
 int fvr_loop_update_packed(const int64_t* packed, int64_t n_kp, const int32_t* kp_index,
                            float* values, float* layout, int32_t layout_kind, fvr_grid_t grid,
                            const fvr_loop_state_t* state, void* stream);

@@ -108,8 +108,8 @@ _SIGNATURES = {
     "fvr_loop_blocks_per_view": (c_int, [c_int32, c_int32]),
     "fvr_loop_render": (
         c_int,
-        [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _P, _P, _P, _P, _GRID, _PARAMS, c_double, _P,
-         _P, _P, _P, _P],
+        [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _P, _P, _P, _P, _GRID, _PARAMS, _P, c_int32, _P,
+         _P, _P, c_int64, _P, _P],
     ),
     "fvr_loop_adjust": (
         c_int,
@@ -133,7 +133,7 @@ _SIGNATURES = {
                                      c_double, c_double, _P, _P, _P, _P, _P, _P]),
     "fvr_loop_weighted_residual": (c_int, [_P, c_int64, _P, c_int32, c_int32, _P, c_uint64, c_double, c_int64,
                                            _P, _P, _P]),
-    "fvr_loop_gather": (c_int, [_P, _P, c_int64, _P, _P, _P, _P, c_int32, _GRID, _P, _P, _P]),
+    "fvr_loop_gather": (c_int, [_P, _P, c_int64, _P, c_int64, c_int32, _P, _P, _P, c_int32, _GRID, _P, _P, _P]),
     "fvr_loop_update_packed": (c_int, [_P, c_int64, _P, _P, _P, c_int32, _GRID, _P, _P]),
     "fvr_pack_correction": (c_int, [_P, _P, c_int64, _P, _P]),
     "fvr_unpack_correction": (c_int, [_P, _P, c_int64, _P, _P]),

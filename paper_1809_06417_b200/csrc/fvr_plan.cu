@@ -256,13 +256,24 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
 // dependent round trips (plan -> residual -> value), so the kernel is bound
 // by how many rows are in flight: G = 4 puts eight rows in each warp
 // (config 2: G=32 0.113 ms, 16 0.098, 8 0.094, 4 0.092, 2 0.122).
-template <bool PACKED, int G, int U>
+// NCH channels share the plan (A depends only on geometry and hull): each
+// entry is read once and multiplies NCH residuals (channel stride
+// res_stride); values / layout are NCH lattice planes, packed (NCH, n_rows),
+// state NCH loop states (a converged channel is left untouched).
+template <bool PACKED, int G, int U, int NCH>
 __global__ void __launch_bounds__(256) gather_kernel(
     const long long* __restrict__ row_off, const int2* __restrict__ entries, int64_t n_rows,
-    const float* __restrict__ residual, const int32_t* __restrict__ kp_index,
-    float* __restrict__ values, float* __restrict__ layout, int layout_kind, int sy, int ny1,
+    const float* __restrict__ residual, int64_t res_stride, const int32_t* __restrict__ kp_index,
+    float* __restrict__ values, int64_t plane, float* __restrict__ layout, int layout_kind, int sy, int ny1,
     long long* __restrict__ packed, const fvr_loop_state_t* __restrict__ state) {
-    if (state && state->done) return;
+    bool live[NCH];
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+        live[c] = !(state && state[c].done);
+        any = any || live[c];
+    }
+    if (!any) return;
     const int lane = threadIdx.x & 31;
     const int sub = lane & (G - 1);
     const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
@@ -270,7 +281,9 @@ __global__ void __launch_bounds__(256) gather_kernel(
     const int64_t n_groups = ((int64_t)gridDim.x * blockDim.x) / G;
     for (int64_t row = group; row < n_rows; row += n_groups) {
         const long long b = row_off[row], e = row_off[row + 1];
-        long long acc = 0;
+        long long acc[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) acc[c] = 0;
         // the plan is read once per iteration: evict-first, keep L2 for the residual
         for (long long base = b; base < e; base += G * U) {
             int2 en[U];
@@ -280,34 +293,43 @@ __global__ void __launch_bounds__(256) gather_kernel(
                 en[u] = i < e ? __ldcs(entries + i) : make_int2(0, 0);
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const float prod = __ldg(residual + en[u].x) * __int_as_float(en[u].y);
-                acc += __float2ll_rn(prod * 4294967296.0f);
-            }
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    const float prod = __ldg(residual + c * res_stride + en[u].x) * __int_as_float(en[u].y);
+                    acc[c] += __float2ll_rn(prod * 4294967296.0f);
+                }
         }
 #pragma unroll
-        for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(gmask, acc, off);
-        if (sub == 0) {
-            if (PACKED) {
-                packed[row] = acc;
-            } else if (acc != 0) {
-                const int64_t idx = kp_index[row];
-                const double nv = (double)values[idx] + (double)acc * kFixInv;
-                const float f = (float)(nv > -1.0 ? nv : -1.0);
-                values[idx] = f;
-                if (layout) {
-                    const float cpos = fmaxf(f, 0.f);
-                    const int z = (int)(idx % sy);
-                    if (layout_kind == 2) {
+        for (int c = 0; c < NCH; ++c)
 #pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            if (z >= k) layout[4 * (idx - k) + k] = cpos;
-                    } else {
-                        const int y = (int)((idx / sy) % ny1);
-                        layout[4 * idx] = cpos;
-                        if (z >= 1) layout[4 * (idx - 1) + 1] = cpos;
-                        if (y >= 1) layout[4 * (idx - sy) + 2] = cpos;
-                        if (y >= 1 && z >= 1) layout[4 * (idx - sy - 1) + 3] = cpos;
+            for (int off = G / 2; off > 0; off >>= 1) acc[c] += __shfl_xor_sync(gmask, acc[c], off);
+        if (sub == 0) {
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                if (PACKED) {
+                    packed[c * n_rows + row] = acc[c];
+                } else if (live[c] && acc[c] != 0) {
+                    const int64_t idx = kp_index[row];
+                    float* vals = values + c * plane;
+                    const double nv = (double)vals[idx] + (double)acc[c] * kFixInv;
+                    const float f = (float)(nv > -1.0 ? nv : -1.0);
+                    vals[idx] = f;
+                    if (layout) {
+                        float* lay = layout + 4 * c * plane;
+                        const float cpos = fmaxf(f, 0.f);
+                        const int z = (int)(idx % sy);
+                        if (layout_kind == 2) {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                if (z >= k) lay[4 * (idx - k) + k] = cpos;
+                        } else {
+                            const int y = (int)((idx / sy) % ny1);
+                            lay[4 * idx] = cpos;
+                            if (z >= 1) lay[4 * (idx - 1) + 1] = cpos;
+                            if (y >= 1) lay[4 * (idx - sy) + 2] = cpos;
+                            if (y >= 1 && z >= 1) lay[4 * (idx - sy - 1) + 3] = cpos;
+                        }
                     }
                 }
             }
@@ -382,11 +404,12 @@ extern "C" int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray
 }
 
 extern "C" int fvr_loop_gather(const int64_t* row_offsets, const int32_t* entries, int64_t n_kp,
-                               const float* residual, const int32_t* kp_index, float* values,
-                               float* layout, int32_t layout_kind, fvr_grid_t grid, int64_t* packed,
-                               const fvr_loop_state_t* state, void* stream) {
+                               const float* residual, int64_t res_stride, int32_t n_channels,
+                               const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
+                               fvr_grid_t grid, int64_t* packed, const fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
     if (n_kp == 0) return FVR_OK;
+    if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "the loop gathers 1 or 3 channels");
     static int group_lanes = 0;
     if (!group_lanes) {
         const char* e = getenv("FVR_GATHER_G");
@@ -396,25 +419,31 @@ extern "C" int fvr_loop_gather(const int64_t* row_offsets, const int32_t* entrie
     int64_t blocks = (n_kp * group_lanes + 255) / 256;
     if (blocks > 148 * 64) blocks = 148 * 64;
     const int sy = grid.nz + 1, ny1 = grid.ny + 1;
+    const int64_t plane = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
     cudaStream_t st = (cudaStream_t)stream;
     const auto* ro = reinterpret_cast<const long long*>(row_offsets);
     const auto* en = reinterpret_cast<const int2*>(entries);
     long long* pk = reinterpret_cast<long long*>(packed);
-#define FVR_GATHER(GL, UL)                                                                                         \
-    do {                                                                                                         \
-        if (packed)                                                                                              \
-            gather_kernel<true, GL, UL><<<(unsigned)blocks, 256, 0, st>>>(ro, en, n_kp, residual, kp_index, values,  \
-                                                                         layout, layout_kind, sy, ny1, pk, state); \
-        else                                                                                                     \
-            gather_kernel<false, GL, UL><<<(unsigned)blocks, 256, 0, st>>>(ro, en, n_kp, residual, kp_index, values, \
-                                                                          layout, layout_kind, sy, ny1, nullptr,  \
-                                                                          state);                                 \
+#define FVR_GATHER(GL, UL, C)                                                                                  \
+    do {                                                                                                     \
+        if (packed)                                                                                          \
+            gather_kernel<true, GL, UL, C><<<(unsigned)blocks, 256, 0, st>>>(                                 \
+                ro, en, n_kp, residual, res_stride, kp_index, values, plane, layout, layout_kind, sy, ny1, pk, \
+                state);                                                                                      \
+        else                                                                                                 \
+            gather_kernel<false, GL, UL, C><<<(unsigned)blocks, 256, 0, st>>>(                                \
+                ro, en, n_kp, residual, res_stride, kp_index, values, plane, layout, layout_kind, sy, ny1,    \
+                nullptr, state);                                                                             \
     } while (0)
-    switch (group_lanes) {
-        case 8: FVR_GATHER(8, 16); break;
-        case 16: FVR_GATHER(16, 8); break;
-        case 32: FVR_GATHER(32, 4); break;
-        default: FVR_GATHER(4, 32); break;
+    if (n_channels == 3) {
+        FVR_GATHER(4, 16, 3);
+    } else {
+        switch (group_lanes) {
+            case 8: FVR_GATHER(8, 16, 1); break;
+            case 16: FVR_GATHER(16, 8, 1); break;
+            case 32: FVR_GATHER(32, 4, 1); break;
+            default: FVR_GATHER(4, 32, 1); break;
+        }
     }
 #undef FVR_GATHER
     return check_launch("loop_gather");

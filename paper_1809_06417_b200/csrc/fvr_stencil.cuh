@@ -163,6 +163,9 @@ __device__ __forceinline__ uint32_t inbox_mask(const double p[3], const Geom& g,
 #ifndef FVR_Q3_TABLE
 #define FVR_Q3_TABLE 0
 #endif
+#ifndef FVR_OMEGA
+#define FVR_OMEGA 1
+#endif
 #ifndef FVR_MOMENT_PACKED
 #define FVR_MOMENT_PACKED 1
 #endif
@@ -498,6 +501,141 @@ __device__ __forceinline__ void moment_eval2(const float4 r[9], float dx, float 
     }
 #endif
     scat = s;
+}
+
+// ---- stencil weights: the evaluation as one dot product per channel --------
+//
+// Both sums are linear in the stencil: e = sum_j v_j hat_j(delta) (the
+// trilinear hat weights) and the direction sum S = sum_k V[k] M[k] =
+// sum_j v_j W_j with W = (T^T)^{(x)3} M, T the per-axis basis transform of
+// moment_eval.  So  sigma_a e + kappa S = kappa * sum_j v_j Omega_j  with
+// Omega = W + (sigma_a / kappa) hat, computed once per sample and shared by
+// every channel; a channel then costs its nine stencil loads and one
+// 27-term dot (9 FFMA2 on the (z-1, z) register pairs + 9 FFMA).
+// om01[l] = (Omega[l][z-1], Omega[l][z]), om2[l] = Omega[l][z+1], l = jx*3 + jy.
+__device__ __forceinline__ void moment_omega(float dx, float dy, float dz, const float* __restrict__ thr,
+                                             const float4* q1, const float4* q2, float ek, float2 om01[9],
+                                             float om2[9]) {
+    const float hx = 0.5f * dx, hy = 0.5f * dy, hz = 0.5f * dz;
+    const int ix = split_index_c(0, thr, -dx), iy = split_index_c(1, thr + kScatDirs, -dy),
+              iz = split_index_c(2, thr + 2 * kScatDirs, -dz);
+    // moments per (kx, ky): M01 = (M[k,0], M[k,1]) = q_A[P >> 1], M2 = M[k,2] = q_{A|z}[P >> 1].y
+    float2 M01[9];
+    float M2[9];
+    auto put = [&](int A, const float2 q[4]) {
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+            for (int ky = 0; ky < 3; ++ky) {
+                const int Axy = ((kx == 2) << 2) | ((ky == 2) << 1);
+                const int pi = ((kx != 0) << 1) | (ky != 0);
+                if (Axy == A) M01[kx * 3 + ky] = q[pi];
+                if ((Axy | 1) == A) M2[kx * 3 + ky] = q[pi].y;
+            }
+    };
+    {
+        float2 q[4] = {make_float2(c_q0[0], c_q0[1]), make_float2(c_q0[2], c_q0[3]),
+                       make_float2(c_q0[4], c_q0[5]), make_float2(c_q0[6], c_q0[7])};
+        zeta8(q, hx, hy, hz);
+        put(0, q);
+    }
+    {
+        float2 q[4];
+        load_q8x2(q1, 0 * kSplits + ix, q);
+        zeta8(q, hx, hy, hz);
+        put(4, q);
+        load_q8x2(q1, 1 * kSplits + iy, q);
+        zeta8(q, hx, hy, hz);
+        put(2, q);
+        load_q8x2(q1, 2 * kSplits + iz, q);
+        zeta8(q, hx, hy, hz);
+        put(1, q);
+        load_q8x2(q2, (0 * kSplits + ix) * kSplits + iy, q);
+        zeta8(q, hx, hy, hz);
+        put(6, q);
+        load_q8x2(q2, (1 * kSplits + ix) * kSplits + iz, q);
+        zeta8(q, hx, hy, hz);
+        put(5, q);
+        load_q8x2(q2, (2 * kSplits + iy) * kSplits + iz, q);
+        zeta8(q, hx, hy, hz);
+        put(3, q);
+    }
+    {
+        // all-|x| moment, directions s and s + 16 paired
+        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const float2 DX = bcast2(dx), DY = bcast2(dy), DZ = bcast2(dz);
+#pragma unroll
+        for (int d = 0; d < kScatDirs / 2; ++d) {
+            const float2 x = __fadd2_rn(DX, c_half_dir2[0][d]);
+            const float2 y = __fadd2_rn(DY, c_half_dir2[1][d]);
+            const float2 z = __fadd2_rn(DZ, c_half_dir2[2][d]);
+            float2 xy = __fmul2_rn(x, y);
+            xy.x = fabsf(xy.x);
+            xy.y = fabsf(xy.y);
+            acc[d & 1] = __ffma2_rn(xy, make_float2(fabsf(z.x), fabsf(z.y)), acc[d & 1]);
+        }
+        const float2 a2 = __fadd2_rn(acc[0], acc[1]);
+        M2[8] = 0.125f * (a2.x + a2.y);
+    }
+    // T^T along z (inside the lines): (M0, M1, M2) -> (M2 - M1, M0 - 2 M2, M1 + M2)
+    float2 W01[9];
+    float W2[9];
+#pragma unroll
+    for (int l = 0; l < 9; ++l) {
+        const float m0 = M01[l].x, m1 = M01[l].y, m2 = M2[l];
+        W01[l] = make_float2(m2 - m1, fmaf(-2.f, m2, m0));
+        W2[l] = m1 + m2;
+    }
+    // along y (l = kx*3 + ky), then along x, on the z-pairs
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx) {
+        const float2 a0 = W01[kx * 3], a1 = W01[kx * 3 + 1], a2 = W01[kx * 3 + 2];
+        const float b0 = W2[kx * 3], b1 = W2[kx * 3 + 1], b2 = W2[kx * 3 + 2];
+        W01[kx * 3] = __fadd2_rn(a2, make_float2(-a1.x, -a1.y));
+        W01[kx * 3 + 1] = __ffma2_rn(bcast2(-2.f), a2, a0);
+        W01[kx * 3 + 2] = __fadd2_rn(a1, a2);
+        W2[kx * 3] = b2 - b1;
+        W2[kx * 3 + 1] = fmaf(-2.f, b2, b0);
+        W2[kx * 3 + 2] = b1 + b2;
+    }
+#pragma unroll
+    for (int jy = 0; jy < 3; ++jy) {
+        const float2 a0 = W01[jy], a1 = W01[3 + jy], a2 = W01[6 + jy];
+        const float b0 = W2[jy], b1 = W2[3 + jy], b2 = W2[6 + jy];
+        W01[jy] = __fadd2_rn(a2, make_float2(-a1.x, -a1.y));
+        W01[3 + jy] = __ffma2_rn(bcast2(-2.f), a2, a0);
+        W01[6 + jy] = __fadd2_rn(a1, a2);
+        W2[jy] = b2 - b1;
+        W2[3 + jy] = fmaf(-2.f, b2, b0);
+        W2[6 + jy] = b1 + b2;
+    }
+    // hat weights (max(-x,0), 1 - |x|, max(x,0)) per axis; sigma_a/kappa folded into x
+    const float hatx[3] = {ek * fmaxf(-dx, 0.f), ek * (1.f - fabsf(dx)), ek * fmaxf(dx, 0.f)};
+    const float haty[3] = {fmaxf(-dy, 0.f), 1.f - fabsf(dy), fmaxf(dy, 0.f)};
+    const float2 hz01 = make_float2(fmaxf(-dz, 0.f), 1.f - fabsf(dz));
+    const float hz2 = fmaxf(dz, 0.f);
+#pragma unroll
+    for (int jx = 0; jx < 3; ++jx)
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) {
+            const int l = jx * 3 + jy;
+            const float hxy = hatx[jx] * haty[jy];
+            om01[l] = __ffma2_rn(bcast2(hxy), hz01, W01[l]);
+            om2[l] = fmaf(hxy, hz2, W2[l]);
+        }
+}
+
+// sum_j v_j Omega_j for one channel's stencil (r as in load_stencil_z4_raw)
+__device__ __forceinline__ float omega_dot(const float4 r[9], const float2 om01[9], const float om2[9]) {
+    float2 a[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    float b = 0.f;
+#pragma unroll
+    for (int l = 0; l < 9; ++l) {
+        a[l & 1] = __ffma2_rn(make_float2(r[l].x, r[l].y), om01[l], a[l & 1]);
+        b = fmaf(r[l].z, om2[l], b);
+    }
+    const float2 s = __fadd2_rn(a[0], a[1]);
+    return s.x + s.y + b;
 }
 
 }  // namespace fvr

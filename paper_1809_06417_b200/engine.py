@@ -78,27 +78,36 @@ def exchange(comm, sq, vol, v_begin: int, v_end: int, rows_per_view: int, rank: 
     (the rank of its view; rank 0 for the replicated volume term): all other
     ranks contribute the bit pattern of +0.0, i.e. integer 0, so the integer
     sum reproduces the owner's bits exactly.  ``sq``/``vol`` are f64 views into
-    ``comm``; works on CUDA (NCCL) and CPU (gloo) tensors alike.
+    ``comm`` (``sq`` may carry a leading channel axis); works on CUDA (NCCL)
+    and CPU (gloo) tensors alike.
     """
     import torch.distributed as dist
 
-    sq[: v_begin * rows_per_view].zero_()
-    sq[v_end * rows_per_view:].zero_()
+    sq[..., : v_begin * rows_per_view].zero_()
+    sq[..., v_end * rows_per_view:].zero_()
     if vol is not None and rank != 0:
         vol.zero_()
     dist.all_reduce(comm, op=dist.ReduceOp.SUM, group=group)
 
 
 class ChannelLoop:
-    """Owns the device buffers of one reconstruct_channel call."""
+    """Owns the device buffers of one reconstruct_channel call -- or of the
+    three channels of reconstruct_color batched into one loop (values of
+    shape (3, *lattice), src (3, V, h, w), backgrounds per channel): the
+    channels share rays, hull, plan and launches, and each keeps its own
+    convergence state (a converged channel is frozen while the others go on).
+    """
 
     def __init__(self, cameras, grid_geom, values, src_blocks, masks, bbox, inside, kp_mask,
                  render_cfg, loop_cfg: LoopConfig, max_iters: int, ground_truth=None,
-                 background: float = 0.0, use_graph: bool = True):
+                 background=0.0, use_graph: bool = True, n_channels: int = 1):
         t = _lib.torch()
         self.t = t
         self.dev = _lib.device()
         self.rank, self.world, self.sharded = _world()
+        if n_channels not in (1, 3):
+            raise ValueError("the loop runs 1 or 3 channels")
+        C = self.nch = int(n_channels)
         V = len(cameras)
         self.n_views = V
         self.v_begin, self.v_end = shard_views(V, self.rank, self.world)
@@ -112,34 +121,41 @@ class ChannelLoop:
 
         # geometry and inputs
         self.cams = _lib.cameras_tensor([cameras[v] for v in local], dev) if local else None
-        if t.is_tensor(src_blocks):  # (V, h, w) f32 device crops (DeviceFrames)
-            self.src = src_blocks[self.v_begin:self.v_end].contiguous() if local else \
-                t.zeros((1, 1, 1), dtype=t.float32, device=dev)
+        if t.is_tensor(src_blocks):  # ([C,] V, h, w) f32 device crops (DeviceFrames)
+            blk = src_blocks if src_blocks.dim() == 4 else src_blocks.unsqueeze(0)
+            self.src = blk[:, self.v_begin:self.v_end].contiguous() if local else \
+                t.zeros((C, 1, 1, 1), dtype=t.float32, device=dev)
         else:
-            self.src = t.from_numpy(np.ascontiguousarray(np.stack([src_blocks[v] for v in local]) if local
-                                                         else np.zeros((1, 1, 1), np.float32))).to(dev)
+            arr = np.stack([src_blocks[v] for v in local]) if local else np.zeros((1, 1, 1), np.float32)
+            arr = arr[None] if C == 1 else np.moveaxis(arr, -1, 0)
+            self.src = t.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to(dev)
+        if self.src.shape[0] != C:
+            raise ValueError("src channels do not match n_channels")
         shape = (grid_geom.nx + 1, grid_geom.ny + 1, grid_geom.nz + 1)
+        self.shape = shape
         self.inside = t.from_numpy(np.ascontiguousarray(inside, dtype=np.uint8)).to(dev)
+        self.values = t.empty((C,) + shape, dtype=t.float32, device=dev)
+        if values is not None:
+            self.values.copy_(t.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).reshape((C,) + shape))
         if kp_mask is None or values is None:
             # hull key points (and the initial lattice when values is None)
             # derived on the device from the inside voxels
             kp_dev = t.empty(shape, dtype=t.uint8, device=dev)
-            self.values = t.empty(shape, dtype=t.float32, device=dev) if values is None else \
-                t.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(dev)
             _lib.call("fvr_hull_keypoints", self.inside.data_ptr(), self.grid, kp_dev.data_ptr(),
                       self.values.data_ptr() if values is None else None, _lib.stream_ptr())
+            if values is None and C > 1:
+                self.values[1:].copy_(self.values[0:1].expand((C - 1,) + shape))
             if kp_mask is not None:
                 kp_dev = t.from_numpy(np.ascontiguousarray(kp_mask, dtype=np.uint8)).to(dev)
             kp_t = t.nonzero(kp_dev.reshape(-1)).reshape(-1).to(t.int32)
             self.n_kp = int(kp_t.numel())
             self.kp = kp_t if self.n_kp else t.zeros(1, dtype=t.int32, device=dev)
         else:
-            self.values = t.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(dev)
             kp_dev = t.from_numpy(np.ascontiguousarray(kp_mask, dtype=np.uint8)).to(dev)
             kp_idx = np.flatnonzero(kp_mask.ravel()).astype(np.int32)
             self.n_kp = int(kp_idx.size)
             self.kp = t.from_numpy(kp_idx if kp_idx.size else np.zeros(1, np.int32)).to(dev)
-        self.accum = t.zeros(shape, dtype=t.int64, device=dev)
+        self.accum = None  # scatter path only
 
         # flame rays of the local views, row-major per view (reconstruct.py:144-149)
         if t.is_tensor(masks):  # (V, H, W) u8 device masks: compact on the device
@@ -178,41 +194,44 @@ class ChannelLoop:
             self.scat = None
             n_scat = 1
         self.params = _lib.render_params(render_cfg, self.scattering, n_scat, 0.0, grid_geom.edge)
-        self.background = float(background)
+        bg = np.broadcast_to(np.asarray(background, dtype=np.float64).reshape(-1), (C,))
+        self.background = (ctypes.c_double * C)(*[float(x) for x in bg])
         # packed copy of max(v, 0) read by the fast render path, kept in sync by K-update
         self.layout_kind = _lib.layout_kind(self.params, self.grid)
         self.layout = None
         if self.layout_kind:
-            self.layout = t.empty(shape + (4,), dtype=t.float32, device=dev)
-            _lib.call("fvr_pack_layout", self.values.data_ptr(), 1, self.grid, self.layout_kind,
+            self.layout = t.empty((C,) + shape + (4,), dtype=t.float32, device=dev)
+            _lib.call("fvr_pack_layout", self.values.data_ptr(), C, self.grid, self.layout_kind,
                       self.layout.data_ptr(), _lib.stream_ptr())
         # empty-space occupancy: hull key points (their values change) plus any
-        # positive initial value; key points outside the hull are never written,
-        # so the map stays valid for the whole loop
+        # positive initial value of any channel; key points outside the hull are
+        # never written, so the map stays valid for the whole loop
         self.occ = None
         if self.layout_kind and os.environ.get("FVR_NO_SKIP") != "1":
             self.occ = t.empty(shape, dtype=t.uint8, device=dev)
-            _lib.call("fvr_occupancy", self.values.data_ptr(), 1, kp_dev.data_ptr(), self.grid,
+            _lib.call("fvr_occupancy", self.values.data_ptr(), C, kp_dev.data_ptr(), self.grid,
                       self.occ.data_ptr(), _lib.stream_ptr())
 
         # work buffers
         self.bpv = int(_lib.load().fvr_loop_blocks_per_view(self.w_bb, self.h_bb))
-        self.residual = t.zeros((max(len(local), 1), self.h_bb, self.w_bb), dtype=t.float32, device=dev)
+        self.residual = t.zeros((C, max(len(local), 1), self.h_bb, self.w_bb), dtype=t.float32, device=dev)
         self.n_sq = V * self.bpv
-        # [packed correction (n_kp) | sq partials (V*bpv) | vol partials] in one int64 buffer
+        # [packed correction (C, n_kp) | sq partials (C, V*bpv) | vol partials (C, n_vol)] in one i64 buffer
         nvb = ctypes.c_int32(0)
         _lib.call("fvr_loop_volume_sq", None, None, None, self.n_kp, None, ctypes.byref(nvb), None, None)
         self.n_vol = int(nvb.value) if ground_truth is not None else 0
-        self.comm = t.zeros(self.n_kp + self.n_sq + self.n_vol + 1, dtype=t.int64, device=dev)
-        self.sq = self.comm[self.n_kp:self.n_kp + self.n_sq].view(t.float64)
-        self.vol = self.comm[self.n_kp + self.n_sq:self.n_kp + self.n_sq + self.n_vol].view(t.float64) \
-            if self.n_vol else None
-        self.packed = self.comm[: self.n_kp]
-        self.truth = (t.from_numpy(np.ascontiguousarray(ground_truth, dtype=np.float32)).to(dev)
-                      if ground_truth is not None else None)
-        self.state = t.zeros(8, dtype=t.int32, device=dev)  # fvr_loop_state_t (32 B)
-        self.trace = t.zeros(max(self.max_iters, 1), dtype=t.float64, device=dev)
-        self.trace_vol = t.zeros(max(self.max_iters, 1), dtype=t.float64, device=dev) \
+        a, b = C * self.n_kp, C * (self.n_kp + self.n_sq)
+        self.comm = t.zeros(C * (self.n_kp + self.n_sq + self.n_vol) + 1, dtype=t.int64, device=dev)
+        self.packed = self.comm[:a].view(C, self.n_kp)
+        self.sq = self.comm[a:b].view(t.float64).view(C, self.n_sq)
+        self.vol = self.comm[b:b + C * self.n_vol].view(t.float64).view(C, self.n_vol) if self.n_vol else None
+        self.truth = None
+        if ground_truth is not None:
+            gt = np.ascontiguousarray(ground_truth, dtype=np.float32).reshape((C,) + shape)
+            self.truth = t.from_numpy(gt).to(dev)
+        self.state = t.zeros((C, 8), dtype=t.int32, device=dev)  # fvr_loop_state_t (32 B) per channel
+        self.trace = t.zeros((C, max(self.max_iters, 1)), dtype=t.float64, device=dev)
+        self.trace_vol = t.zeros((C, max(self.max_iters, 1)), dtype=t.float64, device=dev) \
             if ground_truth is not None else None
         # K-adjust as a voxel-driven gather over a precomputed plan: the merged
         # operator A in deterministic mode, the per-sample plan (weights G
@@ -226,6 +245,8 @@ class ChannelLoop:
         if self.plan:
             self.plan = self._build_plan()
             self.sample_plan = self.plan and self.sample_plan
+        if not self.plan:
+            self.accum = t.zeros((C,) + shape, dtype=t.int64, device=dev)
         # A CUDA graph only pays off when an iteration is launch-bound (a few
         # tens of microseconds of device work); for larger problems the host
         # enqueues 3-4 launches (~30 us) far ahead of the device, and graph
@@ -240,12 +261,12 @@ class ChannelLoop:
     def _render(self, stream):
         if self.v_end <= self.v_begin:
             return 0
-        sq_local = self.sq[self.v_begin * self.bpv:]
         _lib.call(
             "fvr_loop_render", self.cams.data_ptr(), self.v_end - self.v_begin, self.bbox.u0,
             self.bbox.v0, self.w_bb, self.h_bb, self.src.data_ptr(), self.values.data_ptr(),
-            _lib.ptr(self.layout), _lib.ptr(self.occ), self.grid, self.params, self.background, _lib.ptr(self.scat), self.residual.data_ptr(),
-            sq_local.data_ptr(), self.state.data_ptr(), stream,
+            _lib.ptr(self.layout), _lib.ptr(self.occ), self.grid, self.params, self.background, self.nch,
+            _lib.ptr(self.scat), self.residual.data_ptr(), self.sq[0, self.v_begin * self.bpv:].data_ptr(),
+            self.n_sq, self.state.data_ptr(), stream,
         )
         return 1
 
@@ -253,53 +274,59 @@ class ChannelLoop:
         if self.n_rays == 0:
             return 0
         c = self.cfg
-        _lib.call(
-            "fvr_loop_adjust", self.cams.data_ptr(), self.rays.data_ptr(), self.n_rays,
-            self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb, self.residual.data_ptr(),
-            self.inside.data_ptr(), self.grid, c.tau, c.alpha_l, c.alpha_d_eff,
-            1 if c.stochastic else 0, c.g_sigma, c.seed & 0xFFFFFFFFFFFFFFFF, self.ray_base,
-            self.accum.data_ptr(), self.state.data_ptr(), stream,
-        )
-        return 1
+        for ch in range(self.nch):
+            _lib.call(
+                "fvr_loop_adjust", self.cams.data_ptr(), self.rays.data_ptr(), self.n_rays,
+                self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb, self.residual[ch].data_ptr(),
+                self.inside.data_ptr(), self.grid, c.tau, c.alpha_l, c.alpha_d_eff,
+                1 if c.stochastic else 0, c.g_sigma, c.seed & 0xFFFFFFFFFFFFFFFF, self.ray_base,
+                self.accum[ch].data_ptr(), self.state[ch].data_ptr(), stream,
+            )
+        return self.nch
 
     def _volume(self, stream):
         if self.truth is None:
             return 0
         nvb = ctypes.c_int32(0)
-        _lib.call(
-            "fvr_loop_volume_sq", self.values.data_ptr(), self.truth.data_ptr(), self.kp.data_ptr(),
-            self.n_kp, self.vol.data_ptr(), ctypes.byref(nvb), self.state.data_ptr(), stream,
-        )
-        return 1
+        for ch in range(self.nch):
+            _lib.call(
+                "fvr_loop_volume_sq", self.values[ch].data_ptr(), self.truth[ch].data_ptr(), self.kp.data_ptr(),
+                self.n_kp, self.vol[ch].data_ptr(), ctypes.byref(nvb), self.state[ch].data_ptr(), stream,
+            )
+        return self.nch
 
     def _finalize(self, stream):
         pix = self.w_bb * self.h_bb
-        _lib.call(
-            "fvr_loop_finalize", self.sq.data_ptr(), self.n_views, self.bpv, pix,
-            _lib.ptr(self.vol), self.n_vol, self.n_kp, self.cfg.converge_eps,
-            self.trace.data_ptr(), _lib.ptr(self.trace_vol), self.state.data_ptr(), stream,
-        )
-        return 1
+        for ch in range(self.nch):
+            _lib.call(
+                "fvr_loop_finalize", self.sq[ch].data_ptr(), self.n_views, self.bpv, pix,
+                _lib.ptr(None if self.vol is None else self.vol[ch]), self.n_vol, self.n_kp, self.cfg.converge_eps,
+                self.trace[ch].data_ptr(), _lib.ptr(None if self.trace_vol is None else self.trace_vol[ch]),
+                self.state[ch].data_ptr(), stream,
+            )
+        return self.nch
 
     def _update(self, stream):
         if self.n_kp == 0:
             return 0
-        _lib.call(
-            "fvr_loop_update", self.values.data_ptr(), self.accum.data_ptr(), self.kp.data_ptr(),
-            self.n_kp, _lib.ptr(self.layout), self.layout_kind, self.grid, self.state.data_ptr(), stream,
-        )
-        return 1
+        for ch in range(self.nch):
+            _lib.call(
+                "fvr_loop_update", self.values[ch].data_ptr(), self.accum[ch].data_ptr(), self.kp.data_ptr(),
+                self.n_kp, _lib.ptr(None if self.layout is None else self.layout[ch]), self.layout_kind, self.grid,
+                self.state[ch].data_ptr(), stream,
+            )
+        return self.nch
 
     def _allreduce(self, stream):
         """Sum corrections and RMSE partials over ranks (exact: int64)."""
-        if self.n_kp:
-            _lib.call("fvr_pack_correction", self.accum.data_ptr(), self.kp.data_ptr(), self.n_kp,
-                      self.packed.data_ptr(), stream)
+        for ch in range(self.nch if self.n_kp else 0):
+            _lib.call("fvr_pack_correction", self.accum[ch].data_ptr(), self.kp.data_ptr(), self.n_kp,
+                      self.packed[ch].data_ptr(), stream)
         exchange(self.comm, self.sq, self.vol, self.v_begin, self.v_end, self.bpv, self.rank)
-        if self.n_kp:
-            _lib.call("fvr_unpack_correction", self.packed.data_ptr(), self.kp.data_ptr(), self.n_kp,
-                      self.accum.data_ptr(), stream)
-        return 2 if self.n_kp else 0
+        for ch in range(self.nch if self.n_kp else 0):
+            _lib.call("fvr_unpack_correction", self.packed[ch].data_ptr(), self.kp.data_ptr(), self.n_kp,
+                      self.accum[ch].data_ptr(), stream)
+        return 2 * self.nch if self.n_kp else 0
 
     # -- the back-projection plan (deterministic mode) --------------------------
     # plans larger than this fall back to the ray-driven scatter
@@ -313,7 +340,7 @@ class ChannelLoop:
         t = self.t
         dev = self.dev
         stream = _lib.stream_ptr()
-        n_lat = self.values.numel()
+        n_lat = int(np.prod(self.shape))
         kp_map = t.full((n_lat,), -1, dtype=t.int32, device=dev)
         kp_map[self.kp[: self.n_kp].long()] = t.arange(self.n_kp, dtype=t.int32, device=dev)
         counts = t.zeros(self.n_kp, dtype=t.int32, device=dev)
@@ -344,7 +371,7 @@ class ChannelLoop:
                       sid0.data_ptr(), cursor.data_ptr(), entries.data_ptr(), meta.data_ptr(), stream)
             self.sample_meta = meta
             self.n_samples = n_samples
-            self.rho = t.zeros(max(n_samples, 1), dtype=t.float32, device=dev)
+            self.rho = t.zeros((self.nch, max(n_samples, 1)), dtype=t.float32, device=dev)
         else:
             _lib.call("fvr_adjust_plan_fill", *geo, c.tau, c.alpha_l, c.alpha_d_eff, kp_map.data_ptr(),
                       cursor.data_ptr(), entries.data_ptr(), stream)
@@ -356,28 +383,31 @@ class ChannelLoop:
     def _weigh(self, stream):
         """rho = residual * G per in-hull sample (stochastic sample plan)."""
         c = self.cfg
-        _lib.call("fvr_loop_weighted_residual", self.sample_meta.data_ptr(), self.n_samples, self.rays.data_ptr(),
-                  self.w_bb, self.h_bb, self.residual.data_ptr(), c.seed & 0xFFFFFFFFFFFFFFFF, c.g_sigma,
-                  self.ray_base, self.rho.data_ptr(), self.state.data_ptr(), stream)
-        return 1
+        for ch in range(self.nch):
+            _lib.call("fvr_loop_weighted_residual", self.sample_meta.data_ptr(), self.n_samples,
+                      self.rays.data_ptr(), self.w_bb, self.h_bb, self.residual[ch].data_ptr(),
+                      c.seed & 0xFFFFFFFFFFFFFFFF, c.g_sigma, self.ray_base, self.rho[ch].data_ptr(),
+                      self.state[ch].data_ptr(), stream)
+        return self.nch
 
     def _gather(self, stream, packed: bool):
         if self.n_kp == 0:
             return 0
         src = self.rho if self.sample_plan else self.residual
         _lib.call("fvr_loop_gather", self.plan_offsets.data_ptr(), self.plan_entries.data_ptr(), self.n_kp,
-                  src.data_ptr(), self.kp.data_ptr(), self.values.data_ptr(), _lib.ptr(self.layout),
-                  self.layout_kind, self.grid, self.packed.data_ptr() if packed else None,
+                  src.data_ptr(), src[0].numel(), self.nch, self.kp.data_ptr(), self.values.data_ptr(),
+                  _lib.ptr(self.layout), self.layout_kind, self.grid, self.packed.data_ptr() if packed else None,
                   self.state.data_ptr(), stream)
         return 1
 
     def _update_packed(self, stream):
         if self.n_kp == 0:
             return 0
-        _lib.call("fvr_loop_update_packed", self.packed.data_ptr(), self.n_kp, self.kp.data_ptr(),
-                  self.values.data_ptr(), _lib.ptr(self.layout), self.layout_kind, self.grid,
-                  self.state.data_ptr(), stream)
-        return 1
+        for ch in range(self.nch):
+            _lib.call("fvr_loop_update_packed", self.packed[ch].data_ptr(), self.n_kp, self.kp.data_ptr(),
+                      self.values[ch].data_ptr(), _lib.ptr(None if self.layout is None else self.layout[ch]),
+                      self.layout_kind, self.grid, self.state[ch].data_ptr(), stream)
+        return self.nch
 
     def _allreduce_packed(self, stream):
         """All-reduce [packed | sq | vol] once the gather filled ``packed``."""
@@ -450,25 +480,35 @@ class ChannelLoop:
     # -- the loop ----------------------------------------------------------------
     def reset_state(self) -> None:
         self.state.zero_()
-        self.accum.zero_()
+        if self.accum is not None:
+            self.accum.zero_()
+
+    def read_states(self) -> list[dict]:
+        out = []
+        for s in self.state.cpu().numpy():
+            prev = s[4:6].copy().view(np.float64)[0]
+            out.append({"it": int(s[0]), "done": int(s[1]), "converged": int(s[2]), "prev_rmse": float(prev)})
+        return out
 
     def read_state(self) -> dict:
-        s = self.state.cpu().numpy()
-        prev = s[4:6].copy().view(np.float64)[0]
-        return {"it": int(s[0]), "done": int(s[1]), "converged": int(s[2]), "prev_rmse": float(prev)}
+        """Channel 0's state (the only one of a single-channel loop)."""
+        return self.read_states()[0]
 
     def run(self, callback=None, chunk: int = 8):
-        """Iterate until the rule fires or max_iters; returns (iterations,
-        converged, wall_ms per iteration)."""
+        """Iterate until the rule fires (in every channel) or max_iters;
+        returns (iterations, converged, wall_ms per iteration) of channel 0 --
+        read_states() has every channel's."""
         t = self.t
         wall = []
         if callback is not None:
+            if self.nch != 1:
+                raise ValueError("per-iteration callbacks run single-channel loops")
             for _ in range(self.max_iters):
                 t0 = time.perf_counter()
                 stream = _lib.stream_ptr()
                 self.pre_decision(stream)
                 st = self.read_state()
-                rmse = float(self.trace[st["it"] - 1].item())
+                rmse = float(self.trace[0, st["it"] - 1].item())
                 wall.append((time.perf_counter() - t0) * 1e3)
                 callback(st["it"], self.host_values(), rmse)
                 if st["done"]:
@@ -479,8 +519,8 @@ class ChannelLoop:
         if self.use_graph and self.graph is None and self.max_iters > 1:
             self.capture()
         # keep one chunk in flight: after enqueueing chunk i, wait for chunk
-        # i-1's state copy and stop once its sticky `done` flag is set
-        bufs = [t.zeros(8, dtype=t.int32, pin_memory=True) for _ in range(2)]
+        # i-1's state copy and stop once every channel's sticky `done` is set
+        bufs = [t.zeros((self.nch, 8), dtype=t.int32, pin_memory=True) for _ in range(2)]
         events = [None, None]
         issued, i = 0, 0
         t_start = time.perf_counter()
@@ -495,21 +535,22 @@ class ChannelLoop:
             events[b].record()
             if i >= 1:
                 events[b ^ 1].synchronize()
-                if int(bufs[b ^ 1][1]):
+                if bool(bufs[b ^ 1][:, 1].all()):
                     break
             i += 1
         t.cuda.synchronize()
-        total_ms = (time.perf_counter() - t_start) * 1e3
+        self.total_ms = (time.perf_counter() - t_start) * 1e3
         st = self.read_state()
         it = st["it"]
-        wall = [total_ms / max(it, 1)] * it
+        wall = [self.total_ms / max(it, 1)] * it
         return it, bool(st["converged"]), wall
 
     # -- results -----------------------------------------------------------------
     def host_values(self) -> np.ndarray:
-        return self.values.cpu().numpy()
+        v = self.values.cpu().numpy()
+        return v[0] if self.nch == 1 else v
 
-    def host_trace(self, iterations: int):
-        rmse = self.trace[:iterations].cpu().numpy().tolist()
-        vol = self.trace_vol[:iterations].cpu().numpy().tolist() if self.trace_vol is not None else []
+    def host_trace(self, iterations: int, channel: int = 0):
+        rmse = self.trace[channel, :iterations].cpu().numpy().tolist()
+        vol = self.trace_vol[channel, :iterations].cpu().numpy().tolist() if self.trace_vol is not None else []
         return rmse, vol
