@@ -157,6 +157,8 @@ int fvr_render_views(const fvr_camera_t* cams, int32_t n_views, int32_t width, i
  * fvr_set_scatter_dirs (radiometry.py:222-230, gather = edge, g = 0). */
 int fvr_set_scatter_dirs(const double* dirs_host, int32_t n);
 int fvr_render_layout_kind(fvr_render_params_t params, fvr_grid_t grid);
+/* layout: float4 per (key point, channel), channels interleaved (element
+ * j * n_channels + c), so the channels of one key point share cache lines. */
 int fvr_pack_layout(const float* values, int32_t n_channels, fvr_grid_t grid, int32_t kind,
                     float* layout, void* stream);
 /* occ[j] = 1 when a key point within Chebyshev distance 1 of j is positive in
@@ -214,7 +216,7 @@ int fvr_loop_finalize(const double* sq_partials, int32_t n_views, int32_t blocks
 /* Clamped update over hull key points unless the state says done; keeps the
  * renderer's packed layout (may be NULL) in sync. */
 int fvr_loop_update(float* values, int64_t* accum, const int32_t* kp_index, int64_t n_kp,
-                    float* layout, int32_t layout_kind, fvr_grid_t grid,
+                    float* layout, int32_t layout_kind, int32_t layout_nch, fvr_grid_t grid,
                     const fvr_loop_state_t* state, void* stream);
 
 /* ---- deterministic back-projection as a voxel-driven gather ------------
@@ -265,8 +267,8 @@ int fvr_loop_gather(const int64_t* row_offsets, const int32_t* entries, int64_t 
                     const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
                     fvr_grid_t grid, int64_t* packed, const fvr_loop_state_t* state, void* stream);
 int fvr_loop_update_packed(const int64_t* packed, int64_t n_kp, const int32_t* kp_index,
-                           float* values, float* layout, int32_t layout_kind, fvr_grid_t grid,
-                           const fvr_loop_state_t* state, void* stream);
+                           float* values, float* layout, int32_t layout_kind, int32_t layout_nch,
+                           fvr_grid_t grid, const fvr_loop_state_t* state, void* stream);
 
 /* Multi-GPU helpers: gather accum at kp_index into a compact buffer and
  * scatter it back (the NCCL allreduce runs between them). */

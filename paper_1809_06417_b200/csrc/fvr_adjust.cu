@@ -137,27 +137,12 @@ __global__ void __launch_bounds__(128) loop_adjust_kernel(
 // When the renderer's packed copy of max(v, 0) exists (fvr_stencil.cuh), the
 // new value is written into every float4 slot that holds it.
 struct LayoutRef {
-    float* p;   // float4 array viewed as floats, or nullptr
+    float* p;   // channel's first float of the float4 layout (layout + 4c), or nullptr
     int kind;   // 1 = YZQ, 2 = Z4
+    int nch;    // interleaved channels
     int sy;     // nz + 1
     int ny1;    // ny + 1
 };
-
-__device__ __forceinline__ void layout_store(const LayoutRef& L, int64_t idx, float v) {
-    const float c = fmaxf(v, 0.f);
-    const int z = (int)(idx % L.sy);
-    if (L.kind == 2) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (z >= k) L.p[4 * (idx - k) + k] = c;
-    } else {
-        const int y = (int)((idx / L.sy) % L.ny1);
-        L.p[4 * idx] = c;
-        if (z >= 1) L.p[4 * (idx - 1) + 1] = c;
-        if (y >= 1) L.p[4 * (idx - L.sy) + 2] = c;
-        if (y >= 1 && z >= 1) L.p[4 * (idx - L.sy - 1) + 3] = c;
-    }
-}
 
 __device__ __forceinline__ void apply_one(float* __restrict__ values,
                                           long long* __restrict__ accum, int64_t idx,
@@ -168,7 +153,7 @@ __device__ __forceinline__ void apply_one(float* __restrict__ values,
         const float f = (float)(nv > -1.0 ? nv : -1.0);
         values[idx] = f;
         accum[idx] = 0;
-        if (L.p) layout_store(L, idx, f);
+        if (L.p) layout_store(L.p, L.nch, L.kind, L.sy, L.ny1, idx, f);
     }
 }
 
@@ -257,7 +242,7 @@ extern "C" int fvr_apply_correction(float* values, int64_t* accum, const int32_t
     FVR_TRY_BEGIN
     if (n == 0) return FVR_OK;
     apply_correction_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
-        values, reinterpret_cast<long long*>(accum), kp_index, n, LayoutRef{nullptr, 0, 1, 1}, nullptr);
+        values, reinterpret_cast<long long*>(accum), kp_index, n, LayoutRef{nullptr, 0, 1, 1, 1}, nullptr);
     return check_launch("apply_correction");
     FVR_TRY_END
 }
@@ -288,12 +273,12 @@ extern "C" int fvr_loop_adjust(const fvr_camera_t* cams, const int32_t* ray_list
 }
 
 extern "C" int fvr_loop_update(float* values, int64_t* accum, const int32_t* kp_index, int64_t n_kp,
-                               float* layout, int32_t layout_kind, fvr_grid_t grid,
+                               float* layout, int32_t layout_kind, int32_t layout_nch, fvr_grid_t grid,
                                const fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
     if (n_kp == 0) return FVR_OK;
     if (layout && layout_kind != 1 && layout_kind != 2) return set_error(FVR_ERR_INVALID, "unknown layout kind");
-    const LayoutRef L{layout, layout_kind, grid.nz + 1, grid.ny + 1};
+    const LayoutRef L{layout, layout_kind, layout_nch > 0 ? layout_nch : 1, grid.nz + 1, grid.ny + 1};
     apply_correction_kernel<<<grid_for(n_kp, 256), 256, 0, (cudaStream_t)stream>>>(
         values, reinterpret_cast<long long*>(accum), kp_index, n_kp, L, state);
     return check_launch("loop_update");

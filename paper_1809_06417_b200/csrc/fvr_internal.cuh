@@ -48,6 +48,25 @@ inline int check_grid(const fvr_grid_t& g) {
     return FVR_OK;
 }
 
+// Write max(v, 0) of key point idx into every float4 slot of the packed
+// layout that holds it; p points at the channel's first float (layout + 4c).
+__device__ __forceinline__ void layout_store(float* __restrict__ p, int nch, int kind, int sy, int ny1,
+                                             int64_t idx, float v) {
+    const float c = fmaxf(v, 0.f);
+    const int z = (int)(idx % sy);
+    if (kind == 2) {  // Z4 (fvr_stencil.cuh); else YZQ
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (z >= k) p[4 * (idx - k) * nch + k] = c;
+    } else {
+        const int y = (int)((idx / sy) % ny1);
+        p[4 * idx * nch] = c;
+        if (z >= 1) p[4 * (idx - 1) * nch + 1] = c;
+        if (y >= 1) p[4 * (idx - sy) * nch + 2] = c;
+        if (y >= 1 && z >= 1) p[4 * (idx - sy - 1) * nch + 3] = c;
+    }
+}
+
 }  // namespace fvr
 
 #define FVR_TRY_BEGIN try {

@@ -315,22 +315,7 @@ __global__ void __launch_bounds__(256) gather_kernel(
                     const double nv = (double)vals[idx] + (double)acc[c] * kFixInv;
                     const float f = (float)(nv > -1.0 ? nv : -1.0);
                     vals[idx] = f;
-                    if (layout) {
-                        float* lay = layout + 4 * c * plane;
-                        const float cpos = fmaxf(f, 0.f);
-                        const int z = (int)(idx % sy);
-                        if (layout_kind == 2) {
-#pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                if (z >= k) lay[4 * (idx - k) + k] = cpos;
-                        } else {
-                            const int y = (int)((idx / sy) % ny1);
-                            lay[4 * idx] = cpos;
-                            if (z >= 1) lay[4 * (idx - 1) + 1] = cpos;
-                            if (y >= 1) lay[4 * (idx - sy) + 2] = cpos;
-                            if (y >= 1 && z >= 1) lay[4 * (idx - sy - 1) + 3] = cpos;
-                        }
-                    }
+                    if (layout) layout_store(layout + 4 * c, NCH, layout_kind, sy, ny1, idx, f);
                 }
             }
         }
@@ -340,7 +325,7 @@ __global__ void __launch_bounds__(256) gather_kernel(
 // Apply a packed (all-reduced) correction: one thread per hull key point.
 __global__ void update_packed_kernel(const long long* __restrict__ packed, int64_t n_rows,
                                      const int32_t* __restrict__ kp_index, float* __restrict__ values,
-                                     float* __restrict__ layout, int layout_kind, int sy, int ny1,
+                                     float* __restrict__ layout, int layout_kind, int layout_nch, int sy, int ny1,
                                      const fvr_loop_state_t* __restrict__ state) {
     if (state && state->done) return;
     for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n_rows;
@@ -351,21 +336,7 @@ __global__ void update_packed_kernel(const long long* __restrict__ packed, int64
         const double nv = (double)values[idx] + (double)acc * kFixInv;
         const float f = (float)(nv > -1.0 ? nv : -1.0);
         values[idx] = f;
-        if (layout) {
-            const float cpos = fmaxf(f, 0.f);
-            const int z = (int)(idx % sy);
-            if (layout_kind == 2) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (z >= k) layout[4 * (idx - k) + k] = cpos;
-            } else {
-                const int y = (int)((idx / sy) % ny1);
-                layout[4 * idx] = cpos;
-                if (z >= 1) layout[4 * (idx - 1) + 1] = cpos;
-                if (y >= 1) layout[4 * (idx - sy) + 2] = cpos;
-                if (y >= 1 && z >= 1) layout[4 * (idx - sy - 1) + 3] = cpos;
-            }
-        }
+        if (layout) layout_store(layout, layout_nch, layout_kind, sy, ny1, idx, f);
     }
 }
 
@@ -451,15 +422,15 @@ extern "C" int fvr_loop_gather(const int64_t* row_offsets, const int32_t* entrie
 }
 
 extern "C" int fvr_loop_update_packed(const int64_t* packed, int64_t n_kp, const int32_t* kp_index,
-                                      float* values, float* layout, int32_t layout_kind, fvr_grid_t grid,
-                                      const fvr_loop_state_t* state, void* stream) {
+                                      float* values, float* layout, int32_t layout_kind, int32_t layout_nch,
+                                      fvr_grid_t grid, const fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
     if (n_kp == 0) return FVR_OK;
     int64_t blocks = (n_kp + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
     update_packed_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-        reinterpret_cast<const long long*>(packed), n_kp, kp_index, values, layout, layout_kind, grid.nz + 1,
-        grid.ny + 1, state);
+        reinterpret_cast<const long long*>(packed), n_kp, kp_index, values, layout, layout_kind, layout_nch,
+        grid.nz + 1, grid.ny + 1, state);
     return check_launch("loop_update_packed");
     FVR_TRY_END
 }

@@ -176,10 +176,10 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
                     for (int c = 0; c < NCH; ++c) {
                         float e = 0.f, acc = 0.f;
                         if (!SCAT) {
-                            e = tri_yzq(layout + (int64_t)c * plane, g, m[0], m[1], m[2], dl[0], dl[1], dl[2]);
+                            e = tri_yzq(layout + c, NCH, g, m[0], m[1], m[2], dl[0], dl[1], dl[2]);
                         } else if (kOmega && interior) {
                             float4 r[9];
-                            load_stencil_z4_raw(layout + (int64_t)c * plane, SX, SY, m[0], m[1], m[2], r);
+                            load_stencil_z4_raw(layout + c, NCH, SX, SY, m[0], m[1], m[2], r);
                             // a sum of non-negative terms in exact arithmetic; the expanded
                             // form can round a vanishing sum below zero
                             acc = fmaxf(omega_dot(r, om01, om2), 0.f);
@@ -188,11 +188,11 @@ __device__ __forceinline__ void march_render_fast(const double o[3], const doubl
                         } else if (interior) {
 #if FVR_MOMENT_PACKED
                             float4 r[9];
-                            load_stencil_z4_raw(layout + (int64_t)c * plane, SX, SY, m[0], m[1], m[2], r);
+                            load_stencil_z4_raw(layout + c, NCH, SX, SY, m[0], m[1], m[2], r);
                             moment_eval2(r, dl[0], dl[1], dl[2], thr, q1, q2, e, acc);
 #else
                             float v[27];
-                            load_stencil_z4(layout + (int64_t)c * plane, g, m[0], m[1], m[2], v);
+                            load_stencil_z4(layout + c, NCH, g, m[0], m[1], m[2], v);
                             moment_eval(v, dl[0], dl[1], dl[2], thr, q1, q2, e, acc);
 #endif
                             // sums of non-negative terms in exact arithmetic; the
@@ -286,7 +286,7 @@ __global__ void pack_layout_kernel(const float* __restrict__ values, int64_t n_k
             r = make_float4(at(j), at(j + 1), at(j + 2), at(j + 3));
         else
             r = make_float4(at(j), at(j + 1), at(j + sy), at(j + sy + 1));
-        out[i] = r;
+        out[j * nch + c] = r;  // channels interleaved per key point
     }
 }
 

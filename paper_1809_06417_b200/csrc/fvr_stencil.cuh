@@ -32,11 +32,14 @@ __constant__ float c_half_dir[3][kScatDirs];
 __constant__ double c_dir[3][kScatDirs];  // (single TU: fvr_render.cu)
 
 // ---- emission-only: two 16-byte loads per sample --------------------------
-__device__ __forceinline__ float tri_yzq(const float4* __restrict__ Q, const Geom& g, int ix, int iy,
+// Channels are interleaved: key point j of channel c is float4 element
+// j * nch + c (Q points at channel c's first element), so the channels of a
+// batched loop read the same cache lines.
+__device__ __forceinline__ float tri_yzq(const float4* __restrict__ Q, int nch, const Geom& g, int ix, int iy,
                                          int iz, float fx, float fy, float fz) {
     const int j = ix * g.sx + iy * g.sy + iz;
-    const float4 a = __ldg(Q + j);         // x = ix
-    const float4 b = __ldg(Q + j + g.sx);  // x = ix + 1
+    const float4 a = __ldg(Q + j * nch);           // x = ix
+    const float4 b = __ldg(Q + (j + g.sx) * nch);  // x = ix + 1
     const float a0 = fmaf(fz, a.y - a.x, a.x), a1 = fmaf(fz, a.w - a.z, a.z);
     const float b0 = fmaf(fz, b.y - b.x, b.x), b1 = fmaf(fz, b.w - b.z, b.z);
     const float a01 = fmaf(fy, a1 - a0, a0), b01 = fmaf(fy, b1 - b0, b0);
@@ -60,14 +63,14 @@ __device__ __forceinline__ void stencil_from(const float v[27], Stencil& s) {
 }
 
 // v[(jx*3 + jy)*3 + jz] = c at m + (jx-1, jy-1, jz-1); interior: 9 float4 loads
-__device__ __forceinline__ void load_stencil_z4(const float4* __restrict__ Z4, const Geom& g, int mx,
+__device__ __forceinline__ void load_stencil_z4(const float4* __restrict__ Z4, int nch, const Geom& g, int mx,
                                                 int my, int mz, float v[27]) {
     const int base = (mx - 1) * g.sx + (my - 1) * g.sy + (mz - 1);
 #pragma unroll
     for (int jx = 0; jx < 3; ++jx)
 #pragma unroll
         for (int jy = 0; jy < 3; ++jy) {
-            const float4 r = __ldg(Z4 + base + jx * g.sx + jy * g.sy);
+            const float4 r = __ldg(Z4 + (base + jx * g.sx + jy * g.sy) * nch);
             v[(jx * 3 + jy) * 3 + 0] = r.x;
             v[(jx * 3 + jy) * 3 + 1] = r.y;
             v[(jx * 3 + jy) * 3 + 2] = r.z;
@@ -335,14 +338,15 @@ __device__ __forceinline__ float2 bcast2(float a) { return make_float2(a, a); }
 
 // sx, sy: lattice strides -- compile-time constants for the specialised
 // cubic lattices, so the nine loads are one pointer plus immediate offsets
-__device__ __forceinline__ void load_stencil_z4_raw(const float4* __restrict__ Z4, int sx, int sy, int mx, int my,
-                                                    int mz, float4 r[9]) {
-    const float4* p = Z4 + (mx * sx + my * sy + (mz - 1));
+__device__ __forceinline__ void load_stencil_z4_raw(const float4* __restrict__ Z4, int nch, int sx, int sy, int mx,
+                                                    int my, int mz, float4 r[9]) {
+    const float4* p = Z4 + (mx * sx + my * sy + (mz - 1)) * nch;
 #pragma unroll
     for (int jx = 0; jx < 3; ++jx)
 #pragma unroll
-        for (int jy = 0; jy < 3; ++jy) r[jx * 3 + jy] = __ldg(p + ((jx - 1) * sx + (jy - 1) * sy));
+        for (int jy = 0; jy < 3; ++jy) r[jx * 3 + jy] = __ldg(p + ((jx - 1) * sx + (jy - 1) * sy) * nch);
 }
+
 
 __device__ __forceinline__ void zeta8(float2 q[4], float hx, float hy, float hz) {
 #pragma unroll

@@ -200,7 +200,8 @@ class ChannelLoop:
         self.layout_kind = _lib.layout_kind(self.params, self.grid)
         self.layout = None
         if self.layout_kind:
-            self.layout = t.empty((C,) + shape + (4,), dtype=t.float32, device=dev)
+            # float4 per (key point, channel), channels interleaved (fvr_stencil.cuh)
+            self.layout = t.empty(shape + (C, 4), dtype=t.float32, device=dev)
             _lib.call("fvr_pack_layout", self.values.data_ptr(), C, self.grid, self.layout_kind,
                       self.layout.data_ptr(), _lib.stream_ptr())
         # empty-space occupancy: hull key points (their values change) plus any
@@ -257,6 +258,10 @@ class ChannelLoop:
         self.graph = None
         self.launches_per_iter = 0
 
+    def _layout_channel(self, ch: int):
+        """Address of channel ch's first float4 in the interleaved layout."""
+        return None if self.layout is None else self.layout.data_ptr() + 16 * ch
+
     # -- one iteration ---------------------------------------------------------
     def _render(self, stream):
         if self.v_end <= self.v_begin:
@@ -312,7 +317,7 @@ class ChannelLoop:
         for ch in range(self.nch):
             _lib.call(
                 "fvr_loop_update", self.values[ch].data_ptr(), self.accum[ch].data_ptr(), self.kp.data_ptr(),
-                self.n_kp, _lib.ptr(None if self.layout is None else self.layout[ch]), self.layout_kind, self.grid,
+                self.n_kp, self._layout_channel(ch), self.layout_kind, self.nch, self.grid,
                 self.state[ch].data_ptr(), stream,
             )
         return self.nch
@@ -405,8 +410,8 @@ class ChannelLoop:
             return 0
         for ch in range(self.nch):
             _lib.call("fvr_loop_update_packed", self.packed[ch].data_ptr(), self.n_kp, self.kp.data_ptr(),
-                      self.values[ch].data_ptr(), _lib.ptr(None if self.layout is None else self.layout[ch]),
-                      self.layout_kind, self.grid, self.state[ch].data_ptr(), stream)
+                      self.values[ch].data_ptr(), self._layout_channel(ch), self.layout_kind, self.nch, self.grid,
+                      self.state[ch].data_ptr(), stream)
         return self.nch
 
     def _allreduce_packed(self, stream):
