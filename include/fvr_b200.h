@@ -176,7 +176,8 @@ int fvr_loop_blocks_per_view(int32_t bbox_w, int32_t bbox_h);
 /* Render every bbox pixel of every view, residual = src - rec (f32), and
  * per-block squared-residual sums (f64). cams is a device array.
  * n_channels (1, or 3 for the batched RGB loop, reconstruct.py:370-385)
- * channels share the rays: src / residual are (n_channels, V, h, w), values
+ * channels share the rays: src is (n_channels, V, h, w), residual (V, h, w,
+ * pitch) with the channels interleaved (pitch 1, or 4 for 3 channels), values
  * and layout hold n_channels lattice planes, background[c] per channel,
  * sq_partials[c * sq_stride + unit], and state points at n_channels loop
  * states (the launch is a no-op once every channel is done). */
@@ -193,7 +194,7 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
  * draws the same weights as a single-GPU run. */
 int fvr_loop_adjust(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
                     int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
-                    const float* residual, const uint8_t* inside_vox, fvr_grid_t grid,
+                    const float* residual, int32_t res_pitch, const uint8_t* inside_vox, fvr_grid_t grid,
                     double tau, double alpha_l, double alpha_d, int32_t stochastic,
                     double g_sigma, uint64_t seed, int64_t ray_id_base, int64_t* accum,
                     const fvr_loop_state_t* state, void* stream);
@@ -253,19 +254,20 @@ int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int6
                          double alpha_d, const int32_t* kp_map, const int64_t* ray_sid0,
                          int64_t* cursor, int32_t* entries, int32_t* sample_meta, void* stream);
 int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, const int32_t* ray_list,
-                               int32_t bbox_w, int32_t bbox_h, const float* residual, uint64_t seed,
-                               double g_sigma, int64_t ray_id_base, float* rho,
+                               int32_t bbox_w, int32_t bbox_h, const float* residual, int32_t n_channels,
+                               uint64_t seed, double g_sigma, int64_t ray_id_base, float* rho,
                                const fvr_loop_state_t* state, void* stream);
 /* Per iteration: row sums in 32.32 fixed point; with packed == NULL the
  * clamped update is applied in place (and the packed layout refreshed),
  * otherwise the sums go to packed (n_channels, n_kp) for the multi-GPU
- * all-reduce.  n_channels (1 or 3) share the plan: residual channel c starts
- * at residual + c * res_stride, values / layout hold n_channels lattice
- * planes and state n_channels loop states (converged channels are skipped). */
+ * all-reduce.  n_channels (1 or 3) share the plan: the residual (or rho)
+ * holds a pixel's (sample's) channels interleaved with pitch 1 or 4, values /
+ * layout hold n_channels lattice planes and state n_channels loop states
+ * (converged channels are skipped). */
 int fvr_loop_gather(const int64_t* row_offsets, const int32_t* entries, int64_t n_kp,
-                    const float* residual, int64_t res_stride, int32_t n_channels,
-                    const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
-                    fvr_grid_t grid, int64_t* packed, const fvr_loop_state_t* state, void* stream);
+                    const float* residual, int32_t n_channels, const int32_t* kp_index, float* values,
+                    float* layout, int32_t layout_kind, fvr_grid_t grid, int64_t* packed,
+                    const fvr_loop_state_t* state, void* stream);
 int fvr_loop_update_packed(const int64_t* packed, int64_t n_kp, const int32_t* kp_index,
                            float* values, float* layout, int32_t layout_kind, int32_t layout_nch,
                            fvr_grid_t grid, const fvr_loop_state_t* state, void* stream);

@@ -113,7 +113,7 @@ _SIGNATURES = {
     ),
     "fvr_loop_adjust": (
         c_int,
-        [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _P, _GRID, c_double, c_double,
+        [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, c_int32, _P, _GRID, c_double, c_double,
          c_double, c_int32, c_double, c_uint64, c_int64, _P, _P, _P],
     ),
     "fvr_loop_volume_sq": (c_int, [_P, _P, _P, c_int64, _P, POINTER(c_int32), _P, _P]),
@@ -131,9 +131,9 @@ _SIGNATURES = {
                                       _P]),
     "fvr_sample_plan_fill": (c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, c_double,
                                      c_double, c_double, _P, _P, _P, _P, _P, _P]),
-    "fvr_loop_weighted_residual": (c_int, [_P, c_int64, _P, c_int32, c_int32, _P, c_uint64, c_double, c_int64,
-                                           _P, _P, _P]),
-    "fvr_loop_gather": (c_int, [_P, _P, c_int64, _P, c_int64, c_int32, _P, _P, _P, c_int32, _GRID, _P, _P, _P]),
+    "fvr_loop_weighted_residual": (c_int, [_P, c_int64, _P, c_int32, c_int32, _P, c_int32, c_uint64, c_double,
+                                           c_int64, _P, _P, _P]),
+    "fvr_loop_gather": (c_int, [_P, _P, c_int64, _P, c_int32, _P, _P, _P, c_int32, _GRID, _P, _P, _P]),
     "fvr_loop_update_packed": (c_int, [_P, c_int64, _P, _P, _P, c_int32, c_int32, _GRID, _P, _P]),
     "fvr_pack_correction": (c_int, [_P, _P, c_int64, _P, _P]),
     "fvr_unpack_correction": (c_int, [_P, _P, c_int64, _P, _P]),

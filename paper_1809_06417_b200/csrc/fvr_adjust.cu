@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(128) count_hull_kernel(double ox, double oy, d
 template <bool PHILOX>
 __global__ void __launch_bounds__(128) loop_adjust_kernel(
     const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
-    int u0, int v0, int w, int h, const float* __restrict__ residual,
+    int u0, int v0, int w, int h, const float* __restrict__ residual, int res_pitch,
     const uint8_t* __restrict__ inside, Geom g, AdjustConsts ac, int64_t ray_id_base,
     unsigned long long* __restrict__ accum, const fvr_loop_state_t* __restrict__ state) {
     if (state && state->done) return;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(128) loop_adjust_kernel(
     const int32_t e = ray_list[r];
     const int view = e >> 24, pix = e & 0xFFFFFF;
     const int row = pix / w, col = pix - row * w;
-    const float res = residual[(int64_t)view * w * h + pix];
+    const float res = residual[((int64_t)view * w * h + pix) * res_pitch];
     if (res == 0.f && !PHILOX) return;  // every deposit would be exactly zero
     const fvr_camera_t& cam = cams[view];
     double d[3];
@@ -249,8 +249,8 @@ extern "C" int fvr_apply_correction(float* values, int64_t* accum, const int32_t
 
 extern "C" int fvr_loop_adjust(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
                                int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
-                               const float* residual, const uint8_t* inside_vox, fvr_grid_t grid,
-                               double tau, double alpha_l, double alpha_d, int32_t stochastic,
+                               const float* residual, int32_t res_pitch, const uint8_t* inside_vox,
+                               fvr_grid_t grid, double tau, double alpha_l, double alpha_d, int32_t stochastic,
                                double g_sigma, uint64_t seed, int64_t ray_id_base, int64_t* accum,
                                const fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
@@ -264,10 +264,12 @@ extern "C" int fvr_loop_adjust(const fvr_camera_t* cams, const int32_t* ray_list
     auto* acc = reinterpret_cast<unsigned long long*>(accum);
     if (stochastic)
         loop_adjust_kernel<true><<<blocks, 128, 0, st>>>(cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h,
-                                                         residual, inside_vox, g, ac, ray_id_base, acc, state);
+                                                         residual, res_pitch > 0 ? res_pitch : 1, inside_vox, g,
+                                                         ac, ray_id_base, acc, state);
     else
         loop_adjust_kernel<false><<<blocks, 128, 0, st>>>(cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h,
-                                                          residual, inside_vox, g, ac, ray_id_base, acc, state);
+                                                          residual, res_pitch > 0 ? res_pitch : 1, inside_vox, g,
+                                                         ac, ray_id_base, acc, state);
     return check_launch("loop_adjust");
     FVR_TRY_END
 }

@@ -67,6 +67,11 @@ __device__ __forceinline__ void layout_store(float* __restrict__ p, int nch, int
     }
 }
 
+// Per-pixel (and per-sample) channel pitch of the residual / rho buffers of
+// a loop with NCH channels: 1, or 4 (padded) for the batched RGB loop.
+template <int NCH>
+constexpr int kResPitch = NCH == 1 ? 1 : 4;
+
 }  // namespace fvr
 
 #define FVR_TRY_BEGIN try {

@@ -235,18 +235,35 @@ __global__ void __launch_bounds__(128) splan_fill_kernel(
     });
 }
 
+template <int NCH>
 __global__ void __launch_bounds__(256) weighted_residual_kernel(
     const int2* __restrict__ meta, int64_t n_samples, const int32_t* __restrict__ ray_list, int w, int h,
     const float* __restrict__ residual, uint64_t seed, float g_sigma, int64_t ray_id_base,
     float* __restrict__ rho, const fvr_loop_state_t* __restrict__ state) {
-    if (state && state->done) return;
-    const uint32_t it = state ? (uint32_t)state->it : 0u;
+    // the live channels share the iteration count (a converged one stops counting)
+    uint32_t it = 0;
+    bool any = !state;
+    if (state) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            any = any || !state[c].done;
+            it = max(it, (uint32_t)state[c].it);
+        }
+    }
+    if (!any) return;
+    constexpr int P = kResPitch<NCH>;
     for (int64_t sid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sid < n_samples;
          sid += (int64_t)gridDim.x * blockDim.x) {
         const int2 m = meta[sid];
         const int32_t e = __ldg(ray_list + m.x);
-        const float res = __ldg(residual + (int64_t)(e >> 24) * w * h + (e & 0xFFFFFF));
-        rho[sid] = res * gauss_weight(seed, it, (uint32_t)(ray_id_base + m.x), (uint32_t)m.y, g_sigma);
+        const int64_t pix = (int64_t)(e >> 24) * w * h + (e & 0xFFFFFF);
+        const float gw = gauss_weight(seed, it, (uint32_t)(ray_id_base + m.x), (uint32_t)m.y, g_sigma);
+        if (P == 1) {
+            rho[sid] = __ldg(residual + pix) * gw;
+        } else {
+            const float4 r = __ldg(reinterpret_cast<const float4*>(residual) + pix);
+            reinterpret_cast<float4*>(rho)[sid] = make_float4(r.x * gw, r.y * gw, r.z * gw, 0.f);
+        }
     }
 }
 
@@ -257,13 +274,14 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
 // by how many rows are in flight: G = 4 puts eight rows in each warp
 // (config 2: G=32 0.113 ms, 16 0.098, 8 0.094, 4 0.092, 2 0.122).
 // NCH channels share the plan (A depends only on geometry and hull): each
-// entry is read once and multiplies NCH residuals (channel stride
-// res_stride); values / layout are NCH lattice planes, packed (NCH, n_rows),
-// state NCH loop states (a converged channel is left untouched).
+// entry is read once and multiplies NCH residuals (interleaved per pixel /
+// sample: one 16-byte load for three channels); values / layout are NCH
+// lattice planes, packed (NCH, n_rows), state NCH loop states (a converged
+// channel is left untouched).
 template <bool PACKED, int G, int U, int NCH>
 __global__ void __launch_bounds__(256) gather_kernel(
     const long long* __restrict__ row_off, const int2* __restrict__ entries, int64_t n_rows,
-    const float* __restrict__ residual, int64_t res_stride, const int32_t* __restrict__ kp_index,
+    const float* __restrict__ residual, const int32_t* __restrict__ kp_index,
     float* __restrict__ values, int64_t plane, float* __restrict__ layout, int layout_kind, int sy, int ny1,
     long long* __restrict__ packed, const fvr_loop_state_t* __restrict__ state) {
     bool live[NCH];
@@ -293,12 +311,17 @@ __global__ void __launch_bounds__(256) gather_kernel(
                 en[u] = i < e ? __ldcs(entries + i) : make_int2(0, 0);
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u)
+            for (int u = 0; u < U; ++u) {
+                const float wgt = __int_as_float(en[u].y);
+                if (NCH == 1) {
+                    acc[0] += __float2ll_rn(__ldg(residual + en[u].x) * wgt * 4294967296.0f);
+                } else {
+                    const float4 r = __ldg(reinterpret_cast<const float4*>(residual) + en[u].x);
+                    const float rr[3] = {r.x, r.y, r.z};
 #pragma unroll
-                for (int c = 0; c < NCH; ++c) {
-                    const float prod = __ldg(residual + c * res_stride + en[u].x) * __int_as_float(en[u].y);
-                    acc[c] += __float2ll_rn(prod * 4294967296.0f);
+                    for (int c = 0; c < NCH; ++c) acc[c] += __float2ll_rn(rr[c] * wgt * 4294967296.0f);
                 }
+            }
         }
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
@@ -375,7 +398,7 @@ extern "C" int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray
 }
 
 extern "C" int fvr_loop_gather(const int64_t* row_offsets, const int32_t* entries, int64_t n_kp,
-                               const float* residual, int64_t res_stride, int32_t n_channels,
+                               const float* residual, int32_t n_channels,
                                const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
                                fvr_grid_t grid, int64_t* packed, const fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
@@ -399,11 +422,11 @@ extern "C" int fvr_loop_gather(const int64_t* row_offsets, const int32_t* entrie
     do {                                                                                                     \
         if (packed)                                                                                          \
             gather_kernel<true, GL, UL, C><<<(unsigned)blocks, 256, 0, st>>>(                                 \
-                ro, en, n_kp, residual, res_stride, kp_index, values, plane, layout, layout_kind, sy, ny1, pk, \
+                ro, en, n_kp, residual, kp_index, values, plane, layout, layout_kind, sy, ny1, pk,             \
                 state);                                                                                      \
         else                                                                                                 \
             gather_kernel<false, GL, UL, C><<<(unsigned)blocks, 256, 0, st>>>(                                \
-                ro, en, n_kp, residual, res_stride, kp_index, values, plane, layout, layout_kind, sy, ny1,    \
+                ro, en, n_kp, residual, kp_index, values, plane, layout, layout_kind, sy, ny1,                \
                 nullptr, state);                                                                             \
     } while (0)
     if (n_channels == 3) {
@@ -467,16 +490,21 @@ extern "C" int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray
 }
 
 extern "C" int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, const int32_t* ray_list,
-                                          int32_t bbox_w, int32_t bbox_h, const float* residual, uint64_t seed,
-                                          double g_sigma, int64_t ray_id_base, float* rho,
-                                          const fvr_loop_state_t* state, void* stream) {
+                                          int32_t bbox_w, int32_t bbox_h, const float* residual,
+                                          int32_t n_channels, uint64_t seed, double g_sigma, int64_t ray_id_base,
+                                          float* rho, const fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
     if (n_samples == 0) return FVR_OK;
+    if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "1 or 3 channels");
     int64_t blocks = (n_samples + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    weighted_residual_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-        reinterpret_cast<const int2*>(sample_meta), n_samples, ray_list, bbox_w, bbox_h, residual, seed,
-        (float)g_sigma, ray_id_base, rho, state);
+    const auto* meta = reinterpret_cast<const int2*>(sample_meta);
+    if (n_channels == 1)
+        weighted_residual_kernel<1><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+            meta, n_samples, ray_list, bbox_w, bbox_h, residual, seed, (float)g_sigma, ray_id_base, rho, state);
+    else
+        weighted_residual_kernel<3><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+            meta, n_samples, ray_list, bbox_w, bbox_h, residual, seed, (float)g_sigma, ray_id_base, rho, state);
     return check_launch("loop_weighted_residual");
     FVR_TRY_END
 }

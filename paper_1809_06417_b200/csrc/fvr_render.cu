@@ -412,8 +412,10 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// NCH channels share the rays: src / residual are (NCH, V, h, w), values
-// and layout NCH lattice planes, sq_partials[c * sq_stride + unit].
+// NCH channels share the rays: src is (NCH, V, h, w), residual (V, h, w,
+// pitch) with the channels interleaved (pitch 1 for one channel, 4 for
+// three: one 16-byte load serves a pixel's channels in the gather), values
+// NCH lattice planes, sq_partials[c * sq_stride + unit].
 template <int MODE, int NS = 0, int NCH = 1>
 __device__ __forceinline__ void render_unit(int unit, int units_x, int units_per_view,
                                             const fvr_camera_t* __restrict__ cams, int n_views, int u0, int v0,
@@ -446,7 +448,7 @@ __device__ __forceinline__ void render_unit(int unit, int units_x, int units_per
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
             const double r = (double)src[c * cstride + pix] - rec[c];
-            residual[c * cstride + pix] = (float)r;
+            residual[pix * kResPitch<NCH> + c] = (float)r;  // channels interleaved per pixel
             sq[c] = r * r;
         }
     }

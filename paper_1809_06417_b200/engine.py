@@ -215,7 +215,10 @@ class ChannelLoop:
 
         # work buffers
         self.bpv = int(_lib.load().fvr_loop_blocks_per_view(self.w_bb, self.h_bb))
-        self.residual = t.zeros((C, max(len(local), 1), self.h_bb, self.w_bb), dtype=t.float32, device=dev)
+        # channels interleaved per pixel (pitch 1, or 4 for three channels)
+        self.pitch = 1 if C == 1 else 4
+        self.residual = t.zeros((max(len(local), 1), self.h_bb, self.w_bb, self.pitch), dtype=t.float32,
+                                device=dev)
         self.n_sq = V * self.bpv
         # [packed correction (C, n_kp) | sq partials (C, V*bpv) | vol partials (C, n_vol)] in one i64 buffer
         nvb = ctypes.c_int32(0)
@@ -282,7 +285,7 @@ class ChannelLoop:
         for ch in range(self.nch):
             _lib.call(
                 "fvr_loop_adjust", self.cams.data_ptr(), self.rays.data_ptr(), self.n_rays,
-                self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb, self.residual[ch].data_ptr(),
+                self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb, self.residual.data_ptr() + 4 * ch, self.pitch,
                 self.inside.data_ptr(), self.grid, c.tau, c.alpha_l, c.alpha_d_eff,
                 1 if c.stochastic else 0, c.g_sigma, c.seed & 0xFFFFFFFFFFFFFFFF, self.ray_base,
                 self.accum[ch].data_ptr(), self.state[ch].data_ptr(), stream,
@@ -376,7 +379,7 @@ class ChannelLoop:
                       sid0.data_ptr(), cursor.data_ptr(), entries.data_ptr(), meta.data_ptr(), stream)
             self.sample_meta = meta
             self.n_samples = n_samples
-            self.rho = t.zeros((self.nch, max(n_samples, 1)), dtype=t.float32, device=dev)
+            self.rho = t.zeros((max(n_samples, 1), self.pitch), dtype=t.float32, device=dev)
         else:
             _lib.call("fvr_adjust_plan_fill", *geo, c.tau, c.alpha_l, c.alpha_d_eff, kp_map.data_ptr(),
                       cursor.data_ptr(), entries.data_ptr(), stream)
@@ -388,19 +391,18 @@ class ChannelLoop:
     def _weigh(self, stream):
         """rho = residual * G per in-hull sample (stochastic sample plan)."""
         c = self.cfg
-        for ch in range(self.nch):
-            _lib.call("fvr_loop_weighted_residual", self.sample_meta.data_ptr(), self.n_samples,
-                      self.rays.data_ptr(), self.w_bb, self.h_bb, self.residual[ch].data_ptr(),
-                      c.seed & 0xFFFFFFFFFFFFFFFF, c.g_sigma, self.ray_base, self.rho[ch].data_ptr(),
-                      self.state[ch].data_ptr(), stream)
-        return self.nch
+        _lib.call("fvr_loop_weighted_residual", self.sample_meta.data_ptr(), self.n_samples,
+                  self.rays.data_ptr(), self.w_bb, self.h_bb, self.residual.data_ptr(), self.nch,
+                  c.seed & 0xFFFFFFFFFFFFFFFF, c.g_sigma, self.ray_base, self.rho.data_ptr(),
+                  self.state.data_ptr(), stream)
+        return 1
 
     def _gather(self, stream, packed: bool):
         if self.n_kp == 0:
             return 0
         src = self.rho if self.sample_plan else self.residual
         _lib.call("fvr_loop_gather", self.plan_offsets.data_ptr(), self.plan_entries.data_ptr(), self.n_kp,
-                  src.data_ptr(), src[0].numel(), self.nch, self.kp.data_ptr(), self.values.data_ptr(),
+                  src.data_ptr(), self.nch, self.kp.data_ptr(), self.values.data_ptr(),
                   _lib.ptr(self.layout), self.layout_kind, self.grid, self.packed.data_ptr() if packed else None,
                   self.state.data_ptr(), stream)
         return 1

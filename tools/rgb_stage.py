@@ -23,9 +23,9 @@ geom = truth[0].copy()
 frames = DeviceFrames(imgs)
 hull = compute_visual_hull(geom, frames.bits, cams)
 b = frames.bbox
-for nch in (3, 1):
+for det, nch in ((True, 3), (True, 1), (False, 3), (False, 1)):
     cfg = ReconstructionConfig(alpha_l=bench.ALPHA_L, tau=bench.TAU, max_iters=60, converge_eps=1e-12,
-                               deterministic_mode=True)
+                               deterministic_mode=det)
     if nch == 3:
         src = frames.blanked[:, b.v0:b.v1 + 1, b.u0:b.u1 + 1, :].permute(3, 0, 1, 2).contiguous()
     else:
@@ -45,4 +45,5 @@ for nch in (3, 1):
         if it >= 5:
             for i, (n, _) in enumerate(stages):
                 times[n].append(evs[i].elapsed_time(evs[i + 1]))
-    print(nch, {n: round(float(np.mean(v)), 4) for n, v in times.items()})
+    print("det" if det else "sto", nch, {n: round(float(np.mean(v)), 4) for n, v in times.items()})
+    del loop

@@ -80,7 +80,7 @@ def loop_config(n, views, res, iters, temperature):
     out = dict(config=f"{n}^3 x {views} views {res}^2, full RTE", iters=iters, ms_per_iter=ms, iters_per_s=1e3 / ms,
                setup_s=t_setup, plan_nnz=loop.plan_nnz, hull_kp=loop.n_kp, flame_rays=loop.n_rays,
                bbox=[sc["bbox"].u0, sc["bbox"].v0, sc["bbox"].u1, sc["bbox"].v1],
-               rmse_first=float(loop.trace[0].item()), rmse_last=float(loop.trace[st["it"] - 1].item()),
+               rmse_first=float(loop.trace[0, 0].item()), rmse_last=float(loop.trace[0, st["it"] - 1].item()),
                synth_s=sc["t_synth"], render_inputs_s=sc["t_render_inputs"], hull_s=sc["t_hull"],
                max_mem_gb=torch.cuda.max_memory_allocated() / 1e9)
     if temperature:
