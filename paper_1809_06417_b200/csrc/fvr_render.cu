@@ -496,7 +496,8 @@ constexpr size_t kScatSmem = sizeof(float4) * (kQ1Vec + kQ2Vec) + sizeof(float) 
 #ifndef FVR_SCAT_THREADS
 #define FVR_SCAT_THREADS 512
 #endif
-constexpr int kScatThreads = FVR_SCAT_THREADS, kScatWarps = kScatThreads / 32, kScatCtasPerSm = 512 / kScatThreads;
+constexpr int kScatThreads = FVR_SCAT_THREADS, kScatWarps = kScatThreads / 32,
+              kScatCtasPerSm = kScatThreads >= 512 ? 1 : 512 / kScatThreads;
 
 template <int NS, int NCH>
 __global__ void __launch_bounds__(kScatThreads, kScatCtasPerSm) loop_render_scat_kernel(
