@@ -90,6 +90,19 @@ def exchange(comm, sq, vol, v_begin: int, v_end: int, rows_per_view: int, rank: 
     dist.all_reduce(comm, op=dist.ReduceOp.SUM, group=group)
 
 
+_PINNED: dict = {}
+
+
+def _pinned_ring(shape, dtype, depth):
+    """Page-locked host buffers for the snapshot ring, kept for the process
+    (cudaHostAlloc costs milliseconds; snapshots of one shape reuse them)."""
+    key = (shape, dtype, depth)
+    if key not in _PINNED:
+        t = _lib.torch()
+        _PINNED[key] = [t.empty(shape, dtype=dtype, pin_memory=True) for _ in range(depth)]
+    return _PINNED[key]
+
+
 class ChannelLoop:
     """Owns the device buffers of one reconstruct_channel call -- or of the
     three channels of reconstruct_color batched into one loop (values of
@@ -504,25 +517,12 @@ class ChannelLoop:
     def run(self, callback=None, chunk: int = 8):
         """Iterate until the rule fires (in every channel) or max_iters;
         returns (iterations, converged, wall_ms per iteration) of channel 0 --
-        read_states() has every channel's."""
+        read_states() has every channel's.  ``callback(channel, it, values,
+        rmse)`` fires after every iteration's RMSE with a host copy of that
+        channel's lattice (see _run_with_snapshots)."""
         t = self.t
-        wall = []
         if callback is not None:
-            if self.nch != 1:
-                raise ValueError("per-iteration callbacks run single-channel loops")
-            for _ in range(self.max_iters):
-                t0 = time.perf_counter()
-                stream = _lib.stream_ptr()
-                self.pre_decision(stream)
-                st = self.read_state()
-                rmse = float(self.trace[0, st["it"] - 1].item())
-                wall.append((time.perf_counter() - t0) * 1e3)
-                callback(st["it"], self.host_values(), rmse)
-                if st["done"]:
-                    break
-                self.post_decision(stream)
-            st = self.read_state()
-            return st["it"], bool(st["converged"]), wall
+            return self._run_with_snapshots(callback)
         if self.use_graph and self.graph is None and self.max_iters > 1:
             self.capture()
         # keep one chunk in flight: after enqueueing chunk i, wait for chunk
@@ -551,6 +551,74 @@ class ChannelLoop:
         it = st["it"]
         wall = [self.total_ms / max(it, 1)] * it
         return it, bool(st["converged"]), wall
+
+    def _run_with_snapshots(self, callback, depth: int = 3):
+        """The loop with per-iteration snapshots that do not stall it (§8f rank 4).
+
+        After an iteration's RMSE, the lattice and the loop state are copied
+        device-to-device into one of ``depth`` ring slots on the loop's stream
+        (before the update can change them); a side stream moves the slot to
+        page-locked host memory while the device runs the next iterations.
+        The host delivers snapshots in iteration order, at the latest when a
+        slot is about to be reused, so at most ``depth`` iterations run ahead
+        of the callbacks.  Iterations issued after the rule fired are no-ops
+        (sticky ``done``) and deliver nothing."""
+        t = self.t
+        C = self.nch
+        main = t.cuda.current_stream()
+        side = t.cuda.Stream()
+        stream = _lib.stream_ptr()
+        host = _pinned_ring(tuple(self.values.shape), t.float32, depth)
+        host_st = _pinned_ring(tuple(self.state.shape), t.int32, depth)
+        slots = [{"dev": t.empty_like(self.values), "st_dev": t.empty_like(self.state),
+                  "host": host[i], "st": host_st[i], "ev": None} for i in range(depth)]
+        delivered = [0] * C
+
+        def deliver(slot) -> bool:
+            slot["ev"].synchronize()
+            slot["ev"] = None
+            st = slot["st"].numpy()
+            all_done = True
+            for c in range(C):
+                it_c = int(st[c, 0])
+                if it_c > delivered[c]:
+                    rmse = float(st[c, 4:6].copy().view(np.float64)[0])
+                    callback(c, it_c, slot["host"][c].numpy().copy(), rmse)
+                    delivered[c] = it_c
+                all_done = all_done and bool(st[c, 1])
+            return all_done
+
+        t_start = time.perf_counter()
+        issued = k = 0
+        finished = False
+        while issued < self.max_iters and not finished:
+            slot = slots[k % depth]
+            if slot["ev"] is not None and deliver(slot):
+                finished = True
+                break
+            self.pre_decision(stream)
+            slot["dev"].copy_(self.values)
+            slot["st_dev"].copy_(self.state)
+            ready = t.cuda.Event()
+            ready.record(main)
+            side.wait_event(ready)
+            with t.cuda.stream(side):
+                slot["host"].copy_(slot["dev"], non_blocking=True)
+                slot["st"].copy_(slot["st_dev"], non_blocking=True)
+                slot["ev"] = t.cuda.Event()
+                slot["ev"].record(side)
+            self.post_decision(stream)
+            issued += 1
+            k += 1
+        for j in range(depth):  # drain the ring in iteration order
+            slot = slots[(k + j) % depth]
+            if slot["ev"] is not None:
+                deliver(slot)
+        t.cuda.synchronize()
+        self.total_ms = (time.perf_counter() - t_start) * 1e3
+        st = self.read_state()
+        it = st["it"]
+        return it, bool(st["converged"]), [self.total_ms / max(it, 1)] * it
 
     # -- results -----------------------------------------------------------------
     def host_values(self) -> np.ndarray:

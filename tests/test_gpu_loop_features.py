@@ -175,3 +175,44 @@ def test_rgb_batched_loop_matches_sequential(cuda_device, monkeypatch):
                 np.testing.assert_allclose(bat.traces[tag].rmse, seq.traces[tag].rmse, rtol=1e-5)
                 assert rel_err(bat.grids[c].values, seq.grids[c].values) <= 1e-5
             assert np.array_equal(bat.hull.tags, seq.hull.tags)
+
+
+def test_snapshot_callbacks_stop_at_convergence_and_batch(cuda_device, monkeypatch):
+    """Snapshot callbacks run off the loop's critical path (ring of pinned
+    buffers): they still fire once per recorded iteration, in order, with the
+    pre-update grid, none after the rule fires -- for a single channel and
+    for the batched RGB loop."""
+    from paper_1809_06417_b200 import reconstruct_color
+
+    g, cams, hull, images, masks, bbox, geom, rcfg = _inputs()
+    base = dict(alpha_l=0.006, tau=float(g["tau"]), deterministic_mode=True)
+    _, t2 = reconstruct_channel(images, cams, geom, hull, ReconstructionConfig(max_iters=2, converge_eps=1e-12,
+                                                                                **base),
+                                render_cfg=rcfg, masks=masks, bbox=bbox)
+    eps = abs(t2.rmse[1] - t2.rmse[0]) * 1.0001
+    seen = []
+    grid, tr = reconstruct_channel(images, cams, geom, hull, ReconstructionConfig(max_iters=50, converge_eps=eps,
+                                                                                   **base),
+                                   render_cfg=rcfg, masks=masks, bbox=bbox,
+                                   callback=lambda it, gr, rmse: seen.append((it, rmse, gr.values.copy())))
+    assert tr.converged and tr.iterations == 2
+    assert [s[0] for s in seen] == [1, 2] and [s[1] for s in seen] == tr.rmse
+    assert np.array_equal(seen[-1][2], grid.values)  # converged: the grid that produced the last RMSE
+
+    g1 = load_golden("tiny_color.npz")
+    cams1 = cameras_from(g1, Camera)
+    imgs = [Image(im.shape[1], im.shape[0], 3, im) for im in g1["images"]]
+    geom1 = VoxelGrid(12, 12, 12, np.array([-0.1] * 3), 0.2 / 12)
+    cfg = ReconstructionConfig(alpha_l=0.01, deterministic_mode=True, max_iters=40)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("FVR_RGB_BATCH", mode)
+        calls = []
+        res = reconstruct_color(imgs, cams1, geom1, cfg, render_cfg=RenderConfig(),
+                                callback=lambda tag, it, gr, rmse: calls.append((tag, it, rmse)))
+        out[mode] = (calls, res)
+    for tag in ("red", "green", "blue"):
+        bat = [(it, r) for t_, it, r in out["1"][0] if t_ == tag]
+        seq = [(it, r) for t_, it, r in out["0"][0] if t_ == tag]
+        assert [b[0] for b in bat] == [s[0] for s in seq] == list(range(1, out["1"][1].traces[tag].iterations + 1))
+        np.testing.assert_allclose([b[1] for b in bat], [s[1] for s in seq], rtol=1e-5)
