@@ -1,6 +1,6 @@
 """Image container crossing the API boundary (fvr.imgio.Image,
-/root/reference/pkg/src/fvr/imgio.py:21-55).  File formats are out of scope
-for this build."""
+/root/reference/pkg/src/fvr/imgio.py:21-55).  The file formats (FIM1, PNM)
+live in formats.py."""
 
 from __future__ import annotations
 
