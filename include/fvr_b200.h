@@ -187,6 +187,30 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
                     const double* background, int32_t n_channels, const double* scat_dirs, float* residual,
                     double* sq_partials, int64_t sq_stride, fvr_loop_state_t* state, void* stream);
 
+/* K-render as a fixed operator (the render plan, csrc/fvr_rplan.cuh).  The
+ * loop's forward model is linear in max(v, 0) with geometry-only weights, so
+ * rec = B c + base + t_fin * bg.  B is stored SELL-32 by K-render's 8x4
+ * pixel units: unit_len[unit] (count pass) = longest row of the unit;
+ * unit_off = exclusive scan of unit_len; entry t of row (unit, lane) at
+ * int2 index unit_off[unit] * 32 + 32 t + lane = (key point, f32 weight).
+ * Columns are the key points flagged in `dynamic` (the loop's hull key
+ * points); the others fold into base (n_channels x rows f64, rows =
+ * n_units * 32) from `values`.  Needs the fast render modes (g = 0, gather =
+ * edge, 32 directions loaded); occ is the distance map (may be NULL).
+ * fvr_rplan_render replaces fvr_loop_render with identical outputs. */
+int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
+                    int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
+                    const uint8_t* dynamic, int32_t* unit_len, void* stream);
+int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
+                   int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
+                   const uint8_t* dynamic, const float* values, int32_t n_channels, const int64_t* unit_off,
+                   int32_t* entries, double* base, double* t_fin, void* stream);
+int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const int32_t* entries,
+                     const double* base, const double* t_fin, int32_t n_views, int32_t bbox_w, int32_t bbox_h,
+                     const float* src, const float* values, fvr_grid_t grid, int32_t n_channels,
+                     const double* background, float* residual, double* sq_partials, int64_t sq_stride,
+                     const fvr_loop_state_t* state, void* stream);
+
 /* Back-project the residual of every listed flame ray (ray_list entries are
  * view << 24 | (row_in_bbox * bbox_w + col_in_bbox)). stochastic != 0 draws
  * G ~ clip(N(1, g_sigma), 0, 2) from a counter-based Philox stream keyed by

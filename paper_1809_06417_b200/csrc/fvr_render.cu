@@ -550,6 +550,8 @@ __global__ void __launch_bounds__(kScatThreads, kScatCtasPerSm) loop_render_scat
 
 }  // namespace fvr
 
+#include "fvr_rplan.cuh"
+
 using namespace fvr;
 
 namespace {
@@ -989,5 +991,107 @@ extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_
     }
 #undef FVR_LOOP_RENDER
     return check_launch("loop_render");
+    FVR_TRY_END
+}
+
+// ---- K-render as a fixed operator (fvr_rplan.cuh) -----------------------------
+
+namespace {
+// the plan covers the two fast modes (g = 0, gather = edge, 32 loaded directions)
+int rplan_mode(const fvr_render_params_t& params, const fvr_grid_t& grid, bool& scat) {
+    const float4* dummy = reinterpret_cast<const float4*>(&params);  // any non-null layout: mode query only
+    const int mode = effective_mode(params, grid, dummy, scat);
+    if (mode == kModeFastScat) return 1;
+    if (mode == kModeFastPlain) return 0;
+    return -1;
+}
+}  // namespace
+
+extern "C" int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
+                               int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params,
+                               const uint8_t* occ, const uint8_t* dynamic, int32_t* unit_len, void* stream) {
+    FVR_TRY_BEGIN
+    if (n_views < 1 || bbox_w < 1 || bbox_h < 1) return set_error(FVR_ERR_INVALID, "empty render plan");
+    if (!dynamic || !unit_len) return set_error(FVR_ERR_INVALID, "dynamic / unit_len is NULL");
+    if (int rc = check_grid(grid)) return rc;
+    bool scat;
+    const int m = rplan_mode(params, grid, scat);
+    if (m < 0) return set_error(FVR_ERR_INVALID, "render plan needs g = 0, gather = edge and 32 directions");
+    const Geom g = make_geom(grid);
+    const double bg = 0.0;
+    const RenderConsts rc = make_render_consts(params, &bg, 1);
+    const int units_x = (bbox_w + kUnitW - 1) / kUnitW, upv = fvr_loop_blocks_per_view(bbox_w, bbox_h);
+    const int n_units = upv * n_views;
+    const unsigned blocks = (unsigned)(((int64_t)n_units * 32 + 127) / 128);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (m)
+        rplan_count_kernel<true><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
+                                                          occ, dynamic, unit_len);
+    else
+        rplan_count_kernel<false><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
+                                                           occ, dynamic, unit_len);
+    return check_launch("rplan_count");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
+                              int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
+                              const uint8_t* dynamic, const float* values, int32_t n_channels,
+                              const int64_t* unit_off, int32_t* entries, double* base, double* t_fin, void* stream) {
+    FVR_TRY_BEGIN
+    if (n_views < 1 || bbox_w < 1 || bbox_h < 1) return set_error(FVR_ERR_INVALID, "empty render plan");
+    if (n_channels < 1 || n_channels > 4) return set_error(FVR_ERR_INVALID, "n_channels must be 1..4");
+    if (int rc = check_grid(grid)) return rc;
+    bool scat;
+    const int m = rplan_mode(params, grid, scat);
+    if (m < 0) return set_error(FVR_ERR_INVALID, "render plan needs g = 0, gather = edge and 32 directions");
+    const Geom g = make_geom(grid);
+    const double bg = 0.0;
+    const RenderConsts rc = make_render_consts(params, &bg, 1);
+    const int units_x = (bbox_w + kUnitW - 1) / kUnitW, upv = fvr_loop_blocks_per_view(bbox_w, bbox_h);
+    const int n_units = upv * n_views;
+    const int64_t plane = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
+    const unsigned blocks = (unsigned)(((int64_t)n_units * 32 + 127) / 128);
+    cudaStream_t st = (cudaStream_t)stream;
+    const auto* uo = reinterpret_cast<const long long*>(unit_off);
+    auto* en = reinterpret_cast<int2*>(entries);
+    if (m)
+        rplan_fill_kernel<true><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc, occ,
+                                                         dynamic, values, n_channels, plane, uo, en, base, t_fin);
+    else
+        rplan_fill_kernel<false><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
+                                                          occ, dynamic, values, n_channels, plane, uo, en, base, t_fin);
+    return check_launch("rplan_fill");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const int32_t* entries,
+                                const double* base, const double* t_fin, int32_t n_views, int32_t bbox_w,
+                                int32_t bbox_h, const float* src, const float* values, fvr_grid_t grid,
+                                int32_t n_channels, const double* background, float* residual, double* sq_partials,
+                                int64_t sq_stride, const fvr_loop_state_t* state, void* stream) {
+    FVR_TRY_BEGIN
+    if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "the loop renders 1 or 3 channels");
+    if (!background) return set_error(FVR_ERR_INVALID, "background is NULL");
+    fvr_render_params_t p{};
+    p.tau = 0.0;
+    RenderConsts rc = make_render_consts(p, background, n_channels);
+    const int units_x = (bbox_w + kUnitW - 1) / kUnitW, upv = fvr_loop_blocks_per_view(bbox_w, bbox_h);
+    const int n_units = upv * n_views;
+    const int64_t plane = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
+    int64_t blocks = ((int64_t)n_units * 32 + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    cudaStream_t st = (cudaStream_t)stream;
+    const auto* uo = reinterpret_cast<const long long*>(unit_off);
+    const auto* en = reinterpret_cast<const int2*>(entries);
+    if (n_channels == 1)
+        rplan_render_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, en, base, t_fin, n_units, units_x, upv,
+                                                                n_views, bbox_w, bbox_h, src, values, plane, rc,
+                                                                residual, sq_partials, sq_stride, state);
+    else
+        rplan_render_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, en, base, t_fin, n_units, units_x, upv,
+                                                                n_views, bbox_w, bbox_h, src, values, plane, rc,
+                                                                residual, sq_partials, sq_stride, state);
+    return check_launch("rplan_render");
     FVR_TRY_END
 }

@@ -1,0 +1,320 @@
+// fvr_rplan.cuh -- K-render as a fixed sparse operator (included by
+// fvr_render.cu, which owns the direction constants).
+//
+// The loop's forward model is linear in c = max(v, 0): every sample of a
+// pixel's ray adds t_k tau (sigma_a c(p) + kappa sum_d c(p + h s_d)), the
+// transparency t_k = (1-tau)^(k-1) and the in-box masks depend only on the
+// geometry, and the trilinear reads are linear in the 27 key points around
+// the sample.  So one iteration's render is rec = B c + base + t_n bg with a
+// matrix B that never changes during a reconstruction.  The render plan stores
+// B in SELL-32 form: rows are the bbox pixels in K-render's 8x4 warp units,
+// entry t of lane i at unit_off*32 + 32 t + i (coalesced), columns are the key
+// points that can change (hull key points); key points that cannot change
+// fold into `base`.  Consecutive samples of a ray share most of their 27
+// stencil key points, so the weights are merged along the ray in a 3x3x3
+// window that shifts with the nearest key point (~10 entries per live sample
+// instead of 27).
+//
+// Weights are summed directly (hat weights of the sample and of its 32 gather
+// points, fp32), so B's entries are sums of non-negative terms; K-render's
+// moment evaluation reaches the same values up to float rounding.
+#pragma once
+
+namespace fvr {
+
+__device__ __forceinline__ void hat3(float x, float h[3]) {
+    h[0] = fmaxf(-x, 0.f);
+    h[1] = 1.f - fabsf(x);
+    h[2] = fmaxf(x, 0.f);
+}
+
+// w[(jx*3 + jy)*3 + jz]: coefficient of the key point at offset (jx-1, jy-1,
+// jz-1) from the sample's nearest key point in sigma_a e + kappa S.
+template <bool SCAT>
+__device__ __forceinline__ void sample_weights(float dx, float dy, float dz, float sig_a, float kappa,
+                                               uint32_t mask, float w[27]) {
+    float hx[3], hy[3], hz[3];
+    hat3(dx, hx);
+    hat3(dy, hy);
+    hat3(dz, hz);
+#pragma unroll
+    for (int jx = 0; jx < 3; ++jx)
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy)
+#pragma unroll
+            for (int jz = 0; jz < 3; ++jz) w[(jx * 3 + jy) * 3 + jz] = sig_a * (hx[jx] * hy[jy] * hz[jz]);
+    if (SCAT) {
+        float s[27];
+#pragma unroll
+        for (int j = 0; j < 27; ++j) s[j] = 0.f;
+#pragma unroll 2
+        for (int d = 0; d < kScatDirs; ++d) {
+            if (!((mask >> d) & 1u)) continue;
+            hat3(dx + c_half_dir[0][d], hx);
+            hat3(dy + c_half_dir[1][d], hy);
+            hat3(dz + c_half_dir[2][d], hz);
+#pragma unroll
+            for (int jx = 0; jx < 3; ++jx)
+#pragma unroll
+                for (int jy = 0; jy < 3; ++jy) {
+                    const float hxy = hx[jx] * hy[jy];
+#pragma unroll
+                    for (int jz = 0; jz < 3; ++jz) s[(jx * 3 + jy) * 3 + jz] = fmaf(hxy, hz[jz], s[(jx * 3 + jy) * 3 + jz]);
+                }
+        }
+#pragma unroll
+        for (int j = 0; j < 27; ++j) w[j] = fmaf(kappa, s[j], w[j]);
+    }
+}
+
+// shift a 3-slot line by delta in {-1, 0, 1}: new[o] = old[o + delta] (0 outside)
+__device__ __forceinline__ void shift3(float& a0, float& a1, float& a2, int delta) {
+    const float o0 = a0, o1 = a1, o2 = a2;
+    a0 = delta > 0 ? o1 : (delta < 0 ? 0.f : o0);
+    a1 = delta > 0 ? o2 : (delta < 0 ? o0 : o1);
+    a2 = delta > 0 ? 0.f : (delta < 0 ? o1 : o2);
+}
+
+// Walk one pixel's ray exactly as K-render samples it and produce its row of
+// B.  FILL = false only counts the entries.  `dynamic` marks the key points
+// whose value can change (the loop's hull key points); the others contribute
+// max(v, 0) * weight to base[c] (values: nch lattice planes).  Returns the
+// entry count; t_fin receives the transparency after the last sample.
+template <bool SCAT, bool FILL>
+__device__ int rplan_row(const double o[3], const double d[3], const Geom& g, const RenderConsts& rc,
+                         const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
+                         const float* __restrict__ values, int nch, int64_t plane, int2* __restrict__ out,
+                         double* base, double& t_fin) {
+    int count = 0;
+    double t_dst = 1.0;
+    float acc[27];
+#pragma unroll
+    for (int j = 0; j < 27; ++j) acc[j] = 0.f;
+    int wm[3] = {0, 0, 0};  // window centre (nearest key point of the last merged sample)
+    bool have = false;
+    const float sig_a = (float)rc.sigma_a, kappa = (float)rc.scat_scale;
+    auto put = [&](int kp, float wt) {
+        if (FILL) out[(int64_t)count * 32] = make_int2(kp, __float_as_int(wt));
+        ++count;
+    };
+    auto flush = [&]() {
+        if (!have) return;
+        const int base_kp = wm[0] * g.sx + wm[1] * g.sy + wm[2];
+#pragma unroll
+        for (int j = 0; j < 27; ++j) {
+            if (acc[j] != 0.f) put(base_kp + (j / 9 - 1) * g.sx + ((j / 3) % 3 - 1) * g.sy + (j % 3 - 1), acc[j]);
+            acc[j] = 0.f;
+        }
+        have = false;
+    };
+    double te, tx;
+    if (slab_span(o, d, g, te, tx)) {
+        const int n = sample_count(te, tx, g.edge);
+        const double t0 = te - 0.5 * g.edge;
+        double qb[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) qb[a] = ((o[a] - g.lo[a]) + t0 * d[a]) * g.inv_edge;
+        const double nmax[3] = {(double)g.nx, (double)g.ny, (double)g.nz};
+        for (int k = 1; k <= n; ++k, t_dst *= rc.one_minus_tau) {
+            double q[3];
+            int m[3];
+            float dl[3];
+            bool interior = true;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                q[a] = fma((double)k, d[a], qb[a]);
+                interior = interior && q[a] >= 0.5 + 1e-7 && q[a] <= nmax[a] - 0.5 - 1e-7;
+                m[a] = min(max((int)rint(q[a]), 0), a == 0 ? g.nx : (a == 1 ? g.ny : g.nz));
+                dl[a] = (float)(q[a] - (double)m[a]);
+            }
+            const int mlin = m[0] * g.sx + m[1] * g.sy + m[2];
+            if (occ && __ldg(occ + mlin) > 1) continue;  // no key point of the stencil can be non-zero
+            uint32_t mask = 0xffffffffu;
+            if (SCAT && !interior) {
+                double p[3];
+                sample_pos(o, d, te, g.edge, k, p);
+                mask = inbox_mask(p, g, rc.half_gather);
+            }
+            float w[27];
+            sample_weights<SCAT>(dl[0], dl[1], dl[2], sig_a, kappa, mask, w);
+            const float scale = (float)(t_dst * rc.tau);
+            if (!interior) {
+                // within half a voxel of a box face: clamped stencil, entries unmerged
+                flush();
+#pragma unroll 1
+                for (int j = 0; j < 27; ++j) {
+                    const float wt = w[j] * scale;
+                    if (wt == 0.f) continue;
+                    const int x = min(max(m[0] + j / 9 - 1, 0), g.nx), y = min(max(m[1] + (j / 3) % 3 - 1, 0), g.ny),
+                              z = min(max(m[2] + j % 3 - 1, 0), g.nz);
+                    const int kp = x * g.sx + y * g.sy + z;
+                    if (__ldg(dynamic + kp)) {
+                        put(kp, wt);
+                    } else {
+                        for (int c = 0; c < nch; ++c) base[c] += (double)wt * fmaxf(__ldg(values + c * plane + kp), 0.f);
+                    }
+                }
+                continue;
+            }
+            // move the merge window to m: slots leaving it are final
+            const int dx = m[0] - wm[0], dy = m[1] - wm[1], dz = m[2] - wm[2];
+            if (have && abs(dx) <= 1 && abs(dy) <= 1 && abs(dz) <= 1) {
+                if (dx | dy | dz) {
+                    const int base_kp = wm[0] * g.sx + wm[1] * g.sy + wm[2];
+#pragma unroll
+                    for (int j = 0; j < 27; ++j) {
+                        const int ox = j / 9, oy = (j / 3) % 3, oz = j % 3;
+                        const bool leaves = (unsigned)(ox - dx) > 2u || (unsigned)(oy - dy) > 2u || (unsigned)(oz - dz) > 2u;
+                        if (leaves && acc[j] != 0.f)
+                            put(base_kp + (ox - 1) * g.sx + (oy - 1) * g.sy + (oz - 1), acc[j]);
+                    }
+#pragma unroll
+                    for (int l = 0; l < 9; ++l) shift3(acc[3 * l], acc[3 * l + 1], acc[3 * l + 2], dz);
+#pragma unroll
+                    for (int ox = 0; ox < 3; ++ox)
+#pragma unroll
+                        for (int oz = 0; oz < 3; ++oz) shift3(acc[ox * 9 + oz], acc[ox * 9 + 3 + oz], acc[ox * 9 + 6 + oz], dy);
+#pragma unroll
+                    for (int l = 0; l < 9; ++l) shift3(acc[l], acc[9 + l], acc[18 + l], dx);
+                }
+            } else {
+                flush();
+            }
+            wm[0] = m[0];
+            wm[1] = m[1];
+            wm[2] = m[2];
+            have = true;
+#pragma unroll
+            for (int j = 0; j < 27; ++j) {
+                const float wt = w[j] * scale;
+                const int kp = mlin + (j / 9 - 1) * g.sx + ((j / 3) % 3 - 1) * g.sy + (j % 3 - 1);
+                if (__ldg(dynamic + kp)) {
+                    acc[j] += wt;
+                } else if (wt != 0.f) {
+                    for (int c = 0; c < nch; ++c) base[c] += (double)wt * fmaxf(__ldg(values + c * plane + kp), 0.f);
+                }
+            }
+        }
+        flush();
+    }
+    t_fin = t_dst;
+    return count;
+}
+
+// Count pass: one warp per 8x4 unit, unit_len[unit] = longest row of the unit.
+template <bool SCAT>
+__global__ void __launch_bounds__(128) rplan_count_kernel(
+    const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
+    int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
+    int* __restrict__ unit_len) {
+    const int unit = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (unit >= n_units) return;
+    const int lane = threadIdx.x & 31;
+    const int view = unit / units_per_view, u = unit - view * units_per_view;
+    const int col = (u % units_x) * kUnitW + (lane % kUnitW), row = (u / units_x) * kUnitH + (lane / kUnitW);
+    int cnt = 0;
+    if (col < w && row < h) {
+        const fvr_camera_t& cam = cams[view];
+        double d[3], base[1] = {0.0}, t_fin;
+        pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
+        cnt = rplan_row<SCAT, false>(cam.center, d, g, rc, occ, dynamic, nullptr, 0, 0, nullptr, base, t_fin);
+    }
+    cnt = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
+    if (lane == 0) unit_len[unit] = cnt;
+}
+
+// Fill pass: rows in SELL-32 order; base[c * rows + r] and t_fin[r] per row
+// r = unit * 32 + lane (entries beyond a row's length stay (0, 0.0)).
+template <bool SCAT>
+__global__ void __launch_bounds__(128) rplan_fill_kernel(
+    const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
+    int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
+    const float* __restrict__ values, int nch, int64_t plane, const long long* __restrict__ unit_off,
+    int2* __restrict__ entries, double* __restrict__ base_out, double* __restrict__ t_fin_out) {
+    const int unit = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (unit >= n_units) return;
+    const int lane = threadIdx.x & 31;
+    const int view = unit / units_per_view, u = unit - view * units_per_view;
+    const int col = (u % units_x) * kUnitW + (lane % kUnitW), row = (u / units_x) * kUnitH + (lane / kUnitW);
+    const int64_t r = (int64_t)unit * 32 + lane, rows = (int64_t)n_units * 32;
+    double base[4] = {0.0, 0.0, 0.0, 0.0}, t_fin = 0.0;
+    if (col < w && row < h) {
+        const fvr_camera_t& cam = cams[view];
+        double d[3];
+        pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
+        rplan_row<SCAT, true>(cam.center, d, g, rc, occ, dynamic, values, nch, plane,
+                              entries + unit_off[unit] * 32 + lane, base, t_fin);
+    }
+    for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];
+    t_fin_out[r] = t_fin;
+}
+
+// K-render through the plan: one warp per unit, lane = pixel; rec = B c +
+// base + t_fin bg, then the same residual / squared-residual epilogue as the
+// marching kernel.  Products in fp32, summed in fp64 eight at a time.
+template <int NCH>
+__global__ void __launch_bounds__(256) rplan_render_kernel(
+    const int* __restrict__ unit_len, const long long* __restrict__ unit_off, const int2* __restrict__ entries,
+    const double* __restrict__ base, const double* __restrict__ t_fin, int n_units, int units_x,
+    int units_per_view, int n_views, int w, int h, const float* __restrict__ src, const float* __restrict__ values,
+    int64_t plane, RenderConsts rc, float* __restrict__ residual, double* __restrict__ sq_partials,
+    int64_t sq_stride, const fvr_loop_state_t* __restrict__ state) {
+    if (all_done<NCH>(state)) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t rows = (int64_t)n_units * 32;
+    for (int unit = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); unit < n_units;
+         unit += (int)(((int64_t)gridDim.x * blockDim.x) >> 5)) {
+        const int len = unit_len[unit];
+        const int2* e = entries + unit_off[unit] * 32 + lane;
+        double acc[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
+        int t = 0;
+        for (; t + 8 <= len; t += 8) {
+            int2 en[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) en[i] = __ldcs(e + (int64_t)(t + i) * 32);
+            float part[NCH];
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) part[c] = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int c = 0; c < NCH; ++c)
+                    part[c] = fmaf(__int_as_float(en[i].y), fmaxf(__ldg(values + c * plane + en[i].x), 0.f), part[c]);
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) acc[c] += (double)part[c];
+        }
+        for (; t < len; ++t) {
+            const int2 en = __ldcs(e + (int64_t)t * 32);
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+                acc[c] += (double)(__int_as_float(en.y) * fmaxf(__ldg(values + c * plane + en.x), 0.f));
+        }
+        const int view = unit / units_per_view, u = unit - view * units_per_view;
+        const int col = (u % units_x) * kUnitW + (lane % kUnitW), row = (u / units_x) * kUnitH + (lane / kUnitW);
+        const int64_t r = (int64_t)unit * 32 + lane;
+        const int64_t cstride = (int64_t)n_views * h * w;
+        double sq[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) sq[c] = 0.0;
+        if (col < w && row < h) {
+            const int64_t pix = ((int64_t)view * h + row) * w + col;
+            const double tf = t_fin[r];
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                const double rec = acc[c] + base[c * rows + r] + tf * rc.bg[c];
+                const double res = (double)src[c * cstride + pix] - rec;
+                residual[pix * kResPitch<NCH> + c] = (float)res;
+                sq[c] = res * res;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const double tot = warp_sum(sq[c]);
+            if (lane == 0) sq_partials[c * sq_stride + unit] = tot;
+        }
+    }
+}
+
+}  // namespace fvr

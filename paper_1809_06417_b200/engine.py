@@ -225,6 +225,7 @@ class ChannelLoop:
             self.occ = t.empty(shape, dtype=t.uint8, device=dev)
             _lib.call("fvr_occupancy", self.values.data_ptr(), C, kp_dev.data_ptr(), self.grid,
                       self.occ.data_ptr(), _lib.stream_ptr())
+        self.kp_dev = kp_dev
 
         # work buffers
         self.bpv = int(_lib.load().fvr_loop_blocks_per_view(self.w_bb, self.h_bb))
@@ -264,6 +265,11 @@ class ChannelLoop:
             self.sample_plan = self.plan and self.sample_plan
         if not self.plan:
             self.accum = t.zeros((C,) + shape, dtype=t.int64, device=dev)
+        # K-render as a fixed sparse operator (fvr_rplan.cuh) when it fits
+        self.rplan = False
+        self.rplan_nnz = 0
+        if self.layout_kind and os.environ.get("FVR_RENDER", "plan") != "march":
+            self.rplan = self._build_render_plan()
         # A CUDA graph only pays off when an iteration is launch-bound (a few
         # tens of microseconds of device work); for larger problems the host
         # enqueues 3-4 launches (~30 us) far ahead of the device, and graph
@@ -279,9 +285,47 @@ class ChannelLoop:
         return None if self.layout is None else self.layout.data_ptr() + 16 * ch
 
     # -- one iteration ---------------------------------------------------------
+    def _build_render_plan(self) -> bool:
+        """B of rec = B c + base + t_fin bg in SELL-32 form, built once per
+        call (count pass, scan, fill pass); False when it would not fit."""
+        if self.v_end <= self.v_begin:
+            return False
+        t = self.t
+        dev = self.dev
+        stream = _lib.stream_ptr()
+        n_views = self.v_end - self.v_begin
+        n_units = n_views * self.bpv
+        geo = (self.cams.data_ptr(), n_views, self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb, self.grid,
+               self.params, _lib.ptr(self.occ), self.kp_dev.data_ptr())
+        unit_len = t.zeros(n_units, dtype=t.int32, device=dev)
+        _lib.call("fvr_rplan_count", *geo, unit_len.data_ptr(), stream)
+        off = t.zeros(n_units + 1, dtype=t.int64, device=dev)
+        off[1:] = t.cumsum(unit_len.long(), 0)
+        slots = int(off[-1].item()) * 32
+        need = 8 * slots + 8 * (self.nch + 1) * n_units * 32
+        if need > min(self.PLAN_MAX_BYTES, t.cuda.mem_get_info(dev)[0] // 2):
+            return False
+        entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
+        base = t.zeros((self.nch, n_units * 32), dtype=t.float64, device=dev)
+        t_fin = t.zeros(n_units * 32, dtype=t.float64, device=dev)
+        _lib.call("fvr_rplan_fill", *geo, self.values.data_ptr(), self.nch, off.data_ptr(), entries.data_ptr(),
+                  base.data_ptr(), t_fin.data_ptr(), stream)
+        self.rp_len, self.rp_off, self.rp_entries, self.rp_base, self.rp_tfin = unit_len, off, entries, base, t_fin
+        self.rplan_nnz = slots
+        return True
+
     def _render(self, stream):
         if self.v_end <= self.v_begin:
             return 0
+        if self.rplan:
+            _lib.call(
+                "fvr_rplan_render", self.rp_len.data_ptr(), self.rp_off.data_ptr(), self.rp_entries.data_ptr(),
+                self.rp_base.data_ptr(), self.rp_tfin.data_ptr(), self.v_end - self.v_begin, self.w_bb, self.h_bb,
+                self.src.data_ptr(), self.values.data_ptr(), self.grid, self.nch, self.background,
+                self.residual.data_ptr(), self.sq[0, self.v_begin * self.bpv:].data_ptr(), self.n_sq,
+                self.state.data_ptr(), stream,
+            )
+            return 1
         _lib.call(
             "fvr_loop_render", self.cams.data_ptr(), self.v_end - self.v_begin, self.bbox.u0,
             self.bbox.v0, self.w_bb, self.h_bb, self.src.data_ptr(), self.values.data_ptr(),
