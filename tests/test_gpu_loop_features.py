@@ -216,3 +216,42 @@ def test_snapshot_callbacks_stop_at_convergence_and_batch(cuda_device, monkeypat
         seq = [(it, r) for t_, it, r in out["0"][0] if t_ == tag]
         assert [b[0] for b in bat] == [s[0] for s in seq] == list(range(1, out["1"][1].traces[tag].iterations + 1))
         np.testing.assert_allclose([b[1] for b in bat], [s[1] for s in seq], rtol=1e-5)
+
+
+@pytest.mark.parametrize("fixture,scat", [("config1.npz", False), ("loop_scatter.npz", True)])
+def test_render_plan_matches_marching_render(cuda_device, monkeypatch, fixture, scat):
+    """K-render through the render plan (B c + base + t_fin bg) against the
+    marching kernel on the same loop: same iteration counts, traces and
+    grids within float rounding -- deterministic and stochastic, one channel
+    and the batched RGB loop (small grids: many samples sit within half a
+    voxel of a face and take the clamped, unmerged path)."""
+    from paper_1809_06417_b200 import reconstruct_color
+
+    g = load_golden(fixture)
+    cams = cameras_from(g, Camera)
+    n = int(g["n"])
+    hull = HullTags(g["hull_tags"], len(cams))
+    images = [Image(im.shape[1], im.shape[0], 1, im[:, :, 1:2]) for im in g["blanked"]]
+    masks = [FlameMask(m.shape[1], m.shape[0], m) for m in g["masks"]]
+    bbox = Rect(*(int(x) for x in g["bbox"]))
+    geom = VoxelGrid(n, n, n, g["origin"], float(g["edge"]))
+    rcfg = RenderConfig(tau=float(g["tau"]), scattering_enabled=scat, sigma_s=float(g["sigma_s"]))
+    for det in (True, False):
+        cfg = ReconstructionConfig(alpha_l=0.006, tau=float(g["tau"]), max_iters=6, converge_eps=1e-12,
+                                   deterministic_mode=det, g_sigma=0.1, rng_seed=1)
+        monkeypatch.setenv("FVR_RENDER", "march")
+        a, ta = reconstruct_channel(images, cams, geom, hull, cfg, render_cfg=rcfg, masks=masks, bbox=bbox)
+        monkeypatch.setenv("FVR_RENDER", "plan")
+        b, tb = reconstruct_channel(images, cams, geom, hull, cfg, render_cfg=rcfg, masks=masks, bbox=bbox)
+        np.testing.assert_allclose(tb.rmse, ta.rmse, rtol=1e-6)
+        assert rel_err(b.values, a.values) <= 1e-5
+    rgb = [Image(im.shape[1], im.shape[0], 3, im) for im in g["images"]]
+    cfg = ReconstructionConfig(alpha_l=0.006, tau=float(g["tau"]), max_iters=5, converge_eps=1e-12,
+                               deterministic_mode=True)
+    monkeypatch.setenv("FVR_RENDER", "march")
+    a = reconstruct_color(rgb, cams, geom, cfg, render_cfg=rcfg)
+    monkeypatch.setenv("FVR_RENDER", "plan")
+    b = reconstruct_color(rgb, cams, geom, cfg, render_cfg=rcfg)
+    for c, tag in enumerate(("red", "green", "blue")):
+        np.testing.assert_allclose(b.traces[tag].rmse, a.traces[tag].rmse, rtol=1e-6)
+        assert rel_err(b.grids[c].values, a.grids[c].values) <= 1e-5
