@@ -251,9 +251,19 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
 
 // K-render through the plan: one warp per unit, lane = pixel; rec = B c +
 // base + t_fin bg, then the same residual / squared-residual epilogue as the
-// marching kernel.  Products in fp32, summed in fp64 eight at a time.
+// marching kernel.  Products in fp32, summed in fp64 a batch at a time.
+// 32 entries per lane in flight per batch (config 2: B = 8 / 16 / 24 / 32 / 64:
+// 0.163 / 0.164 / 0.156 / 0.154 / 0.178 ms); ptxas keeps the batch's loads ahead
+// of their uses only with the registers to hold them (3 CTAs/SM, 80 regs).
+#ifndef FVR_RPLAN_BATCH
+#define FVR_RPLAN_BATCH 32
+#endif
+#ifndef FVR_RPLAN_MINB
+#define FVR_RPLAN_MINB 3
+#endif
+
 template <int NCH>
-__global__ void __launch_bounds__(256) rplan_render_kernel(
+__global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
     const int* __restrict__ unit_len, const long long* __restrict__ unit_off, const int2* __restrict__ entries,
     const double* __restrict__ base, const double* __restrict__ t_fin, int n_units, int units_x,
     int units_per_view, int n_views, int w, int h, const float* __restrict__ src, const float* __restrict__ values,
@@ -270,15 +280,16 @@ __global__ void __launch_bounds__(256) rplan_render_kernel(
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
         int t = 0;
-        for (; t + 8 <= len; t += 8) {
-            int2 en[8];
+        constexpr int B = FVR_RPLAN_BATCH;
+        for (; t + B <= len; t += B) {
+            int2 en[B];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) en[i] = __ldcs(e + (int64_t)(t + i) * 32);
+            for (int i = 0; i < B; ++i) en[i] = __ldcs(e + (int64_t)(t + i) * 32);
             float part[NCH];
 #pragma unroll
             for (int c = 0; c < NCH; ++c) part[c] = 0.f;
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < B; ++i)
 #pragma unroll
                 for (int c = 0; c < NCH; ++c)
                     part[c] = fmaf(__int_as_float(en[i].y), fmaxf(__ldg(values + c * plane + en[i].x), 0.f), part[c]);
