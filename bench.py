@@ -39,10 +39,12 @@ SIGMA_S = 0.1
 SCAT_DIRS = 32
 TAU = 1.0 - 0.95 ** (64.0 / N_VOX)
 ALPHA_L = 0.006
-# dram__bytes_read.sum + dram__bytes_write.sum of loop_render_scat_kernel from one
-# `ncu --set full` capture (profiles/r1_ncu_render_final_raw.csv)
-TRAFFIC_BYTES_PER_LAUNCH = 10_210_304
-TRAFFIC_SOURCE = "profiles/r1_ncu_render_final_raw.csv (round 1)"
+# dram__bytes_read.sum + dram__bytes_write.sum of K-render from one `ncu --set full`
+# capture: the render-plan SpMV (profiles/r1_ncu_rplan_raw.csv) and the marching
+# kernel it replaced (profiles/r1_ncu_render_final_raw.csv)
+TRAFFIC_BYTES_PER_LAUNCH = {"rplan_render_kernel<1>": 732_744_448, "loop_render_scat_kernel": 10_210_304}
+TRAFFIC_SOURCE = {"rplan_render_kernel<1>": "profiles/r1_ncu_rplan_raw.csv (round 1)",
+                  "loop_render_scat_kernel": "profiles/r1_ncu_render_final_raw.csv (round 1)"}
 METRIC = "recon iters/sec at 128³×8 views 512²; Gsamples/s; % of HBM roofline"
 WORKLOAD = "config 2: 128^3 flame, 8 views 512x512, full RTE (sigma_s 0.1, 32 dirs), green channel"
 
@@ -349,6 +351,20 @@ def run_gpu(args):
     live = w.get("S_r_live", w["S_r"])
     live_bytes = 108 * live + (w["S_r"] - live) + 8 * w["VP"]
     live_achieved = live_bytes / (render_ms * 1e-3) / 1e9
+    if loop.rplan:
+        kname = "rplan_render_kernel<1>"
+        rows = loop.rp_len.numel() * 32
+        kbytes = 8 * loop.rplan_nnz + 16 * rows + 8 * w["VP"]
+        rule = ("render plan: 8 B per stored SELL entry (key point, f32 weight) + 16 B per row (base, t_fin) + "
+                "8 B per bbox pixel (src in, residual out); the lattice gathers hit L2")
+    else:
+        kname = "loop_render_scat_kernel"
+        kbytes = live_bytes
+        rule = "108 B per live sample + 1 B per skipped sample + 8 B per bbox pixel (marching kernel)"
+    kach = kbytes / (render_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": kname, "achieved": kach, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+            "frac": kach / peak, "traffic": TRAFFIC_BYTES_PER_LAUNCH[kname], "traffic_source": TRAFFIC_SOURCE[kname],
+            "bytes_per_launch": kbytes, "bytes_rule": rule}
 
     # e2e: the public API with host buffers (H2D of inputs, D2H of the grid)
     e2e = None
@@ -416,22 +432,23 @@ def run_gpu(args):
         "stage_ms": part_ms,
         "iter_algorithmic_bytes": iter_bytes,
         "iter_roofline_frac": iter_bytes * its / (peak * 1e9),
-        # Dominant kernel = K-render.  Units one launch processes: the live
-        # samples (27-key-point stencil, 108 B each) plus one occupancy-probe
-        # byte per skipped sample (empty-space skipping never reads their
-        # stencil), and 8 B per bbox pixel (src in, residual out).
-        "roofline": {"bound": "hbm", "kernel": "loop_render_scat_kernel", "achieved": live_achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": live_achieved / peak,
-                     "traffic": TRAFFIC_BYTES_PER_LAUNCH, "traffic_source": TRAFFIC_SOURCE,
-                     "bytes_per_launch": live_bytes,
-                     "bytes_rule": "SURVEY 8(d) per-sample figure over the samples K-render processes: 108 B per "
-                                   "live sample + 1 B per skipped sample + 8 B per bbox pixel; the lattice is "
-                                   "L2-resident (DRAM traffic ~10 MB/launch) and the kernel is issue-bound"},
+        # Dominant kernel = K-render.  Through the render plan it streams B
+        # (8 B per stored SELL entry, padding included) plus per-row base and
+        # t_fin (16 B) and src/residual (8 B per pixel); the lattice it
+        # multiplies is L2-resident.
+        "roofline": roof,
+        "roofline_survey_rule": {"bytes_per_launch": live_bytes, "achieved": live_achieved,
+                                 "frac": live_achieved / peak,
+                                 "rule": "SURVEY 8(d) per-sample figure: 108 B per live sample + 1 B per skipped "
+                                         "sample + 8 B per bbox pixel, over the same K-render time"},
         "roofline_dense_equiv": {"bytes_per_launch": render_bytes, "achieved": achieved, "frac": achieved / peak,
                                  "rule": "108 B for every render sample S_r as if none were skipped (the "
                                          "reference's work), over the same K-render time"},
         "gpu_launches": int(launches),
-        "adjust_path": "voxel-driven gather (CSR plan, nnz %d)" % loop.plan_nnz if loop.plan else "ray-driven scatter",
+        "render_path": ("render plan (SELL-32, %d stored entries)" % loop.rplan_nnz) if loop.rplan
+        else "marching kernel",
+        "adjust_path": ("voxel-driven gather (SELL-32 plan, nnz %d, %d stored)" % (loop.plan_nnz, loop.plan_slots))
+        if loop.plan else "ray-driven scatter",
         "clocks": clocks,
         "stochastic": stoch,
         "e2e": e2e,

@@ -258,8 +258,8 @@ int fvr_adjust_plan_count(const fvr_camera_t* cams, const int32_t* ray_list, int
 int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
                          int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
                          const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
-                         double alpha_d, const int32_t* kp_map, int64_t* cursor, int32_t* entries,
-                         void* stream);
+                         double alpha_d, const int32_t* kp_map, const int32_t* row_pos,
+                         const int64_t* slice_off, int64_t* cursor, int32_t* entries, void* stream);
 /* Stochastic mode (random G, reconstruct.py:193-201): the sample plan.
  * Count: per-row entry counts (8 per in-hull sample) and per-ray in-hull
  * sample counts.  Fill (ray_sid0 = exclusive scan of ray_samples): entries
@@ -276,22 +276,28 @@ int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int6
                          int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
                          const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
                          double alpha_d, const int32_t* kp_map, const int64_t* ray_sid0,
-                         int64_t* cursor, int32_t* entries, int32_t* sample_meta, void* stream);
+                         const int32_t* row_pos, const int64_t* slice_off, int64_t* cursor,
+                         int32_t* entries, int32_t* sample_meta, void* stream);
 int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, const int32_t* ray_list,
                                int32_t bbox_w, int32_t bbox_h, const float* residual, int32_t n_channels,
                                uint64_t seed, double g_sigma, int64_t ray_id_base, float* rho,
                                const fvr_loop_state_t* state, void* stream);
-/* Per iteration: row sums in 32.32 fixed point; with packed == NULL the
+/* Plans are SELL-32 (fvr_plan.cu): rows (hull key points) sorted by length,
+ * row_pos[row] = sorted position, row_of_pos its inverse, slices of 32
+ * positions with slice_len (longest row) and slice_off (exclusive scan, in
+ * units of 32 entries); entry t of position p at slice_off[p/32]*32 + 32t +
+ * p%32; cursor (n_rows i64, zeroed) counts the entries written per row.
+ * Per iteration: row sums in 32.32 fixed point; with packed == NULL the
  * clamped update is applied in place (and the packed layout refreshed),
  * otherwise the sums go to packed (n_channels, n_kp) for the multi-GPU
  * all-reduce.  n_channels (1 or 3) share the plan: the residual (or rho)
  * holds a pixel's (sample's) channels interleaved with pitch 1 or 4, values /
  * layout hold n_channels lattice planes and state n_channels loop states
  * (converged channels are skipped). */
-int fvr_loop_gather(const int64_t* row_offsets, const int32_t* entries, int64_t n_kp,
-                    const float* residual, int32_t n_channels, const int32_t* kp_index, float* values,
-                    float* layout, int32_t layout_kind, fvr_grid_t grid, int64_t* packed,
-                    const fvr_loop_state_t* state, void* stream);
+int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_off, const int32_t* row_of_pos,
+                    const int32_t* entries, int64_t n_kp, const float* residual, int32_t n_channels,
+                    const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
+                    fvr_grid_t grid, int64_t* packed, const fvr_loop_state_t* state, void* stream);
 int fvr_loop_update_packed(const int64_t* packed, int64_t n_kp, const int32_t* kp_index,
                            float* values, float* layout, int32_t layout_kind, int32_t layout_nch,
                            fvr_grid_t grid, const fvr_loop_state_t* state, void* stream);

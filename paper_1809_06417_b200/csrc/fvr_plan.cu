@@ -158,18 +158,31 @@ __global__ void __launch_bounds__(128) plan_count_kernel(
                        [&](int kp, float) { atomicAdd(counts + kp_map[kp], 1); });
 }
 
+// Plans are stored SELL-32: rows (hull key points) sorted longest first and
+// cut into slices of 32; entry t of the row at sorted position p sits at
+// slice_off[p / 32] * 32 + 32 t + p % 32, so a warp streams a slice with
+// fully coalesced loads, one lane per row (padding entries are (0, 0.0)).
+struct SellMap {
+    const int32_t* row_pos;          // row -> sorted position
+    const long long* slice_off;      // per slice, in units of 32 entries
+    unsigned long long* cursor;      // per row, entries written so far
+    __device__ __forceinline__ long long slot(int row) const {
+        const int p = row_pos[row];
+        const unsigned long long t = atomicAdd(cursor + row, 1ull);
+        return slice_off[p >> 5] * 32 + (long long)t * 32 + (p & 31);
+    }
+};
+
 __global__ void __launch_bounds__(128) plan_fill_kernel(
     const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
     int u0, int v0, int w, int h, const uint8_t* __restrict__ inside, Geom g, double tau_keep,
-    double alpha_l, float alpha_d, const int32_t* __restrict__ kp_map,
-    unsigned long long* __restrict__ cursor, int2* __restrict__ entries) {
+    double alpha_l, float alpha_d, const int32_t* __restrict__ kp_map, SellMap sm, int2* __restrict__ entries) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_rays) return;
     PlanRay pr;
     plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
     ray_entries<true>(pr, g, inside, tau_keep, alpha_l, alpha_d, [&](int kp, float wgt) {
-        const unsigned long long pos = atomicAdd(cursor + kp_map[kp], 1ull);
-        entries[pos] = make_int2(pr.res_index, __float_as_int(wgt));
+        entries[sm.slot(kp_map[kp])] = make_int2(pr.res_index, __float_as_int(wgt));
     });
 }
 
@@ -205,7 +218,7 @@ __global__ void __launch_bounds__(128) splan_fill_kernel(
     const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
     int u0, int v0, int w, int h, const uint8_t* __restrict__ inside, Geom g, double tau_keep,
     double alpha_l, float alpha_d, const int32_t* __restrict__ kp_map, const long long* __restrict__ ray_sid0,
-    unsigned long long* __restrict__ cursor, int2* __restrict__ entries, int2* __restrict__ meta) {
+    SellMap sm, int2* __restrict__ entries, int2* __restrict__ meta) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_rays) return;
     PlanRay pr;
@@ -228,8 +241,7 @@ __global__ void __launch_bounds__(128) splan_fill_kernel(
             const int cx = k8 >> 2, cy = (k8 >> 1) & 1, cz = k8 & 1;
             const float dist = sqrtf(fmaf(e[0][cx], e[0][cx], fmaf(e[1][cy], e[1][cy], e[2][cz] * e[2][cz])));
             const float wgt = base * expf(-alpha_d * dist);
-            const unsigned long long pos = atomicAdd(cursor + kp_map[base_kp + cx * g.sx + cy * g.sy + cz], 1ull);
-            entries[pos] = make_int2((int)sid, __float_as_int(wgt));
+            entries[sm.slot(kp_map[base_kp + cx * g.sx + cy * g.sy + cz])] = make_int2((int)sid, __float_as_int(wgt));
         }
         ++sid;
     });
@@ -267,20 +279,19 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
     }
 }
 
-// One group of G lanes per hull key point: delta = sum_e res[idx_e] * W_e
-// (32.32 fixed point, so any grouping of the sum gives the same bits).  Each
-// lane keeps U independent streaming loads in flight; a row is three
-// dependent round trips (plan -> residual -> value), so the kernel is bound
-// by how many rows are in flight: G = 4 puts eight rows in each warp
-// (config 2: G=32 0.113 ms, 16 0.098, 8 0.094, 4 0.092, 2 0.122).
 // NCH channels share the plan (A depends only on geometry and hull): each
 // entry is read once and multiplies NCH residuals (interleaved per pixel /
 // sample: one 16-byte load for three channels); values / layout are NCH
 // lattice planes, packed (NCH, n_rows), state NCH loop states (a converged
-// channel is left untouched).
-template <bool PACKED, int G, int U, int NCH>
-__global__ void __launch_bounds__(256) gather_kernel(
-    const long long* __restrict__ row_off, const int2* __restrict__ entries, int64_t n_rows,
+// channel is left untouched).  One warp per SELL slice, one lane per row,
+// delta = sum_e res[idx_e] * W_e in 32.32 fixed point (order-independent).
+#ifndef FVR_GATHER_BATCH
+#define FVR_GATHER_BATCH 32
+#endif
+template <bool PACKED, int NCH>
+__global__ void __launch_bounds__(256, 3) gather_kernel(
+    const int32_t* __restrict__ slice_len, const long long* __restrict__ slice_off,
+    const int32_t* __restrict__ row_of_pos, const int2* __restrict__ entries, int64_t n_rows,
     const float* __restrict__ residual, const int32_t* __restrict__ kp_index,
     float* __restrict__ values, int64_t plane, float* __restrict__ layout, int layout_kind, int sy, int ny1,
     long long* __restrict__ packed, const fvr_loop_state_t* __restrict__ state) {
@@ -293,53 +304,46 @@ __global__ void __launch_bounds__(256) gather_kernel(
     }
     if (!any) return;
     const int lane = threadIdx.x & 31;
-    const int sub = lane & (G - 1);
-    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
-    const int64_t group = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-    const int64_t n_groups = ((int64_t)gridDim.x * blockDim.x) / G;
-    for (int64_t row = group; row < n_rows; row += n_groups) {
-        const long long b = row_off[row], e = row_off[row + 1];
+    const int64_t n_slices = (n_rows + 31) >> 5;
+    constexpr int B = FVR_GATHER_BATCH;
+    for (int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < n_slices;
+         sl += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int len = slice_len[sl];
+        const int2* e = entries + slice_off[sl] * 32 + lane;
         long long acc[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = 0;
-        // the plan is read once per iteration: evict-first, keep L2 for the residual
-        for (long long base = b; base < e; base += G * U) {
-            int2 en[U];
+        for (int t = 0; t < len; t += B) {
+            int2 en[B];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const long long i = base + sub + G * u;
-                en[u] = i < e ? __ldcs(entries + i) : make_int2(0, 0);
-            }
+            for (int i = 0; i < B; ++i) en[i] = t + i < len ? __ldcs(e + (int64_t)(t + i) * 32) : make_int2(0, 0);
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const float wgt = __int_as_float(en[u].y);
+            for (int i = 0; i < B; ++i) {
+                const float wgt = __int_as_float(en[i].y);
                 if (NCH == 1) {
-                    acc[0] += __float2ll_rn(__ldg(residual + en[u].x) * wgt * 4294967296.0f);
+                    acc[0] += __float2ll_rn(__ldg(residual + en[i].x) * wgt * 4294967296.0f);
                 } else {
-                    const float4 r = __ldg(reinterpret_cast<const float4*>(residual) + en[u].x);
+                    const float4 r = __ldg(reinterpret_cast<const float4*>(residual) + en[i].x);
                     const float rr[3] = {r.x, r.y, r.z};
 #pragma unroll
                     for (int c = 0; c < NCH; ++c) acc[c] += __float2ll_rn(rr[c] * wgt * 4294967296.0f);
                 }
             }
         }
+        const int64_t pos = sl * 32 + lane;
+        if (pos >= n_rows) continue;
+        const int64_t row = row_of_pos[pos];
 #pragma unroll
-        for (int c = 0; c < NCH; ++c)
-#pragma unroll
-            for (int off = G / 2; off > 0; off >>= 1) acc[c] += __shfl_xor_sync(gmask, acc[c], off);
-        if (sub == 0) {
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-                if (PACKED) {
-                    packed[c * n_rows + row] = acc[c];
-                } else if (live[c] && acc[c] != 0) {
-                    const int64_t idx = kp_index[row];
-                    float* vals = values + c * plane;
-                    const double nv = (double)vals[idx] + (double)acc[c] * kFixInv;
-                    const float f = (float)(nv > -1.0 ? nv : -1.0);
-                    vals[idx] = f;
-                    if (layout) layout_store(layout + 4 * c, NCH, layout_kind, sy, ny1, idx, f);
-                }
+        for (int c = 0; c < NCH; ++c) {
+            if (PACKED) {
+                packed[c * n_rows + row] = acc[c];
+            } else if (live[c] && acc[c] != 0) {
+                const int64_t idx = kp_index[row];
+                float* vals = values + c * plane;
+                const double nv = (double)vals[idx] + (double)acc[c] * kFixInv;
+                const float f = (float)(nv > -1.0 ? nv : -1.0);
+                vals[idx] = f;
+                if (layout) layout_store(layout + 4 * c, NCH, layout_kind, sy, ny1, idx, f);
             }
         }
     }
@@ -385,59 +389,44 @@ extern "C" int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray
                                     int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
                                     const uint8_t* inside_vox, fvr_grid_t grid, double tau,
                                     double alpha_l, double alpha_d, const int32_t* kp_map,
-                                    int64_t* cursor, int32_t* entries, void* stream) {
+                                    const int32_t* row_pos, const int64_t* slice_off, int64_t* cursor,
+                                    int32_t* entries, void* stream) {
     FVR_TRY_BEGIN
     if (int rc = check_grid(grid)) return rc;
     if (n_rays == 0) return FVR_OK;
     const Geom g = make_geom(grid);
     plan_fill_kernel<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
         cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d,
-        kp_map, reinterpret_cast<unsigned long long*>(cursor), reinterpret_cast<int2*>(entries));
+        kp_map,
+        SellMap{row_pos, reinterpret_cast<const long long*>(slice_off), reinterpret_cast<unsigned long long*>(cursor)},
+        reinterpret_cast<int2*>(entries));
     return check_launch("adjust_plan_fill");
     FVR_TRY_END
 }
 
-extern "C" int fvr_loop_gather(const int64_t* row_offsets, const int32_t* entries, int64_t n_kp,
-                               const float* residual, int32_t n_channels,
+extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_off, const int32_t* row_of_pos,
+                               const int32_t* entries, int64_t n_kp, const float* residual, int32_t n_channels,
                                const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
                                fvr_grid_t grid, int64_t* packed, const fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
     if (n_kp == 0) return FVR_OK;
     if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "the loop gathers 1 or 3 channels");
-    static int group_lanes = 0;
-    if (!group_lanes) {
-        const char* e = getenv("FVR_GATHER_G");
-        group_lanes = e ? atoi(e) : 4;
-        if (group_lanes != 4 && group_lanes != 8 && group_lanes != 16 && group_lanes != 32) group_lanes = 4;
-    }
-    int64_t blocks = (n_kp * group_lanes + 255) / 256;
-    if (blocks > 148 * 64) blocks = 148 * 64;
+    const int64_t n_slices = (n_kp + 31) / 32;
+    int64_t blocks = (n_slices * 32 + 255) / 256;
+    if (blocks > 148 * 24) blocks = 148 * 24;
     const int sy = grid.nz + 1, ny1 = grid.ny + 1;
     const int64_t plane = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
     cudaStream_t st = (cudaStream_t)stream;
-    const auto* ro = reinterpret_cast<const long long*>(row_offsets);
+    const auto* so = reinterpret_cast<const long long*>(slice_off);
     const auto* en = reinterpret_cast<const int2*>(entries);
     long long* pk = reinterpret_cast<long long*>(packed);
-#define FVR_GATHER(GL, UL, C)                                                                                  \
-    do {                                                                                                     \
-        if (packed)                                                                                          \
-            gather_kernel<true, GL, UL, C><<<(unsigned)blocks, 256, 0, st>>>(                                 \
-                ro, en, n_kp, residual, kp_index, values, plane, layout, layout_kind, sy, ny1, pk,             \
-                state);                                                                                      \
-        else                                                                                                 \
-            gather_kernel<false, GL, UL, C><<<(unsigned)blocks, 256, 0, st>>>(                                \
-                ro, en, n_kp, residual, kp_index, values, plane, layout, layout_kind, sy, ny1,                \
-                nullptr, state);                                                                             \
-    } while (0)
-    if (n_channels == 3) {
-        FVR_GATHER(4, 16, 3);
+#define FVR_GATHER(P, C)                                                                                           \
+    gather_kernel<P, C><<<(unsigned)blocks, 256, 0, st>>>(slice_len, so, row_of_pos, en, n_kp, residual, kp_index, \
+                                                          values, plane, layout, layout_kind, sy, ny1, pk, state)
+    if (packed) {
+        if (n_channels == 1) FVR_GATHER(true, 1); else FVR_GATHER(true, 3);
     } else {
-        switch (group_lanes) {
-            case 8: FVR_GATHER(8, 16, 1); break;
-            case 16: FVR_GATHER(16, 8, 1); break;
-            case 32: FVR_GATHER(32, 4, 1); break;
-            default: FVR_GATHER(4, 32, 1); break;
-        }
+        if (n_channels == 1) FVR_GATHER(false, 1); else FVR_GATHER(false, 3);
     }
 #undef FVR_GATHER
     return check_launch("loop_gather");
@@ -476,14 +465,16 @@ extern "C" int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray
                                     int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
                                     const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
                                     double alpha_d, const int32_t* kp_map, const int64_t* ray_sid0,
-                                    int64_t* cursor, int32_t* entries, int32_t* sample_meta, void* stream) {
+                                    const int32_t* row_pos, const int64_t* slice_off, int64_t* cursor,
+                                    int32_t* entries, int32_t* sample_meta, void* stream) {
     FVR_TRY_BEGIN
     if (int rc = check_grid(grid)) return rc;
     if (n_rays == 0) return FVR_OK;
     const Geom g = make_geom(grid);
     splan_fill_kernel<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
         cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d, kp_map,
-        reinterpret_cast<const long long*>(ray_sid0), reinterpret_cast<unsigned long long*>(cursor),
+        reinterpret_cast<const long long*>(ray_sid0),
+        SellMap{row_pos, reinterpret_cast<const long long*>(slice_off), reinterpret_cast<unsigned long long*>(cursor)},
         reinterpret_cast<int2*>(entries), reinterpret_cast<int2*>(sample_meta));
     return check_launch("sample_plan_fill");
     FVR_TRY_END

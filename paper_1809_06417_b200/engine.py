@@ -418,31 +418,50 @@ class ChannelLoop:
                       stream)
         else:
             _lib.call("fvr_adjust_plan_count", *geo, kp_map.data_ptr(), counts.data_ptr(), stream)
-        offsets = t.zeros(self.n_kp + 1, dtype=t.int64, device=dev)
-        offsets[1:] = t.cumsum(counts.long(), 0)
-        nnz = int(offsets[-1].item())
+        # SELL-32 layout: slices of 32 rows; FVR_SELL_SORT=1 sorts rows longest
+        # first (least padding), else key-point order (neighbouring rows share
+        # rays, so their residual / rho reads share cache lines)
+        if os.environ.get("FVR_SELL_SORT", "0") == "1":
+            order = t.argsort(counts, descending=True)
+        else:
+            order = t.arange(self.n_kp, device=dev)
+        row_of_pos = order.to(t.int32)
+        row_pos = t.empty_like(row_of_pos)
+        row_pos[order] = t.arange(self.n_kp, dtype=t.int32, device=dev)
+        n_slices = (self.n_kp + 31) // 32
+        slice_len = t.zeros(n_slices * 32, dtype=t.int32, device=dev)
+        slice_len[: self.n_kp] = counts[order]
+        slice_len = slice_len.view(n_slices, 32).amax(1).contiguous()
+        slice_off = t.zeros(n_slices + 1, dtype=t.int64, device=dev)
+        slice_off[1:] = t.cumsum(slice_len.long(), 0)
+        slots = int(slice_off[-1].item()) * 32
+        nnz = int(counts.long().sum().item())
         n_samples = int(ray_samples.long().sum().item()) if self.sample_plan else 0
         free = t.cuda.mem_get_info(dev)[0]
-        need = 8 * nnz + 12 * n_samples
+        need = 8 * slots + 12 * n_samples
         if need > min(self.PLAN_MAX_BYTES, free // 2) or n_samples >= 2 ** 31:
             return False
-        cursor = offsets[:-1].clone()
-        entries = t.empty(max(2 * nnz, 2), dtype=t.int32, device=dev)
+        cursor = t.zeros(self.n_kp, dtype=t.int64, device=dev)
+        entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
+        sell = (row_pos.data_ptr(), slice_off.data_ptr(), cursor.data_ptr(), entries.data_ptr())
         if self.sample_plan:
             sid0 = t.zeros(self.n_rays, dtype=t.int64, device=dev)
             sid0[1:] = t.cumsum(ray_samples[:-1].long(), 0)
             meta = t.empty(max(2 * n_samples, 2), dtype=t.int32, device=dev)
             _lib.call("fvr_sample_plan_fill", *geo, c.tau, c.alpha_l, c.alpha_d_eff, kp_map.data_ptr(),
-                      sid0.data_ptr(), cursor.data_ptr(), entries.data_ptr(), meta.data_ptr(), stream)
+                      sid0.data_ptr(), *sell, meta.data_ptr(), stream)
             self.sample_meta = meta
             self.n_samples = n_samples
             self.rho = t.zeros((max(n_samples, 1), self.pitch), dtype=t.float32, device=dev)
         else:
-            _lib.call("fvr_adjust_plan_fill", *geo, c.tau, c.alpha_l, c.alpha_d_eff, kp_map.data_ptr(),
-                      cursor.data_ptr(), entries.data_ptr(), stream)
-        self.plan_offsets = offsets
+            _lib.call("fvr_adjust_plan_fill", *geo, c.tau, c.alpha_l, c.alpha_d_eff, kp_map.data_ptr(), *sell,
+                      stream)
+        self.plan_slice_len = slice_len
+        self.plan_slice_off = slice_off
+        self.plan_row_of_pos = row_of_pos
         self.plan_entries = entries
         self.plan_nnz = nnz
+        self.plan_slots = slots
         return True
 
     def _weigh(self, stream):
@@ -458,7 +477,8 @@ class ChannelLoop:
         if self.n_kp == 0:
             return 0
         src = self.rho if self.sample_plan else self.residual
-        _lib.call("fvr_loop_gather", self.plan_offsets.data_ptr(), self.plan_entries.data_ptr(), self.n_kp,
+        _lib.call("fvr_loop_gather", self.plan_slice_len.data_ptr(), self.plan_slice_off.data_ptr(),
+                  self.plan_row_of_pos.data_ptr(), self.plan_entries.data_ptr(), self.n_kp,
                   src.data_ptr(), self.nch, self.kp.data_ptr(), self.values.data_ptr(),
                   _lib.ptr(self.layout), self.layout_kind, self.grid, self.packed.data_ptr() if packed else None,
                   self.state.data_ptr(), stream)
