@@ -755,6 +755,15 @@ int build_moment_tables(const double* dirs) {
                     q3[(((size_t)i * K + j) * K + l) * 8 + e] = (float)acc;
                 }
             }
+    uint32_t nmask[3][K];
+    for (int a = 0; a < 3; ++a)
+        for (int i = 0; i < K; ++i) {
+            uint32_t m = 0;
+            for (int sdir = 0; sdir < S; ++sdir)
+                if (rank[a][sdir] < i) m |= 1u << sdir;
+            nmask[a][i] = m;
+        }
+    if (cudaMemcpyToSymbol(c_nmask, nmask, sizeof(nmask)) != cudaSuccess) return set_error(FVR_ERR_CUDA, "upload");
     if (cudaMemcpyToSymbol(c_thr, thr, sizeof(thr)) != cudaSuccess ||
         cudaMemcpyToSymbol(c_q0, q0, sizeof(q0)) != cudaSuccess ||
         cudaMemcpyToSymbol(g_q1, q1.data(), q1.size() * sizeof(float)) != cudaSuccess ||

@@ -75,21 +75,78 @@ __device__ __forceinline__ void shift3(float& a0, float& a1, float& a2, int delt
     a2 = delta > 0 ? 0.f : (delta < 0 ? o1 : o2);
 }
 
+// the same shift on a 27-bit slot mask (bit (ox*9 + oy*3 + oz))
+__device__ __forceinline__ uint32_t shift_mask(uint32_t m, int dx, int dy, int dz) {
+    constexpr uint32_t kZ0 = 0x1249249u, kZ2 = kZ0 << 2;
+    constexpr uint32_t kY0 = 0x7u | (0x7u << 9) | (0x7u << 18), kY2 = kY0 << 6;
+    constexpr uint32_t kX0 = 0x1FFu, kX2 = kX0 << 18;
+    if (dz > 0) m = (m >> 1) & ~kZ2;
+    else if (dz < 0) m = (m << 1) & ~kZ0;
+    if (dy > 0) m = (m >> 3) & ~kY2;
+    else if (dy < 0) m = (m << 3) & ~kY0;
+    if (dx > 0) m = (m >> 9) & ~kX2;
+    else if (dx < 0) m = (m << 9) & ~kX0 & 0x7FFFFFFu;
+    return m & 0x7FFFFFFu;
+}
+
+// Slots whose weight can be non-zero: the trilinear corners of the sample
+// (emission) and, with scattering, every slot some gather point reaches.  A
+// gather point x_s = delta + s/2 gives slot offset -1 weight iff x_s < 0 and
+// +1 iff x_s > 0 per axis; the directions with x_s < 0 on axis a are the
+// first split_index ones in that axis' sorted order (nm[a][i]), so slot
+// (jx, jy, jz) is reached iff the three per-axis direction sets intersect.
+// Depends on the geometry only: the count pass needs no weights.
+__device__ __forceinline__ uint32_t support_mask(bool scat, const float dl[3], const float* __restrict__ thr,
+                                                 const uint32_t* __restrict__ nm) {
+    uint32_t ax[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ax[a] = 2u | (dl[a] > 0.f ? 4u : 0u) | (dl[a] < 0.f ? 1u : 0u);  // slot bits 0..2
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < 27; ++j)
+        if (((ax[0] >> (j / 9)) & (ax[1] >> ((j / 3) % 3)) & (ax[2] >> (j % 3))) & 1u) m |= 1u << j;
+    if (scat) {
+        uint32_t S[3][3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const uint32_t neg = nm[a * (kScatDirs + 1) + split_index(thr + a * kScatDirs, -dl[a])];
+            S[a][0] = neg;
+            S[a][1] = 0xffffffffu;
+            S[a][2] = ~neg;  // x_s >= 0 (a zero coordinate only adds a zero-weight entry)
+        }
+#pragma unroll
+        for (int jx = 0; jx < 3; ++jx)
+#pragma unroll
+            for (int jy = 0; jy < 3; ++jy) {
+                const uint32_t sxy = S[0][jx] & S[1][jy];
+#pragma unroll
+                for (int jz = 0; jz < 3; ++jz)
+                    if (sxy & S[2][jz]) m |= 1u << ((jx * 3 + jy) * 3 + jz);
+            }
+    }
+    return m;
+}
+
 // Walk one pixel's ray exactly as K-render samples it and produce its row of
-// B.  FILL = false only counts the entries.  `dynamic` marks the key points
-// whose value can change (the loop's hull key points); the others contribute
-// max(v, 0) * weight to base[c] (values: nch lattice planes).  Returns the
-// entry count; t_fin receives the transparency after the last sample.
+// B.  Which entries a row holds depends only on the geometry (a slot holds an
+// entry once a sample whose support covers it placed a `dynamic` key point
+// there), so FILL = false counts them without evaluating any weight.  The
+// key points not in `dynamic` (the loop's hull key points) contribute
+// max(v, 0) * weight to base[c] (values: nch lattice planes).  Interior
+// scattering samples take their 27 weights from the moment form
+// (moment_omega), face samples from the direct masked sum.  Returns the entry
+// count; t_fin receives the transparency after the last sample.
 template <bool SCAT, bool FILL>
 __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, const RenderConsts& rc,
                          const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
-                         const float* __restrict__ values, int nch, int64_t plane, int2* __restrict__ out,
-                         double* base, double& t_fin) {
+                         const float* __restrict__ values, int nch, int64_t plane, const float* __restrict__ thr,
+                         const uint32_t* __restrict__ nm, int2* __restrict__ out, double* base, double& t_fin) {
     int count = 0;
     double t_dst = 1.0;
     float acc[27];
 #pragma unroll
     for (int j = 0; j < 27; ++j) acc[j] = 0.f;
+    uint32_t live = 0;      // slots of the window holding an entry
     int wm[3] = {0, 0, 0};  // window centre (nearest key point of the last merged sample)
     bool have = false;
     const float sig_a = (float)rc.sigma_a, kappa = (float)rc.scat_scale;
@@ -97,14 +154,15 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
         if (FILL) out[(int64_t)count * 32] = make_int2(kp, __float_as_int(wt));
         ++count;
     };
+    auto slot_kp = [&](int j) { return wm[0] * g.sx + wm[1] * g.sy + wm[2] + (j / 9 - 1) * g.sx + ((j / 3) % 3 - 1) * g.sy + (j % 3 - 1); };
     auto flush = [&]() {
         if (!have) return;
-        const int base_kp = wm[0] * g.sx + wm[1] * g.sy + wm[2];
 #pragma unroll
         for (int j = 0; j < 27; ++j) {
-            if (acc[j] != 0.f) put(base_kp + (j / 9 - 1) * g.sx + ((j / 3) % 3 - 1) * g.sy + (j % 3 - 1), acc[j]);
-            acc[j] = 0.f;
+            if ((live >> j) & 1u) put(slot_kp(j), FILL ? acc[j] : 0.f);
+            if (FILL) acc[j] = 0.f;
         }
+        live = 0;
         have = false;
     };
     double te, tx;
@@ -129,28 +187,31 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
             }
             const int mlin = m[0] * g.sx + m[1] * g.sy + m[2];
             if (occ && __ldg(occ + mlin) > 1) continue;  // no key point of the stencil can be non-zero
-            uint32_t mask = 0xffffffffu;
-            if (SCAT && !interior) {
-                double p[3];
-                sample_pos(o, d, te, g.edge, k, p);
-                mask = inbox_mask(p, g, rc.half_gather);
-            }
-            float w[27];
-            sample_weights<SCAT>(dl[0], dl[1], dl[2], sig_a, kappa, mask, w);
+            const uint32_t sup = support_mask(SCAT, dl, thr, nm);
             const float scale = (float)(t_dst * rc.tau);
+            float w[27];
             if (!interior) {
                 // within half a voxel of a box face: clamped stencil, entries unmerged
                 flush();
+                if (FILL) {
+                    uint32_t inbox = 0xffffffffu;
+                    if (SCAT) {
+                        double p[3];
+                        sample_pos(o, d, te, g.edge, k, p);
+                        inbox = inbox_mask(p, g, rc.half_gather);
+                    }
+                    sample_weights<SCAT>(dl[0], dl[1], dl[2], sig_a, kappa, inbox, w);
+                }
 #pragma unroll 1
                 for (int j = 0; j < 27; ++j) {
-                    const float wt = w[j] * scale;
-                    if (wt == 0.f) continue;
+                    if (!((sup >> j) & 1u)) continue;
                     const int x = min(max(m[0] + j / 9 - 1, 0), g.nx), y = min(max(m[1] + (j / 3) % 3 - 1, 0), g.ny),
                               z = min(max(m[2] + j % 3 - 1, 0), g.nz);
                     const int kp = x * g.sx + y * g.sy + z;
+                    const float wt = FILL ? w[j] * scale : 0.f;
                     if (__ldg(dynamic + kp)) {
                         put(kp, wt);
-                    } else {
+                    } else if (FILL) {
                         for (int c = 0; c < nch; ++c) base[c] += (double)wt * fmaxf(__ldg(values + c * plane + kp), 0.f);
                     }
                 }
@@ -160,22 +221,28 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
             const int dx = m[0] - wm[0], dy = m[1] - wm[1], dz = m[2] - wm[2];
             if (have && abs(dx) <= 1 && abs(dy) <= 1 && abs(dz) <= 1) {
                 if (dx | dy | dz) {
-                    const int base_kp = wm[0] * g.sx + wm[1] * g.sy + wm[2];
+                    uint32_t leaving = live;
 #pragma unroll
                     for (int j = 0; j < 27; ++j) {
                         const int ox = j / 9, oy = (j / 3) % 3, oz = j % 3;
                         const bool leaves = (unsigned)(ox - dx) > 2u || (unsigned)(oy - dy) > 2u || (unsigned)(oz - dz) > 2u;
-                        if (leaves && acc[j] != 0.f)
-                            put(base_kp + (ox - 1) * g.sx + (oy - 1) * g.sy + (oz - 1), acc[j]);
+                        if (!leaves) leaving &= ~(1u << j);
                     }
 #pragma unroll
-                    for (int l = 0; l < 9; ++l) shift3(acc[3 * l], acc[3 * l + 1], acc[3 * l + 2], dz);
+                    for (int j = 0; j < 27; ++j)
+                        if ((leaving >> j) & 1u) put(slot_kp(j), FILL ? acc[j] : 0.f);
+                    live = shift_mask(live, dx, dy, dz);
+                    if (FILL) {
 #pragma unroll
-                    for (int ox = 0; ox < 3; ++ox)
+                        for (int l = 0; l < 9; ++l) shift3(acc[3 * l], acc[3 * l + 1], acc[3 * l + 2], dz);
 #pragma unroll
-                        for (int oz = 0; oz < 3; ++oz) shift3(acc[ox * 9 + oz], acc[ox * 9 + 3 + oz], acc[ox * 9 + 6 + oz], dy);
+                        for (int ox = 0; ox < 3; ++ox)
 #pragma unroll
-                    for (int l = 0; l < 9; ++l) shift3(acc[l], acc[9 + l], acc[18 + l], dx);
+                            for (int oz = 0; oz < 3; ++oz)
+                                shift3(acc[ox * 9 + oz], acc[ox * 9 + 3 + oz], acc[ox * 9 + 6 + oz], dy);
+#pragma unroll
+                        for (int l = 0; l < 9; ++l) shift3(acc[l], acc[9 + l], acc[18 + l], dx);
+                    }
                 }
             } else {
                 flush();
@@ -184,14 +251,32 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
             wm[1] = m[1];
             wm[2] = m[2];
             have = true;
+            if (FILL) {
+                if (SCAT) {
+                    float2 om01[9];
+                    float om2[9];
+                    moment_omega(dl[0], dl[1], dl[2], thr, g_q1, g_q2, sig_a / kappa, om01, om2);
+#pragma unroll
+                    for (int l = 0; l < 9; ++l) {
+                        w[3 * l] = kappa * om01[l].x;
+                        w[3 * l + 1] = kappa * om01[l].y;
+                        w[3 * l + 2] = kappa * om2[l];
+                    }
+                } else {
+                    sample_weights<false>(dl[0], dl[1], dl[2], sig_a, kappa, 0xffffffffu, w);
+                }
+            }
 #pragma unroll
             for (int j = 0; j < 27; ++j) {
-                const float wt = w[j] * scale;
+                if (!((sup >> j) & 1u)) continue;
                 const int kp = mlin + (j / 9 - 1) * g.sx + ((j / 3) % 3 - 1) * g.sy + (j % 3 - 1);
                 if (__ldg(dynamic + kp)) {
-                    acc[j] += wt;
-                } else if (wt != 0.f) {
-                    for (int c = 0; c < nch; ++c) base[c] += (double)wt * fmaxf(__ldg(values + c * plane + kp), 0.f);
+                    live |= 1u << j;
+                    if (FILL) acc[j] += w[j] * scale;
+                } else if (FILL) {
+                    const float wt = w[j] * scale;
+                    if (wt != 0.f)
+                        for (int c = 0; c < nch; ++c) base[c] += (double)wt * fmaxf(__ldg(values + c * plane + kp), 0.f);
                 }
             }
         }
@@ -201,12 +286,21 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
     return count;
 }
 
+__device__ __forceinline__ void load_split_tables(float* s_thr, uint32_t* s_nm) {
+    for (int i = threadIdx.x; i < 3 * kScatDirs; i += blockDim.x) s_thr[i] = (&c_thr[0][0])[i];
+    for (int i = threadIdx.x; i < 3 * (kScatDirs + 1); i += blockDim.x) s_nm[i] = (&c_nmask[0][0])[i];
+    __syncthreads();
+}
+
 // Count pass: one warp per 8x4 unit, unit_len[unit] = longest row of the unit.
 template <bool SCAT>
 __global__ void __launch_bounds__(128) rplan_count_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
     int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
     int* __restrict__ unit_len) {
+    __shared__ float s_thr[3 * kScatDirs];
+    __shared__ uint32_t s_nm[3 * (kScatDirs + 1)];
+    load_split_tables(s_thr, s_nm);
     const int unit = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (unit >= n_units) return;
     const int lane = threadIdx.x & 31;
@@ -217,7 +311,8 @@ __global__ void __launch_bounds__(128) rplan_count_kernel(
         const fvr_camera_t& cam = cams[view];
         double d[3], base[1] = {0.0}, t_fin;
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
-        cnt = rplan_row<SCAT, false>(cam.center, d, g, rc, occ, dynamic, nullptr, 0, 0, nullptr, base, t_fin);
+        cnt = rplan_row<SCAT, false>(cam.center, d, g, rc, occ, dynamic, nullptr, 0, 0, s_thr, s_nm, nullptr, base,
+                                     t_fin);
     }
     cnt = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
     if (lane == 0) unit_len[unit] = cnt;
@@ -231,6 +326,9 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
     int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
     const float* __restrict__ values, int nch, int64_t plane, const long long* __restrict__ unit_off,
     int2* __restrict__ entries, double* __restrict__ base_out, double* __restrict__ t_fin_out) {
+    __shared__ float s_thr[3 * kScatDirs];
+    __shared__ uint32_t s_nm[3 * (kScatDirs + 1)];
+    load_split_tables(s_thr, s_nm);
     const int unit = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (unit >= n_units) return;
     const int lane = threadIdx.x & 31;
@@ -242,7 +340,7 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
         const fvr_camera_t& cam = cams[view];
         double d[3];
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
-        rplan_row<SCAT, true>(cam.center, d, g, rc, occ, dynamic, values, nch, plane,
+        rplan_row<SCAT, true>(cam.center, d, g, rc, occ, dynamic, values, nch, plane, s_thr, s_nm,
                               entries + unit_off[unit] * 32 + lane, base, t_fin);
     }
     for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];

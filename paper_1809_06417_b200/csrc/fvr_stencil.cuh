@@ -174,6 +174,7 @@ __device__ __forceinline__ uint32_t inbox_mask(const double p[3], const Geom& g,
 #endif
 constexpr int kSplits = kScatDirs + 1;
 __constant__ float c_thr[3][kScatDirs];  // sorted c_{s,a} = s_a / 2 per axis
+__constant__ uint32_t c_nmask[3][kScatDirs + 1];  // directions of the first i per axis (c_{s,a} < -delta_a)
 __constant__ float c_q0[8];              // Q_{empty}[E]
 __device__ float4 g_q1[3 * kSplits * 2];
 __device__ float4 g_q2[3 * kSplits * kSplits * 2];
