@@ -1006,6 +1006,33 @@ extern "C" int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_
 // ---- K-render as a fixed operator (fvr_rplan.cuh) -----------------------------
 
 namespace {
+// dyn27 masks of `dynamic`: recomputed by every count pass (`fresh`), reused
+// by the fill pass that follows it for the same array; grown on demand and
+// kept for the process
+uint32_t* dyn27_scratch(const fvr_grid_t& grid, const uint8_t* dynamic, cudaStream_t st, bool fresh) {
+    static uint32_t* buf = nullptr;
+    static int64_t cap = 0;
+    static const uint8_t* last = nullptr;
+    static fvr_grid_t last_grid{};
+    const int64_t n = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
+    if (cap < n) {
+        if (buf) cudaFree(buf);
+        buf = nullptr;
+        cap = 0;
+        last = nullptr;
+        if (cudaMalloc(&buf, (size_t)n * 4) != cudaSuccess) return nullptr;
+        cap = n;
+    }
+    if (fresh || last != dynamic || last_grid.nx != grid.nx || last_grid.ny != grid.ny || last_grid.nz != grid.nz) {
+        int64_t blocks = (n + 255) / 256;
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        rplan_dyn27_kernel<<<(unsigned)blocks, 256, 0, st>>>(dynamic, make_geom(grid), buf);
+        count_launch(1);
+        last = dynamic;
+        last_grid = grid;
+    }
+    return buf;
+}
 // the plan covers the two fast modes (g = 0, gather = edge, 32 loaded directions)
 int rplan_mode(const fvr_render_params_t& params, const fvr_grid_t& grid, bool& scat) {
     const float4* dummy = reinterpret_cast<const float4*>(&params);  // any non-null layout: mode query only
@@ -1033,12 +1060,14 @@ extern "C" int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_
     const int n_units = upv * n_views;
     const unsigned blocks = (unsigned)(((int64_t)n_units * 32 + 127) / 128);
     cudaStream_t st = (cudaStream_t)stream;
+    uint32_t* d27 = dyn27_scratch(grid, dynamic, st, true);
+    if (!d27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
     if (m)
         rplan_count_kernel<true><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
-                                                          occ, dynamic, unit_len);
+                                                          occ, dynamic, d27, unit_len);
     else
         rplan_count_kernel<false><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
-                                                           occ, dynamic, unit_len);
+                                                           occ, dynamic, d27, unit_len);
     return check_launch("rplan_count");
     FVR_TRY_END
 }
@@ -1064,12 +1093,15 @@ extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t
     cudaStream_t st = (cudaStream_t)stream;
     const auto* uo = reinterpret_cast<const long long*>(unit_off);
     auto* en = reinterpret_cast<int2*>(entries);
+    uint32_t* d27 = dyn27_scratch(grid, dynamic, st, false);
+    if (!d27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
     if (m)
         rplan_fill_kernel<true><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc, occ,
-                                                         dynamic, values, n_channels, plane, uo, en, base, t_fin);
+                                                         dynamic, d27, values, n_channels, plane, uo, en, base, t_fin);
     else
         rplan_fill_kernel<false><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
-                                                          occ, dynamic, values, n_channels, plane, uo, en, base, t_fin);
+                                                          occ, dynamic, d27, values, n_channels, plane, uo, en, base,
+                                                          t_fin);
     return check_launch("rplan_fill");
     FVR_TRY_END
 }

@@ -67,28 +67,6 @@ __device__ __forceinline__ void sample_weights(float dx, float dy, float dz, flo
     }
 }
 
-// shift a 3-slot line by delta in {-1, 0, 1}: new[o] = old[o + delta] (0 outside)
-__device__ __forceinline__ void shift3(float& a0, float& a1, float& a2, int delta) {
-    const float o0 = a0, o1 = a1, o2 = a2;
-    a0 = delta > 0 ? o1 : (delta < 0 ? 0.f : o0);
-    a1 = delta > 0 ? o2 : (delta < 0 ? o0 : o1);
-    a2 = delta > 0 ? 0.f : (delta < 0 ? o1 : o2);
-}
-
-// the same shift on a 27-bit slot mask (bit (ox*9 + oy*3 + oz))
-__device__ __forceinline__ uint32_t shift_mask(uint32_t m, int dx, int dy, int dz) {
-    constexpr uint32_t kZ0 = 0x1249249u, kZ2 = kZ0 << 2;
-    constexpr uint32_t kY0 = 0x7u | (0x7u << 9) | (0x7u << 18), kY2 = kY0 << 6;
-    constexpr uint32_t kX0 = 0x1FFu, kX2 = kX0 << 18;
-    if (dz > 0) m = (m >> 1) & ~kZ2;
-    else if (dz < 0) m = (m << 1) & ~kZ0;
-    if (dy > 0) m = (m >> 3) & ~kY2;
-    else if (dy < 0) m = (m << 3) & ~kY0;
-    if (dx > 0) m = (m >> 9) & ~kX2;
-    else if (dx < 0) m = (m << 9) & ~kX0 & 0x7FFFFFFu;
-    return m & 0x7FFFFFFu;
-}
-
 // Slots whose weight can be non-zero: the trilinear corners of the sample
 // (emission) and, with scattering, every slot some gather point reaches.  A
 // gather point x_s = delta + s/2 gives slot offset -1 weight iff x_s < 0 and
@@ -128,42 +106,61 @@ __device__ __forceinline__ uint32_t support_mask(bool scat, const float dl[3], c
 }
 
 // Walk one pixel's ray exactly as K-render samples it and produce its row of
-// B.  Which entries a row holds depends only on the geometry (a slot holds an
-// entry once a sample whose support covers it placed a `dynamic` key point
-// there), so FILL = false counts them without evaluating any weight.  The
-// key points not in `dynamic` (the loop's hull key points) contribute
-// max(v, 0) * weight to base[c] (values: nch lattice planes).  Interior
-// scattering samples take their 27 weights from the moment form
-// (moment_omega), face samples from the direct masked sum.  Returns the entry
-// count; t_fin receives the transparency after the last sample.
+// B.  Which entries a row holds depends only on the geometry (a window slot
+// holds an entry once a sample whose support covers it placed a `dynamic`
+// key point there), so FILL = false counts them without evaluating any
+// weight.  Key points not in `dynamic` (the loop's hull key points)
+// contribute max(v, 0) * weight to base[c] (values: nch lattice planes).
+// Interior scattering samples take their 27 weights from the moment form
+// (moment_omega), face samples from the direct masked sum.
+//
+// The merge window holds the 3x3x3 key points around the last sample's
+// nearest key point in toroidal slots (x mod 3, y mod 3, z mod 3) kept in
+// shared memory (acc[slot * stride]): moving the window by one key point
+// only retires the plane of slots it leaves, nothing is shifted.  dyn27[m]
+// is the 27-bit mask of dynamic key points around m (one load per sample).
+// Returns the entry count; t_fin receives the transparency after the last
+// sample.
 template <bool SCAT, bool FILL>
 __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, const RenderConsts& rc,
                          const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
-                         const float* __restrict__ values, int nch, int64_t plane, const float* __restrict__ thr,
-                         const uint32_t* __restrict__ nm, int2* __restrict__ out, double* base, double& t_fin) {
+                         const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch,
+                         int64_t plane, const float* __restrict__ thr, const uint32_t* __restrict__ nm,
+                         float* __restrict__ acc, float* __restrict__ wsm, int stride, int2* __restrict__ out,
+                         double* base, double& t_fin) {
+    constexpr uint32_t kPX[3] = {0x1FFu, 0x1FFu << 9, 0x1FFu << 18};
+    constexpr uint32_t kPY[3] = {0x7u | (0x7u << 9) | (0x7u << 18), (0x7u << 3) | (0x7u << 12) | (0x7u << 21),
+                                 (0x7u << 6) | (0x7u << 15) | (0x7u << 24)};
+    constexpr uint32_t kPZ[3] = {0x1249249u, 0x1249249u << 1, 0x1249249u << 2};
     int count = 0;
     double t_dst = 1.0;
-    float acc[27];
-#pragma unroll
-    for (int j = 0; j < 27; ++j) acc[j] = 0.f;
-    uint32_t live = 0;      // slots of the window holding an entry
-    int wm[3] = {0, 0, 0};  // window centre (nearest key point of the last merged sample)
+    uint32_t live = 0;      // window slots holding an entry
+    int wm[3] = {0, 0, 0};  // window centre
     bool have = false;
     const float sig_a = (float)rc.sigma_a, kappa = (float)rc.scat_scale;
     auto put = [&](int kp, float wt) {
         if (FILL) out[(int64_t)count * 32] = make_int2(kp, __float_as_int(wt));
         ++count;
     };
-    auto slot_kp = [&](int j) { return wm[0] * g.sx + wm[1] * g.sy + wm[2] + (j / 9 - 1) * g.sx + ((j / 3) % 3 - 1) * g.sy + (j % 3 - 1); };
-    auto flush = [&]() {
-        if (!have) return;
+    // key point held by slot s of the window centred on wm
+    auto slot_kp = [&](int s) {
+        int c3[3] = {s / 9, (s / 3) % 3, s % 3}, x[3];
 #pragma unroll
-        for (int j = 0; j < 27; ++j) {
-            if ((live >> j) & 1u) put(slot_kp(j), FILL ? acc[j] : 0.f);
-            if (FILL) acc[j] = 0.f;
+        for (int a = 0; a < 3; ++a) x[a] = wm[a] - 1 + (c3[a] - (wm[a] - 1) % 3 + 3) % 3;
+        return x[0] * g.sx + x[1] * g.sy + x[2];
+    };
+    auto retire = [&](uint32_t slots) {
+#pragma unroll 1
+        for (uint32_t b = slots; b; b &= b - 1) {
+            const int sl = __ffs(b) - 1;
+            float wt = 0.f;
+            if (FILL) {
+                wt = acc[sl * stride];
+                acc[sl * stride] = 0.f;
+            }
+            put(slot_kp(sl), wt);
         }
-        live = 0;
-        have = false;
+        live &= ~slots;
     };
     double te, tx;
     if (slab_span(o, d, g, te, tx)) {
@@ -173,6 +170,7 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
 #pragma unroll
         for (int a = 0; a < 3; ++a) qb[a] = ((o[a] - g.lo[a]) + t0 * d[a]) * g.inv_edge;
         const double nmax[3] = {(double)g.nx, (double)g.ny, (double)g.nz};
+#pragma unroll 1
         for (int k = 1; k <= n; ++k, t_dst *= rc.one_minus_tau) {
             double q[3];
             int m[3];
@@ -189,10 +187,10 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
             if (occ && __ldg(occ + mlin) > 1) continue;  // no key point of the stencil can be non-zero
             const uint32_t sup = support_mask(SCAT, dl, thr, nm);
             const float scale = (float)(t_dst * rc.tau);
-            float w[27];
             if (!interior) {
                 // within half a voxel of a box face: clamped stencil, entries unmerged
-                flush();
+                if (have) retire(live);
+                have = false;
                 if (FILL) {
                     uint32_t inbox = 0xffffffffu;
                     if (SCAT) {
@@ -200,15 +198,18 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                         sample_pos(o, d, te, g.edge, k, p);
                         inbox = inbox_mask(p, g, rc.half_gather);
                     }
+                    float w[27];
                     sample_weights<SCAT>(dl[0], dl[1], dl[2], sig_a, kappa, inbox, w);
+#pragma unroll
+                    for (int j = 0; j < 27; ++j) wsm[j * stride] = w[j] * scale;
                 }
 #pragma unroll 1
-                for (int j = 0; j < 27; ++j) {
-                    if (!((sup >> j) & 1u)) continue;
-                    const int x = min(max(m[0] + j / 9 - 1, 0), g.nx), y = min(max(m[1] + (j / 3) % 3 - 1, 0), g.ny),
-                              z = min(max(m[2] + j % 3 - 1, 0), g.nz);
+                for (uint32_t b = sup; b; b &= b - 1) {
+                    const int j = __ffs(b) - 1, jx = j / 9, jy = (j / 3) % 3, jz = j % 3;
+                    const int x = min(max(m[0] + jx - 1, 0), g.nx), y = min(max(m[1] + jy - 1, 0), g.ny),
+                              z = min(max(m[2] + jz - 1, 0), g.nz);
                     const int kp = x * g.sx + y * g.sy + z;
-                    const float wt = FILL ? w[j] * scale : 0.f;
+                    const float wt = FILL ? wsm[j * stride] : 0.f;
                     if (__ldg(dynamic + kp)) {
                         put(kp, wt);
                     } else if (FILL) {
@@ -217,41 +218,24 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                 }
                 continue;
             }
-            // move the merge window to m: slots leaving it are final
+            const uint32_t dyn = __ldg(dyn27 + mlin);
+            // move the window to m: retire the planes it leaves
             const int dx = m[0] - wm[0], dy = m[1] - wm[1], dz = m[2] - wm[2];
             if (have && abs(dx) <= 1 && abs(dy) <= 1 && abs(dz) <= 1) {
-                if (dx | dy | dz) {
-                    uint32_t leaving = live;
-#pragma unroll
-                    for (int j = 0; j < 27; ++j) {
-                        const int ox = j / 9, oy = (j / 3) % 3, oz = j % 3;
-                        const bool leaves = (unsigned)(ox - dx) > 2u || (unsigned)(oy - dy) > 2u || (unsigned)(oz - dz) > 2u;
-                        if (!leaves) leaving &= ~(1u << j);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 27; ++j)
-                        if ((leaving >> j) & 1u) put(slot_kp(j), FILL ? acc[j] : 0.f);
-                    live = shift_mask(live, dx, dy, dz);
-                    if (FILL) {
-#pragma unroll
-                        for (int l = 0; l < 9; ++l) shift3(acc[3 * l], acc[3 * l + 1], acc[3 * l + 2], dz);
-#pragma unroll
-                        for (int ox = 0; ox < 3; ++ox)
-#pragma unroll
-                            for (int oz = 0; oz < 3; ++oz)
-                                shift3(acc[ox * 9 + oz], acc[ox * 9 + 3 + oz], acc[ox * 9 + 6 + oz], dy);
-#pragma unroll
-                        for (int l = 0; l < 9; ++l) shift3(acc[l], acc[9 + l], acc[18 + l], dx);
-                    }
-                }
-            } else {
-                flush();
+                uint32_t gone = 0;
+                if (dx) gone |= kPX[(wm[0] - dx + 3) % 3];
+                if (dy) gone |= kPY[(wm[1] - dy + 3) % 3];
+                if (dz) gone |= kPZ[(wm[2] - dz + 3) % 3];
+                if (gone & live) retire(gone & live);
+            } else if (have) {
+                retire(live);
             }
             wm[0] = m[0];
             wm[1] = m[1];
             wm[2] = m[2];
             have = true;
             if (FILL) {
+                float w[27];
                 if (SCAT) {
                     float2 om01[9];
                     float om2[9];
@@ -265,25 +249,47 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                 } else {
                     sample_weights<false>(dl[0], dl[1], dl[2], sig_a, kappa, 0xffffffffu, w);
                 }
-            }
 #pragma unroll
-            for (int j = 0; j < 27; ++j) {
-                if (!((sup >> j) & 1u)) continue;
-                const int kp = mlin + (j / 9 - 1) * g.sx + ((j / 3) % 3 - 1) * g.sy + (j % 3 - 1);
-                if (__ldg(dynamic + kp)) {
-                    live |= 1u << j;
-                    if (FILL) acc[j] += w[j] * scale;
-                } else if (FILL) {
-                    const float wt = w[j] * scale;
-                    if (wt != 0.f)
-                        for (int c = 0; c < nch; ++c) base[c] += (double)wt * fmaxf(__ldg(values + c * plane + kp), 0.f);
+                for (int j = 0; j < 27; ++j) wsm[j * stride] = w[j] * scale;
+            }
+            // toroidal slot of offset (jx, jy, jz): ((m + j - 1) mod 3) per axis
+            const int r0 = (m[0] + 2) % 3, r1 = (m[1] + 2) % 3, r2 = (m[2] + 2) % 3;
+#pragma unroll 1
+            for (uint32_t b = sup & dyn; b; b &= b - 1) {
+                const int j = __ffs(b) - 1, jx = j / 9, jy = (j / 3) % 3, jz = j % 3;
+                const int sl = ((r0 + jx) % 3) * 9 + ((r1 + jy) % 3) * 3 + (r2 + jz) % 3;
+                live |= 1u << sl;
+                if (FILL) acc[sl * stride] += wsm[j * stride];
+            }
+            if (FILL) {
+#pragma unroll 1
+                for (uint32_t b = sup & ~dyn; b; b &= b - 1) {
+                    const int j = __ffs(b) - 1;
+                    const float wt = wsm[j * stride];
+                    if (wt == 0.f) continue;
+                    const int kp = mlin + (j / 9 - 1) * g.sx + ((j / 3) % 3 - 1) * g.sy + (j % 3 - 1);
+                    for (int c = 0; c < nch; ++c) base[c] += (double)wt * fmaxf(__ldg(values + c * plane + kp), 0.f);
                 }
             }
         }
-        flush();
+        if (have) retire(live);
     }
     t_fin = t_dst;
     return count;
+}
+
+// dyn27[m] = bit (jx*9 + jy*3 + jz) set when key point m + (jx-1, jy-1, jz-1)
+// is dynamic (interior key points; the border ones are never a window centre)
+__global__ void rplan_dyn27_kernel(const uint8_t* __restrict__ dynamic, Geom g, uint32_t* __restrict__ dyn27) {
+    const int64_t n = (int64_t)(g.nx + 1) * (g.ny + 1) * (g.nz + 1);
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const int z = (int)(k % (g.nz + 1)), y = (int)((k / (g.nz + 1)) % (g.ny + 1)), x = (int)(k / g.sx);
+        uint32_t m = 0;
+        if (x >= 1 && x < g.nx && y >= 1 && y < g.ny && z >= 1 && z < g.nz)
+            for (int j = 0; j < 27; ++j)
+                if (dynamic[k + (j / 9 - 1) * g.sx + ((j / 3) % 3 - 1) * g.sy + (j % 3 - 1)]) m |= 1u << j;
+        dyn27[k] = m;
+    }
 }
 
 __device__ __forceinline__ void load_split_tables(float* s_thr, uint32_t* s_nm) {
@@ -297,7 +303,7 @@ template <bool SCAT>
 __global__ void __launch_bounds__(128) rplan_count_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
     int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
-    int* __restrict__ unit_len) {
+    const uint32_t* __restrict__ dyn27, int* __restrict__ unit_len) {
     __shared__ float s_thr[3 * kScatDirs];
     __shared__ uint32_t s_nm[3 * (kScatDirs + 1)];
     load_split_tables(s_thr, s_nm);
@@ -311,8 +317,8 @@ __global__ void __launch_bounds__(128) rplan_count_kernel(
         const fvr_camera_t& cam = cams[view];
         double d[3], base[1] = {0.0}, t_fin;
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
-        cnt = rplan_row<SCAT, false>(cam.center, d, g, rc, occ, dynamic, nullptr, 0, 0, s_thr, s_nm, nullptr, base,
-                                     t_fin);
+        cnt = rplan_row<SCAT, false>(cam.center, d, g, rc, occ, dynamic, dyn27, nullptr, 0, 0, s_thr, s_nm, nullptr,
+                                     nullptr, 0, nullptr, base, t_fin);
     }
     cnt = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
     if (lane == 0) unit_len[unit] = cnt;
@@ -324,8 +330,11 @@ template <bool SCAT>
 __global__ void __launch_bounds__(128) rplan_fill_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
     int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
-    const float* __restrict__ values, int nch, int64_t plane, const long long* __restrict__ unit_off,
-    int2* __restrict__ entries, double* __restrict__ base_out, double* __restrict__ t_fin_out) {
+    const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch, int64_t plane,
+    const long long* __restrict__ unit_off, int2* __restrict__ entries, double* __restrict__ base_out,
+    double* __restrict__ t_fin_out) {
+    __shared__ float s_acc[27 * 128], s_w[27 * 128];
+    for (int i = threadIdx.x; i < 27 * 128; i += blockDim.x) s_acc[i] = 0.f;
     __shared__ float s_thr[3 * kScatDirs];
     __shared__ uint32_t s_nm[3 * (kScatDirs + 1)];
     load_split_tables(s_thr, s_nm);
@@ -340,8 +349,9 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
         const fvr_camera_t& cam = cams[view];
         double d[3];
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
-        rplan_row<SCAT, true>(cam.center, d, g, rc, occ, dynamic, values, nch, plane, s_thr, s_nm,
-                              entries + unit_off[unit] * 32 + lane, base, t_fin);
+        rplan_row<SCAT, true>(cam.center, d, g, rc, occ, dynamic, dyn27, values, nch, plane, s_thr, s_nm,
+                              s_acc + threadIdx.x, s_w + threadIdx.x, 128, entries + unit_off[unit] * 32 + lane, base,
+                              t_fin);
     }
     for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];
     t_fin_out[r] = t_fin;

@@ -303,11 +303,14 @@ class ChannelLoop:
         off[1:] = t.cumsum(unit_len.long(), 0)
         slots = int(off[-1].item()) * 32
         need = 8 * slots + 8 * (self.nch + 1) * n_units * 32
-        if need > min(self.PLAN_MAX_BYTES, t.cuda.mem_get_info(dev)[0] // 2):
+        if need > self.PLAN_MAX_BYTES:
             return False
-        entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
-        base = t.zeros((self.nch, n_units * 32), dtype=t.float64, device=dev)
-        t_fin = t.zeros(n_units * 32, dtype=t.float64, device=dev)
+        try:  # (no cudaMemGetInfo probe: it synchronises and costs tens of ms)
+            entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
+            base = t.zeros((self.nch, n_units * 32), dtype=t.float64, device=dev)
+            t_fin = t.zeros(n_units * 32, dtype=t.float64, device=dev)
+        except t.cuda.OutOfMemoryError:
+            return False
         _lib.call("fvr_rplan_fill", *geo, self.values.data_ptr(), self.nch, off.data_ptr(), entries.data_ptr(),
                   base.data_ptr(), t_fin.data_ptr(), stream)
         self.rp_len, self.rp_off, self.rp_entries, self.rp_base, self.rp_tfin = unit_len, off, entries, base, t_fin
@@ -394,7 +397,7 @@ class ChannelLoop:
         return 2 * self.nch if self.n_kp else 0
 
     # -- the back-projection plan (deterministic mode) --------------------------
-    # plans larger than this fall back to the ray-driven scatter
+    # plans larger than this (or that do not fit) fall back to the kernels they replace
     PLAN_MAX_BYTES = 48 << 30
 
     def _build_plan(self) -> bool:
@@ -437,12 +440,14 @@ class ChannelLoop:
         slots = int(slice_off[-1].item()) * 32
         nnz = int(counts.long().sum().item())
         n_samples = int(ray_samples.long().sum().item()) if self.sample_plan else 0
-        free = t.cuda.mem_get_info(dev)[0]
         need = 8 * slots + 12 * n_samples
-        if need > min(self.PLAN_MAX_BYTES, free // 2) or n_samples >= 2 ** 31:
+        if need > self.PLAN_MAX_BYTES or n_samples >= 2 ** 31:
             return False
-        cursor = t.zeros(self.n_kp, dtype=t.int64, device=dev)
-        entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
+        try:
+            cursor = t.zeros(self.n_kp, dtype=t.int64, device=dev)
+            entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
+        except t.cuda.OutOfMemoryError:
+            return False
         sell = (row_pos.data_ptr(), slice_off.data_ptr(), cursor.data_ptr(), entries.data_ptr())
         if self.sample_plan:
             sid0 = t.zeros(self.n_rays, dtype=t.int64, device=dev)
