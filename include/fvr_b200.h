@@ -197,7 +197,10 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
  * points); the others fold into base (n_channels x rows f64, rows =
  * n_units * 32) from `values`.  Needs the fast render modes (g = 0, gather =
  * edge, 32 directions loaded); occ is the distance map (may be NULL).
- * fvr_rplan_render replaces fvr_loop_render with identical outputs. */
+ * fvr_rplan_render replaces fvr_loop_render with identical outputs; with 3
+ * channels it first packs max(v, 0) of the listed key points (kp_index,
+ * n_kp: the loop's hull key points) into cpack (lattice x float4 scratch) so
+ * each entry is one 16-byte read. */
 int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                     int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
                     const uint8_t* dynamic, int32_t* unit_len, void* stream);
@@ -208,8 +211,9 @@ int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_
 int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const int32_t* entries,
                      const double* base, const double* t_fin, int32_t n_views, int32_t bbox_w, int32_t bbox_h,
                      const float* src, const float* values, fvr_grid_t grid, int32_t n_channels,
-                     const double* background, float* residual, double* sq_partials, int64_t sq_stride,
-                     const fvr_loop_state_t* state, void* stream);
+                     const double* background, const int32_t* kp_index, int64_t n_kp, float* cpack,
+                     float* residual, double* sq_partials, int64_t sq_stride, const fvr_loop_state_t* state,
+                     void* stream);
 
 /* Back-project the residual of every listed flame ray (ray_list entries are
  * view << 24 | (row_in_bbox * bbox_w + col_in_bbox)). stochastic != 0 draws

@@ -1109,11 +1109,14 @@ extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t
 extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const int32_t* entries,
                                 const double* base, const double* t_fin, int32_t n_views, int32_t bbox_w,
                                 int32_t bbox_h, const float* src, const float* values, fvr_grid_t grid,
-                                int32_t n_channels, const double* background, float* residual, double* sq_partials,
-                                int64_t sq_stride, const fvr_loop_state_t* state, void* stream) {
+                                int32_t n_channels, const double* background, const int32_t* kp_index, int64_t n_kp,
+                                float* cpack, float* residual, double* sq_partials, int64_t sq_stride,
+                                const fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
     if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "the loop renders 1 or 3 channels");
     if (!background) return set_error(FVR_ERR_INVALID, "background is NULL");
+    if (n_channels == 3 && (!cpack || (!kp_index && n_kp > 0)))
+        return set_error(FVR_ERR_INVALID, "three channels need the cpack scratch and the key-point list");
     fvr_render_params_t p{};
     p.tau = 0.0;
     RenderConsts rc = make_render_consts(p, background, n_channels);
@@ -1125,14 +1128,22 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
     cudaStream_t st = (cudaStream_t)stream;
     const auto* uo = reinterpret_cast<const long long*>(unit_off);
     const auto* en = reinterpret_cast<const int2*>(entries);
-    if (n_channels == 1)
+    auto* cp = reinterpret_cast<float4*>(cpack);
+    if (n_channels == 1) {
         rplan_render_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, en, base, t_fin, n_units, units_x, upv,
-                                                                n_views, bbox_w, bbox_h, src, values, plane, rc,
-                                                                residual, sq_partials, sq_stride, state);
-    else
+                                                                n_views, bbox_w, bbox_h, src, values, nullptr, plane,
+                                                                rc, residual, sq_partials, sq_stride, state);
+    } else {
+        if (n_kp > 0) {
+            int64_t cb = (n_kp + 255) / 256;
+            if (cb > 148 * 16) cb = 148 * 16;
+            rplan_cpack_kernel<<<(unsigned)cb, 256, 0, st>>>(values, plane, kp_index, n_kp, cp, state);
+            count_launch(1);
+        }
         rplan_render_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, en, base, t_fin, n_units, units_x, upv,
-                                                                n_views, bbox_w, bbox_h, src, values, plane, rc,
+                                                                n_views, bbox_w, bbox_h, src, values, cp, plane, rc,
                                                                 residual, sq_partials, sq_stride, state);
+    }
     return check_launch("rplan_render");
     FVR_TRY_END
 }

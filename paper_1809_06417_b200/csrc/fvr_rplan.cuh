@@ -375,8 +375,8 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
     const int* __restrict__ unit_len, const long long* __restrict__ unit_off, const int2* __restrict__ entries,
     const double* __restrict__ base, const double* __restrict__ t_fin, int n_units, int units_x,
     int units_per_view, int n_views, int w, int h, const float* __restrict__ src, const float* __restrict__ values,
-    int64_t plane, RenderConsts rc, float* __restrict__ residual, double* __restrict__ sq_partials,
-    int64_t sq_stride, const fvr_loop_state_t* __restrict__ state) {
+    const float4* __restrict__ cpack, int64_t plane, RenderConsts rc, float* __restrict__ residual,
+    double* __restrict__ sq_partials, int64_t sq_stride, const fvr_loop_state_t* __restrict__ state) {
     if (all_done<NCH>(state)) return;
     const int lane = threadIdx.x & 31;
     const int64_t rows = (int64_t)n_units * 32;
@@ -397,18 +397,29 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
 #pragma unroll
             for (int c = 0; c < NCH; ++c) part[c] = 0.f;
 #pragma unroll
-            for (int i = 0; i < B; ++i)
+            for (int i = 0; i < B; ++i) {
+                if (NCH == 1) {
+                    part[0] = fmaf(__int_as_float(en[i].y), fmaxf(__ldg(values + en[i].x), 0.f), part[0]);
+                } else {
+                    const float4 cv = __ldg(cpack + en[i].x);  // max(v, 0) of the three channels
+                    const float cc[3] = {cv.x, cv.y, cv.z};
 #pragma unroll
-                for (int c = 0; c < NCH; ++c)
-                    part[c] = fmaf(__int_as_float(en[i].y), fmaxf(__ldg(values + c * plane + en[i].x), 0.f), part[c]);
+                    for (int c = 0; c < NCH; ++c) part[c] = fmaf(__int_as_float(en[i].y), cc[c], part[c]);
+                }
+            }
 #pragma unroll
             for (int c = 0; c < NCH; ++c) acc[c] += (double)part[c];
         }
         for (; t < len; ++t) {
             const int2 en = __ldcs(e + (int64_t)t * 32);
+            if (NCH == 1) {
+                acc[0] += (double)(__int_as_float(en.y) * fmaxf(__ldg(values + en.x), 0.f));
+            } else {
+                const float4 cv = __ldg(cpack + en.x);
+                const float cc[3] = {cv.x, cv.y, cv.z};
 #pragma unroll
-            for (int c = 0; c < NCH; ++c)
-                acc[c] += (double)(__int_as_float(en.y) * fmaxf(__ldg(values + c * plane + en.x), 0.f));
+                for (int c = 0; c < NCH; ++c) acc[c] += (double)(__int_as_float(en.y) * cc[c]);
+            }
         }
         const int view = unit / units_per_view, u = unit - view * units_per_view;
         const int col = (u % units_x) * kUnitW + (lane % kUnitW), row = (u / units_x) * kUnitH + (lane / kUnitW);
@@ -433,6 +444,18 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
             const double tot = warp_sum(sq[c]);
             if (lane == 0) sq_partials[c * sq_stride + unit] = tot;
         }
+    }
+}
+
+// cpack[kp] = (max(v_0, 0), max(v_1, 0), max(v_2, 0), 0) at the listed key
+// points: the three-channel render plan reads one 16-byte record per entry
+__global__ void rplan_cpack_kernel(const float* __restrict__ values, int64_t plane, const int32_t* __restrict__ kp,
+                                   int64_t n_kp, float4* __restrict__ cpack, const fvr_loop_state_t* __restrict__ state) {
+    if (all_done<3>(state)) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_kp; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = kp[i];
+        cpack[k] = make_float4(fmaxf(values[k], 0.f), fmaxf(values[plane + k], 0.f), fmaxf(values[2 * plane + k], 0.f),
+                               0.f);
     }
 }
 

@@ -314,6 +314,7 @@ class ChannelLoop:
         _lib.call("fvr_rplan_fill", *geo, self.values.data_ptr(), self.nch, off.data_ptr(), entries.data_ptr(),
                   base.data_ptr(), t_fin.data_ptr(), stream)
         self.rp_len, self.rp_off, self.rp_entries, self.rp_base, self.rp_tfin = unit_len, off, entries, base, t_fin
+        self.rp_cpack = t.zeros(self.shape + (4,), dtype=t.float32, device=dev) if self.nch == 3 else None
         self.rplan_nnz = slots
         return True
 
@@ -325,6 +326,7 @@ class ChannelLoop:
                 "fvr_rplan_render", self.rp_len.data_ptr(), self.rp_off.data_ptr(), self.rp_entries.data_ptr(),
                 self.rp_base.data_ptr(), self.rp_tfin.data_ptr(), self.v_end - self.v_begin, self.w_bb, self.h_bb,
                 self.src.data_ptr(), self.values.data_ptr(), self.grid, self.nch, self.background,
+                self.kp.data_ptr(), self.n_kp, _lib.ptr(self.rp_cpack),
                 self.residual.data_ptr(), self.sq[0, self.v_begin * self.bpv:].data_ptr(), self.n_sq,
                 self.state.data_ptr(), stream,
             )
