@@ -14,7 +14,7 @@ timeout 900 python tools/run_configs.py sweep > $O/sweep.jsonl 2> $O/sweep.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
     python bench.py --steps 5 --warmup 3 --e2e-iters 0 --no-cpu-baseline --stochastic-steps 5 > $O/ncu_launch.log 2>&1
 # full captures: deterministic render + gather, then the stochastic weigh + sample-plan gather
-ncu --set full --import-source on --clock-control none -k regex:"loop_render_scat|gather_kernel" -s 4 -c 2 \
+ncu --set full --import-source on --clock-control none -k regex:"rplan_render|gather_kernel" -s 4 -c 2 \
     -o $O/prof_det python bench.py --steps 3 --warmup 3 --e2e-iters 0 --no-cpu-baseline --stochastic-steps 0 \
     > $O/ncu_det.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"weighted_residual|gather_kernel" -s 6 -c 2 \
