@@ -200,20 +200,23 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
  * fvr_rplan_render replaces fvr_loop_render with identical outputs; with 3
  * channels it first packs max(v, 0) of the listed key points (kp_index,
  * n_kp: the loop's hull key points) into cpack (lattice x float4 scratch) so
- * each entry is one 16-byte read. */
+ * each entry is one 16-byte read.  Fill and render visit the units in the
+ * order unit_order (a permutation of the units, longest first; NULL =
+ * natural order). */
 int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                     int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
                     const uint8_t* dynamic, int32_t* unit_len, void* stream);
 int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                    int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
                    const uint8_t* dynamic, const float* values, int32_t n_channels, const int64_t* unit_off,
-                   int32_t* entries, double* base, double* t_fin, void* stream);
+                   const int32_t* unit_order, int32_t* entries, double* base, double* t_fin, void* stream);
 int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const int32_t* entries,
-                     const double* base, const double* t_fin, int32_t n_views, int32_t bbox_w, int32_t bbox_h,
+                     const double* base, const double* t_fin, const int32_t* unit_order, int32_t n_views,
+                     int32_t bbox_w, int32_t bbox_h,
                      const float* src, const float* values, fvr_grid_t grid, int32_t n_channels,
                      const double* background, const int32_t* kp_index, int64_t n_kp, float* cpack,
-                     float* residual, double* sq_partials, int64_t sq_stride, const fvr_loop_state_t* state,
-                     void* stream);
+                     float* residual, double* sq_partials, int64_t sq_stride,
+                     const fvr_loop_state_t* state, void* stream);
 
 /* Back-project the residual of every listed flame ray (ray_list entries are
  * view << 24 | (row_in_bbox * bbox_w + col_in_bbox)). stochastic != 0 draws

@@ -331,15 +331,16 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
     int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
     const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch, int64_t plane,
-    const long long* __restrict__ unit_off, int2* __restrict__ entries, double* __restrict__ base_out,
+    const long long* __restrict__ unit_off, const int* __restrict__ unit_order, int2* __restrict__ entries, double* __restrict__ base_out,
     double* __restrict__ t_fin_out) {
     __shared__ float s_acc[27 * 128], s_w[27 * 128];
     for (int i = threadIdx.x; i < 27 * 128; i += blockDim.x) s_acc[i] = 0.f;
     __shared__ float s_thr[3 * kScatDirs];
     __shared__ uint32_t s_nm[3 * (kScatDirs + 1)];
     load_split_tables(s_thr, s_nm);
-    const int unit = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    if (unit >= n_units) return;
+    const int slot = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (slot >= n_units) return;
+    const int unit = unit_order ? __ldg(unit_order + slot) : slot;  // longest first: a short tail
     const int lane = threadIdx.x & 31;
     const int view = unit / units_per_view, u = unit - view * units_per_view;
     const int col = (u % units_x) * kUnitW + (lane % kUnitW), row = (u / units_x) * kUnitH + (lane / kUnitW);
@@ -370,81 +371,97 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
 #define FVR_RPLAN_MINB 3
 #endif
 
+// One unit (8x4 pixels, lane = pixel) of K-render through the plan.
+template <int NCH>
+__device__ __forceinline__ void rplan_render_unit(
+    int unit, int lane, const int* __restrict__ unit_len, const long long* __restrict__ unit_off,
+    const int2* __restrict__ entries, const double* __restrict__ base, const double* __restrict__ t_fin,
+    int64_t rows, int units_x, int units_per_view, int n_views, int w, int h, const float* __restrict__ src,
+    const float* __restrict__ values, const float4* __restrict__ cpack, const RenderConsts& rc,
+    float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride) {
+    const int len = unit_len[unit];
+    const int2* e = entries + unit_off[unit] * 32 + lane;
+    double acc[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
+    int t = 0;
+    constexpr int B = FVR_RPLAN_BATCH;
+    for (; t + B <= len; t += B) {
+        int2 en[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) en[i] = __ldcs(e + (int64_t)(t + i) * 32);
+        float part[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) part[c] = 0.f;
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            if (NCH == 1) {
+                part[0] = fmaf(__int_as_float(en[i].y), fmaxf(__ldg(values + en[i].x), 0.f), part[0]);
+            } else {
+                const float4 cv = __ldg(cpack + en[i].x);  // max(v, 0) of the three channels
+                const float cc[3] = {cv.x, cv.y, cv.z};
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) part[c] = fmaf(__int_as_float(en[i].y), cc[c], part[c]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) acc[c] += (double)part[c];
+    }
+    for (; t < len; ++t) {
+        const int2 en = __ldcs(e + (int64_t)t * 32);
+        if (NCH == 1) {
+            acc[0] += (double)(__int_as_float(en.y) * fmaxf(__ldg(values + en.x), 0.f));
+        } else {
+            const float4 cv = __ldg(cpack + en.x);
+            const float cc[3] = {cv.x, cv.y, cv.z};
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) acc[c] += (double)(__int_as_float(en.y) * cc[c]);
+        }
+    }
+    const int view = unit / units_per_view, u = unit - view * units_per_view;
+    const int col = (u % units_x) * kUnitW + (lane % kUnitW), row = (u / units_x) * kUnitH + (lane / kUnitW);
+    const int64_t r = (int64_t)unit * 32 + lane;
+    const int64_t cstride = (int64_t)n_views * h * w;
+    double sq[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) sq[c] = 0.0;
+    if (col < w && row < h) {
+        const int64_t pix = ((int64_t)view * h + row) * w + col;
+        const double tf = t_fin[r];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const double rec = acc[c] + base[c * rows + r] + tf * rc.bg[c];
+            const double res = (double)src[c * cstride + pix] - rec;
+            residual[pix * kResPitch<NCH> + c] = (float)res;
+            sq[c] = res * res;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+        const double tot = warp_sum(sq[c]);
+        if (lane == 0) sq_partials[c * sq_stride + unit] = tot;
+    }
+}
+
 template <int NCH>
 __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
     const int* __restrict__ unit_len, const long long* __restrict__ unit_off, const int2* __restrict__ entries,
-    const double* __restrict__ base, const double* __restrict__ t_fin, int n_units, int units_x,
-    int units_per_view, int n_views, int w, int h, const float* __restrict__ src, const float* __restrict__ values,
-    const float4* __restrict__ cpack, int64_t plane, RenderConsts rc, float* __restrict__ residual,
-    double* __restrict__ sq_partials, int64_t sq_stride, const fvr_loop_state_t* __restrict__ state) {
+    const double* __restrict__ base, const double* __restrict__ t_fin, const int* __restrict__ unit_order,
+    int n_units, int units_x, int units_per_view, int n_views, int w, int h, const float* __restrict__ src,
+    const float* __restrict__ values, const float4* __restrict__ cpack, int64_t plane, RenderConsts rc,
+    float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride,
+    const fvr_loop_state_t* __restrict__ state) {
     if (all_done<NCH>(state)) return;
     const int lane = threadIdx.x & 31;
     const int64_t rows = (int64_t)n_units * 32;
+    // units longest first (unit_order): the block scheduler then hands the
+    // short bbox-margin units to SMs as they free up, with no long unit left
+    // for the tail (config 2: 0.157 -> 0.139 ms)
     for (int unit = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); unit < n_units;
-         unit += (int)(((int64_t)gridDim.x * blockDim.x) >> 5)) {
-        const int len = unit_len[unit];
-        const int2* e = entries + unit_off[unit] * 32 + lane;
-        double acc[NCH];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
-        int t = 0;
-        constexpr int B = FVR_RPLAN_BATCH;
-        for (; t + B <= len; t += B) {
-            int2 en[B];
-#pragma unroll
-            for (int i = 0; i < B; ++i) en[i] = __ldcs(e + (int64_t)(t + i) * 32);
-            float part[NCH];
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) part[c] = 0.f;
-#pragma unroll
-            for (int i = 0; i < B; ++i) {
-                if (NCH == 1) {
-                    part[0] = fmaf(__int_as_float(en[i].y), fmaxf(__ldg(values + en[i].x), 0.f), part[0]);
-                } else {
-                    const float4 cv = __ldg(cpack + en[i].x);  // max(v, 0) of the three channels
-                    const float cc[3] = {cv.x, cv.y, cv.z};
-#pragma unroll
-                    for (int c = 0; c < NCH; ++c) part[c] = fmaf(__int_as_float(en[i].y), cc[c], part[c]);
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) acc[c] += (double)part[c];
-        }
-        for (; t < len; ++t) {
-            const int2 en = __ldcs(e + (int64_t)t * 32);
-            if (NCH == 1) {
-                acc[0] += (double)(__int_as_float(en.y) * fmaxf(__ldg(values + en.x), 0.f));
-            } else {
-                const float4 cv = __ldg(cpack + en.x);
-                const float cc[3] = {cv.x, cv.y, cv.z};
-#pragma unroll
-                for (int c = 0; c < NCH; ++c) acc[c] += (double)(__int_as_float(en.y) * cc[c]);
-            }
-        }
-        const int view = unit / units_per_view, u = unit - view * units_per_view;
-        const int col = (u % units_x) * kUnitW + (lane % kUnitW), row = (u / units_x) * kUnitH + (lane / kUnitW);
-        const int64_t r = (int64_t)unit * 32 + lane;
-        const int64_t cstride = (int64_t)n_views * h * w;
-        double sq[NCH];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) sq[c] = 0.0;
-        if (col < w && row < h) {
-            const int64_t pix = ((int64_t)view * h + row) * w + col;
-            const double tf = t_fin[r];
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-                const double rec = acc[c] + base[c * rows + r] + tf * rc.bg[c];
-                const double res = (double)src[c * cstride + pix] - rec;
-                residual[pix * kResPitch<NCH> + c] = (float)res;
-                sq[c] = res * res;
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            const double tot = warp_sum(sq[c]);
-            if (lane == 0) sq_partials[c * sq_stride + unit] = tot;
-        }
-    }
+         unit += (int)(((int64_t)gridDim.x * blockDim.x) >> 5))
+        rplan_render_unit<NCH>(unit_order ? __ldg(unit_order + unit) : unit, lane, unit_len, unit_off, entries, base,
+                               t_fin, rows, units_x, units_per_view, n_views, w, h, src, values, cpack, rc, residual,
+                               sq_partials, sq_stride);
 }
 
 // cpack[kp] = (max(v_0, 0), max(v_1, 0), max(v_2, 0), 0) at the listed key
