@@ -202,17 +202,21 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
  * n_kp: the loop's hull key points) into cpack (lattice x float4 scratch) so
  * each entry is one 16-byte read.  Fill and render visit the units in the
  * order unit_order (a permutation of the units, longest first; NULL =
- * natural order). */
+ * natural order).  Row r = unit * 32 + lane renders the pixel of natural row
+ * row_src[r] (NULL = r; natural row q is lane q % 32 of the 8x4 pixel unit
+ * q / 32): the caller sorts the rows of a few neighbouring units by length
+ * (row_len from the count pass) so a unit's rows need less padding. */
 int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                     int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
-                    const uint8_t* dynamic, int32_t* unit_len, void* stream);
+                    const uint8_t* dynamic, int32_t* unit_len, int32_t* row_len, void* stream);
 int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                    int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
                    const uint8_t* dynamic, const float* values, int32_t n_channels, const int64_t* unit_off,
-                   const int32_t* unit_order, int32_t* entries, double* base, double* t_fin, void* stream);
+                   const int32_t* unit_order, const int32_t* row_src, int32_t* entries, double* base,
+                   double* t_fin, void* stream);
 int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const int32_t* entries,
-                     const double* base, const double* t_fin, const int32_t* unit_order, int32_t n_views,
-                     int32_t bbox_w, int32_t bbox_h,
+                     const double* base, const double* t_fin, const int32_t* unit_order,
+                     const int32_t* row_src, int32_t n_views, int32_t bbox_w, int32_t bbox_h,
                      const float* src, const float* values, fvr_grid_t grid, int32_t n_channels,
                      const double* background, const int32_t* kp_index, int64_t n_kp, float* cpack,
                      float* residual, double* sq_partials, int64_t sq_stride,

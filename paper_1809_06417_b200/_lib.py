@@ -127,10 +127,11 @@ _SIGNATURES = {
     "fvr_adjust_plan_fill": (
         c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, c_double, c_double, c_double,
                 _P, _P, _P, _P, _P, _P]),
-    "fvr_rplan_count": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _GRID, _PARAMS, _P, _P, _P, _P]),
+    "fvr_rplan_count": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _GRID, _PARAMS, _P, _P, _P, _P,
+                                _P]),
     "fvr_rplan_fill": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _GRID, _PARAMS, _P, _P, _P, c_int32,
-                               _P, _P, _P, _P, _P, _P]),
-    "fvr_rplan_render": (c_int, [_P, _P, _P, _P, _P, _P, c_int32, c_int32, c_int32, _P, _P, _GRID, c_int32, _P, _P,
+                               _P, _P, _P, _P, _P, _P, _P]),
+    "fvr_rplan_render": (c_int, [_P, _P, _P, _P, _P, _P, _P, c_int32, c_int32, c_int32, _P, _P, _GRID, c_int32, _P, _P,
                                  c_int64, _P, _P, _P, c_int64, _P, _P]),
     "fvr_sample_plan_count": (c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, _P, _P, _P,
                                       _P]),

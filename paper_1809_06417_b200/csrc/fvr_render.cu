@@ -1045,7 +1045,8 @@ int rplan_mode(const fvr_render_params_t& params, const fvr_grid_t& grid, bool& 
 
 extern "C" int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                                int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params,
-                               const uint8_t* occ, const uint8_t* dynamic, int32_t* unit_len, void* stream) {
+                               const uint8_t* occ, const uint8_t* dynamic, int32_t* unit_len, int32_t* row_len,
+                               void* stream) {
     FVR_TRY_BEGIN
     if (n_views < 1 || bbox_w < 1 || bbox_h < 1) return set_error(FVR_ERR_INVALID, "empty render plan");
     if (!dynamic || !unit_len) return set_error(FVR_ERR_INVALID, "dynamic / unit_len is NULL");
@@ -1064,10 +1065,10 @@ extern "C" int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_
     if (!d27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
     if (m)
         rplan_count_kernel<true><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
-                                                          occ, dynamic, d27, unit_len);
+                                                          occ, dynamic, d27, unit_len, row_len);
     else
         rplan_count_kernel<false><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
-                                                           occ, dynamic, d27, unit_len);
+                                                           occ, dynamic, d27, unit_len, row_len);
     return check_launch("rplan_count");
     FVR_TRY_END
 }
@@ -1075,8 +1076,8 @@ extern "C" int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_
 extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                               int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
                               const uint8_t* dynamic, const float* values, int32_t n_channels,
-                              const int64_t* unit_off, const int32_t* unit_order, int32_t* entries, double* base,
-                              double* t_fin, void* stream) {
+                              const int64_t* unit_off, const int32_t* unit_order, const int32_t* row_src,
+                              int32_t* entries, double* base, double* t_fin, void* stream) {
     FVR_TRY_BEGIN
     if (n_views < 1 || bbox_w < 1 || bbox_h < 1) return set_error(FVR_ERR_INVALID, "empty render plan");
     if (n_channels < 1 || n_channels > 4) return set_error(FVR_ERR_INVALID, "n_channels must be 1..4");
@@ -1098,19 +1099,19 @@ extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t
     if (!d27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
     if (m)
         rplan_fill_kernel<true><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc, occ,
-                                                         dynamic, d27, values, n_channels, plane, uo, unit_order, en, base,
-                                                         t_fin);
+                                                         dynamic, d27, values, n_channels, plane, uo, unit_order,
+                                                         row_src, en, base, t_fin);
     else
         rplan_fill_kernel<false><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
-                                                          occ, dynamic, d27, values, n_channels, plane, uo, unit_order, en,
-                                                          base, t_fin);
+                                                          occ, dynamic, d27, values, n_channels, plane, uo,
+                                                          unit_order, row_src, en, base, t_fin);
     return check_launch("rplan_fill");
     FVR_TRY_END
 }
 
 extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const int32_t* entries,
                                 const double* base, const double* t_fin, const int32_t* unit_order,
-                                int32_t n_views, int32_t bbox_w,
+                                const int32_t* row_src, int32_t n_views, int32_t bbox_w,
                                 int32_t bbox_h, const float* src, const float* values, fvr_grid_t grid,
                                 int32_t n_channels, const double* background, const int32_t* kp_index, int64_t n_kp,
                                 float* cpack, float* residual, double* sq_partials, int64_t sq_stride,
@@ -1133,8 +1134,8 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
     const auto* en = reinterpret_cast<const int2*>(entries);
     auto* cp = reinterpret_cast<float4*>(cpack);
     if (n_channels == 1) {
-        rplan_render_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, en, base, t_fin, unit_order, n_units,
-                                                                units_x, upv,
+        rplan_render_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, en, base, t_fin, unit_order, row_src,
+                                                                n_units, units_x, upv,
                                                                 n_views, bbox_w, bbox_h, src, values, nullptr, plane,
                                                                 rc, residual, sq_partials, sq_stride, state);
     } else {
@@ -1144,8 +1145,8 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
             rplan_cpack_kernel<<<(unsigned)cb, 256, 0, st>>>(values, plane, kp_index, n_kp, cp, state);
             count_launch(1);
         }
-        rplan_render_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, en, base, t_fin, unit_order, n_units,
-                                                                units_x, upv,
+        rplan_render_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, en, base, t_fin, unit_order, row_src,
+                                                                n_units, units_x, upv,
                                                                 n_views, bbox_w, bbox_h, src, values, cp, plane, rc,
                                                                 residual, sq_partials, sq_stride, state);
     }

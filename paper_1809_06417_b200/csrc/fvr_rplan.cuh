@@ -298,12 +298,25 @@ __device__ __forceinline__ void load_split_tables(float* s_thr, uint32_t* s_nm) 
     __syncthreads();
 }
 
-// Count pass: one warp per 8x4 unit, unit_len[unit] = longest row of the unit.
+// Pixel of natural row r = unit * 32 + lane (unit = 8x4 pixel tile, lanes
+// row-major); false when the unit overhangs the bbox there.
+__device__ __forceinline__ bool rplan_pixel(int64_t r, int units_x, int units_per_view, int w, int h, int& view,
+                                            int& col, int& row) {
+    const int unit = (int)(r >> 5), lane = (int)(r & 31);
+    view = unit / units_per_view;
+    const int u = unit - view * units_per_view;
+    col = (u % units_x) * kUnitW + (lane % kUnitW);
+    row = (u / units_x) * kUnitH + (lane / kUnitW);
+    return col < w && row < h;
+}
+
+// Count pass: one warp per 8x4 unit, unit_len[unit] = longest row of the
+// unit and, when row_len is given, row_len[r] = the length of natural row r.
 template <bool SCAT>
 __global__ void __launch_bounds__(128) rplan_count_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
     int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
-    const uint32_t* __restrict__ dyn27, int* __restrict__ unit_len) {
+    const uint32_t* __restrict__ dyn27, int* __restrict__ unit_len, int* __restrict__ row_len) {
     __shared__ float s_thr[3 * kScatDirs];
     __shared__ uint32_t s_nm[3 * (kScatDirs + 1)];
     load_split_tables(s_thr, s_nm);
@@ -320,6 +333,7 @@ __global__ void __launch_bounds__(128) rplan_count_kernel(
         cnt = rplan_row<SCAT, false>(cam.center, d, g, rc, occ, dynamic, dyn27, nullptr, 0, 0, s_thr, s_nm, nullptr,
                                      nullptr, 0, nullptr, base, t_fin);
     }
+    if (row_len) row_len[(int64_t)unit * 32 + lane] = cnt;
     cnt = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
     if (lane == 0) unit_len[unit] = cnt;
 }
@@ -331,8 +345,8 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
     int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
     const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch, int64_t plane,
-    const long long* __restrict__ unit_off, const int* __restrict__ unit_order, int2* __restrict__ entries, double* __restrict__ base_out,
-    double* __restrict__ t_fin_out) {
+    const long long* __restrict__ unit_off, const int* __restrict__ unit_order, const int* __restrict__ row_src,
+    int2* __restrict__ entries, double* __restrict__ base_out, double* __restrict__ t_fin_out) {
     __shared__ float s_acc[27 * 128], s_w[27 * 128];
     for (int i = threadIdx.x; i < 27 * 128; i += blockDim.x) s_acc[i] = 0.f;
     __shared__ float s_thr[3 * kScatDirs];
@@ -342,11 +356,11 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
     if (slot >= n_units) return;
     const int unit = unit_order ? __ldg(unit_order + slot) : slot;  // longest first: a short tail
     const int lane = threadIdx.x & 31;
-    const int view = unit / units_per_view, u = unit - view * units_per_view;
-    const int col = (u % units_x) * kUnitW + (lane % kUnitW), row = (u / units_x) * kUnitH + (lane / kUnitW);
     const int64_t r = (int64_t)unit * 32 + lane, rows = (int64_t)n_units * 32;
+    int view, col, row;
+    const bool in = rplan_pixel(row_src ? __ldg(row_src + r) : r, units_x, units_per_view, w, h, view, col, row);
     double base[4] = {0.0, 0.0, 0.0, 0.0}, t_fin = 0.0;
-    if (col < w && row < h) {
+    if (in) {
         const fvr_camera_t& cam = cams[view];
         double d[3];
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
@@ -376,7 +390,7 @@ template <int NCH>
 __device__ __forceinline__ void rplan_render_unit(
     int unit, int lane, const int* __restrict__ unit_len, const long long* __restrict__ unit_off,
     const int2* __restrict__ entries, const double* __restrict__ base, const double* __restrict__ t_fin,
-    int64_t rows, int units_x, int units_per_view, int n_views, int w, int h, const float* __restrict__ src,
+    const int* __restrict__ row_src, int64_t rows, int units_x, int units_per_view, int n_views, int w, int h, const float* __restrict__ src,
     const float* __restrict__ values, const float4* __restrict__ cpack, const RenderConsts& rc,
     float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride) {
     const int len = unit_len[unit];
@@ -418,14 +432,14 @@ __device__ __forceinline__ void rplan_render_unit(
             for (int c = 0; c < NCH; ++c) acc[c] += (double)(__int_as_float(en.y) * cc[c]);
         }
     }
-    const int view = unit / units_per_view, u = unit - view * units_per_view;
-    const int col = (u % units_x) * kUnitW + (lane % kUnitW), row = (u / units_x) * kUnitH + (lane / kUnitW);
     const int64_t r = (int64_t)unit * 32 + lane;
+    int view, col, row;
+    const bool in = rplan_pixel(row_src ? __ldg(row_src + r) : r, units_x, units_per_view, w, h, view, col, row);
     const int64_t cstride = (int64_t)n_views * h * w;
     double sq[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) sq[c] = 0.0;
-    if (col < w && row < h) {
+    if (in) {
         const int64_t pix = ((int64_t)view * h + row) * w + col;
         const double tf = t_fin[r];
 #pragma unroll
@@ -447,7 +461,7 @@ template <int NCH>
 __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
     const int* __restrict__ unit_len, const long long* __restrict__ unit_off, const int2* __restrict__ entries,
     const double* __restrict__ base, const double* __restrict__ t_fin, const int* __restrict__ unit_order,
-    int n_units, int units_x, int units_per_view, int n_views, int w, int h, const float* __restrict__ src,
+    const int* __restrict__ row_src, int n_units, int units_x, int units_per_view, int n_views, int w, int h, const float* __restrict__ src,
     const float* __restrict__ values, const float4* __restrict__ cpack, int64_t plane, RenderConsts rc,
     float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride,
     const fvr_loop_state_t* __restrict__ state) {
@@ -460,7 +474,7 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
     for (int unit = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); unit < n_units;
          unit += (int)(((int64_t)gridDim.x * blockDim.x) >> 5))
         rplan_render_unit<NCH>(unit_order ? __ldg(unit_order + unit) : unit, lane, unit_len, unit_off, entries, base,
-                               t_fin, rows, units_x, units_per_view, n_views, w, h, src, values, cpack, rc, residual,
+                               t_fin, row_src, rows, units_x, units_per_view, n_views, w, h, src, values, cpack, rc, residual,
                                sq_partials, sq_stride);
 }
 

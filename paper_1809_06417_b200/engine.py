@@ -285,6 +285,30 @@ class ChannelLoop:
         return None if self.layout is None else self.layout.data_ptr() + 16 * ch
 
     # -- one iteration ---------------------------------------------------------
+    def _rplan_row_order(self, row_len, n_units: int, tx: int, ty: int):
+        """Rows of each tile of tx x ty units (one view) sorted longest first
+        and dealt to the tile's units in order, so the 32 rows of a unit have
+        similar lengths (SELL-C-sigma with sigma = the tile's pixels; config
+        2, 16x16-pixel tiles: padded slots / entries 1.118 -> 1.036).
+        Returns (row_src, unit_len) with row_src[r] = the natural row whose
+        pixel row r renders."""
+        t = self.t
+        dev = row_len.device
+        ux = (self.w_bb + 7) // 8
+        uy = self.bpv // ux
+        tiles_x, tiles_y = (ux + tx - 1) // tx, (uy + ty - 1) // ty
+        unit = t.arange(n_units, device=dev)
+        view, u = unit // self.bpv, unit % self.bpv
+        tile = (view * tiles_y + (u // ux) // ty) * tiles_x + (u % ux) // tx
+        tile_row = tile.repeat_interleave(32).long()
+        r = t.arange(n_units * 32, device=dev)
+        dest = t.argsort(tile_row * (n_units * 32) + r)
+        src = t.argsort(tile_row * (1 << 20) + ((1 << 20) - 1 - row_len.long()))
+        row_src = t.empty(n_units * 32, dtype=t.int32, device=dev)
+        row_src[dest] = src.to(t.int32)
+        unit_len = row_len[row_src.long()].view(n_units, 32).amax(1).to(t.int32).contiguous()
+        return row_src, unit_len
+
     def _build_render_plan(self) -> bool:
         """B of rec = B c + base + t_fin bg in SELL-32 form, built once per
         call (count pass, scan, fill pass); False when it would not fit."""
@@ -298,7 +322,13 @@ class ChannelLoop:
         geo = (self.cams.data_ptr(), n_views, self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb, self.grid,
                self.params, _lib.ptr(self.occ), self.kp_dev.data_ptr())
         unit_len = t.zeros(n_units, dtype=t.int32, device=dev)
-        _lib.call("fvr_rplan_count", *geo, unit_len.data_ptr(), stream)
+        tile = os.environ.get("FVR_RPLAN_TILE", "2x4")
+        row_len = t.empty(n_units * 32, dtype=t.int32, device=dev) if tile != "0" else None
+        _lib.call("fvr_rplan_count", *geo, unit_len.data_ptr(), _lib.ptr(row_len), stream)
+        self.rp_row_src = None
+        if row_len is not None:
+            tx, ty = (int(x) for x in tile.split("x"))
+            self.rp_row_src, unit_len = self._rplan_row_order(row_len, n_units, tx, ty)
         off = t.zeros(n_units + 1, dtype=t.int64, device=dev)
         off[1:] = t.cumsum(unit_len.long(), 0)
         slots = int(off[-1].item()) * 32
@@ -315,7 +345,7 @@ class ChannelLoop:
         self.rp_order = t.argsort(unit_len, descending=True).to(t.int32) \
             if os.environ.get("FVR_RPLAN_SORT", "1") == "1" else None
         _lib.call("fvr_rplan_fill", *geo, self.values.data_ptr(), self.nch, off.data_ptr(), _lib.ptr(self.rp_order),
-                  entries.data_ptr(), base.data_ptr(), t_fin.data_ptr(), stream)
+                  _lib.ptr(self.rp_row_src), entries.data_ptr(), base.data_ptr(), t_fin.data_ptr(), stream)
         self.rp_len, self.rp_off, self.rp_entries, self.rp_base, self.rp_tfin = unit_len, off, entries, base, t_fin
         self.rp_cpack = t.zeros(self.shape + (4,), dtype=t.float32, device=dev) if self.nch == 3 else None
         self.rplan_nnz = slots
@@ -327,7 +357,8 @@ class ChannelLoop:
         if self.rplan:
             _lib.call(
                 "fvr_rplan_render", self.rp_len.data_ptr(), self.rp_off.data_ptr(), self.rp_entries.data_ptr(),
-                self.rp_base.data_ptr(), self.rp_tfin.data_ptr(), _lib.ptr(self.rp_order), self.v_end - self.v_begin,
+                self.rp_base.data_ptr(), self.rp_tfin.data_ptr(), _lib.ptr(self.rp_order), _lib.ptr(self.rp_row_src),
+                self.v_end - self.v_begin,
                 self.w_bb, self.h_bb,
                 self.src.data_ptr(), self.values.data_ptr(), self.grid, self.nch, self.background,
                 self.kp.data_ptr(), self.n_kp, _lib.ptr(self.rp_cpack),
