@@ -132,6 +132,9 @@ class ChannelLoop:
         self.max_iters = int(max_iters)
         dev = self.dev
 
+        # FVR_INIT_PROFILE=1: host time and device events at section marks
+        self._marks = [] if os.environ.get("FVR_INIT_PROFILE") == "1" else None
+        self._mark("start")
         # geometry and inputs
         self.cams = _lib.cameras_tensor([cameras[v] for v in local], dev) if local else None
         if t.is_tensor(src_blocks):  # ([C,] V, h, w) f32 device crops (DeviceFrames)
@@ -146,7 +149,11 @@ class ChannelLoop:
             raise ValueError("src channels do not match n_channels")
         shape = (grid_geom.nx + 1, grid_geom.ny + 1, grid_geom.nz + 1)
         self.shape = shape
-        self.inside = t.from_numpy(np.ascontiguousarray(inside, dtype=np.uint8)).to(dev)
+        inside = np.ascontiguousarray(inside)
+        if inside.dtype == np.bool_:  # upload the bytes as they are (no host-side u8 copy)
+            self.inside = t.from_numpy(inside).to(dev).view(t.uint8)
+        else:
+            self.inside = t.from_numpy(inside.astype(np.uint8)).to(dev)
         self.values = t.empty((C,) + shape, dtype=t.float32, device=dev)
         if values is not None:
             self.values.copy_(t.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).reshape((C,) + shape))
@@ -170,31 +177,7 @@ class ChannelLoop:
             self.kp = t.from_numpy(kp_idx if kp_idx.size else np.zeros(1, np.int32)).to(dev)
         self.accum = None  # scatter path only
 
-        # flame rays of the local views, row-major per view (reconstruct.py:144-149)
-        if t.is_tensor(masks):  # (V, H, W) u8 device masks: compact on the device
-            sub = masks[:, bbox.v0:bbox.v1 + 1, bbox.u0:bbox.u1 + 1]
-            per_view = sub.reshape(V, -1).sum(1).cpu().tolist()
-            ray_base = int(sum(per_view[: self.v_begin]))
-            nz = t.nonzero(sub[self.v_begin:self.v_end])  # (N, 3): view, row, col -- lexicographic
-            ray_list_t = ((nz[:, 0] << 24) | (nz[:, 1] * self.w_bb + nz[:, 2])).to(t.int32)
-            self.n_rays = int(ray_list_t.numel())
-            self.rays = ray_list_t if self.n_rays else t.zeros(1, dtype=t.int32, device=dev)
-        else:
-            entries = []
-            ray_base = 0
-            for v in range(V):
-                sub = masks[v].bits[bbox.slices]
-                rows, cols = np.nonzero(sub)
-                if v < self.v_begin:
-                    ray_base += rows.size
-                elif v < self.v_end:
-                    lv = v - self.v_begin
-                    entries.append((np.int64(lv) << 24) | (rows.astype(np.int64) * self.w_bb + cols))
-            ray_list = np.concatenate(entries).astype(np.int32) if entries else np.zeros(0, np.int32)
-            self.n_rays = int(ray_list.size)
-            self.rays = t.from_numpy(ray_list if ray_list.size else np.zeros(1, np.int32)).to(dev)
-        self.ray_base = ray_base
-
+        self._mark("inputs+hull kp")
         # render configuration of the loop (render_pixels without a phase: g = 0)
         self.scattering = bool(render_cfg.scattering_enabled and render_cfg.sigma_s > 0.0)
         if self.scattering:
@@ -227,8 +210,33 @@ class ChannelLoop:
                       self.occ.data_ptr(), _lib.stream_ptr())
         self.kp_dev = kp_dev
 
-        # work buffers
+        # the render plan's count pass only needs the geometry: enqueue it
+        # now so it runs while the host prepares the flame rays
         self.bpv = int(_lib.load().fvr_loop_blocks_per_view(self.w_bb, self.h_bb))
+        self.rplan = False
+        self.rplan_nnz = 0
+        self._rp_counted = None
+        if self.layout_kind and os.environ.get("FVR_RENDER", "plan") != "march":
+            self._rp_counted = self._rplan_count()
+        self._mark("layout+occupancy")
+        # flame rays of the local views, row-major per view (reconstruct.py:144-149)
+        # compacted on the device (host masks: the bbox crops are uploaded)
+        if t.is_tensor(masks):  # (V, H, W) u8 device masks
+            sub = masks[:, bbox.v0:bbox.v1 + 1, bbox.u0:bbox.u1 + 1]
+        else:
+            crops = np.stack([np.asarray(masks[v].bits[bbox.slices], dtype=np.uint8) for v in range(V)])
+            sub = t.from_numpy(crops).to(dev)
+        ray_base = 0
+        if self.v_begin > 0:
+            ray_base = int(sub[: self.v_begin].reshape(-1).count_nonzero().item())
+        nz = t.nonzero(sub[self.v_begin:self.v_end])  # (N, 3): view, row, col -- lexicographic
+        ray_list_t = ((nz[:, 0] << 24) | (nz[:, 1] * self.w_bb + nz[:, 2])).to(t.int32)
+        self.n_rays = int(ray_list_t.numel())
+        self.rays = ray_list_t if self.n_rays else t.zeros(1, dtype=t.int32, device=dev)
+        self.ray_base = ray_base
+
+        self._mark("flame rays")
+        # work buffers
         # channels interleaved per pixel (pitch 1, or 4 for three channels)
         self.pitch = 1 if C == 1 else 4
         self.residual = t.zeros((max(len(local), 1), self.h_bb, self.w_bb, self.pitch), dtype=t.float32,
@@ -260,16 +268,30 @@ class ChannelLoop:
         self.plan_nnz = 0
         self.n_samples = 0
         self.rho = None
-        if self.plan:
-            self.plan = self._build_plan()
+        # Both operators' count passes are enqueued, their sizes read with one
+        # synchronisation, and the two fills run concurrently (the adjust
+        # plan's on a side stream; every buffer is allocated on the loop's
+        # stream, so the caching allocator keeps them across calls).
+        self._mark("work buffers")
+        pc = self._plan_count() if self.plan else None
+        rs = self._rplan_scan(*self._rp_counted) if self._rp_counted is not None else None
+        self._rp_counted = None
+        scalars = (pc["sizes"] if pc else []) + (rs["sizes"] if rs else [])
+        host = t.stack(scalars).cpu().tolist() if scalars else []
+        keep = []
+        if pc is not None:
+            main = t.cuda.current_stream()
+            side = t.cuda.Stream()
+            self.plan = self._plan_fill(pc, host[: len(pc["sizes"])], side, keep)
             self.sample_plan = self.plan and self.sample_plan
+        if rs is not None:
+            self.rplan = self._rplan_fill(rs, host[len(pc["sizes"]) if pc else 0:])
+        if pc is not None:
+            main.wait_stream(side)
+        del keep
+        self._mark("plans")
         if not self.plan:
             self.accum = t.zeros((C,) + shape, dtype=t.int64, device=dev)
-        # K-render as a fixed sparse operator (fvr_rplan.cuh) when it fits
-        self.rplan = False
-        self.rplan_nnz = 0
-        if self.layout_kind and os.environ.get("FVR_RENDER", "plan") != "march":
-            self.rplan = self._build_render_plan()
         # A CUDA graph only pays off when an iteration is launch-bound (a few
         # tens of microseconds of device work); for larger problems the host
         # enqueues 3-4 launches (~30 us) far ahead of the device, and graph
@@ -279,6 +301,18 @@ class ChannelLoop:
                           and os.environ.get("FVR_NO_GRAPH") != "1") or os.environ.get("FVR_GRAPH") == "1"
         self.graph = None
         self.launches_per_iter = 0
+
+    def _mark(self, name: str) -> None:
+        if self._marks is not None:
+            ev = self.t.cuda.Event(enable_timing=True)
+            ev.record()
+            self._marks.append((name, time.perf_counter(), ev))
+
+    def init_profile(self):
+        """[(section, host ms, device ms)] between FVR_INIT_PROFILE marks."""
+        self.t.cuda.synchronize()
+        m = self._marks or []
+        return [(b[0], 1e3 * (b[1] - a[1]), a[2].elapsed_time(b[2])) for a, b in zip(m, m[1:])]
 
     def _layout_channel(self, ch: int):
         """Address of channel ch's first float4 in the interleaved layout."""
@@ -309,29 +343,46 @@ class ChannelLoop:
         unit_len = row_len[row_src.long()].view(n_units, 32).amax(1).to(t.int32).contiguous()
         return row_src, unit_len
 
-    def _build_render_plan(self) -> bool:
-        """B of rec = B c + base + t_fin bg in SELL-32 form, built once per
-        call (count pass, scan, fill pass); False when it would not fit."""
+    def _rplan_geo(self):
+        return (self.cams.data_ptr(), self.v_end - self.v_begin, self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb,
+                self.grid, self.params, _lib.ptr(self.occ), self.kp_dev.data_ptr())
+
+    def _rplan_count(self):
+        """Count pass of the render plan (enqueued only): (unit_len, row_len)."""
         if self.v_end <= self.v_begin:
-            return False
+            return None
+        t = self.t
+        n_units = (self.v_end - self.v_begin) * self.bpv
+        unit_len = t.zeros(n_units, dtype=t.int32, device=self.dev)
+        row_len = t.empty(n_units * 32, dtype=t.int32, device=self.dev) \
+            if os.environ.get("FVR_RPLAN_TILE", "2x4") != "0" else None
+        _lib.call("fvr_rplan_count", *self._rplan_geo(), unit_len.data_ptr(), _lib.ptr(row_len), _lib.stream_ptr())
+        return unit_len, row_len
+
+    def _rplan_scan(self, unit_len, row_len) -> dict:
+        """Row order and unit offsets of the render plan after its count pass
+        (enqueued only; the total is read by _rplan_fill)."""
+        t = self.t
+        n_units = unit_len.numel()
+        row_src = None
+        if row_len is not None:
+            tx, ty = (int(x) for x in os.environ.get("FVR_RPLAN_TILE", "2x4").split("x"))
+            row_src, unit_len = self._rplan_row_order(row_len, n_units, tx, ty)
+        off = t.zeros(n_units + 1, dtype=t.int64, device=self.dev)
+        off[1:] = t.cumsum(unit_len.long(), 0)
+        return dict(unit_len=unit_len, row_src=row_src, off=off, sizes=[off[-1]])
+
+    def _rplan_fill(self, rs: dict, sizes) -> bool:
+        """B of rec = B c + base + t_fin bg in SELL-32 form (fvr_rplan.cuh),
+        filled on the current stream; False when it would not fit."""
         t = self.t
         dev = self.dev
         stream = _lib.stream_ptr()
-        n_views = self.v_end - self.v_begin
-        n_units = n_views * self.bpv
-        geo = (self.cams.data_ptr(), n_views, self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb, self.grid,
-               self.params, _lib.ptr(self.occ), self.kp_dev.data_ptr())
-        unit_len = t.zeros(n_units, dtype=t.int32, device=dev)
-        tile = os.environ.get("FVR_RPLAN_TILE", "2x4")
-        row_len = t.empty(n_units * 32, dtype=t.int32, device=dev) if tile != "0" else None
-        _lib.call("fvr_rplan_count", *geo, unit_len.data_ptr(), _lib.ptr(row_len), stream)
-        self.rp_row_src = None
-        if row_len is not None:
-            tx, ty = (int(x) for x in tile.split("x"))
-            self.rp_row_src, unit_len = self._rplan_row_order(row_len, n_units, tx, ty)
-        off = t.zeros(n_units + 1, dtype=t.int64, device=dev)
-        off[1:] = t.cumsum(unit_len.long(), 0)
-        slots = int(off[-1].item()) * 32
+        unit_len, off = rs["unit_len"], rs["off"]
+        n_units = unit_len.numel()
+        geo = self._rplan_geo()
+        self.rp_row_src = rs["row_src"]
+        slots = int(sizes[0]) * 32
         need = 8 * slots + 8 * (self.nch + 1) * n_units * 32
         if need > self.PLAN_MAX_BYTES:
             return False
@@ -437,11 +488,12 @@ class ChannelLoop:
     # plans larger than this (or that do not fit) fall back to the kernels they replace
     PLAN_MAX_BYTES = 48 << 30
 
-    def _build_plan(self) -> bool:
-        """CSR of the back-projection operator (fvr_plan.cu): row = hull key
-        point, entry = (residual pixel, W) merged per ray run in deterministic
-        mode, (in-hull sample id, W) unmerged in stochastic mode.  Built once
-        per call; returns False (scatter fallback) when it would not fit."""
+    def _plan_count(self) -> dict:
+        """Count pass and SELL layout of the back-projection operator
+        (fvr_plan.cu): row = hull key point, entry = (residual pixel, W)
+        merged per ray run in deterministic mode, (in-hull sample id, W)
+        unmerged in stochastic mode.  Enqueued only: the sizes are read by
+        _plan_fill together with the render plan's (one synchronisation)."""
         t = self.t
         dev = self.dev
         stream = _lib.stream_ptr()
@@ -449,9 +501,9 @@ class ChannelLoop:
         kp_map = t.full((n_lat,), -1, dtype=t.int32, device=dev)
         kp_map[self.kp[: self.n_kp].long()] = t.arange(self.n_kp, dtype=t.int32, device=dev)
         counts = t.zeros(self.n_kp, dtype=t.int32, device=dev)
-        c = self.cfg
         geo = (self.cams.data_ptr(), self.rays.data_ptr(), self.n_rays, self.bbox.u0, self.bbox.v0, self.w_bb,
                self.h_bb, self.inside.data_ptr(), self.grid)
+        ray_samples = None
         if self.sample_plan:
             ray_samples = t.zeros(self.n_rays, dtype=t.int32, device=dev)
             _lib.call("fvr_sample_plan_count", *geo, kp_map.data_ptr(), counts.data_ptr(), ray_samples.data_ptr(),
@@ -481,9 +533,22 @@ class ChannelLoop:
         slice_len = slice_len.view(n_slices, 32).amax(1).contiguous()
         slice_off = t.zeros(n_slices + 1, dtype=t.int64, device=dev)
         slice_off[1:] = t.cumsum(slice_len.long(), 0)
-        slots = int(slice_off[-1].item()) * 32
-        nnz = int(counts.long().sum().item())
-        n_samples = int(ray_samples.long().sum().item()) if self.sample_plan else 0
+        sizes = [slice_off[-1], counts.long().sum()]
+        if ray_samples is not None:
+            sizes.append(ray_samples.long().sum())
+        return dict(geo=geo, kp_map=kp_map, ray_samples=ray_samples, row_of_pos=row_of_pos, row_pos=row_pos,
+                    slice_len=slice_len, slice_off=slice_off, sizes=sizes)
+
+    def _plan_fill(self, pc: dict, sizes, side, keep: list) -> bool:
+        """Allocate and zero (on the current stream) and fill the plan on the
+        stream ``side``; the temporaries the fill reads go to ``keep`` until
+        it is done.  False (scatter fallback) when the plan would not fit."""
+        t = self.t
+        dev = self.dev
+        c = self.cfg
+        slots = int(sizes[0]) * 32
+        nnz = int(sizes[1])
+        n_samples = int(sizes[2]) if self.sample_plan else 0
         need = 8 * slots + 12 * n_samples
         if need > self.PLAN_MAX_BYTES or n_samples >= 2 ** 31:
             return False
@@ -492,22 +557,27 @@ class ChannelLoop:
             entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
         except t.cuda.OutOfMemoryError:
             return False
-        sell = (row_pos.data_ptr(), slice_off.data_ptr(), cursor.data_ptr(), entries.data_ptr())
+        sell = (pc["row_pos"].data_ptr(), pc["slice_off"].data_ptr(), cursor.data_ptr(), entries.data_ptr())
+        keep += [pc, cursor]
+        stream = side.cuda_stream
         if self.sample_plan:
             sid0 = t.zeros(self.n_rays, dtype=t.int64, device=dev)
-            sid0[1:] = t.cumsum(ray_samples[:-1].long(), 0)
+            sid0[1:] = t.cumsum(pc["ray_samples"][:-1].long(), 0)
             meta = t.empty(max(2 * n_samples, 2), dtype=t.int32, device=dev)
-            _lib.call("fvr_sample_plan_fill", *geo, c.tau, c.alpha_l, c.alpha_d_eff, kp_map.data_ptr(),
+            self.rho = t.zeros((max(n_samples, 1), self.pitch), dtype=t.float32, device=dev)
+            keep.append(sid0)
+            side.wait_stream(t.cuda.current_stream())
+            _lib.call("fvr_sample_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff, pc["kp_map"].data_ptr(),
                       sid0.data_ptr(), *sell, meta.data_ptr(), stream)
             self.sample_meta = meta
             self.n_samples = n_samples
-            self.rho = t.zeros((max(n_samples, 1), self.pitch), dtype=t.float32, device=dev)
         else:
-            _lib.call("fvr_adjust_plan_fill", *geo, c.tau, c.alpha_l, c.alpha_d_eff, kp_map.data_ptr(), *sell,
-                      stream)
-        self.plan_slice_len = slice_len
-        self.plan_slice_off = slice_off
-        self.plan_row_of_pos = row_of_pos
+            side.wait_stream(t.cuda.current_stream())
+            _lib.call("fvr_adjust_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff, pc["kp_map"].data_ptr(),
+                      *sell, stream)
+        self.plan_slice_len = pc["slice_len"]
+        self.plan_slice_off = pc["slice_off"]
+        self.plan_row_of_pos = pc["row_of_pos"]
         self.plan_entries = entries
         self.plan_nnz = nnz
         self.plan_slots = slots

@@ -59,3 +59,41 @@ call()
 acc["reconstruct_channel total (synced calls)"] = (time.perf_counter() - t0) * 1e3
 for k, v in sorted(acc.items(), key=lambda kv: -kv[1]):
     print(f"{v:8.3f} ms  {k}")
+
+# section marks inside ChannelLoop.__init__ (host ms = when the host got there)
+import os  # noqa: E402
+
+_lib.call = orig_call
+engine._lib.call = orig_call
+engine.ChannelLoop.__init__ = orig_init
+os.environ["FVR_INIT_PROFILE"] = "1"
+captured = []
+orig_run = engine.ChannelLoop.run
+
+
+def run(self, *a, **k):
+    captured.append(self)
+    return orig_run(self, *a, **k)
+
+
+engine.ChannelLoop.run = run
+t_init = []
+
+
+def init2(self, *a, **k):
+    t_init.append(time.perf_counter())
+    orig_init(self, *a, **k)
+    t_init.append(time.perf_counter())
+
+
+engine.ChannelLoop.__init__ = init2
+for _ in range(2):
+    captured.clear()
+    t_init.clear()
+    t0 = time.perf_counter()
+    call()
+    t1 = time.perf_counter()
+    print(f"call wall {1e3 * (t1 - t0):.2f} ms: before ChannelLoop {1e3 * (t_init[0] - t0):.2f} ms, "
+          f"__init__ {1e3 * (t_init[1] - t_init[0]):.2f} ms, after {1e3 * (t1 - t_init[1]):.2f} ms")
+    for name, host_ms, dev_ms in captured[0].init_profile():
+        print(f"  {name:18s} host {host_ms:7.3f} ms   device {dev_ms:7.3f} ms")
