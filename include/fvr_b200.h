@@ -83,6 +83,25 @@ typedef struct fvr_loop_state {
     int32_t work_retired; /* warps that found the queue empty (the last one resets both) */
 } fvr_loop_state_t;
 
+/* fvr_loop_finalize's arguments for a kernel that runs it in its last block
+ * (fvr_rplan_render): per channel c, the RMSE partials are sq_partials + c *
+ * sq_stride (n_views x blocks_per_view), the volume partials vol_partials +
+ * c * n_vol_blocks (NULL: none), the traces trace_rmse / trace_vol + c *
+ * trace_stride. */
+typedef struct fvr_loop_finalize {
+    int32_t n_views;
+    int32_t blocks_per_view;
+    int64_t pixels_per_view;
+    const double* vol_partials;
+    int32_t n_vol_blocks;
+    int32_t reserved;
+    int64_t n_kp;
+    double converge_eps;
+    double* trace_rmse;
+    double* trace_vol;
+    int64_t trace_stride;
+} fvr_loop_finalize_t;
+
 const char* fvr_last_error(void);
 int fvr_abi_version(void);
 /* Number of kernels this library has launched since load (for bench.py's
@@ -205,7 +224,10 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
  * natural order).  Row r = unit * 32 + lane renders the pixel of natural row
  * row_src[r] (NULL = r; natural row q is lane q % 32 of the 8x4 pixel unit
  * q / 32): the caller sorts the rows of a few neighbouring units by length
- * (row_len from the count pass) so a unit's rows need less padding. */
+ * (row_len from the count pass) so a unit's rows need less padding.  With
+ * `finalize` (single-rank loops) the last block to finish runs
+ * fvr_loop_finalize on state (one launch less per iteration; the block
+ * counter is state[0].work_retired). */
 int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                     int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
                     const uint8_t* dynamic, int32_t* unit_len, int32_t* row_len, void* stream);
@@ -220,7 +242,7 @@ int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const int
                      const float* src, const float* values, fvr_grid_t grid, int32_t n_channels,
                      const double* background, const int32_t* kp_index, int64_t n_kp, float* cpack,
                      float* residual, double* sq_partials, int64_t sq_stride,
-                     const fvr_loop_state_t* state, void* stream);
+                     fvr_loop_state_t* state, const fvr_loop_finalize_t* finalize, void* stream);
 
 /* Back-project the residual of every listed flame ray (ray_list entries are
  * view << 24 | (row_in_bbox * bbox_w + col_in_bbox)). stochastic != 0 draws
@@ -278,7 +300,8 @@ int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int6
  * Per iteration fvr_loop_weighted_residual writes rho[sid] = residual[ray] *
  * G(seed, iteration, ray_id_base + ray, k) -- the Philox stream of
  * fvr_loop_adjust -- and fvr_loop_gather runs over the sample plan with rho
- * in place of the residual. */
+ * in place of the residual.  state_advanced = 1 when the iteration's finalize
+ * has already run (fused into fvr_rplan_render): the key is then it - 1. */
 int fvr_sample_plan_count(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
                           int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
                           const uint8_t* inside_vox, fvr_grid_t grid, const int32_t* kp_map,
@@ -292,7 +315,7 @@ int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int6
 int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, const int32_t* ray_list,
                                int32_t bbox_w, int32_t bbox_h, const float* residual, int32_t n_channels,
                                uint64_t seed, double g_sigma, int64_t ray_id_base, float* rho,
-                               const fvr_loop_state_t* state, void* stream);
+                               const fvr_loop_state_t* state, int32_t state_advanced, void* stream);
 /* Plans are SELL-32 (fvr_plan.cu): rows (hull key points) sorted by length,
  * row_pos[row] = sorted position, row_of_pos its inverse, slices of 32
  * positions with slice_len (longest row) and slice_off (exclusive scan, in

@@ -73,6 +73,22 @@ class FvrLoopState(ctypes.Structure):
     ]
 
 
+class FvrLoopFinalize(ctypes.Structure):
+    _fields_ = [
+        ("n_views", c_int32),
+        ("blocks_per_view", c_int32),
+        ("pixels_per_view", c_int64),
+        ("vol_partials", c_void_p),
+        ("n_vol_blocks", c_int32),
+        ("reserved", c_int32),
+        ("n_kp", c_int64),
+        ("converge_eps", c_double),
+        ("trace_rmse", c_void_p),
+        ("trace_vol", c_void_p),
+        ("trace_stride", c_int64),
+    ]
+
+
 _P = c_void_p  # every pointer argument is passed as an address
 _GRID = FvrGrid
 _PARAMS = FvrRenderParams
@@ -132,13 +148,13 @@ _SIGNATURES = {
     "fvr_rplan_fill": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _GRID, _PARAMS, _P, _P, _P, c_int32,
                                _P, _P, _P, _P, _P, _P, _P]),
     "fvr_rplan_render": (c_int, [_P, _P, _P, _P, _P, _P, _P, c_int32, c_int32, c_int32, _P, _P, _GRID, c_int32, _P, _P,
-                                 c_int64, _P, _P, _P, c_int64, _P, _P]),
+                                 c_int64, _P, _P, _P, c_int64, _P, _P, _P]),
     "fvr_sample_plan_count": (c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, _P, _P, _P,
                                       _P]),
     "fvr_sample_plan_fill": (c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, c_double,
                                      c_double, c_double, _P, _P, _P, _P, _P, _P, _P, _P]),
     "fvr_loop_weighted_residual": (c_int, [_P, c_int64, _P, c_int32, c_int32, _P, c_int32, c_uint64, c_double,
-                                           c_int64, _P, _P, _P]),
+                                           c_int64, _P, _P, c_int32, _P]),
     "fvr_loop_gather": (c_int, [_P, _P, _P, _P, c_int64, _P, c_int32, _P, _P, _P, c_int32, _GRID, _P, _P, _P]),
     "fvr_loop_update_packed": (c_int, [_P, c_int64, _P, _P, _P, c_int32, c_int32, _GRID, _P, _P]),
     "fvr_pack_correction": (c_int, [_P, _P, c_int64, _P, _P]),

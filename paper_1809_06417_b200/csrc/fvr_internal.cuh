@@ -72,6 +72,47 @@ __device__ __forceinline__ void layout_store(float* __restrict__ p, int nch, int
 template <int NCH>
 constexpr int kResPitch = NCH == 1 ? 1 : 4;
 
+// The convergence bookkeeping of one channel (reconstruct.py:311-323), run by
+// one block: per-view RMSE from the kernels' squared-residual partials (warp
+// per view: lane-strided sums, then a fixed shuffle tree), mean over views,
+// trace append, optional vol_rmse and the rule.  Fixed order: bit-identical
+// wherever it runs.  s_view: >= n_views doubles of shared memory.
+__device__ __forceinline__ void finalize_block(const double* sq, int n_views, int bpv, double pixels,
+                                               const double* vol, int n_vol, double n_kp, double eps,
+                                               double* trace, double* trace_vol, fvr_loop_state_t* st,
+                                               double* s_view) {
+    if (st->done) return;  // uniform: every thread reads the same state
+    const int lane = threadIdx.x & 31;
+    for (int v = threadIdx.x >> 5; v < n_views; v += blockDim.x >> 5) {
+        double s = 0.0;
+        for (int b = lane; b < bpv; b += 32) s += __ldcg(sq + (int64_t)v * bpv + b);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) s_view[v] = sqrt(s / pixels);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double acc = 0.0;
+        for (int i = 0; i < n_views; ++i) acc += s_view[i];
+        const double rmse = acc / (double)n_views;
+        const int it = st->it;
+        trace[it] = rmse;
+        if (vol && trace_vol) {
+            double s = 0.0;
+            for (int b = 0; b < n_vol; ++b) s += __ldcg(vol + b);
+            trace_vol[it] = sqrt(s / n_kp);
+        }
+        const bool conv = rmse < eps || (it > 0 && fabs(rmse - st->prev_rmse) < eps);
+        st->prev_rmse = rmse;
+        st->it = it + 1;
+        if (conv) {
+            st->converged = 1;
+            st->done = 1;
+        }
+    }
+    __syncthreads();
+}
+
 }  // namespace fvr
 
 #define FVR_TRY_BEGIN try {

@@ -31,36 +31,8 @@ __global__ void finalize_kernel(const double* __restrict__ sq, int n_views, int 
                                 double pixels, const double* __restrict__ vol, int n_vol,
                                 double n_kp, double eps, double* __restrict__ trace,
                                 double* __restrict__ trace_vol, fvr_loop_state_t* __restrict__ st) {
-    if (st->done) return;
     __shared__ double view_rmse[32];
-    // warp v reduces view v: lane-strided partial sums, then a fixed shuffle tree
-    const int v = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (v < n_views) {
-        double s = 0.0;
-        for (int b = lane; b < bpv; b += 32) s += sq[(int64_t)v * bpv + b];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0) view_rmse[v] = sqrt(s / pixels);
-    }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    double acc = 0.0;
-    for (int i = 0; i < n_views; ++i) acc += view_rmse[i];
-    const double rmse = acc / (double)n_views;
-    const int it = st->it;
-    trace[it] = rmse;
-    if (vol && trace_vol) {
-        double s = 0.0;
-        for (int b = 0; b < n_vol; ++b) s += vol[b];
-        trace_vol[it] = sqrt(s / n_kp);
-    }
-    const bool conv = rmse < eps || (it > 0 && fabs(rmse - st->prev_rmse) < eps);
-    st->prev_rmse = rmse;
-    st->it = it + 1;
-    if (conv) {
-        st->converged = 1;
-        st->done = 1;
-    }
+    finalize_block(sq, n_views, bpv, pixels, vol, n_vol, n_kp, eps, trace, trace_vol, st, view_rmse);
 }
 
 }  // namespace fvr

@@ -251,8 +251,9 @@ template <int NCH>
 __global__ void __launch_bounds__(256) weighted_residual_kernel(
     const int2* __restrict__ meta, int64_t n_samples, const int32_t* __restrict__ ray_list, int w, int h,
     const float* __restrict__ residual, uint64_t seed, float g_sigma, int64_t ray_id_base,
-    float* __restrict__ rho, const fvr_loop_state_t* __restrict__ state) {
-    // the live channels share the iteration count (a converged one stops counting)
+    float* __restrict__ rho, const fvr_loop_state_t* __restrict__ state, int it_back) {
+    // the live channels share the iteration count (a converged one stops
+    // counting); it_back = 1 when this iteration's finalize already ran
     uint32_t it = 0;
     bool any = !state;
     if (state) {
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
         }
     }
     if (!any) return;
+    it -= (uint32_t)it_back;
     constexpr int P = kResPitch<NCH>;
     for (int64_t sid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sid < n_samples;
          sid += (int64_t)gridDim.x * blockDim.x) {
@@ -483,7 +485,8 @@ extern "C" int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray
 extern "C" int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, const int32_t* ray_list,
                                           int32_t bbox_w, int32_t bbox_h, const float* residual,
                                           int32_t n_channels, uint64_t seed, double g_sigma, int64_t ray_id_base,
-                                          float* rho, const fvr_loop_state_t* state, void* stream) {
+                                          float* rho, const fvr_loop_state_t* state, int32_t state_advanced,
+                                          void* stream) {
     FVR_TRY_BEGIN
     if (n_samples == 0) return FVR_OK;
     if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "1 or 3 channels");
@@ -492,10 +495,12 @@ extern "C" int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_
     const auto* meta = reinterpret_cast<const int2*>(sample_meta);
     if (n_channels == 1)
         weighted_residual_kernel<1><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-            meta, n_samples, ray_list, bbox_w, bbox_h, residual, seed, (float)g_sigma, ray_id_base, rho, state);
+            meta, n_samples, ray_list, bbox_w, bbox_h, residual, seed, (float)g_sigma, ray_id_base, rho, state,
+            state_advanced ? 1 : 0);
     else
         weighted_residual_kernel<3><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-            meta, n_samples, ray_list, bbox_w, bbox_h, residual, seed, (float)g_sigma, ray_id_base, rho, state);
+            meta, n_samples, ray_list, bbox_w, bbox_h, residual, seed, (float)g_sigma, ray_id_base, rho, state,
+            state_advanced ? 1 : 0);
     return check_launch("loop_weighted_residual");
     FVR_TRY_END
 }

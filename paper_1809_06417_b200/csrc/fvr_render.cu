@@ -1115,10 +1115,29 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
                                 int32_t bbox_h, const float* src, const float* values, fvr_grid_t grid,
                                 int32_t n_channels, const double* background, const int32_t* kp_index, int64_t n_kp,
                                 float* cpack, float* residual, double* sq_partials, int64_t sq_stride,
-                                const fvr_loop_state_t* state, void* stream) {
+                                fvr_loop_state_t* state, const fvr_loop_finalize_t* finalize, void* stream) {
     FVR_TRY_BEGIN
     if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "the loop renders 1 or 3 channels");
     if (!background) return set_error(FVR_ERR_INVALID, "background is NULL");
+    RplanFinalize fin{};
+    if (finalize) {
+        if (!state) return set_error(FVR_ERR_INVALID, "a fused finalize needs the loop state");
+        if (finalize->n_views < 1 || finalize->n_views > 32)
+            return set_error(FVR_ERR_INVALID, "n_views must be in 1..32");
+        if (finalize->pixels_per_view < 1) return set_error(FVR_ERR_INVALID, "empty bounding box");
+        if (!finalize->trace_rmse) return set_error(FVR_ERR_INVALID, "trace_rmse is NULL");
+        fin.on = true;
+        fin.n_views = finalize->n_views;
+        fin.bpv = finalize->blocks_per_view;
+        fin.n_vol = finalize->n_vol_blocks;
+        fin.pixels = (double)finalize->pixels_per_view;
+        fin.n_kp = (double)finalize->n_kp;
+        fin.eps = finalize->converge_eps;
+        fin.vol = finalize->vol_partials;
+        fin.trace = finalize->trace_rmse;
+        fin.trace_vol = finalize->trace_vol;
+        fin.trace_stride = finalize->trace_stride;
+    }
     if (n_channels == 3 && (!cpack || (!kp_index && n_kp > 0)))
         return set_error(FVR_ERR_INVALID, "three channels need the cpack scratch and the key-point list");
     fvr_render_params_t p{};
@@ -1137,7 +1156,7 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
         rplan_render_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, en, base, t_fin, unit_order, row_src,
                                                                 n_units, units_x, upv,
                                                                 n_views, bbox_w, bbox_h, src, values, nullptr, plane,
-                                                                rc, residual, sq_partials, sq_stride, state);
+                                                                rc, residual, sq_partials, sq_stride, state, fin);
     } else {
         if (n_kp > 0) {
             int64_t cb = (n_kp + 255) / 256;
@@ -1148,7 +1167,7 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
         rplan_render_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, en, base, t_fin, unit_order, row_src,
                                                                 n_units, units_x, upv,
                                                                 n_views, bbox_w, bbox_h, src, values, cp, plane, rc,
-                                                                residual, sq_partials, sq_stride, state);
+                                                                residual, sq_partials, sq_stride, state, fin);
     }
     return check_launch("rplan_render");
     FVR_TRY_END

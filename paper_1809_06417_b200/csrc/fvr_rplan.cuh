@@ -385,6 +385,17 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
 #define FVR_RPLAN_MINB 3
 #endif
 
+// fvr_loop_finalize_t on the device (on = false: no fused finalize).
+struct RplanFinalize {
+    bool on;
+    int n_views, bpv, n_vol;
+    double pixels, n_kp, eps;
+    const double* vol;
+    double* trace;
+    double* trace_vol;
+    int64_t trace_stride;
+};
+
 // One unit (8x4 pixels, lane = pixel) of K-render through the plan.
 template <int NCH>
 __device__ __forceinline__ void rplan_render_unit(
@@ -464,7 +475,7 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
     const int* __restrict__ row_src, int n_units, int units_x, int units_per_view, int n_views, int w, int h, const float* __restrict__ src,
     const float* __restrict__ values, const float4* __restrict__ cpack, int64_t plane, RenderConsts rc,
     float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride,
-    const fvr_loop_state_t* __restrict__ state) {
+    fvr_loop_state_t* __restrict__ state, RplanFinalize fin) {
     if (all_done<NCH>(state)) return;
     const int lane = threadIdx.x & 31;
     const int64_t rows = (int64_t)n_units * 32;
@@ -476,6 +487,24 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
         rplan_render_unit<NCH>(unit_order ? __ldg(unit_order + unit) : unit, lane, unit_len, unit_off, entries, base,
                                t_fin, row_src, rows, units_x, units_per_view, n_views, w, h, src, values, cpack, rc, residual,
                                sq_partials, sq_stride);
+    if (!fin.on) return;
+    // the last block to finish runs the loop's finalize (fvr_loop.cu)
+    __shared__ int s_last;
+    __shared__ double s_view[32];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&state->work_retired, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int c = 0; c < NCH; ++c)
+        finalize_block(sq_partials + c * sq_stride, fin.n_views, fin.bpv, fin.pixels,
+                       fin.vol ? fin.vol + c * fin.n_vol : nullptr, fin.n_vol, fin.n_kp, fin.eps,
+                       fin.trace + c * fin.trace_stride, fin.trace_vol ? fin.trace_vol + c * fin.trace_stride : nullptr,
+                       state + c, s_view);
+    if (threadIdx.x == 0) state->work_retired = 0;
 }
 
 // cpack[kp] = (max(v_0, 0), max(v_1, 0), max(v_2, 0), 0) at the listed key

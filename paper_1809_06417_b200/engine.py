@@ -414,7 +414,7 @@ class ChannelLoop:
                 self.src.data_ptr(), self.values.data_ptr(), self.grid, self.nch, self.background,
                 self.kp.data_ptr(), self.n_kp, _lib.ptr(self.rp_cpack),
                 self.residual.data_ptr(), self.sq[0, self.v_begin * self.bpv:].data_ptr(), self.n_sq,
-                self.state.data_ptr(), stream,
+                self.state.data_ptr(), self._fused_finalize(), stream,
             )
             return 1
         _lib.call(
@@ -450,6 +450,30 @@ class ChannelLoop:
                 self.n_kp, self.vol[ch].data_ptr(), ctypes.byref(nvb), self.state[ch].data_ptr(), stream,
             )
         return self.nch
+
+    def _fused(self) -> bool:
+        """The render plan's last block runs finalize (single-rank loops with
+        the gather adjust; the scatter fallback keeps the separate launch)."""
+        return (self.rplan and self.plan and not self.sharded
+                and os.environ.get("FVR_FUSED_FINALIZE", "1") == "1")
+
+    def _fused_finalize(self):
+        if not self._fused():
+            return None
+        if getattr(self, "_fin_args", None) is None:
+            f = _lib.FvrLoopFinalize()
+            f.n_views = self.n_views
+            f.blocks_per_view = self.bpv
+            f.pixels_per_view = self.w_bb * self.h_bb
+            f.vol_partials = _lib.ptr(self.vol)
+            f.n_vol_blocks = self.n_vol
+            f.n_kp = self.n_kp
+            f.converge_eps = self.cfg.converge_eps
+            f.trace_rmse = self.trace.data_ptr()
+            f.trace_vol = _lib.ptr(self.trace_vol)
+            f.trace_stride = self.trace.shape[1]
+            self._fin_args = f
+        return ctypes.addressof(self._fin_args)
 
     def _finalize(self, stream):
         pix = self.w_bb * self.h_bb
@@ -589,7 +613,7 @@ class ChannelLoop:
         _lib.call("fvr_loop_weighted_residual", self.sample_meta.data_ptr(), self.n_samples,
                   self.rays.data_ptr(), self.w_bb, self.h_bb, self.residual.data_ptr(), self.nch,
                   c.seed & 0xFFFFFFFFFFFFFFFF, c.g_sigma, self.ray_base, self.rho.data_ptr(),
-                  self.state.data_ptr(), stream)
+                  self.state.data_ptr(), 1 if self._fused() else 0, stream)
         return 1
 
     def _gather(self, stream, packed: bool):
@@ -620,6 +644,11 @@ class ChannelLoop:
     def stages(self):
         """[(name, fn(stream) -> launches)] of one iteration, in order; the
         name 'decision' marks where the convergence rule has been evaluated."""
+        if self._fused():  # render -> finalize in one launch; the volume partials first
+            s = [("volume", self._volume), ("render", self._render)]
+            if self.sample_plan:
+                s += [("weigh", self._weigh)]
+            return s + [("decision", None), ("adjust", lambda st: self._gather(st, False))]
         s = [("render", self._render), ("volume", self._volume)]
         if self.sample_plan:
             s += [("weigh", self._weigh)]
