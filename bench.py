@@ -354,9 +354,10 @@ def run_gpu(args):
     if loop.rplan:
         kname = "rplan_render_kernel<1>"
         rows = loop.rp_len.numel() * 32
-        kbytes = 8 * loop.rplan_nnz + 16 * rows + 8 * w["VP"]
-        rule = ("render plan: 8 B per stored SELL entry (key point, f32 weight) + 16 B per row (base, t_fin) + "
-                "8 B per bbox pixel (src in, residual out); the lattice gathers hit L2")
+        kbytes = 6 * loop.rplan_nnz + 16 * rows + 8 * w["VP"]
+        rule = ("render plan: 6 B per stored SELL entry (24-bit key-point index + 24-bit weight) + 16 B per row "
+                "(base, t_fin) + 8 B per bbox pixel (src in, residual out); the key-point operand (1.2 MB) hits "
+                "L1/L2")
     else:
         kname = "loop_render_scat_kernel"
         kbytes = live_bytes
@@ -433,9 +434,9 @@ def run_gpu(args):
         "iter_algorithmic_bytes": iter_bytes,
         "iter_roofline_frac": iter_bytes * its / (peak * 1e9),
         # Dominant kernel = K-render.  Through the render plan it streams B
-        # (8 B per stored SELL entry, padding included) plus per-row base and
-        # t_fin (16 B) and src/residual (8 B per pixel); the lattice it
-        # multiplies is L2-resident.
+        # (6 B per stored SELL entry, padding included) plus per-row base and
+        # t_fin (16 B) and src/residual (8 B per pixel); the key-point operand
+        # it multiplies is cache-resident.
         "roofline": roof,
         "roofline_survey_rule": {"bytes_per_launch": live_bytes, "achieved": live_achieved,
                                  "frac": live_achieved / peak,

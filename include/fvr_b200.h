@@ -209,17 +209,22 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
 /* K-render as a fixed operator (the render plan, csrc/fvr_rplan.cuh).  The
  * loop's forward model is linear in max(v, 0) with geometry-only weights, so
  * rec = B c + base + t_fin * bg.  B is stored SELL-32 by K-render's 8x4
- * pixel units: unit_len[unit] (count pass) = longest row of the unit;
- * unit_off = exclusive scan of unit_len; entry t of row (unit, lane) at
- * int2 index unit_off[unit] * 32 + 32 t + lane = (key point, f32 weight).
- * Columns are the key points flagged in `dynamic` (the loop's hull key
- * points); the others fold into base (n_channels x rows f64, rows =
- * n_units * 32) from `values`.  Needs the fast render modes (g = 0, gather =
- * edge, 32 directions loaded); occ is the distance map (may be NULL).
- * fvr_rplan_render replaces fvr_loop_render with identical outputs; with 3
- * channels it first packs max(v, 0) of the listed key points (kp_index,
- * n_kp: the loop's hull key points) into cpack (lattice x float4 scratch) so
- * each entry is one 16-byte read.  Fill and render visit the units in the
+ * pixel units: unit_len[unit] (count pass) = longest row of the unit
+ * (the caller rounds it up to even); unit_off = exclusive scan of unit_len.
+ * Entry t of row (unit, lane) is 6 bytes: entries_a[(unit_off[unit] + t) *
+ * 32 + lane] = column | weight exponent << 24, and the weight's top 16
+ * mantissa bits in half t % 2 of entries_b[((unit_off[unit] + t) / 2) * 32 +
+ * lane] (weights >= 0, relative rounding <= 2^-17).  Columns are the
+ * key points flagged in `dynamic` (the loop's hull key points), numbered by
+ * kp_map (lattice -> index in the loop's key-point list); the others fold
+ * into base (n_channels x rows f64, rows = n_units * 32) from `values`.
+ * Needs the fast render modes (g = 0, gather = edge, 32 directions loaded);
+ * occ is the distance map (may be NULL).
+ * fvr_rplan_render replaces fvr_loop_render with identical outputs (to the
+ * weight rounding); its operand kp_values holds max(v, 0) per hull key point
+ * (f32, or float4 for 3 channels): fvr_rplan_pack fills it, and
+ * fvr_loop_gather / fvr_loop_update_packed keep it current.  Fill and
+ * render visit the units in the
  * order unit_order (a permutation of the units, longest first; NULL =
  * natural order).  Row r = unit * 32 + lane renders the pixel of natural row
  * row_src[r] (NULL = r; natural row q is lane q % 32 of the 8x4 pixel unit
@@ -234,15 +239,16 @@ int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
 int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                    int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
                    const uint8_t* dynamic, const float* values, int32_t n_channels, const int64_t* unit_off,
-                   const int32_t* unit_order, const int32_t* row_src, int32_t* entries, double* base,
-                   double* t_fin, void* stream);
-int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const int32_t* entries,
-                     const double* base, const double* t_fin, const int32_t* unit_order,
-                     const int32_t* row_src, int32_t n_views, int32_t bbox_w, int32_t bbox_h,
-                     const float* src, const float* values, fvr_grid_t grid, int32_t n_channels,
-                     const double* background, const int32_t* kp_index, int64_t n_kp, float* cpack,
-                     float* residual, double* sq_partials, int64_t sq_stride,
+                   const int32_t* unit_order, const int32_t* row_src, const int32_t* kp_map,
+                   uint32_t* entries_a, uint32_t* entries_b, double* base, double* t_fin, void* stream);
+int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const uint32_t* entries_a,
+                     const uint32_t* entries_b, const double* base, const double* t_fin,
+                     const int32_t* unit_order, const int32_t* row_src, int32_t n_views, int32_t bbox_w,
+                     int32_t bbox_h, const float* src, const float* kp_values, int32_t n_channels,
+                     const double* background, float* residual, double* sq_partials, int64_t sq_stride,
                      fvr_loop_state_t* state, const fvr_loop_finalize_t* finalize, void* stream);
+int fvr_rplan_pack(const float* values, int32_t n_channels, fvr_grid_t grid, const int32_t* kp_index,
+                   int64_t n_kp, float* kp_values, const fvr_loop_state_t* state, void* stream);
 
 /* Back-project the residual of every listed flame ray (ray_list entries are
  * view << 24 | (row_in_bbox * bbox_w + col_in_bbox)). stochastic != 0 draws
@@ -327,14 +333,17 @@ int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, co
  * all-reduce.  n_channels (1 or 3) share the plan: the residual (or rho)
  * holds a pixel's (sample's) channels interleaved with pitch 1 or 4, values /
  * layout hold n_channels lattice planes and state n_channels loop states
- * (converged channels are skipped). */
+ * (converged channels are skipped).  kp_values (may be NULL): the render
+ * plan's operand (fvr_rplan_pack), updated with every written value. */
 int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_off, const int32_t* row_of_pos,
                     const int32_t* entries, int64_t n_kp, const float* residual, int32_t n_channels,
                     const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
-                    fvr_grid_t grid, int64_t* packed, const fvr_loop_state_t* state, void* stream);
+                    fvr_grid_t grid, float* kp_values, int64_t* packed, const fvr_loop_state_t* state,
+                    void* stream);
 int fvr_loop_update_packed(const int64_t* packed, int64_t n_kp, const int32_t* kp_index,
                            float* values, float* layout, int32_t layout_kind, int32_t layout_nch,
-                           fvr_grid_t grid, const fvr_loop_state_t* state, void* stream);
+                           fvr_grid_t grid, float* kp_values, int32_t kp_values_pitch,
+                           const fvr_loop_state_t* state, void* stream);
 
 /* Multi-GPU helpers: gather accum at kp_index into a compact buffer and
  * scatter it back (the NCCL allreduce runs between them). */

@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(256, 3) gather_kernel(
     const int32_t* __restrict__ row_of_pos, const int2* __restrict__ entries, int64_t n_rows,
     const float* __restrict__ residual, const int32_t* __restrict__ kp_index,
     float* __restrict__ values, int64_t plane, float* __restrict__ layout, int layout_kind, int sy, int ny1,
-    long long* __restrict__ packed, const fvr_loop_state_t* __restrict__ state) {
+    float* __restrict__ kpv, long long* __restrict__ packed, const fvr_loop_state_t* __restrict__ state) {
     bool live[NCH];
     bool any = false;
 #pragma unroll
@@ -346,6 +346,7 @@ __global__ void __launch_bounds__(256, 3) gather_kernel(
                 const float f = (float)(nv > -1.0 ? nv : -1.0);
                 vals[idx] = f;
                 if (layout) layout_store(layout + 4 * c, NCH, layout_kind, sy, ny1, idx, f);
+                if (kpv) kpv[row * (NCH == 1 ? 1 : 4) + c] = fmaxf(f, 0.f);  // the render plan's operand
             }
         }
     }
@@ -355,6 +356,7 @@ __global__ void __launch_bounds__(256, 3) gather_kernel(
 __global__ void update_packed_kernel(const long long* __restrict__ packed, int64_t n_rows,
                                      const int32_t* __restrict__ kp_index, float* __restrict__ values,
                                      float* __restrict__ layout, int layout_kind, int layout_nch, int sy, int ny1,
+                                     float* __restrict__ kpv, int kpv_pitch,
                                      const fvr_loop_state_t* __restrict__ state) {
     if (state && state->done) return;
     for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n_rows;
@@ -366,6 +368,7 @@ __global__ void update_packed_kernel(const long long* __restrict__ packed, int64
         const float f = (float)(nv > -1.0 ? nv : -1.0);
         values[idx] = f;
         if (layout) layout_store(layout, layout_nch, layout_kind, sy, ny1, idx, f);
+        if (kpv) kpv[row * kpv_pitch] = fmaxf(f, 0.f);
     }
 }
 
@@ -409,7 +412,8 @@ extern "C" int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray
 extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_off, const int32_t* row_of_pos,
                                const int32_t* entries, int64_t n_kp, const float* residual, int32_t n_channels,
                                const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
-                               fvr_grid_t grid, int64_t* packed, const fvr_loop_state_t* state, void* stream) {
+                               fvr_grid_t grid, float* kp_values, int64_t* packed, const fvr_loop_state_t* state,
+                               void* stream) {
     FVR_TRY_BEGIN
     if (n_kp == 0) return FVR_OK;
     if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "the loop gathers 1 or 3 channels");
@@ -424,7 +428,8 @@ extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_of
     long long* pk = reinterpret_cast<long long*>(packed);
 #define FVR_GATHER(P, C)                                                                                           \
     gather_kernel<P, C><<<(unsigned)blocks, 256, 0, st>>>(slice_len, so, row_of_pos, en, n_kp, residual, kp_index, \
-                                                          values, plane, layout, layout_kind, sy, ny1, pk, state)
+                                                          values, plane, layout, layout_kind, sy, ny1, kp_values, pk, \
+                                                          state)
     if (packed) {
         if (n_channels == 1) FVR_GATHER(true, 1); else FVR_GATHER(true, 3);
     } else {
@@ -437,14 +442,15 @@ extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_of
 
 extern "C" int fvr_loop_update_packed(const int64_t* packed, int64_t n_kp, const int32_t* kp_index,
                                       float* values, float* layout, int32_t layout_kind, int32_t layout_nch,
-                                      fvr_grid_t grid, const fvr_loop_state_t* state, void* stream) {
+                                      fvr_grid_t grid, float* kp_values, int32_t kp_values_pitch,
+                                      const fvr_loop_state_t* state, void* stream) {
     FVR_TRY_BEGIN
     if (n_kp == 0) return FVR_OK;
     int64_t blocks = (n_kp + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
     update_packed_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
         reinterpret_cast<const long long*>(packed), n_kp, kp_index, values, layout, layout_kind, layout_nch,
-        grid.nz + 1, grid.ny + 1, state);
+        grid.nz + 1, grid.ny + 1, kp_values, kp_values_pitch, state);
     return check_launch("loop_update_packed");
     FVR_TRY_END
 }

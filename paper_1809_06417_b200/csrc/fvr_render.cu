@@ -1077,7 +1077,8 @@ extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t
                               int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
                               const uint8_t* dynamic, const float* values, int32_t n_channels,
                               const int64_t* unit_off, const int32_t* unit_order, const int32_t* row_src,
-                              int32_t* entries, double* base, double* t_fin, void* stream) {
+                              const int32_t* kp_map, uint32_t* entries_a, uint32_t* entries_b, double* base,
+                              double* t_fin, void* stream) {
     FVR_TRY_BEGIN
     if (n_views < 1 || bbox_w < 1 || bbox_h < 1) return set_error(FVR_ERR_INVALID, "empty render plan");
     if (n_channels < 1 || n_channels > 4) return set_error(FVR_ERR_INVALID, "n_channels must be 1..4");
@@ -1094,27 +1095,44 @@ extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t
     const unsigned blocks = (unsigned)(((int64_t)n_units * 32 + 127) / 128);
     cudaStream_t st = (cudaStream_t)stream;
     const auto* uo = reinterpret_cast<const long long*>(unit_off);
-    auto* en = reinterpret_cast<int2*>(entries);
+    if (!kp_map || !entries_a || !entries_b) return set_error(FVR_ERR_INVALID, "kp_map / entries are NULL");
     uint32_t* d27 = dyn27_scratch(grid, dynamic, st, false);
     if (!d27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
     if (m)
         rplan_fill_kernel<true><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc, occ,
                                                          dynamic, d27, values, n_channels, plane, uo, unit_order,
-                                                         row_src, en, base, t_fin);
+                                                         row_src, kp_map, entries_a, entries_b, base, t_fin);
     else
         rplan_fill_kernel<false><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
                                                           occ, dynamic, d27, values, n_channels, plane, uo,
-                                                          unit_order, row_src, en, base, t_fin);
+                                                          unit_order, row_src, kp_map, entries_a, entries_b, base,
+                                                          t_fin);
     return check_launch("rplan_fill");
     FVR_TRY_END
 }
 
-extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const int32_t* entries,
-                                const double* base, const double* t_fin, const int32_t* unit_order,
-                                const int32_t* row_src, int32_t n_views, int32_t bbox_w,
-                                int32_t bbox_h, const float* src, const float* values, fvr_grid_t grid,
-                                int32_t n_channels, const double* background, const int32_t* kp_index, int64_t n_kp,
-                                float* cpack, float* residual, double* sq_partials, int64_t sq_stride,
+extern "C" int fvr_rplan_pack(const float* values, int32_t n_channels, fvr_grid_t grid, const int32_t* kp_index,
+                              int64_t n_kp, float* kp_values, const fvr_loop_state_t* state, void* stream) {
+    FVR_TRY_BEGIN
+    if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "1 or 3 channels");
+    if (n_kp <= 0) return FVR_OK;
+    const int64_t plane = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
+    int64_t b = (n_kp + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_channels == 1)
+        rplan_pack_kernel<1><<<(unsigned)b, 256, 0, st>>>(values, plane, kp_index, n_kp, kp_values, state);
+    else
+        rplan_pack_kernel<3><<<(unsigned)b, 256, 0, st>>>(values, plane, kp_index, n_kp, kp_values, state);
+    return check_launch("rplan_pack");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const uint32_t* entries_a,
+                                const uint32_t* entries_b, const double* base, const double* t_fin,
+                                const int32_t* unit_order, const int32_t* row_src, int32_t n_views, int32_t bbox_w,
+                                int32_t bbox_h, const float* src, const float* kp_values, int32_t n_channels,
+                                const double* background, float* residual, double* sq_partials, int64_t sq_stride,
                                 fvr_loop_state_t* state, const fvr_loop_finalize_t* finalize, void* stream) {
     FVR_TRY_BEGIN
     if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "the loop renders 1 or 3 channels");
@@ -1138,37 +1156,26 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
         fin.trace_vol = finalize->trace_vol;
         fin.trace_stride = finalize->trace_stride;
     }
-    if (n_channels == 3 && (!cpack || (!kp_index && n_kp > 0)))
-        return set_error(FVR_ERR_INVALID, "three channels need the cpack scratch and the key-point list");
+    if (!kp_values || !entries_a || !entries_b) return set_error(FVR_ERR_INVALID, "kp_values / entries are NULL");
     fvr_render_params_t p{};
     p.tau = 0.0;
     RenderConsts rc = make_render_consts(p, background, n_channels);
     const int units_x = (bbox_w + kUnitW - 1) / kUnitW, upv = fvr_loop_blocks_per_view(bbox_w, bbox_h);
     const int n_units = upv * n_views;
-    const int64_t plane = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
     int64_t blocks = ((int64_t)n_units * 32 + 255) / 256;
     if (blocks > 148 * 64) blocks = 148 * 64;
     cudaStream_t st = (cudaStream_t)stream;
     const auto* uo = reinterpret_cast<const long long*>(unit_off);
-    const auto* en = reinterpret_cast<const int2*>(entries);
-    auto* cp = reinterpret_cast<float4*>(cpack);
-    if (n_channels == 1) {
-        rplan_render_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, en, base, t_fin, unit_order, row_src,
-                                                                n_units, units_x, upv,
-                                                                n_views, bbox_w, bbox_h, src, values, nullptr, plane,
-                                                                rc, residual, sq_partials, sq_stride, state, fin);
-    } else {
-        if (n_kp > 0) {
-            int64_t cb = (n_kp + 255) / 256;
-            if (cb > 148 * 16) cb = 148 * 16;
-            rplan_cpack_kernel<<<(unsigned)cb, 256, 0, st>>>(values, plane, kp_index, n_kp, cp, state);
-            count_launch(1);
-        }
-        rplan_render_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, en, base, t_fin, unit_order, row_src,
-                                                                n_units, units_x, upv,
-                                                                n_views, bbox_w, bbox_h, src, values, cp, plane, rc,
-                                                                residual, sq_partials, sq_stride, state, fin);
-    }
+    if (n_channels == 1)
+        rplan_render_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, entries_a, entries_b, base, t_fin,
+                                                                unit_order, row_src, n_units, units_x, upv, n_views,
+                                                                bbox_w, bbox_h, src, kp_values, rc, residual,
+                                                                sq_partials, sq_stride, state, fin);
+    else
+        rplan_render_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, entries_a, entries_b, base, t_fin,
+                                                                unit_order, row_src, n_units, units_x, upv, n_views,
+                                                                bbox_w, bbox_h, src, kp_values, rc, residual,
+                                                                sq_partials, sq_stride, state, fin);
     return check_launch("rplan_render");
     FVR_TRY_END
 }

@@ -105,6 +105,31 @@ __device__ __forceinline__ uint32_t support_mask(bool scat, const float dl[3], c
     return m;
 }
 
+// Render-plan entries, 6 bytes each: word a = hull key-point index (24 bits,
+// the row of the loop's key-point list) | the weight's exponent << 24, and a
+// 16-bit word with the weight's top 16 mantissa bits (weights are >= 0;
+// relative rounding error <= 2^-17).  Row r = unit * 32 + lane, entry t: a
+// at u32 index (unit_off + t) * 32 + lane, the 16-bit word in the u32 pair
+// array at ((unit_off + t) / 2) * 32 + lane, half t % 2 (unit_off and unit
+// lengths even).
+constexpr uint32_t kRplanIdxMask = 0xFFFFFFu;
+
+__device__ __forceinline__ float rplan_weight(uint32_t a, uint32_t half16) {
+    return __uint_as_float(((a >> 24) << 23) | (half16 << 7));
+}
+
+struct RplanOut {
+    uint32_t* a;         // this row's first a word
+    uint16_t* b;         // this row's first 16-bit word
+    const int* kp_map;   // lattice -> hull key-point index
+    __device__ __forceinline__ void put(int t, int kp, float w) const {
+        const uint32_t bits = (__float_as_uint(w) + 0x40u) >> 7;  // round to 16 mantissa bits
+        a[(int64_t)t * 32] = (uint32_t)__ldg(kp_map + kp) | ((bits >> 16) << 24);
+        b[(int64_t)(t >> 1) * 64 + (t & 1)] = (uint16_t)(bits & 0xFFFFu);
+    }
+};
+
+
 // Walk one pixel's ray exactly as K-render samples it and produce its row of
 // B.  Which entries a row holds depends only on the geometry (a window slot
 // holds an entry once a sample whose support covers it placed a `dynamic`
@@ -126,7 +151,7 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                          const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
                          const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch,
                          int64_t plane, const float* __restrict__ thr, const uint32_t* __restrict__ nm,
-                         float* __restrict__ acc, float* __restrict__ wsm, int stride, int2* __restrict__ out,
+                         float* __restrict__ acc, float* __restrict__ wsm, int stride, RplanOut out,
                          double* base, double& t_fin) {
     constexpr uint32_t kPX[3] = {0x1FFu, 0x1FFu << 9, 0x1FFu << 18};
     constexpr uint32_t kPY[3] = {0x7u | (0x7u << 9) | (0x7u << 18), (0x7u << 3) | (0x7u << 12) | (0x7u << 21),
@@ -139,7 +164,7 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
     bool have = false;
     const float sig_a = (float)rc.sigma_a, kappa = (float)rc.scat_scale;
     auto put = [&](int kp, float wt) {
-        if (FILL) out[(int64_t)count * 32] = make_int2(kp, __float_as_int(wt));
+        if (FILL) out.put(count, kp, wt);
         ++count;
     };
     // key point held by slot s of the window centred on wm
@@ -331,7 +356,7 @@ __global__ void __launch_bounds__(128) rplan_count_kernel(
         double d[3], base[1] = {0.0}, t_fin;
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         cnt = rplan_row<SCAT, false>(cam.center, d, g, rc, occ, dynamic, dyn27, nullptr, 0, 0, s_thr, s_nm, nullptr,
-                                     nullptr, 0, nullptr, base, t_fin);
+                                     nullptr, 0, RplanOut{}, base, t_fin);
     }
     if (row_len) row_len[(int64_t)unit * 32 + lane] = cnt;
     cnt = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
@@ -346,7 +371,8 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
     int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
     const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch, int64_t plane,
     const long long* __restrict__ unit_off, const int* __restrict__ unit_order, const int* __restrict__ row_src,
-    int2* __restrict__ entries, double* __restrict__ base_out, double* __restrict__ t_fin_out) {
+    const int* __restrict__ kp_map, uint32_t* __restrict__ ent_a, uint32_t* __restrict__ ent_b,
+    double* __restrict__ base_out, double* __restrict__ t_fin_out) {
     __shared__ float s_acc[27 * 128], s_w[27 * 128];
     for (int i = threadIdx.x; i < 27 * 128; i += blockDim.x) s_acc[i] = 0.f;
     __shared__ float s_thr[3 * kScatDirs];
@@ -365,8 +391,10 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
         double d[3];
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         rplan_row<SCAT, true>(cam.center, d, g, rc, occ, dynamic, dyn27, values, nch, plane, s_thr, s_nm,
-                              s_acc + threadIdx.x, s_w + threadIdx.x, 128, entries + unit_off[unit] * 32 + lane, base,
-                              t_fin);
+                              s_acc + threadIdx.x, s_w + threadIdx.x, 128,
+                              RplanOut{ent_a + unit_off[unit] * 32 + lane,
+                                        reinterpret_cast<uint16_t*>(ent_b + (unit_off[unit] >> 1) * 32 + lane), kp_map},
+                              base, t_fin);
     }
     for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];
     t_fin_out[r] = t_fin;
@@ -375,11 +403,13 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
 // K-render through the plan: one warp per unit, lane = pixel; rec = B c +
 // base + t_fin bg, then the same residual / squared-residual epilogue as the
 // marching kernel.  Products in fp32, summed in fp64 a batch at a time.
-// 32 entries per lane in flight per batch (config 2: B = 8 / 16 / 24 / 32 / 64:
-// 0.163 / 0.164 / 0.156 / 0.154 / 0.178 ms); ptxas keeps the batch's loads ahead
-// of their uses only with the registers to hold them (3 CTAs/SM, 80 regs).
+// Entries per lane in flight per batch x CTAs per SM (config 2, 6-byte
+// entries): 16x3 / 24x3 / 32x3 / 32x2 / 24x4 / 16x4 / 48x2 / 64x3:
+// 0.1245 / 0.1245 / 0.128 / 0.1248 / 0.128 / 0.1306 / 0.1307 / 0.1295 ms;
+// ptxas keeps a batch's loads ahead of their uses only with the registers to
+// hold them.
 #ifndef FVR_RPLAN_BATCH
-#define FVR_RPLAN_BATCH 32
+#define FVR_RPLAN_BATCH 24
 #endif
 #ifndef FVR_RPLAN_MINB
 #define FVR_RPLAN_MINB 3
@@ -400,48 +430,61 @@ struct RplanFinalize {
 template <int NCH>
 __device__ __forceinline__ void rplan_render_unit(
     int unit, int lane, const int* __restrict__ unit_len, const long long* __restrict__ unit_off,
-    const int2* __restrict__ entries, const double* __restrict__ base, const double* __restrict__ t_fin,
-    const int* __restrict__ row_src, int64_t rows, int units_x, int units_per_view, int n_views, int w, int h, const float* __restrict__ src,
-    const float* __restrict__ values, const float4* __restrict__ cpack, const RenderConsts& rc,
-    float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride) {
-    const int len = unit_len[unit];
-    const int2* e = entries + unit_off[unit] * 32 + lane;
+    const uint32_t* __restrict__ ent_a, const uint32_t* __restrict__ ent_b, const double* __restrict__ base,
+    const double* __restrict__ t_fin, const int* __restrict__ row_src, int64_t rows, int units_x,
+    int units_per_view, int n_views, int w, int h, const float* __restrict__ src, const float* __restrict__ kpv,
+    const RenderConsts& rc, float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride) {
+    // kpv: max(v, 0) per hull key point (NCH = 1: f32; NCH = 3: float4)
+    const int len = unit_len[unit];  // even
+    const long long off = unit_off[unit];  // even
+    const uint32_t* ea = ent_a + off * 32 + lane;
+    const uint32_t* eb = ent_b + (off >> 1) * 32 + lane;
     double acc[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
+    auto term = [&](uint32_t av, uint32_t half16, float* part) {
+        const float wgt = rplan_weight(av, half16);
+        const uint32_t k = av & kRplanIdxMask;
+        if (NCH == 1) {
+            part[0] = fmaf(wgt, __ldg(kpv + k), part[0]);
+        } else {
+            const float4 cv = __ldg(reinterpret_cast<const float4*>(kpv) + k);
+            const float cc[3] = {cv.x, cv.y, cv.z};
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) part[c] = fmaf(wgt, cc[c], part[c]);
+        }
+    };
     int t = 0;
     constexpr int B = FVR_RPLAN_BATCH;
     for (; t + B <= len; t += B) {
-        int2 en[B];
+        uint32_t av[B], bv[B / 2];
 #pragma unroll
-        for (int i = 0; i < B; ++i) en[i] = __ldcs(e + (int64_t)(t + i) * 32);
+        for (int i = 0; i < B; ++i) av[i] = __ldcs(ea + (int64_t)(t + i) * 32);
+#pragma unroll
+        for (int i = 0; i < B / 2; ++i) bv[i] = __ldcs(eb + (int64_t)(t / 2 + i) * 32);
         float part[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) part[c] = 0.f;
 #pragma unroll
-        for (int i = 0; i < B; ++i) {
-            if (NCH == 1) {
-                part[0] = fmaf(__int_as_float(en[i].y), fmaxf(__ldg(values + en[i].x), 0.f), part[0]);
-            } else {
-                const float4 cv = __ldg(cpack + en[i].x);  // max(v, 0) of the three channels
-                const float cc[3] = {cv.x, cv.y, cv.z};
-#pragma unroll
-                for (int c = 0; c < NCH; ++c) part[c] = fmaf(__int_as_float(en[i].y), cc[c], part[c]);
-            }
-        }
+        for (int i = 0; i < B; ++i) term(av[i], (i & 1) ? (bv[i >> 1] >> 16) : (bv[i >> 1] & 0xFFFFu), part);
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] += (double)part[c];
     }
-    for (; t < len; ++t) {
-        const int2 en = __ldcs(e + (int64_t)t * 32);
-        if (NCH == 1) {
-            acc[0] += (double)(__int_as_float(en.y) * fmaxf(__ldg(values + en.x), 0.f));
-        } else {
-            const float4 cv = __ldg(cpack + en.x);
-            const float cc[3] = {cv.x, cv.y, cv.z};
+    for (; t < len; t += 2) {
+        const uint32_t a0 = __ldcs(ea + (int64_t)t * 32), a1 = __ldcs(ea + (int64_t)(t + 1) * 32);
+        const uint32_t bb = __ldcs(eb + (int64_t)(t / 2) * 32);
+        float part[NCH];
 #pragma unroll
-            for (int c = 0; c < NCH; ++c) acc[c] += (double)(__int_as_float(en.y) * cc[c]);
+        for (int c = 0; c < NCH; ++c) part[c] = 0.f;
+        term(a0, bb & 0xFFFFu, part);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            acc[c] += (double)part[c];
+            part[c] = 0.f;
         }
+        term(a1, bb >> 16, part);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) acc[c] += (double)part[c];
     }
     const int64_t r = (int64_t)unit * 32 + lane;
     int view, col, row;
@@ -470,11 +513,11 @@ __device__ __forceinline__ void rplan_render_unit(
 
 template <int NCH>
 __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
-    const int* __restrict__ unit_len, const long long* __restrict__ unit_off, const int2* __restrict__ entries,
-    const double* __restrict__ base, const double* __restrict__ t_fin, const int* __restrict__ unit_order,
-    const int* __restrict__ row_src, int n_units, int units_x, int units_per_view, int n_views, int w, int h, const float* __restrict__ src,
-    const float* __restrict__ values, const float4* __restrict__ cpack, int64_t plane, RenderConsts rc,
-    float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride,
+    const int* __restrict__ unit_len, const long long* __restrict__ unit_off, const uint32_t* __restrict__ ent_a,
+    const uint32_t* __restrict__ ent_b, const double* __restrict__ base, const double* __restrict__ t_fin,
+    const int* __restrict__ unit_order, const int* __restrict__ row_src, int n_units, int units_x,
+    int units_per_view, int n_views, int w, int h, const float* __restrict__ src, const float* __restrict__ kpv,
+    RenderConsts rc, float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride,
     fvr_loop_state_t* __restrict__ state, RplanFinalize fin) {
     if (all_done<NCH>(state)) return;
     const int lane = threadIdx.x & 31;
@@ -484,9 +527,9 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
     // for the tail (config 2: 0.157 -> 0.139 ms)
     for (int unit = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); unit < n_units;
          unit += (int)(((int64_t)gridDim.x * blockDim.x) >> 5))
-        rplan_render_unit<NCH>(unit_order ? __ldg(unit_order + unit) : unit, lane, unit_len, unit_off, entries, base,
-                               t_fin, row_src, rows, units_x, units_per_view, n_views, w, h, src, values, cpack, rc, residual,
-                               sq_partials, sq_stride);
+        rplan_render_unit<NCH>(unit_order ? __ldg(unit_order + unit) : unit, lane, unit_len, unit_off, ent_a, ent_b,
+                               base, t_fin, row_src, rows, units_x, units_per_view, n_views, w, h, src, kpv, rc,
+                               residual, sq_partials, sq_stride);
     if (!fin.on) return;
     // the last block to finish runs the loop's finalize (fvr_loop.cu)
     __shared__ int s_last;
@@ -509,13 +552,19 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
 
 // cpack[kp] = (max(v_0, 0), max(v_1, 0), max(v_2, 0), 0) at the listed key
 // points: the three-channel render plan reads one 16-byte record per entry
-__global__ void rplan_cpack_kernel(const float* __restrict__ values, int64_t plane, const int32_t* __restrict__ kp,
-                                   int64_t n_kp, float4* __restrict__ cpack, const fvr_loop_state_t* __restrict__ state) {
-    if (all_done<3>(state)) return;
+// kpv[i] = max(v, 0) at hull key point kp[i] of every channel (NCH = 1: f32,
+// NCH = 3: float4): the render plan's operand, kept current by the gather.
+template <int NCH>
+__global__ void rplan_pack_kernel(const float* __restrict__ values, int64_t plane, const int32_t* __restrict__ kp,
+                                  int64_t n_kp, float* __restrict__ kpv, const fvr_loop_state_t* __restrict__ state) {
+    if (state && all_done<NCH>(state)) return;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_kp; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = kp[i];
-        cpack[k] = make_float4(fmaxf(values[k], 0.f), fmaxf(values[plane + k], 0.f), fmaxf(values[2 * plane + k], 0.f),
-                               0.f);
+        if (NCH == 1)
+            kpv[i] = fmaxf(values[k], 0.f);
+        else
+            reinterpret_cast<float4*>(kpv)[i] = make_float4(fmaxf(values[k], 0.f), fmaxf(values[plane + k], 0.f),
+                                                            fmaxf(values[2 * plane + k], 0.f), 0.f);
     }
 }
 

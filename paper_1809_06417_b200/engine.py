@@ -343,6 +343,14 @@ class ChannelLoop:
         unit_len = row_len[row_src.long()].view(n_units, 32).amax(1).to(t.int32).contiguous()
         return row_src, unit_len
 
+    def _kp_map(self):
+        """Lattice index -> index in the key-point list (-1 elsewhere)."""
+        if getattr(self, "_kpmap", None) is None:
+            t = self.t
+            self._kpmap = t.full((int(np.prod(self.shape)),), -1, dtype=t.int32, device=self.dev)
+            self._kpmap[self.kp[: self.n_kp].long()] = t.arange(self.n_kp, dtype=t.int32, device=self.dev)
+        return self._kpmap
+
     def _rplan_geo(self):
         return (self.cams.data_ptr(), self.v_end - self.v_begin, self.bbox.u0, self.bbox.v0, self.w_bb, self.h_bb,
                 self.grid, self.params, _lib.ptr(self.occ), self.kp_dev.data_ptr())
@@ -368,6 +376,7 @@ class ChannelLoop:
         if row_len is not None:
             tx, ty = (int(x) for x in os.environ.get("FVR_RPLAN_TILE", "2x4").split("x"))
             row_src, unit_len = self._rplan_row_order(row_len, n_units, tx, ty)
+        unit_len = (unit_len + 1) & ~1  # even: entries_b holds pairs
         off = t.zeros(n_units + 1, dtype=t.int64, device=self.dev)
         off[1:] = t.cumsum(unit_len.long(), 0)
         return dict(unit_len=unit_len, row_src=row_src, off=off, sizes=[off[-1]])
@@ -383,22 +392,28 @@ class ChannelLoop:
         geo = self._rplan_geo()
         self.rp_row_src = rs["row_src"]
         slots = int(sizes[0]) * 32
-        need = 8 * slots + 8 * (self.nch + 1) * n_units * 32
-        if need > self.PLAN_MAX_BYTES:
+        need = 6 * slots + 8 * (self.nch + 1) * n_units * 32
+        if need > self.PLAN_MAX_BYTES or self.n_kp >= (1 << 24):
             return False
         try:  # (no cudaMemGetInfo probe: it synchronises and costs tens of ms)
-            entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
+            ent_a = t.zeros(max(slots, 2), dtype=t.int32, device=dev)
+            ent_b = t.zeros(max(slots // 2, 1), dtype=t.int32, device=dev)
             base = t.zeros((self.nch, n_units * 32), dtype=t.float64, device=dev)
             t_fin = t.zeros(n_units * 32, dtype=t.float64, device=dev)
+            # the operand: max(v, 0) per hull key point (float4 for 3 channels)
+            kpv = t.empty((max(self.n_kp, 1),) + ((4,) if self.nch == 3 else ()), dtype=t.float32, device=dev)
         except t.cuda.OutOfMemoryError:
             return False
         # fill and render visit the units longest first (a short tail)
         self.rp_order = t.argsort(unit_len, descending=True).to(t.int32) \
             if os.environ.get("FVR_RPLAN_SORT", "1") == "1" else None
         _lib.call("fvr_rplan_fill", *geo, self.values.data_ptr(), self.nch, off.data_ptr(), _lib.ptr(self.rp_order),
-                  _lib.ptr(self.rp_row_src), entries.data_ptr(), base.data_ptr(), t_fin.data_ptr(), stream)
-        self.rp_len, self.rp_off, self.rp_entries, self.rp_base, self.rp_tfin = unit_len, off, entries, base, t_fin
-        self.rp_cpack = t.zeros(self.shape + (4,), dtype=t.float32, device=dev) if self.nch == 3 else None
+                  _lib.ptr(self.rp_row_src), self._kp_map().data_ptr(), ent_a.data_ptr(), ent_b.data_ptr(),
+                  base.data_ptr(), t_fin.data_ptr(), stream)
+        _lib.call("fvr_rplan_pack", self.values.data_ptr(), self.nch, self.grid, self.kp.data_ptr(), self.n_kp,
+                  kpv.data_ptr(), None, stream)
+        self.rp_len, self.rp_off, self.rp_base, self.rp_tfin = unit_len, off, base, t_fin
+        self.rp_a, self.rp_b, self.rp_kpv = ent_a, ent_b, kpv
         self.rplan_nnz = slots
         return True
 
@@ -406,17 +421,20 @@ class ChannelLoop:
         if self.v_end <= self.v_begin:
             return 0
         if self.rplan:
+            n = 1
+            if not self.plan:  # the scatter fallback's update does not maintain the operand
+                _lib.call("fvr_rplan_pack", self.values.data_ptr(), self.nch, self.grid, self.kp.data_ptr(),
+                          self.n_kp, self.rp_kpv.data_ptr(), self.state.data_ptr(), stream)
+                n += 1
             _lib.call(
-                "fvr_rplan_render", self.rp_len.data_ptr(), self.rp_off.data_ptr(), self.rp_entries.data_ptr(),
-                self.rp_base.data_ptr(), self.rp_tfin.data_ptr(), _lib.ptr(self.rp_order), _lib.ptr(self.rp_row_src),
-                self.v_end - self.v_begin,
-                self.w_bb, self.h_bb,
-                self.src.data_ptr(), self.values.data_ptr(), self.grid, self.nch, self.background,
-                self.kp.data_ptr(), self.n_kp, _lib.ptr(self.rp_cpack),
-                self.residual.data_ptr(), self.sq[0, self.v_begin * self.bpv:].data_ptr(), self.n_sq,
-                self.state.data_ptr(), self._fused_finalize(), stream,
+                "fvr_rplan_render", self.rp_len.data_ptr(), self.rp_off.data_ptr(), self.rp_a.data_ptr(),
+                self.rp_b.data_ptr(), self.rp_base.data_ptr(), self.rp_tfin.data_ptr(), _lib.ptr(self.rp_order),
+                _lib.ptr(self.rp_row_src), self.v_end - self.v_begin, self.w_bb, self.h_bb, self.src.data_ptr(),
+                self.rp_kpv.data_ptr(), self.nch, self.background, self.residual.data_ptr(),
+                self.sq[0, self.v_begin * self.bpv:].data_ptr(), self.n_sq, self.state.data_ptr(),
+                self._fused_finalize(), stream,
             )
-            return 1
+            return n
         _lib.call(
             "fvr_loop_render", self.cams.data_ptr(), self.v_end - self.v_begin, self.bbox.u0,
             self.bbox.v0, self.w_bb, self.h_bb, self.src.data_ptr(), self.values.data_ptr(),
@@ -521,9 +539,7 @@ class ChannelLoop:
         t = self.t
         dev = self.dev
         stream = _lib.stream_ptr()
-        n_lat = int(np.prod(self.shape))
-        kp_map = t.full((n_lat,), -1, dtype=t.int32, device=dev)
-        kp_map[self.kp[: self.n_kp].long()] = t.arange(self.n_kp, dtype=t.int32, device=dev)
+        kp_map = self._kp_map()
         counts = t.zeros(self.n_kp, dtype=t.int32, device=dev)
         geo = (self.cams.data_ptr(), self.rays.data_ptr(), self.n_rays, self.bbox.u0, self.bbox.v0, self.w_bb,
                self.h_bb, self.inside.data_ptr(), self.grid)
@@ -623,7 +639,8 @@ class ChannelLoop:
         _lib.call("fvr_loop_gather", self.plan_slice_len.data_ptr(), self.plan_slice_off.data_ptr(),
                   self.plan_row_of_pos.data_ptr(), self.plan_entries.data_ptr(), self.n_kp,
                   src.data_ptr(), self.nch, self.kp.data_ptr(), self.values.data_ptr(),
-                  _lib.ptr(self.layout), self.layout_kind, self.grid, self.packed.data_ptr() if packed else None,
+                  _lib.ptr(self.layout), self.layout_kind, self.grid,
+                  _lib.ptr(self.rp_kpv) if self.rplan else None, self.packed.data_ptr() if packed else None,
                   self.state.data_ptr(), stream)
         return 1
 
@@ -631,9 +648,10 @@ class ChannelLoop:
         if self.n_kp == 0:
             return 0
         for ch in range(self.nch):
+            kpv = self.rp_kpv.data_ptr() + 4 * ch if self.rplan else None
             _lib.call("fvr_loop_update_packed", self.packed[ch].data_ptr(), self.n_kp, self.kp.data_ptr(),
                       self.values[ch].data_ptr(), self._layout_channel(ch), self.layout_kind, self.nch, self.grid,
-                      self.state[ch].data_ptr(), stream)
+                      kpv, 1 if self.nch == 1 else 4, self.state[ch].data_ptr(), stream)
         return self.nch
 
     def _allreduce_packed(self, stream):

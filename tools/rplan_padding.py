@@ -15,9 +15,9 @@ grid0 = _init_grid(sc["geom"], sc["hull"], "green")
 src = [im.data[sc["bbox"].slices][:, :, 0] for im in sc["images"]]
 loop = ChannelLoop(sc["cams"], grid0, grid0.values, src, sc["masks"], sc["bbox"], sc["hull"].inside_voxels(),
                    sc["hull"].key_point_mask(), sc["rcfg"], _loop_config(cfg, grid0), 10, use_graph=False)
-e = loop.rp_entries.view(-1, 2)
-nz = (e[:, 1] != 0)
-slots = e.shape[0]
+a = loop.rp_a
+nz = (a != 0)  # exponent bits in the top byte: zero only for a zero weight (index 0)
+slots = a.shape[0]
 print("slots", slots, "nonzero", int(nz.sum()), "fill", float(nz.sum()) / slots)
 n_units = loop.rp_len.numel()
 rowlen = t.zeros(n_units * 32, dtype=t.int64, device=e.device)
