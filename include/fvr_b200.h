@@ -298,7 +298,8 @@ int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int6
                          int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
                          const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
                          double alpha_d, const int32_t* kp_map, const int32_t* row_pos,
-                         const int64_t* slice_off, int64_t* cursor, int32_t* entries, void* stream);
+                         const int64_t* slice_off, int64_t* cursor, uint32_t* entries_a, uint32_t* entries_b,
+                         void* stream);
 /* Stochastic mode (random G, reconstruct.py:193-201): the sample plan.
  * Count: per-row entry counts (8 per in-hull sample) and per-ray in-hull
  * sample counts.  Fill (ray_sid0 = exclusive scan of ray_samples): entries
@@ -327,6 +328,12 @@ int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, co
  * positions with slice_len (longest row) and slice_off (exclusive scan, in
  * units of 32 entries); entry t of position p at slice_off[p/32]*32 + 32t +
  * p%32; cursor (n_rows i64, zeroed) counts the entries written per row.
+ * The deterministic plan (fvr_adjust_plan_fill) has 6-byte entries: a word
+ * (u32, at that index) = residual index (< 2^24) | weight exponent << 24, and
+ * the weight's top 16 mantissa bits in half t % 2 of entries_b[(slice_off +
+ * t) / 2 * 32 + p % 32] (slice_off and slice_len even); fvr_loop_gather reads
+ * them when entries_b is given, int2 (index, f32 weight) entries otherwise
+ * (the stochastic sample plan).
  * Per iteration: row sums in 32.32 fixed point; with packed == NULL the
  * clamped update is applied in place (and the packed layout refreshed),
  * otherwise the sums go to packed (n_channels, n_kp) for the multi-GPU
@@ -336,7 +343,7 @@ int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, co
  * (converged channels are skipped).  kp_values (may be NULL): the render
  * plan's operand (fvr_rplan_pack), updated with every written value. */
 int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_off, const int32_t* row_of_pos,
-                    const int32_t* entries, int64_t n_kp, const float* residual, int32_t n_channels,
+                    const int32_t* entries, const uint32_t* entries_b, int64_t n_kp, const float* residual, int32_t n_channels,
                     const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
                     fvr_grid_t grid, float* kp_values, int64_t* packed, const fvr_loop_state_t* state,
                     void* stream);

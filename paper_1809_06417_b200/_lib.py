@@ -142,7 +142,7 @@ _SIGNATURES = {
         c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, _P, _P, _P]),
     "fvr_adjust_plan_fill": (
         c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, c_double, c_double, c_double,
-                _P, _P, _P, _P, _P, _P]),
+                _P, _P, _P, _P, _P, _P, _P]),
     "fvr_rplan_count": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _GRID, _PARAMS, _P, _P, _P, _P,
                                 _P]),
     "fvr_rplan_fill": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _GRID, _PARAMS, _P, _P, _P, c_int32,
@@ -156,7 +156,7 @@ _SIGNATURES = {
                                      c_double, c_double, _P, _P, _P, _P, _P, _P, _P, _P]),
     "fvr_loop_weighted_residual": (c_int, [_P, c_int64, _P, c_int32, c_int32, _P, c_int32, c_uint64, c_double,
                                            c_int64, _P, _P, c_int32, _P]),
-    "fvr_loop_gather": (c_int, [_P, _P, _P, _P, c_int64, _P, c_int32, _P, _P, _P, c_int32, _GRID, _P, _P, _P, _P]),
+    "fvr_loop_gather": (c_int, [_P, _P, _P, _P, _P, c_int64, _P, c_int32, _P, _P, _P, c_int32, _GRID, _P, _P, _P, _P]),
     "fvr_loop_update_packed": (c_int, [_P, c_int64, _P, _P, _P, c_int32, c_int32, _GRID, _P, c_int32, _P, _P]),
     "fvr_pack_correction": (c_int, [_P, _P, c_int64, _P, _P]),
     "fvr_unpack_correction": (c_int, [_P, _P, c_int64, _P, _P]),

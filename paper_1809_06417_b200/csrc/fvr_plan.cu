@@ -171,18 +171,29 @@ struct SellMap {
         const unsigned long long t = atomicAdd(cursor + row, 1ull);
         return slice_off[p >> 5] * 32 + (long long)t * 32 + (p & 31);
     }
+    // 6-byte entries (even slice offsets): a at the int2 slot's index, the
+    // 16-bit weight word in half t % 2 of u32 pair ((off + t) / 2) * 32 + lane
+    __device__ __forceinline__ void put6(int row, uint32_t idx, float w, uint32_t* a, uint16_t* b) const {
+        const int p = row_pos[row];
+        const long long t = (long long)atomicAdd(cursor + row, 1ull);
+        const long long off = slice_off[p >> 5];
+        const uint32_t bits = (__float_as_uint(w) + 0x40u) >> 7;  // round to 16 mantissa bits (w >= 0)
+        a[(off + t) * 32 + (p & 31)] = idx | ((bits >> 16) << 24);
+        b[((off + t) >> 1) * 64 + (p & 31) * 2 + (t & 1)] = (uint16_t)(bits & 0xFFFFu);
+    }
 };
 
 __global__ void __launch_bounds__(128) plan_fill_kernel(
     const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
     int u0, int v0, int w, int h, const uint8_t* __restrict__ inside, Geom g, double tau_keep,
-    double alpha_l, float alpha_d, const int32_t* __restrict__ kp_map, SellMap sm, int2* __restrict__ entries) {
+    double alpha_l, float alpha_d, const int32_t* __restrict__ kp_map, SellMap sm, uint32_t* __restrict__ ent_a,
+    uint16_t* __restrict__ ent_b) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_rays) return;
     PlanRay pr;
     plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
     ray_entries<true>(pr, g, inside, tau_keep, alpha_l, alpha_d, [&](int kp, float wgt) {
-        entries[sm.slot(kp_map[kp])] = make_int2(pr.res_index, __float_as_int(wgt));
+        sm.put6(kp_map[kp], (uint32_t)pr.res_index, wgt, ent_a, ent_b);
     });
 }
 
@@ -290,10 +301,17 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
 #ifndef FVR_GATHER_BATCH
 #define FVR_GATHER_BATCH 32
 #endif
-template <bool PACKED, int NCH>
-__global__ void __launch_bounds__(256, 3) gather_kernel(
+// CTAs per SM: 6-byte entries leave room for 4 (config 2, deterministic,
+// batch x CTAs 32x3 / 32x4 / 32x5 / 24x5 / 16x4 / 64x2: 0.0763 / 0.0718 /
+// 0.0718 / 0.0714 / 0.0766 / 0.0845 ms); the int2 sample plan keeps 3.
+#ifndef FVR_GATHER_MINB
+#define FVR_GATHER_MINB(E6) ((E6) ? 4 : 3)
+#endif
+template <bool PACKED, int NCH, bool E6>
+__global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
     const int32_t* __restrict__ slice_len, const long long* __restrict__ slice_off,
-    const int32_t* __restrict__ row_of_pos, const int2* __restrict__ entries, int64_t n_rows,
+    const int32_t* __restrict__ row_of_pos, const int2* __restrict__ entries, const uint32_t* __restrict__ ent_b,
+    int64_t n_rows,
     const float* __restrict__ residual, const int32_t* __restrict__ kp_index,
     float* __restrict__ values, int64_t plane, float* __restrict__ layout, int layout_kind, int sy, int ny1,
     float* __restrict__ kpv, long long* __restrict__ packed, const fvr_loop_state_t* __restrict__ state) {
@@ -311,14 +329,32 @@ __global__ void __launch_bounds__(256, 3) gather_kernel(
     for (int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < n_slices;
          sl += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int len = slice_len[sl];
-        const int2* e = entries + slice_off[sl] * 32 + lane;
+        const long long off = slice_off[sl];
+        const int2* e = entries + off * 32 + lane;
+        // E6: 6-byte entries (fvr_adjust_plan_fill): a words in `entries`
+        // reinterpreted as u32, 16-bit weight words in ent_b pairs
+        const uint32_t* ea = reinterpret_cast<const uint32_t*>(entries) + off * 32 + lane;
+        const uint32_t* eb = ent_b + (off >> 1) * 32 + lane;
         long long acc[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = 0;
         for (int t = 0; t < len; t += B) {
             int2 en[B];
+            if (E6) {
+                uint32_t av[B], bv[B / 2];
 #pragma unroll
-            for (int i = 0; i < B; ++i) en[i] = t + i < len ? __ldcs(e + (int64_t)(t + i) * 32) : make_int2(0, 0);
+                for (int i = 0; i < B; ++i) av[i] = t + i < len ? __ldcs(ea + (int64_t)(t + i) * 32) : 0u;
+#pragma unroll
+                for (int i = 0; i < B / 2; ++i) bv[i] = t + 2 * i < len ? __ldcs(eb + (int64_t)(t / 2 + i) * 32) : 0u;
+#pragma unroll
+                for (int i = 0; i < B; ++i) {
+                    const uint32_t half = (i & 1) ? (bv[i >> 1] >> 16) : (bv[i >> 1] & 0xFFFFu);
+                    en[i] = make_int2((int)(av[i] & 0xFFFFFFu), (int)(((av[i] >> 24) << 23) | (half << 7)));
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < B; ++i) en[i] = t + i < len ? __ldcs(e + (int64_t)(t + i) * 32) : make_int2(0, 0);
+            }
 #pragma unroll
             for (int i = 0; i < B; ++i) {
                 const float wgt = __int_as_float(en[i].y);
@@ -395,7 +431,7 @@ extern "C" int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray
                                     const uint8_t* inside_vox, fvr_grid_t grid, double tau,
                                     double alpha_l, double alpha_d, const int32_t* kp_map,
                                     const int32_t* row_pos, const int64_t* slice_off, int64_t* cursor,
-                                    int32_t* entries, void* stream) {
+                                    uint32_t* entries_a, uint32_t* entries_b, void* stream) {
     FVR_TRY_BEGIN
     if (int rc = check_grid(grid)) return rc;
     if (n_rays == 0) return FVR_OK;
@@ -404,13 +440,13 @@ extern "C" int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray
         cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d,
         kp_map,
         SellMap{row_pos, reinterpret_cast<const long long*>(slice_off), reinterpret_cast<unsigned long long*>(cursor)},
-        reinterpret_cast<int2*>(entries));
+        entries_a, reinterpret_cast<uint16_t*>(entries_b));
     return check_launch("adjust_plan_fill");
     FVR_TRY_END
 }
 
 extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_off, const int32_t* row_of_pos,
-                               const int32_t* entries, int64_t n_kp, const float* residual, int32_t n_channels,
+                               const int32_t* entries, const uint32_t* entries_b, int64_t n_kp, const float* residual, int32_t n_channels,
                                const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
                                fvr_grid_t grid, float* kp_values, int64_t* packed, const fvr_loop_state_t* state,
                                void* stream) {
@@ -426,15 +462,19 @@ extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_of
     const auto* so = reinterpret_cast<const long long*>(slice_off);
     const auto* en = reinterpret_cast<const int2*>(entries);
     long long* pk = reinterpret_cast<long long*>(packed);
-#define FVR_GATHER(P, C)                                                                                           \
-    gather_kernel<P, C><<<(unsigned)blocks, 256, 0, st>>>(slice_len, so, row_of_pos, en, n_kp, residual, kp_index, \
-                                                          values, plane, layout, layout_kind, sy, ny1, kp_values, pk, \
-                                                          state)
+#define FVR_GATHER(P, C, E)                                                                                  \
+    gather_kernel<P, C, E><<<(unsigned)blocks, 256, 0, st>>>(slice_len, so, row_of_pos, en, entries_b, n_kp,   \
+                                                             residual, kp_index, values, plane, layout,           \
+                                                             layout_kind, sy, ny1, kp_values, pk, state)
+#define FVR_GATHER_E(P, C)           \
+    if (entries_b) FVR_GATHER(P, C, true); \
+    else FVR_GATHER(P, C, false)
     if (packed) {
-        if (n_channels == 1) FVR_GATHER(true, 1); else FVR_GATHER(true, 3);
+        if (n_channels == 1) { FVR_GATHER_E(true, 1); } else { FVR_GATHER_E(true, 3); }
     } else {
-        if (n_channels == 1) FVR_GATHER(false, 1); else FVR_GATHER(false, 3);
+        if (n_channels == 1) { FVR_GATHER_E(false, 1); } else { FVR_GATHER_E(false, 3); }
     }
+#undef FVR_GATHER_E
 #undef FVR_GATHER
     return check_launch("loop_gather");
     FVR_TRY_END

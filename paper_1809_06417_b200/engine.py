@@ -571,6 +571,8 @@ class ChannelLoop:
         slice_len = t.zeros(n_slices * 32, dtype=t.int32, device=dev)
         slice_len[: self.n_kp] = counts[order]
         slice_len = slice_len.view(n_slices, 32).amax(1).contiguous()
+        if not self.sample_plan:
+            slice_len = (slice_len + 1) & ~1  # 6-byte entries: weight words in pairs
         slice_off = t.zeros(n_slices + 1, dtype=t.int64, device=dev)
         slice_off[1:] = t.cumsum(slice_len.long(), 0)
         sizes = [slice_off[-1], counts.long().sum()]
@@ -589,12 +591,19 @@ class ChannelLoop:
         slots = int(sizes[0]) * 32
         nnz = int(sizes[1])
         n_samples = int(sizes[2]) if self.sample_plan else 0
-        need = 8 * slots + 12 * n_samples
+        need = (8 if self.sample_plan else 6) * slots + 12 * n_samples
         if need > self.PLAN_MAX_BYTES or n_samples >= 2 ** 31:
             return False
+        if not self.sample_plan and (self.v_end - self.v_begin) * self.w_bb * self.h_bb >= 1 << 24:
+            return False  # residual indices are 24-bit in the 6-byte entries
         try:
             cursor = t.zeros(self.n_kp, dtype=t.int64, device=dev)
-            entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
+            if self.sample_plan:  # int2 (sample id, W)
+                entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
+                entries_b = None
+            else:  # 6 bytes: residual index (24 bits) + 24-bit weight
+                entries = t.zeros(max(slots, 2), dtype=t.int32, device=dev)
+                entries_b = t.zeros(max(slots // 2, 1), dtype=t.int32, device=dev)
         except t.cuda.OutOfMemoryError:
             return False
         sell = (pc["row_pos"].data_ptr(), pc["slice_off"].data_ptr(), cursor.data_ptr(), entries.data_ptr())
@@ -614,11 +623,12 @@ class ChannelLoop:
         else:
             side.wait_stream(t.cuda.current_stream())
             _lib.call("fvr_adjust_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff, pc["kp_map"].data_ptr(),
-                      *sell, stream)
+                      *sell, entries_b.data_ptr(), stream)
         self.plan_slice_len = pc["slice_len"]
         self.plan_slice_off = pc["slice_off"]
         self.plan_row_of_pos = pc["row_of_pos"]
         self.plan_entries = entries
+        self.plan_entries_b = entries_b
         self.plan_nnz = nnz
         self.plan_slots = slots
         return True
@@ -637,7 +647,8 @@ class ChannelLoop:
             return 0
         src = self.rho if self.sample_plan else self.residual
         _lib.call("fvr_loop_gather", self.plan_slice_len.data_ptr(), self.plan_slice_off.data_ptr(),
-                  self.plan_row_of_pos.data_ptr(), self.plan_entries.data_ptr(), self.n_kp,
+                  self.plan_row_of_pos.data_ptr(), self.plan_entries.data_ptr(), _lib.ptr(self.plan_entries_b),
+                  self.n_kp,
                   src.data_ptr(), self.nch, self.kp.data_ptr(), self.values.data_ptr(),
                   _lib.ptr(self.layout), self.layout_kind, self.grid,
                   _lib.ptr(self.rp_kpv) if self.rplan else None, self.packed.data_ptr() if packed else None,
