@@ -118,6 +118,21 @@ __device__ __forceinline__ float rplan_weight(uint32_t a, uint32_t half16) {
     return __uint_as_float(((a >> 24) << 23) | (half16 << 7));
 }
 
+// Move the bits of a 3x3x3 stencil mask (bit jx*9 + jy*3 + jz) to the window
+// slots ((r0 + jx) % 3) * 9 + ((r1 + jy) % 3) * 3 + (r2 + jz) % 3: a cyclic
+// shift along each axis.
+__device__ __forceinline__ uint32_t rotate_axis(uint32_t m, int r, uint32_t a0, int sh) {
+    const uint32_t a1 = a0 << sh, a2 = a0 << (2 * sh);
+    if (r == 1) return ((m & (a0 | a1)) << sh) | ((m & a2) >> (2 * sh));
+    if (r == 2) return ((m & a0) << (2 * sh)) | ((m & (a1 | a2)) >> sh);
+    return m;
+}
+__device__ __forceinline__ uint32_t rotate27(uint32_t m, int r0, int r1, int r2) {
+    m = rotate_axis(m, r2, 0x1249249u, 1);                              // jz
+    m = rotate_axis(m, r1, 0x7u | (0x7u << 9) | (0x7u << 18), 3);       // jy
+    return rotate_axis(m, r0, 0x1FFu, 9);                               // jx
+}
+
 struct RplanOut {
     uint32_t* a;         // this row's first a word
     uint16_t* b;         // this row's first 16-bit word
@@ -175,6 +190,11 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
         return x[0] * g.sx + x[1] * g.sy + x[2];
     };
     auto retire = [&](uint32_t slots) {
+        if (!FILL) {  // count pass: one entry per retired slot
+            count += __popc(slots);
+            live &= ~slots;
+            return;
+        }
 #pragma unroll 1
         for (uint32_t b = slots; b; b &= b - 1) {
             const int sl = __ffs(b) - 1;
@@ -259,6 +279,8 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
             wm[1] = m[1];
             wm[2] = m[2];
             have = true;
+            // toroidal slot of offset (jx, jy, jz): ((m + j - 1) mod 3) per axis
+            const int r0 = (m[0] + 2) % 3, r1 = (m[1] + 2) % 3, r2 = (m[2] + 2) % 3;
             if (FILL) {
                 float w[27];
                 if (SCAT) {
@@ -277,16 +299,17 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
 #pragma unroll
                 for (int j = 0; j < 27; ++j) wsm[j * stride] = w[j] * scale;
             }
-            // toroidal slot of offset (jx, jy, jz): ((m + j - 1) mod 3) per axis
-            const int r0 = (m[0] + 2) % 3, r1 = (m[1] + 2) % 3, r2 = (m[2] + 2) % 3;
-#pragma unroll 1
-            for (uint32_t b = sup & dyn; b; b &= b - 1) {
-                const int j = __ffs(b) - 1, jx = j / 9, jy = (j / 3) % 3, jz = j % 3;
-                const int sl = ((r0 + jx) % 3) * 9 + ((r1 + jy) % 3) * 3 + (r2 + jz) % 3;
-                live |= 1u << sl;
-                if (FILL) acc[sl * stride] += wsm[j * stride];
-            }
+            // the stencil's dynamic key points, moved to window slots at once
+            // (count pass: that is all; config 2: 0.83 -> 0.36 ms)
+            live |= rotate27(sup & dyn, r0, r1, r2);
             if (FILL) {
+                // (weights stay in stencil order: storing them at their slots
+                // costs more address arithmetic than the per-bit slot saves)
+#pragma unroll 1
+                for (uint32_t b = sup & dyn; b; b &= b - 1) {
+                    const int j = __ffs(b) - 1, jx = j / 9, jy = (j / 3) % 3, jz = j % 3;
+                    acc[(((r0 + jx) % 3) * 9 + ((r1 + jy) % 3) * 3 + (r2 + jz) % 3) * stride] += wsm[j * stride];
+                }
 #pragma unroll 1
                 for (uint32_t b = sup & ~dyn; b; b &= b - 1) {
                     const int j = __ffs(b) - 1;
