@@ -255,3 +255,42 @@ def test_render_plan_matches_marching_render(cuda_device, monkeypatch, fixture, 
     for c, tag in enumerate(("red", "green", "blue")):
         np.testing.assert_allclose(b.traces[tag].rmse, a.traces[tag].rmse, rtol=1e-6)
         assert rel_err(b.grids[c].values, a.grids[c].values) <= 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("stochastic", [False, True])
+def test_render_plan_layouts_and_fused_finalize(cuda_device, monkeypatch, stochastic):
+    """The render plan's row order (length-sorted 16x16 tiles or natural),
+    unit order (longest first or natural) and the finalize fused into its last
+    CTA change only the order of float sums (and, for the fused finalize,
+    nothing at all: same trace and grid bits, and the same Philox key for the
+    stochastic weights)."""
+    g = load_golden("config1.npz")
+    cams = cameras_from(g, Camera)
+    n = int(g["n"])
+    hull = HullTags(g["hull_tags"], len(cams))
+    images = [Image(im.shape[1], im.shape[0], 1, im[:, :, 1:2]) for im in g["blanked"]]
+    masks = [FlameMask(m.shape[1], m.shape[0], m) for m in g["masks"]]
+    bbox = Rect(*(int(x) for x in g["bbox"]))
+    geom = VoxelGrid(n, n, n, g["origin"], float(g["edge"]))
+    rcfg = RenderConfig(tau=float(g["tau"]), scattering_enabled=True, sigma_s=float(g["sigma_s"]))
+    cfg = ReconstructionConfig(alpha_l=0.006, tau=float(g["tau"]), max_iters=6, converge_eps=1e-12,
+                               deterministic_mode=not stochastic, g_sigma=0.1, rng_seed=5)
+    monkeypatch.setenv("FVR_RENDER", "plan")
+
+    def run(**env):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        out = reconstruct_channel(images, cams, geom, hull, cfg, render_cfg=rcfg, masks=masks, bbox=bbox)
+        for k in env:
+            monkeypatch.delenv(k)
+        return out
+
+    a, ta = run()
+    b, tb = run(FVR_FUSED_FINALIZE="0")
+    assert ta.rmse == tb.rmse and ta.iterations == tb.iterations
+    assert np.array_equal(a.values, b.values)
+    for env in ({"FVR_RPLAN_TILE": "0"}, {"FVR_RPLAN_SORT": "0"}, {"FVR_RPLAN_TILE": "4x8", "FVR_RPLAN_SORT": "0"}):
+        c, tc = run(**env)
+        np.testing.assert_allclose(tc.rmse, ta.rmse, rtol=1e-6)
+        assert rel_err(c.values, a.values) <= 1e-5
