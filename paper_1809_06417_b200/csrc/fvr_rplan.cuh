@@ -167,7 +167,7 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                          const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch,
                          int64_t plane, const float* __restrict__ thr, const uint32_t* __restrict__ nm,
                          float* __restrict__ acc, float* __restrict__ wsm, int stride, RplanOut out,
-                         double* base, double& t_fin) {
+                         double* base, double& t_fin, const uint8_t* __restrict__ slot_tab = nullptr) {
     constexpr uint32_t kPX[3] = {0x1FFu, 0x1FFu << 9, 0x1FFu << 18};
     constexpr uint32_t kPY[3] = {0x7u | (0x7u << 9) | (0x7u << 18), (0x7u << 3) | (0x7u << 12) | (0x7u << 21),
                                  (0x7u << 6) | (0x7u << 15) | (0x7u << 24)};
@@ -305,10 +305,12 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
             if (FILL) {
                 // (weights stay in stencil order: storing them at their slots
                 // costs more address arithmetic than the per-bit slot saves)
+                // slot of stencil offset j for these residues: a shared-memory table
+                const uint8_t* tab = slot_tab + (r0 * 9 + r1 * 3 + r2) * 27;
 #pragma unroll 1
                 for (uint32_t b = sup & dyn; b; b &= b - 1) {
-                    const int j = __ffs(b) - 1, jx = j / 9, jy = (j / 3) % 3, jz = j % 3;
-                    acc[(((r0 + jx) % 3) * 9 + ((r1 + jy) % 3) * 3 + (r2 + jz) % 3) * stride] += wsm[j * stride];
+                    const int j = __ffs(b) - 1;
+                    acc[tab[j] * stride] += wsm[j * stride];
                 }
 #pragma unroll 1
                 for (uint32_t b = sup & ~dyn; b; b &= b - 1) {
@@ -398,6 +400,11 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
     double* __restrict__ base_out, double* __restrict__ t_fin_out) {
     __shared__ float s_acc[27 * 128], s_w[27 * 128];
     for (int i = threadIdx.x; i < 27 * 128; i += blockDim.x) s_acc[i] = 0.f;
+    __shared__ uint8_t s_slot[27 * 27];  // (residues r0 r1 r2, stencil offset j) -> window slot
+    for (int i = threadIdx.x; i < 27 * 27; i += blockDim.x) {
+        const int rr = i / 27, j = i % 27;
+        s_slot[i] = (uint8_t)(((rr / 9 + j / 9) % 3) * 9 + (((rr / 3) % 3 + (j / 3) % 3) % 3) * 3 + (rr % 3 + j % 3) % 3);
+    }
     __shared__ float s_thr[3 * kScatDirs];
     __shared__ uint32_t s_nm[3 * (kScatDirs + 1)];
     load_split_tables(s_thr, s_nm);
@@ -417,7 +424,7 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
                               s_acc + threadIdx.x, s_w + threadIdx.x, 128,
                               RplanOut{ent_a + unit_off[unit] * 32 + lane,
                                         reinterpret_cast<uint16_t*>(ent_b + (unit_off[unit] >> 1) * 32 + lane), kp_map},
-                              base, t_fin);
+                              base, t_fin, s_slot);
     }
     for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];
     t_fin_out[r] = t_fin;
