@@ -167,7 +167,8 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                          const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch,
                          int64_t plane, const float* __restrict__ thr, const uint32_t* __restrict__ nm,
                          float* __restrict__ acc, float* __restrict__ wsm, int stride, RplanOut out,
-                         double* base, double& t_fin, const uint8_t* __restrict__ slot_tab = nullptr) {
+                         double* base, double& t_fin, const uint8_t* __restrict__ slot_tab = nullptr,
+                         const uint8_t* __restrict__ slot_inv = nullptr) {
     constexpr uint32_t kPX[3] = {0x1FFu, 0x1FFu << 9, 0x1FFu << 18};
     constexpr uint32_t kPY[3] = {0x7u | (0x7u << 9) | (0x7u << 18), (0x7u << 3) | (0x7u << 12) | (0x7u << 21),
                                  (0x7u << 6) | (0x7u << 15) | (0x7u << 24)};
@@ -182,28 +183,24 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
         if (FILL) out.put(count, kp, wt);
         ++count;
     };
-    // key point held by slot s of the window centred on wm
-    auto slot_kp = [&](int s) {
-        int c3[3] = {s / 9, (s / 3) % 3, s % 3}, x[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) x[a] = wm[a] - 1 + (c3[a] - (wm[a] - 1) % 3 + 3) % 3;
-        return x[0] * g.sx + x[1] * g.sy + x[2];
-    };
     auto retire = [&](uint32_t slots) {
         if (!FILL) {  // count pass: one entry per retired slot
             count += __popc(slots);
             live &= ~slots;
             return;
         }
+        // offsets (dx, dy, dz) of each slot from the window's low corner, for
+        // the window's residues: a shared-memory table
+        const int res = (((wm[0] - 1) % 3 + 3) % 3) * 9 + (((wm[1] - 1) % 3 + 3) % 3) * 3 + ((wm[2] - 1) % 3 + 3) % 3;
+        const uint8_t* inv = slot_inv + res * 27;
+        const int corner = (wm[0] - 1) * g.sx + (wm[1] - 1) * g.sy + (wm[2] - 1);
 #pragma unroll 1
         for (uint32_t b = slots; b; b &= b - 1) {
             const int sl = __ffs(b) - 1;
-            float wt = 0.f;
-            if (FILL) {
-                wt = acc[sl * stride];
-                acc[sl * stride] = 0.f;
-            }
-            put(slot_kp(sl), wt);
+            const float wt = acc[sl * stride];
+            acc[sl * stride] = 0.f;
+            const int o = inv[sl];
+            put(corner + (o >> 4) * g.sx + ((o >> 2) & 3) * g.sy + (o & 3), wt);
         }
         live &= ~slots;
     };
@@ -401,9 +398,12 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
     __shared__ float s_acc[27 * 128], s_w[27 * 128];
     for (int i = threadIdx.x; i < 27 * 128; i += blockDim.x) s_acc[i] = 0.f;
     __shared__ uint8_t s_slot[27 * 27];  // (residues r0 r1 r2, stencil offset j) -> window slot
+    __shared__ uint8_t s_inv[27 * 27];   // (window residues, slot) -> offset dx << 4 | dy << 2 | dz
     for (int i = threadIdx.x; i < 27 * 27; i += blockDim.x) {
         const int rr = i / 27, j = i % 27;
         s_slot[i] = (uint8_t)(((rr / 9 + j / 9) % 3) * 9 + (((rr / 3) % 3 + (j / 3) % 3) % 3) * 3 + (rr % 3 + j % 3) % 3);
+        s_inv[i] = (uint8_t)((((j / 9 - rr / 9 + 3) % 3) << 4) | ((((j / 3) % 3 - (rr / 3) % 3 + 3) % 3) << 2) |
+                             ((j % 3 - rr % 3 + 3) % 3));
     }
     __shared__ float s_thr[3 * kScatDirs];
     __shared__ uint32_t s_nm[3 * (kScatDirs + 1)];
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
                               s_acc + threadIdx.x, s_w + threadIdx.x, 128,
                               RplanOut{ent_a + unit_off[unit] * 32 + lane,
                                         reinterpret_cast<uint16_t*>(ent_b + (unit_off[unit] >> 1) * 32 + lane), kp_map},
-                              base, t_fin, s_slot);
+                              base, t_fin, s_slot, s_inv);
     }
     for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];
     t_fin_out[r] = t_fin;
