@@ -129,9 +129,7 @@ __device__ __forceinline__ void ray_entries(const PlanRay& pr, const Geom& g, co
                         if (WEIGHTS) nw[n] += pw[p];
                         carried |= 1u << p;
                     }
-#pragma unroll
-            for (int p = 0; p < 8; ++p)
-                if (!((carried >> p) & 1u)) emit(pk[p], pw[p]);
+            emit(pk, pw, ~carried & 0xFFu);  // the corners whose run ended
         }
 #pragma unroll
         for (int k8 = 0; k8 < 8; ++k8) {
@@ -140,10 +138,7 @@ __device__ __forceinline__ void ray_entries(const PlanRay& pr, const Geom& g, co
         }
         have = true;
     });
-    if (have) {
-#pragma unroll
-        for (int p = 0; p < 8; ++p) emit(pk[p], pw[p]);
-    }
+    if (have) emit(pk, pw, 0xFFu);
 }
 
 __global__ void __launch_bounds__(128) plan_count_kernel(
@@ -154,8 +149,11 @@ __global__ void __launch_bounds__(128) plan_count_kernel(
     if (r >= n_rays) return;
     PlanRay pr;
     plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
-    ray_entries<false>(pr, g, inside, 1.0, 0.0, 0.f,
-                       [&](int kp, float) { atomicAdd(counts + kp_map[kp], 1); });
+    ray_entries<false>(pr, g, inside, 1.0, 0.0, 0.f, [&](const int* pk, const float*, uint32_t mask) {
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+            if ((mask >> p) & 1u) atomicAdd(counts + kp_map[pk[p]], 1);
+    });
 }
 
 // Plans are stored SELL-32: rows (hull key points) sorted longest first and
@@ -181,6 +179,50 @@ struct SellMap {
         a[(off + t) * 32 + (p & 31)] = idx | ((bits >> 16) << 24);
         b[((off + t) >> 1) * 64 + (p & 31) * 2 + (t & 1)] = (uint16_t)(bits & 0xFFFFu);
     }
+    // the 8 corner entries of one sample, int2 (sample id, W), batched as below
+    __device__ __forceinline__ void put8_batch(const int* kp, const float* w, const int32_t* __restrict__ kp_map,
+                                               int sid, int2* entries) const {
+        int row[8], p[8];
+        long long t[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) row[i] = __ldg(kp_map + kp[i]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            t[i] = (long long)atomicAdd(cursor + row[i], 1ull);
+            p[i] = row_pos[row[i]];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            entries[slice_off[p[i] >> 5] * 32 + t[i] * 32 + (p[i] & 31)] = make_int2(sid, __float_as_int(w[i]));
+    }
+    // up to 8 entries of one sample's corners (mask): each dependent step
+    // (row lookup, cursor atomic, slice offset) is issued for all of them
+    // before any result is used, so their latencies overlap
+    __device__ __forceinline__ void put6_batch(const int* kp, const float* w, uint32_t mask,
+                                               const int32_t* __restrict__ kp_map, uint32_t idx, uint32_t* a,
+                                               uint16_t* b) const {
+        int row[8], p[8];
+        long long t[8], off[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) row[i] = ((mask >> i) & 1u) ? __ldg(kp_map + kp[i]) : 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if ((mask >> i) & 1u) {
+                t[i] = (long long)atomicAdd(cursor + row[i], 1ull);
+                p[i] = row_pos[row[i]];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) off[i] = ((mask >> i) & 1u) ? slice_off[p[i] >> 5] : 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if ((mask >> i) & 1u) {
+                const uint32_t bits = (__float_as_uint(w[i]) + 0x40u) >> 7;
+                a[(off[i] + t[i]) * 32 + (p[i] & 31)] = idx | ((bits >> 16) << 24);
+                b[((off[i] + t[i]) >> 1) * 64 + (p[i] & 31) * 2 + (t[i] & 1)] = (uint16_t)(bits & 0xFFFFu);
+            }
+        }
+    }
 };
 
 __global__ void __launch_bounds__(128) plan_fill_kernel(
@@ -192,8 +234,8 @@ __global__ void __launch_bounds__(128) plan_fill_kernel(
     if (r >= n_rays) return;
     PlanRay pr;
     plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
-    ray_entries<true>(pr, g, inside, tau_keep, alpha_l, alpha_d, [&](int kp, float wgt) {
-        sm.put6(kp_map[kp], (uint32_t)pr.res_index, wgt, ent_a, ent_b);
+    ray_entries<true>(pr, g, inside, tau_keep, alpha_l, alpha_d, [&](const int* pk, const float* pw, uint32_t mask) {
+        sm.put6_batch(pk, pw, mask, kp_map, (uint32_t)pr.res_index, ent_a, ent_b);
     });
 }
 
@@ -247,13 +289,16 @@ __global__ void __launch_bounds__(128) splan_fill_kernel(
         }
         const float base = (float)(alpha_l * trans);
         const int base_kp = c[0] * g.sx + c[1] * g.sy + c[2];
+        int kp[8];
+        float wgt[8];
 #pragma unroll
         for (int k8 = 0; k8 < 8; ++k8) {
             const int cx = k8 >> 2, cy = (k8 >> 1) & 1, cz = k8 & 1;
             const float dist = sqrtf(fmaf(e[0][cx], e[0][cx], fmaf(e[1][cy], e[1][cy], e[2][cz] * e[2][cz])));
-            const float wgt = base * expf(-alpha_d * dist);
-            entries[sm.slot(kp_map[base_kp + cx * g.sx + cy * g.sy + cz])] = make_int2((int)sid, __float_as_int(wgt));
+            wgt[k8] = base * expf(-alpha_d * dist);
+            kp[k8] = base_kp + cx * g.sx + cy * g.sy + cz;
         }
+        sm.put8_batch(kp, wgt, kp_map, (int)sid, entries);
         ++sid;
     });
 }
