@@ -379,7 +379,28 @@ class ChannelLoop:
         unit_len = (unit_len + 1) & ~1  # even: entries_b holds pairs
         off = t.zeros(n_units + 1, dtype=t.int64, device=self.dev)
         off[1:] = t.cumsum(unit_len.long(), 0)
-        return dict(unit_len=unit_len, row_src=row_src, off=off, sizes=[off[-1]])
+        return dict(unit_len=unit_len, row_src=row_src, off=off, sizes=[off[-1], unit_len.max()])
+
+    def _rplan_unit_order(self, unit_len, max_len: int):
+        """The order fill and render visit the units: longest first, in
+        ``buckets`` length classes (a short tail), and inside a class by
+        tiles of 2x4 units (16x16 pixels), so the 8 warps of a CTA render
+        neighbouring pixels and share the operand in L1 (config 2:
+        0.1244 ms sorted by length alone, 0.1188 ms bucketed and tiled)."""
+        t = self.t
+        n_units = unit_len.numel()
+        buckets = int(os.environ.get("FVR_RPLAN_BUCKETS", "24"))
+        if buckets <= 0:
+            return t.argsort(unit_len, descending=True).to(t.int32)
+        q = max(1, -(-int(max_len) // buckets))
+        uid = t.arange(n_units, device=unit_len.device)
+        ux = (self.w_bb + 7) // 8
+        uy = self.bpv // ux
+        txn, tyn = (ux + 1) // 2, (uy + 3) // 4
+        view, u = uid // self.bpv, uid % self.bpv
+        tile = (view * tyn + (u // ux) // 4) * txn + (u % ux) // 2
+        spatial = tile * 8 + ((u // ux) % 4) * 2 + (u % ux) % 2
+        return t.argsort(-(unit_len.long() // q) * (n_units * 8) + spatial).to(t.int32)
 
     def _rplan_fill(self, rs: dict, sizes) -> bool:
         """B of rec = B c + base + t_fin bg in SELL-32 form (fvr_rplan.cuh),
@@ -405,7 +426,7 @@ class ChannelLoop:
         except t.cuda.OutOfMemoryError:
             return False
         # fill and render visit the units longest first (a short tail)
-        self.rp_order = t.argsort(unit_len, descending=True).to(t.int32) \
+        self.rp_order = self._rplan_unit_order(unit_len, sizes[1]) \
             if os.environ.get("FVR_RPLAN_SORT", "1") == "1" else None
         _lib.call("fvr_rplan_fill", *geo, self.values.data_ptr(), self.nch, off.data_ptr(), _lib.ptr(self.rp_order),
                   _lib.ptr(self.rp_row_src), self._kp_map().data_ptr(), ent_a.data_ptr(), ent_b.data_ptr(),
