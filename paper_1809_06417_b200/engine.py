@@ -694,12 +694,13 @@ class ChannelLoop:
     def stages(self):
         """[(name, fn(stream) -> launches)] of one iteration, in order; the
         name 'decision' marks where the convergence rule has been evaluated."""
+        vol = [("volume", self._volume)] if self.truth is not None else []  # vol_rmse partials
         if self._fused():  # render -> finalize in one launch; the volume partials first
-            s = [("volume", self._volume), ("render", self._render)]
+            s = vol + [("render", self._render)]
             if self.sample_plan:
                 s += [("weigh", self._weigh)]
             return s + [("decision", None), ("adjust", lambda st: self._gather(st, False))]
-        s = [("render", self._render), ("volume", self._volume)]
+        s = [("render", self._render)] + vol
         if self.sample_plan:
             s += [("weigh", self._weigh)]
         if self.plan:
