@@ -554,7 +554,8 @@ def run_reference(args):
     sample = (f"each step = {views_per_step} of {N_VIEWS} views of one iteration (render w/ scattering + adjust) "
               f"on the C/OpenMP oracle; iters/s = views_per_step / (8 * step time)")
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": its, "unit": "iters/s", "n_gpus": 0,
+        "impl": "reference", "metric": METRIC, "value": its, "unit": "iters/s", "n_gpus": args.gpus,
+        "device": "host cores only (the reference path is CPU code)",
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "n": N_VOX, "views": N_VIEWS, "res": RES, "tau": TAU},
