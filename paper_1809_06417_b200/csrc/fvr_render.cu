@@ -1033,6 +1033,25 @@ uint32_t* dyn27_scratch(const fvr_grid_t& grid, const uint8_t* dynamic, cudaStre
     }
     return buf;
 }
+// pos27 masks of the current values (rplan_pos27_kernel), recomputed per fill
+uint32_t* pos27_scratch(const fvr_grid_t& grid, const uint8_t* dynamic, const float* values, int nch,
+                        cudaStream_t st) {
+    static uint32_t* buf = nullptr;
+    static int64_t cap = 0;
+    const int64_t n = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
+    if (cap < n) {
+        if (buf) cudaFree(buf);
+        buf = nullptr;
+        cap = 0;
+        if (cudaMalloc(&buf, (size_t)n * 4) != cudaSuccess) return nullptr;
+        cap = n;
+    }
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    rplan_pos27_kernel<<<(unsigned)blocks, 256, 0, st>>>(dynamic, values, nch, n, make_geom(grid), buf);
+    count_launch(1);
+    return buf;
+}
 // the plan covers the two fast modes (g = 0, gather = edge, 32 loaded directions)
 int rplan_mode(const fvr_render_params_t& params, const fvr_grid_t& grid, bool& scat) {
     const float4* dummy = reinterpret_cast<const float4*>(&params);  // any non-null layout: mode query only
@@ -1098,15 +1117,17 @@ extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t
     if (!kp_map || !entries_a || !entries_b) return set_error(FVR_ERR_INVALID, "kp_map / entries are NULL");
     uint32_t* d27 = dyn27_scratch(grid, dynamic, st, false);
     if (!d27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
+    uint32_t* p27 = pos27_scratch(grid, dynamic, values, n_channels, st);
+    if (!p27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
     if (m)
         rplan_fill_kernel<true><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc, occ,
                                                          dynamic, d27, values, n_channels, plane, uo, unit_order,
-                                                         row_src, kp_map, entries_a, entries_b, base, t_fin);
+                                                         row_src, kp_map, entries_a, entries_b, p27, base, t_fin);
     else
         rplan_fill_kernel<false><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
                                                           occ, dynamic, d27, values, n_channels, plane, uo,
-                                                          unit_order, row_src, kp_map, entries_a, entries_b, base,
-                                                          t_fin);
+                                                          unit_order, row_src, kp_map, entries_a, entries_b, p27,
+                                                          base, t_fin);
     return check_launch("rplan_fill");
     FVR_TRY_END
 }

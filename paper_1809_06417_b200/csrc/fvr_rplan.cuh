@@ -168,7 +168,8 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                          int64_t plane, const float* __restrict__ thr, const uint32_t* __restrict__ nm,
                          float* __restrict__ acc, float* __restrict__ wsm, int stride, RplanOut out,
                          double* base, double& t_fin, const uint8_t* __restrict__ slot_tab = nullptr,
-                         const uint8_t* __restrict__ slot_inv = nullptr) {
+                         const uint8_t* __restrict__ slot_inv = nullptr,
+                         const uint32_t* __restrict__ pos27 = nullptr) {
     constexpr uint32_t kPX[3] = {0x1FFu, 0x1FFu << 9, 0x1FFu << 18};
     constexpr uint32_t kPY[3] = {0x7u | (0x7u << 9) | (0x7u << 18), (0x7u << 3) | (0x7u << 12) | (0x7u << 21),
                                  (0x7u << 6) | (0x7u << 15) | (0x7u << 24)};
@@ -310,7 +311,9 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                     acc[tab[j] * stride] += wsm[j * stride];
                 }
 #pragma unroll 1
-                for (uint32_t b = sup & ~dyn; b; b &= b - 1) {
+                // static key points with a positive value (pos27; none for the
+                // reference's initial grid) fold into base
+                for (uint32_t b = sup & (pos27 ? __ldg(pos27 + mlin) : ~dyn); b; b &= b - 1) {
                     const int j = __ffs(b) - 1;
                     const float wt = wsm[j * stride];
                     if (wt == 0.f) continue;
@@ -336,6 +339,27 @@ __global__ void rplan_dyn27_kernel(const uint8_t* __restrict__ dynamic, Geom g, 
             for (int j = 0; j < 27; ++j)
                 if (dynamic[k + (j / 9 - 1) * g.sx + ((j / 3) % 3 - 1) * g.sy + (j % 3 - 1)]) m |= 1u << j;
         dyn27[k] = m;
+    }
+}
+
+// pos27[k]: the stencil key points around interior key point k that are
+// static (not in `dynamic`) and positive in some channel -- the only static
+// ones that add to a row's base (max(v, 0) = 0 for the rest).
+__global__ void rplan_pos27_kernel(const uint8_t* __restrict__ dynamic, const float* __restrict__ values, int nch,
+                                   int64_t plane, Geom g, uint32_t* __restrict__ pos27) {
+    const int64_t n = (int64_t)(g.nx + 1) * (g.ny + 1) * (g.nz + 1);
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const int z = (int)(k % (g.nz + 1)), y = (int)((k / (g.nz + 1)) % (g.ny + 1)), x = (int)(k / g.sx);
+        uint32_t m = 0;
+        if (x >= 1 && x < g.nx && y >= 1 && y < g.ny && z >= 1 && z < g.nz)
+            for (int j = 0; j < 27; ++j) {
+                const int64_t q = k + (j / 9 - 1) * g.sx + ((j / 3) % 3 - 1) * g.sy + (j % 3 - 1);
+                if (dynamic[q]) continue;
+                bool pos = false;
+                for (int c = 0; c < nch; ++c) pos = pos || values[c * plane + q] > 0.f;
+                if (pos) m |= 1u << j;
+            }
+        pos27[k] = m;
     }
 }
 
@@ -394,7 +418,7 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
     const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch, int64_t plane,
     const long long* __restrict__ unit_off, const int* __restrict__ unit_order, const int* __restrict__ row_src,
     const int* __restrict__ kp_map, uint32_t* __restrict__ ent_a, uint32_t* __restrict__ ent_b,
-    double* __restrict__ base_out, double* __restrict__ t_fin_out) {
+    const uint32_t* __restrict__ pos27, double* __restrict__ base_out, double* __restrict__ t_fin_out) {
     __shared__ float s_acc[27 * 128], s_w[27 * 128];
     for (int i = threadIdx.x; i < 27 * 128; i += blockDim.x) s_acc[i] = 0.f;
     __shared__ uint8_t s_slot[27 * 27];  // (residues r0 r1 r2, stencil offset j) -> window slot
@@ -424,7 +448,7 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
                               s_acc + threadIdx.x, s_w + threadIdx.x, 128,
                               RplanOut{ent_a + unit_off[unit] * 32 + lane,
                                         reinterpret_cast<uint16_t*>(ent_b + (unit_off[unit] >> 1) * 32 + lane), kp_map},
-                              base, t_fin, s_slot, s_inv);
+                              base, t_fin, s_slot, s_inv, pos27);
     }
     for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];
     t_fin_out[r] = t_fin;

@@ -294,3 +294,32 @@ def test_render_plan_layouts_and_fused_finalize(cuda_device, monkeypatch, stocha
         c, tc = run(**env)
         np.testing.assert_allclose(tc.rmse, ta.rmse, rtol=1e-6)
         assert rel_err(c.values, a.values) <= 1e-5
+
+
+@pytest.mark.gpu
+def test_render_plan_with_positive_initial_grid(cuda_device, monkeypatch):
+    """An initial grid positive outside the hull: the static key points fold
+    into the render plan's base (pos27 masks) and the plan still matches the
+    marching kernel."""
+    g = load_golden("config1.npz")
+    cams = cameras_from(g, Camera)
+    n = int(g["n"])
+    hull = HullTags(g["hull_tags"], len(cams))
+    images = [Image(im.shape[1], im.shape[0], 1, im[:, :, 1:2]) for im in g["blanked"]]
+    masks = [FlameMask(m.shape[1], m.shape[0], m) for m in g["masks"]]
+    bbox = Rect(*(int(x) for x in g["bbox"]))
+    geom = VoxelGrid(n, n, n, g["origin"], float(g["edge"]))
+    rng = np.random.default_rng(3)
+    init = VoxelGrid(n, n, n, g["origin"], float(g["edge"]), "green",
+                     rng.uniform(-0.5, 2.0, size=(n + 1,) * 3).astype(np.float32))
+    rcfg = RenderConfig(tau=float(g["tau"]), scattering_enabled=True, sigma_s=float(g["sigma_s"]))
+    cfg = ReconstructionConfig(alpha_l=0.006, tau=float(g["tau"]), max_iters=4, converge_eps=1e-12,
+                               deterministic_mode=True)
+    out = {}
+    for mode in ("march", "plan"):
+        monkeypatch.setenv("FVR_RENDER", mode)
+        out[mode] = reconstruct_channel(images, cams, geom, hull, cfg, render_cfg=rcfg, masks=masks, bbox=bbox,
+                                        initial=init)
+    (a, ta), (b, tb) = out["march"], out["plan"]
+    np.testing.assert_allclose(tb.rmse, ta.rmse, rtol=1e-6)
+    assert rel_err(b.values, a.values) <= 1e-5
