@@ -7,10 +7,11 @@
 // geometry, and the trilinear reads are linear in the 27 key points around
 // the sample.  So one iteration's render is rec = B c + base + t_n bg with a
 // matrix B that never changes during a reconstruction.  The render plan stores
-// B in SELL-32 form: rows are the bbox pixels in K-render's 8x4 warp units,
-// entry t of lane i at unit_off*32 + 32 t + i (coalesced), columns are the key
-// points that can change (hull key points); key points that cannot change
-// fold into `base`.  Consecutive samples of a ray share most of their 27
+// B in SELL-32 form: rows are the bbox pixels in K-render's 8x4 warp units
+// (a 16x16-pixel tile's rows dealt to its units by length), entry t of lane i
+// at (unit_off + t)*32 + i (coalesced, 6 bytes: see RplanOut), columns are
+// the key points that can change (hull key points, numbered by the loop's
+// key-point list); key points that cannot change fold into `base`.  Consecutive samples of a ray share most of their 27
 // stencil key points, so the weights are merged along the ray in a 3x3x3
 // window that shifts with the nearest key point (~10 entries per live sample
 // instead of 27).
@@ -604,8 +605,6 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
     if (threadIdx.x == 0) state->work_retired = 0;
 }
 
-// cpack[kp] = (max(v_0, 0), max(v_1, 0), max(v_2, 0), 0) at the listed key
-// points: the three-channel render plan reads one 16-byte record per entry
 // kpv[i] = max(v, 0) at hull key point kp[i] of every channel (NCH = 1: f32,
 // NCH = 3: float4): the render plan's operand, kept current by the gather.
 template <int NCH>
