@@ -192,14 +192,11 @@ class ChannelLoop:
         self.params = _lib.render_params(render_cfg, self.scattering, n_scat, 0.0, grid_geom.edge)
         bg = np.broadcast_to(np.asarray(background, dtype=np.float64).reshape(-1), (C,))
         self.background = (ctypes.c_double * C)(*[float(x) for x in bg])
-        # packed copy of max(v, 0) read by the fast render path, kept in sync by K-update
+        # packed copy of max(v, 0) read by the marching render, kept in sync by
+        # K-update; packed once the plans are decided (the render plan reads
+        # its own operand, so with it the layout is neither built nor updated)
         self.layout_kind = _lib.layout_kind(self.params, self.grid)
         self.layout = None
-        if self.layout_kind:
-            # float4 per (key point, channel), channels interleaved (fvr_stencil.cuh)
-            self.layout = t.empty(shape + (C, 4), dtype=t.float32, device=dev)
-            _lib.call("fvr_pack_layout", self.values.data_ptr(), C, self.grid, self.layout_kind,
-                      self.layout.data_ptr(), _lib.stream_ptr())
         # empty-space occupancy: hull key points (their values change) plus any
         # positive initial value of any channel; key points outside the hull are
         # never written, so the map stays valid for the whole loop
@@ -289,6 +286,11 @@ class ChannelLoop:
         if pc is not None:
             main.wait_stream(side)
         del keep
+        if self.layout_kind and not self.rplan:
+            # float4 per (key point, channel), channels interleaved (fvr_stencil.cuh)
+            self.layout = t.empty(shape + (C, 4), dtype=t.float32, device=dev)
+            _lib.call("fvr_pack_layout", self.values.data_ptr(), C, self.grid, self.layout_kind,
+                      self.layout.data_ptr(), _lib.stream_ptr())
         self._mark("plans")
         if not self.plan:
             self.accum = t.zeros((C,) + shape, dtype=t.int64, device=dev)
