@@ -169,15 +169,15 @@ struct SellMap {
         const unsigned long long t = atomicAdd(cursor + row, 1ull);
         return slice_off[p >> 5] * 32 + (long long)t * 32 + (p & 31);
     }
-    // 6-byte entries (even slice offsets): a at the int2 slot's index, the
-    // 16-bit weight word in half t % 2 of u32 pair ((off + t) / 2) * 32 + lane
-    __device__ __forceinline__ void put6(int row, uint32_t idx, float w, uint32_t* a, uint16_t* b) const {
-        const int p = row_pos[row];
-        const long long t = (long long)atomicAdd(cursor + row, 1ull);
-        const long long off = slice_off[p >> 5];
+    // 6-byte entries in 16-byte chunks per lane (slice offsets and lengths
+    // multiples of 8): entry e = off + t of lane l has its a word at u32
+    // (e / 4 * 32 + l) * 4 + e % 4 and its 16-bit weight word at u16
+    // (e / 8 * 32 + l) * 8 + e % 8, so the gather loads LDG.128s
+    __device__ __forceinline__ static void store6(long long e, int l, uint32_t idx, float w, uint32_t* a,
+                                                  uint16_t* b) {
         const uint32_t bits = (__float_as_uint(w) + 0x40u) >> 7;  // round to 16 mantissa bits (w >= 0)
-        a[(off + t) * 32 + (p & 31)] = idx | ((bits >> 16) << 24);
-        b[((off + t) >> 1) * 64 + (p & 31) * 2 + (t & 1)] = (uint16_t)(bits & 0xFFFFu);
+        a[((e >> 2) * 32 + l) * 4 + (e & 3)] = idx | ((bits >> 16) << 24);
+        b[((e >> 3) * 32 + l) * 8 + (e & 7)] = (uint16_t)(bits & 0xFFFFu);
     }
     // the 8 corner entries of one sample, int2 (sample id, W), batched as below
     __device__ __forceinline__ void put8_batch(const int* kp, const float* w, const int32_t* __restrict__ kp_map,
@@ -216,11 +216,7 @@ struct SellMap {
         for (int i = 0; i < 8; ++i) off[i] = ((mask >> i) & 1u) ? slice_off[p[i] >> 5] : 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            if ((mask >> i) & 1u) {
-                const uint32_t bits = (__float_as_uint(w[i]) + 0x40u) >> 7;
-                a[(off[i] + t[i]) * 32 + (p[i] & 31)] = idx | ((bits >> 16) << 24);
-                b[((off[i] + t[i]) >> 1) * 64 + (p[i] & 31) * 2 + (t[i] & 1)] = (uint16_t)(bits & 0xFFFFu);
-            }
+            if ((mask >> i) & 1u) store6(off[i] + t[i], p[i] & 31, idx, w[i], a, b);
         }
     }
 };
@@ -376,25 +372,31 @@ __global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
         const int len = slice_len[sl];
         const long long off = slice_off[sl];
         const int2* e = entries + off * 32 + lane;
-        // E6: 6-byte entries (fvr_adjust_plan_fill): a words in `entries`
-        // reinterpreted as u32, 16-bit weight words in ent_b pairs
-        const uint32_t* ea = reinterpret_cast<const uint32_t*>(entries) + off * 32 + lane;
-        const uint32_t* eb = ent_b + (off >> 1) * 32 + lane;
+        // E6: 6-byte entries (fvr_adjust_plan_fill, SellMap::store6): 16-byte
+        // chunks of a words in `entries`, of 16-bit weight words in ent_b
+        const uint4* ea = reinterpret_cast<const uint4*>(entries) + (off >> 2) * 32 + lane;
+        const uint4* eb = reinterpret_cast<const uint4*>(ent_b) + (off >> 3) * 32 + lane;
         long long acc[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = 0;
         for (int t = 0; t < len; t += B) {
             int2 en[B];
             if (E6) {
-                uint32_t av[B], bv[B / 2];
+                static_assert(B % 8 == 0, "batches of whole 16-byte chunks");
+                uint4 av[B / 4], bv[B / 8];
+                const uint4 z = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-                for (int i = 0; i < B; ++i) av[i] = t + i < len ? __ldcs(ea + (int64_t)(t + i) * 32) : 0u;
+                for (int i = 0; i < B / 4; ++i) av[i] = t + 4 * i < len ? __ldcs(ea + (int64_t)(t / 4 + i) * 32) : z;
 #pragma unroll
-                for (int i = 0; i < B / 2; ++i) bv[i] = t + 2 * i < len ? __ldcs(eb + (int64_t)(t / 2 + i) * 32) : 0u;
+                for (int i = 0; i < B / 8; ++i) bv[i] = t + 8 * i < len ? __ldcs(eb + (int64_t)(t / 8 + i) * 32) : z;
 #pragma unroll
                 for (int i = 0; i < B; ++i) {
-                    const uint32_t half = (i & 1) ? (bv[i >> 1] >> 16) : (bv[i >> 1] & 0xFFFFu);
-                    en[i] = make_int2((int)(av[i] & 0xFFFFFFu), (int)(((av[i] >> 24) << 23) | (half << 7)));
+                    const uint4& q = av[i / 4];
+                    const uint32_t a = (i & 3) == 0 ? q.x : (i & 3) == 1 ? q.y : (i & 3) == 2 ? q.z : q.w;
+                    const uint4& h = bv[i / 8];
+                    const uint32_t hw = ((i & 7) >> 1) == 0 ? h.x : ((i & 7) >> 1) == 1 ? h.y : ((i & 7) >> 1) == 2 ? h.z : h.w;
+                    const uint32_t half = (i & 1) ? (hw >> 16) : (hw & 0xFFFFu);
+                    en[i] = make_int2((int)(a & 0xFFFFFFu), (int)(((a >> 24) << 23) | (half << 7)));
                 }
             } else {
 #pragma unroll

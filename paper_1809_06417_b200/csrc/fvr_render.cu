@@ -9,6 +9,7 @@
 // in the reference; each trilinear read is fp32.  Position and sample count
 // use the exact fp64 helpers of fvr_common.cuh.
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "fvr_stencil.cuh"

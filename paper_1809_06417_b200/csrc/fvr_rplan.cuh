@@ -9,7 +9,7 @@
 // matrix B that never changes during a reconstruction.  The render plan stores
 // B in SELL-32 form: rows are the bbox pixels in K-render's 8x4 warp units
 // (a 16x16-pixel tile's rows dealt to its units by length), entry t of lane i
-// at (unit_off + t)*32 + i (coalesced, 6 bytes: see RplanOut), columns are
+// in 16-byte chunks per lane (coalesced, 6 bytes: see RplanOut), columns are
 // the key points that can change (hull key points, numbered by the loop's
 // key-point list); key points that cannot change fold into `base`.  Consecutive samples of a ray share most of their 27
 // stencil key points, so the weights are merged along the ray in a 3x3x3
@@ -109,10 +109,12 @@ __device__ __forceinline__ uint32_t support_mask(bool scat, const float dl[3], c
 // Render-plan entries, 6 bytes each: word a = hull key-point index (24 bits,
 // the row of the loop's key-point list) | the weight's exponent << 24, and a
 // 16-bit word with the weight's top 16 mantissa bits (weights are >= 0;
-// relative rounding error <= 2^-17).  Row r = unit * 32 + lane, entry t: a
-// at u32 index (unit_off + t) * 32 + lane, the 16-bit word in the u32 pair
-// array at ((unit_off + t) / 2) * 32 + lane, half t % 2 (unit_off and unit
-// lengths even).
+// relative rounding error <= 2^-17).  Row r = unit * 32 + lane: its entries
+// t..t+3 are one 16-byte chunk of a words at u32 ((unit_off + t)/4 * 32 +
+// lane) * 4 + t % 4, its entries t..t+7 one 16-byte chunk of 16-bit words at
+// u16 ((unit_off + t)/8 * 32 + lane) * 8 + t % 8 (unit_off and unit lengths
+// multiples of 8): K-render loads a batch with coalesced LDG.128s (config 2:
+// 0.118 -> 0.105 ms against one u32 per lane per entry).
 constexpr uint32_t kRplanIdxMask = 0xFFFFFFu;
 
 __device__ __forceinline__ float rplan_weight(uint32_t a, uint32_t half16) {
@@ -140,8 +142,8 @@ struct RplanOut {
     const int* kp_map;   // lattice -> hull key-point index
     __device__ __forceinline__ void put(int t, int kp, float w) const {
         const uint32_t bits = (__float_as_uint(w) + 0x40u) >> 7;  // round to 16 mantissa bits
-        a[(int64_t)t * 32] = (uint32_t)__ldg(kp_map + kp) | ((bits >> 16) << 24);
-        b[(int64_t)(t >> 1) * 64 + (t & 1)] = (uint16_t)(bits & 0xFFFFu);
+        a[(int64_t)(t >> 2) * 128 + (t & 3)] = (uint32_t)__ldg(kp_map + kp) | ((bits >> 16) << 24);
+        b[(int64_t)(t >> 3) * 256 + (t & 7)] = (uint16_t)(bits & 0xFFFFu);
     }
 };
 
@@ -447,8 +449,8 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         rplan_row<SCAT, true>(cam.center, d, g, rc, occ, dynamic, dyn27, values, nch, plane, s_thr, s_nm,
                               s_acc + threadIdx.x, s_w + threadIdx.x, 128,
-                              RplanOut{ent_a + unit_off[unit] * 32 + lane,
-                                        reinterpret_cast<uint16_t*>(ent_b + (unit_off[unit] >> 1) * 32 + lane), kp_map},
+                              RplanOut{ent_a + ((unit_off[unit] >> 2) * 32 + lane) * 4,
+                                       reinterpret_cast<uint16_t*>(ent_b) + ((unit_off[unit] >> 3) * 32 + lane) * 8, kp_map},
                               base, t_fin, s_slot, s_inv, pos27);
     }
     for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];
@@ -458,13 +460,14 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
 // K-render through the plan: one warp per unit, lane = pixel; rec = B c +
 // base + t_fin bg, then the same residual / squared-residual epilogue as the
 // marching kernel.  Products in fp32, summed in fp64 a batch at a time.
-// Entries per lane in flight per batch x CTAs per SM (config 2, 6-byte
-// entries): 16x3 / 24x3 / 32x3 / 32x2 / 24x4 / 16x4 / 48x2 / 64x3:
-// 0.1245 / 0.1245 / 0.128 / 0.1248 / 0.128 / 0.1306 / 0.1307 / 0.1295 ms;
-// ptxas keeps a batch's loads ahead of their uses only with the registers to
-// hold them.
+// Entries per lane in flight per batch x CTAs per SM (config 2, 16-byte
+// chunks): 16x3 / 24x3 / 32x3 / 16x4: 0.1059 / 0.1061 / 0.105 / 0.112 ms
+// (one u32 load per entry before: 16x3 / 24x3 / 32x3 / 32x2 / 24x4 / 16x4 /
+// 48x2 / 64x3: 0.1245 / 0.1245 / 0.128 / 0.1248 / 0.128 / 0.1306 / 0.1307 /
+// 0.1295 ms); ptxas keeps a batch's loads ahead of their uses only with the
+// registers to hold them.
 #ifndef FVR_RPLAN_BATCH
-#define FVR_RPLAN_BATCH 24
+#define FVR_RPLAN_BATCH 32
 #endif
 #ifndef FVR_RPLAN_MINB
 #define FVR_RPLAN_MINB 3
@@ -490,10 +493,8 @@ __device__ __forceinline__ void rplan_render_unit(
     int units_per_view, int n_views, int w, int h, const float* __restrict__ src, const float* __restrict__ kpv,
     const RenderConsts& rc, float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride) {
     // kpv: max(v, 0) per hull key point (NCH = 1: f32; NCH = 3: float4)
-    const int len = unit_len[unit];  // even
-    const long long off = unit_off[unit];  // even
-    const uint32_t* ea = ent_a + off * 32 + lane;
-    const uint32_t* eb = ent_b + (off >> 1) * 32 + lane;
+    const int len = unit_len[unit];  // a multiple of 8
+    const long long off = unit_off[unit];  // a multiple of 8
     double acc[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
@@ -511,36 +512,32 @@ __device__ __forceinline__ void rplan_render_unit(
     };
     int t = 0;
     constexpr int B = FVR_RPLAN_BATCH;
-    for (; t + B <= len; t += B) {
-        uint32_t av[B], bv[B / 2];
+    static_assert(B % 8 == 0, "batches of whole 16-byte chunks");
+    const uint4* va = reinterpret_cast<const uint4*>(ent_a) + (off >> 2) * 32 + lane;
+    const uint4* vb = reinterpret_cast<const uint4*>(ent_b) + (off >> 3) * 32 + lane;
+    auto batch = [&](auto nb, int t0) {  // nb = entries (a multiple of 8) from t0
+        constexpr int N = decltype(nb)::value;
+        uint4 av[N / 4], bv[N / 8];
 #pragma unroll
-        for (int i = 0; i < B; ++i) av[i] = __ldcs(ea + (int64_t)(t + i) * 32);
+        for (int i = 0; i < N / 4; ++i) av[i] = __ldcs(va + (int64_t)(t0 / 4 + i) * 32);
 #pragma unroll
-        for (int i = 0; i < B / 2; ++i) bv[i] = __ldcs(eb + (int64_t)(t / 2 + i) * 32);
+        for (int i = 0; i < N / 8; ++i) bv[i] = __ldcs(vb + (int64_t)(t0 / 8 + i) * 32);
         float part[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) part[c] = 0.f;
 #pragma unroll
-        for (int i = 0; i < B; ++i) term(av[i], (i & 1) ? (bv[i >> 1] >> 16) : (bv[i >> 1] & 0xFFFFu), part);
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) acc[c] += (double)part[c];
-    }
-    for (; t < len; t += 2) {
-        const uint32_t a0 = __ldcs(ea + (int64_t)t * 32), a1 = __ldcs(ea + (int64_t)(t + 1) * 32);
-        const uint32_t bb = __ldcs(eb + (int64_t)(t / 2) * 32);
-        float part[NCH];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) part[c] = 0.f;
-        term(a0, bb & 0xFFFFu, part);
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            acc[c] += (double)part[c];
-            part[c] = 0.f;
+        for (int i = 0; i < N; ++i) {
+            const uint4& q = av[i / 4];
+            const uint32_t a = (i & 3) == 0 ? q.x : (i & 3) == 1 ? q.y : (i & 3) == 2 ? q.z : q.w;
+            const uint4& h = bv[i / 8];
+            const uint32_t hw = ((i & 7) >> 1) == 0 ? h.x : ((i & 7) >> 1) == 1 ? h.y : ((i & 7) >> 1) == 2 ? h.z : h.w;
+            term(a, (i & 1) ? (hw >> 16) : (hw & 0xFFFFu), part);
         }
-        term(a1, bb >> 16, part);
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] += (double)part[c];
-    }
+    };
+    for (; t + B <= len; t += B) batch(std::integral_constant<int, B>{}, t);
+    for (; t < len; t += 8) batch(std::integral_constant<int, 8>{}, t);
     const int64_t r = (int64_t)unit * 32 + lane;
     int view, col, row;
     const bool in = rplan_pixel(row_src ? __ldg(row_src + r) : r, units_x, units_per_view, w, h, view, col, row);

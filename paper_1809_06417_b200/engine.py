@@ -378,7 +378,7 @@ class ChannelLoop:
         if row_len is not None:
             tx, ty = (int(x) for x in os.environ.get("FVR_RPLAN_TILE", "2x4").split("x"))
             row_src, unit_len = self._rplan_row_order(row_len, n_units, tx, ty)
-        unit_len = (unit_len + 1) & ~1  # even: entries_b holds pairs
+        unit_len = (unit_len + 7) & ~7  # whole 16-byte chunks of entries (fvr_rplan.cuh)
         off = t.zeros(n_units + 1, dtype=t.int64, device=self.dev)
         off[1:] = t.cumsum(unit_len.long(), 0)
         return dict(unit_len=unit_len, row_src=row_src, off=off, sizes=[off[-1], unit_len.max()])
@@ -595,7 +595,7 @@ class ChannelLoop:
         slice_len[: self.n_kp] = counts[order]
         slice_len = slice_len.view(n_slices, 32).amax(1).contiguous()
         if not self.sample_plan:
-            slice_len = (slice_len + 1) & ~1  # 6-byte entries: weight words in pairs
+            slice_len = (slice_len + 7) & ~7  # 6-byte entries in whole 16-byte chunks (fvr_plan.cu)
         slice_off = t.zeros(n_slices + 1, dtype=t.int64, device=dev)
         slice_off[1:] = t.cumsum(slice_len.long(), 0)
         sizes = [slice_off[-1], counts.long().sum()]

@@ -21,10 +21,10 @@ slots = a.shape[0]
 print("slots", slots, "nonzero", int(nz.sum()), "fill", float(nz.sum()) / slots)
 n_units = loop.rp_len.numel()
 rowlen = t.zeros(n_units * 32, dtype=t.int64, device=e.device)
-# entry t of row (unit, lane) at unit_off[unit]*32 + 32 t + lane
+# a word of entry t of row (unit, lane) at unit_off[unit]*32 + 128 (t // 4) + 4 lane + t % 4
 off = loop.rp_off[:-1]
 unit_of_slot = t.repeat_interleave(t.arange(n_units, device=e.device), loop.rp_len.long() * 32)
-lane = (t.arange(slots, device=e.device) - off[unit_of_slot] * 32) % 32
+lane = ((t.arange(slots, device=e.device) - off[unit_of_slot] * 32) % 128) // 4
 rowlen.index_add_(0, unit_of_slot * 32 + lane, nz.long())
 rl = rowlen.view(n_units, 32).float()
 mx = rl.max(1).values
