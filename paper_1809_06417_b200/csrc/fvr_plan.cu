@@ -156,19 +156,16 @@ __global__ void __launch_bounds__(128) plan_count_kernel(
     });
 }
 
-// Plans are stored SELL-32: rows (hull key points) sorted longest first and
-// cut into slices of 32; entry t of the row at sorted position p sits at
-// slice_off[p / 32] * 32 + 32 t + p % 32, so a warp streams a slice with
-// fully coalesced loads, one lane per row (padding entries are (0, 0.0)).
+// Plans are stored SELL-32: rows (hull key points) sorted by length within
+// windows and cut into slices of 32; the row at sorted position p is lane
+// p % 32 of slice p / 32, whose entries start at entry slice_off[p / 32] of
+// every lane.  A lane's consecutive entries are packed into 16-byte chunks
+// (store6 / put8_batch), so a warp streams a slice with fully coalesced
+// LDG.128s, one lane per row (padding entries are (0, 0.0)).
 struct SellMap {
     const int32_t* row_pos;          // row -> sorted position
     const long long* slice_off;      // per slice, in units of 32 entries
     unsigned long long* cursor;      // per row, entries written so far
-    __device__ __forceinline__ long long slot(int row) const {
-        const int p = row_pos[row];
-        const unsigned long long t = atomicAdd(cursor + row, 1ull);
-        return slice_off[p >> 5] * 32 + (long long)t * 32 + (p & 31);
-    }
     // 6-byte entries in 16-byte chunks per lane (slice offsets and lengths
     // multiples of 8): entry e = off + t of lane l has its a word at u32
     // (e / 4 * 32 + l) * 4 + e % 4 and its 16-bit weight word at u16
@@ -191,9 +188,13 @@ struct SellMap {
             t[i] = (long long)atomicAdd(cursor + row[i], 1ull);
             p[i] = row_pos[row[i]];
         }
+        // entry e = off + t of lane l at int2 (e / 2 * 32 + l) * 2 + e % 2:
+        // a lane's entry pairs are 16-byte chunks (slice offsets and lengths even)
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-            entries[slice_off[p[i] >> 5] * 32 + t[i] * 32 + (p[i] & 31)] = make_int2(sid, __float_as_int(w[i]));
+        for (int i = 0; i < 8; ++i) {
+            const long long e = slice_off[p[i] >> 5] + t[i];
+            entries[((e >> 1) * 32 + (p[i] & 31)) * 2 + (e & 1)] = make_int2(sid, __float_as_int(w[i]));
+        }
     }
     // up to 8 entries of one sample's corners (mask): each dependent step
     // (row lookup, cursor atomic, slice offset) is issued for all of them
@@ -342,6 +343,11 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
 #ifndef FVR_GATHER_BATCH
 #define FVR_GATHER_BATCH 32
 #endif
+// the int2 sample plan (entry pairs per 16-byte load): batch 32 / 24 / 16 =
+// 0.190 (spills) / 0.157 / 0.169 ms at config 2
+#ifndef FVR_SPLAN_BATCH
+#define FVR_SPLAN_BATCH 24
+#endif
 // CTAs per SM: 6-byte entries leave room for 4 (config 2, deterministic,
 // batch x CTAs 32x3 / 32x4 / 32x5 / 24x5 / 16x4 / 64x2: 0.0763 / 0.0718 /
 // 0.0718 / 0.0714 / 0.0766 / 0.0845 ms); the int2 sample plan keeps 3.
@@ -366,12 +372,12 @@ __global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
     if (!any) return;
     const int lane = threadIdx.x & 31;
     const int64_t n_slices = (n_rows + 31) >> 5;
-    constexpr int B = FVR_GATHER_BATCH;
+    constexpr int B = E6 ? FVR_GATHER_BATCH : FVR_SPLAN_BATCH;
     for (int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < n_slices;
          sl += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int len = slice_len[sl];
         const long long off = slice_off[sl];
-        const int2* e = entries + off * 32 + lane;
+        const int4* e = reinterpret_cast<const int4*>(entries) + (off >> 1) * 32 + lane;  // entry pairs
         // E6: 6-byte entries (fvr_adjust_plan_fill, SellMap::store6): 16-byte
         // chunks of a words in `entries`, of 16-bit weight words in ent_b
         const uint4* ea = reinterpret_cast<const uint4*>(entries) + (off >> 2) * 32 + lane;
@@ -400,7 +406,11 @@ __global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
                 }
             } else {
 #pragma unroll
-                for (int i = 0; i < B; ++i) en[i] = t + i < len ? __ldcs(e + (int64_t)(t + i) * 32) : make_int2(0, 0);
+                for (int i = 0; i < B / 2; ++i) {
+                    const int4 v = t + 2 * i < len ? __ldcs(e + (int64_t)(t / 2 + i) * 32) : make_int4(0, 0, 0, 0);
+                    en[2 * i] = make_int2(v.x, v.y);
+                    en[2 * i + 1] = make_int2(v.z, v.w);
+                }
             }
 #pragma unroll
             for (int i = 0; i < B; ++i) {
