@@ -233,6 +233,9 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
  * `finalize` (single-rank loops) the last block to finish runs
  * fvr_loop_finalize on state (one launch less per iteration; the block
  * counter is state[0].work_retired). */
+/* Entries per lane chunk of the render-plan layout: unit_len and unit_off
+ * must be multiples of it (the caller pads unit_len from the count pass). */
+int fvr_rplan_chunk_entries(void);
 int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                     int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
                     const uint8_t* dynamic, int32_t* unit_len, int32_t* row_len, void* stream);

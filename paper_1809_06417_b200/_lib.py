@@ -143,6 +143,7 @@ _SIGNATURES = {
     "fvr_adjust_plan_fill": (
         c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, c_double, c_double, c_double,
                 _P, _P, _P, _P, _P, _P, _P]),
+    "fvr_rplan_chunk_entries": (c_int, []),
     "fvr_rplan_count": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _GRID, _PARAMS, _P, _P, _P, _P,
                                 _P]),
     "fvr_rplan_fill": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _GRID, _PARAMS, _P, _P, _P, c_int32,

@@ -1063,6 +1063,8 @@ int rplan_mode(const fvr_render_params_t& params, const fvr_grid_t& grid, bool& 
 }
 }  // namespace
 
+extern "C" int fvr_rplan_chunk_entries(void) { return kRpB; }
+
 extern "C" int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                                int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params,
                                const uint8_t* occ, const uint8_t* dynamic, int32_t* unit_len, int32_t* row_len,

@@ -109,12 +109,12 @@ __device__ __forceinline__ uint32_t support_mask(bool scat, const float dl[3], c
 // Render-plan entries, 6 bytes each: word a = hull key-point index (24 bits,
 // the row of the loop's key-point list) | the weight's exponent << 24, and a
 // 16-bit word with the weight's top 16 mantissa bits (weights are >= 0;
-// relative rounding error <= 2^-17).  Row r = unit * 32 + lane: its entries
-// t..t+3 are one 16-byte chunk of a words at u32 ((unit_off + t)/4 * 32 +
-// lane) * 4 + t % 4, its entries t..t+7 one 16-byte chunk of 16-bit words at
-// u16 ((unit_off + t)/8 * 32 + lane) * 8 + t % 8 (unit_off and unit lengths
-// multiples of 8): K-render loads a batch with coalesced LDG.128s (config 2:
-// 0.118 -> 0.105 ms against one u32 per lane per entry).
+// relative rounding error <= 2^-17).  Row r = unit * 32 + lane: with
+// A = kRpA a words and 2A 16-bit words per chunk, its entries t..t+A-1 are
+// one chunk of a words at u32 ((unit_off + t)/A * 32 + lane) * A + t % A and
+// its entries t..t+2A-1 one chunk of 16-bit words at u16 ((unit_off +
+// t)/(2A) * 32 + lane) * 2A + t % 2A (unit_off and unit lengths multiples of
+// 2A): K-render loads a batch with coalesced 32-byte loads.
 constexpr uint32_t kRplanIdxMask = 0xFFFFFFu;
 
 __device__ __forceinline__ float rplan_weight(uint32_t a, uint32_t half16) {
@@ -136,14 +136,24 @@ __device__ __forceinline__ uint32_t rotate27(uint32_t m, int r0, int r1, int r2)
     return rotate_axis(m, r0, 0x1FFu, 9);                               // jx
 }
 
+// Bytes per lane chunk of the plan layout: 32 (sm_100 LDG.256, units padded
+// to 16 entries) or 16 (LDG.128, units padded to 8).  Config 2 K-render:
+// 0.1012 / 0.1035 ms; one u32 load per entry was 0.118 ms.  The engine pads
+// units to kRpB entries (fvr_rplan_chunk_entries).
+#ifndef FVR_RPLAN_CHUNK
+#define FVR_RPLAN_CHUNK 32
+#endif
+constexpr int kRpA = FVR_RPLAN_CHUNK / 4;  // a words per chunk
+constexpr int kRpB = FVR_RPLAN_CHUNK / 2;  // 16-bit weight words per chunk
+
 struct RplanOut {
     uint32_t* a;         // this row's first a word
     uint16_t* b;         // this row's first 16-bit word
     const int* kp_map;   // lattice -> hull key-point index
     __device__ __forceinline__ void put(int t, int kp, float w) const {
         const uint32_t bits = (__float_as_uint(w) + 0x40u) >> 7;  // round to 16 mantissa bits
-        a[(int64_t)(t >> 2) * 128 + (t & 3)] = (uint32_t)__ldg(kp_map + kp) | ((bits >> 16) << 24);
-        b[(int64_t)(t >> 3) * 256 + (t & 7)] = (uint16_t)(bits & 0xFFFFu);
+        a[(int64_t)(t / kRpA) * (32 * kRpA) + (t % kRpA)] = (uint32_t)__ldg(kp_map + kp) | ((bits >> 16) << 24);
+        b[(int64_t)(t / kRpB) * (32 * kRpB) + (t % kRpB)] = (uint16_t)(bits & 0xFFFFu);
     }
 };
 
@@ -449,8 +459,9 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         rplan_row<SCAT, true>(cam.center, d, g, rc, occ, dynamic, dyn27, values, nch, plane, s_thr, s_nm,
                               s_acc + threadIdx.x, s_w + threadIdx.x, 128,
-                              RplanOut{ent_a + ((unit_off[unit] >> 2) * 32 + lane) * 4,
-                                       reinterpret_cast<uint16_t*>(ent_b) + ((unit_off[unit] >> 3) * 32 + lane) * 8, kp_map},
+                              RplanOut{ent_a + ((unit_off[unit] / kRpA) * 32 + lane) * kRpA,
+                                       reinterpret_cast<uint16_t*>(ent_b) + ((unit_off[unit] / kRpB) * 32 + lane) * kRpB,
+                                       kp_map},
                               base, t_fin, s_slot, s_inv, pos27);
     }
     for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];
@@ -484,6 +495,26 @@ struct RplanFinalize {
     int64_t trace_stride;
 };
 
+struct RpChunk {
+    uint32_t w[kRpA];
+};
+__device__ __forceinline__ RpChunk rplan_stream(const uint32_t* p) {
+    RpChunk c;
+#if FVR_RPLAN_CHUNK == 32
+    asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(c.w[0]), "=r"(c.w[1]), "=r"(c.w[2]), "=r"(c.w[3]), "=r"(c.w[4]), "=r"(c.w[5]), "=r"(c.w[6]),
+          "=r"(c.w[7])
+        : "l"(p));
+#else
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p));
+    c.w[0] = v.x;
+    c.w[1] = v.y;
+    c.w[2] = v.z;
+    c.w[3] = v.w;
+#endif
+    return c;
+}
+
 // One unit (8x4 pixels, lane = pixel) of K-render through the plan.
 template <int NCH>
 __device__ __forceinline__ void rplan_render_unit(
@@ -512,32 +543,29 @@ __device__ __forceinline__ void rplan_render_unit(
     };
     int t = 0;
     constexpr int B = FVR_RPLAN_BATCH;
-    static_assert(B % 8 == 0, "batches of whole 16-byte chunks");
-    const uint4* va = reinterpret_cast<const uint4*>(ent_a) + (off >> 2) * 32 + lane;
-    const uint4* vb = reinterpret_cast<const uint4*>(ent_b) + (off >> 3) * 32 + lane;
-    auto batch = [&](auto nb, int t0) {  // nb = entries (a multiple of 8) from t0
+    static_assert(B % kRpB == 0, "batches of whole chunks");
+    const uint32_t* va = ent_a + ((off / kRpA) * 32 + lane) * kRpA;
+    const uint32_t* vb = ent_b + ((off / kRpB) * 32 + lane) * kRpA;  // a b chunk is kRpA u32 too
+    auto batch = [&](auto nb, int t0) {  // nb = entries (a multiple of kRpB) from t0
         constexpr int N = decltype(nb)::value;
-        uint4 av[N / 4], bv[N / 8];
+        RpChunk av[N / kRpA], bv[N / kRpB];
 #pragma unroll
-        for (int i = 0; i < N / 4; ++i) av[i] = __ldcs(va + (int64_t)(t0 / 4 + i) * 32);
+        for (int i = 0; i < N / kRpA; ++i) av[i] = rplan_stream(va + (int64_t)(t0 / kRpA + i) * (32 * kRpA));
 #pragma unroll
-        for (int i = 0; i < N / 8; ++i) bv[i] = __ldcs(vb + (int64_t)(t0 / 8 + i) * 32);
+        for (int i = 0; i < N / kRpB; ++i) bv[i] = rplan_stream(vb + (int64_t)(t0 / kRpB + i) * (32 * kRpA));
         float part[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) part[c] = 0.f;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-            const uint4& q = av[i / 4];
-            const uint32_t a = (i & 3) == 0 ? q.x : (i & 3) == 1 ? q.y : (i & 3) == 2 ? q.z : q.w;
-            const uint4& h = bv[i / 8];
-            const uint32_t hw = ((i & 7) >> 1) == 0 ? h.x : ((i & 7) >> 1) == 1 ? h.y : ((i & 7) >> 1) == 2 ? h.z : h.w;
-            term(a, (i & 1) ? (hw >> 16) : (hw & 0xFFFFu), part);
+            const uint32_t hw = bv[i / kRpB].w[(i % kRpB) >> 1];
+            term(av[i / kRpA].w[i % kRpA], (i & 1) ? (hw >> 16) : (hw & 0xFFFFu), part);
         }
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] += (double)part[c];
     };
     for (; t + B <= len; t += B) batch(std::integral_constant<int, B>{}, t);
-    for (; t < len; t += 8) batch(std::integral_constant<int, 8>{}, t);
+    for (; t < len; t += kRpB) batch(std::integral_constant<int, kRpB>{}, t);
     const int64_t r = (int64_t)unit * 32 + lane;
     int view, col, row;
     const bool in = rplan_pixel(row_src ? __ldg(row_src + r) : r, units_x, units_per_view, w, h, view, col, row);

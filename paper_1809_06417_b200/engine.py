@@ -378,7 +378,8 @@ class ChannelLoop:
         if row_len is not None:
             tx, ty = (int(x) for x in os.environ.get("FVR_RPLAN_TILE", "2x4").split("x"))
             row_src, unit_len = self._rplan_row_order(row_len, n_units, tx, ty)
-        unit_len = (unit_len + 7) & ~7  # whole 16-byte chunks of entries (fvr_rplan.cuh)
+        al = int(_lib.load().fvr_rplan_chunk_entries())  # whole lane chunks of entries (fvr_rplan.cuh)
+        unit_len = (unit_len + al - 1) & ~(al - 1)
         off = t.zeros(n_units + 1, dtype=t.int64, device=self.dev)
         off[1:] = t.cumsum(unit_len.long(), 0)
         return dict(unit_len=unit_len, row_src=row_src, off=off, sizes=[off[-1], unit_len.max()])
