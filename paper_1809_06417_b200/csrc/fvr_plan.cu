@@ -156,6 +156,14 @@ __global__ void __launch_bounds__(128) plan_count_kernel(
     });
 }
 
+// int2 sample-plan entries per lane chunk: 2 (16-byte loads) or 4 (sm_100
+// 32-byte loads; the engine pads sample-plan slices to 4 entries).  Config
+// 2 sample-plan gather: 0.157 / 0.1525 ms.
+#ifndef FVR_SPLAN_CHUNK
+#define FVR_SPLAN_CHUNK 32
+#endif
+constexpr int kSE = FVR_SPLAN_CHUNK / 8;
+
 // Plans are stored SELL-32: rows (hull key points) sorted by length within
 // windows and cut into slices of 32; the row at sorted position p is lane
 // p % 32 of slice p / 32, whose entries start at entry slice_off[p / 32] of
@@ -188,12 +196,13 @@ struct SellMap {
             t[i] = (long long)atomicAdd(cursor + row[i], 1ull);
             p[i] = row_pos[row[i]];
         }
-        // entry e = off + t of lane l at int2 (e / 2 * 32 + l) * 2 + e % 2:
-        // a lane's entry pairs are 16-byte chunks (slice offsets and lengths even)
+        // entry e = off + t of lane l at int2 (e / S * 32 + l) * S + e % S with
+        // S = kSE: a lane's S consecutive entries are one chunk (slice offsets
+        // and lengths multiples of S)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const long long e = slice_off[p[i] >> 5] + t[i];
-            entries[((e >> 1) * 32 + (p[i] & 31)) * 2 + (e & 1)] = make_int2(sid, __float_as_int(w[i]));
+            entries[((e / kSE) * 32 + (p[i] & 31)) * kSE + (e % kSE)] = make_int2(sid, __float_as_int(w[i]));
         }
     }
     // up to 8 entries of one sample's corners (mask): each dependent step
@@ -343,8 +352,9 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
 #ifndef FVR_GATHER_BATCH
 #define FVR_GATHER_BATCH 32
 #endif
-// the int2 sample plan (entry pairs per 16-byte load): batch 32 / 24 / 16 =
-// 0.190 (spills) / 0.157 / 0.169 ms at config 2
+// the int2 sample plan: batch 32 / 24 / 16 = 0.190 (spills) / 0.157 / 0.169 ms
+// at config 2 with entry pairs per load; with 32-byte chunks 24 / 16 = 0.1525 /
+// 0.1565 ms
 #ifndef FVR_SPLAN_BATCH
 #define FVR_SPLAN_BATCH 24
 #endif
@@ -377,7 +387,7 @@ __global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
          sl += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int len = slice_len[sl];
         const long long off = slice_off[sl];
-        const int4* e = reinterpret_cast<const int4*>(entries) + (off >> 1) * 32 + lane;  // entry pairs
+        const int2* e = entries + ((off / kSE) * 32 + lane) * kSE;  // chunks of kSE entries
         // E6: 6-byte entries (fvr_adjust_plan_fill, SellMap::store6): 16-byte
         // chunks of a words in `entries`, of 16-bit weight words in ent_b
         const uint4* ea = reinterpret_cast<const uint4*>(entries) + (off >> 2) * 32 + lane;
@@ -405,11 +415,24 @@ __global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
                     en[i] = make_int2((int)(a & 0xFFFFFFu), (int)(((a >> 24) << 23) | (half << 7)));
                 }
             } else {
+                static_assert(E6 || B % kSE == 0, "batches of whole chunks");
 #pragma unroll
-                for (int i = 0; i < B / 2; ++i) {
-                    const int4 v = t + 2 * i < len ? __ldcs(e + (int64_t)(t / 2 + i) * 32) : make_int4(0, 0, 0, 0);
+                for (int i = 0; i < B / kSE; ++i) {
+                    const int2* q = e + (int64_t)(t / kSE + i) * (32 * kSE);
+#if FVR_SPLAN_CHUNK == 32
+                    uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                    if (t + kSE * i < len)
+                        asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                            : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+                              "=r"(w[7])
+                            : "l"(q));
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) en[4 * i + j] = make_int2((int)w[2 * j], (int)w[2 * j + 1]);
+#else
+                    const int4 v = t + 2 * i < len ? __ldcs(reinterpret_cast<const int4*>(q)) : make_int4(0, 0, 0, 0);
                     en[2 * i] = make_int2(v.x, v.y);
                     en[2 * i + 1] = make_int2(v.z, v.w);
+#endif
                 }
             }
 #pragma unroll

@@ -595,9 +595,9 @@ class ChannelLoop:
         slice_len = t.zeros(n_slices * 32, dtype=t.int32, device=dev)
         slice_len[: self.n_kp] = counts[order]
         slice_len = slice_len.view(n_slices, 32).amax(1).contiguous()
-        # whole 16-byte chunks per lane (fvr_plan.cu): 8 six-byte entries or
-        # 2 eight-byte sample entries
-        slice_len = (slice_len + 1) & ~1 if self.sample_plan else (slice_len + 7) & ~7
+        # whole lane chunks (fvr_plan.cu): 16 bytes of six-byte entries (8), or
+        # 32 bytes of eight-byte sample entries (kSE = 4)
+        slice_len = (slice_len + 3) & ~3 if self.sample_plan else (slice_len + 7) & ~7
         slice_off = t.zeros(n_slices + 1, dtype=t.int64, device=dev)
         slice_off[1:] = t.cumsum(slice_len.long(), 0)
         sizes = [slice_off[-1], counts.long().sum()]
