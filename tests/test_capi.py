@@ -59,3 +59,11 @@ def test_abi_version_and_error_string_without_gpu():
     assert b"voxel counts" in lib.fvr_last_error()
     with pytest.raises(ValueError):
         _lib.check(rc)
+
+
+def test_render_plan_chunk_entries_without_gpu():
+    """Units of the render plan are padded to whole 32-byte lane chunks of
+    16-bit weight words (fvr_rplan.cuh kRpB); the engine reads the padding
+    from the library, so a build with another chunk size stays consistent."""
+    n = _lib.load().fvr_rplan_chunk_entries()
+    assert n in (8, 16) and n & (n - 1) == 0
