@@ -40,10 +40,10 @@ SCAT_DIRS = 32
 TAU = 1.0 - 0.95 ** (64.0 / N_VOX)
 ALPHA_L = 0.006
 # dram__bytes_read.sum + dram__bytes_write.sum of K-render from one `ncu --set full`
-# capture: the render-plan SpMV (profiles/r1_ncu_final8_render_gather_raw.csv) and the marching
+# capture: the render-plan SpMV (profiles/r1_ncu_final9_render_gather_raw.csv) and the marching
 # kernel it replaced (profiles/r1_ncu_render_final_raw.csv)
-TRAFFIC_BYTES_PER_LAUNCH = {"rplan_render_kernel<1>": 524_656_640, "loop_render_scat_kernel": 10_210_304}
-TRAFFIC_SOURCE = {"rplan_render_kernel<1>": "profiles/r1_ncu_final8_render_gather_raw.csv (round 1)",
+TRAFFIC_BYTES_PER_LAUNCH = {"rplan_render_kernel<1>": 524_331_008, "loop_render_scat_kernel": 10_210_304}
+TRAFFIC_SOURCE = {"rplan_render_kernel<1>": "profiles/r1_ncu_final9_render_gather_raw.csv (round 1)",
                   "loop_render_scat_kernel": "profiles/r1_ncu_render_final_raw.csv (round 1)"}
 METRIC = "recon iters/sec at 128³×8 views 512²; Gsamples/s; % of HBM roofline"
 WORKLOAD = "config 2: 128^3 flame, 8 views 512x512, full RTE (sigma_s 0.1, 32 dirs), green channel"
