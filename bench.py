@@ -45,8 +45,9 @@ ALPHA_L = 0.006
 TRAFFIC_BYTES_PER_LAUNCH = {"rplan_render_kernel<1>": 524_331_008, "loop_render_scat_kernel": 10_210_304}
 TRAFFIC_SOURCE = {"rplan_render_kernel<1>": "profiles/r1_ncu_final9_render_gather_raw.csv (round 1)",
                   "loop_render_scat_kernel": "profiles/r1_ncu_render_final_raw.csv (round 1)"}
+DTYPE = ("f32 values, 17-bit-mantissa operator weights (render and adjust plans), f64 geometry, "
+         "32.32 fixed-point accumulation")
 METRIC = "recon iters/sec at 128³×8 views 512²; Gsamples/s; % of HBM roofline"
-WORKLOAD = "config 2: 128^3 flame, 8 views 512x512, full RTE (sigma_s 0.1, 32 dirs), green channel"
 
 
 def peaks():
@@ -64,24 +65,10 @@ def peaks():
 
 
 def make_scene():
-    """Synthetic inputs of configs[1], rendered on the device."""
-    from paper_1809_06417_b200 import RenderConfig, VoxelGrid, compute_visual_hull, render_view
-    from paper_1809_06417_b200.preprocess import bounding_box, threshold_mask
-    from paper_1809_06417_b200.synth import synth_cameras, synth_volume
+    """Synthetic inputs of configs[1], rendered on the device (workloads.py)."""
+    import workloads
 
-    vols = synth_volume((N_VOX,) * 3, seed=0, kind="flame")
-    truth = [vols[t] for t in ("red", "green", "blue")]
-    cams = synth_cameras(N_VIEWS, radius=0.38, fov=60.0, elevation_jitter_deg=5.0, width=RES, height=RES, seed=0)
-    rcfg = RenderConfig(tau=TAU, scattering_enabled=True, sigma_s=SIGMA_S, scatter_dirs=SCAT_DIRS)
-    imgs = [render_view(c, truth, None, rcfg) for c in cams]
-    masked = [threshold_mask(im) for im in imgs]
-    masks = [m for m, _ in masked]
-    blanked = [im for _, im in masked]
-    bbox = bounding_box(masks, 4)
-    geom = VoxelGrid(N_VOX, N_VOX, N_VOX, truth[0].origin, truth[0].edge)
-    hull = compute_visual_hull(geom, [m.bits for m in masks], cams)
-    return dict(truth=truth, cams=cams, rcfg=rcfg, images=[im.channel(1) for im in blanked], masks=masks,
-                bbox=bbox, geom=geom, hull=hull)
+    return workloads.device_scene(N_VOX, N_VIEWS, RES)
 
 
 def work_counts(sc):
@@ -246,6 +233,9 @@ class ClockSampler:
 def run_gpu(args):
     import torch
 
+    import ctypes
+
+    import workloads
     from paper_1809_06417_b200 import ReconstructionConfig, _lib, reconstruct_channel
     from paper_1809_06417_b200.engine import ChannelLoop
     from paper_1809_06417_b200.reconstruct import _init_grid, _loop_config
@@ -400,8 +390,13 @@ def run_gpu(args):
             t = torch.tensor([wall], dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             wall = float(t.item())
-        h2d = (sum(s.nbytes for s in src) + grid0.values.nbytes + sc["hull"].inside_voxels().size
-               + 4 * w["hull_kp"] + 4 * w["R_f"] + 160 * N_VIEWS)
+        # what reconstruct_channel copies: the bbox crops of the frames (f32)
+        # and of the masks (u8), the inside-voxel bytes and the camera
+        # structs in; the lattice and the trace out (hull key points, the
+        # initial lattice and the flame-ray list are derived on the device)
+        bb = sc["bbox"]
+        h2d = (sum(s.nbytes for s in src) + N_VIEWS * bb.area + sc["hull"].inside_voxels().size
+               + ctypes.sizeof(_lib.FvrCamera) * N_VIEWS)
         d2h = grid.values.nbytes + 8 * trace.iterations
         e2e = {"value": trace.iterations / wall, "unit": "iters/s", "iterations": trace.iterations,
                "h2d_bytes_per_step": int(h2d / trace.iterations), "d2h_bytes_per_step": int(d2h / trace.iterations),
@@ -420,13 +415,10 @@ def run_gpu(args):
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f32 values / f64 geometry",
+        "dtype": DTYPE,
         "data": "synthetic (synth_volume seed 0, synth_cameras seed 0, inputs rendered on device)",
-        "config": {"workload": WORKLOAD, "n": N_VOX, "views": N_VIEWS, "res": RES, "tau": TAU,
-                   "sigma_s": SIGMA_S, "scatter_dirs": SCAT_DIRS, "bbox": [sc["bbox"].u0, sc["bbox"].v0,
-                                                                          sc["bbox"].u1, sc["bbox"].v1],
-                   "parallelism": f"view-sharded x{world}" if world > 1 else "1 GPU",
-                   "l2": "256 MiB buffer written between timed steps (outside the step events)"},
+        "config": workloads.bench_config(N_VOX, N_VIEWS, RES, (sc["bbox"].u0, sc["bbox"].v0, sc["bbox"].u1,
+                                                               sc["bbox"].v1), world),
         "gsamples_per_s": (w["S_r"] + w["S_a"]) * its / 1e9,
         "render_gsamples_per_s": w["S_r"] / (render_ms * 1e-3) / 1e9,
         "work": w,
@@ -522,48 +514,89 @@ def _cpu_model():
 
 
 def run_reference(args):
+    """The reference arm: the unmodified reference package (baseline/_ref,
+    numba kernels on the host cores) through its own public API, on the same
+    workload and config as the GPU arm.  The scene is built by the reference
+    itself (workloads.reference_scene); this package and its library are never
+    imported.  A step is ``views_per_step`` views of one loop iteration
+    (reconstruct.py:304-331): render_pixels of each view's bbox pixels, the
+    per-view RMSE and residual field, then one adjust_pass over those views;
+    views_per_step is sized from a timed warm-up so that the whole --steps K
+    --warmup W run stays within a few minutes.  iters/s = views_per_step /
+    (V * mean step time)."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
-    import torch
+    import workloads
 
-    from oracle import cpu
-
+    if not workloads.reference_available():
+        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref is not installed (see DESIGN.md §6 for "
+                                                              "the pip --target install of /root/reference/pkg)"}))
+        return
     cores = os.cpu_count() or 1
-    cpu.set_threads(cores)
-    sc = make_scene()  # inputs are generated with the device path (same scene as the GPU arm)
-    from paper_1809_06417_b200.reconstruct import _init_grid
-
-    values = _init_grid(sc["geom"], sc["hull"], "green").values
-    # size a step: views per step so that warmup + steps stay within ~150 s
     t0 = time.perf_counter()
-    values = _oracle_iteration_sample(sc, values, [0], cpu)
+    sc = workloads.reference_scene(N_VOX, N_VIEWS, RES)
+    scene_s = time.perf_counter() - t0
+    ref = sc["ref"]
+    R = ref["reconstruct"]
+    cfg = R.ReconstructionConfig(alpha_l=ALPHA_L, alpha_d=1.0, tau=TAU, max_iters=args.steps + args.warmup,
+                                 converge_eps=1e-12, deterministic_mode=True)
+    grid = R._init_grid(sc["geom"], sc["hull"], "green")
+    rng = np.random.default_rng(cfg.rng_seed)
+    b = sc["bbox"]
+    h_bb, w_bb = b.v1 - b.v0 + 1, b.u1 - b.u0 + 1
+    uu, vv = np.meshgrid(np.arange(b.u0, b.u1 + 1, dtype=np.float64) + 0.5,
+                         np.arange(b.v0, b.v1 + 1, dtype=np.float64) + 0.5, indexing="xy")
+    us, vs = uu.ravel(), vv.ravel()
+    src = [im.data[b.slices][:, :, 0].astype(np.float64) for im in sc["images"]]
+
+    def step(views):
+        residuals = []
+        for v in views:
+            cam = sc["cams"][v]
+            rec = ref["render"].render_pixels(cam, [grid], sc["rcfg"], us, vs).reshape(h_bb, w_bb)
+            float(np.sqrt(np.mean((src[v] - rec) ** 2)))
+            field = np.zeros((cam.height, cam.width))
+            field[b.slices] = src[v] - rec
+            residuals.append(field)
+        R.adjust_pass(grid, sc["hull"], [sc["cams"][v] for v in views], residuals, [sc["masks"][v] for v in views],
+                      cfg, rng, b)
+
+    t0 = time.perf_counter()
+    step([0])  # numba JIT of render_rays / adjust_rays_chunked, then one timed view
+    jit_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    step([1 % N_VIEWS])
     per_view = time.perf_counter() - t0
     n_steps = args.steps + args.warmup
-    views_per_step = int(max(1, min(N_VIEWS, 150.0 / max(per_view * n_steps, 1e-9))))
+    views_per_step = int(max(1, min(N_VIEWS, args.reference_seconds / max(per_view * n_steps, 1e-9))))
     times = []
     for s in range(n_steps):
         views = [(s * views_per_step + i) % N_VIEWS for i in range(views_per_step)]
         t0 = time.perf_counter()
-        values = _oracle_iteration_sample(sc, values, views, cpu)
+        step(views)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(dt)
     per_step = float(np.mean(times))
     its = views_per_step / (N_VIEWS * per_step)
-    sample = (f"each step = {views_per_step} of {N_VIEWS} views of one iteration (render w/ scattering + adjust) "
-              f"on the C/OpenMP oracle; iters/s = views_per_step / (8 * step time)")
+    sample = (f"each step = {views_per_step} of {N_VIEWS} views of one iteration through the reference's public API "
+              f"(fvr.render.render_pixels of the view's bbox pixels with scattering + fvr.reconstruct.adjust_pass), "
+              f"numba on {cores} host threads; iters/s = views_per_step / ({N_VIEWS} * step time); scene built by "
+              f"the reference in {scene_s:.0f} s, JIT warm-up {jit_s:.0f} s")
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": its, "unit": "iters/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": its, "unit": "iters/s", "n_gpus": world,
         "device": "host cores only (the reference path is CPU code)",
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n": N_VOX, "views": N_VIEWS, "res": RES, "tau": TAU},
-        "cpu_baseline": {"value": its, "unit": "iters/s", "cores": cores, "kind": "port", "sample": sample,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64 geometry and accumulation, f32 lattice",
+        "data": "synthetic (synth_volume seed 0, synth_cameras seed 0, inputs rendered by the reference)",
+        "config": workloads.bench_config(N_VOX, N_VIEWS, RES, (b.u0, b.v0, b.u1, b.v1), world),
+        "cpu_baseline": {"value": its, "unit": "iters/s", "cores": cores, "kind": "reference", "sample": sample,
                          "cpu": _cpu_model()},
         "e2e": {"value": its, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
     }))
-    del torch
 
 
 def main():
@@ -575,10 +608,21 @@ def main():
     ap.add_argument("--e2e-iters", type=int, default=50)
     ap.add_argument("--stochastic-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--reference-seconds", type=float, default=120.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch under torchrun (rank 0 prints the line)
+        import socket
+
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -25,6 +25,8 @@
  *   fvr_temp_lookup              radiometry.py:206-219 temp_from_green +
  *                                reconstruct.py:444-455 green_to_temp
  *   fvr_visual_hull              volume.py:272-328 compute_visual_hull
+ *   fvr_comm_* / fvr_allreduce_sum  reconstruct.py:181-226 (the per-view loop and fixed-order
+ *                                merge, sharded over GPUs)
  */
 #ifndef FVR_B200_H
 #define FVR_B200_H
@@ -361,6 +363,28 @@ int fvr_pack_correction(const int64_t* accum, const int32_t* kp_index, int64_t n
                         int64_t* packed, void* stream);
 int fvr_unpack_correction(const int64_t* packed, const int32_t* kp_index, int64_t n_kp,
                           int64_t* accum, void* stream);
+
+/* ---- the per-iteration collective ------------------
+ * Replaces the per-view loop + fixed-order merge of adjust_pass
+ * (reconstruct.py:181-226; the reference itself has no distribution,
+ * SPEC.md:622): every rank back-projects its views into the packed i64
+ * correction and one all-reduce(sum) over NVLink makes the ranks' lattices
+ * identical (integer sums: exact, partition-independent).  The communicator
+ * is an ncclComm_t owned by the caller, resolved from the libnccl.so.2 the
+ * process already mapped (or FVR_NCCL_LIB); the 128-byte unique id travels
+ * through the caller's rendezvous. */
+#define FVR_COMM_ID_BYTES 128
+#define FVR_DT_INT64 0
+#define FVR_DT_FLOAT32 1
+#define FVR_DT_FLOAT64 2
+typedef void* fvr_comm_t;
+int fvr_comm_available(void); /* 1 when NCCL could be resolved */
+int fvr_comm_nccl_version(int32_t* version);
+int fvr_comm_unique_id(uint8_t* id_out /* FVR_COMM_ID_BYTES */);
+int fvr_comm_init(int32_t rank, int32_t world, const uint8_t* unique_id, int32_t device, fvr_comm_t* comm_out);
+/* in place, asynchronous on `stream`; dtype FVR_DT_* */
+int fvr_allreduce_sum(fvr_comm_t comm, void* buf, int64_t count, int32_t dtype, void* stream);
+int fvr_comm_destroy(fvr_comm_t comm);
 
 /* ---- temperature (stage 5) --------------------------------------------- */
 

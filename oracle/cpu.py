@@ -65,6 +65,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_set_threads.argtypes = [I]
         L.oracle_set_threads.restype = I
         L.oracle_get_threads.restype = I
+        L.oracle_set_skip_empty.argtypes = [I]
+        L.oracle_set_skip_empty.restype = I
         _lib = L
     return _lib
 
@@ -75,6 +77,14 @@ def set_threads(n: int) -> int:
 
 def get_threads() -> int:
     return lib().oracle_get_threads()
+
+
+def set_skip_empty(on: bool) -> bool:
+    """Exact empty-space skip in render_rays (fvr_oracle.c): samples whose
+    reads touch only non-positive key points add exactly zero, so skipping
+    them is bit-identical (tests/test_oracle_golden.py checks it).  Off by
+    default; the full-size parity tests turn it on to fit their time budget."""
+    return bool(lib().oracle_set_skip_empty(int(bool(on))))
 
 
 def _c(a, dtype):
@@ -201,9 +211,11 @@ def adjust_pass(values, inside, cams, residuals, masks, bbox, grid_origin, edge,
 
 def reconstruct_channel(src_images, cams, values, inside, masks, bbox, grid_origin, edge, *, tau,
                         sigma_a=1.0, background=0.0, scattering=False, sigma_s=0.0, scatter_dirs=32,
-                        alpha_l, alpha_d_eff, max_iters, converge_eps, n_chunks=16):
+                        alpha_l, alpha_d_eff, max_iters, converge_eps, n_chunks=16, callback=None):
     """reconstruct.py:250-334 in deterministic mode. src_images: list of (H, W)
-    f32; values: initial lattice f32. Returns (values, rmse list, converged, s/it)."""
+    f32; values: initial lattice f32. Returns (values, rmse list, converged, s/it).
+    ``callback(it, values, rmse)`` sees each iteration's rendered lattice
+    (before its adjust), as the reference's callback does (reconstruct.py:316)."""
     u0, v0, u1, v1 = bbox
     us = np.arange(u0, u1 + 1, dtype=np.float64) + 0.5
     vs = np.arange(v0, v1 + 1, dtype=np.float64) + 0.5
@@ -224,6 +236,8 @@ def reconstruct_channel(src_images, cams, values, inside, masks, bbox, grid_orig
             per_view.append(float(np.sqrt(np.mean((src - rec) ** 2))))
         rmse = float(np.mean(per_view))
         rmses.append(rmse)
+        if callback is not None:
+            callback(len(rmses), values, rmse)
         if rmse < converge_eps or (prev is not None and abs(rmse - prev) < converge_eps):
             converged = True
             break

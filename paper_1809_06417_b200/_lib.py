@@ -168,7 +168,16 @@ _SIGNATURES = {
     "fvr_hull_keypoints": (c_int, [_P, _GRID, _P, _P, _P]),
     "fvr_threshold_mask": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_double, _P, _P, _P, _P]),
     "fvr_mask_sat": (c_int, [_P, c_int32, c_int32, _P, _P]),
+    "fvr_comm_available": (c_int, []),
+    "fvr_comm_nccl_version": (c_int, [POINTER(c_int32)]),
+    "fvr_comm_unique_id": (c_int, [_P]),
+    "fvr_comm_init": (c_int, [c_int32, c_int32, _P, c_int32, POINTER(c_void_p)]),
+    "fvr_allreduce_sum": (c_int, [c_void_p, _P, c_int64, c_int32, _P]),
+    "fvr_comm_destroy": (c_int, [c_void_p]),
 }
+
+FVR_COMM_ID_BYTES = 128
+FVR_DT_INT64, FVR_DT_FLOAT32, FVR_DT_FLOAT64 = 0, 1, 2
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 

@@ -68,7 +68,60 @@ def shard_views(n_views: int, rank: int, world: int) -> tuple[int, int]:
     return begin, begin + base + (1 if rank < extra else 0)
 
 
-def exchange(comm, sq, vol, v_begin: int, v_end: int, rows_per_view: int, rank: int, group=None) -> None:
+class DeviceComm:
+    """The data-path collective behind the C ABI: an ncclComm_t owned by
+    libfvr_b200 (fvr_comm_init / fvr_allreduce_sum / fvr_comm_destroy), one per
+    process group.  torch.distributed only carries the 128-byte unique id
+    (a broadcast over the group's store-backed rendezvous)."""
+
+    _cache: dict = {}
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        t = _lib.torch()
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        uid = (ctypes.c_uint8 * _lib.FVR_COMM_ID_BYTES)()
+        if self.rank == 0:
+            _lib.call("fvr_comm_unique_id", ctypes.addressof(uid))
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                   group=group)
+        uid = (ctypes.c_uint8 * _lib.FVR_COMM_ID_BYTES).from_buffer_copy(box[0])
+        self.handle = ctypes.c_void_p()
+        _lib.call("fvr_comm_init", self.rank, self.world, ctypes.addressof(uid), t.cuda.current_device(),
+                  ctypes.byref(self.handle))
+
+    @classmethod
+    def for_group(cls, group=None) -> "DeviceComm":
+        import torch.distributed as dist
+
+        key = (id(group), dist.get_rank(group), dist.get_world_size(group))
+        if key not in cls._cache:
+            cls._cache[key] = cls(group)
+        return cls._cache[key]
+
+    def allreduce_sum_(self, buf, stream) -> None:
+        dt = {"torch.int64": _lib.FVR_DT_INT64, "torch.float32": _lib.FVR_DT_FLOAT32,
+              "torch.float64": _lib.FVR_DT_FLOAT64}[str(buf.dtype)]
+        _lib.call("fvr_allreduce_sum", self.handle, buf.data_ptr(), buf.numel(), dt, stream)
+
+
+def _collective(group=None):
+    """The exchange's transport: the library's own NCCL communicator when the
+    process group runs NCCL (the production path), torch.distributed
+    otherwise (gloo: the CPU tests and the one-GPU multi-process test, whose
+    ranks must not run kernels that wait on each other)."""
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl" and os.environ.get("FVR_TORCH_COLLECTIVE") != "1":
+        return DeviceComm.for_group(group)
+    return None
+
+
+def exchange(comm, sq, vol, v_begin: int, v_end: int, rows_per_view: int, rank: int, group=None,
+             stream=None) -> None:
     """The one collective of an iteration (§8e): all-reduce(sum) of the i64
     buffer ``comm`` = [packed correction | squared-residual partials (f64 bits)
     | volume partials (f64 bits)] across the ranks of ``group``.
@@ -78,8 +131,9 @@ def exchange(comm, sq, vol, v_begin: int, v_end: int, rows_per_view: int, rank: 
     (the rank of its view; rank 0 for the replicated volume term): all other
     ranks contribute the bit pattern of +0.0, i.e. integer 0, so the integer
     sum reproduces the owner's bits exactly.  ``sq``/``vol`` are f64 views into
-    ``comm`` (``sq`` may carry a leading channel axis); works on CUDA (NCCL)
-    and CPU (gloo) tensors alike.
+    ``comm`` (``sq`` may carry a leading channel axis).  CUDA tensors under an
+    NCCL group go through fvr_allreduce_sum on ``stream``; CPU tensors (gloo)
+    through torch.distributed.
     """
     import torch.distributed as dist
 
@@ -87,7 +141,11 @@ def exchange(comm, sq, vol, v_begin: int, v_end: int, rows_per_view: int, rank: 
     sq[..., v_end * rows_per_view:].zero_()
     if vol is not None and rank != 0:
         vol.zero_()
-    dist.all_reduce(comm, op=dist.ReduceOp.SUM, group=group)
+    dc = _collective(group) if comm.is_cuda else None
+    if dc is not None:
+        dc.allreduce_sum_(comm, _lib.stream_ptr() if stream is None else stream)
+    else:
+        dist.all_reduce(comm, op=dist.ReduceOp.SUM, group=group)
 
 
 _PINNED: dict = {}
@@ -108,8 +166,8 @@ def _pinned_ring(shape, dtype, depth):
 # of a 2x2x2 block are neighbours in memory (config 2: K-render 0.1015 ->
 # 0.0995 ms, K-adjust 0.0636 -> 0.0607, stochastic sample-plan gather 0.153 ->
 # 0.114).  FVR_KP_ORDER=lattice keeps the lattice order.
-_MORTON = os.environ.get("FVR_KP_ORDER", "morton") != "lattice"
-_MORTON_PERM = {}
+def _morton_enabled() -> bool:
+    return os.environ.get("FVR_KP_ORDER", "morton") != "lattice"
 
 
 def _morton_code(k, shape):
@@ -131,16 +189,6 @@ def _morton_order(kp, shape):
     if max(shape) > 1024:
         return kp
     return kp[t.argsort(_morton_code(kp.long(), shape))].contiguous()
-
-
-def _morton_perm(shape, dev):
-    """All lattice indices in Morton order (int32, built once per shape)."""
-    key = (tuple(shape), str(dev))
-    if key not in _MORTON_PERM:
-        t = _lib.torch()
-        n = shape[0] * shape[1] * shape[2]
-        _MORTON_PERM[key] = _morton_order(t.arange(n, dtype=t.int32, device=dev), shape)
-    return _MORTON_PERM[key]
 
 
 class ChannelLoop:
@@ -207,11 +255,9 @@ class ChannelLoop:
                 self.values[1:].copy_(self.values[0:1].expand((C - 1,) + shape))
             if kp_mask is not None:
                 kp_dev = t.from_numpy(np.ascontiguousarray(kp_mask, dtype=np.uint8)).to(dev)
-            if _MORTON:  # the lattice's Morton permutation, kept per shape
-                perm = _morton_perm(shape, dev)
-                kp_t = perm[t.nonzero(kp_dev.reshape(-1)[perm]).reshape(-1)]
-            else:
-                kp_t = t.nonzero(kp_dev.reshape(-1)).reshape(-1).to(t.int32)
+            kp_t = t.nonzero(kp_dev.reshape(-1)).reshape(-1).to(t.int32)
+            if _morton_enabled():  # only the key-point list is ordered (no lattice-sized permutation)
+                kp_t = _morton_order(kp_t, shape)
             self.n_kp = int(kp_t.numel())
             self.kp = kp_t if self.n_kp else t.zeros(1, dtype=t.int32, device=dev)
         else:
@@ -219,7 +265,7 @@ class ChannelLoop:
             kp_idx = np.flatnonzero(kp_mask.ravel()).astype(np.int32)
             self.n_kp = int(kp_idx.size)
             self.kp = t.from_numpy(kp_idx if kp_idx.size else np.zeros(1, np.int32)).to(dev)
-            if _MORTON and self.n_kp:
+            if _morton_enabled() and self.n_kp:
                 self.kp = _morton_order(self.kp, shape)
         self.accum = None  # scatter path only
 
@@ -590,7 +636,7 @@ class ChannelLoop:
         for ch in range(self.nch if self.n_kp else 0):
             _lib.call("fvr_pack_correction", self.accum[ch].data_ptr(), self.kp.data_ptr(), self.n_kp,
                       self.packed[ch].data_ptr(), stream)
-        exchange(self.comm, self.sq, self.vol, self.v_begin, self.v_end, self.bpv, self.rank)
+        exchange(self.comm, self.sq, self.vol, self.v_begin, self.v_end, self.bpv, self.rank, stream=stream)
         for ch in range(self.nch if self.n_kp else 0):
             _lib.call("fvr_unpack_correction", self.packed[ch].data_ptr(), self.kp.data_ptr(), self.n_kp,
                       self.accum[ch].data_ptr(), stream)
@@ -662,7 +708,8 @@ class ChannelLoop:
         slots = int(sizes[0]) * 32
         nnz = int(sizes[1])
         n_samples = int(sizes[2]) if self.sample_plan else 0
-        need = (8 if self.sample_plan else 6) * slots + 12 * n_samples
+        # entries + per-sample (meta: 8 B, rho: 4 B per channel slot) + the cursor
+        need = (8 if self.sample_plan else 6) * slots + (8 + 4 * self.pitch) * n_samples + 8 * self.n_kp
         if need > self.PLAN_MAX_BYTES or n_samples >= 2 ** 31:
             return False
         if not self.sample_plan and (self.v_end - self.v_begin) * self.w_bb * self.h_bb >= 1 << 24:
@@ -672,6 +719,9 @@ class ChannelLoop:
             if self.sample_plan:  # int2 (sample id, W)
                 entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
                 entries_b = None
+                sid0 = t.zeros(self.n_rays, dtype=t.int64, device=dev)
+                meta = t.empty(max(2 * n_samples, 2), dtype=t.int32, device=dev)
+                rho = t.zeros((max(n_samples, 1), self.pitch), dtype=t.float32, device=dev)
             else:  # 6 bytes: residual index (24 bits) + 24-bit weight
                 entries = t.zeros(max(slots, 2), dtype=t.int32, device=dev)
                 entries_b = t.zeros(max(slots // 2, 1), dtype=t.int32, device=dev)
@@ -681,10 +731,8 @@ class ChannelLoop:
         keep += [pc, cursor]
         stream = side.cuda_stream
         if self.sample_plan:
-            sid0 = t.zeros(self.n_rays, dtype=t.int64, device=dev)
             sid0[1:] = t.cumsum(pc["ray_samples"][:-1].long(), 0)
-            meta = t.empty(max(2 * n_samples, 2), dtype=t.int32, device=dev)
-            self.rho = t.zeros((max(n_samples, 1), self.pitch), dtype=t.float32, device=dev)
+            self.rho = rho
             keep.append(sid0)
             side.wait_stream(t.cuda.current_stream())
             _lib.call("fvr_sample_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff, pc["kp_map"].data_ptr(),
@@ -738,7 +786,7 @@ class ChannelLoop:
 
     def _allreduce_packed(self, stream):
         """All-reduce [packed | sq | vol] once the gather filled ``packed``."""
-        exchange(self.comm, self.sq, self.vol, self.v_begin, self.v_end, self.bpv, self.rank)
+        exchange(self.comm, self.sq, self.vol, self.v_begin, self.v_end, self.bpv, self.rank, stream=stream)
         return 0
 
     def stages(self):

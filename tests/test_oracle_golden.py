@@ -118,3 +118,29 @@ def test_temp_from_green_matches_reference():
     T, clamped = cpu.temp_from_green(g["entries"][:, 1], g["temps"], g["greens"])
     assert np.array_equal(T, g["T"])
     assert np.array_equal(clamped, g["clamped"])
+
+
+@pytest.mark.parametrize("fixture", ["config1.npz", "loop_scatter.npz"])
+def test_empty_space_skip_is_bit_identical(fixture):
+    """The opt-in exact skip (used by the full-size parity tests) leaves every
+    bit of the reference's loop unchanged, with and without scattering."""
+    g = load_golden(fixture)
+    cams = cameras_from(g, Camera)
+    hull = HullTags(g["hull_tags"], len(cams))
+    init = np.where(hull.key_point_mask(), np.float32(0.0), np.float32(-1.0))
+    cpu.set_skip_empty(True)
+    try:
+        vals, rmse, _, _ = cpu.reconstruct_channel(
+            [im[:, :, 1] for im in g["blanked"]], cams, init, hull.inside_voxels(), list(g["masks"]),
+            tuple(g["bbox"]), g["origin"], float(g["edge"]), tau=float(g["tau"]), scattering=bool(g["scattering"]),
+            sigma_s=float(g["sigma_s"]), alpha_l=0.006, alpha_d_eff=float(g["alpha_d_eff"]),
+            max_iters=int(g["iters"]), converge_eps=1e-12)
+        scat = cpu.render_view(cams[0], g["truth"], g["origin"], float(g["edge"]), float(g["tau"]), 1.0,
+                               np.zeros(3), scattering=True, sigma_s=0.3, scatter_dirs=32)
+    finally:
+        cpu.set_skip_empty(False)
+    assert np.array_equal(np.array(rmse), g["rmse"])
+    assert np.array_equal(vals, g["green"])
+    ref = cpu.render_view(cams[0], g["truth"], g["origin"], float(g["edge"]), float(g["tau"]), 1.0, np.zeros(3),
+                          scattering=True, sigma_s=0.3, scatter_dirs=32)
+    assert np.array_equal(scat, ref)
