@@ -198,6 +198,13 @@ class ClockSampler:
             if len(parts) >= 9:
                 self.rows.append(parts)
 
+    def wait_first(self, timeout: float = 5.0) -> None:
+        """Block until nvidia-smi delivered its first row (its start-up can
+        outlast a short timed region)."""
+        t_end = time.time() + timeout
+        while self.proc is not None and not self.rows and time.time() < t_end:
+            time.sleep(0.02)
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -284,9 +291,6 @@ def run_gpu(args):
         for _ in range(warmup):
             flush.fill_(1.0)
             one_step(new_events())
-        if sampler is not None:
-            sampler.start()
-            time.sleep(0.3)
         barrier()
         all_evs = []
         launches = 0
@@ -296,13 +300,16 @@ def run_gpu(args):
             launches += one_step(evs)
             all_evs.append(evs)
         barrier()
-        clocks = sampler.stop() if sampler is not None else None
         st = loop.read_state()
         assert st["it"] == warmup + steps and not st["done"], st
-        return loop, names, all_evs, launches, clocks, grid0, src
+        return loop, names, all_evs, launches, grid0, src
 
+    # clocks: sampled from before the first timed step to after the last
+    # e2e call (the deterministic, stochastic and e2e regions)
     sampler = ClockSampler(local)
-    loop, names, all_evs, launches, clocks, grid0, src = timed_loop(True, args.steps, args.warmup, sampler)
+    sampler.start()
+    sampler.wait_first()
+    loop, names, all_evs, launches, grid0, src = timed_loop(True, args.steps, args.warmup)
     step_ms = np.array([e[0].elapsed_time(e[-1]) for e in all_evs])
     part_ms = {n: float(np.mean([e[i].elapsed_time(e[i + 1]) for e in all_evs])) for i, n in enumerate(names)}
     total_ms = float(step_ms.sum())
@@ -315,7 +322,7 @@ def run_gpu(args):
     # (deterministic_mode=False): same workload through the stochastic path
     stoch = None
     if args.stochastic_steps > 0:
-        sl, snames, sevs, _, _, _, _ = timed_loop(False, args.stochastic_steps, args.warmup)
+        sl, snames, sevs, _, _, _ = timed_loop(False, args.stochastic_steps, args.warmup)
         s_ms = float(np.mean([e[0].elapsed_time(e[-1]) for e in sevs]))
         if world > 1:
             t = torch.tensor([s_ms], dtype=torch.float64, device=dev)
@@ -404,6 +411,8 @@ def run_gpu(args):
                "note": "reconstruct_channel() on host numpy inputs; H2D of frames/lattice/hull and D2H of the "
                        "grid + trace inside the timed call, amortised over its iterations; median of 5 calls"}
 
+    time.sleep(0.15)  # one more nvidia-smi row after the last timed region
+    clocks = sampler.stop()
     out = {
         "metric": METRIC,
         "value": its,

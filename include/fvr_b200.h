@@ -324,6 +324,12 @@ int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int6
                          double alpha_d, const int32_t* kp_map, const int64_t* ray_sid0,
                          const int32_t* row_pos, const int64_t* slice_off, int64_t* cursor,
                          int32_t* entries, int32_t* sample_meta, void* stream);
+/* The stochastic mode's G = clip(N(1, g_sigma), 0, 2) for (seed, iteration,
+ * ray, march index k) -- the counter-based replacement of the reference's
+ * rng.normal draw (reconstruct.py:191-204); the weigh pass and the ray-driven
+ * scatter evaluate exactly these values.  ray, k, out: n device elements. */
+int fvr_stochastic_g(uint64_t seed, uint32_t iteration, const uint32_t* ray, const uint32_t* k, int64_t n,
+                     double g_sigma, float* out, void* stream);
 int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, const int32_t* ray_list,
                                int32_t bbox_w, int32_t bbox_h, const float* residual, int32_t n_channels,
                                uint64_t seed, double g_sigma, int64_t ray_id_base, float* rho,

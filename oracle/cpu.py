@@ -19,7 +19,7 @@ Functions and the reference lines they follow:
   adjust_rays_chunked    _kernels.py:227-306   (C)
   render_pixels          render.py:183-217
   adjust_pass            reconstruct.py:152-227
-  reconstruct_channel    reconstruct.py:250-334 (deterministic G, no callback)
+  reconstruct_channel    reconstruct.py:250-334 (deterministic or numpy-drawn G)
   key_point_mask         volume.py:146-164
   visual_hull            volume.py:249-328
   color_temp_table       radiometry.py:48-64, 173-203
@@ -186,8 +186,11 @@ def key_point_mask(inside: np.ndarray) -> np.ndarray:
 
 
 def adjust_pass(values, inside, cams, residuals, masks, bbox, grid_origin, edge, tau, alpha_l,
-                alpha_d_eff, n_chunks=16) -> np.ndarray:
-    """Deterministic-mode adjust_pass; bbox = (u0, v0, u1, v1). Returns new values."""
+                alpha_d_eff, n_chunks=16, rng=None, g_sigma=0.1) -> np.ndarray:
+    """adjust_pass (reconstruct.py:152-227); bbox = (u0, v0, u1, v1).  With
+    ``rng`` (a numpy Generator) the stochastic G = clip(N(1, g_sigma), 0, 2)
+    is drawn view-major, row-major, front to back (reconstruct.py:191-204);
+    without it, deterministic mode.  Returns new values."""
     u0, v0, u1, v1 = bbox
     ins = np.ascontiguousarray(inside, dtype=np.uint8)
     partials = np.zeros((n_chunks,) + values.shape)
@@ -198,9 +201,16 @@ def adjust_pass(values, inside, cams, residuals, masks, bbox, grid_origin, edge,
         if rows.size == 0:
             continue
         origin, dirs = pixel_rays(cam, cols + 0.5, rows + 0.5)
-        adjust_rays_chunked(origin, dirs, np.asarray(res, np.float64)[rows, cols], np.ones(1),
-                            np.zeros(rows.size, np.int64), False, ins, grid_origin, edge, tau, alpha_l,
-                            alpha_d_eff, partials)
+        offsets = np.zeros(rows.size, np.int64)
+        g_values, use_g = np.ones(1), False
+        if rng is not None and g_sigma != 0.0:
+            counts = count_hull_samples(origin, dirs, ins, grid_origin, edge)
+            np.cumsum(counts[:-1], out=offsets[1:])
+            total = int(offsets[-1] + counts[-1])
+            g_values = np.clip(rng.normal(1.0, g_sigma, size=total), 0.0, 2.0) if total else np.ones(1)
+            use_g = True
+        adjust_rays_chunked(origin, dirs, np.asarray(res, np.float64)[rows, cols], g_values, offsets, use_g,
+                            ins, grid_origin, edge, tau, alpha_l, alpha_d_eff, partials)
     delta = np.zeros(values.shape)
     for c in range(n_chunks):
         delta += partials[c]
@@ -211,11 +221,15 @@ def adjust_pass(values, inside, cams, residuals, masks, bbox, grid_origin, edge,
 
 def reconstruct_channel(src_images, cams, values, inside, masks, bbox, grid_origin, edge, *, tau,
                         sigma_a=1.0, background=0.0, scattering=False, sigma_s=0.0, scatter_dirs=32,
-                        alpha_l, alpha_d_eff, max_iters, converge_eps, n_chunks=16, callback=None):
+                        alpha_l, alpha_d_eff, max_iters, converge_eps, n_chunks=16, callback=None,
+                        stochastic_seed=None, g_sigma=0.1):
     """reconstruct.py:250-334 in deterministic mode. src_images: list of (H, W)
     f32; values: initial lattice f32. Returns (values, rmse list, converged, s/it).
     ``callback(it, values, rmse)`` sees each iteration's rendered lattice
-    (before its adjust), as the reference's callback does (reconstruct.py:316)."""
+    (before its adjust), as the reference's callback does (reconstruct.py:316).
+    ``stochastic_seed``: the reference's default mode, G drawn from
+    np.random.default_rng(seed) (reconstruct.py:296)."""
+    rng = None if stochastic_seed is None else np.random.default_rng(stochastic_seed)
     u0, v0, u1, v1 = bbox
     us = np.arange(u0, u1 + 1, dtype=np.float64) + 0.5
     vs = np.arange(v0, v1 + 1, dtype=np.float64) + 0.5
@@ -248,7 +262,7 @@ def reconstruct_channel(src_images, cams, values, inside, masks, bbox, grid_orig
             f[v0:v1 + 1, u0:u1 + 1] = src - rec
             residuals.append(f)
         values = adjust_pass(values, inside, cams, residuals, masks, bbox, grid_origin, edge, tau, alpha_l,
-                             alpha_d_eff, n_chunks)
+                             alpha_d_eff, n_chunks, rng=rng, g_sigma=g_sigma)
     secs = (time.perf_counter() - t0) / max(len(rmses), 1)
     return values, rmses, converged, secs
 

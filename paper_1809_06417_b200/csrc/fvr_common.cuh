@@ -186,15 +186,32 @@ __device__ __forceinline__ uint4 philox(uint4 ctr, uint2 key) {
     return ctr;
 }
 
-// G = clip(N(1, sigma), 0, 2) for (seed, iteration, ray, sample).
+// G = clip(N(1, sigma), 0, 2) for (seed, iteration, ray, march index k).
+// One Philox4x32-10 block keyed (k >> 2, ray, iteration) feeds the four
+// samples of a group: words (x, y) and (z, w) are two Box-Muller pairs, and
+// each pair yields both R cos(2 pi u2) and R sin(2 pi u2), so consecutive
+// samples of a ray share one Philox evaluation and one log/sqrt/sincos per
+// pair (the weigh pass reuses them, gauss_weight evaluates one sample).
+__device__ __forceinline__ uint4 gauss_block(uint64_t seed, uint32_t iteration, uint32_t ray, uint32_t group) {
+    return philox(make_uint4(group, ray, iteration, 0x46565242u), make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+}
+// the Box-Muller pair (z_cos, z_sin) of words (a, b)
+__device__ __forceinline__ float2 gauss_pair(uint32_t a, uint32_t b) {
+    const float u1 = ((a >> 8) + 1) * (1.0f / 16777216.0f);  // (0, 1]
+    const float u2 = (b >> 8) * (1.0f / 16777216.0f);
+    const float r = sqrtf(-2.0f * __logf(u1));
+    float s, c;
+    sincospif(2.0f * u2, &s, &c);
+    return make_float2(r * c, r * s);
+}
+__device__ __forceinline__ float gauss_clip(float z, float sigma) {
+    return fminf(fmaxf(fmaf(sigma, z, 1.0f), 0.0f), 2.0f);
+}
 __device__ __forceinline__ float gauss_weight(uint64_t seed, uint32_t iteration, uint32_t ray,
                                               uint32_t k, float sigma) {
-    const uint4 r = philox(make_uint4(k, ray, iteration, 0x46565242u),
-                           make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
-    const float u1 = ((r.x >> 8) + 1) * (1.0f / 16777216.0f);  // (0, 1]
-    const float u2 = (r.y >> 8) * (1.0f / 16777216.0f);
-    const float z = sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
-    return fminf(fmaxf(fmaf(sigma, z, 1.0f), 0.0f), 2.0f);
+    const uint4 r = gauss_block(seed, iteration, ray, k >> 2);
+    const float2 z = (k & 2) ? gauss_pair(r.z, r.w) : gauss_pair(r.x, r.y);
+    return gauss_clip((k & 1) ? z.y : z.x, sigma);
 }
 
 __device__ __forceinline__ long long to_fix(float x) {

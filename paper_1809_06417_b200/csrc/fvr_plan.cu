@@ -328,17 +328,85 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
     if (!any) return;
     it -= (uint32_t)it_back;
     constexpr int P = kResPitch<NCH>;
-    for (int64_t sid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sid < n_samples;
-         sid += (int64_t)gridDim.x * blockDim.x) {
-        const int2 m = meta[sid];
-        const int32_t e = __ldg(ray_list + m.x);
-        const int64_t pix = (int64_t)(e >> 24) * w * h + (e & 0xFFFFFF);
-        const float gw = gauss_weight(seed, it, (uint32_t)(ray_id_base + m.x), (uint32_t)m.y, g_sigma);
-        if (P == 1) {
-            rho[sid] = __ldg(residual + pix) * gw;
+    // kWs consecutive samples per thread (one 64-byte meta read, one
+    // 32-byte rho store): samples of one ray are consecutive, so a thread
+    // reuses the ray's residual, the Philox block of a 4-sample group and the
+    // Box-Muller pair of 2 samples (gauss_weight's values, bit for bit)
+    constexpr int kWs = 8;
+    const int64_t n_groups = (n_samples + kWs - 1) / kWs;
+    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < n_groups;
+         gi += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s0 = gi * kWs;
+        int2 m[kWs];
+        if (s0 + kWs <= n_samples) {
+            const int4* q = reinterpret_cast<const int4*>(meta + s0);
+#pragma unroll
+            for (int i = 0; i < kWs / 2; ++i) {
+                const int4 v = __ldcs(q + i);
+                m[2 * i] = make_int2(v.x, v.y);
+                m[2 * i + 1] = make_int2(v.z, v.w);
+            }
         } else {
-            const float4 r = __ldg(reinterpret_cast<const float4*>(residual) + pix);
-            reinterpret_cast<float4*>(rho)[sid] = make_float4(r.x * gw, r.y * gw, r.z * gw, 0.f);
+#pragma unroll
+            for (int i = 0; i < kWs; ++i) m[i] = s0 + i < n_samples ? meta[s0 + i] : make_int2(-1, 0);
+        }
+        int ray = -1, block_key = -1, pair_key = -1;
+        float4 res = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint4 blk = make_uint4(0u, 0u, 0u, 0u);
+        float2 z = make_float2(0.f, 0.f);
+        float out[kWs][P == 1 ? 1 : 4];
+#pragma unroll
+        for (int i = 0; i < kWs; ++i) {
+            if (m[i].x < 0) {
+#pragma unroll
+                for (int c = 0; c < (P == 1 ? 1 : 4); ++c) out[i][c] = 0.f;
+                continue;
+            }
+            if (m[i].x != ray) {
+                ray = m[i].x;
+                block_key = pair_key = -1;
+                const int32_t e = __ldg(ray_list + ray);
+                const int64_t pix = (int64_t)(e >> 24) * w * h + (e & 0xFFFFFF);
+                if (P == 1)
+                    res.x = __ldg(residual + pix);
+                else
+                    res = __ldg(reinterpret_cast<const float4*>(residual) + pix);
+            }
+            const int k = m[i].y;
+            if ((k >> 2) != block_key) {
+                block_key = k >> 2;
+                pair_key = -1;
+                blk = gauss_block(seed, it, (uint32_t)(ray_id_base + ray), (uint32_t)block_key);
+            }
+            if ((k >> 1) != pair_key) {
+                pair_key = k >> 1;
+                z = (k & 2) ? gauss_pair(blk.z, blk.w) : gauss_pair(blk.x, blk.y);
+            }
+            const float gw = gauss_clip((k & 1) ? z.y : z.x, g_sigma);
+            out[i][0] = res.x * gw;
+            if (P != 1) {
+                out[i][1] = res.y * gw;
+                out[i][2] = res.z * gw;
+                out[i][3] = 0.f;
+            }
+        }
+        if (s0 + kWs <= n_samples) {
+            if (P == 1) {
+                float4* d = reinterpret_cast<float4*>(rho + s0);
+                __stcs(d, make_float4(out[0][0], out[1][0], out[2][0], out[3][0]));
+                __stcs(d + 1, make_float4(out[4][0], out[5][0], out[6][0], out[7][0]));
+            } else {
+                float4* d = reinterpret_cast<float4*>(rho) + s0;
+#pragma unroll
+                for (int i = 0; i < kWs; ++i) __stcs(d + i, make_float4(out[i][0], out[i][1], out[i][2], 0.f));
+            }
+        } else {
+            for (int i = 0; i < kWs && s0 + i < n_samples; ++i) {
+                if (P == 1)
+                    rho[s0 + i] = out[i][0];
+                else
+                    reinterpret_cast<float4*>(rho)[s0 + i] = make_float4(out[i][0], out[i][1], out[i][2], 0.f);
+            }
         }
     }
 }
@@ -608,6 +676,24 @@ extern "C" int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray
     FVR_TRY_END
 }
 
+__global__ void stochastic_g_kernel(uint64_t seed, uint32_t iteration, const uint32_t* __restrict__ ray,
+                                    const uint32_t* __restrict__ k, int64_t n, float sigma, float* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = gauss_weight(seed, iteration, ray[i], k[i], sigma);
+}
+
+extern "C" int fvr_stochastic_g(uint64_t seed, uint32_t iteration, const uint32_t* ray, const uint32_t* k,
+                                int64_t n, double g_sigma, float* out, void* stream) {
+    FVR_TRY_BEGIN
+    if (n <= 0) return FVR_OK;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    stochastic_g_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(seed, iteration, ray, k, n,
+                                                                            (float)g_sigma, out);
+    return check_launch("stochastic_g");
+    FVR_TRY_END
+}
+
 extern "C" int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, const int32_t* ray_list,
                                           int32_t bbox_w, int32_t bbox_h, const float* residual,
                                           int32_t n_channels, uint64_t seed, double g_sigma, int64_t ray_id_base,
@@ -616,7 +702,7 @@ extern "C" int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_
     FVR_TRY_BEGIN
     if (n_samples == 0) return FVR_OK;
     if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "1 or 3 channels");
-    int64_t blocks = (n_samples + 255) / 256;
+    int64_t blocks = ((n_samples + 7) / 8 + 255) / 256;  // 8 samples per thread
     if (blocks > 148 * 16) blocks = 148 * 16;
     const auto* meta = reinterpret_cast<const int2*>(sample_meta);
     if (n_channels == 1)

@@ -20,6 +20,8 @@ Fixtures:
   ctmap.npz        build_color_temp_map(1000, 2300, 1), CIE table,
                    temp_from_green on random / node / clamped greens
   tiny_color.npz   reconstruct_color on the reference tests' tiny_scene
+  stochastic.npz   the reference's default (random G) loop on config1's inputs:
+                   seed 0's grid + trace, mean / std of the grid over 32 seeds
 """
 
 from __future__ import annotations
@@ -231,6 +233,44 @@ def make_tiny_color(fvr, path):
     print(path, {t: res.traces[t].iterations for t in res.traces})
 
 
+def make_stochastic(fvr, path, seeds=32, iters=10):
+    """The reference's default mode (G ~ clip(N(1, 0.1), 0, 2) drawn per
+    in-hull sample from default_rng(seed), reconstruct.py:191-204, 296) on the
+    config-1 inputs: seed 0's grid and trace (pins the oracle bit for bit)
+    and the mean / std of the final grid over ``seeds`` seeds (the device's
+    counter-based stream is checked against these statistically)."""
+    from fvr.geometry import Camera
+    from fvr.imgio import Image
+    from fvr.preprocess import FlameMask, Rect
+    from fvr.reconstruct import ReconstructionConfig, reconstruct_channel
+    from fvr.volume import HullTags, VoxelGrid
+
+    g = dict(np.load(os.path.join(HERE, "config1.npz")))
+    n = int(g["n"])
+    cams = [Camera(fx=float(g["cam_fx"][i]), fy=float(g["cam_fy"][i]), cx=float(g["cam_cx"][i]),
+                   cy=float(g["cam_cy"][i]), rotation=g["cam_R"][i], translation=g["cam_t"][i],
+                   width=int(g["cam_w"][i]), height=int(g["cam_h"][i])) for i in range(len(g["cam_fx"]))]
+    hull = HullTags(g["hull_tags"], len(cams))
+    images = [Image(im.shape[1], im.shape[0], 1, im[:, :, 1:2]) for im in g["blanked"]]
+    masks = [FlameMask(m.shape[1], m.shape[0], m) for m in g["masks"]]
+    bbox = Rect(*(int(x) for x in g["bbox"]))
+    geom = VoxelGrid(n, n, n, g["origin"], float(g["edge"]))
+    rcfg = fvr.render.RenderConfig(tau=float(g["tau"]))
+    grids, traces = [], []
+    for s in range(seeds):
+        cfg = ReconstructionConfig(alpha_l=0.006, alpha_d=1.0, tau=float(g["tau"]), max_iters=iters,
+                                   converge_eps=1e-12, deterministic_mode=False, g_sigma=0.1, rng_seed=s)
+        grid, trace = reconstruct_channel(images, cams, geom, hull, cfg, render_cfg=rcfg, masks=masks, bbox=bbox,
+                                          tag="green")
+        grids.append(grid.values.astype(np.float64))
+        traces.append(trace.rmse)
+    stack = np.stack(grids)
+    np.savez_compressed(path, iters=iters, seeds=seeds, g_sigma=0.1, green_seed0=grids[0].astype(np.float32),
+                        rmse_seed0=np.array(traces[0]), rmse=np.array(traces), mean=stack.mean(0),
+                        std=stack.std(0, ddof=1))
+    print(path, "seeds", seeds, "max std", stack.std(0).max())
+
+
 def main():
     fvr = _import_reference()
     make_kernels(fvr, os.path.join(HERE, "kernels.npz"))
@@ -239,7 +279,12 @@ def main():
     make_loop(fvr, os.path.join(HERE, "config1.npz"), 32, 4, 64, 0.05, 10)
     make_loop(fvr, os.path.join(HERE, "loop_scatter.npz"), 16, 4, 48, 0.05, 5, scattering=True, sigma_s=0.1)
     make_tiny_color(fvr, os.path.join(HERE, "tiny_color.npz"))
+    make_stochastic(fvr, os.path.join(HERE, "stochastic.npz"))
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1:  # regenerate one fixture: python make_golden.py stochastic
+        getattr(sys.modules[__name__], "make_" + sys.argv[1])(_import_reference(),
+                                                                os.path.join(HERE, sys.argv[1] + ".npz"))
+    else:
+        main()

@@ -1,59 +1,126 @@
-"""Parity at BASELINE config 2's full size (128^3, 8 views of 512^2, full RTE):
-two device iterations against the CPU oracle on identical inputs, plus the
-size-independent properties of the loop."""
+"""Parity at BASELINE's full sizes against the CPU oracle on identical inputs
+(SURVEY.md §8c contract: max |gpu - ref| / max(|ref|, 1) <= 1e-4 on the
+lattice, RMSE trace to rtol 1e-6, LUT bracket indices bit-exact):
+
+* config 2 (128^3, 8 x 512^2, full RTE): the bench's own N = 50 iterations,
+  through the render plan and through the marching kernel, every iteration's
+  lattice compared (reconstruct.py:250-334);
+* config 3 (256^3, 16 x 1024^2, full RTE + black-body temperature):
+  reconstruct_temperature for 2 iterations (reconstruct.py:415-477), the green
+  lattice against the oracle and the temperatures / bracket indices
+  bit-exact against numpy's interp / searchsorted on the same greens
+  (radiometry.py:206-219);
+* config 4 (512^3, 32 x 1024^2, full RTE): 1 iteration.
+
+The oracle runs with its exact empty-space skip (pinned bit-identical by
+tests/test_oracle_golden.py), so the whole module takes a few minutes.
+profiles/r2_parity_curve_c*.json hold the per-iteration error curves from
+tools/parity_curve.py."""
 
 import numpy as np
 import pytest
 
+from tests.conftest import rel_err
+from tests.fullsize_common import device_loop, loop_cfg, oracle_loop
+
 pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def _scene(cfg_no):
+    from workloads import CONFIGS, device_scene
+
+    return device_scene(*CONFIGS[cfg_no])
 
 
 @pytest.fixture(scope="module")
-def scene(cuda_device):
-    import bench
-
-    return bench.make_scene()
+def scene2(cuda_device):
+    return _scene(2)
 
 
-def test_config2_two_iterations_match_oracle(scene):
-    import bench
+@pytest.fixture(scope="module")
+def oracle2(scene2):
+    return oracle_loop(scene2, 50)
+
+
+@pytest.mark.parametrize("mode", ["plan", "march"])
+def test_config2_fifty_iterations_match_oracle(scene2, oracle2, mode):
+    ref_final, ref_rmse, ref_seen, _ = oracle2
+    final, rmse, seen = device_loop(scene2, 50, mode)
+    assert len(rmse) == 50 and len(seen) == 50
+    np.testing.assert_allclose(rmse, ref_rmse, rtol=1e-6)
+    per_iter = [rel_err(a, b) for a, b in zip(seen, ref_seen)]
+    assert max(per_iter) <= TOL, per_iter
+    err = rel_err(final, ref_final)
+    assert err <= TOL, err
+    kp = scene2["hull"].key_point_mask()
+    assert np.all(final[~kp] == -1.0)
+
+
+def test_config2_keypoint_order_is_bit_identical(scene2, monkeypatch):
+    """Morton vs lattice numbering of the hull key points (the plans' row
+    order) gives the same bits: the fixed-point sums are order-free."""
+    a, ta, _ = device_loop(scene2, 3, "plan", record=False)
+    monkeypatch.setenv("FVR_KP_ORDER", "lattice")
+    b, tb, _ = device_loop(scene2, 3, "plan", record=False)
+    assert np.array_equal(a, b) and np.array_equal(ta, tb)
+
+
+def test_config2_loop_properties(scene2):
+    """Results are bit-reproducible and the RMSE falls."""
+    a, ta, _ = device_loop(scene2, 3, "plan", record=False)
+    b, tb, _ = device_loop(scene2, 3, "plan", record=False)
+    assert np.array_equal(a, b) and np.array_equal(ta, tb)
+    assert ta[-1] < ta[0]
+
+
+def test_config3_temperature_matches_oracle(cuda_device):
+    import torch
+
     from oracle import cpu
-    from paper_1809_06417_b200 import ReconstructionConfig, reconstruct_channel
-    from paper_1809_06417_b200.reconstruct import _init_grid
+    from paper_1809_06417_b200 import _lib, build_color_temp_map, reconstruct_temperature
 
-    sc = scene
+    sc = _scene(3)
     iters = 2
-    cfg = ReconstructionConfig(alpha_l=bench.ALPHA_L, alpha_d=1.0, tau=bench.TAU, max_iters=iters,
-                               converge_eps=1e-12, deterministic_mode=True)
-    grid, trace = reconstruct_channel(sc["images"], sc["cams"], sc["geom"], sc["hull"], cfg,
-                                      render_cfg=sc["rcfg"], masks=sc["masks"], bbox=sc["bbox"])
-    init = _init_grid(sc["geom"], sc["hull"], "green").values
-    b = sc["bbox"]
-    cpu.set_threads(0 or __import__("os").cpu_count())
-    ref, ref_rmse, _, _ = cpu.reconstruct_channel(
-        [im.data[:, :, 0] for im in sc["images"]], sc["cams"], init, sc["hull"].inside_voxels(),
-        [m.bits for m in sc["masks"]], (b.u0, b.v0, b.u1, b.v1), sc["geom"].origin, sc["geom"].edge,
-        tau=bench.TAU, scattering=True, sigma_s=bench.SIGMA_S, scatter_dirs=bench.SCAT_DIRS,
-        alpha_l=bench.ALPHA_L, alpha_d_eff=cfg.effective_alpha_d(sc["geom"]), max_iters=iters,
-        converge_eps=1e-12)
-    np.testing.assert_allclose(trace.rmse, ref_rmse, rtol=1e-6)
-    err = np.max(np.abs(grid.values.astype(np.float64) - ref) / np.maximum(np.abs(ref), 1.0))
-    assert err <= 1e-4, err
+    cmap = build_color_temp_map()
+    res = reconstruct_temperature(sc["rgb"], sc["cams"], cmap, sc["geom"], loop_cfg(sc, iters),
+                                  render_cfg=sc["rcfg"])
+    assert res.bbox == sc["bbox"]
+    assert np.array_equal(res.hull.tags, sc["hull"].tags)
+    assert res.trace.iterations == iters
+    ref_green, ref_rmse, _, _ = oracle_loop(sc, iters, record=False)
+    np.testing.assert_allclose(res.trace.rmse, ref_rmse, rtol=1e-6)
+    err = rel_err(res.green_grid.values, ref_green)
+    assert err <= TOL, err
+
+    # K-temp on the device's own greens: temperatures equal numpy's interp
+    # and bracket indices equal searchsorted on numpy's table, bit for bit
+    # (the device-built table is within 1e-13 of numpy's: test_gpu_parity)
+    temps, green = np.ascontiguousarray(cmap.temperatures), np.ascontiguousarray(cmap.green)
     kp = sc["hull"].key_point_mask()
-    assert np.all(grid.values[~kp] == -1.0)
+    g = res.green_grid.values[kp].astype(np.float64)
+    T_ref, clamped = cpu.temp_from_green(green, temps, g)
+    assert np.array_equal(res.temp_grid.values[kp], T_ref.astype(np.float32))
+    assert np.all(res.temp_grid.values[~kp] == -1.0)
+    assert res.n_clamped_low + res.n_clamped_high == int(clamped.sum())
+    dev = torch.device("cuda", 0)
+    vals = torch.from_numpy(np.ascontiguousarray(res.green_grid.values[kp])).to(dev)
+    idx = torch.empty(vals.numel(), dtype=torch.int32, device=dev)
+    out = torch.empty_like(vals)
+    d_green, d_temps = torch.from_numpy(green).to(dev), torch.from_numpy(temps).to(dev)
+    _lib.call("fvr_temp_lookup", vals.data_ptr(), None, vals.numel(), d_green.data_ptr(), d_temps.data_ptr(),
+              green.size, out.data_ptr(), idx.data_ptr(), None, _lib.stream_ptr())
+    want = cpu.bracket_index(green, g)
+    got = idx.cpu().numpy()
+    assert np.array_equal(out.cpu().numpy(), T_ref.astype(np.float32))
+    assert np.array_equal(got, want), int((got != want).sum())
 
 
-def test_config2_loop_properties(scene):
-    """Zero residual is a fixed point; results are bit-reproducible."""
-    import bench
-    from paper_1809_06417_b200 import ReconstructionConfig, reconstruct_channel
-
-    sc = scene
-    cfg = ReconstructionConfig(alpha_l=bench.ALPHA_L, alpha_d=1.0, tau=bench.TAU, max_iters=3,
-                               converge_eps=1e-12, deterministic_mode=True)
-    a, ta = reconstruct_channel(sc["images"], sc["cams"], sc["geom"], sc["hull"], cfg, render_cfg=sc["rcfg"],
-                                masks=sc["masks"], bbox=sc["bbox"])
-    b, tb = reconstruct_channel(sc["images"], sc["cams"], sc["geom"], sc["hull"], cfg, render_cfg=sc["rcfg"],
-                                masks=sc["masks"], bbox=sc["bbox"])
-    assert np.array_equal(a.values, b.values) and ta.rmse == tb.rmse
-    assert ta.rmse[-1] < ta.rmse[0]
+def test_config4_one_iteration_matches_oracle(cuda_device):
+    sc = _scene(4)
+    final, rmse, _ = device_loop(sc, 1, "plan", record=False)
+    ref_final, ref_rmse, _, _ = oracle_loop(sc, 1, record=False)
+    np.testing.assert_allclose(rmse, ref_rmse, rtol=1e-6)
+    err = rel_err(final, ref_final)
+    assert err <= TOL, err

@@ -144,3 +144,19 @@ def test_empty_space_skip_is_bit_identical(fixture):
     ref = cpu.render_view(cams[0], g["truth"], g["origin"], float(g["edge"]), float(g["tau"]), 1.0, np.zeros(3),
                           scattering=True, sigma_s=0.3, scatter_dirs=32)
     assert np.array_equal(scat, ref)
+
+
+def test_stochastic_loop_matches_reference():
+    """The reference's default mode: G drawn from default_rng(seed) per
+    in-hull sample, view-major, front to back (reconstruct.py:191-204)."""
+    g = load_golden("config1.npz")
+    s = load_golden("stochastic.npz")
+    cams = cameras_from(g, Camera)
+    hull = HullTags(g["hull_tags"], len(cams))
+    init = np.where(hull.key_point_mask(), np.float32(0.0), np.float32(-1.0))
+    vals, rmse, _, _ = cpu.reconstruct_channel(
+        [im[:, :, 1] for im in g["blanked"]], cams, init, hull.inside_voxels(), list(g["masks"]), tuple(g["bbox"]),
+        g["origin"], float(g["edge"]), tau=float(g["tau"]), alpha_l=0.006, alpha_d_eff=float(g["alpha_d_eff"]),
+        max_iters=int(s["iters"]), converge_eps=1e-12, stochastic_seed=0, g_sigma=float(s["g_sigma"]))
+    assert np.array_equal(np.array(rmse), s["rmse_seed0"])
+    assert np.array_equal(vals, s["green_seed0"])
