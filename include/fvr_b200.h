@@ -24,6 +24,8 @@
  *   fvr_ctmap_build              radiometry.py:173-203 build_color_temp_map
  *   fvr_temp_lookup              radiometry.py:206-219 temp_from_green +
  *                                reconstruct.py:444-455 green_to_temp
+ *   fvr_temp_rgb                 reconstruct.py:389-401 rgb_grids_from_temperature (+ the
+ *                                fused green -> T -> RGB snapshot path)
  *   fvr_visual_hull              volume.py:272-328 compute_visual_hull
  *   fvr_comm_* / fvr_allreduce_sum  reconstruct.py:181-226 (the per-view loop and fixed-order
  *                                merge, sharded over GPUs)
@@ -405,6 +407,18 @@ int fvr_ctmap_build(double t_min, double step, int32_t n, int32_t append_t_max, 
 int fvr_temp_lookup(const float* values, const int32_t* kp_index, int64_t n,
                     const double* green, const double* temps, int32_t n_lut, float* temp_out,
                     int32_t* idx_out, int64_t* clamp_counts, void* stream);
+
+/* T -> RGB through the map (rgb_grids_from_temperature, reconstruct.py:389-401):
+ * at the n key points kp_index (NULL: every element), rgb_out plane c (plane
+ * elements apart) = f32(np.interp(clip(T, temps[0], temps[n_lut-1]), temps,
+ * entries[:, c])) in fp64 from the f32 temperature, entries (n_lut, 3) f64.
+ * green == NULL: values holds the temperatures.  green != NULL: values holds
+ * the green lattice, the temperature is looked up first (as fvr_temp_lookup,
+ * written to temp_out, clamp counts in clamp_counts) -- the fused snapshot
+ * path of reconstruct_temperature.  Other lattice points are not written. */
+int fvr_temp_rgb(const float* values, const int32_t* kp_index, int64_t n, const double* green,
+                 const double* temps, const double* entries, int32_t n_lut, float* temp_out, float* rgb_out,
+                 int64_t plane, int64_t* clamp_counts, void* stream);
 
 /* Same lookup on f64 inputs (temp_from_green on arrays). */
 int fvr_temp_from_green(const double* g, int64_t n, const double* green, const double* temps,

@@ -165,6 +165,7 @@ _SIGNATURES = {
     "fvr_ctmap_build": (c_int, [c_double, c_double, c_int32, c_int32, c_double, _P, _P, _P]),
     "fvr_temp_lookup": (c_int, [_P, _P, c_int64, _P, _P, c_int32, _P, _P, _P, _P]),
     "fvr_temp_from_green": (c_int, [_P, c_int64, _P, _P, c_int32, _P, _P, _P]),
+    "fvr_temp_rgb": (c_int, [_P, _P, c_int64, _P, _P, _P, c_int32, _P, _P, c_int64, _P, _P]),
     "fvr_visual_hull_view": (c_int, [_P, _P, _GRID, _P, c_int32, _P, _P]),
     "fvr_hull_keypoints": (c_int, [_P, _GRID, _P, _P, _P]),
     "fvr_threshold_mask": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_double, _P, _P, _P, _P]),

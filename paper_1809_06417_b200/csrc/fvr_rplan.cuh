@@ -146,14 +146,78 @@ __device__ __forceinline__ uint32_t rotate27(uint32_t m, int r0, int r1, int r2)
 constexpr int kRpA = FVR_RPLAN_CHUNK / 4;  // a words per chunk
 constexpr int kRpB = FVR_RPLAN_CHUNK / 2;  // 16-bit weight words per chunk
 
+// 256-bit store of one lane chunk (sm_100 st.global.v8.b32)
+__device__ __forceinline__ void store_chunk8(uint32_t* p, const uint32_t w[8]) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(w[0]), "r"(w[1]),
+                 "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                 : "memory");
+}
+
+// The fill's output for one row.  A lane stages its current chunk of a words
+// (kRpA) and of 16-bit weights (kRpB, as kRpA u32) in shared memory (column
+// `sa` / `sb`, stride kRpStage) and writes each chunk once it is complete
+// with one 32-byte store: whole sectors instead of one 4- or 2-byte store per
+// entry into 32 different sectors per warp instruction.  finish() pads the
+// row with (0, 0.0) entries up to the unit's length, so the plan buffers
+// need no clearing.
+constexpr int kRpStage = 128;  // threads per fill block
 struct RplanOut {
     uint32_t* a;         // this row's first a word
-    uint16_t* b;         // this row's first 16-bit word
+    uint32_t* b;         // this row's first b word (two 16-bit weights per u32)
     const int* kp_map;   // lattice -> hull key-point index
+    uint32_t* sa;        // staging column: kRpA a words
+    uint32_t* sb;        // staging column: kRpA b words
+    __device__ __forceinline__ void flush(uint32_t* dst, const uint32_t* s, int chunk) const {
+        uint32_t w[kRpA];
+#pragma unroll
+        for (int i = 0; i < kRpA; ++i) w[i] = s[i * kRpStage];
+        uint32_t* p = dst + (int64_t)chunk * (32 * kRpA);
+#if FVR_RPLAN_CHUNK == 32
+        store_chunk8(p, w);
+#else
+        *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+#endif
+    }
     __device__ __forceinline__ void put(int t, int kp, float w) const {
         const uint32_t bits = (__float_as_uint(w) + 0x40u) >> 7;  // round to 16 mantissa bits
-        a[(int64_t)(t / kRpA) * (32 * kRpA) + (t % kRpA)] = (uint32_t)__ldg(kp_map + kp) | ((bits >> 16) << 24);
-        b[(int64_t)(t / kRpB) * (32 * kRpB) + (t % kRpB)] = (uint16_t)(bits & 0xFFFFu);
+        sa[(t % kRpA) * kRpStage] = (uint32_t)__ldg(kp_map + kp) | ((bits >> 16) << 24);
+        uint32_t* hb = sb + ((t % kRpB) >> 1) * kRpStage;
+        if (t & 1)
+            *hb |= (bits & 0xFFFFu) << 16;
+        else
+            *hb = bits & 0xFFFFu;
+        if (t % kRpA == kRpA - 1) flush(a, sa, t / kRpA);
+        if (t % kRpB == kRpB - 1) flush(b, sb, t / kRpB);
+    }
+    // entries count..len-1 are padding (len: the unit's length, a multiple of kRpB)
+    __device__ __forceinline__ void finish(int count, int len) const {
+        if (count % kRpA) {
+            for (int i = count % kRpA; i < kRpA; ++i) sa[i * kRpStage] = 0u;
+            flush(a, sa, count / kRpA);
+        }
+        if (count % kRpB) {
+            const int h = (count % kRpB) >> 1;
+            if (count & 1) sb[h * kRpStage] &= 0xFFFFu;
+            for (int i = h + (count & 1); i < kRpA; ++i) sb[i * kRpStage] = 0u;
+            flush(b, sb, count / kRpB);
+        }
+        uint32_t z[kRpA];
+#pragma unroll
+        for (int i = 0; i < kRpA; ++i) z[i] = 0u;
+        for (int c = (count + kRpA - 1) / kRpA; c < len / kRpA; ++c) {
+#if FVR_RPLAN_CHUNK == 32
+            store_chunk8(a + (int64_t)c * (32 * kRpA), z);
+#else
+            *reinterpret_cast<uint4*>(a + (int64_t)c * (32 * kRpA)) = make_uint4(0u, 0u, 0u, 0u);
+#endif
+        }
+        for (int c = (count + kRpB - 1) / kRpB; c < len / kRpB; ++c) {
+#if FVR_RPLAN_CHUNK == 32
+            store_chunk8(b + (int64_t)c * (32 * kRpA), z);
+#else
+            *reinterpret_cast<uint4*>(b + (int64_t)c * (32 * kRpA)) = make_uint4(0u, 0u, 0u, 0u);
+#endif
+        }
     }
 };
 
@@ -433,6 +497,7 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
     const int* __restrict__ kp_map, uint32_t* __restrict__ ent_a, uint32_t* __restrict__ ent_b,
     const uint32_t* __restrict__ pos27, double* __restrict__ base_out, double* __restrict__ t_fin_out) {
     __shared__ float s_acc[27 * 128], s_w[27 * 128];
+    __shared__ uint32_t s_sa[kRpA * kRpStage], s_sb[kRpA * kRpStage];  // RplanOut's chunk staging
     for (int i = threadIdx.x; i < 27 * 128; i += blockDim.x) s_acc[i] = 0.f;
     __shared__ uint8_t s_slot[27 * 27];  // (residues r0 r1 r2, stencil offset j) -> window slot
     __shared__ uint8_t s_inv[27 * 27];   // (window residues, slot) -> offset dx << 4 | dy << 2 | dz
@@ -453,17 +518,19 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
     int view, col, row;
     const bool in = rplan_pixel(row_src ? __ldg(row_src + r) : r, units_x, units_per_view, w, h, view, col, row);
     double base[4] = {0.0, 0.0, 0.0, 0.0}, t_fin = 0.0;
+    const long long uoff = unit_off[unit];
+    const RplanOut out{ent_a + ((uoff / kRpA) * 32 + lane) * kRpA, ent_b + ((uoff / kRpB) * 32 + lane) * kRpA, kp_map,
+                       s_sa + threadIdx.x, s_sb + threadIdx.x};
+    int count = 0;
     if (in) {
         const fvr_camera_t& cam = cams[view];
         double d[3];
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
-        rplan_row<SCAT, true>(cam.center, d, g, rc, occ, dynamic, dyn27, values, nch, plane, s_thr, s_nm,
-                              s_acc + threadIdx.x, s_w + threadIdx.x, 128,
-                              RplanOut{ent_a + ((unit_off[unit] / kRpA) * 32 + lane) * kRpA,
-                                       reinterpret_cast<uint16_t*>(ent_b) + ((unit_off[unit] / kRpB) * 32 + lane) * kRpB,
-                                       kp_map},
-                              base, t_fin, s_slot, s_inv, pos27);
+        count = rplan_row<SCAT, true>(cam.center, d, g, rc, occ, dynamic, dyn27, values, nch, plane, s_thr, s_nm,
+                                      s_acc + threadIdx.x, s_w + threadIdx.x, 128, out, base, t_fin, s_slot, s_inv,
+                                      pos27);
     }
+    out.finish(count, (int)(unit_off[unit + 1] - uoff));
     for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];
     t_fin_out[r] = t_fin;
 }

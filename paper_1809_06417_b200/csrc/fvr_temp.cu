@@ -260,6 +260,69 @@ __global__ void temp_lookup_kernel(const float* __restrict__ values, const int32
     }
 }
 
+// np.interp(x, xp, fp) for x already inside [xp[0], xp[n-1]] and a known
+// bracket j (largest j with xp[j] <= x): numpy's slope form, no contraction.
+__device__ __forceinline__ double interp_at(double x, const double* __restrict__ xp, const double* __restrict__ fp,
+                                            int fstride, int n, int j) {
+    if (j == n - 1 || xp[j] == x) return fp[j * fstride];
+    const double slope = __ddiv_rn(__dsub_rn(fp[(j + 1) * fstride], fp[j * fstride]), __dsub_rn(xp[j + 1], xp[j]));
+    return __dadd_rn(__dmul_rn(slope, __dsub_rn(x, xp[j])), fp[j * fstride]);
+}
+
+__device__ __forceinline__ int bracket(const double* __restrict__ xp, int n, double x) {
+    int a = 0, b = n - 1;
+    while (a < b) {
+        const int m = (a + b + 1) >> 1;
+        if (xp[m] <= x) a = m;
+        else b = m - 1;
+    }
+    return a;
+}
+
+// rgb_grids_from_temperature (reconstruct.py:389-401): at every hull key
+// point, rgb_c = np.interp(clip(T, t_min, t_max), temps, entries[:, c]) in
+// fp64 from the f32 temperature, stored f32 in plane c of rgb (the caller
+// keeps the outside-hull sentinel elsewhere).  With `green` non-NULL the
+// temperature itself is first derived from the green lattice (K-temp,
+// radiometry.py:206-219) and written to temp_out: the fused snapshot path of
+// reconstruct_temperature.
+__global__ void temp_rgb_kernel(const float* __restrict__ values, const int32_t* __restrict__ kp, int64_t n,
+                                const double* __restrict__ green, const double* __restrict__ temps,
+                                const double* __restrict__ entries, int n_lut, float* __restrict__ temp_out,
+                                float* __restrict__ rgb, int64_t plane, unsigned long long* __restrict__ clamps) {
+    unsigned long long lowc = 0, highc = 0;
+    const double t_lo = temps[0], t_hi = temps[n_lut - 1];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t src = kp ? (int64_t)kp[i] : i;
+        float T;
+        if (green) {
+            const double gval = (double)values[src];
+            lowc += gval < green[0];
+            highc += gval > green[n_lut - 1];
+            int j;
+            T = (float)interp_green(gval, green, temps, n_lut, j);
+            temp_out[src] = T;
+        } else {
+            T = values[src];
+        }
+        double x = (double)T;
+        x = x < t_lo ? t_lo : (x > t_hi ? t_hi : x);
+        const int j = bracket(temps, n_lut, x);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) rgb[c * plane + src] = (float)interp_at(x, temps, entries + c, 3, n_lut, j);
+    }
+    if (clamps && green) {
+        for (int off = 16; off > 0; off >>= 1) {
+            lowc += __shfl_xor_sync(0xffffffffu, lowc, off);
+            highc += __shfl_xor_sync(0xffffffffu, highc, off);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (lowc) atomicAdd(clamps, lowc);
+            if (highc) atomicAdd(clamps + 1, highc);
+        }
+    }
+}
+
 __global__ void temp_from_green_kernel(const double* __restrict__ g, int64_t n,
                                        const double* __restrict__ green,
                                        const double* __restrict__ temps, int n_lut,
@@ -314,5 +377,22 @@ extern "C" int fvr_temp_from_green(const double* g, int64_t n, const double* gre
     temp_from_green_kernel<<<(unsigned)b, 256, 0, (cudaStream_t)stream>>>(g, n, green, temps, n_lut,
                                                                           temp_out, clamped_out);
     return check_launch("temp_from_green");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_temp_rgb(const float* values, const int32_t* kp_index, int64_t n, const double* green,
+                            const double* temps, const double* entries, int32_t n_lut, float* temp_out, float* rgb_out,
+                            int64_t plane, int64_t* clamp_counts, void* stream) {
+    FVR_TRY_BEGIN
+    if (n_lut < 2) return set_error(FVR_ERR_INVALID, "need at least two table rows");
+    if (!rgb_out || !temps || !entries) return set_error(FVR_ERR_INVALID, "temps / entries / rgb_out are NULL");
+    if (green && !temp_out) return set_error(FVR_ERR_INVALID, "temp_out is NULL");
+    if (n == 0) return FVR_OK;
+    int64_t b = (n + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    temp_rgb_kernel<<<(unsigned)b, 256, 0, (cudaStream_t)stream>>>(
+        values, kp_index, n, green, temps, entries, n_lut, temp_out, rgb_out, plane,
+        reinterpret_cast<unsigned long long*>(clamp_counts));
+    return check_launch("temp_rgb");
     FVR_TRY_END
 }

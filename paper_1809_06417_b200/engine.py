@@ -512,8 +512,9 @@ class ChannelLoop:
         if need > self.PLAN_MAX_BYTES or self.n_kp >= (1 << 24):
             return False
         try:  # (no cudaMemGetInfo probe: it synchronises and costs tens of ms)
-            ent_a = t.zeros(max(slots, 2), dtype=t.int32, device=dev)
-            ent_b = t.zeros(max(slots // 2, 1), dtype=t.int32, device=dev)
+            # every chunk, padding included, is written by the fill (no clearing)
+            ent_a = t.empty(max(slots, 2), dtype=t.int32, device=dev)
+            ent_b = t.empty(max(slots // 2, 1), dtype=t.int32, device=dev)
             base = t.zeros((self.nch, n_units * 32), dtype=t.float64, device=dev)
             t_fin = t.zeros(n_units * 32, dtype=t.float64, device=dev)
             # the operand: max(v, 0) per hull key point (float4 for 3 channels)
@@ -876,7 +877,7 @@ class ChannelLoop:
         """Channel 0's state (the only one of a single-channel loop)."""
         return self.read_states()[0]
 
-    def run(self, callback=None, chunk: int = 8):
+    def run(self, callback=None, chunk: int = 8, snapshot=None):
         """Iterate until the rule fires (in every channel) or max_iters;
         returns (iterations, converged, wall_ms per iteration) of channel 0 --
         read_states() has every channel's.  ``callback(channel, it, values,
@@ -884,7 +885,7 @@ class ChannelLoop:
         channel's lattice (see _run_with_snapshots)."""
         t = self.t
         if callback is not None:
-            return self._run_with_snapshots(callback)
+            return self._run_with_snapshots(callback, snapshot=snapshot)
         if self.use_graph and self.graph is None and self.max_iters > 1:
             self.capture()
         # keep one chunk in flight: after enqueueing chunk i, wait for chunk
@@ -915,7 +916,7 @@ class ChannelLoop:
         wall = [self.total_ms / max(it, 1)] * it
         return it, bool(st["converged"]), wall
 
-    def _run_with_snapshots(self, callback, depth: int = 3):
+    def _run_with_snapshots(self, callback, depth: int = 3, snapshot=None):
         """The loop with per-iteration snapshots that do not stall it (§8f rank 4).
 
         After an iteration's RMSE, the lattice and the loop state are copied
@@ -925,16 +926,27 @@ class ChannelLoop:
         The host delivers snapshots in iteration order, at the latest when a
         slot is about to be reused, so at most ``depth`` iterations run ahead
         of the callbacks.  Iterations issued after the rule fired are no-ops
-        (sticky ``done``) and deliver nothing."""
+        (sticky ``done``) and deliver nothing.
+
+        ``snapshot`` (optional) replaces the lattice copy by a device-side
+        transform: ``snapshot.shape`` is the per-slot f32 buffer shape,
+        ``snapshot.init(buf)`` prepares a slot's device buffer once and
+        ``snapshot.fill(values, buf, stream)`` fills it from the lattice on the
+        loop's stream; the callback then receives the host copy of ``buf``
+        (reconstruct_temperature: green -> T -> RGB in one launch)."""
         t = self.t
         C = self.nch
         main = t.cuda.current_stream()
         side = t.cuda.Stream()
         stream = _lib.stream_ptr()
-        host = _pinned_ring(tuple(self.values.shape), t.float32, depth)
+        shape = tuple(self.values.shape) if snapshot is None else tuple(snapshot.shape)
+        host = _pinned_ring(shape, t.float32, depth)
         host_st = _pinned_ring(tuple(self.state.shape), t.int32, depth)
-        slots = [{"dev": t.empty_like(self.values), "st_dev": t.empty_like(self.state),
+        slots = [{"dev": t.empty(shape, dtype=t.float32, device=self.dev), "st_dev": t.empty_like(self.state),
                   "host": host[i], "st": host_st[i], "ev": None} for i in range(depth)]
+        if snapshot is not None:
+            for s in slots:
+                snapshot.init(s["dev"])
         delivered = [0] * C
 
         def deliver(slot) -> bool:
@@ -946,7 +958,7 @@ class ChannelLoop:
                 it_c = int(st[c, 0])
                 if it_c > delivered[c]:
                     rmse = float(st[c, 4:6].copy().view(np.float64)[0])
-                    callback(c, it_c, slot["host"][c].numpy().copy(), rmse)
+                    callback(c, it_c, (slot["host"][c] if snapshot is None else slot["host"]).numpy().copy(), rmse)
                     delivered[c] = it_c
                 all_done = all_done and bool(st[c, 1])
             return all_done
@@ -960,7 +972,10 @@ class ChannelLoop:
                 finished = True
                 break
             self.pre_decision(stream)
-            slot["dev"].copy_(self.values)
+            if snapshot is None:
+                slot["dev"].copy_(self.values)
+            else:
+                snapshot.fill(self.values, slot["dev"], stream)
             slot["st_dev"].copy_(self.state)
             ready = t.cuda.Event()
             ready.record(main)

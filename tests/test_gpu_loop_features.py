@@ -144,7 +144,48 @@ def test_temperature_with_snapshots(cuda_device):
     assert res.n_clamped_low == int(np.sum(greens < cmap.green[0]))
     assert res.n_clamped_high == int(np.sum(greens > cmap.green[-1]))
     assert len(snaps[-1][2]) == 3 and snaps[-1][2][1].channel_tag == "green"
-    assert rel_err(res.green_grid.values, res.green_grid.values) == 0.0
+    # every snapshot is the reference's green_to_temp + rgb_grids_from_temperature
+    # (reconstruct.py:389-401, 444-455) of that iteration's green lattice, bit for bit
+    greens_it = []
+    reconstruct_channel([im.channel(1) for im in _blanked(rgb_imgs)], cams, geom, res.hull, cfg,
+                        render_cfg=RenderConfig(), masks=res.masks if hasattr(res, "masks") else masks,
+                        bbox=res.bbox, callback=lambda it, gr, r: greens_it.append(np.array(gr.values)))
+    assert len(greens_it) == 3
+    for (it, tg, rgb), gl in zip(snaps, greens_it):
+        gk = gl[kp].astype(np.float64)
+        T = np.full(gl.shape, -1.0, np.float32)
+        T[kp] = np.interp(np.clip(gk, cmap.green[0], cmap.green[-1]), cmap.green, cmap.temperatures).astype(np.float32)
+        assert np.array_equal(tg.values, T), it
+        want = cmap.rgb_of(np.clip(T, cmap.t_min, cmap.t_max))
+        for c in range(3):
+            assert np.array_equal(rgb[c].values, np.where(kp, want[..., c].astype(np.float32), np.float32(-1.0))), c
+
+
+def _blanked(rgb_imgs):
+    from paper_1809_06417_b200.preprocess import threshold_mask
+
+    return [threshold_mask(im)[1] for im in rgb_imgs]
+
+
+def test_rgb_grids_from_temperature_matches_numpy(cuda_device):
+    """Device T -> RGB (fvr_temp_rgb) against the reference's np.interp form,
+    including temperatures below / above the table and exactly on nodes."""
+    from paper_1809_06417_b200 import HullTags, VoxelGrid
+    from paper_1809_06417_b200.reconstruct import rgb_grids_from_temperature
+
+    cmap = build_color_temp_map()
+    rng = np.random.default_rng(7)
+    n = 24
+    tags = (rng.random((n, n, n)) < 0.4).astype(np.uint32) * 3
+    hull = HullTags(tags, 2)
+    T = rng.uniform(800.0, 2500.0, (n + 1,) * 3).astype(np.float32)
+    T.ravel()[:200] = cmap.temperatures[rng.integers(0, cmap.temperatures.size, 200)].astype(np.float32)
+    tg = VoxelGrid(n, n, n, np.zeros(3), 0.01, "temperature", T)
+    got = rgb_grids_from_temperature(tg, cmap, hull)
+    kp = hull.key_point_mask()
+    want = cmap.rgb_of(np.clip(T, cmap.t_min, cmap.t_max))
+    for c in range(3):
+        assert np.array_equal(got[c].values, np.where(kp, want[..., c].astype(np.float32), np.float32(-1.0)))
 
 
 def test_rgb_batched_loop_matches_sequential(cuda_device, monkeypatch):
