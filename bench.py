@@ -250,9 +250,18 @@ def run_gpu(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FVR_BENCH_ONE_GPU=1 (tests only): every rank on cuda:0 over gloo, to
+    # exercise the multi-rank plumbing on one GPU (NCCL ranks sharing a GPU
+    # would wait on each other inside kernels)
+    one_gpu = os.environ.get("FVR_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     sc = make_scene()
     dev = torch.device("cuda", local)

@@ -253,6 +253,22 @@ def device():
     return t.device("cuda", t.cuda.current_device())
 
 
+class nvtx:
+    """NVTX range around a host-side stage (the C-ABI entry points carry their
+    own ranges); a no-op cost when no profiler is attached."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        torch().cuda.nvtx.range_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        torch().cuda.nvtx.range_pop()
+        return False
+
+
 def stream_ptr() -> int:
     return torch().cuda.current_stream().cuda_stream
 

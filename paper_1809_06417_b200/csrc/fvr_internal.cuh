@@ -3,6 +3,8 @@
 // and the render constants block passed by value to the kernels.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <atomic>
 #include <cstdio>
 #include <stdexcept>
@@ -115,7 +117,20 @@ __device__ __forceinline__ void finalize_block(const double* sq, int n_views, in
 
 }  // namespace fvr
 
-#define FVR_TRY_BEGIN try {
+namespace fvr {
+// Every C-ABI entry point is an NVTX range named after it (NVTX v3 is
+// header-only: without an attached tool a range costs a pointer check).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace fvr
+
+#define FVR_TRY_BEGIN \
+    try {             \
+        ::fvr::NvtxRange fvr_nvtx_range_(__func__);
 #define FVR_TRY_END                                                   \
     }                                                                 \
     catch (const std::exception& e) {                                 \

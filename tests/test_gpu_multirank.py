@@ -157,3 +157,25 @@ def test_nccl_comm_single_rank(cuda_device):
     one_vals, one_rmse = _loop("config1.npz", True, 10)
     assert np.array_equal(vals, one_vals)
     assert list(rmse) == list(one_rmse)
+
+
+def test_bench_two_ranks_plumbing(cuda_device):
+    """bench.py --gpus 2 relaunches itself under torchrun, shards the views,
+    times max-over-ranks and prints ONE line from rank 0 (ranks on cuda:0 over
+    gloo here: FVR_BENCH_ONE_GPU; the driver's multi-GPU run uses NCCL)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FVR_BENCH_ONE_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup",
+                          "3", "--e2e-iters", "4", "--stochastic-steps", "2", "--no-cpu-baseline"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["value"] > 0 and rec["config"]["parallelism"] == "view-sharded x2"
+    assert rec["e2e"]["value"] > 0 and rec["stochastic"]["value"] > 0
