@@ -309,10 +309,14 @@ int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int6
                          void* stream);
 /* Stochastic mode (random G, reconstruct.py:193-201): the sample plan.
  * Count: per-row entry counts (8 per in-hull sample) and per-ray in-hull
- * sample counts.  Fill (ray_sid0 = exclusive scan of ray_samples): entries
- * (sample id, W) unmerged, sample_meta[sid] = (ray index, march index k).
- * Per iteration fvr_loop_weighted_residual writes rho[sid] = residual[ray] *
- * G(seed, iteration, ray_id_base + ray, k) -- the Philox stream of
+ * sample slots.  Sample ids come in blocks of 4 slots, one block per (ray,
+ * k >> 2) group holding in-hull samples; sample (ray, k) has id 4 * block +
+ * (k & 3), so ray_samples[r] = 4 * (groups of ray r).  Fill (ray_sid0 =
+ * exclusive scan of ray_samples): entries (sample id, W) unmerged,
+ * sample_meta[block] = (ray index, group << 4 | mask of used slots).
+ * Per iteration fvr_loop_weighted_residual (n_samples = total slots) writes
+ * rho[sid] = residual[ray] * G(seed, iteration, ray_id_base + ray, k) -- one
+ * Philox block per 4-slot block, the stream of
  * fvr_loop_adjust -- and fvr_loop_gather runs over the sample plan with rho
  * in place of the residual.  state_advanced = 1 when the iteration's finalize
  * has already run (fused into fvr_rplan_render): the key is then it - 1. */

@@ -254,23 +254,32 @@ __global__ void __launch_bounds__(128) plan_fill_kernel(
 // flat kernel writes rho[sid] = res[ray] * G(seed, it, ray, k) with the same
 // Philox key as the ray-driven scatter (fvr_adjust.cu), and the gather above
 // runs over the plan with rho in place of the residual.
+// Sample ids are laid out in blocks of 4 slots, one block per (ray, k >> 2)
+// group with in-hull samples: sample (ray, k) has id 4 * block + (k & 3).  The
+// 4 draws of a block come from one Philox block (gauss_block), so the weigh
+// pass is one uniform thread per block (no divergence between lanes whose
+// samples start a new group at different places); empty slots are never
+// referenced by the plan.  ray_slots[r] = 4 * (groups of ray r).
 __global__ void __launch_bounds__(128) splan_count_kernel(
     const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
     int u0, int v0, int w, int h, const uint8_t* __restrict__ inside, Geom g,
-    const int32_t* __restrict__ kp_map, int32_t* __restrict__ counts, int32_t* __restrict__ ray_samples) {
+    const int32_t* __restrict__ kp_map, int32_t* __restrict__ counts, int32_t* __restrict__ ray_slots) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_rays) return;
     PlanRay pr;
     plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
-    int ns = 0;
-    visit_inhull(pr.o, pr.d, g, inside, 1.0, [&](int, const double*, const int* c, double) {
+    int groups = 0, prev = -1;
+    visit_inhull(pr.o, pr.d, g, inside, 1.0, [&](int k, const double*, const int* c, double) {
         const int base_kp = c[0] * g.sx + c[1] * g.sy + c[2];
 #pragma unroll
         for (int k8 = 0; k8 < 8; ++k8)
             atomicAdd(counts + kp_map[base_kp + (k8 >> 2) * g.sx + ((k8 >> 1) & 1) * g.sy + (k8 & 1)], 1);
-        ++ns;
+        if ((k >> 2) != prev) {
+            prev = k >> 2;
+            ++groups;
+        }
     });
-    ray_samples[r] = ns;
+    ray_slots[r] = 4 * groups;
 }
 
 __global__ void __launch_bounds__(128) splan_fill_kernel(
@@ -282,10 +291,18 @@ __global__ void __launch_bounds__(128) splan_fill_kernel(
     if (r >= n_rays) return;
     PlanRay pr;
     plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
-    long long sid = ray_sid0[r];
+    long long blk = ray_sid0[r] / 4 - 1;  // block of the current group
+    int prev = -1, mask = 0;
     const float edge = (float)g.edge;
     visit_inhull(pr.o, pr.d, g, inside, tau_keep, [&](int k, const double* q, const int* c, double trans) {
-        meta[sid] = make_int2((int)r, k);
+        if ((k >> 2) != prev) {
+            if (prev >= 0) meta[blk] = make_int2((int)r, (prev << 4) | mask);
+            prev = k >> 2;
+            mask = 0;
+            ++blk;
+        }
+        mask |= 1 << (k & 3);
+        const long long sid = blk * 4 + (k & 3);
         float e[3][2];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
@@ -305,13 +322,13 @@ __global__ void __launch_bounds__(128) splan_fill_kernel(
             kp[k8] = base_kp + cx * g.sx + cy * g.sy + cz;
         }
         sm.put8_batch(kp, wgt, kp_map, (int)sid, entries);
-        ++sid;
     });
+    if (prev >= 0) meta[blk] = make_int2((int)r, (prev << 4) | mask);
 }
 
 template <int NCH>
 __global__ void __launch_bounds__(256) weighted_residual_kernel(
-    const int2* __restrict__ meta, int64_t n_samples, const int32_t* __restrict__ ray_list, int w, int h,
+    const int2* __restrict__ bmeta, int64_t n_blocks, const int32_t* __restrict__ ray_list, int w, int h,
     const float* __restrict__ residual, uint64_t seed, float g_sigma, int64_t ray_id_base,
     float* __restrict__ rho, const fvr_loop_state_t* __restrict__ state, int it_back) {
     // the live channels share the iteration count (a converged one stops
@@ -327,86 +344,29 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
     }
     if (!any) return;
     it -= (uint32_t)it_back;
-    constexpr int P = kResPitch<NCH>;
-    // kWs consecutive samples per thread (one 64-byte meta read, one
-    // 32-byte rho store): samples of one ray are consecutive, so a thread
-    // reuses the ray's residual, the Philox block of a 4-sample group and the
-    // Box-Muller pair of 2 samples (gauss_weight's values, bit for bit)
-    constexpr int kWs = 8;
-    const int64_t n_groups = (n_samples + kWs - 1) / kWs;
-    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < n_groups;
-         gi += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s0 = gi * kWs;
-        int2 m[kWs];
-        if (s0 + kWs <= n_samples) {
-            const int4* q = reinterpret_cast<const int4*>(meta + s0);
+    // one thread per 4-slot block (ray, group k >> 2): one Philox block and two
+    // Box-Muller pairs give the group's four G values (gauss_weight's values,
+    // bit for bit); every lane does the same work
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n_blocks;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int2 m = __ldcs(bmeta + b);
+        const int32_t e = __ldg(ray_list + m.x);
+        const int64_t pix = (int64_t)(e >> 24) * w * h + (e & 0xFFFFFF);
+        const uint4 blk = gauss_block(seed, it, (uint32_t)(ray_id_base + m.x), (uint32_t)(m.y >> 4));
+        const float2 z01 = gauss_pair(blk.x, blk.y), z23 = gauss_pair(blk.z, blk.w);
+        float gw[4] = {gauss_clip(z01.x, g_sigma), gauss_clip(z01.y, g_sigma), gauss_clip(z23.x, g_sigma),
+                       gauss_clip(z23.y, g_sigma)};
 #pragma unroll
-            for (int i = 0; i < kWs / 2; ++i) {
-                const int4 v = __ldcs(q + i);
-                m[2 * i] = make_int2(v.x, v.y);
-                m[2 * i + 1] = make_int2(v.z, v.w);
-            }
+        for (int i = 0; i < 4; ++i)
+            if (!((m.y >> i) & 1)) gw[i] = 0.f;  // empty slot (never referenced by the plan)
+        if (NCH == 1) {
+            const float r = __ldg(residual + pix);
+            __stcs(reinterpret_cast<float4*>(rho) + b, make_float4(r * gw[0], r * gw[1], r * gw[2], r * gw[3]));
         } else {
+            const float4 r = __ldg(reinterpret_cast<const float4*>(residual) + pix);
+            float4* d = reinterpret_cast<float4*>(rho) + 4 * b;
 #pragma unroll
-            for (int i = 0; i < kWs; ++i) m[i] = s0 + i < n_samples ? meta[s0 + i] : make_int2(-1, 0);
-        }
-        int ray = -1, block_key = -1, pair_key = -1;
-        float4 res = make_float4(0.f, 0.f, 0.f, 0.f);
-        uint4 blk = make_uint4(0u, 0u, 0u, 0u);
-        float2 z = make_float2(0.f, 0.f);
-        float out[kWs][P == 1 ? 1 : 4];
-#pragma unroll
-        for (int i = 0; i < kWs; ++i) {
-            if (m[i].x < 0) {
-#pragma unroll
-                for (int c = 0; c < (P == 1 ? 1 : 4); ++c) out[i][c] = 0.f;
-                continue;
-            }
-            if (m[i].x != ray) {
-                ray = m[i].x;
-                block_key = pair_key = -1;
-                const int32_t e = __ldg(ray_list + ray);
-                const int64_t pix = (int64_t)(e >> 24) * w * h + (e & 0xFFFFFF);
-                if (P == 1)
-                    res.x = __ldg(residual + pix);
-                else
-                    res = __ldg(reinterpret_cast<const float4*>(residual) + pix);
-            }
-            const int k = m[i].y;
-            if ((k >> 2) != block_key) {
-                block_key = k >> 2;
-                pair_key = -1;
-                blk = gauss_block(seed, it, (uint32_t)(ray_id_base + ray), (uint32_t)block_key);
-            }
-            if ((k >> 1) != pair_key) {
-                pair_key = k >> 1;
-                z = (k & 2) ? gauss_pair(blk.z, blk.w) : gauss_pair(blk.x, blk.y);
-            }
-            const float gw = gauss_clip((k & 1) ? z.y : z.x, g_sigma);
-            out[i][0] = res.x * gw;
-            if (P != 1) {
-                out[i][1] = res.y * gw;
-                out[i][2] = res.z * gw;
-                out[i][3] = 0.f;
-            }
-        }
-        if (s0 + kWs <= n_samples) {
-            if (P == 1) {
-                float4* d = reinterpret_cast<float4*>(rho + s0);
-                __stcs(d, make_float4(out[0][0], out[1][0], out[2][0], out[3][0]));
-                __stcs(d + 1, make_float4(out[4][0], out[5][0], out[6][0], out[7][0]));
-            } else {
-                float4* d = reinterpret_cast<float4*>(rho) + s0;
-#pragma unroll
-                for (int i = 0; i < kWs; ++i) __stcs(d + i, make_float4(out[i][0], out[i][1], out[i][2], 0.f));
-            }
-        } else {
-            for (int i = 0; i < kWs && s0 + i < n_samples; ++i) {
-                if (P == 1)
-                    rho[s0 + i] = out[i][0];
-                else
-                    reinterpret_cast<float4*>(rho)[s0 + i] = make_float4(out[i][0], out[i][1], out[i][2], 0.f);
-            }
+            for (int i = 0; i < 4; ++i) __stcs(d + i, make_float4(r.x * gw[i], r.y * gw[i], r.z * gw[i], 0.f));
         }
     }
 }
@@ -702,16 +662,18 @@ extern "C" int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_
     FVR_TRY_BEGIN
     if (n_samples == 0) return FVR_OK;
     if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "1 or 3 channels");
-    int64_t blocks = ((n_samples + 7) / 8 + 255) / 256;  // 8 samples per thread
+    if (n_samples % 4) return set_error(FVR_ERR_INVALID, "sample slots come in blocks of 4");
+    const int64_t n_blocks = n_samples / 4;
+    int64_t blocks = (n_blocks + 255) / 256;  // one thread per 4-slot block
     if (blocks > 148 * 16) blocks = 148 * 16;
     const auto* meta = reinterpret_cast<const int2*>(sample_meta);
     if (n_channels == 1)
         weighted_residual_kernel<1><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-            meta, n_samples, ray_list, bbox_w, bbox_h, residual, seed, (float)g_sigma, ray_id_base, rho, state,
+            meta, n_blocks, ray_list, bbox_w, bbox_h, residual, seed, (float)g_sigma, ray_id_base, rho, state,
             state_advanced ? 1 : 0);
     else
         weighted_residual_kernel<3><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-            meta, n_samples, ray_list, bbox_w, bbox_h, residual, seed, (float)g_sigma, ray_id_base, rho, state,
+            meta, n_blocks, ray_list, bbox_w, bbox_h, residual, seed, (float)g_sigma, ray_id_base, rho, state,
             state_advanced ? 1 : 0);
     return check_launch("loop_weighted_residual");
     FVR_TRY_END

@@ -710,7 +710,7 @@ class ChannelLoop:
         nnz = int(sizes[1])
         n_samples = int(sizes[2]) if self.sample_plan else 0
         # entries + per-sample (meta: 8 B, rho: 4 B per channel slot) + the cursor
-        need = (8 if self.sample_plan else 6) * slots + (8 + 4 * self.pitch) * n_samples + 8 * self.n_kp
+        need = (8 if self.sample_plan else 6) * slots + (2 + 4 * self.pitch) * n_samples + 8 * self.n_kp
         if need > self.PLAN_MAX_BYTES or n_samples >= 2 ** 31:
             return False
         if not self.sample_plan and (self.v_end - self.v_begin) * self.w_bb * self.h_bb >= 1 << 24:
@@ -721,7 +721,7 @@ class ChannelLoop:
                 entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
                 entries_b = None
                 sid0 = t.zeros(self.n_rays, dtype=t.int64, device=dev)
-                meta = t.empty(max(2 * n_samples, 2), dtype=t.int32, device=dev)
+                meta = t.empty(max(n_samples // 2, 2), dtype=t.int32, device=dev)  # int2 per 4-slot block
                 rho = t.zeros((max(n_samples, 1), self.pitch), dtype=t.float32, device=dev)
             else:  # 6 bytes: residual index (24 bits) + 24-bit weight
                 entries = t.zeros(max(slots, 2), dtype=t.int32, device=dev)
