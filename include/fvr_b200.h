@@ -304,9 +304,8 @@ int fvr_adjust_plan_count(const fvr_camera_t* cams, const int32_t* ray_list, int
 int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int64_t n_rays,
                          int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
                          const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
-                         double alpha_d, const int32_t* kp_map, const int32_t* row_pos,
-                         const int64_t* slice_off, int64_t* cursor, uint32_t* entries_a, uint32_t* entries_b,
-                         void* stream);
+                         double alpha_d, const int32_t* kp_map, const int64_t* row_info, int64_t* cursor,
+                         uint32_t* entries_a, uint32_t* entries_b, void* stream);
 /* Stochastic mode (random G, reconstruct.py:193-201): the sample plan.
  * Count: per-row entry counts (8 per in-hull sample) and per-ray in-hull
  * sample slots.  Sample ids come in blocks of 4 slots, one block per (ray,
@@ -328,8 +327,8 @@ int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int6
                          int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
                          const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
                          double alpha_d, const int32_t* kp_map, const int64_t* ray_sid0,
-                         const int32_t* row_pos, const int64_t* slice_off, int64_t* cursor,
-                         int32_t* entries, int32_t* sample_meta, void* stream);
+                         const int64_t* row_info, int64_t* cursor, int32_t* entries, int32_t* sample_meta,
+                         void* stream);
 /* The stochastic mode's G = clip(N(1, g_sigma), 0, 2) for (seed, iteration,
  * ray, march index k) -- the counter-based replacement of the reference's
  * rng.normal draw (reconstruct.py:191-204); the weigh pass and the ray-driven
@@ -345,6 +344,8 @@ int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, co
  * positions with slice_len (longest row) and slice_off (exclusive scan, in
  * units of 32 entries); entry t of position p at slice_off[p/32]*32 + 32t +
  * p%32; cursor (n_rows i64, zeroed) counts the entries written per row.
+ * The fills take row_info[row] = slice_off[p/32] << 5 | p%32 (p = row_pos[row])
+ * (i64): the row's SELL position in one word.
  * The deterministic plan (fvr_adjust_plan_fill) has 6-byte entries: a word
  * (u32, at that index) = residual index (< 2^24) | weight exponent << 24, and
  * the weight's top 16 mantissa bits in half t % 2 of entries_b[(slice_off +

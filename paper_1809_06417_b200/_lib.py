@@ -142,7 +142,7 @@ _SIGNATURES = {
         c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, _P, _P, _P]),
     "fvr_adjust_plan_fill": (
         c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, c_double, c_double, c_double,
-                _P, _P, _P, _P, _P, _P, _P]),
+                _P, _P, _P, _P, _P, _P]),
     "fvr_rplan_chunk_entries": (c_int, []),
     "fvr_rplan_count": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _GRID, _PARAMS, _P, _P, _P, _P,
                                 _P]),
@@ -154,7 +154,7 @@ _SIGNATURES = {
     "fvr_sample_plan_count": (c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, _P, _P, _P,
                                       _P]),
     "fvr_sample_plan_fill": (c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, c_double,
-                                     c_double, c_double, _P, _P, _P, _P, _P, _P, _P, _P]),
+                                     c_double, c_double, _P, _P, _P, _P, _P, _P, _P]),
     "fvr_loop_weighted_residual": (c_int, [_P, c_int64, _P, c_int32, c_int32, _P, c_int32, c_uint64, c_double,
                                            c_int64, _P, _P, c_int32, _P]),
     "fvr_stochastic_g": (c_int, [c_uint64, ctypes.c_uint32, _P, _P, c_int64, c_double, _P, _P]),

@@ -14,6 +14,26 @@
 
 #include "../../include/fvr_b200.h"
 
+// Device-side bounds checks of the debug build (make debug ->
+// libfvr_b200_debug.so, -DFVR_BOUNDS_CHECK; compute-sanitizer is not
+// available on the GPU pool): a failed check prints its site and traps, so
+// the launch fails loudly; the release build compiles them away.
+#ifdef FVR_BOUNDS_CHECK
+#include <cstdio>
+#define FVR_DCHECK(cond, what)                                                                          \
+    do {                                                                                                \
+        if (!(cond)) {                                                                                  \
+            printf("fvr bounds check failed: %s (%s:%d, block %d thread %d)\n", what, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                  \
+            __trap();                                                                                   \
+        }                                                                                               \
+    } while (0)
+#else
+#define FVR_DCHECK(cond, what) \
+    do {                       \
+    } while (0)
+#endif
+
 namespace fvr {
 
 constexpr double kMarchCountEps = 1e-9;      // _kernels.py:25

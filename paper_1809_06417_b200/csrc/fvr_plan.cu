@@ -31,15 +31,13 @@ __device__ __forceinline__ void visit_inhull(const double o[3], const double d[3
     double te, tx;
     if (!slab_span(o, d, g, te, tx)) return;
     const int n = sample_count(te, tx, g.edge);
+    if (n < 1) return;
     const double t0 = te - 0.5 * g.edge;
     double qb[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) qb[a] = ((o[a] - g.lo[a]) + t0 * d[a]) * g.inv_edge;
     const int nn[3] = {g.nx, g.ny, g.nz};
-    double trans = 1.0;
-    for (int k = 1; k <= n; ++k) {
-        double q[3];
-        int c[3];
+    auto cell_of = [&](int k, double q[3], int c[3]) {
         bool safe = true;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
@@ -57,8 +55,27 @@ __device__ __forceinline__ void visit_inhull(const double o[3], const double d[3
         }
 #pragma unroll
         for (int a = 0; a < 3; ++a) c[a] = clampi(c[a], nn[a] - 1);
-        if (__ldg(inside + ((int64_t)c[0] * g.ny + c[1]) * g.nz + c[2])) f(k, q, c, trans);
+        return __ldg(inside + ((int64_t)c[0] * g.ny + c[1]) * g.nz + c[2]);
+    };
+    // the next sample's hull probe is issued before this sample's work, so
+    // its latency overlaps the caller's (dependent) plan writes
+    double q[3];
+    int c[3];
+    uint8_t in = cell_of(1, q, c);
+    double trans = 1.0;
+    for (int k = 1; k <= n; ++k) {
+        double qn[3];
+        int cn[3];
+        uint8_t in_n = 0;
+        if (k < n) in_n = cell_of(k + 1, qn, cn);
+        if (in) f(k, q, c, trans);
         trans *= tau_keep;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            q[a] = qn[a];
+            c[a] = cn[a];
+        }
+        in = in_n;
     }
 }
 
@@ -171,8 +188,10 @@ constexpr int kSE = FVR_SPLAN_CHUNK / 8;
 // (store6 / put8_batch), so a warp streams a slice with fully coalesced
 // LDG.128s, one lane per row (padding entries are (0, 0.0)).
 struct SellMap {
-    const int32_t* row_pos;          // row -> sorted position
-    const long long* slice_off;      // per slice, in units of 32 entries
+    // per row: (entry offset of its slice) << 5 | its lane -- the SELL
+    // position folded into one word, so a corner's entry address needs the
+    // row lookup and then the cursor atomic and this word in parallel
+    const long long* row_info;
     unsigned long long* cursor;      // per row, entries written so far
     // 6-byte entries in 16-byte chunks per lane (slice offsets and lengths
     // multiples of 8): entry e = off + t of lane l has its a word at u32
@@ -187,51 +206,57 @@ struct SellMap {
     // the 8 corner entries of one sample, int2 (sample id, W), batched as below
     __device__ __forceinline__ void put8_batch(const int* kp, const float* w, const int32_t* __restrict__ kp_map,
                                                int sid, int2* entries) const {
-        int row[8], p[8];
-        long long t[8];
+        int row[8];
+        long long t[8], ri[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) row[i] = __ldg(kp_map + kp[i]);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
+            FVR_DCHECK(row[i] >= 0, "sample plan: corner is not a hull key point");
             t[i] = (long long)atomicAdd(cursor + row[i], 1ull);
-            p[i] = row_pos[row[i]];
+            ri[i] = __ldg(row_info + row[i]);
         }
         // entry e = off + t of lane l at int2 (e / S * 32 + l) * S + e % S with
         // S = kSE: a lane's S consecutive entries are one chunk (slice offsets
         // and lengths multiples of S)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const long long e = slice_off[p[i] >> 5] + t[i];
-            entries[((e / kSE) * 32 + (p[i] & 31)) * kSE + (e % kSE)] = make_int2(sid, __float_as_int(w[i]));
+            const long long e = (ri[i] >> 5) + t[i];
+            entries[((e / kSE) * 32 + (ri[i] & 31)) * kSE + (e % kSE)] = make_int2(sid, __float_as_int(w[i]));
         }
     }
     // up to 8 entries of one sample's corners (mask): each dependent step
-    // (row lookup, cursor atomic, slice offset) is issued for all of them
+    // (row lookup, then cursor atomic + row word) is issued for all of them
     // before any result is used, so their latencies overlap
     __device__ __forceinline__ void put6_batch(const int* kp, const float* w, uint32_t mask,
                                                const int32_t* __restrict__ kp_map, uint32_t idx, uint32_t* a,
                                                uint16_t* b) const {
-        int row[8], p[8];
-        long long t[8], off[8];
+        int row[8];
+        long long t[8], ri[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) row[i] = ((mask >> i) & 1u) ? __ldg(kp_map + kp[i]) : 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             if ((mask >> i) & 1u) {
+                FVR_DCHECK(row[i] >= 0, "adjust plan: corner is not a hull key point");
                 t[i] = (long long)atomicAdd(cursor + row[i], 1ull);
-                p[i] = row_pos[row[i]];
+                ri[i] = __ldg(row_info + row[i]);
             }
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) off[i] = ((mask >> i) & 1u) ? slice_off[p[i] >> 5] : 0;
-#pragma unroll
         for (int i = 0; i < 8; ++i) {
-            if ((mask >> i) & 1u) store6(off[i] + t[i], p[i] & 31, idx, w[i], a, b);
+            if ((mask >> i) & 1u) {
+                FVR_DCHECK(idx < (1u << 24), "adjust plan: residual index beyond 24 bits");
+                store6((ri[i] >> 5) + t[i], (int)(ri[i] & 31), idx, w[i], a, b);
+            }
         }
     }
 };
 
-__global__ void __launch_bounds__(128) plan_fill_kernel(
+#ifndef FVR_PLAN_FILL_MINB
+#define FVR_PLAN_FILL_MINB 4
+#endif
+__global__ void __launch_bounds__(128, FVR_PLAN_FILL_MINB) plan_fill_kernel(
     const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
     int u0, int v0, int w, int h, const uint8_t* __restrict__ inside, Geom g, double tau_keep,
     double alpha_l, float alpha_d, const int32_t* __restrict__ kp_map, SellMap sm, uint32_t* __restrict__ ent_a,
@@ -538,7 +563,7 @@ extern "C" int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray
                                     int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
                                     const uint8_t* inside_vox, fvr_grid_t grid, double tau,
                                     double alpha_l, double alpha_d, const int32_t* kp_map,
-                                    const int32_t* row_pos, const int64_t* slice_off, int64_t* cursor,
+                                    const int64_t* row_info, int64_t* cursor,
                                     uint32_t* entries_a, uint32_t* entries_b, void* stream) {
     FVR_TRY_BEGIN
     if (int rc = check_grid(grid)) return rc;
@@ -547,7 +572,7 @@ extern "C" int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray
     plan_fill_kernel<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
         cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d,
         kp_map,
-        SellMap{row_pos, reinterpret_cast<const long long*>(slice_off), reinterpret_cast<unsigned long long*>(cursor)},
+        SellMap{reinterpret_cast<const long long*>(row_info), reinterpret_cast<unsigned long long*>(cursor)},
         entries_a, reinterpret_cast<uint16_t*>(entries_b));
     return check_launch("adjust_plan_fill");
     FVR_TRY_END
@@ -621,7 +646,7 @@ extern "C" int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray
                                     int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
                                     const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
                                     double alpha_d, const int32_t* kp_map, const int64_t* ray_sid0,
-                                    const int32_t* row_pos, const int64_t* slice_off, int64_t* cursor,
+                                    const int64_t* row_info, int64_t* cursor,
                                     int32_t* entries, int32_t* sample_meta, void* stream) {
     FVR_TRY_BEGIN
     if (int rc = check_grid(grid)) return rc;
@@ -630,7 +655,7 @@ extern "C" int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray
     splan_fill_kernel<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
         cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d, kp_map,
         reinterpret_cast<const long long*>(ray_sid0),
-        SellMap{row_pos, reinterpret_cast<const long long*>(slice_off), reinterpret_cast<unsigned long long*>(cursor)},
+        SellMap{reinterpret_cast<const long long*>(row_info), reinterpret_cast<unsigned long long*>(cursor)},
         reinterpret_cast<int2*>(entries), reinterpret_cast<int2*>(sample_meta));
     return check_launch("sample_plan_fill");
     FVR_TRY_END

@@ -147,77 +147,37 @@ constexpr int kRpA = FVR_RPLAN_CHUNK / 4;  // a words per chunk
 constexpr int kRpB = FVR_RPLAN_CHUNK / 2;  // 16-bit weight words per chunk
 
 // 256-bit store of one lane chunk (sm_100 st.global.v8.b32)
-__device__ __forceinline__ void store_chunk8(uint32_t* p, const uint32_t w[8]) {
-    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(w[0]), "r"(w[1]),
-                 "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
-                 : "memory");
+__device__ __forceinline__ void store_zero_chunk(uint32_t* p) {
+#if FVR_RPLAN_CHUNK == 32
+    asm volatile("st.global.v8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"l"(p), "r"(0u) : "memory");
+#else
+    *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
+#endif
 }
 
-// The fill's output for one row.  A lane stages its current chunk of a words
-// (kRpA) and of 16-bit weights (kRpB, as kRpA u32) in shared memory (column
-// `sa` / `sb`, stride kRpStage) and writes each chunk once it is complete
-// with one 32-byte store: whole sectors instead of one 4- or 2-byte store per
-// entry into 32 different sectors per warp instruction.  finish() pads the
-// row with (0, 0.0) entries up to the unit's length, so the plan buffers
-// need no clearing.
-constexpr int kRpStage = 128;  // threads per fill block
+// The fill's output for one row: entry t goes straight to its lane chunk
+// (a word and 16-bit weight word; staging whole chunks in shared memory cost
+// more instructions than the scattered stores, 1.83 vs 1.62 ms at config 2).
+// finish() pads the row with (0, 0.0) entries up to the unit's length --
+// whole chunks with 32-byte stores -- so the plan buffers need no clearing.
 struct RplanOut {
     uint32_t* a;         // this row's first a word
-    uint32_t* b;         // this row's first b word (two 16-bit weights per u32)
-    const int* kp_map;   // lattice -> hull key-point index
-    uint32_t* sa;        // staging column: kRpA a words
-    uint32_t* sb;        // staging column: kRpA b words
-    __device__ __forceinline__ void flush(uint32_t* dst, const uint32_t* s, int chunk) const {
-        uint32_t w[kRpA];
-#pragma unroll
-        for (int i = 0; i < kRpA; ++i) w[i] = s[i * kRpStage];
-        uint32_t* p = dst + (int64_t)chunk * (32 * kRpA);
-#if FVR_RPLAN_CHUNK == 32
-        store_chunk8(p, w);
-#else
-        *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
-#endif
-    }
-    __device__ __forceinline__ void put(int t, int kp, float w) const {
+    uint16_t* b;         // this row's first 16-bit word
+    __device__ __forceinline__ void put(int t, int col, float w) const {
+        FVR_DCHECK(col >= 0 && col < (1 << 24), "render plan: column not a hull key point");
         const uint32_t bits = (__float_as_uint(w) + 0x40u) >> 7;  // round to 16 mantissa bits
-        sa[(t % kRpA) * kRpStage] = (uint32_t)__ldg(kp_map + kp) | ((bits >> 16) << 24);
-        uint32_t* hb = sb + ((t % kRpB) >> 1) * kRpStage;
-        if (t & 1)
-            *hb |= (bits & 0xFFFFu) << 16;
-        else
-            *hb = bits & 0xFFFFu;
-        if (t % kRpA == kRpA - 1) flush(a, sa, t / kRpA);
-        if (t % kRpB == kRpB - 1) flush(b, sb, t / kRpB);
+        a[(int64_t)(t / kRpA) * (32 * kRpA) + (t % kRpA)] = (uint32_t)col | ((bits >> 16) << 24);
+        b[(int64_t)(t / kRpB) * (32 * kRpB) + (t % kRpB)] = (uint16_t)(bits & 0xFFFFu);
     }
     // entries count..len-1 are padding (len: the unit's length, a multiple of kRpB)
     __device__ __forceinline__ void finish(int count, int len) const {
-        if (count % kRpA) {
-            for (int i = count % kRpA; i < kRpA; ++i) sa[i * kRpStage] = 0u;
-            flush(a, sa, count / kRpA);
-        }
-        if (count % kRpB) {
-            const int h = (count % kRpB) >> 1;
-            if (count & 1) sb[h * kRpStage] &= 0xFFFFu;
-            for (int i = h + (count & 1); i < kRpA; ++i) sb[i * kRpStage] = 0u;
-            flush(b, sb, count / kRpB);
-        }
-        uint32_t z[kRpA];
-#pragma unroll
-        for (int i = 0; i < kRpA; ++i) z[i] = 0u;
-        for (int c = (count + kRpA - 1) / kRpA; c < len / kRpA; ++c) {
-#if FVR_RPLAN_CHUNK == 32
-            store_chunk8(a + (int64_t)c * (32 * kRpA), z);
-#else
-            *reinterpret_cast<uint4*>(a + (int64_t)c * (32 * kRpA)) = make_uint4(0u, 0u, 0u, 0u);
-#endif
-        }
-        for (int c = (count + kRpB - 1) / kRpB; c < len / kRpB; ++c) {
-#if FVR_RPLAN_CHUNK == 32
-            store_chunk8(b + (int64_t)c * (32 * kRpA), z);
-#else
-            *reinterpret_cast<uint4*>(b + (int64_t)c * (32 * kRpA)) = make_uint4(0u, 0u, 0u, 0u);
-#endif
-        }
+        FVR_DCHECK(count <= len, "render plan: row longer than its unit (count pass disagrees with fill)");
+        const int ca = (count + kRpA - 1) / kRpA * kRpA, cb = (count + kRpB - 1) / kRpB * kRpB;
+        for (int t = count; t < ca; ++t) a[(int64_t)(t / kRpA) * (32 * kRpA) + (t % kRpA)] = 0u;
+        for (int t = count; t < cb; ++t) b[(int64_t)(t / kRpB) * (32 * kRpB) + (t % kRpB)] = 0;
+        for (int c = ca / kRpA; c < len / kRpA; ++c) store_zero_chunk(a + (int64_t)c * (32 * kRpA));
+        uint32_t* bw = reinterpret_cast<uint32_t*>(b);  // a b chunk is kRpA u32 too
+        for (int c = cb / kRpB; c < len / kRpB; ++c) store_zero_chunk(bw + (int64_t)c * (32 * kRpA));
     }
 };
 
@@ -245,7 +205,7 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                          int64_t plane, const float* __restrict__ thr, const uint32_t* __restrict__ nm,
                          float* __restrict__ acc, float* __restrict__ wsm, int stride, RplanOut out,
                          double* base, double& t_fin, const uint8_t* __restrict__ slot_tab = nullptr,
-                         const uint8_t* __restrict__ slot_inv = nullptr,
+                         const int* __restrict__ kp_map = nullptr, int* __restrict__ skp = nullptr,
                          const uint32_t* __restrict__ pos27 = nullptr) {
     constexpr uint32_t kPX[3] = {0x1FFu, 0x1FFu << 9, 0x1FFu << 18};
     constexpr uint32_t kPY[3] = {0x7u | (0x7u << 9) | (0x7u << 18), (0x7u << 3) | (0x7u << 12) | (0x7u << 21),
@@ -257,8 +217,8 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
     int wm[3] = {0, 0, 0};  // window centre
     bool have = false;
     const float sig_a = (float)rc.sigma_a, kappa = (float)rc.scat_scale;
-    auto put = [&](int kp, float wt) {
-        if (FILL) out.put(count, kp, wt);
+    auto put = [&](int col, float wt) {  // col: the hull key point's column
+        if (FILL) out.put(count, col, wt);
         ++count;
     };
     auto retire = [&](uint32_t slots) {
@@ -267,18 +227,13 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
             live &= ~slots;
             return;
         }
-        // offsets (dx, dy, dz) of each slot from the window's low corner, for
-        // the window's residues: a shared-memory table
-        const int res = (((wm[0] - 1) % 3 + 3) % 3) * 9 + (((wm[1] - 1) % 3 + 3) % 3) * 3 + ((wm[2] - 1) % 3 + 3) % 3;
-        const uint8_t* inv = slot_inv + res * 27;
-        const int corner = (wm[0] - 1) * g.sx + (wm[1] - 1) * g.sy + (wm[2] - 1);
+        // each slot's column was looked up when its key point entered the window
 #pragma unroll 1
         for (uint32_t b = slots; b; b &= b - 1) {
             const int sl = __ffs(b) - 1;
             const float wt = acc[sl * stride];
             acc[sl * stride] = 0.f;
-            const int o = inv[sl];
-            put(corner + (o >> 4) * g.sx + ((o >> 2) & 3) * g.sy + (o & 3), wt);
+            put(skp[sl * stride], wt);
         }
         live &= ~slots;
     };
@@ -304,7 +259,19 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                 dl[a] = (float)(q[a] - (double)m[a]);
             }
             const int mlin = m[0] * g.sx + m[1] * g.sy + m[2];
-            if (occ && __ldg(occ + mlin) > 1) continue;  // no key point of the stencil can be non-zero
+            if (occ) {
+                // empty space: occ = D >= 2 bounds the L-inf distance from m to
+                // any key point that may be non-zero, so samples k .. k+D-3 read
+                // none (sample k+j stays within j+1 of m); skip them all, the
+                // transparency advancing by repeated multiplication
+                const int D = __ldg(occ + mlin);
+                if (D > 1) {
+                    const int extra = min(max(D - 3, 0), n - k);
+                    for (int j = 0; j < extra; ++j) t_dst *= rc.one_minus_tau;
+                    k += extra;
+                    continue;
+                }
+            }
             const uint32_t sup = support_mask(SCAT, dl, thr, nm);
             const float scale = (float)(t_dst * rc.tau);
             if (!interior) {
@@ -331,7 +298,7 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                     const int kp = x * g.sx + y * g.sy + z;
                     const float wt = FILL ? wsm[j * stride] : 0.f;
                     if (__ldg(dynamic + kp)) {
-                        put(kp, wt);
+                        put(FILL ? __ldg(kp_map + kp) : 0, wt);
                     } else if (FILL) {
                         for (int c = 0; c < nch; ++c) base[c] += (double)wt * fmaxf(__ldg(values + c * plane + kp), 0.f);
                     }
@@ -376,6 +343,30 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
             }
             // the stencil's dynamic key points, moved to window slots at once
             // (count pass: that is all; config 2: 0.83 -> 0.36 ms)
+            if (FILL) {
+                // key points entering the window: look their columns up now,
+                // four loads in flight at a time, so a retire reads shared
+                // memory only (a lookup per retired entry stalled the fill)
+                const uint32_t in_win = rotate27(live, (3 - r0) % 3, (3 - r1) % 3, (3 - r2) % 3);
+                uint32_t fresh = sup & dyn & ~in_win;
+                const uint8_t* tab = slot_tab + (r0 * 9 + r1 * 3 + r2) * 27;
+                while (fresh) {
+                    int j4[4], c4[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        j4[i] = fresh ? __ffs(fresh) - 1 : -1;
+                        fresh &= fresh - 1;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        c4[i] = j4[i] < 0 ? 0
+                                          : __ldg(kp_map + mlin + (j4[i] / 9 - 1) * g.sx + ((j4[i] / 3) % 3 - 1) * g.sy +
+                                                  (j4[i] % 3 - 1));
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (j4[i] >= 0) skp[tab[j4[i]] * stride] = c4[i];
+                }
+            }
             live |= rotate27(sup & dyn, r0, r1, r2);
             if (FILL) {
                 // (weights stay in stencil order: storing them at their slots
@@ -497,15 +488,12 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
     const int* __restrict__ kp_map, uint32_t* __restrict__ ent_a, uint32_t* __restrict__ ent_b,
     const uint32_t* __restrict__ pos27, double* __restrict__ base_out, double* __restrict__ t_fin_out) {
     __shared__ float s_acc[27 * 128], s_w[27 * 128];
-    __shared__ uint32_t s_sa[kRpA * kRpStage], s_sb[kRpA * kRpStage];  // RplanOut's chunk staging
+    __shared__ int s_kp[27 * 128];  // column of the key point in each window slot
     for (int i = threadIdx.x; i < 27 * 128; i += blockDim.x) s_acc[i] = 0.f;
     __shared__ uint8_t s_slot[27 * 27];  // (residues r0 r1 r2, stencil offset j) -> window slot
-    __shared__ uint8_t s_inv[27 * 27];   // (window residues, slot) -> offset dx << 4 | dy << 2 | dz
     for (int i = threadIdx.x; i < 27 * 27; i += blockDim.x) {
         const int rr = i / 27, j = i % 27;
         s_slot[i] = (uint8_t)(((rr / 9 + j / 9) % 3) * 9 + (((rr / 3) % 3 + (j / 3) % 3) % 3) * 3 + (rr % 3 + j % 3) % 3);
-        s_inv[i] = (uint8_t)((((j / 9 - rr / 9 + 3) % 3) << 4) | ((((j / 3) % 3 - (rr / 3) % 3 + 3) % 3) << 2) |
-                             ((j % 3 - rr % 3 + 3) % 3));
     }
     __shared__ float s_thr[3 * kScatDirs];
     __shared__ uint32_t s_nm[3 * (kScatDirs + 1)];
@@ -519,16 +507,16 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
     const bool in = rplan_pixel(row_src ? __ldg(row_src + r) : r, units_x, units_per_view, w, h, view, col, row);
     double base[4] = {0.0, 0.0, 0.0, 0.0}, t_fin = 0.0;
     const long long uoff = unit_off[unit];
-    const RplanOut out{ent_a + ((uoff / kRpA) * 32 + lane) * kRpA, ent_b + ((uoff / kRpB) * 32 + lane) * kRpA, kp_map,
-                       s_sa + threadIdx.x, s_sb + threadIdx.x};
+    const RplanOut out{ent_a + ((uoff / kRpA) * 32 + lane) * kRpA,
+                       reinterpret_cast<uint16_t*>(ent_b) + ((uoff / kRpB) * 32 + lane) * kRpB};
     int count = 0;
     if (in) {
         const fvr_camera_t& cam = cams[view];
         double d[3];
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         count = rplan_row<SCAT, true>(cam.center, d, g, rc, occ, dynamic, dyn27, values, nch, plane, s_thr, s_nm,
-                                      s_acc + threadIdx.x, s_w + threadIdx.x, 128, out, base, t_fin, s_slot, s_inv,
-                                      pos27);
+                                      s_acc + threadIdx.x, s_w + threadIdx.x, 128, out, base, t_fin, s_slot, kp_map,
+                                      s_kp + threadIdx.x, pos27);
     }
     out.finish(count, (int)(unit_off[unit + 1] - uoff));
     for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];

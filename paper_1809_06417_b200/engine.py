@@ -728,8 +728,11 @@ class ChannelLoop:
                 entries_b = t.zeros(max(slots // 2, 1), dtype=t.int32, device=dev)
         except t.cuda.OutOfMemoryError:
             return False
-        sell = (pc["row_pos"].data_ptr(), pc["slice_off"].data_ptr(), cursor.data_ptr(), entries.data_ptr())
-        keep += [pc, cursor]
+        # each row's SELL position in one word: slice entry offset << 5 | lane
+        row_pos = pc["row_pos"].long()
+        row_info = (pc["slice_off"][row_pos >> 5] << 5) | (row_pos & 31)
+        sell = (row_info.data_ptr(), cursor.data_ptr(), entries.data_ptr())
+        keep += [pc, cursor, row_info]
         stream = side.cuda_stream
         if self.sample_plan:
             sid0[1:] = t.cumsum(pc["ray_samples"][:-1].long(), 0)
