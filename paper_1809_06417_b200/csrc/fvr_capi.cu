@@ -1,6 +1,7 @@
 // fvr_capi.cu -- error state, launch accounting and the synchronous *_host
 // variants of the operator layer (drop-in targets for a ctypes/cffi shim of
 // fvr._kernels).
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -20,6 +21,14 @@ int set_error(int code, const std::string& msg) {
 }
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FVR_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 int check_launch(const char* what) {
     count_launch(1);

@@ -40,6 +40,34 @@ inline RenderConsts make_render_consts(const fvr_render_params_t& p, const doubl
 
 int set_error(int code, const std::string& msg);
 int check_launch(const char* what);
+
+// Programmatic dependent launch (sm_90+): the loop's per-iteration kernels
+// (render plan -> weigh -> gather -> next render) are launched with
+// programmatic stream serialisation.  Each calls pdl_trigger() once running,
+// so the next one is scheduled onto SMs as this one's last CTAs retire, and
+// pdl_wait() before it touches anything its predecessor wrote: the launch
+// latency and the grid ramp-up hide under the predecessor's tail.  A kernel
+// launched this way must call pdl_wait() before dependent reads (it is a
+// no-op for a normal launch).  FVR_PDL=0 launches them normally.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 void count_launch(int n = 1);
 
 inline int check_grid(const fvr_grid_t& g) {

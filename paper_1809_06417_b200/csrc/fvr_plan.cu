@@ -356,6 +356,8 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
     const int2* __restrict__ bmeta, int64_t n_blocks, const int32_t* __restrict__ ray_list, int w, int h,
     const float* __restrict__ residual, uint64_t seed, float g_sigma, int64_t ray_id_base,
     float* __restrict__ rho, const fvr_loop_state_t* __restrict__ state, int it_back) {
+    pdl_trigger();
+    pdl_wait();  // the render's residual and state
     // the live channels share the iteration count (a converged one stops
     // counting); it_back = 1 when this iteration's finalize already ran
     uint32_t it = 0;
@@ -425,6 +427,8 @@ __global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
     const float* __restrict__ residual, const int32_t* __restrict__ kp_index,
     float* __restrict__ values, int64_t plane, float* __restrict__ layout, int layout_kind, int sy, int ny1,
     float* __restrict__ kpv, long long* __restrict__ packed, const fvr_loop_state_t* __restrict__ state) {
+    pdl_trigger();
+    pdl_wait();  // the render's residual / the weigh's rho, and the state
     bool live[NCH];
     bool any = false;
 #pragma unroll
@@ -595,10 +599,10 @@ extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_of
     const auto* so = reinterpret_cast<const long long*>(slice_off);
     const auto* en = reinterpret_cast<const int2*>(entries);
     long long* pk = reinterpret_cast<long long*>(packed);
+    cudaError_t e = cudaSuccess;
 #define FVR_GATHER(P, C, E)                                                                                  \
-    gather_kernel<P, C, E><<<(unsigned)blocks, 256, 0, st>>>(slice_len, so, row_of_pos, en, entries_b, n_kp,   \
-                                                             residual, kp_index, values, plane, layout,           \
-                                                             layout_kind, sy, ny1, kp_values, pk, state)
+    e = launch_pdl(gather_kernel<P, C, E>, (unsigned)blocks, 256, st, slice_len, so, row_of_pos, en, entries_b,  \
+                   n_kp, residual, kp_index, values, plane, layout, layout_kind, sy, ny1, kp_values, pk, state)
 #define FVR_GATHER_E(P, C)           \
     if (entries_b) FVR_GATHER(P, C, true); \
     else FVR_GATHER(P, C, false)
@@ -609,6 +613,7 @@ extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_of
     }
 #undef FVR_GATHER_E
 #undef FVR_GATHER
+    if (e != cudaSuccess) return set_error(FVR_ERR_CUDA, std::string("loop_gather: ") + cudaGetErrorString(e));
     return check_launch("loop_gather");
     FVR_TRY_END
 }
@@ -692,14 +697,16 @@ extern "C" int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_
     int64_t blocks = (n_blocks + 255) / 256;  // one thread per 4-slot block
     if (blocks > 148 * 16) blocks = 148 * 16;
     const auto* meta = reinterpret_cast<const int2*>(sample_meta);
+    cudaError_t e;
     if (n_channels == 1)
-        weighted_residual_kernel<1><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        e = launch_pdl(weighted_residual_kernel<1>, (unsigned)blocks, 256, (cudaStream_t)stream,
             meta, n_blocks, ray_list, bbox_w, bbox_h, residual, seed, (float)g_sigma, ray_id_base, rho, state,
             state_advanced ? 1 : 0);
     else
-        weighted_residual_kernel<3><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        e = launch_pdl(weighted_residual_kernel<3>, (unsigned)blocks, 256, (cudaStream_t)stream,
             meta, n_blocks, ray_list, bbox_w, bbox_h, residual, seed, (float)g_sigma, ray_id_base, rho, state,
             state_advanced ? 1 : 0);
+    if (e != cudaSuccess) return set_error(FVR_ERR_CUDA, std::string("loop_weighted_residual: ") + cudaGetErrorString(e));
     return check_launch("loop_weighted_residual");
     FVR_TRY_END
 }

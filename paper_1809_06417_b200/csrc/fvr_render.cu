@@ -1190,16 +1190,17 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
     if (blocks > 148 * 64) blocks = 148 * 64;
     cudaStream_t st = (cudaStream_t)stream;
     const auto* uo = reinterpret_cast<const long long*>(unit_off);
+    cudaError_t e;
     if (n_channels == 1)
-        rplan_render_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, entries_a, entries_b, base, t_fin,
-                                                                unit_order, row_src, n_units, units_x, upv, n_views,
-                                                                bbox_w, bbox_h, src, kp_values, rc, residual,
-                                                                sq_partials, sq_stride, state, fin);
+        e = launch_pdl(rplan_render_kernel<1>, (unsigned)blocks, 256, st, unit_len, uo, entries_a, entries_b, base, t_fin,
+                       unit_order, row_src, n_units, units_x, upv, n_views, bbox_w, bbox_h, src, kp_values, rc,
+                       residual, sq_partials, sq_stride, state, fin);
     else
-        rplan_render_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(unit_len, uo, entries_a, entries_b, base, t_fin,
+        e = launch_pdl(rplan_render_kernel<3>, (unsigned)blocks, 256, st, unit_len, uo, entries_a, entries_b, base, t_fin,
                                                                 unit_order, row_src, n_units, units_x, upv, n_views,
                                                                 bbox_w, bbox_h, src, kp_values, rc, residual,
                                                                 sq_partials, sq_stride, state, fin);
+    if (e != cudaSuccess) return set_error(FVR_ERR_CUDA, std::string("rplan_render: ") + cudaGetErrorString(e));
     return check_launch("rplan_render");
     FVR_TRY_END
 }

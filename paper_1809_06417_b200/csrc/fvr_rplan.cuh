@@ -654,6 +654,8 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
     int units_per_view, int n_views, int w, int h, const float* __restrict__ src, const float* __restrict__ kpv,
     RenderConsts rc, float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride,
     fvr_loop_state_t* __restrict__ state, RplanFinalize fin) {
+    pdl_trigger();
+    pdl_wait();  // the previous gather's operand update and state
     if (all_done<NCH>(state)) return;
     const int lane = threadIdx.x & 31;
     const int64_t rows = (int64_t)n_units * 32;
