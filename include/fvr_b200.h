@@ -377,6 +377,24 @@ int fvr_pack_correction(const int64_t* accum, const int32_t* kp_index, int64_t n
 int fvr_unpack_correction(const int64_t* packed, const int32_t* kp_index, int64_t n_kp,
                           int64_t* accum, void* stream);
 
+/* ---- loop setup: index preparation (once per reconstruct_channel) -------- */
+
+/* Morton (x, y, z) key of each of the n lattice indices kp_index (C order):
+ * the hull key points are numbered in this order (plan rows and columns). */
+int fvr_morton_keys(const int32_t* kp_index, int64_t n, fvr_grid_t grid, int64_t* keys, void* stream);
+/* SELL row order of the adjust plans: positions in windows of `window` (a
+ * power of two <= 1024), rows longest first inside a window (ties in row
+ * order); row_of_pos[pos] = row. */
+int fvr_sell_window_order(const int32_t* counts, int64_t n, int32_t window, int32_t* row_of_pos, void* stream);
+/* Render-plan row order: each tile of tile_units_x x tile_units_y units
+ * (8x4-pixel warp units of one view) deals its rows, longest first, to its
+ * slots in natural order: row_src[slot] = natural row; unit_len[unit] = the
+ * unit's longest row rounded up to `align` entries.  row_len from
+ * fvr_rplan_count. */
+int fvr_rplan_tile_rows(const int32_t* row_len, int32_t n_views, int32_t bbox_w, int32_t bbox_h,
+                        int32_t tile_units_x, int32_t tile_units_y, int32_t align, int32_t* row_src,
+                        int32_t* unit_len, void* stream);
+
 /* ---- the per-iteration collective ------------------
  * Replaces the per-view loop + fixed-order merge of adjust_pass
  * (reconstruct.py:181-226; the reference itself has no distribution,

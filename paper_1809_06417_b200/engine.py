@@ -170,25 +170,19 @@ def _morton_enabled() -> bool:
     return os.environ.get("FVR_KP_ORDER", "morton") != "lattice"
 
 
-def _morton_code(k, shape):
-    sy, sx = shape[2], shape[1] * shape[2]
-
-    def spread(v):  # 10 bits -> every third bit
-        v = (v | (v << 16)) & 0x030000FF
-        v = (v | (v << 8)) & 0x0300F00F
-        v = (v | (v << 4)) & 0x030C30C3
-        return (v | (v << 2)) & 0x09249249
-
-    return (spread(k // sx) << 2) | (spread((k // sy) % shape[1]) << 1) | spread(k % sy)
-
-
 def _morton_order(kp, shape):
-    """A list of lattice indices sorted by Morton code (kept as is beyond
-    1024 key points per axis, the code's 10 bits)."""
+    """The list of lattice indices ``kp`` (int32, device) sorted by Morton
+    (x, y, z) code: one key kernel (fvr_morton_keys) and one sort."""
     t = _lib.torch()
-    if max(shape) > 1024:
+    n = int(kp.numel())
+    if n == 0:
         return kp
-    return kp[t.argsort(_morton_code(kp.long(), shape))].contiguous()
+    keys = t.empty(n, dtype=t.int64, device=kp.device)
+    g = _lib.FvrGrid()
+    g.nx, g.ny, g.nz = shape[0] - 1, shape[1] - 1, shape[2] - 1
+    g.edge = 1.0
+    _lib.call("fvr_morton_keys", kp.data_ptr(), n, g, keys.data_ptr(), _lib.stream_ptr())
+    return kp[t.sort(keys).indices].contiguous()
 
 
 class ChannelLoop:
@@ -467,10 +461,16 @@ class ChannelLoop:
         t = self.t
         n_units = unit_len.numel()
         row_src = None
+        al = int(_lib.load().fvr_rplan_chunk_entries())  # whole lane chunks of entries (fvr_rplan.cuh)
         if row_len is not None:
             tx, ty = (int(x) for x in os.environ.get("FVR_RPLAN_TILE", "2x4").split("x"))
-            row_src, unit_len = self._rplan_row_order(row_len, n_units, tx, ty)
-        al = int(_lib.load().fvr_rplan_chunk_entries())  # whole lane chunks of entries (fvr_rplan.cuh)
+            if (32 * tx * ty) & (32 * tx * ty - 1) == 0 and 32 * tx * ty <= 1024:  # one kernel per call
+                row_src = t.empty(n_units * 32, dtype=t.int32, device=self.dev)
+                unit_len = t.empty(n_units, dtype=t.int32, device=self.dev)
+                _lib.call("fvr_rplan_tile_rows", row_len.data_ptr(), self.v_end - self.v_begin, self.w_bb, self.h_bb,
+                          tx, ty, al, row_src.data_ptr(), unit_len.data_ptr(), _lib.stream_ptr())
+            else:
+                row_src, unit_len = self._rplan_row_order(row_len, n_units, tx, ty)
         unit_len = (unit_len + al - 1) & ~(al - 1)
         off = t.zeros(n_units + 1, dtype=t.int64, device=self.dev)
         off[1:] = t.cumsum(unit_len.long(), 0)
@@ -676,6 +676,9 @@ class ChannelLoop:
         sigma = int(os.environ.get("FVR_SELL_SIGMA", "128"))
         if os.environ.get("FVR_SELL_SORT", "0") == "1":
             order = t.argsort(counts, descending=True)
+        elif 2 <= sigma <= 1024 and sigma & (sigma - 1) == 0:  # one kernel: bitonic per window
+            order = t.empty(self.n_kp, dtype=t.int32, device=dev)
+            _lib.call("fvr_sell_window_order", counts.data_ptr(), self.n_kp, sigma, order.data_ptr(), stream)
         elif sigma > 0:  # sorted within windows of sigma neighbouring rows
             pos = t.arange(self.n_kp, device=dev)
             order = t.argsort((pos // sigma) * (1 << 24) + ((1 << 24) - 1 - counts.long()))
@@ -683,7 +686,7 @@ class ChannelLoop:
             order = t.arange(self.n_kp, device=dev)
         row_of_pos = order.to(t.int32)
         row_pos = t.empty_like(row_of_pos)
-        row_pos[order] = t.arange(self.n_kp, dtype=t.int32, device=dev)
+        row_pos[order.long()] = t.arange(self.n_kp, dtype=t.int32, device=dev)
         n_slices = (self.n_kp + 31) // 32
         slice_len = t.zeros(n_slices * 32, dtype=t.int32, device=dev)
         slice_len[: self.n_kp] = counts[order]
