@@ -247,7 +247,19 @@ int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_
                    int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
                    const uint8_t* dynamic, const float* values, int32_t n_channels, const int64_t* unit_off,
                    const int32_t* unit_order, const int32_t* row_src, const int32_t* kp_map,
-                   uint32_t* entries_a, uint32_t* entries_b, double* base, double* t_fin, void* stream);
+                   uint32_t* entries_a, uint32_t* entries_b, double* base, double* t_fin, const uint32_t* pos27, void* stream);
+/* pos27[k] (lattice, u32): the stencil key points around interior key point k
+ * that are static (not in dynamic) and positive in some channel -- the only
+ * static ones a row's base needs.  fvr_rplan_fill computes it itself when its
+ * pos27 argument is NULL; computing it early (right after the count pass)
+ * keeps it off the fill's critical path. */
+int fvr_rplan_pos27(fvr_grid_t grid, const uint8_t* dynamic, const float* values, int32_t n_channels,
+                    uint32_t* pos27, void* stream);
+/* Sort keys of the render plan's unit order (units longest class first, in
+ * classes of `bucket` entries; 2x4-unit tiles inside a class): ascending keys
+ * = visiting order. */
+int fvr_rplan_unit_keys(const int32_t* unit_len, int32_t n_views, int32_t bbox_w, int32_t bbox_h, int32_t bucket,
+                        int64_t* keys, void* stream);
 int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const uint32_t* entries_a,
                      const uint32_t* entries_b, const double* base, const double* t_fin,
                      const int32_t* unit_order, const int32_t* row_src, int32_t n_views, int32_t bbox_w,

@@ -1095,12 +1095,56 @@ extern "C" int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_
     FVR_TRY_END
 }
 
+extern "C" int fvr_rplan_pos27(fvr_grid_t grid, const uint8_t* dynamic, const float* values, int32_t n_channels,
+                               uint32_t* pos27, void* stream) {
+    FVR_TRY_BEGIN
+    if (int rc = check_grid(grid)) return rc;
+    if (!dynamic || !values || !pos27) return set_error(FVR_ERR_INVALID, "dynamic / values / pos27 are NULL");
+    const int64_t n = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    rplan_pos27_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(dynamic, values, n_channels, n,
+                                                                          make_geom(grid), pos27);
+    return check_launch("rplan_pos27");
+    FVR_TRY_END
+}
+
+// Unit order of the render plan: key = (length class, descending) << 40 |
+// spatial rank (2x4-unit tiles, row-major, then the units inside a tile), so
+// one sort visits the units longest class first and neighbouring units
+// together inside a class.
+__global__ void rplan_unit_keys_kernel(const int32_t* __restrict__ unit_len, int n_units, int upv, int units_x,
+                                       int q, uint64_t* __restrict__ keys) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_units) return;
+    const int units_y = upv / units_x;
+    const int txn = (units_x + 1) / 2, tyn = (units_y + 3) / 4;
+    const int view = i / upv, u = i - view * upv;
+    const int64_t tile = ((int64_t)view * tyn + (u / units_x) / 4) * txn + (u % units_x) / 2;
+    const uint64_t spatial = (uint64_t)(tile * 8 + ((u / units_x) % 4) * 2 + (u % units_x) % 2);
+    const uint64_t cls = (uint64_t)(unit_len[i] / q);
+    keys[i] = ((0xFFFFFull - cls) << 40) | spatial;
+}
+
+extern "C" int fvr_rplan_unit_keys(const int32_t* unit_len, int32_t n_views, int32_t bbox_w, int32_t bbox_h,
+                                   int32_t bucket, int64_t* keys, void* stream) {
+    FVR_TRY_BEGIN
+    if (bucket < 1) return set_error(FVR_ERR_INVALID, "bucket must be positive");
+    const int units_x = (bbox_w + kUnitW - 1) / kUnitW, upv = fvr_loop_blocks_per_view(bbox_w, bbox_h);
+    const int n_units = upv * n_views;
+    if (n_units == 0) return FVR_OK;
+    rplan_unit_keys_kernel<<<(n_units + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        unit_len, n_units, upv, units_x, bucket, reinterpret_cast<uint64_t*>(keys));
+    return check_launch("rplan_unit_keys");
+    FVR_TRY_END
+}
+
 extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                               int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
                               const uint8_t* dynamic, const float* values, int32_t n_channels,
                               const int64_t* unit_off, const int32_t* unit_order, const int32_t* row_src,
                               const int32_t* kp_map, uint32_t* entries_a, uint32_t* entries_b, double* base,
-                              double* t_fin, void* stream) {
+                              double* t_fin, const uint32_t* pos27, void* stream) {
     FVR_TRY_BEGIN
     if (n_views < 1 || bbox_w < 1 || bbox_h < 1) return set_error(FVR_ERR_INVALID, "empty render plan");
     if (n_channels < 1 || n_channels > 4) return set_error(FVR_ERR_INVALID, "n_channels must be 1..4");
@@ -1120,7 +1164,7 @@ extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t
     if (!kp_map || !entries_a || !entries_b) return set_error(FVR_ERR_INVALID, "kp_map / entries are NULL");
     uint32_t* d27 = dyn27_scratch(grid, dynamic, st, false);
     if (!d27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
-    uint32_t* p27 = pos27_scratch(grid, dynamic, values, n_channels, st);
+    const uint32_t* p27 = pos27 ? pos27 : pos27_scratch(grid, dynamic, values, n_channels, st);
     if (!p27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
     if (m)
         rplan_fill_kernel<true><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc, occ,

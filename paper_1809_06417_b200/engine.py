@@ -304,15 +304,22 @@ class ChannelLoop:
         self._mark("layout+occupancy")
         # flame rays of the local views, row-major per view (reconstruct.py:144-149)
         # compacted on the device (host masks: the bbox crops are uploaded)
+        n_host = None
         if t.is_tensor(masks):  # (V, H, W) u8 device masks
             sub = masks[:, bbox.v0:bbox.v1 + 1, bbox.u0:bbox.u1 + 1]
         else:
             crops = np.stack([np.asarray(masks[v].bits[bbox.slices], dtype=np.uint8) for v in range(V)])
+            per_view = np.count_nonzero(crops.reshape(V, -1), axis=1)
+            n_host = int(per_view[self.v_begin:self.v_end].sum())
             sub = t.from_numpy(crops).to(dev)
         ray_base = 0
         if self.v_begin > 0:
-            ray_base = int(sub[: self.v_begin].reshape(-1).count_nonzero().item())
-        nz = t.nonzero(sub[self.v_begin:self.v_end])  # (N, 3): view, row, col -- lexicographic
+            ray_base = int(per_view[: self.v_begin].sum()) if n_host is not None else \
+                int(sub[: self.v_begin].reshape(-1).count_nonzero().item())
+        if n_host is not None:  # count known on the host: no device synchronisation
+            nz = t.nonzero_static(sub[self.v_begin:self.v_end], size=n_host)
+        else:
+            nz = t.nonzero(sub[self.v_begin:self.v_end])  # (N, 3): view, row, col -- lexicographic
         ray_list_t = ((nz[:, 0] << 24) | (nz[:, 1] * self.w_bb + nz[:, 2])).to(t.int32)
         self.n_rays = int(ray_list_t.numel())
         self.rays = ray_list_t if self.n_rays else t.zeros(1, dtype=t.int32, device=dev)
@@ -363,13 +370,19 @@ class ChannelLoop:
         host = t.stack(scalars).cpu().tolist() if scalars else []
         keep = []
         if pc is not None:
+            # the adjust plan's buffers and inputs are ready once this event
+            # fires; its fill then runs on a side stream next to the render
+            # plan's (the longer one, enqueued first on the loop's stream)
             main = t.cuda.current_stream()
             side = t.cuda.Stream()
-            self.plan = self._plan_fill(pc, host[: len(pc["sizes"])], side, keep)
-            self.sample_plan = self.plan and self.sample_plan
+            launch_adjust = self._plan_fill(pc, host[: len(pc["sizes"])], side, keep)
         if rs is not None:
             self.rplan = self._rplan_fill(rs, host[len(pc["sizes"]) if pc else 0:])
         if pc is not None:
+            self.plan = launch_adjust is not None
+            if self.plan:
+                launch_adjust()
+            self.sample_plan = self.plan and self.sample_plan
             main.wait_stream(side)
         del keep
         if self.layout_kind and not self.rplan:
@@ -453,6 +466,10 @@ class ChannelLoop:
         row_len = t.empty(n_units * 32, dtype=t.int32, device=self.dev) \
             if os.environ.get("FVR_RPLAN_TILE", "2x4") != "0" else None
         _lib.call("fvr_rplan_count", *self._rplan_geo(), unit_len.data_ptr(), _lib.ptr(row_len), _lib.stream_ptr())
+        # the fill's static-positive stencil masks, computed now (off the fill's critical path)
+        self._pos27 = t.empty(int(np.prod(self.shape)), dtype=t.int32, device=self.dev)
+        _lib.call("fvr_rplan_pos27", self.grid, self.kp_dev.data_ptr(), self.values.data_ptr(), self.nch,
+                  self._pos27.data_ptr(), _lib.stream_ptr())
         return unit_len, row_len
 
     def _rplan_scan(self, unit_len, row_len) -> dict:
@@ -488,6 +505,11 @@ class ChannelLoop:
         if buckets <= 0:
             return t.argsort(unit_len, descending=True).to(t.int32)
         q = max(1, -(-int(max_len) // buckets))
+        if n_units == (self.v_end - self.v_begin) * self.bpv:  # one key kernel + one sort
+            keys = t.empty(n_units, dtype=t.int64, device=unit_len.device)
+            _lib.call("fvr_rplan_unit_keys", unit_len.data_ptr(), self.v_end - self.v_begin, self.w_bb, self.h_bb, q,
+                      keys.data_ptr(), _lib.stream_ptr())
+            return t.sort(keys).indices.to(t.int32)
         uid = t.arange(n_units, device=unit_len.device)
         ux = (self.w_bb + 7) // 8
         uy = self.bpv // ux
@@ -526,7 +548,8 @@ class ChannelLoop:
             if os.environ.get("FVR_RPLAN_SORT", "1") == "1" else None
         _lib.call("fvr_rplan_fill", *geo, self.values.data_ptr(), self.nch, off.data_ptr(), _lib.ptr(self.rp_order),
                   _lib.ptr(self.rp_row_src), self._kp_map().data_ptr(), ent_a.data_ptr(), ent_b.data_ptr(),
-                  base.data_ptr(), t_fin.data_ptr(), stream)
+                  base.data_ptr(), t_fin.data_ptr(), _lib.ptr(getattr(self, "_pos27", None)), stream)
+        self._pos27 = None
         _lib.call("fvr_rplan_pack", self.values.data_ptr(), self.nch, self.grid, self.kp.data_ptr(), self.n_kp,
                   kpv.data_ptr(), None, stream)
         self.rp_len, self.rp_off, self.rp_base, self.rp_tfin = unit_len, off, base, t_fin
@@ -702,10 +725,12 @@ class ChannelLoop:
         return dict(geo=geo, kp_map=kp_map, ray_samples=ray_samples, row_of_pos=row_of_pos, row_pos=row_pos,
                     slice_len=slice_len, slice_off=slice_off, sizes=sizes)
 
-    def _plan_fill(self, pc: dict, sizes, side, keep: list) -> bool:
-        """Allocate and zero (on the current stream) and fill the plan on the
-        stream ``side``; the temporaries the fill reads go to ``keep`` until
-        it is done.  False (scatter fallback) when the plan would not fit."""
+    def _plan_fill(self, pc: dict, sizes, side, keep: list):
+        """Allocate and zero the plan on the current stream and return a
+        function that enqueues its fill on the stream ``side`` (after the
+        work enqueued so far on the current stream); the temporaries the fill
+        reads go to ``keep`` until it is done.  None (scatter fallback) when
+        the plan would not fit."""
         t = self.t
         dev = self.dev
         c = self.cfg
@@ -715,9 +740,9 @@ class ChannelLoop:
         # entries + per-sample (meta: 8 B, rho: 4 B per channel slot) + the cursor
         need = (8 if self.sample_plan else 6) * slots + (2 + 4 * self.pitch) * n_samples + 8 * self.n_kp
         if need > self.PLAN_MAX_BYTES or n_samples >= 2 ** 31:
-            return False
+            return None
         if not self.sample_plan and (self.v_end - self.v_begin) * self.w_bb * self.h_bb >= 1 << 24:
-            return False  # residual indices are 24-bit in the 6-byte entries
+            return None  # residual indices are 24-bit in the 6-byte entries
         try:
             cursor = t.zeros(self.n_kp, dtype=t.int64, device=dev)
             if self.sample_plan:  # int2 (sample id, W)
@@ -730,26 +755,33 @@ class ChannelLoop:
                 entries = t.zeros(max(slots, 2), dtype=t.int32, device=dev)
                 entries_b = t.zeros(max(slots // 2, 1), dtype=t.int32, device=dev)
         except t.cuda.OutOfMemoryError:
-            return False
+            return None
         # each row's SELL position in one word: slice entry offset << 5 | lane
         row_pos = pc["row_pos"].long()
         row_info = (pc["slice_off"][row_pos >> 5] << 5) | (row_pos & 31)
         sell = (row_info.data_ptr(), cursor.data_ptr(), entries.data_ptr())
         keep += [pc, cursor, row_info]
         stream = side.cuda_stream
+        ready = t.cuda.Event()
         if self.sample_plan:
             sid0[1:] = t.cumsum(pc["ray_samples"][:-1].long(), 0)
             self.rho = rho
             keep.append(sid0)
-            side.wait_stream(t.cuda.current_stream())
-            _lib.call("fvr_sample_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff, pc["kp_map"].data_ptr(),
-                      sid0.data_ptr(), *sell, meta.data_ptr(), stream)
+            ready.record()
+
+            def launch():
+                side.wait_event(ready)
+                _lib.call("fvr_sample_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff,
+                          pc["kp_map"].data_ptr(), sid0.data_ptr(), *sell, meta.data_ptr(), stream)
             self.sample_meta = meta
             self.n_samples = n_samples
         else:
-            side.wait_stream(t.cuda.current_stream())
-            _lib.call("fvr_adjust_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff, pc["kp_map"].data_ptr(),
-                      *sell, entries_b.data_ptr(), stream)
+            ready.record()
+
+            def launch():
+                side.wait_event(ready)
+                _lib.call("fvr_adjust_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff,
+                          pc["kp_map"].data_ptr(), *sell, entries_b.data_ptr(), stream)
         self.plan_slice_len = pc["slice_len"]
         self.plan_slice_off = pc["slice_off"]
         self.plan_row_of_pos = pc["row_of_pos"]
@@ -757,7 +789,7 @@ class ChannelLoop:
         self.plan_entries_b = entries_b
         self.plan_nnz = nnz
         self.plan_slots = slots
-        return True
+        return launch
 
     def _weigh(self, stream):
         """rho = residual * G per in-hull sample (stochastic sample plan)."""
