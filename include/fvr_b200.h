@@ -389,6 +389,21 @@ int fvr_pack_correction(const int64_t* accum, const int32_t* kp_index, int64_t n
 int fvr_unpack_correction(const int64_t* packed, const int32_t* kp_index, int64_t n_kp,
                           int64_t* accum, void* stream);
 
+/* ---- loop setup: host staging (once per reconstruct_channel) ------------- */
+
+/* One multithreaded host pass over the caller's arrays into page-locked
+ * staging (all outputs are host pointers; NULL skips a part): inside_out
+ * (n_vox u8) = tags == full_mask (HullTags.inside_voxels, volume.py:142-145);
+ * src_out (V, h, w) f32 and masks_out (V, h, w) u8 = the bbox crops
+ * [v0:v0+h, u0:u0+w] of each view's image (row / column strides in
+ * elements) and flame mask (row stride in bytes, bool bytes);
+ * counts_out[v] = flame pixels of view v in the bbox (needs masks_out). */
+int fvr_stage_inputs_host(const uint32_t* tags, int64_t n_vox, uint32_t full_mask, int32_t n_views,
+                          const float* const* images, const int64_t* image_row_stride, int64_t image_col_stride,
+                          const uint8_t* const* masks, const int64_t* mask_row_stride, int32_t u0, int32_t v0,
+                          int32_t w, int32_t h, uint8_t* inside_out, float* src_out, uint8_t* masks_out,
+                          int64_t* counts_out);
+
 /* ---- loop setup: index preparation (once per reconstruct_channel) -------- */
 
 /* Morton (x, y, z) key of each of the n lattice indices kp_index (C order):

@@ -172,6 +172,8 @@ _SIGNATURES = {
     "fvr_hull_keypoints": (c_int, [_P, _GRID, _P, _P, _P]),
     "fvr_threshold_mask": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_double, _P, _P, _P, _P]),
     "fvr_mask_sat": (c_int, [_P, c_int32, c_int32, _P, _P]),
+    "fvr_stage_inputs_host": (c_int, [_P, c_int64, ctypes.c_uint32, c_int32, _P, _P, c_int64, _P, _P, c_int32, c_int32,
+                                      c_int32, c_int32, _P, _P, _P, _P]),
     "fvr_morton_keys": (c_int, [_P, c_int64, _GRID, _P, _P]),
     "fvr_sell_window_order": (c_int, [_P, c_int64, c_int32, _P, _P]),
     "fvr_rplan_tile_rows": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, _P, _P, _P]),

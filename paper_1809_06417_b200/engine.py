@@ -195,7 +195,7 @@ class ChannelLoop:
 
     def __init__(self, cameras, grid_geom, values, src_blocks, masks, bbox, inside, kp_mask,
                  render_cfg, loop_cfg: LoopConfig, max_iters: int, ground_truth=None,
-                 background=0.0, use_graph: bool = True, n_channels: int = 1):
+                 background=0.0, use_graph: bool = True, n_channels: int = 1, mask_crops=None):
         t = _lib.torch()
         self.t = t
         self.dev = _lib.device()
@@ -231,11 +231,14 @@ class ChannelLoop:
             raise ValueError("src channels do not match n_channels")
         shape = (grid_geom.nx + 1, grid_geom.ny + 1, grid_geom.nz + 1)
         self.shape = shape
-        inside = np.ascontiguousarray(inside)
-        if inside.dtype == np.bool_:  # upload the bytes as they are (no host-side u8 copy)
-            self.inside = t.from_numpy(inside).to(dev).view(t.uint8)
+        if t.is_tensor(inside):  # u8 (nx, ny, nz), staged on the device already
+            self.inside = inside
         else:
-            self.inside = t.from_numpy(inside.astype(np.uint8)).to(dev)
+            inside = np.ascontiguousarray(inside)
+            if inside.dtype == np.bool_:  # upload the bytes as they are (no host-side u8 copy)
+                self.inside = t.from_numpy(inside).to(dev).view(t.uint8)
+            else:
+                self.inside = t.from_numpy(inside.astype(np.uint8)).to(dev)
         self.values = t.empty((C,) + shape, dtype=t.float32, device=dev)
         if values is not None:
             self.values.copy_(t.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).reshape((C,) + shape))
@@ -305,7 +308,10 @@ class ChannelLoop:
         # flame rays of the local views, row-major per view (reconstruct.py:144-149)
         # compacted on the device (host masks: the bbox crops are uploaded)
         n_host = None
-        if t.is_tensor(masks):  # (V, H, W) u8 device masks
+        if mask_crops is not None:  # (V, h, w) u8 device crops + host flame counts per view
+            sub, per_view = mask_crops
+            n_host = int(per_view[self.v_begin:self.v_end].sum())
+        elif t.is_tensor(masks):  # (V, H, W) u8 device masks
             sub = masks[:, bbox.v0:bbox.v1 + 1, bbox.u0:bbox.u1 + 1]
         else:
             crops = np.stack([np.asarray(masks[v].bits[bbox.slices], dtype=np.uint8) for v in range(V)])

@@ -26,4 +26,5 @@ reconstruct_channel(*args, **kw)
 torch.cuda.synchronize()
 pr.disable()
 print(f"total {(time.perf_counter() - t0) * 1e3:.1f} ms")
-pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
+pstats.Stats(pr).sort_stats("tottime").print_stats(30)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(30)
