@@ -280,9 +280,13 @@ def run_gpu(args):
                                    converge_eps=1e-12, deterministic_mode=deterministic, g_sigma=0.1, rng_seed=0)
         grid0 = _init_grid(sc["geom"], sc["hull"], "green")
         src = [im.data[sc["bbox"].slices][:, :, 0] for im in sc["images"]]
+        torch.cuda.synchronize()
+        t_setup = time.perf_counter()
         loop = ChannelLoop(sc["cams"], grid0, grid0.values, src, sc["masks"], sc["bbox"],
                            sc["hull"].inside_voxels(), sc["hull"].key_point_mask(), sc["rcfg"],
                            _loop_config(cfg, grid0), cfg.max_iters + 8, background=0.0, use_graph=False)
+        torch.cuda.synchronize()
+        loop.setup_ms = (time.perf_counter() - t_setup) * 1e3
         stages = [(n, f) for n, f in loop.stages() if f is not None]
         names = [n for n, _ in stages]
 
@@ -373,6 +377,28 @@ def run_gpu(args):
             "frac": kach / peak, "traffic": TRAFFIC_BYTES_PER_LAUNCH[kname], "traffic_source": TRAFFIC_SOURCE[kname],
             "bytes_per_launch": kbytes, "bytes_rule": rule}
 
+    # What one step streams from HBM (the plans are re-read every iteration;
+    # the operands they index are cache-resident): render plan (6 B per stored
+    # entry + 16 B per row + 8 B per pixel) and adjust plan (6 B per stored
+    # entry + 20 B per hull key point: row order, key-point index, value
+    # read/write, operand write)
+    adj_bytes = 6 * loop.plan_slots + 20 * loop.n_kp if loop.plan else 0
+    step_bytes = kbytes + adj_bytes
+    step_streamed = {"bytes": step_bytes, "render_bytes": kbytes, "adjust_bytes": adj_bytes,
+                     "achieved_gbs": step_bytes / (ms * 1e-3) / 1e9, "frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
+                     "rule": "render plan 6 B/stored entry + 16 B/row + 8 B/pixel; adjust plan 6 B/stored entry + "
+                             "20 B/hull key point; over the whole step time (both launches + gaps)"}
+    # Per-call model of the public API: the plans are built once per
+    # reconstruct_channel call (count + fill passes over every ray), then
+    # streamed every iteration
+    plan_bytes = 6 * loop.rplan_nnz + 16 * (loop.rp_len.numel() * 32 if loop.rplan else 0) + \
+        (6 * loop.plan_slots if loop.plan else 0)
+    per_call = {"setup_ms": loop.setup_ms, "plan_bytes_written": plan_bytes,
+                "plan_write_gbs": plan_bytes / (loop.setup_ms * 1e-3) / 1e9,
+                "step_ms": ms, "modeled_call_ms_50": loop.setup_ms + 50 * ms,
+                "note": "setup = ChannelLoop construction (host prep, uploads, hull key points, both plans' count "
+                        "and fill passes), synchronised wall time; the plans are write-once per call"}
+
     # e2e: the public API with host buffers (H2D of inputs, D2H of the grid)
     e2e = None
     if args.e2e_iters > 0:
@@ -441,8 +467,12 @@ def run_gpu(args):
         "render_gsamples_per_s": w["S_r"] / (render_ms * 1e-3) / 1e9,
         "work": w,
         "stage_ms": part_ms,
-        "iter_algorithmic_bytes": iter_bytes,
-        "iter_roofline_frac": iter_bytes * its / (peak * 1e9),
+        # the SURVEY 8(d) per-iteration bytes of the reference's work (what a
+        # marching implementation would move); the plans make the step move
+        # far less, so this is a work rate, not an HBM fraction
+        "iter_survey_bytes": iter_bytes,
+        "step_streamed": step_streamed,
+        "per_call": per_call,
         # Dominant kernel = K-render.  Through the render plan it streams B
         # (6 B per stored SELL entry, padding included) plus per-row base and
         # t_fin (16 B) and src/residual (8 B per pixel); the key-point operand
