@@ -236,7 +236,11 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
  * (row_len from the count pass) so a unit's rows need less padding.  With
  * `finalize` (single-rank loops) the last block to finish runs
  * fvr_loop_finalize on state (one launch less per iteration; the block
- * counter is state[0].work_retired). */
+ * counter is state[0].work_retired).
+ * wide != 0 (fill and render must agree): 8-byte entries, u32 column in
+ * entries_a and f32 weight in entries_b at the same layout as entries_a
+ * (entries_b holds unit_off-total u32) -- for hulls of >= 2^24 key points,
+ * whose columns do not fit the 24-bit field. */
 /* Entries per lane chunk of the render-plan layout: unit_len and unit_off
  * must be multiples of it (the caller pads unit_len from the count pass). */
 int fvr_rplan_chunk_entries(void);
@@ -247,7 +251,7 @@ int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_
                    int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
                    const uint8_t* dynamic, const float* values, int32_t n_channels, const int64_t* unit_off,
                    const int32_t* unit_order, const int32_t* row_src, const int32_t* kp_map,
-                   uint32_t* entries_a, uint32_t* entries_b, double* base, double* t_fin, const uint32_t* pos27, void* stream);
+                   uint32_t* entries_a, uint32_t* entries_b, double* base, double* t_fin, const uint32_t* pos27, int32_t wide, void* stream);
 /* pos27[k] (lattice, u32): the stencil key points around interior key point k
  * that are static (not in dynamic) and positive in some channel -- the only
  * static ones a row's base needs.  fvr_rplan_fill computes it itself when its
@@ -265,7 +269,7 @@ int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const uin
                      const int32_t* unit_order, const int32_t* row_src, int32_t n_views, int32_t bbox_w,
                      int32_t bbox_h, const float* src, const float* kp_values, int32_t n_channels,
                      const double* background, float* residual, double* sq_partials, int64_t sq_stride,
-                     fvr_loop_state_t* state, const fvr_loop_finalize_t* finalize, void* stream);
+                     fvr_loop_state_t* state, const fvr_loop_finalize_t* finalize, int32_t wide, void* stream);
 int fvr_rplan_pack(const float* values, int32_t n_channels, fvr_grid_t grid, const int32_t* kp_index,
                    int64_t n_kp, float* kp_values, const fvr_loop_state_t* state, void* stream);
 
@@ -357,7 +361,11 @@ int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, co
  * units of 32 entries); entry t of position p at slice_off[p/32]*32 + 32t +
  * p%32; cursor (n_rows i64, zeroed) counts the entries written per row.
  * The fills take row_info[row] = slice_off[p/32] << 5 | p%32 (p = row_pos[row])
- * (i64): the row's SELL position in one word.
+ * (i64): the row's SELL position in one word.  fvr_adjust_plan_fill with
+ * entries_b == NULL writes the wide format: int2 (residual index, f32 W) in
+ * entries_a, chunks of 4 (slices padded to 4) -- for V * P >= 2^24, where
+ * the residual index outgrows the 24-bit field; fvr_loop_gather reads it as
+ * the int2 path (entries_b == NULL).
  * The deterministic plan (fvr_adjust_plan_fill) has 6-byte entries: a word
  * (u32, at that index) = residual index (< 2^24) | weight exponent << 24, and
  * the weight's top 16 mantissa bits in half t % 2 of entries_b[(slice_off +

@@ -225,6 +225,31 @@ struct SellMap {
             entries[((e / kSE) * 32 + (ri[i] & 31)) * kSE + (e % kSE)] = make_int2(sid, __float_as_int(w[i]));
         }
     }
+    // int2 (residual index, f32 W) entries of up to 8 corner runs (mask): the
+    // wide deterministic plan, for residual indices of >= 2^24 (V * P)
+    __device__ __forceinline__ void put_wide_batch(const int* kp, const float* w, uint32_t mask,
+                                                   const int32_t* __restrict__ kp_map, uint32_t idx,
+                                                   int2* entries) const {
+        int row[8];
+        long long t[8], ri[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) row[i] = ((mask >> i) & 1u) ? __ldg(kp_map + kp[i]) : 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if ((mask >> i) & 1u) {
+                FVR_DCHECK(row[i] >= 0, "adjust plan: corner is not a hull key point");
+                t[i] = (long long)atomicAdd(cursor + row[i], 1ull);
+                ri[i] = __ldg(row_info + row[i]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if ((mask >> i) & 1u) {
+                const long long e = (ri[i] >> 5) + t[i];
+                entries[((e / kSE) * 32 + (ri[i] & 31)) * kSE + (e % kSE)] = make_int2((int)idx, __float_as_int(w[i]));
+            }
+        }
+    }
     // up to 8 entries of one sample's corners (mask): each dependent step
     // (row lookup, then cursor atomic + row word) is issued for all of them
     // before any result is used, so their latencies overlap
@@ -266,7 +291,10 @@ __global__ void __launch_bounds__(128, FVR_PLAN_FILL_MINB) plan_fill_kernel(
     PlanRay pr;
     plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
     ray_entries<true>(pr, g, inside, tau_keep, alpha_l, alpha_d, [&](const int* pk, const float* pw, uint32_t mask) {
-        sm.put6_batch(pk, pw, mask, kp_map, (uint32_t)pr.res_index, ent_a, ent_b);
+        if (ent_b)
+            sm.put6_batch(pk, pw, mask, kp_map, (uint32_t)pr.res_index, ent_a, ent_b);
+        else  // wide plan: int2 entries in ent_a
+            sm.put_wide_batch(pk, pw, mask, kp_map, (uint32_t)pr.res_index, reinterpret_cast<int2*>(ent_a));
     });
 }
 

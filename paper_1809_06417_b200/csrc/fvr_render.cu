@@ -1144,7 +1144,7 @@ extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t
                               const uint8_t* dynamic, const float* values, int32_t n_channels,
                               const int64_t* unit_off, const int32_t* unit_order, const int32_t* row_src,
                               const int32_t* kp_map, uint32_t* entries_a, uint32_t* entries_b, double* base,
-                              double* t_fin, const uint32_t* pos27, void* stream) {
+                              double* t_fin, const uint32_t* pos27, int32_t wide, void* stream) {
     FVR_TRY_BEGIN
     if (n_views < 1 || bbox_w < 1 || bbox_h < 1) return set_error(FVR_ERR_INVALID, "empty render plan");
     if (n_channels < 1 || n_channels > 4) return set_error(FVR_ERR_INVALID, "n_channels must be 1..4");
@@ -1166,15 +1166,15 @@ extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t
     if (!d27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
     const uint32_t* p27 = pos27 ? pos27 : pos27_scratch(grid, dynamic, values, n_channels, st);
     if (!p27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
-    if (m)
-        rplan_fill_kernel<true><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc, occ,
-                                                         dynamic, d27, values, n_channels, plane, uo, unit_order,
-                                                         row_src, kp_map, entries_a, entries_b, p27, base, t_fin);
-    else
-        rplan_fill_kernel<false><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
-                                                          occ, dynamic, d27, values, n_channels, plane, uo,
-                                                          unit_order, row_src, kp_map, entries_a, entries_b, p27,
-                                                          base, t_fin);
+#define FVR_RPLAN_FILL(S, W)                                                                                   \
+    rplan_fill_kernel<S, W><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc, occ, \
+                                                     dynamic, d27, values, n_channels, plane, uo, unit_order, row_src, \
+                                                     kp_map, entries_a, entries_b, p27, base, t_fin)
+    if (m && wide) FVR_RPLAN_FILL(true, true);
+    else if (m) FVR_RPLAN_FILL(true, false);
+    else if (wide) FVR_RPLAN_FILL(false, true);
+    else FVR_RPLAN_FILL(false, false);
+#undef FVR_RPLAN_FILL
     return check_launch("rplan_fill");
     FVR_TRY_END
 }
@@ -1201,7 +1201,8 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
                                 const int32_t* unit_order, const int32_t* row_src, int32_t n_views, int32_t bbox_w,
                                 int32_t bbox_h, const float* src, const float* kp_values, int32_t n_channels,
                                 const double* background, float* residual, double* sq_partials, int64_t sq_stride,
-                                fvr_loop_state_t* state, const fvr_loop_finalize_t* finalize, void* stream) {
+                                fvr_loop_state_t* state, const fvr_loop_finalize_t* finalize, int32_t wide,
+                                void* stream) {
     FVR_TRY_BEGIN
     if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "the loop renders 1 or 3 channels");
     if (!background) return set_error(FVR_ERR_INVALID, "background is NULL");
@@ -1235,15 +1236,15 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
     cudaStream_t st = (cudaStream_t)stream;
     const auto* uo = reinterpret_cast<const long long*>(unit_off);
     cudaError_t e;
-    if (n_channels == 1)
-        e = launch_pdl(rplan_render_kernel<1>, (unsigned)blocks, 256, st, unit_len, uo, entries_a, entries_b, base, t_fin,
-                       unit_order, row_src, n_units, units_x, upv, n_views, bbox_w, bbox_h, src, kp_values, rc,
-                       residual, sq_partials, sq_stride, state, fin);
-    else
-        e = launch_pdl(rplan_render_kernel<3>, (unsigned)blocks, 256, st, unit_len, uo, entries_a, entries_b, base, t_fin,
-                                                                unit_order, row_src, n_units, units_x, upv, n_views,
-                                                                bbox_w, bbox_h, src, kp_values, rc, residual,
-                                                                sq_partials, sq_stride, state, fin);
+#define FVR_RPLAN_RENDER(C, W)                                                                                       \
+    e = launch_pdl(rplan_render_kernel<C, W>, (unsigned)blocks, 256, st, unit_len, uo, entries_a, entries_b, base,    \
+                   t_fin, unit_order, row_src, n_units, units_x, upv, n_views, bbox_w, bbox_h, src, kp_values, rc,    \
+                   residual, sq_partials, sq_stride, state, fin)
+    if (n_channels == 1 && !wide) FVR_RPLAN_RENDER(1, false);
+    else if (n_channels == 1) FVR_RPLAN_RENDER(1, true);
+    else if (!wide) FVR_RPLAN_RENDER(3, false);
+    else FVR_RPLAN_RENDER(3, true);
+#undef FVR_RPLAN_RENDER
     if (e != cudaSuccess) return set_error(FVR_ERR_CUDA, std::string("rplan_render: ") + cudaGetErrorString(e));
     return check_launch("rplan_render");
     FVR_TRY_END

@@ -160,24 +160,36 @@ __device__ __forceinline__ void store_zero_chunk(uint32_t* p) {
 // more instructions than the scattered stores, 1.83 vs 1.62 ms at config 2).
 // finish() pads the row with (0, 0.0) entries up to the unit's length --
 // whole chunks with 32-byte stores -- so the plan buffers need no clearing.
+template <bool WIDE>
 struct RplanOut {
     uint32_t* a;         // this row's first a word
-    uint16_t* b;         // this row's first 16-bit word
+    void* b;             // this row's first weight word (u16; u32 when WIDE)
     __device__ __forceinline__ void put(int t, int col, float w) const {
+        if (WIDE) {  // 8-byte entries: u32 column, f32 weight (hulls of >= 2^24 key points)
+            a[(int64_t)(t / kRpA) * (32 * kRpA) + (t % kRpA)] = (uint32_t)col;
+            static_cast<uint32_t*>(b)[(int64_t)(t / kRpA) * (32 * kRpA) + (t % kRpA)] = __float_as_uint(w);
+            return;
+        }
         FVR_DCHECK(col >= 0 && col < (1 << 24), "render plan: column not a hull key point");
         const uint32_t bits = (__float_as_uint(w) + 0x40u) >> 7;  // round to 16 mantissa bits
         a[(int64_t)(t / kRpA) * (32 * kRpA) + (t % kRpA)] = (uint32_t)col | ((bits >> 16) << 24);
-        b[(int64_t)(t / kRpB) * (32 * kRpB) + (t % kRpB)] = (uint16_t)(bits & 0xFFFFu);
+        static_cast<uint16_t*>(b)[(int64_t)(t / kRpB) * (32 * kRpB) + (t % kRpB)] = (uint16_t)(bits & 0xFFFFu);
     }
     // entries count..len-1 are padding (len: the unit's length, a multiple of kRpB)
     __device__ __forceinline__ void finish(int count, int len) const {
         FVR_DCHECK(count <= len, "render plan: row longer than its unit (count pass disagrees with fill)");
-        const int ca = (count + kRpA - 1) / kRpA * kRpA, cb = (count + kRpB - 1) / kRpB * kRpB;
+        constexpr int kB = WIDE ? kRpA : kRpB;  // weight words per chunk
+        const int ca = (count + kRpA - 1) / kRpA * kRpA, cb = (count + kB - 1) / kB * kB;
         for (int t = count; t < ca; ++t) a[(int64_t)(t / kRpA) * (32 * kRpA) + (t % kRpA)] = 0u;
-        for (int t = count; t < cb; ++t) b[(int64_t)(t / kRpB) * (32 * kRpB) + (t % kRpB)] = 0;
+        for (int t = count; t < cb; ++t) {
+            if (WIDE)
+                static_cast<uint32_t*>(b)[(int64_t)(t / kRpA) * (32 * kRpA) + (t % kRpA)] = 0u;
+            else
+                static_cast<uint16_t*>(b)[(int64_t)(t / kRpB) * (32 * kRpB) + (t % kRpB)] = 0;
+        }
         for (int c = ca / kRpA; c < len / kRpA; ++c) store_zero_chunk(a + (int64_t)c * (32 * kRpA));
-        uint32_t* bw = reinterpret_cast<uint32_t*>(b);  // a b chunk is kRpA u32 too
-        for (int c = cb / kRpB; c < len / kRpB; ++c) store_zero_chunk(bw + (int64_t)c * (32 * kRpA));
+        uint32_t* bw = static_cast<uint32_t*>(b);  // a weight chunk is kRpA u32 too
+        for (int c = cb / kB; c < len / kB; ++c) store_zero_chunk(bw + (int64_t)c * (32 * kRpA));
     }
 };
 
@@ -198,12 +210,12 @@ struct RplanOut {
 // is the 27-bit mask of dynamic key points around m (one load per sample).
 // Returns the entry count; t_fin receives the transparency after the last
 // sample.
-template <bool SCAT, bool FILL>
+template <bool SCAT, bool FILL, bool WIDE = false>
 __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, const RenderConsts& rc,
                          const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
                          const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch,
                          int64_t plane, const float* __restrict__ thr, const uint32_t* __restrict__ nm,
-                         float* __restrict__ acc, float* __restrict__ wsm, int stride, RplanOut out,
+                         float* __restrict__ acc, float* __restrict__ wsm, int stride, RplanOut<WIDE> out,
                          double* base, double& t_fin, const uint8_t* __restrict__ slot_tab = nullptr,
                          const int* __restrict__ kp_map = nullptr, int* __restrict__ skp = nullptr,
                          const uint32_t* __restrict__ pos27 = nullptr) {
@@ -470,7 +482,7 @@ __global__ void __launch_bounds__(128) rplan_count_kernel(
         double d[3], base[1] = {0.0}, t_fin;
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         cnt = rplan_row<SCAT, false>(cam.center, d, g, rc, occ, dynamic, dyn27, nullptr, 0, 0, s_thr, s_nm, nullptr,
-                                     nullptr, 0, RplanOut{}, base, t_fin);
+                                     nullptr, 0, RplanOut<false>{}, base, t_fin);
     }
     if (row_len) row_len[(int64_t)unit * 32 + lane] = cnt;
     cnt = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
@@ -479,7 +491,7 @@ __global__ void __launch_bounds__(128) rplan_count_kernel(
 
 // Fill pass: rows in SELL-32 order; base[c * rows + r] and t_fin[r] per row
 // r = unit * 32 + lane (entries beyond a row's length stay (0, 0.0)).
-template <bool SCAT>
+template <bool SCAT, bool WIDE>
 __global__ void __launch_bounds__(128) rplan_fill_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
     int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
@@ -507,14 +519,18 @@ __global__ void __launch_bounds__(128) rplan_fill_kernel(
     const bool in = rplan_pixel(row_src ? __ldg(row_src + r) : r, units_x, units_per_view, w, h, view, col, row);
     double base[4] = {0.0, 0.0, 0.0, 0.0}, t_fin = 0.0;
     const long long uoff = unit_off[unit];
-    const RplanOut out{ent_a + ((uoff / kRpA) * 32 + lane) * kRpA,
-                       reinterpret_cast<uint16_t*>(ent_b) + ((uoff / kRpB) * 32 + lane) * kRpB};
+    RplanOut<WIDE> out;
+    out.a = ent_a + ((uoff / kRpA) * 32 + lane) * kRpA;
+    if (WIDE)
+        out.b = ent_b + ((uoff / kRpA) * 32 + lane) * kRpA;
+    else
+        out.b = reinterpret_cast<uint16_t*>(ent_b) + ((uoff / kRpB) * 32 + lane) * kRpB;
     int count = 0;
     if (in) {
         const fvr_camera_t& cam = cams[view];
         double d[3];
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
-        count = rplan_row<SCAT, true>(cam.center, d, g, rc, occ, dynamic, dyn27, values, nch, plane, s_thr, s_nm,
+        count = rplan_row<SCAT, true, WIDE>(cam.center, d, g, rc, occ, dynamic, dyn27, values, nch, plane, s_thr, s_nm,
                                       s_acc + threadIdx.x, s_w + threadIdx.x, 128, out, base, t_fin, s_slot, kp_map,
                                       s_kp + threadIdx.x, pos27);
     }
@@ -571,7 +587,7 @@ __device__ __forceinline__ RpChunk rplan_stream(const uint32_t* p) {
 }
 
 // One unit (8x4 pixels, lane = pixel) of K-render through the plan.
-template <int NCH>
+template <int NCH, bool WIDE>
 __device__ __forceinline__ void rplan_render_unit(
     int unit, int lane, const int* __restrict__ unit_len, const long long* __restrict__ unit_off,
     const uint32_t* __restrict__ ent_a, const uint32_t* __restrict__ ent_b, const double* __restrict__ base,
@@ -584,9 +600,9 @@ __device__ __forceinline__ void rplan_render_unit(
     double acc[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
-    auto term = [&](uint32_t av, uint32_t half16, float* part) {
-        const float wgt = rplan_weight(av, half16);
-        const uint32_t k = av & kRplanIdxMask;
+    auto term = [&](uint32_t av, uint32_t bw, float* part) {  // bw: 16-bit weight word (u32 weight when WIDE)
+        const float wgt = WIDE ? __uint_as_float(bw) : rplan_weight(av, bw);
+        const uint32_t k = WIDE ? av : (av & kRplanIdxMask);
         if (NCH == 1) {
             part[0] = fmaf(wgt, __ldg(kpv + k), part[0]);
         } else {
@@ -600,21 +616,26 @@ __device__ __forceinline__ void rplan_render_unit(
     constexpr int B = FVR_RPLAN_BATCH;
     static_assert(B % kRpB == 0, "batches of whole chunks");
     const uint32_t* va = ent_a + ((off / kRpA) * 32 + lane) * kRpA;
-    const uint32_t* vb = ent_b + ((off / kRpB) * 32 + lane) * kRpA;  // a b chunk is kRpA u32 too
+    constexpr int kB = WIDE ? kRpA : kRpB;  // weight entries per (kRpA-word) chunk
+    const uint32_t* vb = ent_b + ((off / kB) * 32 + lane) * kRpA;  // a weight chunk is kRpA u32 too
     auto batch = [&](auto nb, int t0) {  // nb = entries (a multiple of kRpB) from t0
         constexpr int N = decltype(nb)::value;
-        RpChunk av[N / kRpA], bv[N / kRpB];
+        RpChunk av[N / kRpA], bv[N / kB];
 #pragma unroll
         for (int i = 0; i < N / kRpA; ++i) av[i] = rplan_stream(va + (int64_t)(t0 / kRpA + i) * (32 * kRpA));
 #pragma unroll
-        for (int i = 0; i < N / kRpB; ++i) bv[i] = rplan_stream(vb + (int64_t)(t0 / kRpB + i) * (32 * kRpA));
+        for (int i = 0; i < N / kB; ++i) bv[i] = rplan_stream(vb + (int64_t)(t0 / kB + i) * (32 * kRpA));
         float part[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) part[c] = 0.f;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-            const uint32_t hw = bv[i / kRpB].w[(i % kRpB) >> 1];
-            term(av[i / kRpA].w[i % kRpA], (i & 1) ? (hw >> 16) : (hw & 0xFFFFu), part);
+            if (WIDE) {
+                term(av[i / kRpA].w[i % kRpA], bv[i / kRpA].w[i % kRpA], part);
+            } else {
+                const uint32_t hw = bv[i / kRpB].w[(i % kRpB) >> 1];
+                term(av[i / kRpA].w[i % kRpA], (i & 1) ? (hw >> 16) : (hw & 0xFFFFu), part);
+            }
         }
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] += (double)part[c];
@@ -646,7 +667,7 @@ __device__ __forceinline__ void rplan_render_unit(
     }
 }
 
-template <int NCH>
+template <int NCH, bool WIDE>
 __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
     const int* __restrict__ unit_len, const long long* __restrict__ unit_off, const uint32_t* __restrict__ ent_a,
     const uint32_t* __restrict__ ent_b, const double* __restrict__ base, const double* __restrict__ t_fin,
@@ -664,7 +685,7 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
     // for the tail (config 2: 0.157 -> 0.139 ms)
     for (int unit = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); unit < n_units;
          unit += (int)(((int64_t)gridDim.x * blockDim.x) >> 5))
-        rplan_render_unit<NCH>(unit_order ? __ldg(unit_order + unit) : unit, lane, unit_len, unit_off, ent_a, ent_b,
+        rplan_render_unit<NCH, WIDE>(unit_order ? __ldg(unit_order + unit) : unit, lane, unit_len, unit_off, ent_a, ent_b,
                                base, t_fin, row_src, rows, units_x, units_per_view, n_views, w, h, src, kpv, rc,
                                residual, sq_partials, sq_stride);
     if (!fin.on) return;

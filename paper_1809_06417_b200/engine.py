@@ -536,13 +536,16 @@ class ChannelLoop:
         geo = self._rplan_geo()
         self.rp_row_src = rs["row_src"]
         slots = int(sizes[0]) * 32
-        need = 6 * slots + 8 * (self.nch + 1) * n_units * 32
-        if need > self.PLAN_MAX_BYTES or self.n_kp >= (1 << 24):
+        # 6-byte entries (24-bit column) unless the hull has >= 2^24 key
+        # points (or FVR_WIDE_PLANS=1): then 8-byte (u32 column, f32 weight)
+        self.rp_wide = self.n_kp >= (1 << 24) or os.environ.get("FVR_WIDE_PLANS") == "1"
+        need = (8 if self.rp_wide else 6) * slots + 8 * (self.nch + 1) * n_units * 32
+        if need > self.PLAN_MAX_BYTES:
             return False
         try:  # (no cudaMemGetInfo probe: it synchronises and costs tens of ms)
             # every chunk, padding included, is written by the fill (no clearing)
             ent_a = t.empty(max(slots, 2), dtype=t.int32, device=dev)
-            ent_b = t.empty(max(slots // 2, 1), dtype=t.int32, device=dev)
+            ent_b = t.empty(max(slots if self.rp_wide else slots // 2, 1), dtype=t.int32, device=dev)
             base = t.zeros((self.nch, n_units * 32), dtype=t.float64, device=dev)
             t_fin = t.zeros(n_units * 32, dtype=t.float64, device=dev)
             # the operand: max(v, 0) per hull key point (float4 for 3 channels)
@@ -554,7 +557,8 @@ class ChannelLoop:
             if os.environ.get("FVR_RPLAN_SORT", "1") == "1" else None
         _lib.call("fvr_rplan_fill", *geo, self.values.data_ptr(), self.nch, off.data_ptr(), _lib.ptr(self.rp_order),
                   _lib.ptr(self.rp_row_src), self._kp_map().data_ptr(), ent_a.data_ptr(), ent_b.data_ptr(),
-                  base.data_ptr(), t_fin.data_ptr(), _lib.ptr(getattr(self, "_pos27", None)), stream)
+                  base.data_ptr(), t_fin.data_ptr(), _lib.ptr(getattr(self, "_pos27", None)), int(self.rp_wide),
+                  stream)
         self._pos27 = None
         _lib.call("fvr_rplan_pack", self.values.data_ptr(), self.nch, self.grid, self.kp.data_ptr(), self.n_kp,
                   kpv.data_ptr(), None, stream)
@@ -578,7 +582,7 @@ class ChannelLoop:
                 _lib.ptr(self.rp_row_src), self.v_end - self.v_begin, self.w_bb, self.h_bb, self.src.data_ptr(),
                 self.rp_kpv.data_ptr(), self.nch, self.background, self.residual.data_ptr(),
                 self.sq[0, self.v_begin * self.bpv:].data_ptr(), self.n_sq, self.state.data_ptr(),
-                self._fused_finalize(), stream,
+                self._fused_finalize(), int(self.rp_wide), stream,
             )
             return n
         _lib.call(
@@ -685,6 +689,10 @@ class ChannelLoop:
         t = self.t
         dev = self.dev
         stream = _lib.stream_ptr()
+        # deterministic entries are 6 bytes (24-bit residual index) unless V * P
+        # >= 2^24 (or FVR_WIDE_PLANS=1): then int2 (residual index, f32 W)
+        self.adj_wide = not self.sample_plan and (
+            (self.v_end - self.v_begin) * self.w_bb * self.h_bb >= (1 << 24) or os.environ.get("FVR_WIDE_PLANS") == "1")
         kp_map = self._kp_map()
         counts = t.zeros(self.n_kp, dtype=t.int32, device=dev)
         geo = (self.cams.data_ptr(), self.rays.data_ptr(), self.n_rays, self.bbox.u0, self.bbox.v0, self.w_bb,
@@ -721,8 +729,8 @@ class ChannelLoop:
         slice_len[: self.n_kp] = counts[order]
         slice_len = slice_len.view(n_slices, 32).amax(1).contiguous()
         # whole lane chunks (fvr_plan.cu): 16 bytes of six-byte entries (8), or
-        # 32 bytes of eight-byte sample entries (kSE = 4)
-        slice_len = (slice_len + 3) & ~3 if self.sample_plan else (slice_len + 7) & ~7
+        # 32 bytes of eight-byte (sample / wide) entries (kSE = 4)
+        slice_len = (slice_len + 3) & ~3 if (self.sample_plan or self.adj_wide) else (slice_len + 7) & ~7
         slice_off = t.zeros(n_slices + 1, dtype=t.int64, device=dev)
         slice_off[1:] = t.cumsum(slice_len.long(), 0)
         sizes = [slice_off[-1], counts.long().sum()]
@@ -744,19 +752,19 @@ class ChannelLoop:
         nnz = int(sizes[1])
         n_samples = int(sizes[2]) if self.sample_plan else 0
         # entries + per-sample (meta: 8 B, rho: 4 B per channel slot) + the cursor
-        need = (8 if self.sample_plan else 6) * slots + (2 + 4 * self.pitch) * n_samples + 8 * self.n_kp
+        need = (8 if (self.sample_plan or self.adj_wide) else 6) * slots + (2 + 4 * self.pitch) * n_samples + \
+            8 * self.n_kp
         if need > self.PLAN_MAX_BYTES or n_samples >= 2 ** 31:
             return None
-        if not self.sample_plan and (self.v_end - self.v_begin) * self.w_bb * self.h_bb >= 1 << 24:
-            return None  # residual indices are 24-bit in the 6-byte entries
         try:
             cursor = t.zeros(self.n_kp, dtype=t.int64, device=dev)
-            if self.sample_plan:  # int2 (sample id, W)
+            if self.sample_plan or self.adj_wide:  # int2 (sample id or residual index, W)
                 entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
                 entries_b = None
-                sid0 = t.zeros(self.n_rays, dtype=t.int64, device=dev)
-                meta = t.empty(max(n_samples // 2, 2), dtype=t.int32, device=dev)  # int2 per 4-slot block
-                rho = t.zeros((max(n_samples, 1), self.pitch), dtype=t.float32, device=dev)
+                if self.sample_plan:
+                    sid0 = t.zeros(self.n_rays, dtype=t.int64, device=dev)
+                    meta = t.empty(max(n_samples // 2, 2), dtype=t.int32, device=dev)  # int2 per 4-slot block
+                    rho = t.zeros((max(n_samples, 1), self.pitch), dtype=t.float32, device=dev)
             else:  # 6 bytes: residual index (24 bits) + 24-bit weight
                 entries = t.zeros(max(slots, 2), dtype=t.int32, device=dev)
                 entries_b = t.zeros(max(slots // 2, 1), dtype=t.int32, device=dev)
@@ -787,7 +795,7 @@ class ChannelLoop:
             def launch():
                 side.wait_event(ready)
                 _lib.call("fvr_adjust_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff,
-                          pc["kp_map"].data_ptr(), *sell, entries_b.data_ptr(), stream)
+                          pc["kp_map"].data_ptr(), *sell, _lib.ptr(entries_b), stream)
         self.plan_slice_len = pc["slice_len"]
         self.plan_slice_off = pc["slice_off"]
         self.plan_row_of_pos = pc["row_of_pos"]
