@@ -260,10 +260,10 @@ int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_
 int fvr_rplan_pos27(fvr_grid_t grid, const uint8_t* dynamic, const float* values, int32_t n_channels,
                     uint32_t* pos27, void* stream);
 /* Sort keys of the render plan's unit order (units longest class first, in
- * classes of `bucket` entries; 2x4-unit tiles inside a class): ascending keys
- * = visiting order. */
-int fvr_rplan_unit_keys(const int32_t* unit_len, int32_t n_views, int32_t bbox_w, int32_t bbox_h, int32_t bucket,
-                        int64_t* keys, void* stream);
+ * `buckets` classes up to the longest unit, *max_len on the device; 2x4-unit
+ * tiles inside a class): ascending keys = visiting order. */
+int fvr_rplan_unit_keys(const int32_t* unit_len, int32_t n_views, int32_t bbox_w, int32_t bbox_h, int32_t buckets,
+                        const int32_t* max_len, int64_t* keys, void* stream);
 int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off, const uint32_t* entries_a,
                      const uint32_t* entries_b, const double* base, const double* t_fin,
                      const int32_t* unit_order, const int32_t* row_src, int32_t n_views, int32_t bbox_w,

@@ -149,7 +149,7 @@ _SIGNATURES = {
     "fvr_rplan_fill": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _GRID, _PARAMS, _P, _P, _P, c_int32,
                                _P, _P, _P, _P, _P, _P, _P, _P, _P, c_int32, _P]),
     "fvr_rplan_pos27": (c_int, [_GRID, _P, _P, c_int32, _P, _P]),
-    "fvr_rplan_unit_keys": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, _P, _P]),
+    "fvr_rplan_unit_keys": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, _P, _P, _P]),
     "fvr_rplan_render": (c_int, [_P, _P, _P, _P, _P, _P, _P, _P, c_int32, c_int32, c_int32, _P, _P, c_int32, _P, _P,
                                  _P, c_int64, _P, _P, c_int32, _P]),
     "fvr_rplan_pack": (c_int, [_P, c_int32, _GRID, _P, c_int64, _P, _P, _P]),

@@ -1114,9 +1114,11 @@ extern "C" int fvr_rplan_pos27(fvr_grid_t grid, const uint8_t* dynamic, const fl
 // one sort visits the units longest class first and neighbouring units
 // together inside a class.
 __global__ void rplan_unit_keys_kernel(const int32_t* __restrict__ unit_len, int n_units, int upv, int units_x,
-                                       int q, uint64_t* __restrict__ keys) {
+                                       int buckets, const int32_t* __restrict__ max_len,
+                                       uint64_t* __restrict__ keys) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_units) return;
+    const int q = max(1, (*max_len + buckets - 1) / buckets);  // class width: buckets classes up to the longest
     const int units_y = upv / units_x;
     const int txn = (units_x + 1) / 2, tyn = (units_y + 3) / 4;
     const int view = i / upv, u = i - view * upv;
@@ -1127,14 +1129,15 @@ __global__ void rplan_unit_keys_kernel(const int32_t* __restrict__ unit_len, int
 }
 
 extern "C" int fvr_rplan_unit_keys(const int32_t* unit_len, int32_t n_views, int32_t bbox_w, int32_t bbox_h,
-                                   int32_t bucket, int64_t* keys, void* stream) {
+                                   int32_t buckets, const int32_t* max_len, int64_t* keys, void* stream) {
     FVR_TRY_BEGIN
-    if (bucket < 1) return set_error(FVR_ERR_INVALID, "bucket must be positive");
+    if (buckets < 1) return set_error(FVR_ERR_INVALID, "buckets must be positive");
+    if (!max_len) return set_error(FVR_ERR_INVALID, "max_len is NULL");
     const int units_x = (bbox_w + kUnitW - 1) / kUnitW, upv = fvr_loop_blocks_per_view(bbox_w, bbox_h);
     const int n_units = upv * n_views;
     if (n_units == 0) return FVR_OK;
     rplan_unit_keys_kernel<<<(n_units + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
-        unit_len, n_units, upv, units_x, bucket, reinterpret_cast<uint64_t*>(keys));
+        unit_len, n_units, upv, units_x, buckets, max_len, reinterpret_cast<uint64_t*>(keys));
     return check_launch("rplan_unit_keys");
     FVR_TRY_END
 }

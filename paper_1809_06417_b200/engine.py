@@ -148,6 +148,20 @@ def exchange(comm, sq, vol, v_begin: int, v_end: int, rows_per_view: int, rank: 
         dist.all_reduce(comm, op=dist.ReduceOp.SUM, group=group)
 
 
+_SIDE: dict = {}
+
+
+def _side_stream(dev):
+    """One persistent side stream per device: buffers allocated on it come
+    from its own caching-allocator pool, which a per-call stream would never
+    reuse (a fresh cudaMalloc every call)."""
+    t = _lib.torch()
+    key = str(dev)
+    if key not in _SIDE:
+        _SIDE[key] = t.cuda.Stream(device=dev)
+    return _SIDE[key]
+
+
 _PINNED: dict = {}
 
 
@@ -375,19 +389,18 @@ class ChannelLoop:
         scalars = (pc["sizes"] if pc else []) + (rs["sizes"] if rs else [])
         host = t.stack(scalars).cpu().tolist() if scalars else []
         keep = []
-        if pc is not None:
-            # the adjust plan's buffers and inputs are ready once this event
-            # fires; its fill then runs on a side stream next to the render
-            # plan's (the longer one, enqueued first on the loop's stream)
-            main = t.cuda.current_stream()
-            side = t.cuda.Stream()
-            launch_adjust = self._plan_fill(pc, host[: len(pc["sizes"])], side, keep)
+        # the render plan's fill (the longer one) goes first on the loop's
+        # stream; the adjust plan's buffers are allocated, cleared and filled
+        # on a persistent side stream (its own allocator pool, reused across
+        # calls) next to it
         if rs is not None:
             self.rplan = self._rplan_fill(rs, host[len(pc["sizes"]) if pc else 0:])
         if pc is not None:
-            self.plan = launch_adjust is not None
-            if self.plan:
-                launch_adjust()
+            main = t.cuda.current_stream()
+            side = _side_stream(self.dev)
+            side.wait_stream(main)
+            with t.cuda.stream(side):
+                self.plan = self._plan_fill(pc, host[: len(pc["sizes"])], side, keep)
             self.sample_plan = self.plan and self.sample_plan
             main.wait_stream(side)
         del keep
@@ -497,9 +510,13 @@ class ChannelLoop:
         unit_len = (unit_len + al - 1) & ~(al - 1)
         off = t.zeros(n_units + 1, dtype=t.int64, device=self.dev)
         off[1:] = t.cumsum(unit_len.long(), 0)
-        return dict(unit_len=unit_len, row_src=row_src, off=off, sizes=[off[-1], unit_len.max()])
+        mx = unit_len.max()
+        # fill and render visit the units longest first (a short tail); the
+        # order is computed before the sizes reach the host
+        order = self._rplan_unit_order(unit_len, mx) if os.environ.get("FVR_RPLAN_SORT", "1") == "1" else None
+        return dict(unit_len=unit_len, row_src=row_src, off=off, order=order, sizes=[off[-1], mx])
 
-    def _rplan_unit_order(self, unit_len, max_len: int):
+    def _rplan_unit_order(self, unit_len, max_len):
         """The order fill and render visit the units: longest first, in
         ``buckets`` length classes (a short tail), and inside a class by
         tiles of 2x4 units (16x16 pixels), so the 8 warps of a CTA render
@@ -510,20 +527,11 @@ class ChannelLoop:
         buckets = int(os.environ.get("FVR_RPLAN_BUCKETS", "24"))
         if buckets <= 0:
             return t.argsort(unit_len, descending=True).to(t.int32)
-        q = max(1, -(-int(max_len) // buckets))
-        if n_units == (self.v_end - self.v_begin) * self.bpv:  # one key kernel + one sort
-            keys = t.empty(n_units, dtype=t.int64, device=unit_len.device)
-            _lib.call("fvr_rplan_unit_keys", unit_len.data_ptr(), self.v_end - self.v_begin, self.w_bb, self.h_bb, q,
-                      keys.data_ptr(), _lib.stream_ptr())
-            return t.sort(keys).indices.to(t.int32)
-        uid = t.arange(n_units, device=unit_len.device)
-        ux = (self.w_bb + 7) // 8
-        uy = self.bpv // ux
-        txn, tyn = (ux + 1) // 2, (uy + 3) // 4
-        view, u = uid // self.bpv, uid % self.bpv
-        tile = (view * tyn + (u // ux) // 4) * txn + (u % ux) // 2
-        spatial = tile * 8 + ((u // ux) % 4) * 2 + (u % ux) % 2
-        return t.argsort(-(unit_len.long() // q) * (n_units * 8) + spatial).to(t.int32)
+        mx = max_len.to(t.int32).reshape(1)  # device scalar: no synchronisation
+        keys = t.empty(n_units, dtype=t.int64, device=unit_len.device)
+        _lib.call("fvr_rplan_unit_keys", unit_len.data_ptr(), self.v_end - self.v_begin, self.w_bb, self.h_bb,
+                  buckets, mx.data_ptr(), keys.data_ptr(), _lib.stream_ptr())
+        return t.sort(keys).indices.to(t.int32)
 
     def _rplan_fill(self, rs: dict, sizes) -> bool:
         """B of rec = B c + base + t_fin bg in SELL-32 form (fvr_rplan.cuh),
@@ -546,15 +554,14 @@ class ChannelLoop:
             # every chunk, padding included, is written by the fill (no clearing)
             ent_a = t.empty(max(slots, 2), dtype=t.int32, device=dev)
             ent_b = t.empty(max(slots if self.rp_wide else slots // 2, 1), dtype=t.int32, device=dev)
-            base = t.zeros((self.nch, n_units * 32), dtype=t.float64, device=dev)
-            t_fin = t.zeros(n_units * 32, dtype=t.float64, device=dev)
+            # the fill writes every row's base and t_fin (overhanging rows too)
+            base = t.empty((self.nch, n_units * 32), dtype=t.float64, device=dev)
+            t_fin = t.empty(n_units * 32, dtype=t.float64, device=dev)
             # the operand: max(v, 0) per hull key point (float4 for 3 channels)
             kpv = t.empty((max(self.n_kp, 1),) + ((4,) if self.nch == 3 else ()), dtype=t.float32, device=dev)
         except t.cuda.OutOfMemoryError:
             return False
-        # fill and render visit the units longest first (a short tail)
-        self.rp_order = self._rplan_unit_order(unit_len, sizes[1]) \
-            if os.environ.get("FVR_RPLAN_SORT", "1") == "1" else None
+        self.rp_order = rs["order"]
         _lib.call("fvr_rplan_fill", *geo, self.values.data_ptr(), self.nch, off.data_ptr(), _lib.ptr(self.rp_order),
                   _lib.ptr(self.rp_row_src), self._kp_map().data_ptr(), ent_a.data_ptr(), ent_b.data_ptr(),
                   base.data_ptr(), t_fin.data_ptr(), _lib.ptr(getattr(self, "_pos27", None)), int(self.rp_wide),
@@ -736,15 +743,17 @@ class ChannelLoop:
         sizes = [slice_off[-1], counts.long().sum()]
         if ray_samples is not None:
             sizes.append(ray_samples.long().sum())
+        # each row's SELL position in one word: slice entry offset << 5 | lane
+        rp = row_pos.long()
+        row_info = (slice_off[rp >> 5] << 5) | (rp & 31)
         return dict(geo=geo, kp_map=kp_map, ray_samples=ray_samples, row_of_pos=row_of_pos, row_pos=row_pos,
-                    slice_len=slice_len, slice_off=slice_off, sizes=sizes)
+                    slice_len=slice_len, slice_off=slice_off, row_info=row_info, sizes=sizes)
 
-    def _plan_fill(self, pc: dict, sizes, side, keep: list):
-        """Allocate and zero the plan on the current stream and return a
-        function that enqueues its fill on the stream ``side`` (after the
-        work enqueued so far on the current stream); the temporaries the fill
-        reads go to ``keep`` until it is done.  None (scatter fallback) when
-        the plan would not fit."""
+    def _plan_fill(self, pc: dict, sizes, side, keep: list) -> bool:
+        """Allocate, clear and fill the plan on the stream ``side`` (the
+        current stream when called); the temporaries the fill reads go to
+        ``keep`` until it is done.  False (scatter fallback) when the plan
+        would not fit."""
         t = self.t
         dev = self.dev
         c = self.cfg
@@ -755,7 +764,7 @@ class ChannelLoop:
         need = (8 if (self.sample_plan or self.adj_wide) else 6) * slots + (2 + 4 * self.pitch) * n_samples + \
             8 * self.n_kp
         if need > self.PLAN_MAX_BYTES or n_samples >= 2 ** 31:
-            return None
+            return False
         try:
             cursor = t.zeros(self.n_kp, dtype=t.int64, device=dev)
             if self.sample_plan or self.adj_wide:  # int2 (sample id or residual index, W)
@@ -769,33 +778,21 @@ class ChannelLoop:
                 entries = t.zeros(max(slots, 2), dtype=t.int32, device=dev)
                 entries_b = t.zeros(max(slots // 2, 1), dtype=t.int32, device=dev)
         except t.cuda.OutOfMemoryError:
-            return None
-        # each row's SELL position in one word: slice entry offset << 5 | lane
-        row_pos = pc["row_pos"].long()
-        row_info = (pc["slice_off"][row_pos >> 5] << 5) | (row_pos & 31)
-        sell = (row_info.data_ptr(), cursor.data_ptr(), entries.data_ptr())
-        keep += [pc, cursor, row_info]
+            return False
+        sell = (pc["row_info"].data_ptr(), cursor.data_ptr(), entries.data_ptr())
+        keep += [pc, cursor]
         stream = side.cuda_stream
-        ready = t.cuda.Event()
         if self.sample_plan:
             sid0[1:] = t.cumsum(pc["ray_samples"][:-1].long(), 0)
             self.rho = rho
             keep.append(sid0)
-            ready.record()
-
-            def launch():
-                side.wait_event(ready)
-                _lib.call("fvr_sample_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff,
-                          pc["kp_map"].data_ptr(), sid0.data_ptr(), *sell, meta.data_ptr(), stream)
+            _lib.call("fvr_sample_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff,
+                      pc["kp_map"].data_ptr(), sid0.data_ptr(), *sell, meta.data_ptr(), stream)
             self.sample_meta = meta
             self.n_samples = n_samples
         else:
-            ready.record()
-
-            def launch():
-                side.wait_event(ready)
-                _lib.call("fvr_adjust_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff,
-                          pc["kp_map"].data_ptr(), *sell, _lib.ptr(entries_b), stream)
+            _lib.call("fvr_adjust_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff,
+                      pc["kp_map"].data_ptr(), *sell, _lib.ptr(entries_b), stream)
         self.plan_slice_len = pc["slice_len"]
         self.plan_slice_off = pc["slice_off"]
         self.plan_row_of_pos = pc["row_of_pos"]
@@ -803,7 +800,7 @@ class ChannelLoop:
         self.plan_entries_b = entries_b
         self.plan_nnz = nnz
         self.plan_slots = slots
-        return launch
+        return True
 
     def _weigh(self, stream):
         """rho = residual * G per in-hull sample (stochastic sample plan)."""
