@@ -67,3 +67,23 @@ def test_render_plan_chunk_entries_without_gpu():
     from the library, so a build with another chunk size stays consistent."""
     n = _lib.load().fvr_rplan_chunk_entries()
     assert n in (8, 16) and n & (n - 1) == 0
+
+
+def test_ctypes_signatures_match_header():
+    """Every prototype in include/fvr_b200.h has a ctypes signature with the
+    same number of parameters (the compiler already ties the header to the
+    definitions: extern "C" functions cannot overload)."""
+    import re
+
+    from paper_1809_06417_b200 import _lib
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    h = open(os.path.join(root, "include", "fvr_b200.h")).read()
+    protos = {}
+    for m in re.finditer(r"^(?:int|int64_t|const char\*)\s+(fvr_\w+)\(([^;]*?)\);", h, re.M | re.S):
+        args = m.group(2).strip()
+        protos[m.group(1)] = 0 if args in ("void", "") else args.count(",") + 1
+    assert protos, "no prototypes parsed"
+    assert sorted(set(protos) - set(_lib._SIGNATURES)) == []
+    bad = {k: (len(v[1]), protos[k]) for k, v in _lib._SIGNATURES.items() if k in protos and len(v[1]) != protos[k]}
+    assert bad == {}, bad
