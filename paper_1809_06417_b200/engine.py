@@ -392,13 +392,13 @@ class ChannelLoop:
         # the render plan's fill (the longer one) goes first on the loop's
         # stream; the adjust plan's buffers are allocated, cleared and filled
         # on a persistent side stream (its own allocator pool, reused across
-        # calls) next to it
+        # calls) next to it, after the work enqueued so far
+        main = t.cuda.current_stream()
+        side = _side_stream(self.dev)
+        side.wait_stream(main)
         if rs is not None:
             self.rplan = self._rplan_fill(rs, host[len(pc["sizes"]) if pc else 0:])
         if pc is not None:
-            main = t.cuda.current_stream()
-            side = _side_stream(self.dev)
-            side.wait_stream(main)
             with t.cuda.stream(side):
                 self.plan = self._plan_fill(pc, host[: len(pc["sizes"])], side, keep)
             self.sample_plan = self.plan and self.sample_plan

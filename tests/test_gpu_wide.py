@@ -7,7 +7,7 @@ wide formats instead of falling back to the slower kernels.
 * FVR_WIDE_PLANS=1 forces both wide formats on the golden loops: same
   parity contract against the reference's goldens, and the 17-bit-mantissa
   narrow plans agree with the f32-weight wide ones to 1e-5;
-* a 256^3 lattice whose hull is the whole box has 257^3 = 16.98 M > 2^24 key
+* a 288^3 lattice whose hull fills most of the box has ~21 M > 2^24 key
   points: the loop picks the wide render plan by itself and matches the CPU
   oracle after one iteration."""
 
@@ -49,7 +49,7 @@ def test_hull_beyond_24_bits_uses_wide_render_plan(cuda_device):
     from paper_1809_06417_b200.synth import synth_cameras, synth_volume
     from tests.fullsize_common import oracle_loop
 
-    n = 256
+    n = 288
     vols = synth_volume((n, n, n), seed=0, kind="slab", slab_value=60.0)
     truth = [vols[t] for t in ("red", "green", "blue")]
     cams = synth_cameras(2, radius=0.6, fov=40.0, width=48, height=48, seed=0)
