@@ -281,6 +281,7 @@ struct SellMap {
 #ifndef FVR_PLAN_FILL_MINB
 #define FVR_PLAN_FILL_MINB 4
 #endif
+template <bool WIDE>
 __global__ void __launch_bounds__(128, FVR_PLAN_FILL_MINB) plan_fill_kernel(
     const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
     int u0, int v0, int w, int h, const uint8_t* __restrict__ inside, Geom g, double tau_keep,
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(128, FVR_PLAN_FILL_MINB) plan_fill_kernel(
     PlanRay pr;
     plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
     ray_entries<true>(pr, g, inside, tau_keep, alpha_l, alpha_d, [&](const int* pk, const float* pw, uint32_t mask) {
-        if (ent_b)
+        if (!WIDE)
             sm.put6_batch(pk, pw, mask, kp_map, (uint32_t)pr.res_index, ent_a, ent_b);
         else  // wide plan: int2 entries in ent_a
             sm.put_wide_batch(pk, pw, mask, kp_map, (uint32_t)pr.res_index, reinterpret_cast<int2*>(ent_a));
@@ -601,11 +602,16 @@ extern "C" int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray
     if (int rc = check_grid(grid)) return rc;
     if (n_rays == 0) return FVR_OK;
     const Geom g = make_geom(grid);
-    plan_fill_kernel<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-        cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d,
-        kp_map,
-        SellMap{reinterpret_cast<const long long*>(row_info), reinterpret_cast<unsigned long long*>(cursor)},
-        entries_a, reinterpret_cast<uint16_t*>(entries_b));
+    const SellMap sm{reinterpret_cast<const long long*>(row_info), reinterpret_cast<unsigned long long*>(cursor)};
+    const unsigned blocks = (unsigned)((n_rays + 127) / 128);
+    if (entries_b)  // 6-byte entries (the wide path is a separate instance: its registers slowed this one 0.92 -> 1.54 ms)
+        plan_fill_kernel<false><<<blocks, 128, 0, (cudaStream_t)stream>>>(
+            cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d, kp_map,
+            sm, entries_a, reinterpret_cast<uint16_t*>(entries_b));
+    else
+        plan_fill_kernel<true><<<blocks, 128, 0, (cudaStream_t)stream>>>(
+            cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d, kp_map,
+            sm, entries_a, nullptr);
     return check_launch("adjust_plan_fill");
     FVR_TRY_END
 }

@@ -375,11 +375,9 @@ class ChannelLoop:
         scalars = (pc["sizes"] if pc else []) + (rs["sizes"] if rs else [])
         host = t.stack(scalars).cpu().tolist() if scalars else []
         keep = []
-        # the two fills run back to back on the loop's stream, the adjust
-        # plan's first: side by side on two streams each slowed the other
-        # (config 2: 1.73 + 1.78 ms overlapped), and after the render fill's
-        # 0.5 GB of writes the adjust fill's atomics took 1.54 ms instead of
-        # 0.92
+        # the two fills run back to back on the loop's stream: side by side on
+        # two streams each slowed the other (config 2: 1.73 + 1.78 ms
+        # overlapped, against 1.59 + 0.92 ms in sequence)
         if pc is not None:
             self.plan = self._plan_fill(pc, host[: len(pc["sizes"])], t.cuda.current_stream(), keep)
             self.sample_plan = self.plan and self.sample_plan
