@@ -237,6 +237,8 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
  * `finalize` (single-rank loops) the last block to finish runs
  * fvr_loop_finalize on state (one launch less per iteration; the block
  * counter is state[0].work_retired).
+ * fvr_rplan_fill with values == NULL asserts that no key point outside
+ * `dynamic` is positive (base then holds nothing but the background term).
  * wide != 0 (fill and render must agree): 8-byte entries, u32 column in
  * entries_a and f32 weight in entries_b at the same layout as entries_a
  * (entries_b holds unit_off-total u32) -- for hulls of >= 2^24 key points,

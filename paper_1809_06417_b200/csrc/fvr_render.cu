@@ -1167,8 +1167,10 @@ extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t
     if (!kp_map || !entries_a || !entries_b) return set_error(FVR_ERR_INVALID, "kp_map / entries are NULL");
     uint32_t* d27 = dyn27_scratch(grid, dynamic, st, false);
     if (!d27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
-    const uint32_t* p27 = pos27 ? pos27 : pos27_scratch(grid, dynamic, values, n_channels, st);
-    if (!p27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
+    // values == NULL: every key point outside `dynamic` is <= 0 (the loop's
+    // own initial lattice), so nothing static folds into base
+    const uint32_t* p27 = pos27 || !values ? pos27 : pos27_scratch(grid, dynamic, values, n_channels, st);
+    if (values && !p27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
 #define FVR_RPLAN_FILL(S, W)                                                                                   \
     rplan_fill_kernel<S, W><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc, occ, \
                                                      dynamic, d27, values, n_channels, plane, uo, unit_order, row_src, \

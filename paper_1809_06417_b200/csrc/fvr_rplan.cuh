@@ -311,7 +311,7 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                     const float wt = FILL ? wsm[j * stride] : 0.f;
                     if (__ldg(dynamic + kp)) {
                         put(FILL ? __ldg(kp_map + kp) : 0, wt);
-                    } else if (FILL) {
+                    } else if (FILL && values) {  // values == NULL: no static key point is positive
                         for (int c = 0; c < nch; ++c) base[c] += (double)wt * fmaxf(__ldg(values + c * plane + kp), 0.f);
                     }
                 }
@@ -393,7 +393,7 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
 #pragma unroll 1
                 // static key points with a positive value (pos27; none for the
                 // reference's initial grid) fold into base
-                for (uint32_t b = sup & (pos27 ? __ldg(pos27 + mlin) : ~dyn); b; b &= b - 1) {
+                for (uint32_t b = values ? sup & (pos27 ? __ldg(pos27 + mlin) : ~dyn) : 0u; b; b &= b - 1) {
                     const int j = __ffs(b) - 1;
                     const float wt = wsm[j * stride];
                     if (wt == 0.f) continue;

@@ -242,6 +242,10 @@ class ChannelLoop:
         self.values = t.empty((C,) + shape, dtype=t.float32, device=dev)
         if values is not None:
             self.values.copy_(t.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).reshape((C,) + shape))
+        # the loop's own initial lattice (0 on hull key points, -1 elsewhere)
+        # has no positive key point outside the hull: the render plan's base
+        # then needs no static term (no pos27 pass)
+        self._static_zero = values is None
         if kp_mask is None or values is None:
             # hull key points (and the initial lattice when values is None)
             # derived on the device from the inside voxels
@@ -466,9 +470,11 @@ class ChannelLoop:
             if os.environ.get("FVR_RPLAN_TILE", "2x4") != "0" else None
         _lib.call("fvr_rplan_count", *self._rplan_geo(), unit_len.data_ptr(), _lib.ptr(row_len), _lib.stream_ptr())
         # the fill's static-positive stencil masks, computed now (off the fill's critical path)
-        self._pos27 = t.empty(int(np.prod(self.shape)), dtype=t.int32, device=self.dev)
-        _lib.call("fvr_rplan_pos27", self.grid, self.kp_dev.data_ptr(), self.values.data_ptr(), self.nch,
-                  self._pos27.data_ptr(), _lib.stream_ptr())
+        self._pos27 = None
+        if not self._static_zero:
+            self._pos27 = t.empty(int(np.prod(self.shape)), dtype=t.int32, device=self.dev)
+            _lib.call("fvr_rplan_pos27", self.grid, self.kp_dev.data_ptr(), self.values.data_ptr(), self.nch,
+                      self._pos27.data_ptr(), _lib.stream_ptr())
         return unit_len, row_len
 
     def _rplan_scan(self, unit_len, row_len) -> dict:
@@ -542,7 +548,8 @@ class ChannelLoop:
         except t.cuda.OutOfMemoryError:
             return False
         self.rp_order = rs["order"]
-        _lib.call("fvr_rplan_fill", *geo, self.values.data_ptr(), self.nch, off.data_ptr(), _lib.ptr(self.rp_order),
+        _lib.call("fvr_rplan_fill", *geo, None if self._static_zero else self.values.data_ptr(), self.nch,
+                  off.data_ptr(), _lib.ptr(self.rp_order),
                   _lib.ptr(self.rp_row_src), self._kp_map().data_ptr(), ent_a.data_ptr(), ent_b.data_ptr(),
                   base.data_ptr(), t_fin.data_ptr(), _lib.ptr(getattr(self, "_pos27", None)), int(self.rp_wide),
                   stream)
