@@ -104,58 +104,71 @@ __device__ __forceinline__ bool plan_ray(const fvr_camera_t* __restrict__ cams,
 // contiguous run, so carrying the previous sample's 8 corners and summing
 // matches removes most duplicates (about 2-3x fewer plan entries).  Count and
 // fill run the identical merge, so their entry counts agree.
+//
+// A corner's plan row (kp_map) is looked up when its run starts and carried
+// with it, so when the run ends one sample later the emit can go straight to
+// the row's cursor atomic: the lookup's latency overlaps a whole sample
+// instead of sitting on the fill's dependent chain.
+// emit(kp[8], row[8], w[8], mask): the corners (bits of mask) whose run ended.
 template <bool WEIGHTS, class Emit>
 __device__ __forceinline__ void ray_entries(const PlanRay& pr, const Geom& g, const uint8_t* __restrict__ inside,
-                                            double tau_keep, double alpha_l, float alpha_d, Emit&& emit) {
-    int pk[8];
+                                            double tau_keep, double alpha_l, float alpha_d,
+                                            const int32_t* __restrict__ kp_map, Emit&& emit) {
+    int pk[8], prow[8];
     float pw[8];
     bool have = false;
     const float edge = (float)g.edge;
     visit_inhull(pr.o, pr.d, g, inside, tau_keep, [&](int, const double* q, const int* c, double trans) {
-        int nk[8];
+        int nk[8], nrow[8];
         float nw[8];
         const int base_kp = c[0] * g.sx + c[1] * g.sy + c[2];
-        float e[3][2];
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8) nk[k8] = base_kp + (k8 >> 2) * g.sx + ((k8 >> 1) & 1) * g.sy + (k8 & 1);
+        // which corners continue a run of the previous sample (their row and
+        // weight so far come along), and which of the previous runs end
+        uint32_t carried = 0, cont = 0;
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+            nrow[n] = 0;
+            nw[n] = 0.f;
+#pragma unroll
+            for (int p = 0; p < 8; ++p)
+                if (have && pk[p] == nk[n]) {
+                    nrow[n] = prow[p];
+                    if (WEIGHTS) nw[n] = pw[p];
+                    carried |= 1u << p;
+                    cont |= 1u << n;
+                }
+        }
+#pragma unroll
+        for (int n = 0; n < 8; ++n)
+            if (!((cont >> n) & 1u)) nrow[n] = __ldg(kp_map + nk[n]);  // a run starts: its row
         if (WEIGHTS) {
+            float e[3][2];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const float f = (float)(q[a] - (double)c[a]);
                 e[a][0] = f * edge;
                 e[a][1] = (f - 1.0f) * edge;
             }
-        }
-        const float base = WEIGHTS ? (float)(alpha_l * trans) : 0.f;
+            const float base = (float)(alpha_l * trans);
 #pragma unroll
-        for (int k8 = 0; k8 < 8; ++k8) {
-            const int cx = k8 >> 2, cy = (k8 >> 1) & 1, cz = k8 & 1;
-            nk[k8] = base_kp + cx * g.sx + cy * g.sy + cz;
-            if (WEIGHTS) {
+            for (int k8 = 0; k8 < 8; ++k8) {
+                const int cx = k8 >> 2, cy = (k8 >> 1) & 1, cz = k8 & 1;
                 const float dist = sqrtf(fmaf(e[0][cx], e[0][cx], fmaf(e[1][cy], e[1][cy], e[2][cz] * e[2][cz])));
-                nw[k8] = base * expf(-alpha_d * dist);
-            } else {
-                nw[k8] = 0.f;
+                nw[k8] += base * expf(-alpha_d * dist);
             }
         }
-        if (have) {
-            uint32_t carried = 0;
-#pragma unroll
-            for (int n = 0; n < 8; ++n)
-#pragma unroll
-                for (int p = 0; p < 8; ++p)
-                    if (pk[p] == nk[n]) {
-                        if (WEIGHTS) nw[n] += pw[p];
-                        carried |= 1u << p;
-                    }
-            emit(pk, pw, ~carried & 0xFFu);  // the corners whose run ended
-        }
+        if (have) emit(pk, prow, pw, ~carried & 0xFFu);  // the corners whose run ended
 #pragma unroll
         for (int k8 = 0; k8 < 8; ++k8) {
             pk[k8] = nk[k8];
+            prow[k8] = nrow[k8];
             pw[k8] = nw[k8];
         }
         have = true;
     });
-    if (have) emit(pk, pw, 0xFFu);
+    if (have) emit(pk, prow, pw, 0xFFu);
 }
 
 __global__ void __launch_bounds__(128) plan_count_kernel(
@@ -166,10 +179,11 @@ __global__ void __launch_bounds__(128) plan_count_kernel(
     if (r >= n_rays) return;
     PlanRay pr;
     plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
-    ray_entries<false>(pr, g, inside, 1.0, 0.0, 0.f, [&](const int* pk, const float*, uint32_t mask) {
+    ray_entries<false>(pr, g, inside, 1.0, 0.0, 0.f, kp_map, [&](const int*, const int* row, const float*,
+                                                                    uint32_t mask) {
 #pragma unroll
         for (int p = 0; p < 8; ++p)
-            if ((mask >> p) & 1u) atomicAdd(counts + kp_map[pk[p]], 1);
+            if ((mask >> p) & 1u) atomicAdd(counts + row[p], 1);
     });
 }
 
@@ -227,13 +241,9 @@ struct SellMap {
     }
     // int2 (residual index, f32 W) entries of up to 8 corner runs (mask): the
     // wide deterministic plan, for residual indices of >= 2^24 (V * P)
-    __device__ __forceinline__ void put_wide_batch(const int* kp, const float* w, uint32_t mask,
-                                                   const int32_t* __restrict__ kp_map, uint32_t idx,
+    __device__ __forceinline__ void put_wide_batch(const int* row, const float* w, uint32_t mask, uint32_t idx,
                                                    int2* entries) const {
-        int row[8];
         long long t[8], ri[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) row[i] = ((mask >> i) & 1u) ? __ldg(kp_map + kp[i]) : 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             if ((mask >> i) & 1u) {
@@ -253,13 +263,9 @@ struct SellMap {
     // up to 8 entries of one sample's corners (mask): each dependent step
     // (row lookup, then cursor atomic + row word) is issued for all of them
     // before any result is used, so their latencies overlap
-    __device__ __forceinline__ void put6_batch(const int* kp, const float* w, uint32_t mask,
-                                               const int32_t* __restrict__ kp_map, uint32_t idx, uint32_t* a,
-                                               uint16_t* b) const {
-        int row[8];
+    __device__ __forceinline__ void put6_batch(const int* row, const float* w, uint32_t mask, uint32_t idx,
+                                               uint32_t* a, uint16_t* b) const {
         long long t[8], ri[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) row[i] = ((mask >> i) & 1u) ? __ldg(kp_map + kp[i]) : 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             if ((mask >> i) & 1u) {
@@ -291,11 +297,12 @@ __global__ void __launch_bounds__(128, FVR_PLAN_FILL_MINB) plan_fill_kernel(
     if (r >= n_rays) return;
     PlanRay pr;
     plan_ray(cams, ray_list, r, u0, v0, w, h, pr);
-    ray_entries<true>(pr, g, inside, tau_keep, alpha_l, alpha_d, [&](const int* pk, const float* pw, uint32_t mask) {
+    ray_entries<true>(pr, g, inside, tau_keep, alpha_l, alpha_d, kp_map,
+                      [&](const int*, const int* row, const float* pw, uint32_t mask) {
         if (!WIDE)
-            sm.put6_batch(pk, pw, mask, kp_map, (uint32_t)pr.res_index, ent_a, ent_b);
+            sm.put6_batch(row, pw, mask, (uint32_t)pr.res_index, ent_a, ent_b);
         else  // wide plan: int2 entries in ent_a
-            sm.put_wide_batch(pk, pw, mask, kp_map, (uint32_t)pr.res_index, reinterpret_cast<int2*>(ent_a));
+            sm.put_wide_batch(row, pw, mask, (uint32_t)pr.res_index, reinterpret_cast<int2*>(ent_a));
     });
 }
 
