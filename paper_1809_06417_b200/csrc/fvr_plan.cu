@@ -285,7 +285,7 @@ struct SellMap {
 };
 
 #ifndef FVR_PLAN_FILL_MINB
-#define FVR_PLAN_FILL_MINB 4
+#define FVR_PLAN_FILL_MINB 3
 #endif
 template <bool WIDE>
 __global__ void __launch_bounds__(128, FVR_PLAN_FILL_MINB) plan_fill_kernel(
