@@ -480,6 +480,14 @@ __global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
          sl += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int len = slice_len[sl];
         const long long off = slice_off[sl];
+        // the row's update operands, loaded now so their latency hides under
+        // the row's entries (the end-of-slice update stalled on them)
+        const int64_t pos0 = sl * 32 + lane;
+        const int64_t row0 = pos0 < n_rows ? (int64_t)__ldg(row_of_pos + pos0) : 0;
+        const int64_t idx0 = (!PACKED && pos0 < n_rows) ? (int64_t)__ldg(kp_index + row0) : 0;
+        float v0[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) v0[c] = (!PACKED && pos0 < n_rows) ? values[c * plane + idx0] : 0.f;
         const int2* e = entries + ((off / kSE) * 32 + lane) * kSE;  // chunks of kSE entries
         // E6: 6-byte entries (fvr_adjust_plan_fill, SellMap::store6): 16-byte
         // chunks of a words in `entries`, of 16-bit weight words in ent_b
@@ -541,17 +549,16 @@ __global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
                 }
             }
         }
-        const int64_t pos = sl * 32 + lane;
-        if (pos >= n_rows) continue;
-        const int64_t row = row_of_pos[pos];
+        if (pos0 >= n_rows) continue;
+        const int64_t row = row0;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
             if (PACKED) {
                 packed[c * n_rows + row] = acc[c];
             } else if (live[c] && acc[c] != 0) {
-                const int64_t idx = kp_index[row];
+                const int64_t idx = idx0;
                 float* vals = values + c * plane;
-                const double nv = (double)vals[idx] + (double)acc[c] * kFixInv;
+                const double nv = (double)v0[c] + (double)acc[c] * kFixInv;
                 const float f = (float)(nv > -1.0 ? nv : -1.0);
                 vals[idx] = f;
                 if (layout) layout_store(layout + 4 * c, NCH, layout_kind, sy, ny1, idx, f);

@@ -689,23 +689,23 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
                                base, t_fin, row_src, rows, units_x, units_per_view, n_views, w, h, src, kpv, rc,
                                residual, sq_partials, sq_stride);
     if (!fin.on) return;
-    // the last block to finish runs the loop's finalize (fvr_loop.cu)
-    __shared__ int s_last;
-    __shared__ double s_view[32];
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    // the last warp to finish runs the loop's finalize (fvr_loop.cu): a
+    // per-warp count, so no warp waits at a block barrier for its siblings
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
         __threadfence();
-        s_last = atomicAdd(&state->work_retired, 1) == (int)gridDim.x - 1;
+        last = atomicAdd(&state->work_retired, 1) == (int)((gridDim.x * blockDim.x) >> 5) - 1;
     }
-    __syncthreads();
-    if (!s_last) return;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
     __threadfence();
     for (int c = 0; c < NCH; ++c)
-        finalize_block(sq_partials + c * sq_stride, fin.n_views, fin.bpv, fin.pixels,
-                       fin.vol ? fin.vol + c * fin.n_vol : nullptr, fin.n_vol, fin.n_kp, fin.eps,
-                       fin.trace + c * fin.trace_stride, fin.trace_vol ? fin.trace_vol + c * fin.trace_stride : nullptr,
-                       state + c, s_view);
-    if (threadIdx.x == 0) state->work_retired = 0;
+        finalize_warp(sq_partials + c * sq_stride, fin.n_views, fin.bpv, fin.pixels,
+                      fin.vol ? fin.vol + c * fin.n_vol : nullptr, fin.n_vol, fin.n_kp, fin.eps,
+                      fin.trace + c * fin.trace_stride, fin.trace_vol ? fin.trace_vol + c * fin.trace_stride : nullptr,
+                      state + c);
+    if (lane == 0) state->work_retired = 0;
 }
 
 // kpv[i] = max(v, 0) at hull key point kp[i] of every channel (NCH = 1: f32,
