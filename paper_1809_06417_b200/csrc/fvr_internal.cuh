@@ -115,6 +115,7 @@ __device__ __forceinline__ void finalize_block(const double* sq, int n_views, in
     const int lane = threadIdx.x & 31;
     for (int v = threadIdx.x >> 5; v < n_views; v += blockDim.x >> 5) {
         double s = 0.0;
+#pragma unroll 4
         for (int b = lane; b < bpv; b += 32) s += __ldcg(sq + (int64_t)v * bpv + b);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -152,12 +153,26 @@ __device__ __forceinline__ void finalize_warp(const double* sq, int n_views, int
     if (st->done) return;
     const int lane = threadIdx.x & 31;
     double mine = 0.0;  // lane v keeps view v's RMSE (n_views <= 32)
-    for (int v = 0; v < n_views; ++v) {
-        double s = 0.0;
-        for (int b = lane; b < bpv; b += 32) s += __ldcg(sq + (int64_t)v * bpv + b);
+    // eight views at a time, loads of a view's lane-strided sequence issued
+    // ahead (the sums keep finalize_block's order: b = lane, lane + 32, ...)
+    constexpr int kV = 8;
+    for (int v0 = 0; v0 < n_views; v0 += kV) {
+        double s[kV];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == v) mine = sqrt(s / pixels);
+        for (int j = 0; j < kV; ++j) s[j] = 0.0;
+#pragma unroll 4
+        for (int b = lane; b < bpv; b += 32) {
+#pragma unroll
+            for (int j = 0; j < kV; ++j)
+                if (v0 + j < n_views) s[j] += __ldcg(sq + (int64_t)(v0 + j) * bpv + b);
+        }
+#pragma unroll
+        for (int j = 0; j < kV; ++j) {
+            double t = s[j];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+            if (lane == v0 + j) mine = sqrt(t / pixels);
+        }
     }
     double acc = 0.0;
     for (int i = 0; i < n_views; ++i) acc += __shfl_sync(0xffffffffu, mine, i);
