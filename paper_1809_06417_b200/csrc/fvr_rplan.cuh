@@ -679,9 +679,6 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
     pdl_wait();  // the previous gather's operand update and state
     if (all_done<NCH>(state)) return;
     const int lane = threadIdx.x & 31;
-    __shared__ int s_warps_done;  // the block's finished warps (fused finalize, see the end)
-    if (threadIdx.x == 0) s_warps_done = 0;
-    __syncthreads();
     const int64_t rows = (int64_t)n_units * 32;
     // units longest first (unit_order): the block scheduler then hands the
     // short bbox-margin units to SMs as they free up, with no long unit left
@@ -692,27 +689,23 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
                                base, t_fin, row_src, rows, units_x, units_per_view, n_views, w, h, src, kpv, rc,
                                residual, sq_partials, sq_stride);
     if (!fin.on) return;
-    // the last warp to finish runs the loop's finalize (fvr_loop.cu): warps
-    // count out of their block in shared memory and the block's last one
-    // counts the block out globally, so no warp waits at a block barrier for
-    // its siblings and the global counter sees one atomic per block (one per
-    // warp cost 10 us of serialised atomics at config 2)
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
+    // the last block to finish runs the loop's finalize (fvr_loop.cu)
+    __shared__ int s_last;
+    __shared__ double s_view[32];
+    __syncthreads();
+    if (threadIdx.x == 0) {
         __threadfence();
-        if (atomicAdd(&s_warps_done, 1) == (int)(blockDim.x >> 5) - 1)
-            last = atomicAdd(&state->work_retired, 1) == (int)gridDim.x - 1;
+        s_last = atomicAdd(&state->work_retired, 1) == (int)gridDim.x - 1;
     }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) return;
+    __syncthreads();
+    if (!s_last) return;
     __threadfence();
     for (int c = 0; c < NCH; ++c)
-        finalize_warp(sq_partials + c * sq_stride, fin.n_views, fin.bpv, fin.pixels,
-                      fin.vol ? fin.vol + c * fin.n_vol : nullptr, fin.n_vol, fin.n_kp, fin.eps,
-                      fin.trace + c * fin.trace_stride, fin.trace_vol ? fin.trace_vol + c * fin.trace_stride : nullptr,
-                      state + c);
-    if (lane == 0) state->work_retired = 0;
+        finalize_block(sq_partials + c * sq_stride, fin.n_views, fin.bpv, fin.pixels,
+                       fin.vol ? fin.vol + c * fin.n_vol : nullptr, fin.n_vol, fin.n_kp, fin.eps,
+                       fin.trace + c * fin.trace_stride, fin.trace_vol ? fin.trace_vol + c * fin.trace_stride : nullptr,
+                       state + c, s_view);
+    if (threadIdx.x == 0) state->work_retired = 0;
 }
 
 // kpv[i] = max(v, 0) at hull key point kp[i] of every channel (NCH = 1: f32,
