@@ -340,7 +340,8 @@ def run_gpu(args):
         stoch = {"value": 1000.0 / s_ms, "unit": "iters/s", "ms_per_step": s_ms, "steps": args.stochastic_steps,
                  "stage_ms": {n: float(np.mean([e[i].elapsed_time(e[i + 1]) for e in sevs]))
                               for i, n in enumerate(snames)},
-                 "adjust_path": ("sample-plan gather (nnz %d, %d samples)" % (sl.plan_nnz, sl.n_samples))
+                 "adjust_path": ("sample-plan gather (nnz %d, %d sample slots, %s entries)"
+                                 % (sl.plan_nnz, sl.n_samples, "6-byte" if sl.splan_e6 else "8-byte"))
                  if sl.plan else "ray-driven scatter",
                  "note": "deterministic_mode=False, g_sigma 0.1 (the reference default): per-sample Philox G"}
         del sl

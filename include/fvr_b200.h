@@ -329,7 +329,9 @@ int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int6
  * sample slots.  Sample ids come in blocks of 4 slots, one block per (ray,
  * k >> 2) group holding in-hull samples; sample (ray, k) has id 4 * block +
  * (k & 3), so ray_samples[r] = 4 * (groups of ray r).  Fill (ray_sid0 =
- * exclusive scan of ray_samples): entries (sample id, W) unmerged,
+ * exclusive scan of ray_samples): entries (sample id, W) unmerged -- 6-byte
+ * (the deterministic plan's layout, sample id < 2^24) when entries_b is
+ * given, int2 otherwise --
  * sample_meta[block] = (ray index, group << 4 | mask of used slots).
  * Per iteration fvr_loop_weighted_residual (n_samples = total slots) writes
  * rho[sid] = residual[ray] * G(seed, iteration, ray_id_base + ray, k) -- one
@@ -345,8 +347,8 @@ int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int6
                          int32_t u0, int32_t v0, int32_t bbox_w, int32_t bbox_h,
                          const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
                          double alpha_d, const int32_t* kp_map, const int64_t* ray_sid0,
-                         const int64_t* row_info, int64_t* cursor, int32_t* entries, int32_t* sample_meta,
-                         void* stream);
+                         const int64_t* row_info, int64_t* cursor, int32_t* entries, uint32_t* entries_b,
+                         int32_t* sample_meta, void* stream);
 /* The stochastic mode's G = clip(N(1, g_sigma), 0, 2) for (seed, iteration,
  * ray, march index k) -- the counter-based replacement of the reference's
  * rng.normal draw (reconstruct.py:191-204); the weigh pass and the ray-driven

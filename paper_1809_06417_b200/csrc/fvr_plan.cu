@@ -343,11 +343,14 @@ __global__ void __launch_bounds__(128) splan_count_kernel(
     ray_slots[r] = 4 * groups;
 }
 
+// E6: 6-byte entries (sample id < 2^24 | weight exponent, 16 mantissa bits;
+// SellMap::store6 layout, read by the gather's 6-byte path); else int2.
+template <bool E6>
 __global__ void __launch_bounds__(128) splan_fill_kernel(
     const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
     int u0, int v0, int w, int h, const uint8_t* __restrict__ inside, Geom g, double tau_keep,
     double alpha_l, float alpha_d, const int32_t* __restrict__ kp_map, const long long* __restrict__ ray_sid0,
-    SellMap sm, int2* __restrict__ entries, int2* __restrict__ meta) {
+    SellMap sm, int2* __restrict__ entries, uint16_t* __restrict__ ent_b, int2* __restrict__ meta) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_rays) return;
     PlanRay pr;
@@ -382,7 +385,14 @@ __global__ void __launch_bounds__(128) splan_fill_kernel(
             wgt[k8] = base * expf(-alpha_d * dist);
             kp[k8] = base_kp + cx * g.sx + cy * g.sy + cz;
         }
-        sm.put8_batch(kp, wgt, kp_map, (int)sid, entries);
+        if (E6) {
+            int row[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) row[i] = __ldg(kp_map + kp[i]);
+            sm.put6_batch(row, wgt, 0xFFu, (uint32_t)sid, reinterpret_cast<uint32_t*>(entries), ent_b);
+        } else {
+            sm.put8_batch(kp, wgt, kp_map, (int)sid, entries);
+        }
     });
     if (prev >= 0) meta[blk] = make_int2((int)r, (prev << 4) | mask);
 }
@@ -700,16 +710,23 @@ extern "C" int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray
                                     const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
                                     double alpha_d, const int32_t* kp_map, const int64_t* ray_sid0,
                                     const int64_t* row_info, int64_t* cursor,
-                                    int32_t* entries, int32_t* sample_meta, void* stream) {
+                                    int32_t* entries, uint32_t* entries_b, int32_t* sample_meta, void* stream) {
     FVR_TRY_BEGIN
     if (int rc = check_grid(grid)) return rc;
     if (n_rays == 0) return FVR_OK;
     const Geom g = make_geom(grid);
-    splan_fill_kernel<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-        cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d, kp_map,
-        reinterpret_cast<const long long*>(ray_sid0),
-        SellMap{reinterpret_cast<const long long*>(row_info), reinterpret_cast<unsigned long long*>(cursor)},
-        reinterpret_cast<int2*>(entries), reinterpret_cast<int2*>(sample_meta));
+    const SellMap sm{reinterpret_cast<const long long*>(row_info), reinterpret_cast<unsigned long long*>(cursor)};
+    const unsigned blocks = (unsigned)((n_rays + 127) / 128);
+    if (entries_b)
+        splan_fill_kernel<true><<<blocks, 128, 0, (cudaStream_t)stream>>>(
+            cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d, kp_map,
+            reinterpret_cast<const long long*>(ray_sid0), sm, reinterpret_cast<int2*>(entries),
+            reinterpret_cast<uint16_t*>(entries_b), reinterpret_cast<int2*>(sample_meta));
+    else
+        splan_fill_kernel<false><<<blocks, 128, 0, (cudaStream_t)stream>>>(
+            cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d, kp_map,
+            reinterpret_cast<const long long*>(ray_sid0), sm, reinterpret_cast<int2*>(entries), nullptr,
+            reinterpret_cast<int2*>(sample_meta));
     return check_launch("sample_plan_fill");
     FVR_TRY_END
 }

@@ -367,6 +367,7 @@ class ChannelLoop:
         self.sample_plan = self.plan and loop_cfg.stochastic
         self.plan_nnz = 0
         self.n_samples = 0
+        self.splan_e6 = False
         self.rho = None
         # Both operators' count passes are enqueued, their sizes read with one
         # synchronisation, and the two fills run concurrently (the adjust
@@ -723,8 +724,9 @@ class ChannelLoop:
         slice_len[: self.n_kp] = counts[order]
         slice_len = slice_len.view(n_slices, 32).amax(1).contiguous()
         # whole lane chunks (fvr_plan.cu): 16 bytes of six-byte entries (8), or
-        # 32 bytes of eight-byte (sample / wide) entries (kSE = 4)
-        slice_len = (slice_len + 3) & ~3 if (self.sample_plan or self.adj_wide) else (slice_len + 7) & ~7
+        # 32 bytes of eight-byte (wide) entries (kSE = 4); the sample plan's
+        # format is decided after the sizes reach the host, so it pads to 8
+        slice_len = (slice_len + 3) & ~3 if self.adj_wide else (slice_len + 7) & ~7
         slice_off = t.zeros(n_slices + 1, dtype=t.int64, device=dev)
         slice_off[1:] = t.cumsum(slice_len.long(), 0)
         sizes = [slice_off[-1], counts.long().sum()]
@@ -746,23 +748,25 @@ class ChannelLoop:
         slots = int(sizes[0]) * 32
         nnz = int(sizes[1])
         n_samples = int(sizes[2]) if self.sample_plan else 0
+        # the sample plan's entries are 6 bytes while sample ids fit 24 bits
+        self.splan_e6 = self.sample_plan and n_samples < (1 << 24) and os.environ.get("FVR_WIDE_PLANS") != "1"
         # entries + per-sample (meta: 8 B, rho: 4 B per channel slot) + the cursor
-        need = (8 if (self.sample_plan or self.adj_wide) else 6) * slots + (2 + 4 * self.pitch) * n_samples + \
-            8 * self.n_kp
+        need = (8 if ((self.sample_plan and not self.splan_e6) or self.adj_wide) else 6) * slots + \
+            (2 + 4 * self.pitch) * n_samples + 8 * self.n_kp
         if need > self.PLAN_MAX_BYTES or n_samples >= 2 ** 31:
             return False
         try:
             cursor = t.zeros(self.n_kp, dtype=t.int64, device=dev)
-            if self.sample_plan or self.adj_wide:  # int2 (sample id or residual index, W)
+            if (self.sample_plan and not self.splan_e6) or self.adj_wide:  # int2 (sample id / residual index, W)
                 entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
                 entries_b = None
-                if self.sample_plan:
-                    sid0 = t.zeros(self.n_rays, dtype=t.int64, device=dev)
-                    meta = t.empty(max(n_samples // 2, 2), dtype=t.int32, device=dev)  # int2 per 4-slot block
-                    rho = t.zeros((max(n_samples, 1), self.pitch), dtype=t.float32, device=dev)
-            else:  # 6 bytes: residual index (24 bits) + 24-bit weight
+            else:  # 6 bytes: sample id or residual index (24 bits) + 24-bit weight
                 entries = t.zeros(max(slots, 2), dtype=t.int32, device=dev)
                 entries_b = t.zeros(max(slots // 2, 1), dtype=t.int32, device=dev)
+            if self.sample_plan:
+                sid0 = t.zeros(self.n_rays, dtype=t.int64, device=dev)
+                meta = t.empty(max(n_samples // 2, 2), dtype=t.int32, device=dev)  # int2 per 4-slot block
+                rho = t.zeros((max(n_samples, 1), self.pitch), dtype=t.float32, device=dev)
         except t.cuda.OutOfMemoryError:
             return False
         sell = (pc["row_info"].data_ptr(), cursor.data_ptr(), entries.data_ptr())
@@ -773,7 +777,7 @@ class ChannelLoop:
             self.rho = rho
             keep.append(sid0)
             _lib.call("fvr_sample_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff,
-                      pc["kp_map"].data_ptr(), sid0.data_ptr(), *sell, meta.data_ptr(), stream)
+                      pc["kp_map"].data_ptr(), sid0.data_ptr(), *sell, _lib.ptr(entries_b), meta.data_ptr(), stream)
             self.sample_meta = meta
             self.n_samples = n_samples
         else:
