@@ -491,8 +491,13 @@ __global__ void __launch_bounds__(128) rplan_count_kernel(
 
 // Fill pass: rows in SELL-32 order; base[c * rows + r] and t_fin[r] per row
 // r = unit * 32 + lane (entries beyond a row's length stay (0, 0.0)).
+// 5 CTAs per SM (96 registers, no spills): config 2 fill 1.44 ms, against
+// 2.10 at the compiler's 122 registers (4 CTAs) and 1.48 at 6 (spills)
+#ifndef FVR_RPLAN_FILL_MINB
+#define FVR_RPLAN_FILL_MINB 5
+#endif
 template <bool SCAT, bool WIDE>
-__global__ void __launch_bounds__(128) rplan_fill_kernel(
+__global__ void __launch_bounds__(128, FVR_RPLAN_FILL_MINB) rplan_fill_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
     int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
     const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch, int64_t plane,
