@@ -16,8 +16,6 @@
 // ncu on the ray-driven scatter (fvr_adjust.cu, kept for stochastic mode and
 // the operator layer): 504 us per iteration at config 2, L2 56% busy with
 // 62 M RED.ADD.64, IPC 1.25 (profiles/r1a_*).
-#include <cstdlib>
-
 #include "fvr_internal.cuh"
 
 namespace fvr {
@@ -580,124 +578,6 @@ __global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
     }
 }
 
-// The 6-byte gather with its entry stream double-buffered through shared
-// memory by cp.async: while a warp gathers the residuals of batch t, batch
-// t + 1 of its slice is already on its way, with no registers held for it
-// (the plain gather waits for its entries, then for the residual gathers
-// they index: two dependent latencies per batch).  16 entries per lane per
-// batch = four 16-byte a chunks + two 16-byte weight chunks per lane.
-constexpr int kGaB = 16;               // entries per lane per batch
-constexpr int kGaChunks = kGaB / 4 + kGaB / 8;  // 16-byte chunks per lane per batch
-constexpr int kGaWarps = 8;            // warps per CTA
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <bool PACKED, int NCH>
-__global__ void __launch_bounds__(32 * kGaWarps, 4) gather_async_kernel(
-    const int32_t* __restrict__ slice_len, const long long* __restrict__ slice_off,
-    const int32_t* __restrict__ row_of_pos, const uint32_t* __restrict__ ent_a, const uint32_t* __restrict__ ent_b,
-    int64_t n_rows, const float* __restrict__ residual, const int32_t* __restrict__ kp_index,
-    float* __restrict__ values, int64_t plane, float* __restrict__ layout, int layout_kind, int sy, int ny1,
-    float* __restrict__ kpv, long long* __restrict__ packed, const fvr_loop_state_t* __restrict__ state) {
-    pdl_trigger();
-    pdl_wait();
-    __shared__ uint4 s_buf[kGaWarps][2][kGaChunks][32];
-    bool live[NCH];
-    bool any = false;
-#pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-        live[c] = !(state && state[c].done);
-        any = any || live[c];
-    }
-    if (!any) return;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t n_slices = (n_rows + 31) >> 5;
-    for (int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < n_slices;
-         sl += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int len = slice_len[sl];
-        const long long off = slice_off[sl];
-        const int64_t pos0 = sl * 32 + lane;
-        const int64_t row0 = pos0 < n_rows ? (int64_t)__ldg(row_of_pos + pos0) : 0;
-        const int64_t idx0 = (!PACKED && pos0 < n_rows) ? (int64_t)__ldg(kp_index + row0) : 0;
-        float v0[NCH];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) v0[c] = (!PACKED && pos0 < n_rows) ? values[c * plane + idx0] : 0.f;
-        const uint4* ea = reinterpret_cast<const uint4*>(ent_a) + (off >> 2) * 32 + lane;
-        const uint4* eb = reinterpret_cast<const uint4*>(ent_b) + (off >> 3) * 32 + lane;
-        auto issue = [&](int t, int buf) {  // batch t's chunks -> buffer buf (zero past len)
-#pragma unroll
-            for (int i = 0; i < kGaB / 4; ++i)
-                cp_async16(&s_buf[wib][buf][i][lane], ea + (int64_t)(t / 4 + i) * 32, t + 4 * i < len);
-#pragma unroll
-            for (int i = 0; i < kGaB / 8; ++i)
-                cp_async16(&s_buf[wib][buf][kGaB / 4 + i][lane], eb + (int64_t)(t / 8 + i) * 32, t + 8 * i < len);
-            cp_async_commit();
-        };
-        long long acc[NCH];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) acc[c] = 0;
-        __syncwarp();
-        if (len > 0) issue(0, 0);
-        for (int t = 0, buf = 0; t < len; t += kGaB, buf ^= 1) {
-            if (t + kGaB < len) {
-                issue(t + kGaB, buf ^ 1);
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
-            __syncwarp();
-            uint4 av[kGaB / 4], bv[kGaB / 8];
-#pragma unroll
-            for (int i = 0; i < kGaB / 4; ++i) av[i] = s_buf[wib][buf][i][lane];
-#pragma unroll
-            for (int i = 0; i < kGaB / 8; ++i) bv[i] = s_buf[wib][buf][kGaB / 4 + i][lane];
-            __syncwarp();  // the buffer is refilled two batches on
-#pragma unroll
-            for (int i = 0; i < kGaB; ++i) {
-                const uint4& q = av[i / 4];
-                const uint32_t a = (i & 3) == 0 ? q.x : (i & 3) == 1 ? q.y : (i & 3) == 2 ? q.z : q.w;
-                const uint4& hq = bv[i / 8];
-                const uint32_t hw = ((i & 7) >> 1) == 0 ? hq.x : ((i & 7) >> 1) == 1 ? hq.y : ((i & 7) >> 1) == 2 ? hq.z : hq.w;
-                const uint32_t half = (i & 1) ? (hw >> 16) : (hw & 0xFFFFu);
-                const float wgt = __uint_as_float(((a >> 24) << 23) | (half << 7));
-                const uint32_t ridx = a & 0xFFFFFFu;
-                if (NCH == 1) {
-                    acc[0] += __float2ll_rn(__ldg(residual + ridx) * wgt * 4294967296.0f);
-                } else {
-                    const float4 r = __ldg(reinterpret_cast<const float4*>(residual) + ridx);
-                    const float rr[3] = {r.x, r.y, r.z};
-#pragma unroll
-                    for (int c = 0; c < NCH; ++c) acc[c] += __float2ll_rn(rr[c] * wgt * 4294967296.0f);
-                }
-            }
-        }
-        if (pos0 >= n_rows) continue;
-        const int64_t row = row0;
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            if (PACKED) {
-                packed[c * n_rows + row] = acc[c];
-            } else if (live[c] && acc[c] != 0) {
-                float* vals = values + c * plane;
-                const double nv = (double)v0[c] + (double)acc[c] * kFixInv;
-                const float f = (float)(nv > -1.0 ? nv : -1.0);
-                vals[idx0] = f;
-                if (layout) layout_store(layout + 4 * c, NCH, layout_kind, sy, ny1, idx0, f);
-                if (kpv) kpv[row * (NCH == 1 ? 1 : 4) + c] = fmaxf(f, 0.f);
-            }
-        }
-    }
-}
-
 // Apply a packed (all-reduced) correction: one thread per hull key point.
 __global__ void update_packed_kernel(const long long* __restrict__ packed, int64_t n_rows,
                                      const int32_t* __restrict__ kp_index, float* __restrict__ values,
@@ -760,14 +640,6 @@ extern "C" int fvr_adjust_plan_fill(const fvr_camera_t* cams, const int32_t* ray
     FVR_TRY_END
 }
 
-static bool gather_async_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("FVR_GATHER_ASYNC");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
 extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_off, const int32_t* row_of_pos,
                                const int32_t* entries, const uint32_t* entries_b, int64_t n_kp, const float* residual, int32_t n_channels,
                                const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
@@ -789,13 +661,8 @@ extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_of
 #define FVR_GATHER(P, C, E)                                                                                  \
     e = launch_pdl(gather_kernel<P, C, E>, (unsigned)blocks, 256, st, slice_len, so, row_of_pos, en, entries_b,  \
                    n_kp, residual, kp_index, values, plane, layout, layout_kind, sy, ny1, kp_values, pk, state)
-#define FVR_GATHER_ASYNC(P, C)                                                                            \
-    e = launch_pdl(gather_async_kernel<P, C>, (unsigned)blocks, 32 * kGaWarps, st, slice_len, so, row_of_pos,  \
-                   reinterpret_cast<const uint32_t*>(entries), entries_b, n_kp, residual, kp_index, values,      \
-                   plane, layout, layout_kind, sy, ny1, kp_values, pk, state)
-#define FVR_GATHER_E(P, C)                                  \
-    if (entries_b && gather_async_enabled()) FVR_GATHER_ASYNC(P, C); \
-    else if (entries_b) FVR_GATHER(P, C, true);           \
+#define FVR_GATHER_E(P, C)           \
+    if (entries_b) FVR_GATHER(P, C, true); \
     else FVR_GATHER(P, C, false)
     if (packed) {
         if (n_channels == 1) { FVR_GATHER_E(true, 1); } else { FVR_GATHER_E(true, 3); }
@@ -803,7 +670,6 @@ extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_of
         if (n_channels == 1) { FVR_GATHER_E(false, 1); } else { FVR_GATHER_E(false, 3); }
     }
 #undef FVR_GATHER_E
-#undef FVR_GATHER_ASYNC
 #undef FVR_GATHER
     if (e != cudaSuccess) return set_error(FVR_ERR_CUDA, std::string("loop_gather: ") + cudaGetErrorString(e));
     return check_launch("loop_gather");
