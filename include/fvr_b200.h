@@ -348,7 +348,14 @@ int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int6
                          const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
                          double alpha_d, const int32_t* kp_map, const int64_t* ray_sid0,
                          const int64_t* row_info, int64_t* cursor, int32_t* entries, uint32_t* entries_b,
-                         int32_t* sample_meta, void* stream);
+                         int32_t* sample_meta, int64_t* block_keys, void* stream);
+/* Spatial renumbering of the sample plan's blocks (block_keys from the fill,
+ * sorted: new_of_nat[natural block] = rank), so the sample ids one SELL slice
+ * of neighbouring key points reads sit close together (the gather's rho reads
+ * hit cache lines): entries (n_slots stored entries, 6-byte layout when e6)
+ * have their sample ids rewritten in place, meta_out[new] = meta_in[natural]. */
+int fvr_sample_plan_reorder(int32_t* entries, int64_t n_slots, int32_t e6, const int32_t* new_of_nat,
+                            int64_t n_blocks, const int32_t* meta_in, int32_t* meta_out, void* stream);
 /* The stochastic mode's G = clip(N(1, g_sigma), 0, 2) for (seed, iteration,
  * ray, march index k) -- the counter-based replacement of the reference's
  * rng.normal draw (reconstruct.py:191-204); the weigh pass and the ray-driven

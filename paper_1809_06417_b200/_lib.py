@@ -156,7 +156,8 @@ _SIGNATURES = {
     "fvr_sample_plan_count": (c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, _P, _P, _P,
                                       _P]),
     "fvr_sample_plan_fill": (c_int, [_P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _GRID, c_double,
-                                     c_double, c_double, _P, _P, _P, _P, _P, _P, _P, _P]),
+                                     c_double, c_double, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "fvr_sample_plan_reorder": (c_int, [_P, c_int64, c_int32, _P, c_int64, _P, _P, _P]),
     "fvr_loop_weighted_residual": (c_int, [_P, c_int64, _P, c_int32, c_int32, _P, c_int32, c_uint64, c_double,
                                            c_int64, _P, _P, c_int32, _P]),
     "fvr_stochastic_g": (c_int, [c_uint64, ctypes.c_uint32, _P, _P, c_int64, c_double, _P, _P]),

@@ -345,12 +345,24 @@ __global__ void __launch_bounds__(128) splan_count_kernel(
 
 // E6: 6-byte entries (sample id < 2^24 | weight exponent, 16 mantissa bits;
 // SellMap::store6 layout, read by the gather's 6-byte path); else int2.
+// blk_keys (may be NULL): per block, (Morton code of the cell of its first
+// sample) << 32 | block -- sorted, they renumber the blocks spatially
+// (fvr_sample_plan_reorder).
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {
+    v &= 0x3FFu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    return (v | (v << 2)) & 0x09249249u;
+}
+
 template <bool E6>
 __global__ void __launch_bounds__(128) splan_fill_kernel(
     const fvr_camera_t* __restrict__ cams, const int32_t* __restrict__ ray_list, int64_t n_rays,
     int u0, int v0, int w, int h, const uint8_t* __restrict__ inside, Geom g, double tau_keep,
     double alpha_l, float alpha_d, const int32_t* __restrict__ kp_map, const long long* __restrict__ ray_sid0,
-    SellMap sm, int2* __restrict__ entries, uint16_t* __restrict__ ent_b, int2* __restrict__ meta) {
+    SellMap sm, int2* __restrict__ entries, uint16_t* __restrict__ ent_b, int2* __restrict__ meta,
+    unsigned long long* __restrict__ blk_keys) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_rays) return;
     PlanRay pr;
@@ -364,6 +376,9 @@ __global__ void __launch_bounds__(128) splan_fill_kernel(
             prev = k >> 2;
             mask = 0;
             ++blk;
+            if (blk_keys)
+                blk_keys[blk] = ((unsigned long long)((spread10(c[0]) << 2) | (spread10(c[1]) << 1) | spread10(c[2]))
+                                 << 32) | (unsigned long long)blk;
         }
         mask |= 1 << (k & 3);
         const long long sid = blk * 4 + (k & 3);
@@ -710,7 +725,8 @@ extern "C" int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray
                                     const uint8_t* inside_vox, fvr_grid_t grid, double tau, double alpha_l,
                                     double alpha_d, const int32_t* kp_map, const int64_t* ray_sid0,
                                     const int64_t* row_info, int64_t* cursor,
-                                    int32_t* entries, uint32_t* entries_b, int32_t* sample_meta, void* stream) {
+                                    int32_t* entries, uint32_t* entries_b, int32_t* sample_meta,
+                                    int64_t* block_keys, void* stream) {
     FVR_TRY_BEGIN
     if (int rc = check_grid(grid)) return rc;
     if (n_rays == 0) return FVR_OK;
@@ -721,13 +737,63 @@ extern "C" int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray
         splan_fill_kernel<true><<<blocks, 128, 0, (cudaStream_t)stream>>>(
             cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d, kp_map,
             reinterpret_cast<const long long*>(ray_sid0), sm, reinterpret_cast<int2*>(entries),
-            reinterpret_cast<uint16_t*>(entries_b), reinterpret_cast<int2*>(sample_meta));
+            reinterpret_cast<uint16_t*>(entries_b), reinterpret_cast<int2*>(sample_meta),
+            reinterpret_cast<unsigned long long*>(block_keys));
     else
         splan_fill_kernel<false><<<blocks, 128, 0, (cudaStream_t)stream>>>(
             cams, ray_list, n_rays, u0, v0, bbox_w, bbox_h, inside_vox, g, 1.0 - tau, alpha_l, (float)alpha_d, kp_map,
             reinterpret_cast<const long long*>(ray_sid0), sm, reinterpret_cast<int2*>(entries), nullptr,
-            reinterpret_cast<int2*>(sample_meta));
+            reinterpret_cast<int2*>(sample_meta), reinterpret_cast<unsigned long long*>(block_keys));
     return check_launch("sample_plan_fill");
+    FVR_TRY_END
+}
+
+// Renumber the sample plan's blocks: sid -> new_of_nat[sid >> 2] * 4 + (sid & 3)
+// in every stored entry (6-byte: the low 24 bits of the a word; int2: .x),
+// and meta_out[new] = meta_in[nat].
+template <bool E6>
+__global__ void splan_renumber_kernel(uint32_t* __restrict__ words, int64_t n_entries,
+                                      const int32_t* __restrict__ new_of_nat) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_entries;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (E6) {
+            const uint32_t a = words[i];
+            const uint32_t sid = a & 0xFFFFFFu;
+            words[i] = (a & 0xFF000000u) | (uint32_t)(__ldg(new_of_nat + (sid >> 2)) * 4 + (sid & 3));
+        } else {
+            const uint32_t sid = words[2 * i];
+            words[2 * i] = (uint32_t)(__ldg(new_of_nat + (sid >> 2)) * 4 + (sid & 3));
+        }
+    }
+}
+__global__ void splan_permute_meta_kernel(const int2* __restrict__ meta_in, int64_t n_blocks,
+                                          const int32_t* __restrict__ new_of_nat, int2* __restrict__ meta_out) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n_blocks; b += (int64_t)gridDim.x * blockDim.x)
+        meta_out[__ldg(new_of_nat + b)] = meta_in[b];
+}
+
+extern "C" int fvr_sample_plan_reorder(int32_t* entries, int64_t n_slots, int32_t e6, const int32_t* new_of_nat,
+                                       int64_t n_blocks, const int32_t* meta_in, int32_t* meta_out, void* stream) {
+    FVR_TRY_BEGIN
+    if (!entries || !new_of_nat || !meta_in || !meta_out) return set_error(FVR_ERR_INVALID, "NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t b = (n_slots + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    if (n_slots > 0) {
+        if (e6)
+            splan_renumber_kernel<true><<<(unsigned)b, 256, 0, st>>>(reinterpret_cast<uint32_t*>(entries), n_slots,
+                                                                      new_of_nat);
+        else
+            splan_renumber_kernel<false><<<(unsigned)b, 256, 0, st>>>(reinterpret_cast<uint32_t*>(entries), n_slots,
+                                                                       new_of_nat);
+        count_launch(1);
+    }
+    int64_t bb = (n_blocks + 255) / 256;
+    if (bb > 148 * 16) bb = 148 * 16;
+    if (n_blocks > 0)
+        splan_permute_meta_kernel<<<(unsigned)bb, 256, 0, st>>>(reinterpret_cast<const int2*>(meta_in), n_blocks,
+                                                                new_of_nat, reinterpret_cast<int2*>(meta_out));
+    return check_launch("sample_plan_reorder");
     FVR_TRY_END
 }
 

@@ -776,8 +776,22 @@ class ChannelLoop:
             sid0[1:] = t.cumsum(pc["ray_samples"][:-1].long(), 0)
             self.rho = rho
             keep.append(sid0)
+            n_blocks = n_samples // 4
+            # renumber the blocks spatially (Morton order of each group's first
+            # cell) so a slice's rho reads sit close together
+            spatial = max(self.shape) <= 1024 and os.environ.get("FVR_SPLAN_SPATIAL", "1") == "1" and n_blocks > 0
+            keys = t.empty(n_blocks, dtype=t.int64, device=dev) if spatial else None
             _lib.call("fvr_sample_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff,
-                      pc["kp_map"].data_ptr(), sid0.data_ptr(), *sell, _lib.ptr(entries_b), meta.data_ptr(), stream)
+                      pc["kp_map"].data_ptr(), sid0.data_ptr(), *sell, _lib.ptr(entries_b), meta.data_ptr(),
+                      _lib.ptr(keys), stream)
+            if spatial:
+                order = t.sort(keys).indices
+                new_of_nat = t.empty(n_blocks, dtype=t.int32, device=dev)
+                new_of_nat[order] = t.arange(n_blocks, dtype=t.int32, device=dev)
+                meta_new = t.empty_like(meta)
+                _lib.call("fvr_sample_plan_reorder", entries.data_ptr(), slots, int(entries_b is not None),
+                          new_of_nat.data_ptr(), n_blocks, meta.data_ptr(), meta_new.data_ptr(), stream)
+                meta = meta_new
             self.sample_meta = meta
             self.n_samples = n_samples
         else:
