@@ -418,6 +418,8 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
     const float* __restrict__ residual, uint64_t seed, float g_sigma, int64_t ray_id_base,
     float* __restrict__ rho, const fvr_loop_state_t* __restrict__ state, int it_back) {
     pdl_trigger();
+    if ((int64_t)blockIdx.x * blockDim.x + threadIdx.x < n_blocks)  // its first meta word into L2
+        prefetch_l2(bmeta + (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
     pdl_wait();  // the render's residual and state
     // the live channels share the iteration count (a converged one stops
     // counting); it_back = 1 when this iteration's finalize already ran
@@ -489,6 +491,23 @@ __global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
     float* __restrict__ values, int64_t plane, float* __restrict__ layout, int layout_kind, int sy, int ny1,
     float* __restrict__ kpv, long long* __restrict__ packed, const fvr_loop_state_t* __restrict__ state) {
     pdl_trigger();
+    {  // the first slice's first chunks into L2 while the predecessor finishes
+        const int64_t sl0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        if (sl0 < ((n_rows + 31) >> 5)) {
+            const long long off = __ldg(slice_off + sl0);
+            const int len = __ldg(slice_len + sl0);
+            const int ln = threadIdx.x & 31;
+            if (E6) {
+                for (int i = 0; i < 8 && 4 * i < len; ++i)
+                    prefetch_l2(reinterpret_cast<const uint4*>(entries) + ((off >> 2) + i) * 32 + ln);
+                for (int i = 0; i < 4 && 8 * i < len; ++i)
+                    prefetch_l2(reinterpret_cast<const uint4*>(ent_b) + ((off >> 3) + i) * 32 + ln);
+            } else {
+                for (int i = 0; i < 6 && kSE * i < len; ++i)
+                    prefetch_l2(entries + ((off / kSE + i) * 32 + ln) * kSE);
+            }
+        }
+    }
     pdl_wait();  // the render's residual / the weigh's rho, and the state
     bool live[NCH];
     bool any = false;

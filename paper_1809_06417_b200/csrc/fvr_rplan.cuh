@@ -681,9 +681,21 @@ __global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
     RenderConsts rc, float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride,
     fvr_loop_state_t* __restrict__ state, RplanFinalize fin) {
     pdl_trigger();
+    const int lane = threadIdx.x & 31;
+    {  // the first unit's first chunks into L2 while the previous gather finishes
+        const int u0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+        if (u0 < n_units) {
+            const int unit = unit_order ? __ldg(unit_order + u0) : u0;
+            const long long off = __ldg(unit_off + unit);
+            const int len = __ldg(unit_len + unit);
+            constexpr int kB = WIDE ? kRpA : kRpB;
+            for (int i = 0; i < 4 && i * kRpA < len; ++i)
+                prefetch_l2(ent_a + ((off / kRpA + i) * 32 + lane) * kRpA);
+            for (int i = 0; i < 2 && i * kB < len; ++i) prefetch_l2(ent_b + ((off / kB + i) * 32 + lane) * kRpA);
+        }
+    }
     pdl_wait();  // the previous gather's operand update and state
     if (all_done<NCH>(state)) return;
-    const int lane = threadIdx.x & 31;
     const int64_t rows = (int64_t)n_units * 32;
     // units longest first (unit_order): the block scheduler then hands the
     // short bbox-margin units to SMs as they free up, with no long unit left
