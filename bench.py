@@ -265,7 +265,6 @@ def run_gpu(args):
 
     sc = make_scene()
     dev = torch.device("cuda", local)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
     def barrier():
         if world > 1:
@@ -275,8 +274,14 @@ def run_gpu(args):
     stream = _lib.stream_ptr()
 
     def timed_loop(deterministic: bool, steps: int, warmup: int, sampler=None):
-        """K timed iterations of one ChannelLoop; per-stage CUDA events."""
-        cfg = ReconstructionConfig(alpha_l=ALPHA_L, alpha_d=1.0, tau=TAU, max_iters=steps + warmup,
+        """K timed iterations of one ChannelLoop, then K more with an event
+        between every stage (the per-kernel breakdown the roofline uses).
+
+        The timed pass is one event pair around the K steps: the loop's
+        kernels chain through programmatic dependent launch, which an event
+        between them would break.  No L2 flush: every step streams the two
+        plans (0.75 GB at config 2) through a 126 MB L2."""
+        cfg = ReconstructionConfig(alpha_l=ALPHA_L, alpha_d=1.0, tau=TAU, max_iters=2 * steps + warmup,
                                    converge_eps=1e-12, deterministic_mode=deterministic, g_sigma=0.1, rng_seed=0)
         grid0 = _init_grid(sc["geom"], sc["hull"], "green")
         src = [im.data[sc["bbox"].slices][:, :, 0] for im in sc["images"]]
@@ -286,42 +291,47 @@ def run_gpu(args):
         stages = [(n, f) for n, f in loop.stages() if f is not None]
         names = [n for n, _ in stages]
 
-        def one_step(evs):
+        def one_step(evs=None):
             launches = 0
-            evs[0].record()
+            if evs:
+                evs[0].record()
             for i, (_, fn) in enumerate(stages):
                 launches += fn(stream)
-                evs[i + 1].record()
+                if evs:
+                    evs[i + 1].record()
             return launches
 
         def new_events():
             return [torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)]
 
         for _ in range(warmup):
-            flush.fill_(1.0)
-            one_step(new_events())
+            one_step()
         barrier()
-        all_evs = []
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         launches = 0
+        e0.record()
         for _ in range(steps):
-            flush.fill_(1.0)  # L2 flush between timed steps, outside the step's events
+            launches += one_step()
+        e1.record()
+        barrier()
+        timed_ms = e0.elapsed_time(e1)
+        all_evs = []
+        for _ in range(steps):  # the per-stage breakdown
             evs = new_events()
-            launches += one_step(evs)
+            one_step(evs)
             all_evs.append(evs)
         barrier()
         st = loop.read_state()
-        assert st["it"] == warmup + steps and not st["done"], st
-        return loop, names, all_evs, launches, grid0, src
+        assert st["it"] == warmup + 2 * steps and not st["done"], st
+        return loop, names, all_evs, launches, grid0, src, timed_ms
 
     # clocks: sampled from before the first timed step to after the last
     # e2e call (the deterministic, stochastic and e2e regions)
     sampler = ClockSampler(local)
     sampler.start()
     sampler.wait_first()
-    loop, names, all_evs, launches, grid0, src = timed_loop(True, args.steps, args.warmup)
-    step_ms = np.array([e[0].elapsed_time(e[-1]) for e in all_evs])
+    loop, names, all_evs, launches, grid0, src, total_ms = timed_loop(True, args.steps, args.warmup)
     part_ms = {n: float(np.mean([e[i].elapsed_time(e[i + 1]) for e in all_evs])) for i, n in enumerate(names)}
-    total_ms = float(step_ms.sum())
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -331,8 +341,8 @@ def run_gpu(args):
     # (deterministic_mode=False): same workload through the stochastic path
     stoch = None
     if args.stochastic_steps > 0:
-        sl, snames, sevs, _, _, _ = timed_loop(False, args.stochastic_steps, args.warmup)
-        s_ms = float(np.mean([e[0].elapsed_time(e[-1]) for e in sevs]))
+        sl, snames, sevs, _, _, _, s_total = timed_loop(False, args.stochastic_steps, args.warmup)
+        s_ms = s_total / args.stochastic_steps
         if world > 1:
             t = torch.tensor([s_ms], dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)

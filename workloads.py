@@ -29,7 +29,8 @@ CONFIGS = {1: (32, 4, 64), 2: (128, 8, 512), 3: (256, 16, 1024), 4: (512, 32, 10
 SIGMA_S = 0.1
 SCAT_DIRS = 32
 ALPHA_L = 0.006
-L2_NOTE = "256 MiB buffer written between timed steps (outside the step events)"
+L2_NOTE = ("no flush: inputs larger than L2 -- every step streams the render and adjust plans (0.75 GB at "
+           "config 2) through the 126 MB L2")
 
 
 def tau_n(n: int) -> float:
