@@ -151,49 +151,65 @@ __device__ double np_pairwise(const double* a, int n) {
     return res;
 }
 
-// One block: rows are temperatures; thread t handles rows t, t+blockDim, ...
-__global__ void __launch_bounds__(1024) ctmap_kernel(double t_min, double step, int n_steps,
-                                                     int append_max, double t_max,
-                                                     double* __restrict__ temps,
-                                                     double* __restrict__ entries) {
-    const int n = n_steps + (append_max ? 1 : 0);
+// The table in three launches (it was one 1024-thread block, 3.4 ms):
+// (1) one thread per (temperature, wavelength) node evaluates the Planck
+// radiance once (the three channels share it); (2) one thread per
+// temperature integrates the three channels (numpy's trapezoid terms and
+// pairwise sum) and maps XYZ to clipped linear sRGB; (3) one block finds the
+// peak and scales to 255.  Same operations per element as before, so the
+// same bits.
+__device__ __forceinline__ double ctmap_temperature(int row, double t_min, double step, int n, int append_max,
+                                                    double t_max) {
+    return (append_max && row == n - 1) ? t_max : __dadd_rn(t_min, __dmul_rn(step, (double)row));
+}
+
+__global__ void planck_nodes_kernel(double t_min, double step, int n, int append_max, double t_max,
+                                    double* __restrict__ temps, double* __restrict__ radiance) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * 81) return;
+    const int row = i / 81, j = i % 81;
+    const double T = ctmap_temperature(row, t_min, step, n, append_max, t_max);
+    if (j == 0) temps[row] = T;
+    const double lam = __dmul_rn(380.0 + 5.0 * j, 1e-9);
+    const double x = __ddiv_rn(kPlanckH * kLightC, __dmul_rn(__dmul_rn(lam, kBoltzmann), T));
+    const double amp = __ddiv_rn(2.0 * kPlanckH * (kLightC * kLightC), pow5_cr(lam));
+    radiance[i] = x > 700.0 ? __dmul_rn(amp, exp(-fmin(x, 1e6))) : __ddiv_rn(amp, expm1_cr(x));
+}
+
+__global__ void ctmap_rows_kernel(int n, const double* __restrict__ radiance, double* __restrict__ entries) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= n) return;
+    const double* L = radiance + (int64_t)row * 81;
+    double terms[80];
+    double xyz[3];
+    for (int c = 0; c < 3; ++c) {
+        const double* cmf = c == 0 ? kCieX : (c == 1 ? kCieY : kCieZ);
+        double y_prev = 0.0, lam_prev = 0.0;
+        for (int j = 0; j < 81; ++j) {
+            const double lam = __dmul_rn(380.0 + 5.0 * j, 1e-9);
+            const double y = __dmul_rn(L[j], cmf[j]);
+            if (j > 0) {
+                const double dl = __dsub_rn(lam, lam_prev);
+                terms[j - 1] = __ddiv_rn(__dmul_rn(dl, __dadd_rn(y, y_prev)), 2.0);
+            }
+            y_prev = y;
+            lam_prev = lam;
+        }
+        xyz[c] = np_pairwise(terms, 80);
+    }
+    for (int j = 0; j < 3; ++j) {
+        double t = __dmul_rn(xyz[0], kXyzToSrgb[3 * j]);
+        t = __fma_rn(xyz[1], kXyzToSrgb[3 * j + 1], t);
+        t = __fma_rn(xyz[2], kXyzToSrgb[3 * j + 2], t);
+        entries[3 * row + j] = t > 0.0 ? t : 0.0;  // np.maximum(rgb, 0)
+    }
+}
+
+// the peak (max is order independent), then entries / peak * 255
+__global__ void __launch_bounds__(1024) ctmap_normalize_kernel(int n, double* __restrict__ entries) {
     __shared__ double red[32];
     double local_max = 0.0;
-    double terms[80];
-    for (int row = threadIdx.x; row < n; row += blockDim.x) {
-        const double T = (append_max && row == n - 1) ? t_max
-                                                      : __dadd_rn(t_min, __dmul_rn(step, (double)row));
-        temps[row] = T;
-        double xyz[3];
-        for (int c = 0; c < 3; ++c) {
-            const double* cmf = c == 0 ? kCieX : (c == 1 ? kCieY : kCieZ);
-            double y_prev = 0.0, lam_prev = 0.0;
-            for (int j = 0; j < 81; ++j) {
-                const double lam = __dmul_rn(380.0 + 5.0 * j, 1e-9);
-                const double x = __ddiv_rn(kPlanckH * kLightC, __dmul_rn(__dmul_rn(lam, kBoltzmann), T));
-                const double amp = __ddiv_rn(2.0 * kPlanckH * (kLightC * kLightC), pow5_cr(lam));
-                const double L = x > 700.0 ? __dmul_rn(amp, exp(-fmin(x, 1e6)))
-                                           : __ddiv_rn(amp, expm1_cr(x));
-                const double y = __dmul_rn(L, cmf[j]);
-                if (j > 0) {
-                    const double dl = __dsub_rn(lam, lam_prev);
-                    terms[j - 1] = __ddiv_rn(__dmul_rn(dl, __dadd_rn(y, y_prev)), 2.0);
-                }
-                y_prev = y;
-                lam_prev = lam;
-            }
-            xyz[c] = np_pairwise(terms, 80);
-        }
-        for (int j = 0; j < 3; ++j) {
-            double t = __dmul_rn(xyz[0], kXyzToSrgb[3 * j]);
-            t = __fma_rn(xyz[1], kXyzToSrgb[3 * j + 1], t);
-            t = __fma_rn(xyz[2], kXyzToSrgb[3 * j + 2], t);
-            t = t > 0.0 ? t : 0.0;  // np.maximum(rgb, 0)
-            entries[3 * row + j] = t;
-            local_max = fmax(local_max, t);
-        }
-    }
-    // global peak (max is order independent)
+    for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) local_max = fmax(local_max, entries[i]);
     for (int off = 16; off > 0; off >>= 1)
         local_max = fmax(local_max, __shfl_xor_sync(0xffffffffu, local_max, off));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local_max;
@@ -205,10 +221,7 @@ __global__ void __launch_bounds__(1024) ctmap_kernel(double t_min, double step, 
     }
     __syncthreads();
     const double peak = red[0];
-    __syncthreads();
-    for (int row = threadIdx.x; row < n; row += blockDim.x)
-        for (int j = 0; j < 3; ++j)
-            entries[3 * row + j] = __dmul_rn(__ddiv_rn(entries[3 * row + j], peak), 255.0);
+    for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) entries[i] = __dmul_rn(__ddiv_rn(entries[i], peak), 255.0);
 }
 
 // np.interp(clip(g, lo, hi), green, temps) -- see the file comment.
@@ -344,8 +357,17 @@ extern "C" int fvr_ctmap_build(double t_min, double step, int32_t n, int32_t app
                                double t_max, double* temps, double* entries, void* stream) {
     FVR_TRY_BEGIN
     if (n < 1) return set_error(FVR_ERR_INVALID, "empty temperature table");
-    ctmap_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(t_min, step, n, append_t_max, t_max, temps,
-                                                       entries);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int rows = n + (append_t_max ? 1 : 0);
+    double* radiance = nullptr;
+    if (cudaMallocAsync(&radiance, sizeof(double) * (size_t)rows * 81, st) != cudaSuccess)
+        return set_error(FVR_ERR_CUDA, "ctmap_build: cannot allocate the radiance scratch");
+    planck_nodes_kernel<<<(rows * 81 + 127) / 128, 128, 0, st>>>(t_min, step, rows, append_t_max, t_max, temps,
+                                                                 radiance);
+    ctmap_rows_kernel<<<(rows + 63) / 64, 64, 0, st>>>(rows, radiance, entries);
+    ctmap_normalize_kernel<<<1, 1024, 0, st>>>(rows, entries);
+    count_launch(2);
+    cudaFreeAsync(radiance, st);
     return check_launch("ctmap_build");
     FVR_TRY_END
 }
