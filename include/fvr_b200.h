@@ -237,12 +237,6 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
  * `finalize` (single-rank loops) the last block to finish runs
  * fvr_loop_finalize on state (one launch less per iteration; the block
  * counter is state[0].work_retired).
- * halves != 0 (count) / half0_len != NULL (fill): every row is built by two
- * threads, samples 1..n/2 and n/2+1..n, each with its own merge window (a run
- * cut at the middle gives two entries); the count writes row_len as [half 0
- * rows | half 1 rows] (natural rows) and leaves unit_len to the caller (from
- * the sums); the fill takes the half-0 lengths and writes the second half
- * after the first (base must be zeroed when values != NULL: the halves add).
  * fvr_rplan_fill with values == NULL asserts that no key point outside
  * `dynamic` is positive (base then holds nothing but the background term).
  * wide != 0 (fill and render must agree): 8-byte entries, u32 column in
@@ -254,14 +248,12 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
 int fvr_rplan_chunk_entries(void);
 int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                     int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
-                    const uint8_t* dynamic, int32_t* unit_len, int32_t* row_len,
-                    int32_t halves, void* stream);
+                    const uint8_t* dynamic, int32_t* unit_len, int32_t* row_len, void* stream);
 int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                    int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params, const uint8_t* occ,
                    const uint8_t* dynamic, const float* values, int32_t n_channels, const int64_t* unit_off,
                    const int32_t* unit_order, const int32_t* row_src, const int32_t* kp_map,
-                   uint32_t* entries_a, uint32_t* entries_b, double* base, double* t_fin, const uint32_t* pos27, int32_t wide,
-                   const int32_t* half0_len, void* stream);
+                   uint32_t* entries_a, uint32_t* entries_b, double* base, double* t_fin, const uint32_t* pos27, int32_t wide, void* stream);
 /* pos27[k] (lattice, u32): the stencil key points around interior key point k
  * that are static (not in dynamic) and positive in some channel -- the only
  * static ones a row's base needs.  fvr_rplan_fill computes it itself when its

@@ -145,9 +145,9 @@ _SIGNATURES = {
                 _P, _P, _P, _P, _P, _P]),
     "fvr_rplan_chunk_entries": (c_int, []),
     "fvr_rplan_count": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _GRID, _PARAMS, _P, _P, _P, _P,
-                                c_int32, _P]),
+                                _P]),
     "fvr_rplan_fill": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, _GRID, _PARAMS, _P, _P, _P, c_int32,
-                               _P, _P, _P, _P, _P, _P, _P, _P, _P, c_int32, _P, _P]),
+                               _P, _P, _P, _P, _P, _P, _P, _P, _P, c_int32, _P]),
     "fvr_rplan_pos27": (c_int, [_GRID, _P, _P, c_int32, _P, _P]),
     "fvr_rplan_unit_keys": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, _P, _P, _P]),
     "fvr_rplan_render": (c_int, [_P, _P, _P, _P, _P, _P, _P, _P, c_int32, c_int32, c_int32, _P, _P, c_int32, _P, _P,

@@ -1068,11 +1068,10 @@ extern "C" int fvr_rplan_chunk_entries(void) { return kRpB; }
 extern "C" int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32_t v0, int32_t bbox_w,
                                int32_t bbox_h, fvr_grid_t grid, fvr_render_params_t params,
                                const uint8_t* occ, const uint8_t* dynamic, int32_t* unit_len, int32_t* row_len,
-                               int32_t halves, void* stream) {
+                               void* stream) {
     FVR_TRY_BEGIN
     if (n_views < 1 || bbox_w < 1 || bbox_h < 1) return set_error(FVR_ERR_INVALID, "empty render plan");
     if (!dynamic || !unit_len) return set_error(FVR_ERR_INVALID, "dynamic / unit_len is NULL");
-    if (halves && !row_len) return set_error(FVR_ERR_INVALID, "halves need row_len");
     if (int rc = check_grid(grid)) return rc;
     bool scat;
     const int m = rplan_mode(params, grid, scat);
@@ -1082,16 +1081,16 @@ extern "C" int fvr_rplan_count(const fvr_camera_t* cams, int32_t n_views, int32_
     const RenderConsts rc = make_render_consts(params, &bg, 1);
     const int units_x = (bbox_w + kUnitW - 1) / kUnitW, upv = fvr_loop_blocks_per_view(bbox_w, bbox_h);
     const int n_units = upv * n_views;
-    const unsigned blocks = (unsigned)(((int64_t)n_units * 32 * (halves ? 2 : 1) + 127) / 128);
+    const unsigned blocks = (unsigned)(((int64_t)n_units * 32 + 127) / 128);
     cudaStream_t st = (cudaStream_t)stream;
     uint32_t* d27 = dyn27_scratch(grid, dynamic, st, true);
     if (!d27) return set_error(FVR_ERR_CUDA, "cannot allocate the render-plan scratch");
     if (m)
         rplan_count_kernel<true><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
-                                                          occ, dynamic, d27, unit_len, row_len, halves ? 1 : 0);
+                                                          occ, dynamic, d27, unit_len, row_len);
     else
         rplan_count_kernel<false><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc,
-                                                           occ, dynamic, d27, unit_len, row_len, halves ? 1 : 0);
+                                                           occ, dynamic, d27, unit_len, row_len);
     return check_launch("rplan_count");
     FVR_TRY_END
 }
@@ -1148,8 +1147,7 @@ extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t
                               const uint8_t* dynamic, const float* values, int32_t n_channels,
                               const int64_t* unit_off, const int32_t* unit_order, const int32_t* row_src,
                               const int32_t* kp_map, uint32_t* entries_a, uint32_t* entries_b, double* base,
-                              double* t_fin, const uint32_t* pos27, int32_t wide, const int32_t* half0_len,
-                              void* stream) {
+                              double* t_fin, const uint32_t* pos27, int32_t wide, void* stream) {
     FVR_TRY_BEGIN
     if (n_views < 1 || bbox_w < 1 || bbox_h < 1) return set_error(FVR_ERR_INVALID, "empty render plan");
     if (n_channels < 1 || n_channels > 4) return set_error(FVR_ERR_INVALID, "n_channels must be 1..4");
@@ -1163,7 +1161,7 @@ extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t
     const int units_x = (bbox_w + kUnitW - 1) / kUnitW, upv = fvr_loop_blocks_per_view(bbox_w, bbox_h);
     const int n_units = upv * n_views;
     const int64_t plane = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
-    const unsigned blocks = (unsigned)(((int64_t)n_units * 32 * (half0_len ? 2 : 1) + 127) / 128);
+    const unsigned blocks = (unsigned)(((int64_t)n_units * 32 + 127) / 128);
     cudaStream_t st = (cudaStream_t)stream;
     const auto* uo = reinterpret_cast<const long long*>(unit_off);
     if (!kp_map || !entries_a || !entries_b) return set_error(FVR_ERR_INVALID, "kp_map / entries are NULL");
@@ -1176,7 +1174,7 @@ extern "C" int fvr_rplan_fill(const fvr_camera_t* cams, int32_t n_views, int32_t
 #define FVR_RPLAN_FILL(S, W)                                                                                   \
     rplan_fill_kernel<S, W><<<blocks, 128, 0, st>>>(cams, u0, v0, bbox_w, bbox_h, units_x, upv, n_units, g, rc, occ, \
                                                      dynamic, d27, values, n_channels, plane, uo, unit_order, row_src, \
-                                                     kp_map, entries_a, entries_b, p27, base, t_fin, half0_len)
+                                                     kp_map, entries_a, entries_b, p27, base, t_fin)
     if (m && wide) FVR_RPLAN_FILL(true, true);
     else if (m) FVR_RPLAN_FILL(true, false);
     else if (wide) FVR_RPLAN_FILL(false, true);

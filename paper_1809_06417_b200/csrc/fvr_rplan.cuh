@@ -218,12 +218,12 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                          float* __restrict__ acc, float* __restrict__ wsm, int stride, RplanOut<WIDE> out,
                          double* base, double& t_fin, const uint8_t* __restrict__ slot_tab = nullptr,
                          const int* __restrict__ kp_map = nullptr, int* __restrict__ skp = nullptr,
-                         const uint32_t* __restrict__ pos27 = nullptr, int half = -1, int count0 = 0) {
+                         const uint32_t* __restrict__ pos27 = nullptr) {
     constexpr uint32_t kPX[3] = {0x1FFu, 0x1FFu << 9, 0x1FFu << 18};
     constexpr uint32_t kPY[3] = {0x7u | (0x7u << 9) | (0x7u << 18), (0x7u << 3) | (0x7u << 12) | (0x7u << 21),
                                  (0x7u << 6) | (0x7u << 15) | (0x7u << 24)};
     constexpr uint32_t kPZ[3] = {0x1249249u, 0x1249249u << 1, 0x1249249u << 2};
-    int count = count0;     // half 1 writes after half 0's entries
+    int count = 0;
     double t_dst = 1.0;
     uint32_t live = 0;      // window slots holding an entry
     int wm[3] = {0, 0, 0};  // window centre
@@ -257,12 +257,8 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
 #pragma unroll
         for (int a = 0; a < 3; ++a) qb[a] = ((o[a] - g.lo[a]) + t0 * d[a]) * g.inv_edge;
         const double nmax[3] = {(double)g.nx, (double)g.ny, (double)g.nz};
-        // half 0: samples 1 .. n/2, half 1: n/2 + 1 .. n (each with a fresh
-        // window, so a run cut at n/2 gives two entries); otherwise all
-        const int k_lo = half == 1 ? n / 2 + 1 : 1, k_hi = half == 0 ? n / 2 : n;
 #pragma unroll 1
-        for (int k = 1; k <= k_hi; ++k, t_dst *= rc.one_minus_tau) {
-            if (k < k_lo) continue;  // the first half's transparency, by the same multiplications
+        for (int k = 1; k <= n; ++k, t_dst *= rc.one_minus_tau) {
             double q[3];
             int m[3];
             float dl[3];
@@ -282,7 +278,7 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                 // transparency advancing by repeated multiplication
                 const int D = __ldg(occ + mlin);
                 if (D > 1) {
-                    const int extra = min(max(D - 3, 0), k_hi - k);
+                    const int extra = min(max(D - 3, 0), n - k);
                     for (int j = 0; j < extra; ++j) t_dst *= rc.one_minus_tau;
                     k += extra;
                     continue;
@@ -471,15 +467,11 @@ template <bool SCAT>
 __global__ void __launch_bounds__(128) rplan_count_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
     int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
-    const uint32_t* __restrict__ dyn27, int* __restrict__ unit_len, int* __restrict__ row_len, int halves) {
+    const uint32_t* __restrict__ dyn27, int* __restrict__ unit_len, int* __restrict__ row_len) {
     __shared__ float s_thr[3 * kScatDirs];
     __shared__ uint32_t s_nm[3 * (kScatDirs + 1)];
     load_split_tables(s_thr, s_nm);
-    // halves: two warps per unit (warp 2u: samples 1..n/2 of each row, warp
-    // 2u + 1: the rest); row_len then holds [half 0 rows | half 1 rows] and
-    // unit_len is left to the caller (the rows' sums)
-    const int wid = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    const int unit = halves ? wid >> 1 : wid, half = halves ? (wid & 1) : -1;
+    const int unit = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (unit >= n_units) return;
     const int lane = threadIdx.x & 31;
     const int view = unit / units_per_view, u = unit - view * units_per_view;
@@ -490,14 +482,11 @@ __global__ void __launch_bounds__(128) rplan_count_kernel(
         double d[3], base[1] = {0.0}, t_fin;
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         cnt = rplan_row<SCAT, false>(cam.center, d, g, rc, occ, dynamic, dyn27, nullptr, 0, 0, s_thr, s_nm, nullptr,
-                                     nullptr, 0, RplanOut<false>{}, base, t_fin, nullptr, nullptr, nullptr, nullptr,
-                                     half);
+                                     nullptr, 0, RplanOut<false>{}, base, t_fin);
     }
-    if (row_len) row_len[(half > 0 ? (int64_t)n_units * 32 : 0) + (int64_t)unit * 32 + lane] = cnt;
-    if (!halves) {
-        cnt = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
-        if (lane == 0) unit_len[unit] = cnt;
-    }
+    if (row_len) row_len[(int64_t)unit * 32 + lane] = cnt;
+    cnt = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
+    if (lane == 0) unit_len[unit] = cnt;
 }
 
 // Fill pass: rows in SELL-32 order; base[c * rows + r] and t_fin[r] per row
@@ -514,8 +503,7 @@ __global__ void __launch_bounds__(128, FVR_RPLAN_FILL_MINB) rplan_fill_kernel(
     const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch, int64_t plane,
     const long long* __restrict__ unit_off, const int* __restrict__ unit_order, const int* __restrict__ row_src,
     const int* __restrict__ kp_map, uint32_t* __restrict__ ent_a, uint32_t* __restrict__ ent_b,
-    const uint32_t* __restrict__ pos27, double* __restrict__ base_out, double* __restrict__ t_fin_out,
-    const int* __restrict__ half0_len) {
+    const uint32_t* __restrict__ pos27, double* __restrict__ base_out, double* __restrict__ t_fin_out) {
     __shared__ float s_acc[27 * 128], s_w[27 * 128];
     __shared__ int s_kp[27 * 128];  // column of the key point in each window slot
     for (int i = threadIdx.x; i < 27 * 128; i += blockDim.x) s_acc[i] = 0.f;
@@ -527,18 +515,13 @@ __global__ void __launch_bounds__(128, FVR_RPLAN_FILL_MINB) rplan_fill_kernel(
     __shared__ float s_thr[3 * kScatDirs];
     __shared__ uint32_t s_nm[3 * (kScatDirs + 1)];
     load_split_tables(s_thr, s_nm);
-    // half0_len (the count pass's half-0 row lengths, natural rows): two warps
-    // per unit, the second writing after the first's entries
-    const int wid = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    const int slot = half0_len ? wid >> 1 : wid, half = half0_len ? (wid & 1) : -1;
+    const int slot = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (slot >= n_units) return;
     const int unit = unit_order ? __ldg(unit_order + slot) : slot;  // longest first: a short tail
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)unit * 32 + lane, rows = (int64_t)n_units * 32;
     int view, col, row;
-    const int64_t nat = row_src ? __ldg(row_src + r) : r;
-    const bool in = rplan_pixel(nat, units_x, units_per_view, w, h, view, col, row);
-    const int count0 = half == 1 ? __ldg(half0_len + nat) : 0;
+    const bool in = rplan_pixel(row_src ? __ldg(row_src + r) : r, units_x, units_per_view, w, h, view, col, row);
     double base[4] = {0.0, 0.0, 0.0, 0.0}, t_fin = 0.0;
     const long long uoff = unit_off[unit];
     RplanOut<WIDE> out;
@@ -547,29 +530,17 @@ __global__ void __launch_bounds__(128, FVR_RPLAN_FILL_MINB) rplan_fill_kernel(
         out.b = ent_b + ((uoff / kRpA) * 32 + lane) * kRpA;
     else
         out.b = reinterpret_cast<uint16_t*>(ent_b) + ((uoff / kRpB) * 32 + lane) * kRpB;
-    int count = count0;
-    t_fin = 1.0;  // a ray that misses the box
+    int count = 0;
     if (in) {
         const fvr_camera_t& cam = cams[view];
         double d[3];
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         count = rplan_row<SCAT, true, WIDE>(cam.center, d, g, rc, occ, dynamic, dyn27, values, nch, plane, s_thr, s_nm,
                                       s_acc + threadIdx.x, s_w + threadIdx.x, 128, out, base, t_fin, s_slot, kp_map,
-                                      s_kp + threadIdx.x, pos27, half, count0);
-    } else {
-        t_fin = 0.0;
-    }
-    if (half == 0) {  // the second half pads the row, writes t_fin; base adds up (two terms: exact)
-        if (values)
-            for (int c = 0; c < nch; ++c) atomicAdd(base_out + c * rows + r, base[c]);
-        return;
+                                      s_kp + threadIdx.x, pos27);
     }
     out.finish(count, (int)(unit_off[unit + 1] - uoff));
-    if (half == 1 && values) {
-        for (int c = 0; c < nch; ++c) atomicAdd(base_out + c * rows + r, base[c]);
-    } else {
-        for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];
-    }
+    for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];
     t_fin_out[r] = t_fin;
 }
 

@@ -467,21 +467,9 @@ class ChannelLoop:
         t = self.t
         n_units = (self.v_end - self.v_begin) * self.bpv
         unit_len = t.zeros(n_units, dtype=t.int32, device=self.dev)
-        # halves: each row built by two threads (samples 1..n/2, n/2+1..n): twice
-        # the parallelism for the latency-bound fill, a few duplicate entries
-        # where a run is cut (FVR_RPLAN_HALVES=0: one thread per row)
-        self._rp_halves = os.environ.get("FVR_RPLAN_HALVES", "1") == "1"
-        if self._rp_halves or os.environ.get("FVR_RPLAN_TILE", "2x4") != "0":
-            row_len = t.empty(n_units * 32 * (2 if self._rp_halves else 1), dtype=t.int32, device=self.dev)
-        else:
-            row_len = None
-        _lib.call("fvr_rplan_count", *self._rplan_geo(), unit_len.data_ptr(), _lib.ptr(row_len),
-                  int(self._rp_halves), _lib.stream_ptr())
-        if self._rp_halves:  # the fill needs the first halves; the layout the sums
-            self._rp_half0 = row_len[: n_units * 32]
-            row_len = row_len[: n_units * 32] + row_len[n_units * 32:]
-            if os.environ.get("FVR_RPLAN_TILE", "2x4") == "0":
-                unit_len = row_len.view(n_units, 32).amax(1).to(t.int32).contiguous()
+        row_len = t.empty(n_units * 32, dtype=t.int32, device=self.dev) \
+            if os.environ.get("FVR_RPLAN_TILE", "2x4") != "0" else None
+        _lib.call("fvr_rplan_count", *self._rplan_geo(), unit_len.data_ptr(), _lib.ptr(row_len), _lib.stream_ptr())
         # the fill's static-positive stencil masks, computed now (off the fill's critical path)
         self._pos27 = None
         if not self._static_zero:
@@ -553,10 +541,8 @@ class ChannelLoop:
             # every chunk, padding included, is written by the fill (no clearing)
             ent_a = t.empty(max(slots, 2), dtype=t.int32, device=dev)
             ent_b = t.empty(max(slots if self.rp_wide else slots // 2, 1), dtype=t.int32, device=dev)
-            # the fill writes every row's base and t_fin (overhanging rows too);
-            # with halves and a static term the two halves add into a zeroed base
-            base = (t.zeros if (self._rp_halves and not self._static_zero) else t.empty)(
-                (self.nch, n_units * 32), dtype=t.float64, device=dev)
+            # the fill writes every row's base and t_fin (overhanging rows too)
+            base = t.empty((self.nch, n_units * 32), dtype=t.float64, device=dev)
             t_fin = t.empty(n_units * 32, dtype=t.float64, device=dev)
             # the operand: max(v, 0) per hull key point (float4 for 3 channels)
             kpv = t.empty((max(self.n_kp, 1),) + ((4,) if self.nch == 3 else ()), dtype=t.float32, device=dev)
@@ -567,7 +553,7 @@ class ChannelLoop:
                   off.data_ptr(), _lib.ptr(self.rp_order),
                   _lib.ptr(self.rp_row_src), self._kp_map().data_ptr(), ent_a.data_ptr(), ent_b.data_ptr(),
                   base.data_ptr(), t_fin.data_ptr(), _lib.ptr(getattr(self, "_pos27", None)), int(self.rp_wide),
-                  _lib.ptr(self._rp_half0 if self._rp_halves else None), stream)
+                  stream)
         self._pos27 = None
         _lib.call("fvr_rplan_pack", self.values.data_ptr(), self.nch, self.grid, self.kp.data_ptr(), self.n_kp,
                   kpv.data_ptr(), None, stream)
