@@ -218,7 +218,7 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                          float* __restrict__ acc, float* __restrict__ wsm, int stride, RplanOut<WIDE> out,
                          double* base, double& t_fin, const uint8_t* __restrict__ slot_tab = nullptr,
                          const int* __restrict__ kp_map = nullptr, int* __restrict__ skp = nullptr,
-                         const uint32_t* __restrict__ pos27 = nullptr) {
+                         const uint32_t* __restrict__ pos27 = nullptr, const int* __restrict__ off27 = nullptr) {
     constexpr uint32_t kPX[3] = {0x1FFu, 0x1FFu << 9, 0x1FFu << 18};
     constexpr uint32_t kPY[3] = {0x7u | (0x7u << 9) | (0x7u << 18), (0x7u << 3) | (0x7u << 12) | (0x7u << 21),
                                  (0x7u << 6) | (0x7u << 15) | (0x7u << 24)};
@@ -335,8 +335,8 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
             have = true;
             // toroidal slot of offset (jx, jy, jz): ((m + j - 1) mod 3) per axis
             const int r0 = (m[0] + 2) % 3, r1 = (m[1] + 2) % 3, r2 = (m[2] + 2) % 3;
+            float w[27];  // the sample's stencil weights (fill only; kept in registers for the merge)
             if (FILL) {
-                float w[27];
                 if (SCAT) {
                     float2 om01[9];
                     float om2[9];
@@ -351,7 +351,11 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                     sample_weights<false>(dl[0], dl[1], dl[2], sig_a, kappa, 0xffffffffu, w);
                 }
 #pragma unroll
-                for (int j = 0; j < 27; ++j) wsm[j * stride] = w[j] * scale;
+                for (int j = 0; j < 27; ++j) w[j] = __fmul_rn(w[j], scale);
+                if (values) {  // the static base term reads them by stencil offset
+#pragma unroll
+                    for (int j = 0; j < 27; ++j) wsm[j * stride] = w[j];
+                }
             }
             // the stencil's dynamic key points, moved to window slots at once
             // (count pass: that is all; config 2: 0.83 -> 0.36 ms)
@@ -370,10 +374,7 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                         fresh &= fresh - 1;
                     }
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        c4[i] = j4[i] < 0 ? 0
-                                          : __ldg(kp_map + mlin + (j4[i] / 9 - 1) * g.sx + ((j4[i] / 3) % 3 - 1) * g.sy +
-                                                  (j4[i] % 3 - 1));
+                    for (int i = 0; i < 4; ++i) c4[i] = j4[i] < 0 ? 0 : __ldg(kp_map + mlin + off27[j4[i]]);
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
                         if (j4[i] >= 0) skp[tab[j4[i]] * stride] = c4[i];
@@ -381,15 +382,16 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
             }
             live |= rotate27(sup & dyn, r0, r1, r2);
             if (FILL) {
-                // (weights stay in stencil order: storing them at their slots
-                // costs more address arithmetic than the per-bit slot saves)
-                // slot of stencil offset j for these residues: a shared-memory table
-                const uint8_t* tab = slot_tab + (r0 * 9 + r1 * 3 + r2) * 27;
-#pragma unroll 1
-                for (uint32_t b = sup & dyn; b; b &= b - 1) {
-                    const int j = __ffs(b) - 1;
-                    acc[tab[j] * stride] += wsm[j * stride];
-                }
+                // merge into the window: unrolled over the 27 stencil offsets
+                // (weights in registers, slot = per-axis residues), predicated
+                // on the dynamic support -- no shared-memory weight round trip
+                const uint32_t md = sup & dyn;
+                const int SX[3] = {(r0 % 3) * 9, ((r0 + 1) % 3) * 9, ((r0 + 2) % 3) * 9};
+                const int SY[3] = {(r1 % 3) * 3, ((r1 + 1) % 3) * 3, ((r1 + 2) % 3) * 3};
+                const int SZ[3] = {r2 % 3, (r2 + 1) % 3, (r2 + 2) % 3};
+#pragma unroll
+                for (int j = 0; j < 27; ++j)
+                    if ((md >> j) & 1u) acc[(SX[j / 9] + SY[(j / 3) % 3] + SZ[j % 3]) * stride] += w[j];
 #pragma unroll 1
                 // static key points with a positive value (pos27; none for the
                 // reference's initial grid) fold into base
@@ -512,9 +514,12 @@ __global__ void __launch_bounds__(128, FVR_RPLAN_FILL_MINB) rplan_fill_kernel(
         const int rr = i / 27, j = i % 27;
         s_slot[i] = (uint8_t)(((rr / 9 + j / 9) % 3) * 9 + (((rr / 3) % 3 + (j / 3) % 3) % 3) * 3 + (rr % 3 + j % 3) % 3);
     }
+    __shared__ int s_off27[27];  // lattice offset of stencil slot j from the centre key point
+    if (threadIdx.x < 27)
+        s_off27[threadIdx.x] = (threadIdx.x / 9 - 1) * g.sx + ((threadIdx.x / 3) % 3 - 1) * g.sy + (threadIdx.x % 3 - 1);
     __shared__ float s_thr[3 * kScatDirs];
     __shared__ uint32_t s_nm[3 * (kScatDirs + 1)];
-    load_split_tables(s_thr, s_nm);
+    load_split_tables(s_thr, s_nm);  // (its barrier also publishes s_off27)
     const int slot = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (slot >= n_units) return;
     const int unit = unit_order ? __ldg(unit_order + slot) : slot;  // longest first: a short tail
@@ -537,7 +542,7 @@ __global__ void __launch_bounds__(128, FVR_RPLAN_FILL_MINB) rplan_fill_kernel(
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
         count = rplan_row<SCAT, true, WIDE>(cam.center, d, g, rc, occ, dynamic, dyn27, values, nch, plane, s_thr, s_nm,
                                       s_acc + threadIdx.x, s_w + threadIdx.x, 128, out, base, t_fin, s_slot, kp_map,
-                                      s_kp + threadIdx.x, pos27);
+                                      s_kp + threadIdx.x, pos27, s_off27);
     }
     out.finish(count, (int)(unit_off[unit + 1] - uoff));
     for (int c = 0; c < nch; ++c) base_out[c * rows + r] = base[c];
