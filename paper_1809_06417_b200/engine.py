@@ -148,6 +148,20 @@ def exchange(comm, sq, vol, v_begin: int, v_end: int, rows_per_view: int, rank: 
         dist.all_reduce(comm, op=dist.ReduceOp.SUM, group=group)
 
 
+_SIDE: dict = {}
+
+
+def _side_stream(dev):
+    """One persistent side stream per device: buffers allocated on it come
+    from its own caching-allocator pool, which a per-call stream would never
+    reuse (a fresh cudaMalloc every call)."""
+    t = _lib.torch()
+    key = str(dev)
+    if key not in _SIDE:
+        _SIDE[key] = t.cuda.Stream(device=dev)
+    return _SIDE[key]
+
+
 _PINNED: dict = {}
 
 
@@ -300,14 +314,10 @@ class ChannelLoop:
                       self.occ.data_ptr(), _lib.stream_ptr())
         self.kp_dev = kp_dev
 
-        # the render plan's count pass only needs the geometry: enqueue it
-        # now so it runs while the host prepares the flame rays
         self.bpv = int(_lib.load().fvr_loop_blocks_per_view(self.w_bb, self.h_bb))
         self.rplan = False
         self.rplan_nnz = 0
         self._rp_counted = None
-        if self.layout_kind and os.environ.get("FVR_RENDER", "plan") != "march":
-            self._rp_counted = self._rplan_count()
         self._mark("layout+occupancy")
         # flame rays of the local views, row-major per view (reconstruct.py:144-149)
         # compacted on the device (host masks: the bbox crops are uploaded)
@@ -374,9 +384,23 @@ class ChannelLoop:
         # plan's on a side stream; every buffer is allocated on the loop's
         # stream, so the caching allocator keeps them across calls).
         self._mark("work buffers")
-        pc = self._plan_count() if self.plan else None
+        # the two plans' count passes side by side: the adjust plan's (with
+        # its SELL layout) on a persistent side stream, the render plan's on
+        # the loop's stream; both are latency-bound at moderate occupancy
+        main = t.cuda.current_stream()
+        pc = None
+        if self.plan:
+            side = _side_stream(dev)
+            side.wait_stream(main)
+            with t.cuda.stream(side):
+                self._kp_map()
+                pc = self._plan_count()
+        if self.layout_kind and os.environ.get("FVR_RENDER", "plan") != "march":
+            self._rp_counted = self._rplan_count()
         rs = self._rplan_scan(*self._rp_counted) if self._rp_counted is not None else None
         self._rp_counted = None
+        if pc is not None:
+            main.wait_stream(side)
         scalars = (pc["sizes"] if pc else []) + (rs["sizes"] if rs else [])
         host = t.stack(scalars).cpu().tolist() if scalars else []
         keep = []
