@@ -388,15 +388,17 @@ class ChannelLoop:
         # its SELL layout) on a persistent side stream, the render plan's on
         # the loop's stream; both are latency-bound at moderate occupancy
         main = t.cuda.current_stream()
+        ready = t.cuda.Event()
+        ready.record(main)
+        if self.layout_kind and os.environ.get("FVR_RENDER", "plan") != "march":
+            self._rp_counted = self._rplan_count()
         pc = None
         if self.plan:
             side = _side_stream(dev)
-            side.wait_stream(main)
+            side.wait_event(ready)
             with t.cuda.stream(side):
                 self._kp_map()
                 pc = self._plan_count()
-        if self.layout_kind and os.environ.get("FVR_RENDER", "plan") != "march":
-            self._rp_counted = self._rplan_count()
         rs = self._rplan_scan(*self._rp_counted) if self._rp_counted is not None else None
         self._rp_counted = None
         if pc is not None:
