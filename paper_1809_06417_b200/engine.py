@@ -1,28 +1,36 @@
-"""Device-resident reconstruction loop (one scalar channel).
+"""Device-resident reconstruction loop (one scalar channel, or three).
 
-One iteration of reconstruct_channel (reconstruct.py:304-334) is four
-kernels on one stream, in this order:
+One iteration of reconstruct_channel (reconstruct.py:304-334) is two
+launches on one stream (deterministic mode; the stochastic mode adds a
+weigh launch between them):
 
-  K-render   every bbox pixel of every view: ray, march, residual, per-block
-             squared-residual partials                    (csrc/fvr_render.cu)
-  K-adjust   every flame ray: march again, back-project the residual into a
-             32.32 fixed-point correction lattice          (csrc/fvr_adjust.cu)
-  K-finalize per-view RMSE, mean, trace append, convergence rule (1 block)
-  K-update   v = f32(max(v + delta, -1)) on hull key points, skipped when the
-             rule fired                                      (csrc/fvr_loop.cu)
+  K-render   the render plan B (SELL-32, csrc/fvr_rplan.cuh): every bbox
+             pixel's row of B times the hull key-point values, plus its
+             static base and t_fin * background; residual and squared-
+             residual partials; the last CTA finalizes the iteration (per-
+             view RMSE, mean, trace append, convergence rule, done flag)
+  K-adjust   the adjust plan A (SELL-32 gather by hull key point,
+             csrc/fvr_plan.cu): every hull key point sums its weighted
+             residuals in 32.32 fixed point and updates its value,
+             v = f32(max(v + delta, -1)), skipped when the rule fired
 
-The adjust runs speculatively before the convergence decision; when the rule
-fires the correction is discarded, which is exactly the reference's
-break-before-adjust.  Once the state says ``done`` every later launch is a
-no-op, so the host can enqueue iterations (or replay a captured CUDA graph)
-without a per-iteration round trip and read the trace back at the end.
+Both plans are built once per call on the device from the geometry (count
+pass, scan, fill).  Hull key points are renumbered in Morton order so both
+operands stay L2-local.  The reference's break-before-adjust holds because
+the adjust reads the done flag the render's finalize wrote; once ``done`` is
+set every later launch is a no-op, so the host enqueues iterations (or
+replays a captured CUDA graph) without a per-iteration round trip and reads
+the trace back at the end.  Where a plan cannot be built (device memory) the
+loop uses the marching kernels (csrc/fvr_render.cu, csrc/fvr_adjust.cu) on
+the same contract.
 
-With torch.distributed initialised (world_size > 1) the views are sharded in
-contiguous ranges across ranks; each rank renders and back-projects its own
-views into a full-size correction, and one NCCL all-reduce per iteration of
-an int64 buffer [packed correction at hull key points | squared-residual
-partials of every view] makes every rank's lattice identical.  Integer sums
-are exact, so 1, 2, 4 or 8 GPUs give bit-identical grids.
+With a process group (world_size > 1) the views are sharded in contiguous
+ranges across ranks; each rank renders and back-projects its own views and
+one all-reduce per iteration of an int64 buffer [packed correction at hull
+key points | squared-residual partials of every view] -- NCCL behind the
+C ABI (fvr_comm_init / fvr_allreduce_sum, csrc/fvr_comm.cu) on CUDA, gloo in
+the CPU tests -- makes every rank's lattice identical.  Integer sums are
+exact, so 1, 2, 4 or 8 GPUs give bit-identical grids.
 """
 
 from __future__ import annotations
