@@ -441,6 +441,36 @@ int fvr_rplan_tile_rows(const int32_t* row_len, int32_t n_views, int32_t bbox_w,
                         int32_t tile_units_x, int32_t tile_units_y, int32_t align, int32_t* row_src,
                         int32_t* unit_len, void* stream);
 
+/* The setup's layout steps as one call each (csrc/fvr_layout.cu; CUB scans
+ * and radix sorts on `stream`, scratch from the device's default pool). */
+/* kp_index sorted by Morton key into out (n < 2^31; out != kp_index). */
+int fvr_morton_order(const int32_t* kp_index, int64_t n, fvr_grid_t grid, int32_t* out, void* stream);
+/* map[lattice index] = position in kp_index, -1 elsewhere (n_vox entries). */
+int fvr_kp_map(const int32_t* kp_index, int64_t n_kp, int64_t n_vox, int32_t* map, void* stream);
+/* The adjust plan's SELL layout after its count pass: row_of_pos
+ * (fvr_sell_window_order), slice_len[s] = the slice's longest row rounded up
+ * to `pad` entries, slice_off (n_slices + 1, exclusive scan of slice_len),
+ * row_info[row] = slice_off[pos >> 5] << 5 | (pos & 31); totals[0] = entries
+ * per lane over all slices, totals[1] = sum of counts, totals[2] = sum of
+ * ray_samples (0 when ray_samples is NULL).  n_slices = ceil(n_rows / 32). */
+int fvr_sell_layout(const int32_t* counts, int64_t n_rows, int32_t window, int32_t pad,
+                    const int32_t* ray_samples, int64_t n_rays, int32_t* row_of_pos, int32_t* slice_len,
+                    int64_t* slice_off, int64_t* row_info, int64_t* totals, void* stream);
+/* The render plan's layout after its count pass: fvr_rplan_tile_rows
+ * (row_src, unit_len), unit_off (n_units + 1, exclusive scan of unit_len),
+ * unit_order (the fvr_rplan_unit_keys order: longest class first, 2x4-unit
+ * tiles inside a class); totals[0] = unit_off[n_units], totals[1] = the
+ * longest unit. */
+int fvr_rplan_layout(const int32_t* row_len, int32_t n_views, int32_t bbox_w, int32_t bbox_h, int32_t tile_units_x,
+                     int32_t tile_units_y, int32_t align, int32_t buckets, int32_t* row_src, int32_t* unit_len,
+                     int64_t* unit_off, int32_t* unit_order, int64_t* totals, void* stream);
+/* Flame rays of the bbox crops (u8, n_views x bbox_h x bbox_w, row-major):
+ * rays[i] = view << 24 | (row * bbox_w + col) of the i-th nonzero pixel in
+ * that order (reconstruct.py:144-149), at most `capacity` of them;
+ * *n_rays (device) = the number found. */
+int fvr_flame_rays(const uint8_t* crops, int32_t n_views, int32_t bbox_w, int32_t bbox_h, int64_t capacity,
+                   int32_t* rays, int64_t* n_rays, void* stream);
+
 /* ---- the per-iteration collective ------------------
  * Replaces the per-view loop + fixed-order merge of adjust_pass
  * (reconstruct.py:181-226; the reference itself has no distribution,

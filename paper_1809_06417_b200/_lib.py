@@ -178,6 +178,12 @@ _SIGNATURES = {
     "fvr_morton_keys": (c_int, [_P, c_int64, _GRID, _P, _P]),
     "fvr_sell_window_order": (c_int, [_P, c_int64, c_int32, _P, _P]),
     "fvr_rplan_tile_rows": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, _P, _P, _P]),
+    "fvr_morton_order": (c_int, [_P, c_int64, _GRID, _P, _P]),
+    "fvr_kp_map": (c_int, [_P, c_int64, c_int64, _P, _P]),
+    "fvr_sell_layout": (c_int, [_P, c_int64, c_int32, c_int32, _P, c_int64, _P, _P, _P, _P, _P, _P]),
+    "fvr_rplan_layout": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, _P, _P, _P, _P,
+                                 _P, _P]),
+    "fvr_flame_rays": (c_int, [_P, c_int32, c_int32, c_int32, c_int64, _P, _P, _P]),
     "fvr_comm_available": (c_int, []),
     "fvr_comm_nccl_version": (c_int, [POINTER(c_int32)]),
     "fvr_comm_unique_id": (c_int, [_P]),

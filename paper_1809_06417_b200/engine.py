@@ -194,17 +194,18 @@ def _morton_enabled() -> bool:
 
 def _morton_order(kp, shape):
     """The list of lattice indices ``kp`` (int32, device) sorted by Morton
-    (x, y, z) code: one key kernel (fvr_morton_keys) and one sort."""
+    (x, y, z) code: one key kernel and one radix sort over the code's bits
+    (fvr_morton_order)."""
     t = _lib.torch()
     n = int(kp.numel())
     if n == 0:
         return kp
-    keys = t.empty(n, dtype=t.int64, device=kp.device)
+    out = t.empty_like(kp)
     g = _lib.FvrGrid()
     g.nx, g.ny, g.nz = shape[0] - 1, shape[1] - 1, shape[2] - 1
     g.edge = 1.0
-    _lib.call("fvr_morton_keys", kp.data_ptr(), n, g, keys.data_ptr(), _lib.stream_ptr())
-    return kp[t.sort(keys).indices].contiguous()
+    _lib.call("fvr_morton_order", kp.contiguous().data_ptr(), n, g, out.data_ptr(), _lib.stream_ptr())
+    return out
 
 
 class ChannelLoop:
@@ -344,11 +345,20 @@ class ChannelLoop:
         if self.v_begin > 0:
             ray_base = int(per_view[: self.v_begin].sum()) if n_host is not None else \
                 int(sub[: self.v_begin].reshape(-1).count_nonzero().item())
-        if n_host is not None:  # count known on the host: no device synchronisation
-            nz = t.nonzero_static(sub[self.v_begin:self.v_end], size=n_host)
+        local_sub = sub[self.v_begin:self.v_end]
+        if n_host is not None and local_sub.is_contiguous() and local_sub.dtype == t.uint8:
+            # count known on the host: one native compaction, no synchronisation
+            ray_list_t = t.empty(n_host, dtype=t.int32, device=dev)
+            n_found = t.empty(1, dtype=t.int64, device=dev)
+            if n_host:
+                _lib.call("fvr_flame_rays", local_sub.data_ptr(), self.v_end - self.v_begin, self.w_bb, self.h_bb,
+                          n_host, ray_list_t.data_ptr(), n_found.data_ptr(), _lib.stream_ptr())
         else:
-            nz = t.nonzero(sub[self.v_begin:self.v_end])  # (N, 3): view, row, col -- lexicographic
-        ray_list_t = ((nz[:, 0] << 24) | (nz[:, 1] * self.w_bb + nz[:, 2])).to(t.int32)
+            if n_host is not None:
+                nz = t.nonzero_static(local_sub, size=n_host)
+            else:
+                nz = t.nonzero(local_sub)  # (N, 3): view, row, col -- lexicographic
+            ray_list_t = ((nz[:, 0] << 24) | (nz[:, 1] * self.w_bb + nz[:, 2])).to(t.int32)
         self.n_rays = int(ray_list_t.numel())
         self.rays = ray_list_t if self.n_rays else t.zeros(1, dtype=t.int32, device=dev)
         self.ray_base = ray_base
@@ -394,34 +404,46 @@ class ChannelLoop:
         self._mark("work buffers")
         # the two plans' count passes side by side: the adjust plan's (with
         # its SELL layout) on a persistent side stream, the render plan's on
-        # the loop's stream; both are latency-bound at moderate occupancy
+        # the loop's stream; both are latency-bound at moderate occupancy.
+        # The adjust plan's sizes come back first, so its fill runs on the
+        # device while the host enqueues the render plan's scan; the two
+        # fills still run one after the other (side by side on two streams
+        # each slowed the other: config 2, 1.73 + 1.78 ms overlapped against
+        # 1.59 + 0.92 ms in sequence)
         main = t.cuda.current_stream()
         ready = t.cuda.Event()
         ready.record(main)
         if self.layout_kind and os.environ.get("FVR_RENDER", "plan") != "march":
             self._rp_counted = self._rplan_count()
-        pc = None
+        keep = []
+        adjust_done = None
         if self.plan:
             side = _side_stream(dev)
             side.wait_event(ready)
             with t.cuda.stream(side):
                 self._kp_map()
                 pc = self._plan_count()
+                sizes = pc["sizes"].cpu().tolist()  # synchronises the side stream only
+                self.plan = self._plan_fill(pc, sizes, side, keep)
+                self.sample_plan = self.plan and self.sample_plan
+                adjust_done = t.cuda.Event()
+                adjust_done.record(side)
+            # buffers from the side stream's pool that the loop's stream uses
+            for buf in (self._kpmap, getattr(self, "plan_entries", None), getattr(self, "plan_entries_b", None),
+                        getattr(self, "plan_slice_len", None), getattr(self, "plan_slice_off", None),
+                        getattr(self, "plan_row_of_pos", None), getattr(self, "sample_meta", None),
+                        getattr(self, "rho", None)):
+                if buf is not None:
+                    buf.record_stream(main)
         rs = self._rplan_scan(*self._rp_counted) if self._rp_counted is not None else None
         self._rp_counted = None
-        if pc is not None:
-            main.wait_stream(side)
-        scalars = (pc["sizes"] if pc else []) + (rs["sizes"] if rs else [])
-        host = t.stack(scalars).cpu().tolist() if scalars else []
-        keep = []
-        # the two fills run back to back on the loop's stream: side by side on
-        # two streams each slowed the other (config 2: 1.73 + 1.78 ms
-        # overlapped, against 1.59 + 0.92 ms in sequence)
-        if pc is not None:
-            self.plan = self._plan_fill(pc, host[: len(pc["sizes"])], t.cuda.current_stream(), keep)
-            self.sample_plan = self.plan and self.sample_plan
         if rs is not None:
-            self.rplan = self._rplan_fill(rs, host[len(pc["sizes"]) if pc else 0:])
+            sizes = rs["sizes"].cpu().tolist()
+            if adjust_done is not None:
+                main.wait_event(adjust_done)
+            self.rplan = self._rplan_fill(rs, sizes)
+        if adjust_done is not None:
+            main.wait_event(adjust_done)
         del keep
         if self.layout_kind and not self.rplan:
             # float4 per (key point, channel), channels interleaved (fvr_stencil.cuh)
@@ -486,8 +508,9 @@ class ChannelLoop:
         """Lattice index -> index in the key-point list (-1 elsewhere)."""
         if getattr(self, "_kpmap", None) is None:
             t = self.t
-            self._kpmap = t.full((int(np.prod(self.shape)),), -1, dtype=t.int32, device=self.dev)
-            self._kpmap[self.kp[: self.n_kp].long()] = t.arange(self.n_kp, dtype=t.int32, device=self.dev)
+            n_vox = int(np.prod(self.shape))
+            self._kpmap = t.empty((n_vox,), dtype=t.int32, device=self.dev)
+            _lib.call("fvr_kp_map", self.kp.data_ptr(), self.n_kp, n_vox, self._kpmap.data_ptr(), _lib.stream_ptr())
         return self._kpmap
 
     def _rplan_geo(self):
@@ -519,8 +542,22 @@ class ChannelLoop:
         n_units = unit_len.numel()
         row_src = None
         al = int(_lib.load().fvr_rplan_chunk_entries())  # whole lane chunks of entries (fvr_rplan.cuh)
+        tx, ty = (int(x) for x in os.environ.get("FVR_RPLAN_TILE", "2x4").split("x")) if row_len is not None \
+            else (0, 0)
+        buckets = int(os.environ.get("FVR_RPLAN_BUCKETS", "24"))
+        if row_len is not None and (32 * tx * ty) & (32 * tx * ty - 1) == 0 and 32 * tx * ty <= 1024 \
+                and buckets > 0 and os.environ.get("FVR_RPLAN_SORT", "1") == "1":
+            # the whole layout in one native call (fvr_layout.cu)
+            row_src = t.empty(n_units * 32, dtype=t.int32, device=self.dev)
+            unit_len = t.empty(n_units, dtype=t.int32, device=self.dev)
+            off = t.empty(n_units + 1, dtype=t.int64, device=self.dev)
+            order = t.empty(n_units, dtype=t.int32, device=self.dev)
+            totals = t.empty(2, dtype=t.int64, device=self.dev)
+            _lib.call("fvr_rplan_layout", row_len.data_ptr(), self.v_end - self.v_begin, self.w_bb, self.h_bb, tx, ty,
+                      al, buckets, row_src.data_ptr(), unit_len.data_ptr(), off.data_ptr(), order.data_ptr(),
+                      totals.data_ptr(), _lib.stream_ptr())
+            return dict(unit_len=unit_len, row_src=row_src, off=off, order=order, sizes=totals)
         if row_len is not None:
-            tx, ty = (int(x) for x in os.environ.get("FVR_RPLAN_TILE", "2x4").split("x"))
             if (32 * tx * ty) & (32 * tx * ty - 1) == 0 and 32 * tx * ty <= 1024:  # one kernel per call
                 row_src = t.empty(n_units * 32, dtype=t.int32, device=self.dev)
                 unit_len = t.empty(n_units, dtype=t.int32, device=self.dev)
@@ -535,7 +572,7 @@ class ChannelLoop:
         # fill and render visit the units longest first (a short tail); the
         # order is computed before the sizes reach the host
         order = self._rplan_unit_order(unit_len, mx) if os.environ.get("FVR_RPLAN_SORT", "1") == "1" else None
-        return dict(unit_len=unit_len, row_src=row_src, off=off, order=order, sizes=[off[-1], mx])
+        return dict(unit_len=unit_len, row_src=row_src, off=off, order=order, sizes=t.stack([off[-1], mx.long()]))
 
     def _rplan_unit_order(self, unit_len, max_len):
         """The order fill and render visit the units: longest first, in
@@ -740,6 +777,23 @@ class ChannelLoop:
         # sigma 0 / 64 / 128 / 512 / 4096: 0.0783 / 0.0773 / 0.0760 / 0.0767 /
         # 0.0844 ms)
         sigma = int(os.environ.get("FVR_SELL_SIGMA", "128"))
+        # whole lane chunks (fvr_plan.cu): 16 bytes of six-byte entries (8), or
+        # 32 bytes of eight-byte (wide) entries (kSE = 4); the sample plan's
+        # format is decided after the sizes reach the host, so it pads to 8
+        pad = 4 if self.adj_wide else 8
+        if os.environ.get("FVR_SELL_SORT", "0") != "1" and 2 <= sigma <= 1024 and sigma & (sigma - 1) == 0:
+            # the whole layout in one native call (fvr_layout.cu)
+            n_slices = (self.n_kp + 31) // 32
+            row_of_pos = t.empty(self.n_kp, dtype=t.int32, device=dev)
+            slice_len = t.empty(n_slices, dtype=t.int32, device=dev)
+            slice_off = t.empty(n_slices + 1, dtype=t.int64, device=dev)
+            row_info = t.empty(self.n_kp, dtype=t.int64, device=dev)
+            totals = t.empty(3, dtype=t.int64, device=dev)
+            _lib.call("fvr_sell_layout", counts.data_ptr(), self.n_kp, sigma, pad, _lib.ptr(ray_samples), self.n_rays,
+                      row_of_pos.data_ptr(), slice_len.data_ptr(), slice_off.data_ptr(), row_info.data_ptr(),
+                      totals.data_ptr(), stream)
+            return dict(geo=geo, kp_map=kp_map, ray_samples=ray_samples, row_of_pos=row_of_pos, slice_len=slice_len,
+                        slice_off=slice_off, row_info=row_info, sizes=totals)
         if os.environ.get("FVR_SELL_SORT", "0") == "1":
             order = t.argsort(counts, descending=True)
         elif 2 <= sigma <= 1024 and sigma & (sigma - 1) == 0:  # one kernel: bitonic per window
@@ -757,20 +811,16 @@ class ChannelLoop:
         slice_len = t.zeros(n_slices * 32, dtype=t.int32, device=dev)
         slice_len[: self.n_kp] = counts[order]
         slice_len = slice_len.view(n_slices, 32).amax(1).contiguous()
-        # whole lane chunks (fvr_plan.cu): 16 bytes of six-byte entries (8), or
-        # 32 bytes of eight-byte (wide) entries (kSE = 4); the sample plan's
-        # format is decided after the sizes reach the host, so it pads to 8
-        slice_len = (slice_len + 3) & ~3 if self.adj_wide else (slice_len + 7) & ~7
+        slice_len = (slice_len + pad - 1) & ~(pad - 1)
         slice_off = t.zeros(n_slices + 1, dtype=t.int64, device=dev)
         slice_off[1:] = t.cumsum(slice_len.long(), 0)
         sizes = [slice_off[-1], counts.long().sum()]
-        if ray_samples is not None:
-            sizes.append(ray_samples.long().sum())
+        sizes.append(ray_samples.long().sum() if ray_samples is not None else sizes[1] * 0)
         # each row's SELL position in one word: slice entry offset << 5 | lane
         rp = row_pos.long()
         row_info = (slice_off[rp >> 5] << 5) | (rp & 31)
-        return dict(geo=geo, kp_map=kp_map, ray_samples=ray_samples, row_of_pos=row_of_pos, row_pos=row_pos,
-                    slice_len=slice_len, slice_off=slice_off, row_info=row_info, sizes=sizes)
+        return dict(geo=geo, kp_map=kp_map, ray_samples=ray_samples, row_of_pos=row_of_pos, slice_len=slice_len,
+                    slice_off=slice_off, row_info=row_info, sizes=t.stack(sizes))
 
     def _plan_fill(self, pc: dict, sizes, stream, keep: list) -> bool:
         """Allocate, clear and fill the plan on ``stream`` (the current

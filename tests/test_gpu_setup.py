@@ -94,3 +94,116 @@ def test_rplan_tile_rows(cuda_device, tile):
     assert np.array_equal(row_src.cpu().numpy(), want)
     ul = row_len[want].reshape(n_units, 32).max(1)
     assert np.array_equal(unit_len.cpu().numpy(), (ul + 15) // 16 * 16)
+
+
+def test_sell_layout_matches_restatement(cuda_device):
+    """fvr_sell_layout = window order + per-slice padded max + exclusive scan
+    + row_info + the count / ray-sample totals (engine._plan_count)."""
+    import torch
+
+    from paper_1809_06417_b200 import _lib
+
+    rng = np.random.default_rng(7)
+    for n, window, pad in ((100_003, 128, 8), (31, 32, 4), (4096, 1024, 8)):
+        counts = rng.integers(0, 60, n).astype(np.int32)
+        ray_samples = rng.integers(0, 9, 5001).astype(np.int32)
+        d = torch.from_numpy(counts).to(cuda_device)
+        rs = torch.from_numpy(ray_samples).to(cuda_device)
+        ns = (n + 31) // 32
+        row_of_pos = torch.empty(n, dtype=torch.int32, device=cuda_device)
+        slice_len = torch.empty(ns, dtype=torch.int32, device=cuda_device)
+        slice_off = torch.empty(ns + 1, dtype=torch.int64, device=cuda_device)
+        row_info = torch.empty(n, dtype=torch.int64, device=cuda_device)
+        totals = torch.empty(3, dtype=torch.int64, device=cuda_device)
+        _lib.call("fvr_sell_layout", d.data_ptr(), n, window, pad, rs.data_ptr(), rs.numel(), row_of_pos.data_ptr(),
+                  slice_len.data_ptr(), slice_off.data_ptr(), row_info.data_ptr(), totals.data_ptr(),
+                  _lib.stream_ptr())
+        pos = np.arange(n)
+        order = np.lexsort((pos, -counts.astype(np.int64), pos // window))
+        assert np.array_equal(row_of_pos.cpu().numpy(), order)
+        sl = np.zeros(ns * 32, np.int64)
+        sl[:n] = counts[order]
+        sl = sl.reshape(ns, 32).max(1)
+        sl = (sl + pad - 1) // pad * pad
+        assert np.array_equal(slice_len.cpu().numpy(), sl)
+        off = np.concatenate([[0], np.cumsum(sl)])
+        assert np.array_equal(slice_off.cpu().numpy(), off)
+        rp = np.empty(n, np.int64)
+        rp[order] = pos
+        assert np.array_equal(row_info.cpu().numpy(), (off[rp >> 5] << 5) | (rp & 31))
+        assert totals.cpu().tolist() == [int(off[-1]), int(counts.sum()), int(ray_samples.sum())]
+
+
+@pytest.mark.parametrize("buckets", [24, 1, 5])
+def test_rplan_layout_matches_restatement(cuda_device, buckets):
+    """fvr_rplan_layout = tile rows + exclusive scan of the unit lengths +
+    the unit order of fvr_rplan_unit_keys (engine._rplan_scan)."""
+    import torch
+
+    from paper_1809_06417_b200 import _lib
+
+    rng = np.random.default_rng(buckets)
+    n_views, w, h = 3, 139, 255
+    ux, uy = (w + 7) // 8, (h + 3) // 4
+    n_units = n_views * ux * uy
+    row_len = rng.integers(0, 700, n_units * 32).astype(np.int32)
+    d = torch.from_numpy(row_len).to(cuda_device)
+    # restatement from the separately tested pieces
+    rs_ref = torch.empty(n_units * 32, dtype=torch.int32, device=cuda_device)
+    ul_ref = torch.empty(n_units, dtype=torch.int32, device=cuda_device)
+    _lib.call("fvr_rplan_tile_rows", d.data_ptr(), n_views, w, h, 2, 4, 16, rs_ref.data_ptr(), ul_ref.data_ptr(),
+              _lib.stream_ptr())
+    ul = ul_ref.cpu().numpy().astype(np.int64)
+    mx = torch.tensor([int(ul.max())], dtype=torch.int32, device=cuda_device)
+    keys = torch.empty(n_units, dtype=torch.int64, device=cuda_device)
+    _lib.call("fvr_rplan_unit_keys", ul_ref.data_ptr(), n_views, w, h, buckets, mx.data_ptr(), keys.data_ptr(),
+              _lib.stream_ptr())
+    order_ref = np.argsort(keys.cpu().numpy(), kind="stable")
+    row_src = torch.empty(n_units * 32, dtype=torch.int32, device=cuda_device)
+    unit_len = torch.empty(n_units, dtype=torch.int32, device=cuda_device)
+    off = torch.empty(n_units + 1, dtype=torch.int64, device=cuda_device)
+    order = torch.empty(n_units, dtype=torch.int32, device=cuda_device)
+    totals = torch.empty(2, dtype=torch.int64, device=cuda_device)
+    _lib.call("fvr_rplan_layout", d.data_ptr(), n_views, w, h, 2, 4, 16, buckets, row_src.data_ptr(),
+              unit_len.data_ptr(), off.data_ptr(), order.data_ptr(), totals.data_ptr(), _lib.stream_ptr())
+    assert np.array_equal(row_src.cpu().numpy(), rs_ref.cpu().numpy())
+    assert np.array_equal(unit_len.cpu().numpy(), ul)
+    assert np.array_equal(off.cpu().numpy(), np.concatenate([[0], np.cumsum(ul)]))
+    assert np.array_equal(order.cpu().numpy(), order_ref)
+    assert totals.cpu().tolist() == [int(ul.sum()), int(ul.max())]
+
+
+def test_flame_rays_kp_map_morton_order(cuda_device):
+    import torch
+
+    from paper_1809_06417_b200 import _lib
+
+    rng = np.random.default_rng(3)
+    crops = (rng.random((5, 77, 131)) < 0.3).astype(np.uint8)
+    d = torch.from_numpy(crops).to(cuda_device)
+    n = int(crops.sum())
+    rays = torch.empty(n, dtype=torch.int32, device=cuda_device)
+    cnt = torch.empty(1, dtype=torch.int64, device=cuda_device)
+    _lib.call("fvr_flame_rays", d.data_ptr(), 5, 131, 77, n, rays.data_ptr(), cnt.data_ptr(), _lib.stream_ptr())
+    v, r, c = np.nonzero(crops)
+    assert int(cnt.item()) == n
+    assert np.array_equal(rays.cpu().numpy(), (v << 24) | (r * 131 + c))
+    # key-point map: position in the list, -1 elsewhere
+    shape = (33, 40, 17)
+    n_vox = int(np.prod(shape))
+    kp = np.sort(rng.choice(n_vox, 5000, replace=False)).astype(np.int32)
+    kp = kp[rng.permutation(kp.size)]
+    dk = torch.from_numpy(kp).to(cuda_device)
+    m = torch.empty(n_vox, dtype=torch.int32, device=cuda_device)
+    _lib.call("fvr_kp_map", dk.data_ptr(), kp.size, n_vox, m.data_ptr(), _lib.stream_ptr())
+    want = np.full(n_vox, -1, np.int32)
+    want[kp] = np.arange(kp.size)
+    assert np.array_equal(m.cpu().numpy(), want)
+    # Morton order of the permuted list
+    out = torch.empty_like(dk)
+    g = _lib.FvrGrid()
+    g.nx, g.ny, g.nz = shape[0] - 1, shape[1] - 1, shape[2] - 1
+    g.edge = 1.0
+    _lib.call("fvr_morton_order", dk.data_ptr(), kp.size, g, out.data_ptr(), _lib.stream_ptr())
+    mk = _morton_ref(kp.astype(np.int64), shape)
+    assert np.array_equal(out.cpu().numpy(), kp[np.argsort(mk, kind="stable")])
