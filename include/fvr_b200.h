@@ -390,12 +390,15 @@ int fvr_loop_weighted_residual(const int32_t* sample_meta, int64_t n_samples, co
  * holds a pixel's (sample's) channels interleaved with pitch 1 or 4, values /
  * layout hold n_channels lattice planes and state n_channels loop states
  * (converged channels are skipped).  kp_values (may be NULL): the render
- * plan's operand (fvr_rplan_pack), updated with every written value. */
+ * plan's operand (fvr_rplan_pack), updated with every written value.
+ * sample_plan = 1 when the plan is the stochastic sample plan (residual =
+ * rho): it selects the loop schedule tuned for each (the merged plan's
+ * gather is software-pipelined); results do not depend on it. */
 int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_off, const int32_t* row_of_pos,
                     const int32_t* entries, const uint32_t* entries_b, int64_t n_kp, const float* residual, int32_t n_channels,
                     const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
                     fvr_grid_t grid, float* kp_values, int64_t* packed, const fvr_loop_state_t* state,
-                    void* stream);
+                    int32_t sample_plan, void* stream);
 int fvr_loop_update_packed(const int64_t* packed, int64_t n_kp, const int32_t* kp_index,
                            float* values, float* layout, int32_t layout_kind, int32_t layout_nch,
                            fvr_grid_t grid, float* kp_values, int32_t kp_values_pitch,

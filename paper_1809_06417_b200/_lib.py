@@ -161,7 +161,8 @@ _SIGNATURES = {
     "fvr_loop_weighted_residual": (c_int, [_P, c_int64, _P, c_int32, c_int32, _P, c_int32, c_uint64, c_double,
                                            c_int64, _P, _P, c_int32, _P]),
     "fvr_stochastic_g": (c_int, [c_uint64, ctypes.c_uint32, _P, _P, c_int64, c_double, _P, _P]),
-    "fvr_loop_gather": (c_int, [_P, _P, _P, _P, _P, c_int64, _P, c_int32, _P, _P, _P, c_int32, _GRID, _P, _P, _P, _P]),
+    "fvr_loop_gather": (c_int, [_P, _P, _P, _P, _P, c_int64, _P, c_int32, _P, _P, _P, c_int32, _GRID, _P, _P, _P,
+                                c_int32, _P]),
     "fvr_loop_update_packed": (c_int, [_P, c_int64, _P, _P, _P, c_int32, c_int32, _GRID, _P, c_int32, _P, _P]),
     "fvr_pack_correction": (c_int, [_P, _P, c_int64, _P, _P]),
     "fvr_unpack_correction": (c_int, [_P, _P, c_int64, _P, _P]),

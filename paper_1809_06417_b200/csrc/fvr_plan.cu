@@ -470,6 +470,15 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
 #ifndef FVR_GATHER_BATCH
 #define FVR_GATHER_BATCH 32
 #endif
+// The merged plan's gather (6-byte entries) is software-pipelined in batches
+// of FVR_GATHER_PIPE entries at 5 CTAs per SM (46 registers): config 2
+// K-adjust 0.0527 ms unpipelined (batch 32, 4 CTAs) -> 0.0500 / 0.0514 /
+// 0.0489 ms pipelined at 16 / 24 / 8 (8: 5 CTAs).  The sample plan's gather
+// (rho reads instead of residuals) keeps the unpipelined loop: pipelined it
+// took 0.100 / 0.107 ms against 0.0985 (profiles/r2_ab_gather_pipelined.log).
+#ifndef FVR_GATHER_PIPE
+#define FVR_GATHER_PIPE 8
+#endif
 // the int2 sample plan: batch 32 / 24 / 16 = 0.190 (spills) / 0.157 / 0.169 ms
 // at config 2 with entry pairs per load; with 32-byte chunks 24 / 16 = 0.1525 /
 // 0.1565 ms
@@ -479,11 +488,25 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
 // CTAs per SM: 6-byte entries leave room for 4 (config 2, deterministic,
 // batch x CTAs 32x3 / 32x4 / 32x5 / 24x5 / 16x4 / 64x2: 0.0763 / 0.0718 /
 // 0.0718 / 0.0714 / 0.0766 / 0.0845 ms); the int2 sample plan keeps 3.
-#ifndef FVR_GATHER_MINB
-#define FVR_GATHER_MINB(E6) ((E6) ? 4 : 3)
+#ifndef FVR_GATHER_E6_MINB
+#define FVR_GATHER_E6_MINB 4
 #endif
-template <bool PACKED, int NCH, bool E6>
-__global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
+#ifndef FVR_GATHER_PIPE_MINB
+#define FVR_GATHER_PIPE_MINB 5
+#endif
+// (three channels, unpipelined: FVR_GATHER3_MINB CTAs, batch FVR_GATHER3_BATCH)
+#ifndef FVR_GATHER3_E6_MINB
+#define FVR_GATHER3_E6_MINB 3
+#endif
+#define FVR_GATHER3_MINB(E6) ((E6) ? FVR_GATHER3_E6_MINB : 2)
+#ifndef FVR_GATHER3_BATCH
+#define FVR_GATHER3_BATCH 16
+#endif
+#define FVR_GATHER_MINB(E6, PIPE, NCH)                                                         \
+    ((PIPE) ? ((NCH) == 1 ? FVR_GATHER_PIPE_MINB : 4)                                          \
+            : (NCH) > 1 ? FVR_GATHER3_MINB(E6) : (E6) ? FVR_GATHER_E6_MINB : 3)
+template <bool PACKED, int NCH, bool E6, bool PIPE>
+__global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6, PIPE, NCH)) gather_kernel(
     const int32_t* __restrict__ slice_len, const long long* __restrict__ slice_off,
     const int32_t* __restrict__ row_of_pos, const int2* __restrict__ entries, const uint32_t* __restrict__ ent_b,
     int64_t n_rows,
@@ -519,7 +542,8 @@ __global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
     if (!any) return;
     const int lane = threadIdx.x & 31;
     const int64_t n_slices = (n_rows + 31) >> 5;
-    constexpr int B = E6 ? FVR_GATHER_BATCH : FVR_SPLAN_BATCH;
+    // three channels: a float4 residual per entry, so half the batch (no spills)
+    constexpr int B = NCH > 1 ? (PIPE ? 16 : FVR_GATHER3_BATCH) : E6 ? FVR_GATHER_BATCH : FVR_SPLAN_BATCH;
     for (int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < n_slices;
          sl += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int len = slice_len[sl];
@@ -540,6 +564,48 @@ __global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6)) gather_kernel(
         long long acc[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] = 0;
+        if constexpr (E6 && PIPE) {
+            // software-pipelined: the next batch's chunks are loaded before
+            // this batch's residual reads, so the plan stream keeps flowing
+            // while the warp waits on L1/L2
+            constexpr int D = FVR_GATHER_PIPE;  // entries per batch (a multiple of 8)
+            static_assert(D % 8 == 0, "batches of whole 16-byte chunks");
+            const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+            uint4 ca[D / 4], cb[D / 8], na[D / 4], nb[D / 8];
+#pragma unroll
+            for (int i = 0; i < D / 4; ++i) ca[i] = 4 * i < len ? __ldcs(ea + (int64_t)i * 32) : z;
+#pragma unroll
+            for (int i = 0; i < D / 8; ++i) cb[i] = 8 * i < len ? __ldcs(eb + (int64_t)i * 32) : z;
+            for (int t = 0; t < len; t += D) {
+                const int tn = t + D;
+#pragma unroll
+                for (int i = 0; i < D / 4; ++i) na[i] = tn + 4 * i < len ? __ldcs(ea + (int64_t)(tn / 4 + i) * 32) : z;
+#pragma unroll
+                for (int i = 0; i < D / 8; ++i) nb[i] = tn + 8 * i < len ? __ldcs(eb + (int64_t)(tn / 8 + i) * 32) : z;
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    const uint4& q = ca[i / 4];
+                    const uint32_t a = (i & 3) == 0 ? q.x : (i & 3) == 1 ? q.y : (i & 3) == 2 ? q.z : q.w;
+                    const uint4& h = cb[i / 8];
+                    const uint32_t hw = ((i & 7) >> 1) == 0 ? h.x : ((i & 7) >> 1) == 1 ? h.y : ((i & 7) >> 1) == 2 ? h.z : h.w;
+                    const uint32_t half = (i & 1) ? (hw >> 16) : (hw & 0xFFFFu);
+                    const int idx = (int)(a & 0xFFFFFFu);
+                    const float wgt = __uint_as_float(((a >> 24) << 23) | (half << 7));
+                    if (NCH == 1) {
+                        acc[0] += __float2ll_rn(__ldg(residual + idx) * wgt * 4294967296.0f);
+                    } else {
+                        const float4 r = __ldg(reinterpret_cast<const float4*>(residual) + idx);
+                        const float rr[3] = {r.x, r.y, r.z};
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c) acc[c] += __float2ll_rn(rr[c] * wgt * 4294967296.0f);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < D / 4; ++i) ca[i] = na[i];
+#pragma unroll
+                for (int i = 0; i < D / 8; ++i) cb[i] = nb[i];
+            }
+        } else
         for (int t = 0; t < len; t += B) {
             int2 en[B];
             if (E6) {
@@ -678,7 +744,7 @@ extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_of
                                const int32_t* entries, const uint32_t* entries_b, int64_t n_kp, const float* residual, int32_t n_channels,
                                const int32_t* kp_index, float* values, float* layout, int32_t layout_kind,
                                fvr_grid_t grid, float* kp_values, int64_t* packed, const fvr_loop_state_t* state,
-                               void* stream) {
+                               int32_t sample_plan, void* stream) {
     FVR_TRY_BEGIN
     if (n_kp == 0) return FVR_OK;
     if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "the loop gathers 1 or 3 channels");
@@ -692,12 +758,13 @@ extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_of
     const auto* en = reinterpret_cast<const int2*>(entries);
     long long* pk = reinterpret_cast<long long*>(packed);
     cudaError_t e = cudaSuccess;
-#define FVR_GATHER(P, C, E)                                                                                  \
-    e = launch_pdl(gather_kernel<P, C, E>, (unsigned)blocks, 256, st, slice_len, so, row_of_pos, en, entries_b,  \
+#define FVR_GATHER(P, C, E, Q)                                                                                \
+    e = launch_pdl(gather_kernel<P, C, E, Q>, (unsigned)blocks, 256, st, slice_len, so, row_of_pos, en, entries_b,  \
                    n_kp, residual, kp_index, values, plane, layout, layout_kind, sy, ny1, kp_values, pk, state)
-#define FVR_GATHER_E(P, C)           \
-    if (entries_b) FVR_GATHER(P, C, true); \
-    else FVR_GATHER(P, C, false)
+#define FVR_GATHER_E(P, C)                                 \
+    if (entries_b && !sample_plan) FVR_GATHER(P, C, true, true); \
+    else if (entries_b) FVR_GATHER(P, C, true, false);           \
+    else FVR_GATHER(P, C, false, false)
     if (packed) {
         if (n_channels == 1) { FVR_GATHER_E(true, 1); } else { FVR_GATHER_E(true, 3); }
     } else {

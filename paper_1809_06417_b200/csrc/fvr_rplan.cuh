@@ -623,7 +623,8 @@ __device__ __forceinline__ void rplan_render_unit(
         }
     };
     int t = 0;
-    constexpr int B = FVR_RPLAN_BATCH;
+    // three channels: a float4 operand per entry, so half the batch (no spills)
+    constexpr int B = NCH > 1 ? 16 : FVR_RPLAN_BATCH;
     static_assert(B % kRpB == 0, "batches of whole chunks");
     const uint32_t* va = ent_a + ((off / kRpA) * 32 + lane) * kRpA;
     constexpr int kB = WIDE ? kRpA : kRpB;  // weight entries per (kRpA-word) chunk
@@ -678,7 +679,7 @@ __device__ __forceinline__ void rplan_render_unit(
 }
 
 template <int NCH, bool WIDE>
-__global__ void __launch_bounds__(256, FVR_RPLAN_MINB) rplan_render_kernel(
+__global__ void __launch_bounds__(256, NCH == 1 ? FVR_RPLAN_MINB : 2) rplan_render_kernel(
     const int* __restrict__ unit_len, const long long* __restrict__ unit_off, const uint32_t* __restrict__ ent_a,
     const uint32_t* __restrict__ ent_b, const double* __restrict__ base, const double* __restrict__ t_fin,
     const int* __restrict__ unit_order, const int* __restrict__ row_src, int n_units, int units_x,

@@ -909,7 +909,7 @@ class ChannelLoop:
                   src.data_ptr(), self.nch, self.kp.data_ptr(), self.values.data_ptr(),
                   _lib.ptr(self.layout), self.layout_kind, self.grid,
                   _lib.ptr(self.rp_kpv) if self.rplan else None, self.packed.data_ptr() if packed else None,
-                  self.state.data_ptr(), stream)
+                  self.state.data_ptr(), int(self.sample_plan), stream)
         return 1
 
     def _update_packed(self, stream):
