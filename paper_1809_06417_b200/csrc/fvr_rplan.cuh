@@ -564,6 +564,14 @@ __global__ void __launch_bounds__(128, FVR_RPLAN_FILL_MINB) rplan_fill_kernel(
 #ifndef FVR_RPLAN_MINB
 #define FVR_RPLAN_MINB 3
 #endif
+// The one-channel 6-byte render software-pipelined in batches of
+// FVR_RPLAN_PIPE entries (0: the batch loop above): config 2 K-render 0.0911
+// -> 0.0903 ms at 16 entries and 3 CTAs (80 registers); 16 at 4 / 5 CTAs and
+// 32 at 2 CTAs lose (0.0912 / 0.1034 / 0.0976 ms;
+// profiles/r2_ab_render_pipelined.log)
+#ifndef FVR_RPLAN_PIPE
+#define FVR_RPLAN_PIPE 16
+#endif
 
 // fvr_loop_finalize_t on the device (on = false: no fused finalize).
 struct RplanFinalize {
@@ -651,8 +659,46 @@ __device__ __forceinline__ void rplan_render_unit(
 #pragma unroll
         for (int c = 0; c < NCH; ++c) acc[c] += (double)part[c];
     };
-    for (; t + B <= len; t += B) batch(std::integral_constant<int, B>{}, t);
-    for (; t < len; t += kRpB) batch(std::integral_constant<int, kRpB>{}, t);
+#if FVR_RPLAN_PIPE
+    if constexpr (!WIDE && NCH == 1) {
+        // software-pipelined: the next batch's chunks are loaded before this
+        // batch's operand reads
+        constexpr int D = FVR_RPLAN_PIPE;  // a multiple of kRpB
+        static_assert(D % kRpB == 0, "batches of whole chunks");
+        RpChunk ca[D / kRpA], cb[D / kRpB], na[D / kRpA], nb[D / kRpB];
+        RpChunk zc;
+#pragma unroll
+        for (int i = 0; i < kRpA; ++i) zc.w[i] = 0u;
+#pragma unroll
+        for (int i = 0; i < D / kRpA; ++i) ca[i] = i * kRpA < len ? rplan_stream(va + (int64_t)i * (32 * kRpA)) : zc;
+#pragma unroll
+        for (int i = 0; i < D / kRpB; ++i) cb[i] = i * kRpB < len ? rplan_stream(vb + (int64_t)i * (32 * kRpA)) : zc;
+        for (; t < len; t += D) {
+            const int tn = t + D;
+#pragma unroll
+            for (int i = 0; i < D / kRpA; ++i)
+                na[i] = tn + i * kRpA < len ? rplan_stream(va + (int64_t)(tn / kRpA + i) * (32 * kRpA)) : zc;
+#pragma unroll
+            for (int i = 0; i < D / kRpB; ++i)
+                nb[i] = tn + i * kRpB < len ? rplan_stream(vb + (int64_t)(tn / kRpB + i) * (32 * kRpA)) : zc;
+            float part[1] = {0.f};
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                const uint32_t hw = cb[i / kRpB].w[(i % kRpB) >> 1];
+                term(ca[i / kRpA].w[i % kRpA], (i & 1) ? (hw >> 16) : (hw & 0xFFFFu), part);
+            }
+            acc[0] += (double)part[0];
+#pragma unroll
+            for (int i = 0; i < D / kRpA; ++i) ca[i] = na[i];
+#pragma unroll
+            for (int i = 0; i < D / kRpB; ++i) cb[i] = nb[i];
+        }
+    } else
+#endif
+    {
+        for (; t + B <= len; t += B) batch(std::integral_constant<int, B>{}, t);
+        for (; t < len; t += kRpB) batch(std::integral_constant<int, kRpB>{}, t);
+    }
     const int64_t r = (int64_t)unit * 32 + lane;
     int view, col, row;
     const bool in = rplan_pixel(row_src ? __ldg(row_src + r) : r, units_x, units_per_view, w, h, view, col, row);
