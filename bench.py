@@ -415,7 +415,7 @@ def run_gpu(args):
             import cProfile
 
             prof = cProfile.Profile()
-        for _ in range(5):  # median of five calls: one call is ~30 ms of host + device time
+        for _ in range(9):  # median of nine calls (~11 ms each; the clock sampler's 100 ms nvidia-smi query stalls one or two)
             barrier()
             if prof:
                 prof.enable()
@@ -454,7 +454,7 @@ def run_gpu(args):
                "h2d_bytes_per_step": int(h2d / trace.iterations), "d2h_bytes_per_step": int(d2h / trace.iterations),
                "calls_ms": [1e3 * x for x in walls],
                "note": "reconstruct_channel() on host numpy inputs; H2D of frames/lattice/hull and D2H of the "
-                       "grid + trace inside the timed call, amortised over its iterations; median of 5 calls"}
+                       "grid + trace inside the timed call, amortised over its iterations; median of 9 calls"}
 
     time.sleep(0.15)  # one more nvidia-smi row after the last timed region
     clocks = sampler.stop()

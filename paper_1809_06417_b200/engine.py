@@ -157,6 +157,17 @@ def exchange(comm, sq, vol, v_begin: int, v_end: int, rows_per_view: int, rank: 
 
 
 _SIDE: dict = {}
+_SCAT: dict = {}
+
+
+def _scatter_dirs(n: int, dev):
+    """fibonacci_sphere(n) on the device, built once per (n, device)."""
+    key = (n, str(dev))
+    if key not in _SCAT:
+        from .radiometry import fibonacci_sphere
+
+        _SCAT[key] = _lib.torch().from_numpy(np.ascontiguousarray(fibonacci_sphere(n))).to(dev)
+    return _SCAT[key]
 
 
 def _side_stream(dev):
@@ -166,7 +177,10 @@ def _side_stream(dev):
     t = _lib.torch()
     key = str(dev)
     if key not in _SIDE:
-        _SIDE[key] = t.cuda.Stream(device=dev)
+        # higher priority than the loop's stream: the side stream's short
+        # layout kernels are scheduled ahead of a running fill's remaining
+        # CTAs instead of after them
+        _SIDE[key] = t.cuda.Stream(device=dev, priority=-1)
     return _SIDE[key]
 
 
@@ -262,6 +276,7 @@ class ChannelLoop:
                 self.inside = t.from_numpy(inside).to(dev).view(t.uint8)
             else:
                 self.inside = t.from_numpy(inside.astype(np.uint8)).to(dev)
+        self._mark("cams+src+inside")
         self.values = t.empty((C,) + shape, dtype=t.float32, device=dev)
         if values is not None:
             self.values.copy_(t.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).reshape((C,) + shape))
@@ -279,11 +294,7 @@ class ChannelLoop:
                 self.values[1:].copy_(self.values[0:1].expand((C - 1,) + shape))
             if kp_mask is not None:
                 kp_dev = t.from_numpy(np.ascontiguousarray(kp_mask, dtype=np.uint8)).to(dev)
-            kp_t = t.nonzero(kp_dev.reshape(-1)).reshape(-1).to(t.int32)
-            if _morton_enabled():  # only the key-point list is ordered (no lattice-sized permutation)
-                kp_t = _morton_order(kp_t, shape)
-            self.n_kp = int(kp_t.numel())
-            self.kp = kp_t if self.n_kp else t.zeros(1, dtype=t.int32, device=dev)
+            self.kp = None  # listed below, after the work that needs only kp_dev is enqueued
         else:
             kp_dev = t.from_numpy(np.ascontiguousarray(kp_mask, dtype=np.uint8)).to(dev)
             kp_idx = np.flatnonzero(kp_mask.ravel()).astype(np.int32)
@@ -292,16 +303,15 @@ class ChannelLoop:
             if _morton_enabled() and self.n_kp:
                 self.kp = _morton_order(self.kp, shape)
         self.accum = None  # scatter path only
+        kp_ready = t.cuda.Event()  # kp_dev (and the initial lattice) on the loop's stream
+        kp_ready.record()
 
         self._mark("inputs+hull kp")
         # render configuration of the loop (render_pixels without a phase: g = 0)
         self.scattering = bool(render_cfg.scattering_enabled and render_cfg.sigma_s > 0.0)
         if self.scattering:
-            from .radiometry import fibonacci_sphere
-
-            sd = fibonacci_sphere(render_cfg.scatter_dirs)
-            self.scat = t.from_numpy(np.ascontiguousarray(sd)).to(dev)
-            n_scat = sd.shape[0]
+            self.scat = _scatter_dirs(int(render_cfg.scatter_dirs), dev)
+            n_scat = int(self.scat.shape[0])
         else:
             self.scat = None
             n_scat = 1
@@ -362,11 +372,103 @@ class ChannelLoop:
         self.n_rays = int(ray_list_t.numel())
         self.rays = ray_list_t if self.n_rays else t.zeros(1, dtype=t.int32, device=dev)
         self.ray_base = ray_base
+        # the render plan's count pass needs only the geometry, the occupancy
+        # and kp_dev: it is queued on the loop's stream before anything waits
+        # on the host; the hull key-point list (whose count the host must
+        # read) and later the adjust plan's count are built on a persistent
+        # side stream meanwhile
+        main = t.cuda.current_stream()
+        side = _side_stream(dev)
+        pre = t.cuda.Event()
+        pre.record(main)
+        if self.layout_kind and os.environ.get("FVR_RENDER", "plan") != "march":
+            self._rp_counted = self._rplan_count()
+        self._mark("render count queued")
+        side.wait_event(kp_ready)  # (the key-point list does not wait for the occupancy)
+        if self.kp is None:
+            with t.cuda.stream(side):
+                kp_t = t.nonzero(kp_dev.reshape(-1)).reshape(-1).to(t.int32)  # synchronises the side stream
+                if _morton_enabled():  # only the key-point list is ordered (no lattice-sized permutation)
+                    kp_t = _morton_order(kp_t, shape)
+            self.n_kp = int(kp_t.numel())
+            self.kp = kp_t if self.n_kp else t.zeros(1, dtype=t.int32, device=dev)
+            self.kp.record_stream(main)
+            main.wait_stream(side)  # (later work on the loop's stream reads the list)
+        self._mark("kp list")
+        side.wait_event(pre)  # the flame rays, for the adjust plan's count
+        if self.n_rays > 0 and self.n_kp > 0 and os.environ.get("FVR_ADJUST") != "scatter":
+            with t.cuda.stream(side):  # the key-point map both plan fills read
+                self._kp_map()
+                self._kpmap.record_stream(main)
 
         self._mark("flame rays")
-        # work buffers
         # channels interleaved per pixel (pitch 1, or 4 for three channels)
         self.pitch = 1 if C == 1 else 4
+        # K-adjust as a voxel-driven gather over a precomputed plan: the merged
+        # operator A in deterministic mode, the per-sample plan (weights G
+        # applied through rho each iteration) in stochastic mode; the
+        # ray-driven scatter remains for plans that would not fit
+        self.plan = (self.n_rays > 0 and self.n_kp > 0 and os.environ.get("FVR_ADJUST") != "scatter")
+        self.sample_plan = self.plan and loop_cfg.stochastic
+        self.plan_nnz = 0
+        self.n_samples = 0
+        self.splan_e6 = False
+        self.rho = None
+        self._mark("work buffers")
+        # The plan builds on two streams.  The render plan's count pass was
+        # queued on the loop's stream above, so its layout and fill go first
+        # there (the fill waits only for the key-point map); the adjust plan's
+        # map, count pass and layout run on the side stream meanwhile, and its
+        # fill follows the render plan's.  Side by side on two streams the
+        # fills slowed each other (config 2: 1.73 + 1.78 ms overlapped,
+        # against 1.59 + 0.92 ms in sequence); FVR_FILL_SERIAL=0 overlaps them.
+        keep = []
+        adjust_done = kpmap_ready = pc = None
+        rs = self._rplan_scan(*self._rp_counted) if self._rp_counted is not None else None
+        self._rp_counted = None
+        self._mark("render layout queued")
+        if self.plan:
+            kpmap_ready = t.cuda.Event()
+            kpmap_ready.record(side)
+            with t.cuda.stream(side):  # queued ahead of the render fill, which would hold every SM
+                pc = self._plan_count()
+        self._mark("adjust count queued")
+        rfill_done = None
+        if rs is not None:
+            sizes = rs["sizes"].cpu().tolist()
+            self._mark("render sizes read")
+            if kpmap_ready is not None:
+                main.wait_event(kpmap_ready)
+            self.rplan = self._rplan_fill(rs, sizes)
+            rfill_done = t.cuda.Event()
+            rfill_done.record(main)
+            self._mark("render fill queued")
+        if pc is not None:
+            with t.cuda.stream(side):
+                sizes = pc["sizes"].cpu().tolist()  # synchronises the side stream only
+                self._mark("adjust sizes read")
+                if rfill_done is not None and os.environ.get("FVR_FILL_SERIAL", "1") == "1":
+                    side.wait_event(rfill_done)
+                self.plan = self._plan_fill(pc, sizes, side, keep)
+                self.sample_plan = self.plan and self.sample_plan
+                adjust_done = t.cuda.Event()
+                adjust_done.record(side)
+            # buffers from the side stream's pool that the loop's stream uses
+            for buf in (getattr(self, "plan_entries", None), getattr(self, "plan_entries_b", None),
+                        getattr(self, "plan_slice_len", None), getattr(self, "plan_slice_off", None),
+                        getattr(self, "plan_row_of_pos", None), getattr(self, "sample_meta", None),
+                        getattr(self, "rho", None)):
+                if buf is not None:
+                    buf.record_stream(main)
+            main.wait_event(adjust_done)
+        del keep
+        self._mark("adjust fill queued")
+        if self.layout_kind and not self.rplan:
+            # float4 per (key point, channel), channels interleaved (fvr_stencil.cuh)
+            self.layout = t.empty(shape + (C, 4), dtype=t.float32, device=dev)
+            _lib.call("fvr_pack_layout", self.values.data_ptr(), C, self.grid, self.layout_kind,
+                      self.layout.data_ptr(), _lib.stream_ptr())
+        # work buffers (allocated once the plan builds are queued)
         self.residual = t.zeros((max(len(local), 1), self.h_bb, self.w_bb, self.pitch), dtype=t.float32,
                                 device=dev)
         self.n_sq = V * self.bpv
@@ -387,69 +489,6 @@ class ChannelLoop:
         self.trace = t.zeros((C, max(self.max_iters, 1)), dtype=t.float64, device=dev)
         self.trace_vol = t.zeros((C, max(self.max_iters, 1)), dtype=t.float64, device=dev) \
             if ground_truth is not None else None
-        # K-adjust as a voxel-driven gather over a precomputed plan: the merged
-        # operator A in deterministic mode, the per-sample plan (weights G
-        # applied through rho each iteration) in stochastic mode; the
-        # ray-driven scatter remains for plans that would not fit
-        self.plan = (self.n_rays > 0 and self.n_kp > 0 and os.environ.get("FVR_ADJUST") != "scatter")
-        self.sample_plan = self.plan and loop_cfg.stochastic
-        self.plan_nnz = 0
-        self.n_samples = 0
-        self.splan_e6 = False
-        self.rho = None
-        # Both operators' count passes are enqueued, their sizes read with one
-        # synchronisation, and the two fills run concurrently (the adjust
-        # plan's on a side stream; every buffer is allocated on the loop's
-        # stream, so the caching allocator keeps them across calls).
-        self._mark("work buffers")
-        # the two plans' count passes side by side: the adjust plan's (with
-        # its SELL layout) on a persistent side stream, the render plan's on
-        # the loop's stream; both are latency-bound at moderate occupancy.
-        # The adjust plan's sizes come back first, so its fill runs on the
-        # device while the host enqueues the render plan's scan; the two
-        # fills still run one after the other (side by side on two streams
-        # each slowed the other: config 2, 1.73 + 1.78 ms overlapped against
-        # 1.59 + 0.92 ms in sequence)
-        main = t.cuda.current_stream()
-        ready = t.cuda.Event()
-        ready.record(main)
-        if self.layout_kind and os.environ.get("FVR_RENDER", "plan") != "march":
-            self._rp_counted = self._rplan_count()
-        keep = []
-        adjust_done = None
-        if self.plan:
-            side = _side_stream(dev)
-            side.wait_event(ready)
-            with t.cuda.stream(side):
-                self._kp_map()
-                pc = self._plan_count()
-                sizes = pc["sizes"].cpu().tolist()  # synchronises the side stream only
-                self.plan = self._plan_fill(pc, sizes, side, keep)
-                self.sample_plan = self.plan and self.sample_plan
-                adjust_done = t.cuda.Event()
-                adjust_done.record(side)
-            # buffers from the side stream's pool that the loop's stream uses
-            for buf in (self._kpmap, getattr(self, "plan_entries", None), getattr(self, "plan_entries_b", None),
-                        getattr(self, "plan_slice_len", None), getattr(self, "plan_slice_off", None),
-                        getattr(self, "plan_row_of_pos", None), getattr(self, "sample_meta", None),
-                        getattr(self, "rho", None)):
-                if buf is not None:
-                    buf.record_stream(main)
-        rs = self._rplan_scan(*self._rp_counted) if self._rp_counted is not None else None
-        self._rp_counted = None
-        if rs is not None:
-            sizes = rs["sizes"].cpu().tolist()
-            if adjust_done is not None:
-                main.wait_event(adjust_done)
-            self.rplan = self._rplan_fill(rs, sizes)
-        if adjust_done is not None:
-            main.wait_event(adjust_done)
-        del keep
-        if self.layout_kind and not self.rplan:
-            # float4 per (key point, channel), channels interleaved (fvr_stencil.cuh)
-            self.layout = t.empty(shape + (C, 4), dtype=t.float32, device=dev)
-            _lib.call("fvr_pack_layout", self.values.data_ptr(), C, self.grid, self.layout_kind,
-                      self.layout.data_ptr(), _lib.stream_ptr())
         self._mark("plans")
         if not self.plan:
             self.accum = t.zeros((C,) + shape, dtype=t.int64, device=dev)
