@@ -207,3 +207,44 @@ def test_flame_rays_kp_map_morton_order(cuda_device):
     _lib.call("fvr_morton_order", dk.data_ptr(), kp.size, g, out.data_ptr(), _lib.stream_ptr())
     mk = _morton_ref(kp.astype(np.int64), shape)
     assert np.array_equal(out.cpu().numpy(), kp[np.argsort(mk, kind="stable")])
+
+
+def _dist_ref(values, force, cap=30):
+    """fvr_occupancy restated: seed 0 at positive or forced key points (cap + 1
+    elsewhere), then the separable z, y, x passes min_d max(|d|, f) over
+    |d| <= cap inside the lattice."""
+    m = (values > 0).any(0) | force.astype(bool)
+    f = np.where(m, 0, cap + 1).astype(np.int64)
+    for axis in (2, 1, 0):
+        out = f.copy()
+        n = f.shape[axis]
+        for dd in range(1, cap + 1):
+            if dd >= n:
+                break
+            lo = [slice(None)] * 3
+            hi = [slice(None)] * 3
+            lo[axis], hi[axis] = slice(dd, None), slice(None, n - dd)
+            # neighbour at p - dd for positions p >= dd, and at p + dd for p < n - dd
+            out[tuple(lo)] = np.minimum(out[tuple(lo)], np.maximum(dd, f[tuple(hi)]))
+            out[tuple(hi)] = np.minimum(out[tuple(hi)], np.maximum(dd, f[tuple(lo)]))
+        f = out
+    return f.astype(np.uint8)
+
+
+@pytest.mark.parametrize("shape", [(33, 70, 17), (65, 65, 65), (129, 40, 129)])
+def test_occupancy_distance_map(cuda_device, shape):
+    import torch
+
+    from paper_1809_06417_b200 import _lib
+
+    rng = np.random.default_rng(shape[1])
+    values = np.where(rng.random((2,) + shape) < 0.002, 1.0, -1.0).astype(np.float32)
+    force = (rng.random(shape) < 0.001).astype(np.uint8)
+    g = _lib.FvrGrid()
+    g.nx, g.ny, g.nz = shape[0] - 1, shape[1] - 1, shape[2] - 1
+    g.edge = 1.0
+    dv = torch.from_numpy(values).to(cuda_device)
+    df = torch.from_numpy(force).to(cuda_device)
+    occ = torch.empty(shape, dtype=torch.uint8, device=cuda_device)
+    _lib.call("fvr_occupancy", dv.data_ptr(), 2, df.data_ptr(), g, occ.data_ptr(), _lib.stream_ptr())
+    assert np.array_equal(occ.cpu().numpy(), _dist_ref(values, force))
