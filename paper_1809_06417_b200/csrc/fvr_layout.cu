@@ -17,31 +17,11 @@ namespace fvr {
 
 namespace {
 
-// Stream-ordered scratch from the default pool; the pool keeps up to
-// kKeepBytes across synchronisations (the default threshold, 0, hands every
-// block back to the driver at each sync, so every call would pay a fresh
-// allocation).
-constexpr uint64_t kKeepBytes = 256ull << 20;
-
-void keep_pool(cudaStream_t st) {
-    static bool done[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64 || done[dev]) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = kKeepBytes;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    done[dev] = true;
-    (void)st;
-}
-
 struct Scratch {
     cudaStream_t st;
     void* p[6] = {};
     int n = 0;
-    explicit Scratch(cudaStream_t s) : st(s) { keep_pool(s); }
+    explicit Scratch(cudaStream_t s) : st(s) { keep_default_pool(); }
     template <typename T>
     T* get(size_t count) {
         void* q = nullptr;

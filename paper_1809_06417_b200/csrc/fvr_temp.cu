@@ -360,6 +360,7 @@ extern "C" int fvr_ctmap_build(double t_min, double step, int32_t n, int32_t app
     cudaStream_t st = (cudaStream_t)stream;
     const int rows = n + (append_t_max ? 1 : 0);
     double* radiance = nullptr;
+    keep_default_pool();
     if (cudaMallocAsync(&radiance, sizeof(double) * (size_t)rows * 81, st) != cudaSuccess)
         return set_error(FVR_ERR_CUDA, "ctmap_build: cannot allocate the radiance scratch");
     planck_nodes_kernel<<<(rows * 81 + 127) / 128, 128, 0, st>>>(t_min, step, rows, append_t_max, t_max, temps,
