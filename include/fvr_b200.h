@@ -356,6 +356,11 @@ int fvr_sample_plan_fill(const fvr_camera_t* cams, const int32_t* ray_list, int6
  * have their sample ids rewritten in place, meta_out[new] = meta_in[natural]. */
 int fvr_sample_plan_reorder(int32_t* entries, int64_t n_slots, int32_t e6, const int32_t* new_of_nat,
                             int64_t n_blocks, const int32_t* meta_in, int32_t* meta_out, void* stream);
+/* The same from the fill's block_keys directly (csrc/fvr_layout.cu): a
+ * stable radix sort of their 30-bit Morton part gives new_of_nat, then
+ * fvr_sample_plan_reorder. */
+int fvr_sample_plan_spatial(int32_t* entries, int64_t n_slots, int32_t e6, const int64_t* block_keys,
+                            int64_t n_blocks, const int32_t* meta_in, int32_t* meta_out, void* stream);
 /* The stochastic mode's G = clip(N(1, g_sigma), 0, 2) for (seed, iteration,
  * ray, march index k) -- the counter-based replacement of the reference's
  * rng.normal draw (reconstruct.py:191-204); the weigh pass and the ray-driven
@@ -455,10 +460,12 @@ int fvr_kp_map(const int32_t* kp_index, int64_t n_kp, int64_t n_vox, int32_t* ma
  * to `pad` entries, slice_off (n_slices + 1, exclusive scan of slice_len),
  * row_info[row] = slice_off[pos >> 5] << 5 | (pos & 31); totals[0] = entries
  * per lane over all slices, totals[1] = sum of counts, totals[2] = sum of
- * ray_samples (0 when ray_samples is NULL).  n_slices = ceil(n_rows / 32). */
+ * ray_samples (0 when ray_samples is NULL) and, when ray_sid0 is given, its
+ * exclusive scan (n_rays int64: the sample plan's first sample id per ray).
+ * n_slices = ceil(n_rows / 32). */
 int fvr_sell_layout(const int32_t* counts, int64_t n_rows, int32_t window, int32_t pad,
-                    const int32_t* ray_samples, int64_t n_rays, int32_t* row_of_pos, int32_t* slice_len,
-                    int64_t* slice_off, int64_t* row_info, int64_t* totals, void* stream);
+                    const int32_t* ray_samples, int64_t n_rays, int64_t* ray_sid0, int32_t* row_of_pos,
+                    int32_t* slice_len, int64_t* slice_off, int64_t* row_info, int64_t* totals, void* stream);
 /* The render plan's layout after its count pass: fvr_rplan_tile_rows
  * (row_src, unit_len), unit_off (n_units + 1, exclusive scan of unit_len),
  * unit_order (the fvr_rplan_unit_keys order: longest class first, 2x4-unit
@@ -467,6 +474,12 @@ int fvr_sell_layout(const int32_t* counts, int64_t n_rows, int32_t window, int32
 int fvr_rplan_layout(const int32_t* row_len, int32_t n_views, int32_t bbox_w, int32_t bbox_h, int32_t tile_units_x,
                      int32_t tile_units_y, int32_t align, int32_t buckets, int32_t* row_src, int32_t* unit_len,
                      int64_t* unit_off, int32_t* unit_order, int64_t* totals, void* stream);
+/* Nonzero bytes of v (n of them): *count (device) = how many; the select
+ * writes their indices in order (at most `capacity`; *n_sel = the number
+ * found) -- the hull key-point list from fvr_hull_keypoints' mask. */
+int fvr_count_nonzero_u8(const uint8_t* v, int64_t n, int64_t* count, void* stream);
+int fvr_select_nonzero_u8(const uint8_t* v, int64_t n, int64_t capacity, int32_t* out, int64_t* n_sel,
+                          void* stream);
 /* Flame rays of the bbox crops (u8, n_views x bbox_h x bbox_w, row-major):
  * rays[i] = view << 24 | (row * bbox_w + col) of the i-th nonzero pixel in
  * that order (reconstruct.py:144-149), at most `capacity` of them;

@@ -181,7 +181,10 @@ _SIGNATURES = {
     "fvr_rplan_tile_rows": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, _P, _P, _P]),
     "fvr_morton_order": (c_int, [_P, c_int64, _GRID, _P, _P]),
     "fvr_kp_map": (c_int, [_P, c_int64, c_int64, _P, _P]),
-    "fvr_sell_layout": (c_int, [_P, c_int64, c_int32, c_int32, _P, c_int64, _P, _P, _P, _P, _P, _P]),
+    "fvr_sell_layout": (c_int, [_P, c_int64, c_int32, c_int32, _P, c_int64, _P, _P, _P, _P, _P, _P, _P]),
+    "fvr_sample_plan_spatial": (c_int, [_P, c_int64, c_int32, _P, c_int64, _P, _P, _P]),
+    "fvr_count_nonzero_u8": (c_int, [_P, c_int64, _P, _P]),
+    "fvr_select_nonzero_u8": (c_int, [_P, c_int64, c_int64, _P, _P, _P]),
     "fvr_rplan_layout": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, _P, _P, _P, _P,
                                  _P, _P]),
     "fvr_flame_rays": (c_int, [_P, c_int32, c_int32, c_int32, c_int64, _P, _P, _P]),

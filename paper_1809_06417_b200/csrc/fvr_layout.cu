@@ -107,6 +107,37 @@ __global__ void sell_row_info_kernel(const int32_t* __restrict__ row_of_pos, int
         row_info[row_of_pos[p]] = (off[p >> 5] << 5) | (p & 31);
 }
 
+// sid0[r + 1] = ray_samples[r] (int64, scanned in place afterwards); sid0[0] = 0
+__global__ void shift_to_i64_kernel(const int32_t* __restrict__ v, int64_t n, int64_t* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i + 1] = v[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = 0;
+}
+
+// the sample plan's block keys ((Morton code << 32) | block) split into a
+// 32-bit key and the block index for a stable pair sort
+__global__ void split_keys_kernel(const unsigned long long* __restrict__ keys, int64_t n, uint32_t* __restrict__ k,
+                                  uint32_t* __restrict__ v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long x = keys[i];
+        k[i] = (uint32_t)(x >> 32);
+        v[i] = (uint32_t)x;
+    }
+}
+
+__global__ void inverse_perm_kernel(const uint32_t* __restrict__ sorted_blk, int64_t n, int32_t* __restrict__ inv) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        inv[sorted_blk[i]] = (int32_t)i;
+}
+
+__global__ void count_u8_kernel(const uint8_t* __restrict__ v, int64_t n, unsigned long long* __restrict__ out) {
+    unsigned long long s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        s += v[i] != 0;
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
 __global__ void sum_kernel(const int32_t* __restrict__ v, int64_t n, unsigned long long* __restrict__ out) {
     unsigned long long s = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -194,15 +225,28 @@ extern "C" int fvr_kp_map(const int32_t* kp_index, int64_t n_kp, int64_t n_vox, 
 }
 
 extern "C" int fvr_sell_layout(const int32_t* counts, int64_t n_rows, int32_t window, int32_t pad,
-                               const int32_t* ray_samples, int64_t n_rays, int32_t* row_of_pos, int32_t* slice_len,
-                               int64_t* slice_off, int64_t* row_info, int64_t* totals, void* stream) {
+                               const int32_t* ray_samples, int64_t n_rays, int64_t* ray_sid0, int32_t* row_of_pos,
+                               int32_t* slice_len, int64_t* slice_off, int64_t* row_info, int64_t* totals,
+                               void* stream) {
     FVR_TRY_BEGIN
     if (pad < 1) return set_error(FVR_ERR_INVALID, "pad must be positive");
     cudaStream_t st = (cudaStream_t)stream;
     cudaMemsetAsync(totals, 0, 3 * sizeof(int64_t), st);
     cudaMemsetAsync(slice_off, 0, sizeof(int64_t), st);
     auto* tot = reinterpret_cast<unsigned long long*>(totals);
-    if (ray_samples && n_rays > 0) sum_kernel<<<grid_for(n_rays, 256), 256, 0, st>>>(ray_samples, n_rays, tot + 2);
+    if (ray_samples && n_rays > 0) {
+        sum_kernel<<<grid_for(n_rays, 256), 256, 0, st>>>(ray_samples, n_rays, tot + 2);
+        if (ray_sid0) {  // exclusive scan of the rays' sample slots
+            shift_to_i64_kernel<<<grid_for(n_rays - 1, 256), 256, 0, st>>>(ray_samples, n_rays - 1, ray_sid0);
+            if (n_rays > 1) {
+                Scratch sc(st);
+                size_t tmp = 0;
+                cub::DeviceScan::InclusiveSum(nullptr, tmp, ray_sid0 + 1, ray_sid0 + 1, (int)(n_rays - 1), st);
+                void* t = sc.get<uint8_t>(tmp);
+                cub::DeviceScan::InclusiveSum(t, tmp, ray_sid0 + 1, ray_sid0 + 1, (int)(n_rays - 1), st);
+            }
+        }
+    }
     if (n_rows <= 0) return check_launch("sell_layout");
     if (int rc = fvr_sell_window_order(counts, n_rows, window, row_of_pos, stream)) return rc;
     const int64_t n_slices = (n_rows + 31) / 32;
@@ -257,6 +301,60 @@ extern "C" int fvr_rplan_layout(const int32_t* row_len, int32_t n_views, int32_t
                                                                              buckets, sb, tot, keys, vals);
     cub::DeviceRadixSort::SortPairs(t, tmp_sort, keys, keys2, vals, unit_order, (int)n_units, 0, end_bit, st);
     return check_launch("rplan_layout");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_count_nonzero_u8(const uint8_t* v, int64_t n, int64_t* count, void* stream) {
+    FVR_TRY_BEGIN
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(count, 0, sizeof(int64_t), st);
+    if (n > 0) count_u8_kernel<<<grid_for(n, 256), 256, 0, st>>>(v, n, reinterpret_cast<unsigned long long*>(count));
+    return check_launch("count_nonzero_u8");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_select_nonzero_u8(const uint8_t* v, int64_t n, int64_t capacity, int32_t* out, int64_t* n_sel,
+                                     void* stream) {
+    FVR_TRY_BEGIN
+    if (n >= (1ll << 31)) return set_error(FVR_ERR_INVALID, "at most 2^31 - 1 elements");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(n_sel, 0, sizeof(int64_t), st);
+    if (n <= 0 || capacity <= 0) return check_launch("select_nonzero_u8");
+    Scratch sc(st);
+    int32_t* sel = capacity >= n ? out : sc.get<int32_t>(n);
+    cub::CountingInputIterator<int32_t> idx(0);
+    size_t tmp = 0;
+    cub::DeviceSelect::Flagged(nullptr, tmp, idx, v, sel, n_sel, (int)n, st);
+    void* t = sc.get<uint8_t>(tmp);
+    cub::DeviceSelect::Flagged(t, tmp, idx, v, sel, n_sel, (int)n, st);
+    if (sel != out) cudaMemcpyAsync(out, sel, sizeof(int32_t) * (size_t)capacity, cudaMemcpyDeviceToDevice, st);
+    return check_launch("select_nonzero_u8");
+    FVR_TRY_END
+}
+
+extern "C" int fvr_sample_plan_spatial(int32_t* entries, int64_t n_slots, int32_t e6, const int64_t* block_keys,
+                                       int64_t n_blocks, const int32_t* meta_in, int32_t* meta_out, void* stream) {
+    FVR_TRY_BEGIN
+    if (n_blocks <= 0) return FVR_OK;
+    if (n_blocks >= (1ll << 31)) return set_error(FVR_ERR_INVALID, "at most 2^31 - 1 sample blocks");
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch sc(st);
+    uint32_t* k = sc.get<uint32_t>(n_blocks);
+    uint32_t* k2 = sc.get<uint32_t>(n_blocks);
+    uint32_t* v = sc.get<uint32_t>(n_blocks);
+    uint32_t* v2 = sc.get<uint32_t>(n_blocks);
+    int32_t* inv = sc.get<int32_t>(n_blocks);
+    split_keys_kernel<<<grid_for(n_blocks, 256), 256, 0, st>>>(
+        reinterpret_cast<const unsigned long long*>(block_keys), n_blocks, k, v);
+    // the Morton part holds 30 bits; the radix sort is stable, so ties keep
+    // block order (= sorting the full (Morton << 32 | block) keys)
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, k, k2, v, v2, (int)n_blocks, 0, 30, st);
+    void* t = sc.get<uint8_t>(tmp);
+    cub::DeviceRadixSort::SortPairs(t, tmp, k, k2, v, v2, (int)n_blocks, 0, 30, st);
+    inverse_perm_kernel<<<grid_for(n_blocks, 256), 256, 0, st>>>(v2, n_blocks, inv);
+    if (int rc = fvr_sample_plan_reorder(entries, n_slots, e6, inv, n_blocks, meta_in, meta_out, stream)) return rc;
+    return check_launch("sample_plan_spatial");
     FVR_TRY_END
 }
 

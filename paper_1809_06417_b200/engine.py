@@ -206,6 +206,21 @@ def _morton_enabled() -> bool:
     return os.environ.get("FVR_KP_ORDER", "morton") != "lattice"
 
 
+def _nonzero_u8(mask):
+    """Indices (int32, device) of the nonzero bytes of ``mask``: a native
+    count, one synchronisation for the size, a native select."""
+    t = _lib.torch()
+    flat = mask.reshape(-1)
+    n = int(flat.numel())
+    cnt = t.empty(1, dtype=t.int64, device=flat.device)
+    _lib.call("fvr_count_nonzero_u8", flat.data_ptr(), n, cnt.data_ptr(), _lib.stream_ptr())
+    m = int(cnt.item())
+    out = t.empty(m, dtype=t.int32, device=flat.device)
+    if m:
+        _lib.call("fvr_select_nonzero_u8", flat.data_ptr(), n, m, out.data_ptr(), cnt.data_ptr(), _lib.stream_ptr())
+    return out
+
+
 def _morton_order(kp, shape):
     """The list of lattice indices ``kp`` (int32, device) sorted by Morton
     (x, y, z) code: one key kernel and one radix sort over the code's bits
@@ -356,19 +371,20 @@ class ChannelLoop:
             ray_base = int(per_view[: self.v_begin].sum()) if n_host is not None else \
                 int(sub[: self.v_begin].reshape(-1).count_nonzero().item())
         local_sub = sub[self.v_begin:self.v_end]
-        if n_host is not None and local_sub.is_contiguous() and local_sub.dtype == t.uint8:
-            # count known on the host: one native compaction, no synchronisation
-            ray_list_t = t.empty(n_host, dtype=t.int32, device=dev)
-            n_found = t.empty(1, dtype=t.int64, device=dev)
-            if n_host:
-                _lib.call("fvr_flame_rays", local_sub.data_ptr(), self.v_end - self.v_begin, self.w_bb, self.h_bb,
-                          n_host, ray_list_t.data_ptr(), n_found.data_ptr(), _lib.stream_ptr())
-        else:
-            if n_host is not None:
-                nz = t.nonzero_static(local_sub, size=n_host)
-            else:
-                nz = t.nonzero(local_sub)  # (N, 3): view, row, col -- lexicographic
-            ray_list_t = ((nz[:, 0] << 24) | (nz[:, 1] * self.w_bb + nz[:, 2])).to(t.int32)
+        if local_sub.dtype != t.uint8:
+            local_sub = local_sub.to(t.uint8)
+        local_sub = local_sub.contiguous()
+        if n_host is None:  # device masks: count them (one synchronisation)
+            cnt = t.empty(1, dtype=t.int64, device=dev)
+            _lib.call("fvr_count_nonzero_u8", local_sub.data_ptr(), local_sub.numel(), cnt.data_ptr(),
+                      _lib.stream_ptr())
+            n_host = int(cnt.item())
+        # one native compaction (rows in view, row, col order)
+        ray_list_t = t.empty(n_host, dtype=t.int32, device=dev)
+        n_found = t.empty(1, dtype=t.int64, device=dev)
+        if n_host:
+            _lib.call("fvr_flame_rays", local_sub.data_ptr(), self.v_end - self.v_begin, self.w_bb, self.h_bb,
+                      n_host, ray_list_t.data_ptr(), n_found.data_ptr(), _lib.stream_ptr())
         self.n_rays = int(ray_list_t.numel())
         self.rays = ray_list_t if self.n_rays else t.zeros(1, dtype=t.int32, device=dev)
         self.ray_base = ray_base
@@ -387,7 +403,7 @@ class ChannelLoop:
         side.wait_event(kp_ready)  # (the key-point list does not wait for the occupancy)
         if self.kp is None:
             with t.cuda.stream(side):
-                kp_t = t.nonzero(kp_dev.reshape(-1)).reshape(-1).to(t.int32)  # synchronises the side stream
+                kp_t = _nonzero_u8(kp_dev)  # synchronises the side stream
                 if _morton_enabled():  # only the key-point list is ordered (no lattice-sized permutation)
                     kp_t = _morton_order(kp_t, shape)
             self.n_kp = int(kp_t.numel())
@@ -828,11 +844,12 @@ class ChannelLoop:
             slice_off = t.empty(n_slices + 1, dtype=t.int64, device=dev)
             row_info = t.empty(self.n_kp, dtype=t.int64, device=dev)
             totals = t.empty(3, dtype=t.int64, device=dev)
+            sid0 = t.empty(self.n_rays, dtype=t.int64, device=dev) if ray_samples is not None else None
             _lib.call("fvr_sell_layout", counts.data_ptr(), self.n_kp, sigma, pad, _lib.ptr(ray_samples), self.n_rays,
-                      row_of_pos.data_ptr(), slice_len.data_ptr(), slice_off.data_ptr(), row_info.data_ptr(),
-                      totals.data_ptr(), stream)
-            return dict(geo=geo, kp_map=kp_map, ray_samples=ray_samples, row_of_pos=row_of_pos, slice_len=slice_len,
-                        slice_off=slice_off, row_info=row_info, sizes=totals)
+                      _lib.ptr(sid0), row_of_pos.data_ptr(), slice_len.data_ptr(), slice_off.data_ptr(),
+                      row_info.data_ptr(), totals.data_ptr(), stream)
+            return dict(geo=geo, kp_map=kp_map, ray_samples=ray_samples, sid0=sid0, row_of_pos=row_of_pos,
+                        slice_len=slice_len, slice_off=slice_off, row_info=row_info, sizes=totals)
         if os.environ.get("FVR_SELL_SORT", "0") == "1":
             order = t.argsort(counts, descending=True)
         elif 2 <= sigma <= 1024 and sigma & (sigma - 1) == 0:  # one kernel: bitonic per window
@@ -887,7 +904,6 @@ class ChannelLoop:
                 entries = t.zeros(max(slots, 2), dtype=t.int32, device=dev)
                 entries_b = t.zeros(max(slots // 2, 1), dtype=t.int32, device=dev)
             if self.sample_plan:
-                sid0 = t.zeros(self.n_rays, dtype=t.int64, device=dev)
                 meta = t.empty(max(n_samples // 2, 2), dtype=t.int32, device=dev)  # int2 per 4-slot block
                 rho = t.zeros((max(n_samples, 1), self.pitch), dtype=t.float32, device=dev)
         except t.cuda.OutOfMemoryError:
@@ -896,7 +912,10 @@ class ChannelLoop:
         keep += [pc, cursor]
         stream = stream.cuda_stream
         if self.sample_plan:
-            sid0[1:] = t.cumsum(pc["ray_samples"][:-1].long(), 0)
+            sid0 = pc.get("sid0")
+            if sid0 is None:  # (the non-native SELL layout variants)
+                sid0 = t.zeros(self.n_rays, dtype=t.int64, device=dev)
+                sid0[1:] = t.cumsum(pc["ray_samples"][:-1].long(), 0)
             self.rho = rho
             keep.append(sid0)
             n_blocks = n_samples // 4
@@ -908,12 +927,9 @@ class ChannelLoop:
                       pc["kp_map"].data_ptr(), sid0.data_ptr(), *sell, _lib.ptr(entries_b), meta.data_ptr(),
                       _lib.ptr(keys), stream)
             if spatial:
-                order = t.sort(keys).indices
-                new_of_nat = t.empty(n_blocks, dtype=t.int32, device=dev)
-                new_of_nat[order] = t.arange(n_blocks, dtype=t.int32, device=dev)
                 meta_new = t.empty_like(meta)
-                _lib.call("fvr_sample_plan_reorder", entries.data_ptr(), slots, int(entries_b is not None),
-                          new_of_nat.data_ptr(), n_blocks, meta.data_ptr(), meta_new.data_ptr(), stream)
+                _lib.call("fvr_sample_plan_spatial", entries.data_ptr(), slots, int(entries_b is not None),
+                          keys.data_ptr(), n_blocks, meta.data_ptr(), meta_new.data_ptr(), stream)
                 meta = meta_new
             self.sample_meta = meta
             self.n_samples = n_samples

@@ -115,9 +115,11 @@ def test_sell_layout_matches_restatement(cuda_device):
         slice_off = torch.empty(ns + 1, dtype=torch.int64, device=cuda_device)
         row_info = torch.empty(n, dtype=torch.int64, device=cuda_device)
         totals = torch.empty(3, dtype=torch.int64, device=cuda_device)
-        _lib.call("fvr_sell_layout", d.data_ptr(), n, window, pad, rs.data_ptr(), rs.numel(), row_of_pos.data_ptr(),
-                  slice_len.data_ptr(), slice_off.data_ptr(), row_info.data_ptr(), totals.data_ptr(),
-                  _lib.stream_ptr())
+        sid0 = torch.empty(rs.numel(), dtype=torch.int64, device=cuda_device)
+        _lib.call("fvr_sell_layout", d.data_ptr(), n, window, pad, rs.data_ptr(), rs.numel(), sid0.data_ptr(),
+                  row_of_pos.data_ptr(), slice_len.data_ptr(), slice_off.data_ptr(), row_info.data_ptr(),
+                  totals.data_ptr(), _lib.stream_ptr())
+        assert np.array_equal(sid0.cpu().numpy(), np.concatenate([[0], np.cumsum(ray_samples)[:-1]]))
         pos = np.arange(n)
         order = np.lexsort((pos, -counts.astype(np.int64), pos // window))
         assert np.array_equal(row_of_pos.cpu().numpy(), order)
@@ -188,6 +190,16 @@ def test_flame_rays_kp_map_morton_order(cuda_device):
     v, r, c = np.nonzero(crops)
     assert int(cnt.item()) == n
     assert np.array_equal(rays.cpu().numpy(), (v << 24) | (r * 131 + c))
+    # count + select of nonzero bytes (the hull key-point list)
+    flat = torch.from_numpy((rng.random(300_007) < 0.1).astype(np.uint8) * 7).to(cuda_device)
+    c = torch.empty(1, dtype=torch.int64, device=cuda_device)
+    _lib.call("fvr_count_nonzero_u8", flat.data_ptr(), flat.numel(), c.data_ptr(), _lib.stream_ptr())
+    want_idx = np.flatnonzero(flat.cpu().numpy())
+    assert int(c.item()) == want_idx.size
+    sel = torch.empty(want_idx.size, dtype=torch.int32, device=cuda_device)
+    _lib.call("fvr_select_nonzero_u8", flat.data_ptr(), flat.numel(), want_idx.size, sel.data_ptr(), c.data_ptr(),
+              _lib.stream_ptr())
+    assert np.array_equal(sel.cpu().numpy(), want_idx)
     # key-point map: position in the list, -1 elsewhere
     shape = (33, 40, 17)
     n_vox = int(np.prod(shape))
