@@ -309,10 +309,14 @@ def run_gpu(args):
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         launches = 0
+        # (NVTX range "timed": the launch list of exactly this region is
+        # `ncu --nvtx --nvtx-include "timed/" ...`)
+        torch.cuda.nvtx.range_push("timed")
         e0.record()
         for _ in range(steps):
             launches += one_step()
         e1.record()
+        torch.cuda.nvtx.range_pop()
         barrier()
         timed_ms = e0.elapsed_time(e1)
         all_evs = []
