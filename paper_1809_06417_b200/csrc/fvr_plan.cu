@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6, PIPE, NCH)) gather_ke
             // software-pipelined: the next batch's chunks are loaded before
             // this batch's residual reads, so the plan stream keeps flowing
             // while the warp waits on L1/L2
-            constexpr int D = FVR_GATHER_PIPE;  // entries per batch (a multiple of 8)
+            constexpr int D = FVR_GATHER_PIPE > 0 ? FVR_GATHER_PIPE : 8;  // entries per batch (a multiple of 8)
             static_assert(D % 8 == 0, "batches of whole 16-byte chunks");
             const uint4 z = make_uint4(0u, 0u, 0u, 0u);
             uint4 ca[D / 4], cb[D / 8], na[D / 4], nb[D / 8];
@@ -762,7 +762,7 @@ extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_of
     e = launch_pdl(gather_kernel<P, C, E, Q>, (unsigned)blocks, 256, st, slice_len, so, row_of_pos, en, entries_b,  \
                    n_kp, residual, kp_index, values, plane, layout, layout_kind, sy, ny1, kp_values, pk, state)
 #define FVR_GATHER_E(P, C)                                 \
-    if (entries_b && !sample_plan) FVR_GATHER(P, C, true, true); \
+    if (entries_b && !sample_plan && FVR_GATHER_PIPE > 0) FVR_GATHER(P, C, true, true); \
     else if (entries_b) FVR_GATHER(P, C, true, false);           \
     else FVR_GATHER(P, C, false, false)
     if (packed) {
