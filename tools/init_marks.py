@@ -11,7 +11,7 @@ from paper_1809_06417_b200 import engine  # noqa: E402
 
 sc = bench.make_scene()
 cfg = ReconstructionConfig(alpha_l=bench.ALPHA_L, alpha_d=1.0, tau=bench.TAU, max_iters=50,
-                           converge_eps=1e-12, deterministic_mode=True)
+                           converge_eps=1e-12, deterministic_mode=os.environ.get("E2E_STOCHASTIC") != "1", g_sigma=0.1, rng_seed=0)
 loops = []
 orig = engine.ChannelLoop.__init__
 
