@@ -480,6 +480,9 @@ int fvr_rplan_layout(const int32_t* row_len, int32_t n_views, int32_t bbox_w, in
 int fvr_count_nonzero_u8(const uint8_t* v, int64_t n, int64_t* count, void* stream);
 int fvr_select_nonzero_u8(const uint8_t* v, int64_t n, int64_t capacity, int32_t* out, int64_t* n_sel,
                           void* stream);
+/* Host-side concatenation of n buffers into dst (page-locked staging for one
+ * H2D copy), all host threads (OpenMP). */
+int fvr_copy_host_parallel(const void* const* srcs, const int64_t* nbytes, int32_t n, void* dst);
 /* Flame rays of the bbox crops (u8, n_views x bbox_h x bbox_w, row-major):
  * rays[i] = view << 24 | (row * bbox_w + col) of the i-th nonzero pixel in
  * that order (reconstruct.py:144-149), at most `capacity` of them;

@@ -184,6 +184,7 @@ _SIGNATURES = {
     "fvr_sell_layout": (c_int, [_P, c_int64, c_int32, c_int32, _P, c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "fvr_sample_plan_spatial": (c_int, [_P, c_int64, c_int32, _P, c_int64, _P, _P, _P]),
     "fvr_count_nonzero_u8": (c_int, [_P, c_int64, _P, _P]),
+    "fvr_copy_host_parallel": (c_int, [_P, _P, c_int32, _P]),
     "fvr_select_nonzero_u8": (c_int, [_P, c_int64, c_int64, _P, _P, _P]),
     "fvr_rplan_layout": (c_int, [_P, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, _P, _P, _P, _P,
                                  _P, _P]),
@@ -318,6 +319,37 @@ def camera_struct(cam) -> FvrCamera:
         c.center[a] = float(ctr[a])
     c.width, c.height = int(cam.width), int(cam.height)
     return c
+
+
+def to_host(tensor):
+    """D2H of a device tensor through page-locked memory (torch's caching host
+    allocator): several times a pageable .cpu() for the tens-of-MB lattices
+    of the larger configs.  Returns a numpy array viewing the pinned buffer."""
+    t = torch()
+    host = t.empty(tuple(tensor.shape), dtype=tensor.dtype, pin_memory=True)
+    host.copy_(tensor, non_blocking=True)
+    t.cuda.current_stream().synchronize()
+    return host.numpy()
+
+
+def upload_host(arrays, dtype, shape, dev):
+    """Host arrays concatenated (fvr_copy_host_parallel, all host threads) into
+    page-locked staging, then one asynchronous H2D into a new device tensor of
+    ``shape``."""
+    import numpy as np
+
+    t = torch()
+    arrs = [np.ascontiguousarray(a) for a in arrays]
+    nbytes = [a.nbytes for a in arrs]
+    total = sum(nbytes)
+    stage = t.empty(total, dtype=t.uint8, pin_memory=True)
+    n = len(arrs)
+    srcs = (ctypes.c_void_p * n)(*[a.ctypes.data for a in arrs])
+    sizes = (ctypes.c_int64 * n)(*nbytes)
+    call("fvr_copy_host_parallel", ctypes.addressof(srcs), ctypes.addressof(sizes), n, stage.data_ptr())
+    out = t.empty(total, dtype=t.uint8, device=dev)
+    out.copy_(stage, non_blocking=True)  # (the caching host allocator keeps stage until the copy is done)
+    return out.view(dtype).view(shape)
 
 
 def cameras_tensor(cameras, dev):

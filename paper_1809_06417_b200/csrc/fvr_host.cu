@@ -13,7 +13,9 @@
 //            compaction of the flame rays needs no synchronisation).
 #include <omp.h>
 
+#include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "fvr_internal.cuh"
 
@@ -56,6 +58,31 @@ extern "C" int fvr_stage_inputs_host(const uint32_t* tags, int64_t n_vox, uint32
             for (int64_t i = 0; i < pix; ++i) n += m[i];
             counts_out[v] = n;
         }
+    }
+    return FVR_OK;
+    FVR_TRY_END
+}
+
+// n host buffers concatenated into dst (a page-locked staging buffer) by all
+// host threads: big buffers are split into 1 MiB pieces so every thread has
+// work (one 12 MB frame per thread would leave most of them idle).
+extern "C" int fvr_copy_host_parallel(const void* const* srcs, const int64_t* nbytes, int32_t n, void* dst) {
+    FVR_TRY_BEGIN
+    if (n < 0) return set_error(FVR_ERR_INVALID, "bad buffer count");
+    constexpr int64_t kPiece = 1 << 20;
+    std::vector<int64_t> first(n + 1, 0), off(n + 1, 0);
+    for (int i = 0; i < n; ++i) {
+        if (nbytes[i] < 0) return set_error(FVR_ERR_INVALID, "negative size");
+        first[i + 1] = first[i] + (nbytes[i] + kPiece - 1) / kPiece;
+        off[i + 1] = off[i] + nbytes[i];
+    }
+    const int64_t pieces = first[n];
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t q = 0; q < pieces; ++q) {
+        int i = 0;
+        while (first[i + 1] <= q) ++i;
+        const int64_t s = (q - first[i]) * kPiece, len = std::min(kPiece, nbytes[i] - s);
+        std::memcpy(static_cast<char*>(dst) + off[i] + s, static_cast<const char*>(srcs[i]) + s, (size_t)len);
     }
     return FVR_OK;
     FVR_TRY_END
