@@ -155,16 +155,54 @@ __device__ __forceinline__ void store_zero_chunk(uint32_t* p) {
 #endif
 }
 
-// The fill's output for one row: entry t goes straight to its lane chunk
-// (a word and 16-bit weight word; staging whole chunks in shared memory cost
-// more instructions than the scattered stores, 1.83 vs 1.62 ms at config 2).
+// The fill's output for one row: entry t goes to its lane chunk (a word and
+// 16-bit weight word) -- staged in registers and stored 32 bytes at a time
+// (FVR_RPLAN_FILL_BUF); staging whole chunks in shared memory cost more
+// instructions than the scattered stores (1.83 vs 1.62 ms at config 2).
 // finish() pads the row with (0, 0.0) entries up to the unit's length --
 // whole chunks with 32-byte stores -- so the plan buffers need no clearing.
+// 6-byte fill output staged per lane chunk in registers (one 32-byte store
+// per full chunk): config 2 render fill 1.42 -> 1.22 ms at 4 CTAs per SM
+// (128 registers; 1.30 ms at 5 CTAs with spills)
+#ifndef FVR_RPLAN_FILL_BUF
+#define FVR_RPLAN_FILL_BUF 1
+#endif
+__device__ __forceinline__ void store_chunk(uint32_t* p, const uint32_t (&v)[8]) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]),
+                 "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
 template <bool WIDE>
 struct RplanOut {
     uint32_t* a;         // this row's first a word
     void* b;             // this row's first weight word (u16; u32 when WIDE)
-    __device__ __forceinline__ void put(int t, int col, float w) const {
+#if FVR_RPLAN_FILL_BUF
+    // (6-byte entries) the current lane chunks in registers, written as one
+    // 32-byte store each when full: a warp's scattered 4- and 2-byte stores
+    // touched 32 sectors per instruction
+    uint32_t ab[8], bb[8];
+    __device__ __forceinline__ void shift_in(uint32_t aw, uint32_t h) {
+#pragma unroll
+        for (int i = 0; i < 7; ++i) ab[i] = ab[i + 1];
+        ab[7] = aw;
+#pragma unroll
+        for (int i = 0; i < 7; ++i) bb[i] = __funnelshift_r(bb[i], bb[i + 1], 16);
+        bb[7] = (bb[7] >> 16) | (h << 16);
+    }
+#endif
+    __device__ __forceinline__ void put(int t, int col, float w) {
+#if FVR_RPLAN_FILL_BUF
+        if (!WIDE) {
+            FVR_DCHECK(col >= 0 && col < (1 << 24), "render plan: column not a hull key point");
+            const uint32_t bits = (__float_as_uint(w) + 0x40u) >> 7;  // round to 16 mantissa bits
+            shift_in((uint32_t)col | ((bits >> 16) << 24), bits & 0xFFFFu);
+            if ((t & (kRpA - 1)) == kRpA - 1) store_chunk(a + (int64_t)(t / kRpA) * (32 * kRpA), ab);
+            if ((t & (kRpB - 1)) == kRpB - 1)
+                store_chunk(static_cast<uint32_t*>(b) + (int64_t)(t / kRpB) * (32 * kRpA), bb);
+            return;
+        }
+#endif
         if (WIDE) {  // 8-byte entries: u32 column, f32 weight (hulls of >= 2^24 key points)
             a[(int64_t)(t / kRpA) * (32 * kRpA) + (t % kRpA)] = (uint32_t)col;
             static_cast<uint32_t*>(b)[(int64_t)(t / kRpA) * (32 * kRpA) + (t % kRpA)] = __float_as_uint(w);
@@ -176,10 +214,24 @@ struct RplanOut {
         static_cast<uint16_t*>(b)[(int64_t)(t / kRpB) * (32 * kRpB) + (t % kRpB)] = (uint16_t)(bits & 0xFFFFu);
     }
     // entries count..len-1 are padding (len: the unit's length, a multiple of kRpB)
-    __device__ __forceinline__ void finish(int count, int len) const {
+    __device__ __forceinline__ void finish(int count, int len) {
         FVR_DCHECK(count <= len, "render plan: row longer than its unit (count pass disagrees with fill)");
         constexpr int kB = WIDE ? kRpA : kRpB;  // weight words per chunk
         const int ca = (count + kRpA - 1) / kRpA * kRpA, cb = (count + kB - 1) / kB * kB;
+#if FVR_RPLAN_FILL_BUF
+        if (!WIDE) {  // pad the partial chunks in registers with (0, 0.0) and store them
+            for (int t = count; t < cb; ++t) {
+                shift_in(0u, 0u);
+                if ((t & (kRpA - 1)) == kRpA - 1) store_chunk(a + (int64_t)(t / kRpA) * (32 * kRpA), ab);
+                if ((t & (kRpB - 1)) == kRpB - 1)
+                    store_chunk(static_cast<uint32_t*>(b) + (int64_t)(t / kRpB) * (32 * kRpA), bb);
+            }
+            for (int c = cb / kRpA; c < len / kRpA; ++c) store_zero_chunk(a + (int64_t)c * (32 * kRpA));
+            for (int c = cb / kRpB; c < len / kRpB; ++c)
+                store_zero_chunk(static_cast<uint32_t*>(b) + (int64_t)c * (32 * kRpA));
+            return;
+        }
+#endif
         for (int t = count; t < ca; ++t) a[(int64_t)(t / kRpA) * (32 * kRpA) + (t % kRpA)] = 0u;
         for (int t = count; t < cb; ++t) {
             if (WIDE)
@@ -215,7 +267,7 @@ __device__ int rplan_row(const double o[3], const double d[3], const Geom& g, co
                          const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
                          const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch,
                          int64_t plane, const float* __restrict__ thr, const uint32_t* __restrict__ nm,
-                         float* __restrict__ acc, float* __restrict__ wsm, int stride, RplanOut<WIDE> out,
+                         float* __restrict__ acc, float* __restrict__ wsm, int stride, RplanOut<WIDE>& out,
                          double* base, double& t_fin, const uint8_t* __restrict__ slot_tab = nullptr,
                          const int* __restrict__ kp_map = nullptr, int* __restrict__ skp = nullptr,
                          const uint32_t* __restrict__ pos27 = nullptr, const int* __restrict__ off27 = nullptr) {
@@ -483,8 +535,9 @@ __global__ void __launch_bounds__(128) rplan_count_kernel(
         const fvr_camera_t& cam = cams[view];
         double d[3], base[1] = {0.0}, t_fin;
         pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, d);
+        RplanOut<false> none{};
         cnt = rplan_row<SCAT, false>(cam.center, d, g, rc, occ, dynamic, dyn27, nullptr, 0, 0, s_thr, s_nm, nullptr,
-                                     nullptr, 0, RplanOut<false>{}, base, t_fin);
+                                     nullptr, 0, none, base, t_fin);
     }
     if (row_len) row_len[(int64_t)unit * 32 + lane] = cnt;
     cnt = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
@@ -493,13 +546,17 @@ __global__ void __launch_bounds__(128) rplan_count_kernel(
 
 // Fill pass: rows in SELL-32 order; base[c * rows + r] and t_fin[r] per row
 // r = unit * 32 + lane (entries beyond a row's length stay (0, 0.0)).
-// 5 CTAs per SM (96 registers, no spills): config 2 fill 1.44 ms, against
-// 2.10 at the compiler's 122 registers (4 CTAs) and 1.48 at 6 (spills)
+// Unbuffered stores: 5 CTAs per SM (96 registers, no spills): config 2 fill
+// 1.44 ms, against 2.10 at the compiler's 122 registers (4 CTAs) and 1.48 at
+// 6 (spills).  Register-staged chunks (FVR_RPLAN_FILL_BUF): 4 CTAs, 1.22 ms.
 #ifndef FVR_RPLAN_FILL_MINB
-#define FVR_RPLAN_FILL_MINB 5
+#define FVR_RPLAN_FILL_MINB (FVR_RPLAN_FILL_BUF ? 4 : 5)
+#endif
+#ifndef FVR_RPLAN_FILL_WIDE_MINB
+#define FVR_RPLAN_FILL_WIDE_MINB 5
 #endif
 template <bool SCAT, bool WIDE>
-__global__ void __launch_bounds__(128, FVR_RPLAN_FILL_MINB) rplan_fill_kernel(
+__global__ void __launch_bounds__(128, WIDE ? FVR_RPLAN_FILL_WIDE_MINB : FVR_RPLAN_FILL_MINB) rplan_fill_kernel(
     const fvr_camera_t* __restrict__ cams, int u0, int v0, int w, int h, int units_x, int units_per_view,
     int n_units, Geom g, RenderConsts rc, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ dynamic,
     const uint32_t* __restrict__ dyn27, const float* __restrict__ values, int nch, int64_t plane,
