@@ -475,8 +475,9 @@ int fvr_rplan_layout(const int32_t* row_len, int32_t n_views, int32_t bbox_w, in
                      int32_t tile_units_y, int32_t align, int32_t buckets, int32_t* row_src, int32_t* unit_len,
                      int64_t* unit_off, int32_t* unit_order, int64_t* totals, void* stream);
 /* Nonzero bytes of v (n of them): *count (device) = how many; the select
- * writes their indices in order (at most `capacity`; *n_sel = the number
- * found) -- the hull key-point list from fvr_hull_keypoints' mask. */
+ * writes their indices in order (*n_sel = the number found) into out, which
+ * must hold them all: capacity >= the count (fvr_count_nonzero_u8's) -- the
+ * hull key-point list from fvr_hull_keypoints' mask. */
 int fvr_count_nonzero_u8(const uint8_t* v, int64_t n, int64_t* count, void* stream);
 int fvr_select_nonzero_u8(const uint8_t* v, int64_t n, int64_t capacity, int32_t* out, int64_t* n_sel,
                           void* stream);
@@ -485,8 +486,8 @@ int fvr_select_nonzero_u8(const uint8_t* v, int64_t n, int64_t capacity, int32_t
 int fvr_copy_host_parallel(const void* const* srcs, const int64_t* nbytes, int32_t n, void* dst);
 /* Flame rays of the bbox crops (u8, n_views x bbox_h x bbox_w, row-major):
  * rays[i] = view << 24 | (row * bbox_w + col) of the i-th nonzero pixel in
- * that order (reconstruct.py:144-149), at most `capacity` of them;
- * *n_rays (device) = the number found. */
+ * that order (reconstruct.py:144-149); capacity must be >= their number
+ * (the host's flame count); *n_rays (device) = the number found. */
 int fvr_flame_rays(const uint8_t* crops, int32_t n_views, int32_t bbox_w, int32_t bbox_h, int64_t capacity,
                    int32_t* rays, int64_t* n_rays, void* stream);
 

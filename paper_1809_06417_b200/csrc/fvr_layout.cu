@@ -321,13 +321,11 @@ extern "C" int fvr_select_nonzero_u8(const uint8_t* v, int64_t n, int64_t capaci
     cudaMemsetAsync(n_sel, 0, sizeof(int64_t), st);
     if (n <= 0 || capacity <= 0) return check_launch("select_nonzero_u8");
     Scratch sc(st);
-    int32_t* sel = capacity >= n ? out : sc.get<int32_t>(n);
     cub::CountingInputIterator<int32_t> idx(0);
     size_t tmp = 0;
-    cub::DeviceSelect::Flagged(nullptr, tmp, idx, v, sel, n_sel, (int)n, st);
+    cub::DeviceSelect::Flagged(nullptr, tmp, idx, v, out, n_sel, (int)n, st);
     void* t = sc.get<uint8_t>(tmp);
-    cub::DeviceSelect::Flagged(t, tmp, idx, v, sel, n_sel, (int)n, st);
-    if (sel != out) cudaMemcpyAsync(out, sel, sizeof(int32_t) * (size_t)capacity, cudaMemcpyDeviceToDevice, st);
+    cub::DeviceSelect::Flagged(t, tmp, idx, v, out, n_sel, (int)n, st);
     return check_launch("select_nonzero_u8");
     FVR_TRY_END
 }
@@ -369,15 +367,13 @@ extern "C" int fvr_flame_rays(const uint8_t* crops, int32_t n_views, int32_t bbo
     cudaMemsetAsync(n_rays, 0, sizeof(int64_t), st);
     if (n == 0 || capacity <= 0) return check_launch("flame_rays");
     Scratch sc(st);
-    // selected indices go to a scratch of the full crop size (the capacity
-    // is the caller's count, which the selection may not exceed)
-    int32_t* sel = capacity >= n ? rays : sc.get<int32_t>(n);
+    // (the selection writes exactly the flagged count, which the caller's
+    // capacity covers: no full-size scratch)
     cub::CountingInputIterator<int32_t> idx(0);
     size_t tmp = 0;
-    cub::DeviceSelect::Flagged(nullptr, tmp, idx, crops, sel, n_rays, (int)n, st);
+    cub::DeviceSelect::Flagged(nullptr, tmp, idx, crops, rays, n_rays, (int)n, st);
     void* t = sc.get<uint8_t>(tmp);
-    cub::DeviceSelect::Flagged(t, tmp, idx, crops, sel, n_rays, (int)n, st);
-    if (sel != rays) cudaMemcpyAsync(rays, sel, sizeof(int32_t) * (size_t)capacity, cudaMemcpyDeviceToDevice, st);
+    cub::DeviceSelect::Flagged(t, tmp, idx, crops, rays, n_rays, (int)n, st);
     flame_ray_kernel<<<grid_for(capacity, 256), 256, 0, st>>>(rays, n_rays, capacity, (int)pix);
     return check_launch("flame_rays");
     FVR_TRY_END
