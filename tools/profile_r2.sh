@@ -20,6 +20,10 @@ ncu --set full --import-source on --clock-control none -k regex:"weighted_residu
     -o $O/prof_sto python bench.py --steps 3 --warmup 3 --e2e-iters 0 --no-cpu-baseline --stochastic-steps 3 \
     > $O/ncu_sto.log 2>&1
 ncu --set full --import-source on --clock-control none \
-    -k regex:"rplan_fill_kernel|plan_fill_kernel|rplan_count_kernel|plan_count_kernel|dist_lines" -c 8 \
-    -o $O/prof_setup python tools/profile_setup.py > $O/ncu_setup.log 2>&1
+    -k regex:"rplan_fill_kernel|plan_fill_kernel|rplan_count_kernel|plan_count_kernel" -c 4 \
+    -o $O/prof_fill python tools/profile_setup.py > $O/ncu_fill.log 2>&1
+ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
+    -k regex:"weighted_residual|gather_kernel<0, 1, 1, 0>" -c 2 \
+    -o $O/prof_sto2 python bench.py --steps 3 --warmup 3 --e2e-iters 0 --no-cpu-baseline --stochastic-steps 3 \
+    > $O/ncu_sto2.log 2>&1
 ls -la $O
