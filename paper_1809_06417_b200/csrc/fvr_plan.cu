@@ -506,7 +506,14 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
     ((PIPE) ? ((NCH) == 1 ? FVR_GATHER_PIPE_MINB : 4)                                          \
             : (NCH) > 1 ? FVR_GATHER3_MINB(E6) : (E6) ? FVR_GATHER_E6_MINB : 3)
 template <bool PACKED, int NCH, bool E6, bool PIPE>
-__global__ void __launch_bounds__(256, FVR_GATHER_MINB(E6, PIPE, NCH)) gather_kernel(
+// CTA size: 128 threads (4 slices) at the same warps per SM as 256-thread
+// CTAs (the MINB counts above are per 256 threads): config 2 K-adjust 0.0490
+// -> 0.0485 ms (512: 0.0563; profiles/r2_ab_gather_cta_size.log)
+#ifndef FVR_GATHER_THREADS
+#define FVR_GATHER_THREADS 128
+#endif
+__global__ void __launch_bounds__(FVR_GATHER_THREADS, FVR_GATHER_MINB(E6, PIPE, NCH) * 256 / FVR_GATHER_THREADS)
+gather_kernel(
     const int32_t* __restrict__ slice_len, const long long* __restrict__ slice_off,
     const int32_t* __restrict__ row_of_pos, const int2* __restrict__ entries, const uint32_t* __restrict__ ent_b,
     int64_t n_rows,
@@ -749,7 +756,7 @@ extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_of
     if (n_kp == 0) return FVR_OK;
     if (n_channels != 1 && n_channels != 3) return set_error(FVR_ERR_INVALID, "the loop gathers 1 or 3 channels");
     const int64_t n_slices = (n_kp + 31) / 32;
-    int64_t blocks = (n_slices * 32 + 255) / 256;
+    int64_t blocks = (n_slices * 32 + FVR_GATHER_THREADS - 1) / FVR_GATHER_THREADS;
     if (blocks > 148 * 24) blocks = 148 * 24;
     const int sy = grid.nz + 1, ny1 = grid.ny + 1;
     const int64_t plane = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);
@@ -759,7 +766,7 @@ extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_of
     long long* pk = reinterpret_cast<long long*>(packed);
     cudaError_t e = cudaSuccess;
 #define FVR_GATHER(P, C, E, Q)                                                                                \
-    e = launch_pdl(gather_kernel<P, C, E, Q>, (unsigned)blocks, 256, st, slice_len, so, row_of_pos, en, entries_b,  \
+    e = launch_pdl(gather_kernel<P, C, E, Q>, (unsigned)blocks, FVR_GATHER_THREADS, st, slice_len, so, row_of_pos, en, entries_b,  \
                    n_kp, residual, kp_index, values, plane, layout, layout_kind, sy, ny1, kp_values, pk, state)
 #define FVR_GATHER_E(P, C)                                 \
     if (entries_b && !sample_plan && FVR_GATHER_PIPE > 0) FVR_GATHER(P, C, true, true); \
