@@ -1283,13 +1283,13 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
     RenderConsts rc = make_render_consts(p, background, n_channels);
     const int units_x = (bbox_w + kUnitW - 1) / kUnitW, upv = fvr_loop_blocks_per_view(bbox_w, bbox_h);
     const int n_units = upv * n_views;
-    int64_t blocks = ((int64_t)n_units * 32 + 255) / 256;
+    int64_t blocks = ((int64_t)n_units * 32 + FVR_RPLAN_THREADS - 1) / FVR_RPLAN_THREADS;
     if (blocks > 148 * 64) blocks = 148 * 64;
     cudaStream_t st = (cudaStream_t)stream;
     const auto* uo = reinterpret_cast<const long long*>(unit_off);
     cudaError_t e;
 #define FVR_RPLAN_RENDER(C, W)                                                                                       \
-    e = launch_pdl(rplan_render_kernel<C, W>, (unsigned)blocks, 256, st, unit_len, uo, entries_a, entries_b, base,    \
+    e = launch_pdl(rplan_render_kernel<C, W>, (unsigned)blocks, FVR_RPLAN_THREADS, st, unit_len, uo, entries_a, entries_b, base,    \
                    t_fin, unit_order, row_src, n_units, units_x, upv, n_views, bbox_w, bbox_h, src, kp_values, rc,    \
                    residual, sq_partials, sq_stride, state, fin)
     if (n_channels == 1 && !wide) FVR_RPLAN_RENDER(1, false);

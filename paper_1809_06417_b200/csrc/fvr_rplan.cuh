@@ -782,7 +782,13 @@ __device__ __forceinline__ void rplan_render_unit(
 }
 
 template <int NCH, bool WIDE>
-__global__ void __launch_bounds__(256, NCH == 1 ? FVR_RPLAN_MINB : 2) rplan_render_kernel(
+// CTA size (MINB counts are per 256 threads): 256 is the measured best
+// (128 / 512: 0.0918 / 0.1018 ms against 0.0894; r2_ab_render_cta_size.log)
+#ifndef FVR_RPLAN_THREADS
+#define FVR_RPLAN_THREADS 256
+#endif
+__global__ void __launch_bounds__(FVR_RPLAN_THREADS, (NCH == 1 ? FVR_RPLAN_MINB : 2) * 256 / FVR_RPLAN_THREADS)
+rplan_render_kernel(
     const int* __restrict__ unit_len, const long long* __restrict__ unit_off, const uint32_t* __restrict__ ent_a,
     const uint32_t* __restrict__ ent_b, const double* __restrict__ base, const double* __restrict__ t_fin,
     const int* __restrict__ unit_order, const int* __restrict__ row_src, int n_units, int units_x,
