@@ -125,6 +125,10 @@ constexpr int kResPitch = NCH == 1 ? 1 : 4;
 // The convergence bookkeeping of one channel (reconstruct.py:311-323), run by
 // one block: per-view RMSE from the kernels' squared-residual partials (warp
 // per view: lane-strided sums, then a fixed shuffle tree), mean over views,
+#ifndef FVR_FINALIZE_UNROLL
+#define FVR_FINALIZE_UNROLL 16  // (config 2 render + finalize 0.0892 -> 0.0887 ms; full unroll: 0.0985)
+#endif
+constexpr int kFinalizeUnroll = FVR_FINALIZE_UNROLL;
 // trace append, optional vol_rmse and the rule.  Fixed order: bit-identical
 // wherever it runs.  s_view: >= n_views doubles of shared memory.
 __device__ __forceinline__ void finalize_block(const double* sq, int n_views, int bpv, double pixels,
@@ -135,7 +139,8 @@ __device__ __forceinline__ void finalize_block(const double* sq, int n_views, in
     const int lane = threadIdx.x & 31;
     for (int v = threadIdx.x >> 5; v < n_views; v += blockDim.x >> 5) {
         double s = 0.0;
-#pragma unroll 4
+        // FVR_FINALIZE_UNROLL loads in flight per lane (the sum keeps its order)
+#pragma unroll kFinalizeUnroll
         for (int b = lane; b < bpv; b += 32) s += __ldcg(sq + (int64_t)v * bpv + b);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
