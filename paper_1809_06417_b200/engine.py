@@ -416,8 +416,7 @@ class ChannelLoop:
             with t.cuda.stream(side):  # the key-point map both plan fills read
                 self._kp_map()
                 self._kpmap.record_stream(main)
-
-        self._mark("flame rays")
+        self._mark("kp map")
         # channels interleaved per pixel (pitch 1, or 4 for three channels)
         self.pitch = 1 if C == 1 else 4
         # K-adjust as a voxel-driven gather over a precomputed plan: the merged
@@ -430,7 +429,7 @@ class ChannelLoop:
         self.n_samples = 0
         self.splan_e6 = False
         self.rho = None
-        self._mark("work buffers")
+        self._mark("plan flags")
         # The plan builds on two streams.  The render plan's count pass was
         # queued on the loop's stream above, so its layout and fill go first
         # there (the fill waits only for the key-point map); the adjust plan's
