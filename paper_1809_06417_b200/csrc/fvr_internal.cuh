@@ -169,58 +169,6 @@ __device__ __forceinline__ void finalize_block(const double* sq, int n_views, in
     __syncthreads();
 }
 
-// The same bookkeeping run by one warp (the render plan's last warp to
-// finish): views one after the other, each with the lane-strided sums and
-// shuffle tree of finalize_block, so the trace is bit-identical to it.
-__device__ __forceinline__ void finalize_warp(const double* sq, int n_views, int bpv, double pixels,
-                                              const double* vol, int n_vol, double n_kp, double eps,
-                                              double* trace, double* trace_vol, fvr_loop_state_t* st) {
-    if (st->done) return;
-    const int lane = threadIdx.x & 31;
-    double mine = 0.0;  // lane v keeps view v's RMSE (n_views <= 32)
-    // eight views at a time, loads of a view's lane-strided sequence issued
-    // ahead (the sums keep finalize_block's order: b = lane, lane + 32, ...)
-    constexpr int kV = 8;
-    for (int v0 = 0; v0 < n_views; v0 += kV) {
-        double s[kV];
-#pragma unroll
-        for (int j = 0; j < kV; ++j) s[j] = 0.0;
-#pragma unroll 4
-        for (int b = lane; b < bpv; b += 32) {
-#pragma unroll
-            for (int j = 0; j < kV; ++j)
-                if (v0 + j < n_views) s[j] += __ldcg(sq + (int64_t)(v0 + j) * bpv + b);
-        }
-#pragma unroll
-        for (int j = 0; j < kV; ++j) {
-            double t = s[j];
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-            if (lane == v0 + j) mine = sqrt(t / pixels);
-        }
-    }
-    double acc = 0.0;
-    for (int i = 0; i < n_views; ++i) acc += __shfl_sync(0xffffffffu, mine, i);
-    if (lane == 0) {
-        const double rmse = acc / (double)n_views;
-        const int it = st->it;
-        trace[it] = rmse;
-        if (vol && trace_vol) {
-            double s = 0.0;
-            for (int b = 0; b < n_vol; ++b) s += __ldcg(vol + b);
-            trace_vol[it] = sqrt(s / n_kp);
-        }
-        const bool conv = rmse < eps || (it > 0 && fabs(rmse - st->prev_rmse) < eps);
-        st->prev_rmse = rmse;
-        st->it = it + 1;
-        if (conv) {
-            st->converged = 1;
-            st->done = 1;
-        }
-    }
-    __syncwarp();
-}
-
 }  // namespace fvr
 
 namespace fvr {
