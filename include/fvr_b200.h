@@ -91,7 +91,13 @@ typedef struct fvr_loop_state {
  * (fvr_rplan_render): per channel c, the RMSE partials are sq_partials + c *
  * sq_stride (n_views x blocks_per_view), the volume partials vol_partials +
  * c * n_vol_blocks (NULL: none), the traces trace_rmse / trace_vol + c *
- * trace_stride. */
+ * trace_stride.  sq_accum (may be NULL; zeroed once by the caller): per
+ * channel n_views + 1 int64 -- the per-view squared-residual sums in fixed
+ * point (2^-24) that the render's units accumulate, then an overflow flag;
+ * the finalize reads and re-zeroes them.  Per-view sums are integer sums of
+ * the per-unit partials rounded to 2^-24 in every finalize (fused, separate,
+ * sharded), so all agree to the bit; a partial beyond 2^38 / blocks_per_view
+ * switches every path to the f64 sums of the partials. */
 typedef struct fvr_loop_finalize {
     int32_t n_views;
     int32_t blocks_per_view;
@@ -104,6 +110,7 @@ typedef struct fvr_loop_finalize {
     double* trace_rmse;
     double* trace_vol;
     int64_t trace_stride;
+    int64_t* sq_accum;
 } fvr_loop_finalize_t;
 
 const char* fvr_last_error(void);

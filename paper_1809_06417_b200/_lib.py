@@ -86,6 +86,7 @@ class FvrLoopFinalize(ctypes.Structure):
         ("trace_rmse", c_void_p),
         ("trace_vol", c_void_p),
         ("trace_stride", c_int64),
+        ("sq_accum", c_void_p),
     ]
 
 

@@ -129,23 +129,69 @@ constexpr int kResPitch = NCH == 1 ? 1 : 4;
 #define FVR_FINALIZE_UNROLL 16  // (config 2 render + finalize 0.0892 -> 0.0887 ms; full unroll: 0.0985)
 #endif
 constexpr int kFinalizeUnroll = FVR_FINALIZE_UNROLL;
+// Per-view squared-residual sums in fixed point: each unit's f64 partial is
+// rounded to an integer multiple of 2^-kSqFixBits and the per-view sums are
+// integer sums -- order-free, so a fused finalize fed by per-unit atomics, a
+// separate finalize over the partials and any view sharding agree to the bit.
+// While every partial stays below sq_fix_limit(bpv) no per-view sum can
+// overflow; beyond that the f64 sums of the partials (in unit order) are used
+// by every path alike.
+constexpr int kSqFixBits = 24;
+__device__ __forceinline__ long long sq_fix(double s) { return __double2ll_rn(ldexp(s, kSqFixBits)); }
+__device__ __forceinline__ double sq_fix_limit(int bpv) { return ldexp(1.0, 62 - kSqFixBits) / (double)bpv; }
+
 // trace append, optional vol_rmse and the rule.  Fixed order: bit-identical
-// wherever it runs.  s_view: >= n_views doubles of shared memory.
+// wherever it runs.  s_view: >= n_views doubles of shared memory (plus one int
+// slot after them).  acc (may be NULL): n_views fixed-point sums accumulated by
+// the partials' producers, acc[n_views] = their overflow flag; they are reset
+// here for the next iteration.  Without acc the sums come from the partials.
 __device__ __forceinline__ void finalize_block(const double* sq, int n_views, int bpv, double pixels,
                                                const double* vol, int n_vol, double n_kp, double eps,
                                                double* trace, double* trace_vol, fvr_loop_state_t* st,
-                                               double* s_view) {
+                                               double* s_view, long long* acc = nullptr) {
     if (st->done) return;  // uniform: every thread reads the same state
     const int lane = threadIdx.x & 31;
-    for (int v = threadIdx.x >> 5; v < n_views; v += blockDim.x >> 5) {
-        double s = 0.0;
-        // FVR_FINALIZE_UNROLL loads in flight per lane (the sum keeps its order)
-#pragma unroll kFinalizeUnroll
-        for (int b = lane; b < bpv; b += 32) s += __ldcg(sq + (int64_t)v * bpv + b);
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0) s_view[v] = sqrt(s / pixels);
+    int* s_ovf = reinterpret_cast<int*>(s_view + n_views);
+    bool ovf;
+    if (acc) {
+        ovf = __ldcg(acc + n_views) != 0;
+    } else {  // any partial beyond the fixed-point range?
+        if (threadIdx.x == 0) *s_ovf = 0;
+        __syncthreads();
+        const double lim = sq_fix_limit(bpv);
+        bool big = false;
+        for (int64_t b = threadIdx.x; b < (int64_t)n_views * bpv; b += blockDim.x) big |= !(__ldcg(sq + b) < lim);
+        if (__any_sync(0xffffffffu, big) && lane == 0) *s_ovf = 1;
+        __syncthreads();
+        ovf = *s_ovf != 0;
     }
+    if (!ovf && acc) {
+        if (threadIdx.x < n_views) {
+            s_view[threadIdx.x] = sqrt(ldexp((double)__ldcg(acc + threadIdx.x), -kSqFixBits) / pixels);
+            acc[threadIdx.x] = 0;
+        }
+    } else {
+        for (int v = threadIdx.x >> 5; v < n_views; v += blockDim.x >> 5) {
+            if (!ovf) {  // the fixed-point sums from the partials
+                long long s = 0;
+#pragma unroll kFinalizeUnroll
+                for (int b = lane; b < bpv; b += 32) s += sq_fix(__ldcg(sq + (int64_t)v * bpv + b));
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+                if (lane == 0) s_view[v] = sqrt(ldexp((double)s, -kSqFixBits) / pixels);
+            } else {
+                double s = 0.0;
+                // FVR_FINALIZE_UNROLL loads in flight per lane (the sum keeps its order)
+#pragma unroll kFinalizeUnroll
+                for (int b = lane; b < bpv; b += 32) s += __ldcg(sq + (int64_t)v * bpv + b);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+                if (lane == 0) s_view[v] = sqrt(s / pixels);
+            }
+        }
+        if (acc && threadIdx.x < n_views) acc[threadIdx.x] = 0;
+    }
+    if (acc && threadIdx.x == 0) acc[n_views] = 0;
     __syncthreads();
     if (threadIdx.x == 0) {
         double acc = 0.0;

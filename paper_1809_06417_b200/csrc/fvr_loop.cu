@@ -31,7 +31,7 @@ __global__ void finalize_kernel(const double* __restrict__ sq, int n_views, int 
                                 double pixels, const double* __restrict__ vol, int n_vol,
                                 double n_kp, double eps, double* __restrict__ trace,
                                 double* __restrict__ trace_vol, fvr_loop_state_t* __restrict__ st) {
-    __shared__ double view_rmse[32];
+    __shared__ double view_rmse[33];
     finalize_block(sq, n_views, bpv, pixels, vol, n_vol, n_kp, eps, trace, trace_vol, st, view_rmse);
 }
 

@@ -1276,6 +1276,7 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
         fin.trace = finalize->trace_rmse;
         fin.trace_vol = finalize->trace_vol;
         fin.trace_stride = finalize->trace_stride;
+        fin.acc = reinterpret_cast<long long*>(finalize->sq_accum);
     }
     if (!kp_values || !entries_a || !entries_b) return set_error(FVR_ERR_INVALID, "kp_values / entries are NULL");
     fvr_render_params_t p{};

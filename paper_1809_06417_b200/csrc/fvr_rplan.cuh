@@ -635,6 +635,7 @@ struct RplanFinalize {
     bool on;
     int n_views, bpv, n_vol;
     double pixels, n_kp, eps;
+    long long* acc;  // (NCH, n_views + 1) fixed-point sums + overflow flag, or NULL
     const double* vol;
     double* trace;
     double* trace_vol;
@@ -668,7 +669,8 @@ __device__ __forceinline__ void rplan_render_unit(
     const uint32_t* __restrict__ ent_a, const uint32_t* __restrict__ ent_b, const double* __restrict__ base,
     const double* __restrict__ t_fin, const int* __restrict__ row_src, int64_t rows, int units_x,
     int units_per_view, int n_views, int w, int h, const float* __restrict__ src, const float* __restrict__ kpv,
-    const RenderConsts& rc, float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride) {
+    const RenderConsts& rc, float* __restrict__ residual, double* __restrict__ sq_partials, int64_t sq_stride,
+    long long* __restrict__ sq_acc = nullptr, int bpv = 0) {
     // kpv: max(v, 0) per hull key point (NCH = 1: f32; NCH = 3: float4)
     const int len = unit_len[unit];  // a multiple of 8
     const long long off = unit_off[unit];  // a multiple of 8
@@ -777,7 +779,15 @@ __device__ __forceinline__ void rplan_render_unit(
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
         const double tot = warp_sum(sq[c]);
-        if (lane == 0) sq_partials[c * sq_stride + unit] = tot;
+        if (lane == 0) {
+            sq_partials[c * sq_stride + unit] = tot;
+            if (sq_acc) {  // the fused finalize's per-view fixed-point sum (see finalize_block)
+                long long* a = sq_acc + c * (n_views + 1);
+                atomicAdd(reinterpret_cast<unsigned long long*>(a + unit / units_per_view),
+                          (unsigned long long)sq_fix(tot));
+                if (!(tot < sq_fix_limit(bpv))) atomicExch(reinterpret_cast<unsigned long long*>(a + n_views), 1ull);
+            }
+        }
     }
 }
 
@@ -819,11 +829,11 @@ rplan_render_kernel(
          unit += (int)(((int64_t)gridDim.x * blockDim.x) >> 5))
         rplan_render_unit<NCH, WIDE>(unit_order ? __ldg(unit_order + unit) : unit, lane, unit_len, unit_off, ent_a, ent_b,
                                base, t_fin, row_src, rows, units_x, units_per_view, n_views, w, h, src, kpv, rc,
-                               residual, sq_partials, sq_stride);
+                               residual, sq_partials, sq_stride, fin.on ? fin.acc : nullptr, fin.bpv);
     if (!fin.on) return;
     // the last block to finish runs the loop's finalize (fvr_loop.cu)
     __shared__ int s_last;
-    __shared__ double s_view[32];
+    __shared__ double s_view[33];  // (n_views + an overflow slot)
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -836,7 +846,7 @@ rplan_render_kernel(
         finalize_block(sq_partials + c * sq_stride, fin.n_views, fin.bpv, fin.pixels,
                        fin.vol ? fin.vol + c * fin.n_vol : nullptr, fin.n_vol, fin.n_kp, fin.eps,
                        fin.trace + c * fin.trace_stride, fin.trace_vol ? fin.trace_vol + c * fin.trace_stride : nullptr,
-                       state + c, s_view);
+                       state + c, s_view, fin.acc ? fin.acc + c * (fin.n_views + 1) : nullptr);
     if (threadIdx.x == 0) state->work_retired = 0;
 }
 

@@ -760,6 +760,9 @@ class ChannelLoop:
             f.trace_rmse = self.trace.data_ptr()
             f.trace_vol = _lib.ptr(self.trace_vol)
             f.trace_stride = self.trace.shape[1]
+            # per-view fixed-point sums the render's units accumulate (+ an overflow flag per channel)
+            self._sq_acc = self.t.zeros(self.nch * (self.n_views + 1), dtype=self.t.int64, device=self.dev)
+            f.sq_accum = self._sq_acc.data_ptr()
             self._fin_args = f
         return ctypes.addressof(self._fin_args)
 
