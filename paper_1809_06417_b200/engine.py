@@ -688,6 +688,7 @@ class ChannelLoop:
         return True
 
     def _render(self, stream):
+        self._host_small = None  # (every iteration starts here: staged states / traces are stale)
         if self.v_end <= self.v_begin:
             return 0
         if self.rplan:
@@ -1048,7 +1049,7 @@ class ChannelLoop:
         self.graph = g
 
     def step(self) -> None:
-        self._host_values = None  # a staged result copy is stale once the lattice moves
+        self._host_values = self._host_small = None  # staged result copies are stale once the loop moves
         if self.graph is not None:
             self.graph.replay()
         else:
@@ -1056,13 +1057,16 @@ class ChannelLoop:
 
     # -- the loop ----------------------------------------------------------------
     def reset_state(self) -> None:
+        self._host_small = None
         self.state.zero_()
         if self.accum is not None:
             self.accum.zero_()
 
     def read_states(self) -> list[dict]:
+        small = getattr(self, "_host_small", None)
+        states = small[0] if small is not None else self.state.cpu().numpy()
         out = []
-        for s in self.state.cpu().numpy():
+        for s in states:
             prev = s[4:6].copy().view(np.float64)[0]
             out.append({"it": int(s[0]), "done": int(s[1]), "converged": int(s[2]), "prev_rmse": float(prev)})
         return out
@@ -1197,10 +1201,22 @@ class ChannelLoop:
     def _stage_values(self) -> None:
         """Queue the lattice's D2H into page-locked memory behind the last
         iteration; the pinned allocation overlaps the device work still in
-        flight (a pageable .cpu() of 8.6 MB at 128^3 costs about 3 ms)."""
-        host = self.t.empty(tuple(self.values.shape), dtype=self.t.float32, pin_memory=True)
+        flight (a pageable .cpu() of 8.6 MB at 128^3 costs about 3 ms).  The
+        loop states and traces ride along, so reading them after the run
+        costs no further round trip."""
+        t = self.t
+        host = t.empty(tuple(self.values.shape), dtype=t.float32, pin_memory=True)
         host.copy_(self.values, non_blocking=True)
         self._host_values = host
+        st = t.empty(tuple(self.state.shape), dtype=self.state.dtype, pin_memory=True)
+        st.copy_(self.state, non_blocking=True)
+        tr = t.empty(tuple(self.trace.shape), dtype=self.trace.dtype, pin_memory=True)
+        tr.copy_(self.trace, non_blocking=True)
+        tv = None
+        if self.trace_vol is not None:
+            tv = t.empty(tuple(self.trace_vol.shape), dtype=self.trace_vol.dtype, pin_memory=True)
+            tv.copy_(self.trace_vol, non_blocking=True)
+        self._host_small = (st.numpy(), tr.numpy(), None if tv is None else tv.numpy())
 
     def host_values(self) -> np.ndarray:
         host, self._host_values = getattr(self, "_host_values", None), None
@@ -1212,6 +1228,11 @@ class ChannelLoop:
         return v[0] if self.nch == 1 else v
 
     def host_trace(self, iterations: int, channel: int = 0):
+        small = getattr(self, "_host_small", None)
+        if small is not None:  # staged with the lattice after run()
+            rmse = small[1][channel, :iterations].tolist()
+            vol = small[2][channel, :iterations].tolist() if small[2] is not None else []
+            return rmse, vol
         rmse = self.trace[channel, :iterations].cpu().numpy().tolist()
         vol = self.trace_vol[channel, :iterations].cpu().numpy().tolist() if self.trace_vol is not None else []
         return rmse, vol
