@@ -833,8 +833,10 @@ class ChannelLoop:
         # rays, so their residual / rho reads share cache lines) sorted by
         # length within windows of sigma rows (SELL-C-sigma; config 2:
         # sigma 0 / 64 / 128 / 512 / 4096: 0.0783 / 0.0773 / 0.0760 / 0.0767 /
-        # 0.0844 ms)
-        sigma = int(os.environ.get("FVR_SELL_SIGMA", "128"))
+        # 0.0844 ms; with the final pipelined gather 32 / 64 / 128 / 256:
+        # 0.0501 / 0.0488 / 0.0486 / 0.0519 ms, and the sample plan's gather
+        # 0.0978 / 0.0969 / 0.0985 / 0.1025 ms -- so 64 for the sample plan)
+        sigma = int(os.environ.get("FVR_SELL_SIGMA", "64" if self.sample_plan else "128"))
         # whole lane chunks (fvr_plan.cu): 16 bytes of six-byte entries (8), or
         # 32 bytes of eight-byte (wide) entries (kSE = 4); the sample plan's
         # format is decided after the sizes reach the host, so it pads to 8
