@@ -97,7 +97,10 @@ typedef struct fvr_loop_state {
  * the finalize reads and re-zeroes them.  Per-view sums are integer sums of
  * the per-unit partials rounded to 2^-24 in every finalize (fused, separate,
  * sharded), so all agree to the bit; a partial beyond 2^38 / blocks_per_view
- * switches every path to the f64 sums of the partials. */
+ * switches every path to the f64 sums of the partials.  l2_discard: the
+ * stochastic mode's rho, consumed by the previous gather and rewritten by the
+ * next weigh pass -- discard.global.L2 over it (128-byte lines) keeps its
+ * ~33 MB of dirty lines from being written back while the render streams. */
 typedef struct fvr_loop_finalize {
     int32_t n_views;
     int32_t blocks_per_view;
@@ -111,6 +114,8 @@ typedef struct fvr_loop_finalize {
     double* trace_vol;
     int64_t trace_stride;
     int64_t* sq_accum;
+    void* l2_discard;           /* (may be NULL) a buffer that is dead once this render starts: its */
+    int64_t l2_discard_bytes;   /* dirty L2 lines are dropped instead of written back (see below) */
 } fvr_loop_finalize_t;
 
 const char* fvr_last_error(void);

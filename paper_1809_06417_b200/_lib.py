@@ -87,6 +87,8 @@ class FvrLoopFinalize(ctypes.Structure):
         ("trace_vol", c_void_p),
         ("trace_stride", c_int64),
         ("sq_accum", c_void_p),
+        ("l2_discard", c_void_p),
+        ("l2_discard_bytes", c_int64),
     ]
 
 

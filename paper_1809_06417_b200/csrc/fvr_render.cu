@@ -1277,6 +1277,12 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
         fin.trace_vol = finalize->trace_vol;
         fin.trace_stride = finalize->trace_stride;
         fin.acc = reinterpret_cast<long long*>(finalize->sq_accum);
+        if (finalize->l2_discard && finalize->l2_discard_bytes >= 128) {
+            if (reinterpret_cast<uintptr_t>(finalize->l2_discard) % 128)
+                return set_error(FVR_ERR_INVALID, "l2_discard must be 128-byte aligned");
+            fin.discard = static_cast<char*>(finalize->l2_discard);
+            fin.discard_lines = finalize->l2_discard_bytes / 128;
+        }
     }
     if (!kp_values || !entries_a || !entries_b) return set_error(FVR_ERR_INVALID, "kp_values / entries are NULL");
     fvr_render_params_t p{};

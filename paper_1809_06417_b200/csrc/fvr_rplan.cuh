@@ -636,6 +636,8 @@ struct RplanFinalize {
     int n_views, bpv, n_vol;
     double pixels, n_kp, eps;
     long long* acc;  // (NCH, n_views + 1) fixed-point sums + overflow flag, or NULL
+    char* discard;   // a dead buffer whose dirty L2 lines are dropped (rho), or NULL
+    int64_t discard_lines;
     const double* vol;
     double* trace;
     double* trace_vol;
@@ -821,6 +823,11 @@ rplan_render_kernel(
     }
     pdl_wait();  // the previous gather's operand update and state
     if (all_done<NCH>(state)) return;
+    if (fin.discard) {  // (after the wait: the previous gather has read it)
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < fin.discard_lines;
+             i += (int64_t)gridDim.x * blockDim.x)
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(fin.discard + i * 128) : "memory");
+    }
     const int64_t rows = (int64_t)n_units * 32;
     // units longest first (unit_order): the block scheduler then hands the
     // short bbox-margin units to SMs as they free up, with no long unit left

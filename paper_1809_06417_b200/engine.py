@@ -764,6 +764,10 @@ class ChannelLoop:
             # per-view fixed-point sums the render's units accumulate (+ an overflow flag per channel)
             self._sq_acc = self.t.zeros(self.nch * (self.n_views + 1), dtype=self.t.int64, device=self.dev)
             f.sq_accum = self._sq_acc.data_ptr()
+            if self.sample_plan and self.rho is not None and os.environ.get("FVR_L2_DISCARD", "1") == "1":
+                # rho is dead between the gather and the next weigh pass: drop its dirty L2 lines
+                f.l2_discard = self.rho.data_ptr()
+                f.l2_discard_bytes = self.rho.numel() * self.rho.element_size()
             self._fin_args = f
         return ctypes.addressof(self._fin_args)
 

@@ -18,7 +18,7 @@ torch.cuda.set_device(0)
 cfg_no = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 sc = workloads.device_scene(*workloads.CONFIGS[cfg_no])
 cfg = ReconstructionConfig(alpha_l=0.006, alpha_d=1.0, tau=sc["tau"], max_iters=20, converge_eps=1e-12,
-                           deterministic_mode=True)
+                           deterministic_mode=os.environ.get("STAGE_STOCHASTIC") != "1", g_sigma=0.1, rng_seed=0)
 grid0 = _init_grid(sc["geom"], sc["hull"], "green")
 src = [im.data[sc["bbox"].slices][:, :, 0] for im in sc["images"]]
 loop = ChannelLoop(sc["cams"], grid0, grid0.values, src, sc["masks"], sc["bbox"], sc["hull"].inside_voxels(),
