@@ -250,7 +250,9 @@ int fvr_loop_render(const fvr_camera_t* cams, int32_t n_views, int32_t u0, int32
  * fvr_loop_finalize on state (one launch less per iteration; the block
  * counter is state[0].work_retired).
  * fvr_rplan_fill with values == NULL asserts that no key point outside
- * `dynamic` is positive (base then holds nothing but the background term).
+ * `dynamic` is positive (base then holds zeros); fvr_rplan_render may then
+ * take base == NULL, and t_fin == NULL when every background is 0 (each adds
+ * exactly +0.0, so the outputs are the same bits without streaming them).
  * wide != 0 (fill and render must agree): 8-byte entries, u32 column in
  * entries_a and f32 weight in entries_b at the same layout as entries_a
  * (entries_b holds unit_off-total u32) -- for hulls of >= 2^24 key points,

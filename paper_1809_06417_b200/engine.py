@@ -699,7 +699,12 @@ class ChannelLoop:
                 n += 1
             _lib.call(
                 "fvr_rplan_render", self.rp_len.data_ptr(), self.rp_off.data_ptr(), self.rp_a.data_ptr(),
-                self.rp_b.data_ptr(), self.rp_base.data_ptr(), self.rp_tfin.data_ptr(), _lib.ptr(self.rp_order),
+                self.rp_b.data_ptr(),
+                # the loop's own initial lattice has no static term (base is all zeros), and a zero
+                # background needs no t_fin: neither is streamed then
+                None if self._static_zero else self.rp_base.data_ptr(),
+                self.rp_tfin.data_ptr() if any(b != 0.0 for b in self.background) else None,
+                _lib.ptr(self.rp_order),
                 _lib.ptr(self.rp_row_src), self.v_end - self.v_begin, self.w_bb, self.h_bb, self.src.data_ptr(),
                 self.rp_kpv.data_ptr(), self.nch, self.background, self.residual.data_ptr(),
                 self.sq[0, self.v_begin * self.bpv:].data_ptr(), self.n_sq, self.state.data_ptr(),
