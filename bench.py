@@ -375,10 +375,12 @@ def run_gpu(args):
     if loop.rplan:
         kname = "rplan_render_kernel<1>"
         rows = loop.rp_len.numel() * 32
-        kbytes = 6 * loop.rplan_nnz + 16 * rows + 8 * w["VP"]
-        rule = ("render plan: 6 B per stored SELL entry (24-bit key-point index + 24-bit weight) + 16 B per row "
-                "(base, t_fin) + 8 B per bbox pixel (src in, residual out); the key-point operand (1.2 MB) hits "
-                "L1/L2")
+        # per row: base (8 B) unless the loop started from its own lattice, t_fin (8 B) for a nonzero background
+        row_b = (0 if loop._static_zero else 8) + (8 if any(b != 0.0 for b in loop.background) else 0)
+        kbytes = 6 * loop.rplan_nnz + row_b * rows + 8 * w["VP"]
+        rule = (f"render plan: 6 B per stored SELL entry (24-bit key-point index + 24-bit weight) + {row_b} B per "
+                "row (base f64 unless the loop starts from its own lattice, t_fin f64 for a nonzero background) + "
+                "8 B per bbox pixel (src in, residual out); the key-point operand (1.2 MB) hits L1/L2")
     else:
         kname = "loop_render_scat_kernel"
         kbytes = live_bytes
@@ -390,14 +392,14 @@ def run_gpu(args):
 
     # What one step streams from HBM (the plans are re-read every iteration;
     # the operands they index are cache-resident): render plan (6 B per stored
-    # entry + 16 B per row + 8 B per pixel) and adjust plan (6 B per stored
+    # entry + base/t_fin per row as streamed + 8 B per pixel) and adjust plan (6 B per stored
     # entry + 20 B per hull key point: row order, key-point index, value
     # read/write, operand write)
     adj_bytes = 6 * loop.plan_slots + 20 * loop.n_kp if loop.plan else 0
     step_bytes = kbytes + adj_bytes
     step_streamed = {"bytes": step_bytes, "render_bytes": kbytes, "adjust_bytes": adj_bytes,
                      "achieved_gbs": step_bytes / (ms * 1e-3) / 1e9, "frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
-                     "rule": "render plan 6 B/stored entry + 16 B/row + 8 B/pixel; adjust plan 6 B/stored entry + "
+                     "rule": "render plan 6 B/stored entry + base/t_fin as streamed + 8 B/pixel; adjust plan 6 B/stored entry + "
                              "20 B/hull key point; over the whole step time (both launches + gaps)"}
     # Per-call model of the public API: the plans are built once per
     # reconstruct_channel call (count + fill passes over every ray), then

@@ -290,7 +290,8 @@ int fvr_rplan_pack(const float* values, int32_t n_channels, fvr_grid_t grid, con
                    int64_t n_kp, float* kp_values, const fvr_loop_state_t* state, void* stream);
 
 /* Back-project the residual of every listed flame ray (ray_list entries are
- * view << 24 | (row_in_bbox * bbox_w + col_in_bbox)). stochastic != 0 draws
+ * view << 24 | (row_in_bbox * bbox_w + col_in_bbox); the top byte is read
+ * unsigned, so a view index never decodes negative). stochastic != 0 draws
  * G ~ clip(N(1, g_sigma), 0, 2) from a counter-based Philox stream keyed by
  * seed and (iteration, ray_id_base + ray, sample), so a view-sharded run
  * draws the same weights as a single-GPU run. */

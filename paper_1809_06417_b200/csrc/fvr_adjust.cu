@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(128) loop_adjust_kernel(
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_rays) return;
     const int32_t e = ray_list[r];
-    const int view = e >> 24, pix = e & 0xFFFFFF;
+    const int view = (int)((uint32_t)e >> 24), pix = e & 0xFFFFFF;
     const int row = pix / w, col = pix - row * w;
     const float res = residual[((int64_t)view * w * h + pix) * res_pitch];
     if (res == 0.f && !PHILOX) return;  // every deposit would be exactly zero

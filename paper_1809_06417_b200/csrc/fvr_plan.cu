@@ -89,7 +89,7 @@ __device__ __forceinline__ bool plan_ray(const fvr_camera_t* __restrict__ cams,
                                          const int32_t* __restrict__ ray_list, int64_t r, int u0,
                                          int v0, int w, int h, PlanRay& pr) {
     const int32_t e = ray_list[r];
-    const int view = e >> 24, pix = e & 0xFFFFFF;
+    const int view = (int)((uint32_t)e >> 24), pix = e & 0xFFFFFF;
     const int row = pix / w, col = pix - row * w;
     const fvr_camera_t& cam = cams[view];
     pixel_dir(cam, (double)(u0 + col) + 0.5, (double)(v0 + row) + 0.5, pr.d);
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(256) weighted_residual_kernel(
          b += (int64_t)gridDim.x * blockDim.x) {
         const int2 m = __ldcs(bmeta + b);
         const int32_t e = __ldg(ray_list + m.x);
-        const int64_t pix = (int64_t)(e >> 24) * w * h + (e & 0xFFFFFF);
+        const int64_t pix = (int64_t)((uint32_t)e >> 24) * w * h + (e & 0xFFFFFF);
         const uint4 blk = gauss_block(seed, it, (uint32_t)(ray_id_base + m.x), (uint32_t)(m.y >> 4));
         const float2 z01 = gauss_pair(blk.x, blk.y), z23 = gauss_pair(blk.z, blk.w);
         float gw[4] = {gauss_clip(z01.x, g_sigma), gauss_clip(z01.y, g_sigma), gauss_clip(z23.x, g_sigma),
