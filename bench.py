@@ -42,7 +42,7 @@ ALPHA_L = 0.006
 # dram__bytes_read.sum + dram__bytes_write.sum of K-render from one `ncu --set full`
 # capture: the render-plan SpMV (profiles/r1_ncu_final9_render_gather_raw.csv) and the marching
 # kernel it replaced (profiles/r1_ncu_render_final_raw.csv)
-TRAFFIC_BYTES_PER_LAUNCH = {"rplan_render_kernel<1>": 523_784_960, "loop_render_scat_kernel": 10_210_304}
+TRAFFIC_BYTES_PER_LAUNCH = {"rplan_render_kernel<1>": 522_099_968, "loop_render_scat_kernel": 10_210_304}
 TRAFFIC_SOURCE = {"rplan_render_kernel<1>": "profiles/r2final_ncu_det_raw.csv (round 2 final, ID 0)",
                   "loop_render_scat_kernel": "profiles/r1_ncu_render_final_raw.csv (round 1)"}
 DTYPE = ("f32 values, 17-bit-mantissa operator weights (render and adjust plans), f64 geometry, "

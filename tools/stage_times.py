@@ -38,7 +38,8 @@ for _ in range(5):
     evs.append(e)
 torch.cuda.synchronize()
 ms = {n: float(np.mean([e[i].elapsed_time(e[i + 1]) for e in evs])) for i, (n, _) in enumerate(stages)}
-rb = 6 * loop.rplan_nnz + 16 * loop.rp_len.numel() * 32 + 8 * sum(s.size for s in src)
+row_b = (0 if loop._static_zero else 8) + (8 if any(b != 0.0 for b in loop.background) else 0)  # base, t_fin
+rb = 6 * loop.rplan_nnz + row_b * loop.rp_len.numel() * 32 + 8 * sum(s.size for s in src)
 ab = 6 * loop.plan_slots + 20 * loop.n_kp
 print(json.dumps({"config": cfg_no, "stage_ms": ms, "render_gb": rb / 1e9, "adjust_gb": ab / 1e9,
                   "render_tbs": rb / ms.get("render", 1e9) / 1e9, "adjust_tbs": ab / ms.get("adjust", 1e9) / 1e9,
