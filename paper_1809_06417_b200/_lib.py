@@ -335,6 +335,23 @@ def to_host(tensor):
     return host.numpy()
 
 
+class HostRead:
+    """A small D2H queued now on the current stream into page-locked memory,
+    read later: ``get()`` waits for this copy only (an event), so the host can
+    queue other work while the device catches up."""
+
+    def __init__(self, tensor):
+        t = torch()
+        self.host = t.empty(tuple(tensor.shape), dtype=tensor.dtype, pin_memory=True)
+        self.host.copy_(tensor, non_blocking=True)
+        self.event = t.cuda.Event()
+        self.event.record()
+
+    def get(self):
+        self.event.synchronize()
+        return self.host.tolist()
+
+
 def upload_host(arrays, dtype, shape, dev):
     """Host arrays concatenated (fvr_copy_host_parallel, all host threads) into
     page-locked staging, then one asynchronous H2D into a new device tensor of

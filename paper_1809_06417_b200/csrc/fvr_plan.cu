@@ -758,7 +758,11 @@ extern "C" int fvr_loop_gather(const int32_t* slice_len, const int64_t* slice_of
     const int64_t n_slices = (n_kp + 31) / 32;
     int64_t blocks = (n_slices * 32 + FVR_GATHER_THREADS - 1) / FVR_GATHER_THREADS;
     // (a grid-stride loop beyond 148 x 24 CTAs of 256 threads: the same warps for any CTA size)
+#ifdef FVR_GATHER_CAP
+    const int64_t cap = FVR_GATHER_CAP;
+#else
     const int64_t cap = 148 * 24 * 256 / FVR_GATHER_THREADS;
+#endif
     if (blocks > cap) blocks = cap;
     const int sy = grid.nz + 1, ny1 = grid.ny + 1;
     const int64_t plane = (int64_t)(grid.nx + 1) * (grid.ny + 1) * (grid.nz + 1);

@@ -441,16 +441,19 @@ class ChannelLoop:
         adjust_done = kpmap_ready = pc = None
         rs = self._rplan_scan(*self._rp_counted) if self._rp_counted is not None else None
         self._rp_counted = None
+        if rs is not None:  # the sizes leave as soon as the layout is done
+            rs["sizes"] = _lib.HostRead(rs["sizes"])
         self._mark("render layout queued")
         if self.plan:
             kpmap_ready = t.cuda.Event()
             kpmap_ready.record(side)
             with t.cuda.stream(side):  # queued ahead of the render fill, which would hold every SM
                 pc = self._plan_count()
+                pc["sizes"] = _lib.HostRead(pc["sizes"])
         self._mark("adjust count queued")
         rfill_done = None
         if rs is not None:
-            sizes = rs["sizes"].cpu().tolist()
+            sizes = rs["sizes"].get()
             self._mark("render sizes read")
             if kpmap_ready is not None:
                 main.wait_event(kpmap_ready)
@@ -460,7 +463,7 @@ class ChannelLoop:
             self._mark("render fill queued")
         if pc is not None:
             with t.cuda.stream(side):
-                sizes = pc["sizes"].cpu().tolist()  # synchronises the side stream only
+                sizes = pc["sizes"].get()  # waits for the side stream's copy only
                 self._mark("adjust sizes read")
                 if rfill_done is not None and os.environ.get("FVR_FILL_SERIAL", "1") == "1":
                     side.wait_event(rfill_done)
