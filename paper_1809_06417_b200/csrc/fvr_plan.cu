@@ -657,7 +657,15 @@ gather_kernel(
             for (int i = 0; i < B; ++i) {
                 const float wgt = __int_as_float(en[i].y);
                 if (NCH == 1) {
+#if FVR_RHO_EVICT_LAST
+                    float rv;
+                    uint64_t pol;
+                    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+                    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(rv) : "l"(residual + en[i].x), "l"(pol));
+                    acc[0] += __float2ll_rn(rv * wgt * 4294967296.0f);
+#else
                     acc[0] += __float2ll_rn(__ldg(residual + en[i].x) * wgt * 4294967296.0f);
+#endif
                 } else {
                     const float4 r = __ldg(reinterpret_cast<const float4*>(residual) + en[i].x);
                     const float rr[3] = {r.x, r.y, r.z};
