@@ -376,6 +376,12 @@ int fvr_sample_plan_reorder(int32_t* entries, int64_t n_slots, int32_t e6, const
  * fvr_sample_plan_reorder. */
 int fvr_sample_plan_spatial(int32_t* entries, int64_t n_slots, int32_t e6, const int64_t* block_keys,
                             int64_t n_blocks, const int32_t* meta_in, int32_t* meta_out, void* stream);
+/* Sort every row of a 6-byte SELL plan (fvr_adjust_plan_fill /
+ * fvr_sample_plan_fill layout) by column in place; rows of slices longer than
+ * 1024 entries keep their order.  The gather's sums are order-independent
+ * (32.32 fixed point), so only the memory access pattern changes. */
+int fvr_plan_sort_rows(const int32_t* slice_len, const int64_t* slice_off, int64_t n_slices, int32_t* entries,
+                       uint32_t* entries_b, void* stream);
 /* The stochastic mode's G = clip(N(1, g_sigma), 0, 2) for (seed, iteration,
  * ray, march index k) -- the counter-based replacement of the reference's
  * rng.normal draw (reconstruct.py:191-204); the weigh pass and the ray-driven

@@ -188,9 +188,80 @@ __global__ void flame_ray_kernel(int32_t* __restrict__ rays, const int64_t* __re
     }
 }
 
+// Rows of a 6-byte SELL plan sorted by column (the a-word's low 24 bits), one
+// warp per row: the row is read out of its lane's 16-byte chunks into shared
+// memory as (column << 32 | exponent << 16 | mantissa half), bitonic-sorted,
+// and written back.  The gather's fixed-point sums do not depend on entry
+// order, so this only changes which rho lines a warp's lanes touch together.
+constexpr int kRowSortMax = 1024;
+constexpr int kRowSortWarps = 4;
+__global__ void __launch_bounds__(32 * kRowSortWarps)
+plan_sort_rows_kernel(const int32_t* __restrict__ slice_len, const long long* __restrict__ slice_off,
+                      int64_t n_slices, uint32_t* __restrict__ ea, uint16_t* __restrict__ eb) {
+    __shared__ unsigned long long buf[kRowSortWarps][kRowSortMax];
+    const int lane = threadIdx.x & 31;
+    unsigned long long* s = buf[threadIdx.x >> 5];
+    const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_slices * 32; r += stride) {
+        const int64_t sl = r >> 5;
+        const int ln = (int)(r & 31);
+        const int len = slice_len[sl];
+        if (len <= 1 || len > kRowSortMax) continue;
+        const long long off = slice_off[sl];
+        int n = 32;
+        while (n < len) n <<= 1;
+        for (int p = lane; p < n; p += 32) {
+            unsigned long long v = ~0ull;
+            if (p < len) {
+                const uint32_t a = ea[(((off >> 2) + (p >> 2)) * 32 + ln) * 4 + (p & 3)];
+                const uint16_t b = eb[(((off >> 3) + (p >> 3)) * 32 + ln) * 8 + (p & 7)];
+                v = ((unsigned long long)(a & 0xFFFFFFu) << 32) | ((unsigned long long)(a >> 24) << 16) | b;
+            }
+            s[p] = v;
+        }
+        __syncwarp();
+        for (int k = 2; k <= n; k <<= 1)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = lane; i < n; i += 32) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const unsigned long long x = s[i], y = s[ixj];
+                        if ((x > y) == ((i & k) == 0)) {
+                            s[i] = y;
+                            s[ixj] = x;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        for (int p = lane; p < len; p += 32) {
+            const unsigned long long v = s[p];
+            ea[(((off >> 2) + (p >> 2)) * 32 + ln) * 4 + (p & 3)] =
+                (uint32_t)(v >> 32) | ((uint32_t)((v >> 16) & 0xFFu) << 24);
+            eb[(((off >> 3) + (p >> 3)) * 32 + ln) * 8 + (p & 7)] = (uint16_t)(v & 0xFFFFu);
+        }
+        __syncwarp();
+    }
+}
+
 }  // namespace fvr
 
 using namespace fvr;
+
+extern "C" int fvr_plan_sort_rows(const int32_t* slice_len, const int64_t* slice_off, int64_t n_slices,
+                                  int32_t* entries, uint32_t* entries_b, void* stream) {
+    FVR_TRY_BEGIN
+    if (n_slices <= 0) return FVR_OK;
+    if (!entries_b) return set_error(FVR_ERR_INVALID, "row sort: 6-byte plans only");
+    const int64_t warps = n_slices * 32;
+    int64_t blocks = (warps + kRowSortWarps - 1) / kRowSortWarps;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    plan_sort_rows_kernel<<<(unsigned)blocks, 32 * kRowSortWarps, 0, (cudaStream_t)stream>>>(
+        slice_len, reinterpret_cast<const long long*>(slice_off), n_slices, reinterpret_cast<uint32_t*>(entries),
+        reinterpret_cast<uint16_t*>(entries_b));
+    return check_launch("plan_sort_rows");
+    FVR_TRY_END
+}
 
 extern "C" int fvr_morton_order(const int32_t* kp_index, int64_t n, fvr_grid_t grid, int32_t* out, void* stream) {
     FVR_TRY_BEGIN

@@ -948,6 +948,10 @@ class ChannelLoop:
                 _lib.call("fvr_sample_plan_spatial", entries.data_ptr(), slots, int(entries_b is not None),
                           keys.data_ptr(), n_blocks, meta.data_ptr(), meta_new.data_ptr(), stream)
                 meta = meta_new
+            if entries_b is not None and os.environ.get("FVR_SPLAN_SORT", "0") == "1":
+                # each row by sample id: a warp's lanes then read nearby rho lines together
+                _lib.call("fvr_plan_sort_rows", pc["slice_len"].data_ptr(), pc["slice_off"].data_ptr(),
+                          pc["slice_len"].numel(), entries.data_ptr(), entries_b.data_ptr(), stream)
             self.sample_meta = meta
             self.n_samples = n_samples
         else:

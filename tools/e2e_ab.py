@@ -36,6 +36,10 @@ class SyncRead:
 
 def setup(name):
     _lib.HostRead = SyncRead if name == "sync_sizes" else HostRead
+    if name == "no_row_sort":
+        os.environ["FVR_SPLAN_SORT"] = "0"
+    else:
+        os.environ.pop("FVR_SPLAN_SORT", None)
 
 
 def call():
@@ -46,7 +50,7 @@ def call():
     return (time.perf_counter() - t0) * 1e3
 
 
-names = ["base", "sync_sizes"]
+names = sys.argv[2].split(",") if len(sys.argv) > 2 else ["base", "sync_sizes"]
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 12
 for n in names:  # warm each variant
     setup(n)
