@@ -619,10 +619,25 @@ gather_kernel(
                 static_assert(B % 8 == 0, "batches of whole 16-byte chunks");
                 uint4 av[B / 4], bv[B / 8];
                 const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+#if FVR_PLAN_EVICT_FIRST
+                uint64_t pol;
+                asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+                auto ldp = [&](const uint4* ptr) {
+                    uint4 r;
+                    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr), "l"(pol));
+                    return r;
+                };
+#pragma unroll
+                for (int i = 0; i < B / 4; ++i) av[i] = t + 4 * i < len ? ldp(ea + (int64_t)(t / 4 + i) * 32) : z;
+#pragma unroll
+                for (int i = 0; i < B / 8; ++i) bv[i] = t + 8 * i < len ? ldp(eb + (int64_t)(t / 8 + i) * 32) : z;
+#else
 #pragma unroll
                 for (int i = 0; i < B / 4; ++i) av[i] = t + 4 * i < len ? __ldcs(ea + (int64_t)(t / 4 + i) * 32) : z;
 #pragma unroll
                 for (int i = 0; i < B / 8; ++i) bv[i] = t + 8 * i < len ? __ldcs(eb + (int64_t)(t / 8 + i) * 32) : z;
+#endif
 #pragma unroll
                 for (int i = 0; i < B; ++i) {
                     const uint4& q = av[i / 4];
