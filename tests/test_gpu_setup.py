@@ -260,3 +260,52 @@ def test_occupancy_distance_map(cuda_device, shape):
     occ = torch.empty(shape, dtype=torch.uint8, device=cuda_device)
     _lib.call("fvr_occupancy", dv.data_ptr(), 2, df.data_ptr(), g, occ.data_ptr(), _lib.stream_ptr())
     assert np.array_equal(occ.cpu().numpy(), _dist_ref(values, force))
+
+
+def test_plan_row_sort(cuda_device):
+    """fvr_plan_sort_rows: every lane-row of a 6-byte SELL slice sorted by its
+    24-bit column, the weight (exponent byte + mantissa half) travelling with
+    it; slices longer than 1024 entries are left alone."""
+    import torch
+
+    from paper_1809_06417_b200 import _lib
+
+    rng = np.random.default_rng(7)
+    lens = np.array([8, 40, 1032, 16], dtype=np.int32)  # multiples of 8; the third is too long to sort
+    offs = np.concatenate([[0], np.cumsum(lens.astype(np.int64))])
+    total = int(offs[-1])
+    # per (slice, lane, position): column, exponent, half
+    col = rng.integers(0, 1 << 24, size=(32 * total,), dtype=np.uint32)
+    ex = rng.integers(100, 140, size=(32 * total,), dtype=np.uint32)
+    half = rng.integers(0, 1 << 16, size=(32 * total,), dtype=np.uint32)
+    a = np.zeros(32 * total, dtype=np.uint32)
+    b = np.zeros(32 * total, dtype=np.uint16)
+    where = {}
+    for s, (ln_, off) in enumerate(zip(lens, offs[:-1])):
+        for lane in range(32):
+            for p in range(ln_):
+                ia = (((off >> 2) + (p >> 2)) * 32 + lane) * 4 + (p & 3)
+                ib = (((off >> 3) + (p >> 3)) * 32 + lane) * 8 + (p & 7)
+                where[(s, lane, p)] = (ia, ib)
+    keys = np.arange(32 * total)
+    for (s, lane, p), (ia, ib) in where.items():
+        a[ia] = col[keys[ia]] | (ex[keys[ia]] << 24)
+        b[ib] = half[keys[ia]]
+    dev = torch.device("cuda", 0)
+    ta = torch.from_numpy(a.view(np.int32).copy()).to(dev)
+    tb = torch.from_numpy(np.ascontiguousarray(b).view(np.int32).copy()).to(dev)
+    sl = torch.from_numpy(lens).to(dev)
+    so = torch.from_numpy(offs[:-1].copy()).to(dev)
+    _lib.call("fvr_plan_sort_rows", sl.data_ptr(), so.data_ptr(), len(lens), ta.data_ptr(), tb.data_ptr(),
+              _lib.stream_ptr())
+    ga = ta.cpu().numpy().view(np.uint32)
+    gb = tb.cpu().numpy().view(np.uint16)
+    for s, (ln_, off) in enumerate(zip(lens, offs[:-1])):
+        for lane in range(32):
+            idx = [where[(s, lane, p)] for p in range(ln_)]
+            before = sorted((int(a[ia]) & 0xFFFFFF, int(a[ia]) >> 24, int(b[ib])) for ia, ib in idx)
+            after = [(int(ga[ia]) & 0xFFFFFF, int(ga[ia]) >> 24, int(gb[ib])) for ia, ib in idx]
+            if ln_ > 1024:
+                assert [(int(a[ia]), int(b[ib])) for ia, ib in idx] == [(int(ga[ia]), int(gb[ib])) for ia, ib in idx]
+            else:
+                assert after == before
