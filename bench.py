@@ -45,6 +45,9 @@ ALPHA_L = 0.006
 TRAFFIC_BYTES_PER_LAUNCH = {"rplan_render_kernel<1>": 522_099_968, "loop_render_scat_kernel": 10_210_304}
 TRAFFIC_SOURCE = {"rplan_render_kernel<1>": "profiles/r2final_ncu_det_raw.csv (round 2 final, ID 0)",
                   "loop_render_scat_kernel": "profiles/r1_ncu_render_final_raw.csv (round 1)"}
+# a pure 32-byte-load read stream over 2 GiB on a B200 of this pool (best variant, median of 20 launches)
+READ_STREAM_GBS = 7261.3
+READ_STREAM_SOURCE = "profiles/r2_read_peak.json (tools/read_peak.cu)"
 DTYPE = ("f32 values, 17-bit-mantissa operator weights (render and adjust plans), f64 geometry, "
          "32.32 fixed-point accumulation")
 METRIC = "recon iters/sec at 128³×8 views 512²; Gsamples/s; % of HBM roofline"
@@ -388,7 +391,9 @@ def run_gpu(args):
     kach = kbytes / (render_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "kernel": kname, "achieved": kach, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
             "frac": kach / peak, "traffic": TRAFFIC_BYTES_PER_LAUNCH[kname], "traffic_source": TRAFFIC_SOURCE[kname],
-            "bytes_per_launch": kbytes, "bytes_rule": rule}
+            "bytes_per_launch": kbytes, "bytes_rule": rule,
+            # the render only reads (516 MB in, ~1 MB out): the read-only stream ceiling next to the copy peak
+            "read_stream_peak": {"gbs": READ_STREAM_GBS, "frac": kach / READ_STREAM_GBS, "source": READ_STREAM_SOURCE}}
 
     # What one step streams from HBM (the plans are re-read every iteration;
     # the operands they index are cache-resident): render plan (6 B per stored
