@@ -1291,6 +1291,9 @@ extern "C" int fvr_rplan_render(const int32_t* unit_len, const int64_t* unit_off
     const int units_x = (bbox_w + kUnitW - 1) / kUnitW, upv = fvr_loop_blocks_per_view(bbox_w, bbox_h);
     const int n_units = upv * n_views;
     int64_t blocks = ((int64_t)n_units * 32 + FVR_RPLAN_THREADS - 1) / FVR_RPLAN_THREADS;
+#ifdef FVR_RPLAN_GRID_CAP
+    if (blocks > FVR_RPLAN_GRID_CAP) blocks = FVR_RPLAN_GRID_CAP;
+#endif
     if (blocks > 148 * 64) blocks = 148 * 64;
     cudaStream_t st = (cudaStream_t)stream;
     const auto* uo = reinterpret_cast<const long long*>(unit_off);

@@ -835,10 +835,25 @@ rplan_render_kernel(
     // short bbox-margin units to SMs as they free up, with no long unit left
     // for the tail (config 2: 0.157 -> 0.139 ms)
     for (int unit = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); unit < n_units;
-         unit += (int)(((int64_t)gridDim.x * blockDim.x) >> 5))
+         unit += (int)(((int64_t)gridDim.x * blockDim.x) >> 5)) {
+#if FVR_RPLAN_NEXT_PREFETCH
+        {  // (persistent grids) the warp's next unit's first chunks into L2
+            const int nu = unit + (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+            if (nu < n_units) {
+                const int un = unit_order ? __ldg(unit_order + nu) : nu;
+                const long long off = __ldg(unit_off + un);
+                const int len = __ldg(unit_len + un);
+                constexpr int kB = WIDE ? kRpA : kRpB;
+                for (int i = 0; i < 4 && i * kRpA < len; ++i)
+                    prefetch_l2(ent_a + ((off / kRpA + i) * 32 + lane) * kRpA);
+                for (int i = 0; i < 2 && i * kB < len; ++i) prefetch_l2(ent_b + ((off / kB + i) * 32 + lane) * kRpA);
+            }
+        }
+#endif
         rplan_render_unit<NCH, WIDE>(unit_order ? __ldg(unit_order + unit) : unit, lane, unit_len, unit_off, ent_a, ent_b,
                                base, t_fin, row_src, rows, units_x, units_per_view, n_views, w, h, src, kpv, rc,
                                residual, sq_partials, sq_stride, fin.on ? fin.acc : nullptr, fin.bpv);
+    }
     if (!fin.on) return;
     // the last block to finish runs the loop's finalize (fvr_loop.cu)
     __shared__ int s_last;
