@@ -434,9 +434,11 @@ class ChannelLoop:
         # queued on the loop's stream above, so its layout and fill go first
         # there (the fill waits only for the key-point map); the adjust plan's
         # map, count pass and layout run on the side stream meanwhile, and its
-        # fill follows the render plan's.  Side by side on two streams the
-        # fills slowed each other (config 2: 1.73 + 1.78 ms overlapped,
-        # against 1.59 + 0.92 ms in sequence); FVR_FILL_SERIAL=0 overlaps them.
+        # fill runs beside the render plan's (the side stream has the higher
+        # priority).  Once both fills were trimmed (register-staged chunk
+        # stores, 4-5 CTAs per SM) the overlap pays: config 2 call 10.23 ->
+        # 10.11 ms, stochastic 14.47 -> 14.26 ms (tools/e2e_ab.py); earlier
+        # fills slowed each other.  FVR_FILL_SERIAL=1 runs them in sequence.
         keep = []
         adjust_done = kpmap_ready = pc = None
         rs = self._rplan_scan(*self._rp_counted) if self._rp_counted is not None else None
@@ -465,7 +467,7 @@ class ChannelLoop:
             with t.cuda.stream(side):
                 sizes = pc["sizes"].get()  # waits for the side stream's copy only
                 self._mark("adjust sizes read")
-                if rfill_done is not None and os.environ.get("FVR_FILL_SERIAL", "1") == "1":
+                if rfill_done is not None and os.environ.get("FVR_FILL_SERIAL", "0") == "1":
                     side.wait_event(rfill_done)
                 self.plan = self._plan_fill(pc, sizes, side, keep)
                 self.sample_plan = self.plan and self.sample_plan

@@ -40,6 +40,10 @@ def setup(name):
         os.environ["FVR_SPLAN_SORT"] = "0"
     else:
         os.environ.pop("FVR_SPLAN_SORT", None)
+    if name == "fill_overlap":
+        os.environ["FVR_FILL_SERIAL"] = "0"
+    else:
+        os.environ.pop("FVR_FILL_SERIAL", None)
 
 
 def call():
