@@ -175,12 +175,13 @@ def _side_stream(dev):
     from its own caching-allocator pool, which a per-call stream would never
     reuse (a fresh cudaMalloc every call)."""
     t = _lib.torch()
-    key = str(dev)
+    # higher priority than the loop's stream (FVR_SIDE_PRIORITY, default -1):
+    # the side stream's short layout kernels are scheduled ahead of a running
+    # fill's remaining CTAs instead of after them
+    prio = int(os.environ.get("FVR_SIDE_PRIORITY", "-1"))
+    key = (str(dev), prio)
     if key not in _SIDE:
-        # higher priority than the loop's stream: the side stream's short
-        # layout kernels are scheduled ahead of a running fill's remaining
-        # CTAs instead of after them
-        _SIDE[key] = t.cuda.Stream(device=dev, priority=-1)
+        _SIDE[key] = t.cuda.Stream(device=dev, priority=prio)
     return _SIDE[key]
 
 

@@ -40,8 +40,12 @@ def setup(name):
         os.environ["FVR_SPLAN_SORT"] = "0"
     else:
         os.environ.pop("FVR_SPLAN_SORT", None)
-    if name == "fill_overlap":
-        os.environ["FVR_FILL_SERIAL"] = "0"
+    if name == "side_prio0":
+        os.environ["FVR_SIDE_PRIORITY"] = "0"
+    else:
+        os.environ.pop("FVR_SIDE_PRIORITY", None)
+    if name in ("fill_overlap", "fill_serial"):
+        os.environ["FVR_FILL_SERIAL"] = "0" if name == "fill_overlap" else "1"
     else:
         os.environ.pop("FVR_FILL_SERIAL", None)
 
