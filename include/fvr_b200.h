@@ -382,6 +382,13 @@ int fvr_sample_plan_spatial(int32_t* entries, int64_t n_slots, int32_t e6, const
  * (32.32 fixed point), so only the memory access pattern changes. */
 int fvr_plan_sort_rows(const int32_t* slice_len, const int64_t* slice_off, int64_t n_slices, int32_t* entries,
                        uint32_t* entries_b, void* stream);
+/* Zero the padding of a filled 6-byte SELL plan: lane-row pos of slice s holds
+ * cursor[row_of_pos[pos]] entries (the fill's final per-row cursors); positions
+ * from there to slice_len[s] are cleared, so the entry buffers need no
+ * clearing before the fill. */
+int fvr_sell_pad_zero(const int64_t* cursor, const int32_t* row_of_pos, int64_t n_rows, const int32_t* slice_len,
+                      const int64_t* slice_off, int64_t n_slices, int32_t* entries, uint32_t* entries_b,
+                      void* stream);
 /* The stochastic mode's G = clip(N(1, g_sigma), 0, 2) for (seed, iteration,
  * ray, march index k) -- the counter-based replacement of the reference's
  * rng.normal draw (reconstruct.py:191-204); the weigh pass and the ray-driven

@@ -187,6 +187,7 @@ _SIGNATURES = {
     "fvr_sell_layout": (c_int, [_P, c_int64, c_int32, c_int32, _P, c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "fvr_sample_plan_spatial": (c_int, [_P, c_int64, c_int32, _P, c_int64, _P, _P, _P]),
     "fvr_plan_sort_rows": (c_int, [_P, _P, c_int64, _P, _P, _P]),
+    "fvr_sell_pad_zero": (c_int, [_P, _P, c_int64, _P, _P, c_int64, _P, _P, _P]),
     "fvr_count_nonzero_u8": (c_int, [_P, c_int64, _P, _P]),
     "fvr_copy_host_parallel": (c_int, [_P, _P, c_int32, _P]),
     "fvr_select_nonzero_u8": (c_int, [_P, c_int64, c_int64, _P, _P, _P]),

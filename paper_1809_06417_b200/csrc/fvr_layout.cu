@@ -244,9 +244,47 @@ plan_sort_rows_kernel(const int32_t* __restrict__ slice_len, const long long* __
     }
 }
 
+// The padding of a 6-byte SELL plan zeroed after its fill: lane-row `pos`
+// holds cursor[row] entries (the fill's final cursors), positions up to the
+// slice length are padding the gather reads with weight 0.
+__global__ void sell_pad_zero_kernel(const long long* __restrict__ cursor, const int32_t* __restrict__ row_of_pos,
+                                     int64_t n_rows, const int32_t* __restrict__ slice_len,
+                                     const long long* __restrict__ slice_off, int64_t n_pos, uint32_t* __restrict__ ea,
+                                     uint16_t* __restrict__ eb) {
+    for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < n_pos;
+         pos += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t sl = pos >> 5;
+        const int ln = (int)(pos & 31);
+        const int len = slice_len[sl];
+        const long long off = slice_off[sl];
+        const int c = pos < n_rows ? (int)cursor[row_of_pos[pos]] : 0;
+        for (int p = c; p < len; ++p) {
+            ea[(((off >> 2) + (p >> 2)) * 32 + ln) * 4 + (p & 3)] = 0u;
+            eb[(((off >> 3) + (p >> 3)) * 32 + ln) * 8 + (p & 7)] = 0;
+        }
+    }
+}
+
 }  // namespace fvr
 
 using namespace fvr;
+
+extern "C" int fvr_sell_pad_zero(const int64_t* cursor, const int32_t* row_of_pos, int64_t n_rows,
+                                 const int32_t* slice_len, const int64_t* slice_off, int64_t n_slices,
+                                 int32_t* entries, uint32_t* entries_b, void* stream) {
+    FVR_TRY_BEGIN
+    if (n_slices <= 0) return FVR_OK;
+    if (!entries_b) return set_error(FVR_ERR_INVALID, "pad zero: 6-byte plans only");
+    const int64_t n_pos = n_slices * 32;
+    int64_t blocks = (n_pos + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    sell_pad_zero_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const long long*>(cursor), row_of_pos, n_rows, slice_len,
+        reinterpret_cast<const long long*>(slice_off), n_pos, reinterpret_cast<uint32_t*>(entries),
+        reinterpret_cast<uint16_t*>(entries_b));
+    return check_launch("sell_pad_zero");
+    FVR_TRY_END
+}
 
 extern "C" int fvr_plan_sort_rows(const int32_t* slice_len, const int64_t* slice_off, int64_t n_slices,
                                   int32_t* entries, uint32_t* entries_b, void* stream) {

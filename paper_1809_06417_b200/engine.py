@@ -915,14 +915,18 @@ class ChannelLoop:
             (2 + 4 * self.pitch) * n_samples + 8 * self.n_kp
         if need > self.PLAN_MAX_BYTES or n_samples >= 2 ** 31:
             return False
+        pad_zero = os.environ.get("FVR_PAD_ZERO", "1") == "1"
         try:
             cursor = t.zeros(self.n_kp, dtype=t.int64, device=dev)
             if (self.sample_plan and not self.splan_e6) or self.adj_wide:  # int2 (sample id / residual index, W)
                 entries = t.zeros(max(2 * slots, 2), dtype=t.int32, device=dev)
                 entries_b = None
             else:  # 6 bytes: sample id or residual index (24 bits) + 24-bit weight
-                entries = t.zeros(max(slots, 2), dtype=t.int32, device=dev)
-                entries_b = t.zeros(max(slots // 2, 1), dtype=t.int32, device=dev)
+                # (the padding is cleared after the fill from its final cursors:
+                # no full-buffer clear on the side stream ahead of the fill)
+                alloc = t.empty if pad_zero else t.zeros
+                entries = alloc(max(slots, 2), dtype=t.int32, device=dev)
+                entries_b = alloc(max(slots // 2, 1), dtype=t.int32, device=dev)
             if self.sample_plan:
                 meta = t.empty(max(n_samples // 2, 2), dtype=t.int32, device=dev)  # int2 per 4-slot block
                 rho = t.zeros((max(n_samples, 1), self.pitch), dtype=t.float32, device=dev)
@@ -946,6 +950,8 @@ class ChannelLoop:
             _lib.call("fvr_sample_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff,
                       pc["kp_map"].data_ptr(), sid0.data_ptr(), *sell, _lib.ptr(entries_b), meta.data_ptr(),
                       _lib.ptr(keys), stream)
+            if pad_zero and entries_b is not None:  # before the renumbering reads every slot
+                self._pad_zero(pc, cursor, entries, entries_b, stream)
             if spatial:
                 meta_new = t.empty_like(meta)
                 _lib.call("fvr_sample_plan_spatial", entries.data_ptr(), slots, int(entries_b is not None),
@@ -960,6 +966,8 @@ class ChannelLoop:
         else:
             _lib.call("fvr_adjust_plan_fill", *pc["geo"], c.tau, c.alpha_l, c.alpha_d_eff,
                       pc["kp_map"].data_ptr(), *sell, _lib.ptr(entries_b), stream)
+            if pad_zero and entries_b is not None:
+                self._pad_zero(pc, cursor, entries, entries_b, stream)
         self.plan_slice_len = pc["slice_len"]
         self.plan_slice_off = pc["slice_off"]
         self.plan_row_of_pos = pc["row_of_pos"]
@@ -968,6 +976,11 @@ class ChannelLoop:
         self.plan_nnz = nnz
         self.plan_slots = slots
         return True
+
+    def _pad_zero(self, pc, cursor, entries, entries_b, stream):
+        _lib.call("fvr_sell_pad_zero", cursor.data_ptr(), pc["row_of_pos"].data_ptr(), self.n_kp,
+                  pc["slice_len"].data_ptr(), pc["slice_off"].data_ptr(), pc["slice_len"].numel(),
+                  entries.data_ptr(), entries_b.data_ptr(), stream)
 
     def _weigh(self, stream):
         """rho = residual * G per in-hull sample (stochastic sample plan)."""

@@ -40,6 +40,10 @@ def setup(name):
         os.environ["FVR_SPLAN_SORT"] = "0"
     else:
         os.environ.pop("FVR_SPLAN_SORT", None)
+    if name == "clear_first":
+        os.environ["FVR_PAD_ZERO"] = "0"
+    else:
+        os.environ.pop("FVR_PAD_ZERO", None)
     if name == "side_prio0":
         os.environ["FVR_SIDE_PRIORITY"] = "0"
     else:
