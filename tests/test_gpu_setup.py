@@ -309,3 +309,42 @@ def test_plan_row_sort(cuda_device):
                 assert [(int(a[ia]), int(b[ib])) for ia, ib in idx] == [(int(ga[ia]), int(gb[ib])) for ia, ib in idx]
             else:
                 assert after == before
+
+
+def test_sell_pad_zero(cuda_device):
+    """fvr_sell_pad_zero clears exactly the padding of each lane-row (from the
+    fill's cursor to the slice length) and leaves the filled entries alone."""
+    import torch
+
+    from paper_1809_06417_b200 import _lib
+
+    rng = np.random.default_rng(11)
+    lens = np.array([8, 16, 24], dtype=np.int32)
+    offs = np.concatenate([[0], np.cumsum(lens.astype(np.int64))])
+    total = int(offs[-1])
+    n_rows = 3 * 32 - 5  # the last slice is partly unused
+    row_of_pos = rng.permutation(n_rows).astype(np.int32)
+    cursor = np.zeros(n_rows, dtype=np.int64)
+    for pos in range(n_rows):
+        cursor[row_of_pos[pos]] = rng.integers(0, lens[pos >> 5] + 1)
+    a = np.full(32 * total, 0xDEADBEEF, dtype=np.uint32)
+    b = np.full(32 * total, 0xBEEF, dtype=np.uint16)
+    dev = torch.device("cuda", 0)
+    ta = torch.from_numpy(a.view(np.int32).copy()).to(dev)
+    tb = torch.from_numpy(b.view(np.int32).copy()).to(dev)
+    args = [torch.from_numpy(x).to(dev) for x in (cursor, row_of_pos, lens, offs[:-1].copy())]
+    _lib.call("fvr_sell_pad_zero", args[0].data_ptr(), args[1].data_ptr(), n_rows, args[2].data_ptr(),
+              args[3].data_ptr(), len(lens), ta.data_ptr(), tb.data_ptr(), _lib.stream_ptr())
+    ga = ta.cpu().numpy().view(np.uint32)
+    gb = tb.cpu().numpy().view(np.uint16)
+    for pos in range(3 * 32):
+        s, lane = pos >> 5, pos & 31
+        off, ln_ = int(offs[s]), int(lens[s])
+        c = int(cursor[row_of_pos[pos]]) if pos < n_rows else 0
+        for p in range(ln_):
+            ia = (((off >> 2) + (p >> 2)) * 32 + lane) * 4 + (p & 3)
+            ib = (((off >> 3) + (p >> 3)) * 32 + lane) * 8 + (p & 7)
+            if p < c:
+                assert ga[ia] == 0xDEADBEEF and gb[ib] == 0xBEEF
+            else:
+                assert ga[ia] == 0 and gb[ib] == 0
